@@ -1,0 +1,253 @@
+"""Seeded synthetic inputs for the BASELINE.json configurations.
+
+The paper's ARDRA transport runs are not available; BASELINE.json defines
+synthetic stand-ins and these generators build them deterministically (numpy
+``default_rng`` seeds, draw order as SURVEY.md section 8(d) lists).  Nothing
+here is on the timed path: they produce the snapshot streams, sparse operators
+and bases that the device kernels consume.
+
+* cfg1 -- 1D periodic upwind advection + central diffusion, N = 1024 cells.
+* cfg2 -- low-rank-plus-noise stream X = Q diag(sigma) W^T + E, n_s = 2^20.
+* cfg4 -- 3D 7-point advection-diffusion on a 100^3 grid with random
+  per-cell diffusivity, plus a Haar spatial basis and Haar temporal blocks.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import scipy.sparse as sp
+
+
+def haar(rng: np.random.Generator, rows: int, cols: int) -> np.ndarray:
+    """Haar-random orthonormal columns: Q of QR(Gaussian) with diag(R) >= 0.
+
+    Same recipe as the reference's ``verify._random_orthonormal``
+    (pkg/src/strom/verify.py:52-54 -> linalg.qr, linalg.py:60-72).
+    """
+    q, r = np.linalg.qr(rng.standard_normal((rows, cols)), mode="reduced")
+    d = np.sign(np.diag(r))
+    d[d == 0.0] = 1.0
+    return q * d
+
+
+# --------------------------------------------------------------------------
+# cfg1: periodic advection-diffusion (BASELINE.json configs[0])
+# --------------------------------------------------------------------------
+
+CFG1_N = 1024
+CFG1_TRAIN_NU = (0.01, 0.02, 0.03, 0.04)
+CFG1_TEST_NU = 0.025
+CFG1_DT = 1e-3
+CFG1_NT = 100
+CFG1_TOL = 1e-8
+CFG1_NS = 10
+CFG1_NTMODES = 4  # n_t = 5 is infeasible with 4 training nu (SURVEY Finding 3)
+
+
+@dataclass
+class LinearSystemData:
+    """Plain operator data of one parameter instance: x' = A x + B f, y = C^T x."""
+
+    a: sp.csr_array
+    b: sp.csr_array
+    c: np.ndarray
+    x0: np.ndarray
+    f_const: np.ndarray  # constant input vector
+
+    def inputs(self, k: int) -> np.ndarray:
+        return self.f_const
+
+
+def cfg1_system(nu: float, n: int = CFG1_N, speed: float = 1.0) -> LinearSystemData:
+    """A = -c D1_upwind + nu D2_central on a periodic grid, x_i = (i + 1/2)/n.
+
+    B = 0 (one input column), f = 0, x0 = Gaussian bump at 0.3 (width 0.05),
+    output C = cell mean.
+    """
+    dx = 1.0 / n
+    idx = np.arange(n)
+    left = (idx - 1) % n
+    right = (idx + 1) % n
+    diag = np.full(n, -speed / dx - 2.0 * nu / dx**2)
+    lo = np.full(n, speed / dx + nu / dx**2)
+    hi = np.full(n, nu / dx**2)
+    rows = np.concatenate([idx, idx, idx])
+    cols = np.concatenate([idx, left, right])
+    vals = np.concatenate([diag, lo, hi])
+    a = sp.csr_array((vals, (rows, cols)), shape=(n, n))
+    a.sum_duplicates()
+    a.sort_indices()
+    x = (idx + 0.5) * dx
+    x0 = np.exp(-(((x - 0.3) / 0.05) ** 2))
+    b = sp.csr_array((n, 1))
+    c = np.full((n, 1), 1.0 / n)
+    return LinearSystemData(a=a, b=b, c=c, x0=x0, f_const=np.zeros(1))
+
+
+def cfg1_dt() -> np.ndarray:
+    return np.full(CFG1_NT, CFG1_DT)
+
+
+# --------------------------------------------------------------------------
+# cfg2: synthetic low-rank stream (BASELINE.json configs[1])
+# --------------------------------------------------------------------------
+
+CFG2_N = 1 << 20
+CFG2_COLS = 500
+CFG2_RANK = 64
+CFG2_TOL = 1e-9
+CFG2_RMAX = 64
+
+
+def cfg2_sigma(rank: int = CFG2_RANK, decades_per: float = 8.0) -> np.ndarray:
+    return 10.0 ** (-np.arange(rank) / decades_per)
+
+
+def cfg2_stream_numpy(n: int = CFG2_N, cols: int = CFG2_COLS, rank: int = CFG2_RANK,
+                      seed: int = 0, noise: float = 1e-12, decades_per: float = 8.0):
+    """X = Q diag(sigma) W^T + noise * N(0,1); draw order Q, W, E.
+
+    Returns (X (n x cols, Fortran order so columns are contiguous), Q, W, sigma).
+    """
+    rng = np.random.default_rng(seed)
+    q = haar(rng, n, rank)
+    w = haar(rng, cols, rank)
+    s = cfg2_sigma(rank, decades_per)
+    e = rng.standard_normal((n, cols))
+    x = np.asfortranarray((q * s) @ w.T + noise * e)
+    return x, q, w, s
+
+
+def cfg2_stream_torch(n: int = CFG2_N, cols: int = CFG2_COLS, rank: int = CFG2_RANK,
+                      seed: int = 0, noise: float = 1e-12, decades_per: float = 8.0,
+                      device: str = "cuda"):
+    """Device-side generator of the same construction (torch RNG, for the bench).
+
+    Statistically identical to :func:`cfg2_stream_numpy` (different draws).
+    Returns X as a (cols, n) contiguous tensor, i.e. column t is X[t].
+    """
+    import torch
+
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+
+    def _haar(rows, c):
+        a = torch.randn(rows, c, generator=g, device=device, dtype=torch.float64)
+        q, r = torch.linalg.qr(a, mode="reduced")
+        d = torch.sign(torch.diagonal(r))
+        d[d == 0] = 1.0
+        return q * d
+
+    q = _haar(n, rank)
+    w = _haar(cols, rank)
+    s = torch.tensor(cfg2_sigma(rank, decades_per), device=device, dtype=torch.float64)
+    xt = (w * s) @ q.T  # (cols, n)
+    xt += noise * torch.randn(cols, n, generator=g, device=device, dtype=torch.float64)
+    return xt, q, w, s
+
+
+# --------------------------------------------------------------------------
+# cfg4: 3D 7-point advection-diffusion operator build (BASELINE.json configs[3])
+# --------------------------------------------------------------------------
+
+CFG4_NX = 100
+CFG4_NS = 50
+CFG4_NT_MODES = 20
+CFG4_NSTEPS = 500
+CFG4_DT = 1e-3
+CFG4_VELOCITY = (1.0, 0.5, 0.25)
+
+
+def cfg4_operator(nx: int = CFG4_NX, seed: int = 1,
+                  velocity=CFG4_VELOCITY) -> sp.csr_array:
+    """7-point operator on nx^3 interior cells of the unit cube, h = 1/(nx+1).
+
+    (A u)_i = kappa_i sum_nb (u_nb - u_i)/h^2 - sum_d v_d (u_i - u_{i-e_d})/h,
+    kappa_i ~ U[0.5, 1.5] per cell (seed), Dirichlet-zero (missing neighbours
+    drop out), x fastest.  int32 indices; nnz = 7 nx^3 - 6 nx^2.
+    """
+    rng = np.random.default_rng(seed)
+    n = nx ** 3
+    h = 1.0 / (nx + 1)
+    kappa = rng.uniform(0.5, 1.5, n)
+    vx, vy, vz = velocity
+    idx = np.arange(n)
+    ix = idx % nx
+    iy = (idx // nx) % nx
+    iz = idx // (nx * nx)
+    diag = -6.0 * kappa / h**2 - (vx + vy + vz) / h
+    rows, cols, vals = [idx], [idx], [diag]
+    for (coord, stride, v) in ((ix, 1, vx), (iy, nx, vy), (iz, nx * nx, vz)):
+        m = coord > 0  # lower neighbour: diffusion + upwind inflow (v > 0)
+        rows.append(idx[m]); cols.append(idx[m] - stride)
+        vals.append(kappa[m] / h**2 + v / h)
+        m = coord < nx - 1  # upper neighbour: diffusion only
+        rows.append(idx[m]); cols.append(idx[m] + stride)
+        vals.append(kappa[m] / h**2)
+    a = sp.csr_array((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                     shape=(n, n))
+    a.sum_duplicates()
+    a.sort_indices()
+    a.indices = a.indices.astype(np.int32)
+    a.indptr = a.indptr.astype(np.int32)
+    return a
+
+
+@dataclass
+class Cfg4Inputs:
+    a: sp.csr_array
+    phi_s: np.ndarray          # N x n_s
+    temporal: tuple            # n_s arrays of N_t x n_t
+    dt: np.ndarray
+    b: sp.csr_array            # N x 1
+    x0: np.ndarray
+    c: np.ndarray              # N x 1
+    f_const: np.ndarray
+
+    def inputs(self, k: int) -> np.ndarray:
+        return self.f_const
+
+
+def cfg4_inputs(nx: int = CFG4_NX, n_s: int = CFG4_NS, n_t: int = CFG4_NT_MODES,
+                n_steps: int = CFG4_NSTEPS, dt: float = CFG4_DT) -> Cfg4Inputs:
+    """Operator (seed 1), Haar Phi_s (seed 2), Haar temporal blocks (seed 3),
+    dense B column (seed 4), x0 (seed 5); f = 1 constant."""
+    a = cfg4_operator(nx, seed=1)
+    n = a.shape[0]
+    phi = haar(np.random.default_rng(2), n, n_s)
+    rng3 = np.random.default_rng(3)
+    temporal = tuple(haar(rng3, n_steps, n_t) for _ in range(n_s))
+    bcol = np.random.default_rng(4).standard_normal((n, 1))
+    x0 = np.random.default_rng(5).standard_normal(n)
+    c = np.full((n, 1), 1.0 / n)
+    return Cfg4Inputs(a=a, phi_s=phi, temporal=temporal, dt=np.full(n_steps, dt),
+                      b=sp.csr_array(bcol), x0=x0, c=c, f_const=np.ones(1))
+
+
+# --------------------------------------------------------------------------
+# small random instances (same recipes as the reference's verify.py:52-82)
+# --------------------------------------------------------------------------
+
+def random_basis(rng, n_states, n_steps, n_s, n_t):
+    phi = haar(rng, n_states, n_s)
+    temporal = tuple(haar(rng, n_steps, n_t) for _ in range(n_s))
+    return phi, temporal
+
+
+def random_stable_system(rng, n_states, n_inputs=1):
+    """Dense diagonally-shifted Gaussian A, Gaussian B/C/x0; per-step random inputs."""
+    a = rng.standard_normal((n_states, n_states))
+    a -= (np.abs(a).sum(axis=1).max() + 0.5) * np.eye(n_states)
+    sig_rng = np.random.default_rng(rng.integers(2**63))
+    cache = {}
+
+    def signal(k):
+        if k not in cache:
+            cache[k] = np.asarray(sig_rng.standard_normal(n_inputs))
+        return cache[k]
+
+    return dict(a=sp.csr_array(a), b=sp.csr_array(rng.standard_normal((n_states, n_inputs))),
+                c=rng.standard_normal((n_states, 1)), x0=rng.standard_normal(n_states),
+                inputs=signal)
