@@ -1,0 +1,198 @@
+/*
+ * strom_b200 -- C ABI of the B200-native (sm_100a) hot path of arXiv 1910.01260
+ * (streaming incremental SVD, per-mode temporal bases, block-structured
+ * space-time reduced operator and its solve).
+ *
+ * Conventions
+ *   - plain C types only; every pointer argument named *_dev is DEVICE memory,
+ *     *_host is host memory; `stream` is a cudaStream_t passed as void*
+ *     (NULL = legacy default stream).  All work is stream-ordered and
+ *     asynchronous unless the comment says "synchronizes".
+ *   - return value: 0 on success, otherwise a STROM_E* code; the message is
+ *     strom_last_error() (thread-local).  The Python mirror maps the codes to
+ *     the reference's exception types (ValueError, BasisError,
+ *     SingularMatrixError).
+ *   - dense matrices are column-major with an explicit leading dimension
+ *     unless a parameter says row-major.
+ *
+ * Each entry point cites the reference interface it replaces (file:line
+ * under the reference's pkg/src/strom/).
+ */
+#ifndef STROM_B200_H
+#define STROM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define STROM_B200_ABI_VERSION 1
+
+#define STROM_OK 0
+#define STROM_EINVAL 1     /* shape / argument error        -> ValueError          */
+#define STROM_ECUDA 2      /* CUDA runtime failure                                 */
+#define STROM_ENUMERIC 3   /* non-finite input              -> ValueError          */
+#define STROM_ESINGULAR 4  /* pivot below floor             -> SingularMatrixError */
+#define STROM_ERANK 5      /* rank / ceiling violation      -> BasisError          */
+#define STROM_EINTERNAL 6
+
+const char* strom_last_error(void);
+int strom_abi_version(void);
+int strom_device_synchronize(void);
+
+/* Built-in profiling (used by bench.py for the live roofline): per kernel kind
+ * (0 proj pass, 1 residual pass, 2 step A, 3 step B, 4 V update, 5 compaction,
+ * 6 tall GEMM, 7 spatial, 8 ST Gram, 9 ST small, 10 LU, 11 temporal, 12 other)
+ * the launch count, the summed CUDA-event duration (only while enabled) and
+ * the algorithmic bytes moved.  strom_profile_read synchronizes the device. */
+void strom_profile_enable(int32_t on);
+int strom_profile_reset(void);
+int strom_profile_read(int32_t nkinds, int64_t* launches_host, double* ms_host, double* bytes_host);
+
+/* fp64 tensor-pipe (DMMA) throughput probe: launches ctas_per_sm x SMs CTAs of
+ * `iters` DMMA rounds on `stream`; *flops_out = flops issued (time it with events). */
+int strom_fp64_probe(int32_t iters, int32_t ctas_per_sm, void* stream, double* flops_out);
+
+/* ------------------------------------------------------------------------
+ * Streaming incremental SVD  (basis.py:30-194, PAPER.md Algorithms 1-2)
+ *
+ * A strom_isvd is one immutable SvdState (basis.py:30-62).  Updates are
+ * functional like the reference's dataclasses.replace (basis.py:127,176): the
+ * source handle stays valid; every call returns a new handle that the caller
+ * frees with strom_isvd_free.  Decisions (dependent / truncate / drift-QR /
+ * restart) are taken on the device; no host round trip per snapshot.
+ * ------------------------------------------------------------------------ */
+typedef struct strom_isvd strom_isvd;
+
+#define STROM_CAP_RESTART 0
+#define STROM_CAP_TRUNCATE 1
+
+/* decision bits of the update that produced a state (strom_isvd_info.flags) */
+#define STROM_F_DEPENDENT 1
+#define STROM_F_TRUNCATED 2
+#define STROM_F_QR 4
+#define STROM_F_RESTART 8
+#define STROM_F_REJECTED 16
+
+typedef struct {
+  int64_t n;          /* rows (spatial DOFs)                              */
+  int64_t k;          /* columns ingested (SvdState.k, basis.py:45)       */
+  int32_t rank;       /* sigma.size (basis.py:60-62)                      */
+  int32_t ncols_u;    /* columns of the append-only store in use          */
+  int32_t n_rejected, n_dependent, n_truncated, n_restarts; /* basis.py:50-54 */
+  int32_t flags;      /* STROM_F_* of the last update                     */
+  int32_t status;     /* 0, or STROM_ENUMERIC after a non-finite column   */
+  double last_p;      /* Pythagorean residual norm of the last update     */
+  double last_drift;  /* |phi_0 . phi_last| of the last update            */
+  double last_xnorm;  /* ||x|| of the last update                         */
+  double tol_svd, tol_sv;
+  int64_t r_max;      /* -1 = uncapped                                    */
+  int32_t cap_mode;   /* STROM_CAP_*                                      */
+  int32_t pad;
+} strom_isvd_info;
+
+/* isvd_init (basis.py:65-102): start the stream at its k-th column x_dev[n]. */
+int strom_isvd_init(int64_t n, const double* x_dev, int64_t k, double tol_svd, double tol_sv,
+                    int64_t r_max, int32_t cap_mode, void* stream, strom_isvd** out);
+
+/* isvd_update (basis.py:105-184): fold one column; *out is a new state. */
+int strom_isvd_update(strom_isvd* src, const double* x_dev, void* stream, strom_isvd** out);
+
+/* ingest_simulation (basis.py:187-194): fold ncols columns of X (column-major,
+ * leading dimension ldx) left to right.  x_on_host != 0: X is host memory
+ * (pinned for overlap); the columns are streamed to the device in chunks on a
+ * copy stream overlapped with the updates. */
+int strom_isvd_ingest(strom_isvd* src, const double* X, int64_t ldx, int64_t ncols, int32_t x_on_host,
+                      void* stream, strom_isvd** out);
+
+/* SvdState fields: synchronizes `stream` and reads the device header. */
+int strom_isvd_query(strom_isvd* h, void* stream, strom_isvd_info* out);
+
+/* Materialise phi (n x rank, ROW-major like the reference's C-ordered array),
+ * sigma (rank) and v (k x rank, row-major).  Any output may be NULL. */
+int strom_isvd_export(strom_isvd* h, double* phi_dev, double* sigma_dev, double* v_dev, void* stream);
+
+/* SvdState(phi, sigma, v, k, ...) constructor (basis.py:30-58) from explicit
+ * device arrays (phi n x r row-major, v k x r row-major).  phi need not be
+ * orthonormal; it must have full column rank (its Gram is Cholesky-factored).
+ * counters4 = {n_rejected, n_dependent, n_truncated, n_restarts} (host). */
+int strom_isvd_load(int64_t n, int64_t k, int64_t r, const double* phi_dev, const double* sigma_dev,
+                    const double* v_dev, double tol_svd, double tol_sv, int64_t r_max, int32_t cap_mode,
+                    const int32_t* counters4_host, void* stream, strom_isvd** out);
+
+/* Same state given in factored form phi = U W with U (n x c, column-major,
+ * ldu) and W (c x r, column-major, ldw); L (c x c lower, ldl) is the Cholesky
+ * factor of U^T U, or NULL when U has orthonormal columns. */
+int strom_isvd_load_factored(int64_t n, int64_t k, int64_t c, int64_t r, const double* u_dev, int64_t ldu,
+                             const double* w_dev, int64_t ldw, const double* l_dev, int64_t ldl,
+                             const double* sigma_dev, const double* v_dev, double tol_svd, double tol_sv,
+                             int64_t r_max, int32_t cap_mode, const int32_t* counters4_host, void* stream,
+                             strom_isvd** out);
+
+void strom_isvd_free(strom_isvd* h);
+
+/* ------------------------------------------------------------------------
+ * Temporal bases  (basis.py:275-302 build_basis_set's per-mode loop)
+ * v_dev: the k x r right singular matrix, column-major (ld ldv >= n_mu*n_steps).
+ * For every mode i < n_s: T_i = v[:, i] reshaped N_t x n_mu (basis.py:215-228),
+ * thin SVD with the reference's sign rule; psi_dev receives the first n_t
+ * left vectors as (n_s, N_t, n_t) C-order, ranks_dev (int32 n_s) the rank
+ * #{sigma > max(N_t, n_mu) eps sigma_0}, sigma_dev (n_s x min(N_t, n_mu)).
+ * The caller raises BasisError when n_t > ranks[i] (basis.py:297-300).
+ * ------------------------------------------------------------------------ */
+int strom_temporal_bases(const double* v_dev, int64_t ldv, int64_t r, int64_t n_steps, int64_t n_mu,
+                         int64_t n_s, int64_t n_t, double* psi_dev, int32_t* ranks_dev, double* sigma_dev,
+                         void* stream);
+
+/* ------------------------------------------------------------------------
+ * Spatial reduced operators  (spatial.py:45-67 build_spatial_rom)
+ * CSR A (indptr n+1, indices, data; index_bits 32 or 64), phi element (i, j)
+ * at phi_dev[i*phi_rs + j*phi_cs] (row- or column-major), extra: column-major
+ * n x ne (ld ext_ld) right-hand columns, xref: n-vector or NULL.
+ * out_dev: row-major ns x q, q = ns + ne + (xref != NULL):
+ *   [A_hat | phi^T extra | phi^T (A xref)].   A phi is never materialised.
+ * ------------------------------------------------------------------------ */
+int strom_spatial_reduce_csr(int64_t n, const void* indptr_dev, const void* indices_dev, const double* data_dev,
+                             int32_t index_bits, const double* phi_dev, int64_t phi_rs, int64_t phi_cs,
+                             int64_t ns, const double* extra_dev, int64_t ext_ld, int64_t ne,
+                             const double* xref_dev, double* out_dev, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Space-time reduced system  (spacetime.py:43-115 build_st_matrix /
+ * build_st_input / build_st_init, spacetime.py:128-151 build_st_rom)
+ *   ahat n_s x n_s row-major; psi (n_s, N_t, n_t) C-order; dt N_t;
+ *   bhat n_s x m row-major; f: m values (constant_input) or N_t x m row-major;
+ *   x0hat n_s.  Outputs a_st (NT x NT row-major), f_st, x0_st (NT = n_s n_t,
+ *   index j*n_s + i); pass NULL for outputs not wanted (a_st NULL skips the
+ *   matrix; f_st and x0_st come together).
+ * ------------------------------------------------------------------------ */
+int strom_st_assemble(const double* ahat_dev, const double* psi_dev, const double* dt_dev, int64_t nsteps,
+                      int64_t ns, int64_t nt, const double* bhat_dev, int64_t m, const double* f_dev,
+                      int32_t constant_input, const double* x0hat_dev, double* ast_dev, double* fst_dev,
+                      double* x0st_dev, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Dense kernels  (linalg.py:41-99)
+ * ------------------------------------------------------------------------ */
+/* solve_dense: LU with partial pivoting of a (n x n column-major, overwritten)
+ * and nrhs right-hand sides x (n x nrhs column-major, overwritten by the
+ * solution).  STROM_ESINGULAR with "pivot i" when |U_ii| <= 1e-14 ||a||_F
+ * (synchronizes).  piv_dev (int32 n) and info_dev (3 doubles) may be NULL. */
+int strom_dense_solve(int64_t n, double* a_dev, double* x_dev, int64_t nrhs, int32_t* piv_dev, double* info_dev,
+                      void* stream);
+
+/* qr: thin QR with diag(R) >= 0; m (rows x cols, column-major, ld) <- Q, r_dev <- R (cols x cols). */
+int strom_qr(int64_t rows, int64_t cols, double* m_dev, int64_t ld, double* r_dev, void* stream);
+
+/* thin_svd: m (rows x cols column-major) = w diag(s) v^T, sigma descending, the
+ * largest-|.| entry of every column of w made >= 0 (linalg.py:31-38).
+ * w: rows x kmin, v: cols x kmin (column-major), kmin = min(rows, cols). */
+int strom_thin_svd(int64_t rows, int64_t cols, const double* m_dev, double* w_dev, double* s_dev, double* v_dev,
+                   void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* STROM_B200_H */

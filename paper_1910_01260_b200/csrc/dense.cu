@@ -1,0 +1,270 @@
+// Dense fp64 factorizations on the device:
+//   strom_dense_solve -- LU with partial pivoting + the reference's pivot
+//                        floor (linalg.py:75-99), used by solve_st_rom
+//                        (spacetime.py:154-162)
+//   strom_qr          -- positive-diagonal Householder QR (linalg.py:60-72)
+//
+// LU: blocked right-looking.  Each 32-column panel is factored by one CTA
+// (pivot search, row swap across the full width, scale, rank-1 update inside
+// the panel); the trailing matrix is updated by a unit-lower TRSM and a
+// register-blocked GEMM across all SMs.  The matrix (<= a few thousand) stays
+// L2-resident between kernels.
+#include <algorithm>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/strom_b200.h"
+#include "runtime.cuh"
+#include "small_dense.cuh"
+
+using namespace strom;
+
+namespace {
+
+constexpr int kNb = 32;
+
+__global__ void k_fro_norm(const double* A, int64_t ld, int64_t n, double* out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int64_t idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+    const int64_t i = idx % n, j = idx / n;
+    const double v = A[j * ld + i];
+    s = fma(v, v, s);
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) out[0] = sqrt(s);
+}
+
+// Factor panel columns [k0, k0+nb) of A (n x n, ld), swapping full rows.
+__global__ void __launch_bounds__(1024) k_lu_panel(double* A, int64_t ld, int n, int k0, int nb, int* piv) {
+  __shared__ double sv[32];
+  __shared__ int si[32];
+  __shared__ int s_p;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int j = k0; j < k0 + nb; ++j) {
+    double* cj = A + (int64_t)j * ld;
+    // argmax |A[i, j]| over i >= j, first index on ties (idamax)
+    double best = -1.0;
+    int bi = 0x7fffffff;
+    for (int i = j + threadIdx.x; i < n; i += blockDim.x) {
+      const double a = fabs(cj[i]);
+      if (a > best || (a == best && i < bi)) { best = a; bi = i; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    if (lane == 0) { sv[wid] = best; si[wid] = bi; }
+    __syncthreads();
+    if (wid == 0) {
+      best = (lane < nw) ? sv[lane] : -1.0;
+      bi = (lane < nw) ? si[lane] : 0x7fffffff;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (lane == 0) {
+        s_p = (bi == 0x7fffffff) ? j : bi;
+        piv[j] = s_p;
+      }
+    }
+    __syncthreads();
+    const int p = s_p;
+    if (p != j) {
+      for (int c = threadIdx.x; c < n; c += blockDim.x) {
+        const double t = A[(int64_t)c * ld + j];
+        A[(int64_t)c * ld + j] = A[(int64_t)c * ld + p];
+        A[(int64_t)c * ld + p] = t;
+      }
+    }
+    __syncthreads();
+    const double d = cj[j];
+    if (d != 0.0) {
+      const double inv = 1.0 / d;
+      for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) cj[i] *= inv;
+    }
+    __syncthreads();
+    // rank-1 update of the rest of the panel
+    const int rem_c = k0 + nb - j - 1;
+    for (int c = wid; c < rem_c; c += nw) {
+      double* cc = A + (int64_t)(j + 1 + c) * ld;
+      const double u = cc[j];
+      for (int i = j + 1 + lane; i < n; i += 32) cc[i] = fma(-cj[i], u, cc[i]);
+    }
+    __syncthreads();
+  }
+}
+
+// A12 <- L11^{-1} A12 for columns [k0+nb, n): one thread per column.
+__global__ void k_lu_trsm(double* A, int64_t ld, int n, int k0, int nb) {
+  const int c = k0 + nb + blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  double x[kNb];
+  double* col = A + (int64_t)c * ld;
+#pragma unroll
+  for (int i = 0; i < kNb; ++i) x[i] = (i < nb) ? col[k0 + i] : 0.0;
+#pragma unroll
+  for (int j = 0; j < kNb; ++j) {
+    if (j >= nb) break;
+    const double xj = x[j];
+#pragma unroll
+    for (int i = j + 1; i < kNb; ++i)
+      if (i < nb) x[i] = fma(-A[(int64_t)(k0 + j) * ld + k0 + i], xj, x[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < kNb; ++i)
+    if (i < nb) col[k0 + i] = x[i];
+}
+
+// A22 -= L21 U12 ; tiles of 64 x 64, 256 threads, 4 x 4 per thread.
+__global__ void __launch_bounds__(256) k_lu_gemm(double* A, int64_t ld, int n, int k0, int nb) {
+  __shared__ double Ls[64][kNb + 1];
+  __shared__ double Us[kNb][64 + 1];
+  const int s0 = k0 + nb;
+  const int r0 = s0 + blockIdx.x * 64, c0 = s0 + blockIdx.y * 64;
+  if (r0 >= n || c0 >= n) return;
+  for (int idx = threadIdx.x; idx < 64 * kNb; idx += blockDim.x) {
+    const int i = idx % 64, kk = idx / 64;
+    Ls[i][kk] = (r0 + i < n && kk < nb) ? A[(int64_t)(k0 + kk) * ld + r0 + i] : 0.0;
+    const int c = idx / kNb, k2 = idx % kNb;
+    Us[k2][c] = (c0 + c < n && k2 < nb) ? A[(int64_t)(c0 + c) * ld + k0 + k2] : 0.0;
+  }
+  __syncthreads();
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double acc[4][4] = {};
+#pragma unroll 8
+  for (int kk = 0; kk < kNb; ++kk) {
+    double a[4], b[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) a[q] = Ls[tx + 16 * q][kk];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) b[q] = Us[kk][ty + 16 * q];
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[p][q] = fma(a[p], b[q], acc[p][q]);
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int c = c0 + ty + 16 * q;
+    if (c >= n) continue;
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const int r = r0 + tx + 16 * p;
+      if (r < n) A[(int64_t)c * ld + r] -= acc[p][q];
+    }
+  }
+}
+
+// Pivot check (first |U_ii| <= floor) + triangular solves, one CTA.
+// info[0] = first bad index (or -1), info[1] = its |pivot|, info[2] = floor.
+__global__ void __launch_bounds__(1024) k_lu_solve(const double* A, int64_t ld, int n, const int* piv, double* X,
+                                                   int64_t ldx, int nrhs, const double* fro, double* info) {
+  __shared__ int s_bad;
+  if (threadIdx.x == 0) s_bad = 0x7fffffff;
+  __syncthreads();
+  const double floor = 1e-14 * fro[0];
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    if (fabs(A[(int64_t)i * ld + i]) <= floor) atomicMin(&s_bad, i);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    info[0] = (s_bad == 0x7fffffff) ? -1.0 : (double)s_bad;
+    info[1] = (s_bad == 0x7fffffff) ? 0.0 : fabs(A[(int64_t)s_bad * ld + s_bad]);
+    info[2] = floor;
+  }
+  if (s_bad != 0x7fffffff) return;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int c = wid; c < nrhs; c += nw) {
+    double* x = X + (int64_t)c * ldx;
+    if (lane == 0)
+      for (int j = 0; j < n; ++j) {
+        const int p = piv[j];
+        if (p != j) { const double t = x[j]; x[j] = x[p]; x[p] = t; }
+      }
+    __syncwarp();
+    // forward: unit lower
+    for (int j = 0; j < n; ++j) {
+      const double xj = x[j];
+      for (int i = j + 1 + lane; i < n; i += 32) x[i] = fma(-A[(int64_t)j * ld + i], xj, x[i]);
+      __syncwarp();
+    }
+    // backward: upper
+    for (int j = n - 1; j >= 0; --j) {
+      double xj = 0.0;
+      if (lane == 0) { xj = x[j] / A[(int64_t)j * ld + j]; x[j] = xj; }
+      xj = __shfl_sync(0xffffffffu, xj, 0);
+      for (int i = lane; i < j; i += 32) x[i] = fma(-A[(int64_t)j * ld + i], xj, x[i]);
+      __syncwarp();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_qr(double* M, int64_t ld, int rows, int cols, double* R, double* work) {
+  __shared__ double red[32];
+  cta_householder_qr(M, (int)ld, rows, cols, R, cols, work, work + cols, red);
+}
+
+}  // namespace
+
+extern "C" {
+
+// LU factorization with partial pivoting of A (n x n, column-major, in place)
+// and solve for nrhs right-hand sides X (in place).  On a pivot with
+// |U_ii| <= 1e-14 ||A||_F returns STROM_ESINGULAR ("pivot i") -- synchronizes.
+// piv_dev may be NULL; info_dev (3 doubles) may be NULL.
+int strom_dense_solve(int64_t n, double* a_dev, double* x_dev, int64_t nrhs, int32_t* piv_dev,
+                      double* info_dev, void* stream) {
+  return guarded([&] {
+    STROM_REQUIRE(n >= 1 && a_dev && x_dev && nrhs >= 0, "bad solve arguments");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    auto scratch = dev_alloc(8 * 8 + (size_t)n * 4, s, true);
+    double* fro = scratch->as<double>();
+    double* info = info_dev ? info_dev : fro + 2;
+    int* piv = piv_dev ? piv_dev : reinterpret_cast<int*>(fro + 8);
+    k_fro_norm<<<1, 1024, 0, s>>>(a_dev, n, n, fro);
+    STROM_LAUNCH_CHECK();
+    for (int64_t k0 = 0; k0 < n; k0 += kNb) {
+      const int nb = (int)std::min<int64_t>(kNb, n - k0);
+      k_lu_panel<<<1, 1024, 0, s>>>(a_dev, n, (int)n, (int)k0, nb, piv);
+      STROM_LAUNCH_CHECK();
+      const int64_t rest = n - k0 - nb;
+      if (rest > 0) {
+        k_lu_trsm<<<(unsigned)ceil_div(rest, 128), 128, 0, s>>>(a_dev, n, (int)n, (int)k0, nb);
+        STROM_LAUNCH_CHECK();
+        dim3 g((unsigned)ceil_div(rest, 64), (unsigned)ceil_div(rest, 64));
+        k_lu_gemm<<<g, 256, 0, s>>>(a_dev, n, (int)n, (int)k0, nb);
+        STROM_LAUNCH_CHECK();
+      }
+    }
+    k_lu_solve<<<1, 1024, 0, s>>>(a_dev, n, (int)n, piv, x_dev, n, (int)nrhs, fro, info);
+    STROM_LAUNCH_CHECK();
+    double h[3];
+    STROM_CUDA(cudaMemcpyAsync(h, info, 3 * 8, cudaMemcpyDeviceToHost, s));
+    STROM_CUDA(cudaStreamSynchronize(s));
+    if (h[0] >= 0.0) {
+      char buf[160];
+      snprintf(buf, sizeof(buf), "matrix numerically singular: pivot %lld is %.3e (floor %.3e)",
+               (long long)h[0], h[1], h[2]);
+      throw Error(kSingularMatrix, buf);
+    }
+  });
+}
+
+// Positive-diagonal thin QR of M (rows x cols, column-major, ld) in place
+// (M <- Q); R (cols x cols, column-major) receives the matching R.
+int strom_qr(int64_t rows, int64_t cols, double* m_dev, int64_t ld, double* r_dev, void* stream) {
+  return guarded([&] {
+    STROM_REQUIRE(rows >= cols && cols >= 1 && m_dev && r_dev, "need rows >= cols");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    auto work = dev_alloc((size_t)2 * cols * 8, s, false);
+    k_qr<<<1, 1024, 0, s>>>(m_dev, ld, (int)rows, (int)cols, r_dev, work->as<double>());
+    STROM_LAUNCH_CHECK();
+  });
+}
+
+}  // extern "C"

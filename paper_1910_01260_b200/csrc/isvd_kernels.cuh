@@ -1,0 +1,727 @@
+// Device kernels of the streaming incremental SVD (reference basis.py:105-184).
+//
+// Representation: the reference keeps the
+// n x r left basis Phi explicitly and rewrites it every snapshot
+// (Phi' = [Phi j] W_bar, basis.py:155-156).  Here Phi = U[:, base:base+c] W:
+//   U  n x c_cap   append-only column store in HBM (column-major, ld = ldu),
+//                  columns nearly orthogonal; G = U^T U = L L^T tracked exactly
+//   W  c x r       small coefficient matrix (HBM, read by one CTA)
+// so one snapshot costs one projection pass (g = U^T x) and, when the column is
+// independent, one residual pass that appends r1 = x - U G^{-1} g and measures
+// e = U^T r1, |r1|^2.  Everything else -- the bordered core SVD, the W and V
+// rotations, truncation, drift test, re-orthogonalisation -- is small-space
+// work on one CTA.  The reference's tall QR (basis.py:174) becomes a QR of the
+// (c x r) matrix L^T W; its Q is the same unique positive-diagonal Q.
+#pragma once
+
+#include "common.cuh"
+#include "small_dense.cuh"
+
+namespace strom {
+
+// -------- per-state header (lives in the state's small block) --------------
+struct IsvdHdr {
+  int32_t r;       // rank = sigma.size
+  int32_t c;       // logical columns of U in use
+  int32_t base;    // physical column of logical column 0
+  int32_t status;  // 0 ok, 1 non-finite input
+  int32_t n_rejected, n_dependent, n_truncated, n_restarts;
+  int32_t flags;   // decision bits of the update that produced this state
+  int32_t pad0;
+  double p;        // Pythagorean residual norm of that update
+  double drift;    // |phi_0 . phi_last| of that update
+  double xnorm;    // ||x|| of that update
+  double pad1;
+};
+
+enum : int32_t {
+  F_DEPENDENT = 1, F_TRUNCATED = 2, F_QR = 4, F_RESTART = 8, F_REJECTED = 16,
+  F_APPENDED = 32, F_FOLDED = 64, F_ERROR = 128,
+};
+
+enum : int32_t { M_NORMAL_DEP = 0, M_NORMAL_INDEP = 1, M_RESTART_ACCEPT = 2, M_REJECT = 3, M_ERROR = 4 };
+
+// -------- transient per-update scalars (scratch) ---------------------------
+struct IsvdStep {
+  int32_t mode, write_slot, c_dot, restart;
+  int32_t m, mkeep, appended, pad;
+  double xx, rho2, p, norm;
+};
+
+struct StateView {
+  IsvdHdr* hdr;
+  double* W;      // c_cap x (r_cap + 1), ld = ldw
+  double* L;      // c_cap x c_cap lower, ld = ldl
+  double* sigma;  // r_cap + 1
+  double* V;      // k_cap x (r_cap + 1), ld = ldv
+  int32_t ldw, ldl;
+  int64_t ldv;
+};
+
+struct Scratch {
+  double* g;      // c_cap   U^T x
+  double* gt;     // c_cap   G^{-1} g
+  double* y;      // c_cap   W ell
+  double* ell;    // r_cap+1 Phi^T x
+  double* e;      // c_cap   U^T r1
+  double* vbar;   // (r_cap+2)^2 sorted, sign-fixed V_bar of the core
+  double* work;   // large fallback workspace (global) for the one-CTA kernels
+  double* T;      // c_cap x (r_cap+1) compaction transform
+  double* part;   // per-CTA partial sums
+  unsigned* counter;
+  IsvdStep* step;
+};
+
+struct IsvdParams {
+  int64_t n, ldu;
+  int32_t ccap, rcap;
+  double tol_svd, tol_sv;
+  int32_t r_max;     // -1: no cap
+  int32_t cap_mode;  // 0 restart, 1 truncate
+  int64_t k_new;     // column counter after this update
+  int32_t pstride;   // stride of one CTA's partial row
+  int32_t work_stride;
+  unsigned long long* prof;  // device byte counters (runtime.cuh ProfKind) or null
+};
+
+constexpr int kTileRows = 64;
+constexpr int kPassThreads = 256;
+
+// Deterministic grid finish: the last CTA to arrive sums the per-CTA partials
+// in CTA order.  Returns true in that CTA (after the counter is reset).
+__device__ inline bool last_cta_arrives(unsigned* counter, int* s_is_last) {
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(counter, 1u);
+    *s_is_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (*s_is_last) {
+    __threadfence();
+    if (threadIdx.x == 0) *counter = 0u;
+    return true;
+  }
+  return false;
+}
+
+// ---------------------------------------------------------------------------
+// Projection pass: g = U[:, base:base+c]^T x and xx = x.x  (basis.py:135-136)
+// Warp w owns columns w, w+8, ...; lane l owns rows 2l, 2l+1 of each 64-row
+// tile (128-bit loads of U).  Contiguous tile ranges per CTA.
+// ---------------------------------------------------------------------------
+template <int MAXJ>
+__global__ void __launch_bounds__(kPassThreads) k_proj(const double* __restrict__ U,
+                                                        const double* __restrict__ x,
+                                                        StateView src, Scratch sc, IsvdParams P) {
+  __shared__ int s_last;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int c = src.hdr->c, base = src.hdr->base;
+  if (P.prof && blockIdx.x == 0 && threadIdx.x == 0)
+    atomicAdd(P.prof + 0, 8ull * (unsigned long long)P.n * (unsigned long long)(c + 1));  // U cols + x
+  const int64_t ntiles = P.ldu / kTileRows;
+  const int64_t per = ceil_div(ntiles, gridDim.x);
+  const int64_t t0 = blockIdx.x * per;
+  const int64_t t1 = min(ntiles, t0 + per);
+  double acc[MAXJ];
+#pragma unroll
+  for (int q = 0; q < MAXJ; ++q) acc[q] = 0.0;
+  double xx = 0.0;
+  for (int64_t t = t0; t < t1; ++t) {
+    const int64_t row = t * kTileRows + 2 * lane;
+    const double x0 = (row < P.n) ? __ldg(x + row) : 0.0;
+    const double x1 = (row + 1 < P.n) ? __ldg(x + row + 1) : 0.0;
+    if (wid == 0) xx = fma(x1, x1, fma(x0, x0, xx));
+#pragma unroll
+    for (int q = 0; q < MAXJ; ++q) {
+      const int j = wid + 8 * q;
+      if (j < c) {
+        const double2 u = __ldg(reinterpret_cast<const double2*>(U + (int64_t)(base + j) * P.ldu + row));
+        acc[q] = fma(u.y, x1, fma(u.x, x0, acc[q]));
+      }
+    }
+  }
+  double* mypart = sc.part + (int64_t)blockIdx.x * P.pstride;
+#pragma unroll
+  for (int q = 0; q < MAXJ; ++q) {
+    const int j = wid + 8 * q;
+    const double v = warp_sum(acc[q]);
+    if (lane == 0 && j < c) mypart[j] = v;
+  }
+  if (wid == 0) {
+    const double v = warp_sum(xx);
+    if (lane == 0) mypart[P.ccap] = v;
+  }
+  if (!last_cta_arrives(sc.counter, &s_last)) return;
+  for (int j = threadIdx.x; j <= c; j += blockDim.x) {
+    const int col = (j == c) ? P.ccap : j;
+    double s = 0.0;
+    for (int b = 0; b < (int)gridDim.x; ++b) s += sc.part[(int64_t)b * P.pstride + col];
+    if (j == c) sc.step->xx = s;
+    else sc.g[j] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Step A (one CTA): ell = W^T g, Pythagorean p, dependent test, restart /
+// reject branch (basis.py:112-139); y = W ell and gt = G^{-1} g for the
+// residual pass.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_step_a(StateView src, Scratch sc, IsvdParams P) {
+  __shared__ double red[32];
+  __shared__ int s_mode;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const IsvdHdr h = *src.hdr;
+  IsvdStep* st = sc.step;
+  const double xx = st->xx;
+  if (threadIdx.x == 0) {
+    int mode;
+    st->restart = 0;
+    st->write_slot = -1;
+    st->c_dot = 0;
+    st->norm = sqrt(xx);
+    if (h.status != 0 || !isfinite(xx)) {
+      mode = M_ERROR;
+    } else {
+      const bool at_cap = P.r_max >= 0 && h.r >= P.r_max;
+      if (h.r == 0 || (at_cap && P.cap_mode == 0)) {
+        st->restart = at_cap ? 1 : 0;
+        if (sqrt(xx) > P.tol_svd) {
+          mode = M_RESTART_ACCEPT;
+          st->write_slot = h.base + h.c;
+          st->c_dot = 0;
+        } else {
+          mode = M_REJECT;
+        }
+      } else {
+        mode = -1;  // decided below
+      }
+    }
+    s_mode = mode;
+  }
+  __syncthreads();
+  if (s_mode != -1) {
+    if (threadIdx.x == 0) st->mode = s_mode;
+    return;
+  }
+  const int r = h.r, c = h.c;
+  // ell_i = sum_j W[j, i] g[j]
+  for (int i = wid; i < r; i += nw) {
+    const double* wi = src.W + (int64_t)i * src.ldw;
+    double s = 0.0;
+    for (int j = lane; j < c; j += 32) s = fma(wi[j], sc.g[j], s);
+    s = warp_sum(s);
+    if (lane == 0) sc.ell[i] = s;
+  }
+  __syncthreads();
+  double part = 0.0;
+  for (int i = threadIdx.x; i < r; i += blockDim.x) part = fma(sc.ell[i], sc.ell[i], part);
+  const double ll = block_sum(part, red);
+  const double p_sq = xx - ll;
+  const double p = (p_sq > 0.0) ? sqrt(p_sq) : 0.0;
+  const bool dep = (p < P.tol_svd) || (p == 0.0) || ((int64_t)r >= P.n);
+  if (threadIdx.x == 0) {
+    st->p = p;
+    st->mode = dep ? M_NORMAL_DEP : M_NORMAL_INDEP;
+    if (!dep) {
+      st->write_slot = h.base + c;
+      st->c_dot = c;
+    }
+  }
+  // y = W ell (needed for the new W column), gt = g then solved in place
+  for (int j = threadIdx.x; j < c; j += blockDim.x) {
+    double s = 0.0;
+    for (int i = 0; i < r; ++i) s = fma(src.W[(int64_t)i * src.ldw + j], sc.ell[i], s);
+    sc.y[j] = s;
+    sc.gt[j] = sc.g[j];
+  }
+  __syncthreads();
+  if (!dep && wid == 0) {
+    warp_lower_solve(src.L, src.ldl, c, sc.gt);
+    warp_lower_t_solve(src.L, src.ldl, c, sc.gt);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Residual pass: r1 = x - U[:, base:base+c_dot] gt written to U[:, slot];
+// e = U[:, ...]^T r1 and rho2 = r1.r1.  Two phases per 64-row tile through
+// shared memory (row dots, then column dots against the fresh residual).
+// ---------------------------------------------------------------------------
+template <int MAXJ>
+__global__ void __launch_bounds__(kPassThreads) k_resid(double* __restrict__ U, const double* __restrict__ x,
+                                                         StateView src, Scratch sc, IsvdParams P) {
+  extern __shared__ double smem[];
+  __shared__ int s_last;
+  __shared__ double red[8];
+  const IsvdStep* st = sc.step;
+  const int mode = st->mode;
+  if (mode != M_NORMAL_INDEP && mode != M_RESTART_ACCEPT) return;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int cd = st->c_dot, slot = st->write_slot, base = src.hdr->base;
+  if (P.prof && blockIdx.x == 0 && threadIdx.x == 0)
+    atomicAdd(P.prof + 1, 8ull * (unsigned long long)P.n * (unsigned long long)(cd + 2));  // U, x; r1 out
+  double* tile = smem;                            // cd x 64 (column-major, 64 rows)
+  double* gts = tile + (int64_t)P.ccap * kTileRows;  // ccap
+  double* xs = gts + P.ccap;                      // 64
+  double* rs = xs + kTileRows;                    // 64
+  double* pp = rs + kTileRows;                    // 4 x 64 partial row dots
+  for (int j = threadIdx.x; j < cd; j += blockDim.x) gts[j] = sc.gt[j];
+  const int64_t ntiles = P.ldu / kTileRows;
+  const int64_t per = ceil_div(ntiles, gridDim.x);
+  const int64_t t0 = blockIdx.x * per;
+  const int64_t t1 = min(ntiles, t0 + per);
+  double acc[MAXJ];
+#pragma unroll
+  for (int q = 0; q < MAXJ; ++q) acc[q] = 0.0;
+  double rr = 0.0;
+  for (int64_t t = t0; t < t1; ++t) {
+    const int64_t row0 = t * kTileRows;
+    __syncthreads();  // previous tile fully consumed
+#pragma unroll
+    for (int q = 0; q < MAXJ; ++q) {
+      const int j = wid + 8 * q;
+      if (j < cd) {
+        const double2 u = __ldg(reinterpret_cast<const double2*>(U + (int64_t)(base + j) * P.ldu + row0 + 2 * lane));
+        reinterpret_cast<double2*>(tile + (int64_t)j * kTileRows)[lane] = u;
+      }
+    }
+    if (threadIdx.x < kTileRows) {
+      const int64_t row = row0 + threadIdx.x;
+      xs[threadIdx.x] = (row < P.n) ? __ldg(x + row) : 0.0;
+    }
+    __syncthreads();
+    {
+      const int rrow = threadIdx.x & (kTileRows - 1), quarter = threadIdx.x >> 6;
+      double s = 0.0;
+      for (int j = quarter; j < cd; j += 4) s = fma(tile[(int64_t)j * kTileRows + rrow], gts[j], s);
+      pp[quarter * kTileRows + rrow] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x < kTileRows) {
+      const int i = threadIdx.x;
+      const double dot = (pp[i] + pp[kTileRows + i]) + (pp[2 * kTileRows + i] + pp[3 * kTileRows + i]);
+      const double r1 = (row0 + i < P.n) ? xs[i] - dot : 0.0;
+      rs[i] = r1;
+      U[(int64_t)slot * P.ldu + row0 + i] = r1;
+      rr = fma(r1, r1, rr);
+    }
+    __syncthreads();
+    const double2 r2 = reinterpret_cast<const double2*>(rs)[lane];
+#pragma unroll
+    for (int q = 0; q < MAXJ; ++q) {
+      const int j = wid + 8 * q;
+      if (j < cd) {
+        const double2 u = reinterpret_cast<const double2*>(tile + (int64_t)j * kTileRows)[lane];
+        acc[q] = fma(u.y, r2.y, fma(u.x, r2.x, acc[q]));
+      }
+    }
+  }
+  double* mypart = sc.part + (int64_t)blockIdx.x * P.pstride;
+#pragma unroll
+  for (int q = 0; q < MAXJ; ++q) {
+    const int j = wid + 8 * q;
+    const double v = warp_sum(acc[q]);
+    if (lane == 0 && j < cd) mypart[j] = v;
+  }
+  const double rtot = block_sum(rr, red);
+  if (threadIdx.x == 0) mypart[P.ccap] = rtot;
+  if (!last_cta_arrives(sc.counter, &s_last)) return;
+  for (int j = threadIdx.x; j <= cd; j += blockDim.x) {
+    const int col = (j == cd) ? P.ccap : j;
+    double s = 0.0;
+    for (int b = 0; b < (int)gridDim.x; ++b) s += sc.part[(int64_t)b * P.pstride + col];
+    if (j == cd) sc.step->rho2 = s;
+    else sc.e[j] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Step B (one CTA, 1024 threads): everything in small space.
+//   * extend the Cholesky factor of G with the appended column (or fold an
+//     in-span residual back into U's existing columns)
+//   * bordered core Q = [[diag(sigma), ell], [0, p]] (basis.py:141-144) and its
+//     SVD by one-sided Jacobi on Q^T (accumulated rotations give W_bar)
+//   * sort descending + sign rule (linalg.py:31-38, 53)
+//   * W' = [W w_j] W_bar  (basis.py:150-158), truncation (basis.py:160-168)
+//   * drift |phi_0 . phi_last| = |(L^T w_0) . (L^T w_last)|, and on drift the
+//     small-space QR replacing linalg.qr(phi) (basis.py:170-174)
+// ---------------------------------------------------------------------------
+constexpr double kFoldTau = 1e-3;  // append r1 only if its out-of-span part is >= tau |r1|
+
+__global__ void __launch_bounds__(1024) k_step_b(StateView src, StateView dst, Scratch sc, IsvdParams P,
+                                                 int use_smem) {
+  extern __shared__ double smem[];
+  __shared__ double red[32];
+  __shared__ double s_misc[4];
+  __shared__ int s_int[8];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const IsvdHdr h = *src.hdr;
+  IsvdStep* st = sc.step;
+  const int mode = st->mode;
+  IsvdHdr o = h;
+  o.flags = 0;
+  o.p = 0.0;
+  o.drift = 0.0;
+  o.xnorm = st->norm;
+  if (mode == M_ERROR) {
+    if (threadIdx.x == 0) {
+      o.status = 1;
+      o.flags = F_ERROR;
+      *dst.hdr = o;
+      st->m = 0;
+      st->mkeep = -1;
+    }
+    return;
+  }
+  if (mode == M_REJECT || mode == M_RESTART_ACCEPT) {
+    if (threadIdx.x == 0) {
+      if (st->restart) { o.n_restarts += 1; o.flags |= F_RESTART; }
+      if (mode == M_REJECT) {
+        o.r = 0;
+        o.c = 0;
+        o.base = h.base + h.c;
+        o.n_rejected += 1;
+        o.flags |= F_REJECTED;
+        st->mkeep = 0;
+      } else {
+        o.r = 1;
+        o.c = 1;
+        o.base = st->write_slot;
+        dst.W[0] = 1.0 / st->norm;
+        dst.L[0] = sqrt(st->rho2);
+        dst.sigma[0] = st->norm;
+        st->mkeep = 1;
+      }
+      st->m = 0;
+      *dst.hdr = o;
+    }
+    return;
+  }
+  const bool dep = (mode == M_NORMAL_DEP);
+  const int r = h.r, c = h.c, m = r + 1;
+  const double p = st->p;
+  o.p = p;
+  // ---- 1. Cholesky factor of G for the (possibly) appended column ----------
+  int cn = c;
+  double* lvec = sc.work + 2 * (int64_t)P.work_stride;  // l = L^{-1} e, then G^{-1} e
+  if (!dep) {
+    for (int j = threadIdx.x; j < c; j += blockDim.x) lvec[j] = sc.e[j];
+    __syncthreads();
+    if (wid == 0) warp_lower_solve(src.L, src.ldl, c, lvec);
+    __syncthreads();
+    double part = 0.0;
+    for (int j = threadIdx.x; j < c; j += blockDim.x) part = fma(lvec[j], lvec[j], part);
+    const double ll = block_sum(part, red);
+    const double rho2 = st->rho2;
+    const double lam2 = rho2 - ll;
+    const bool app = (lam2 > kFoldTau * kFoldTau * rho2) && (st->write_slot < P.ccap) && (rho2 > 0.0);
+    if (threadIdx.x == 0) {
+      s_int[0] = app;
+      s_misc[0] = app ? sqrt(lam2) : 0.0;
+    }
+    __syncthreads();
+    if (s_int[0]) {
+      cn = c + 1;
+    } else if (wid == 0) {
+      warp_lower_t_solve(src.L, src.ldl, c, lvec);  // lvec = G^{-1} e
+    }
+    __syncthreads();
+  }
+  const bool appended = (!dep) && (cn == c + 1);
+  // copy L (lower) into dst, extended by the new row when appended
+  for (int64_t idx = threadIdx.x; idx < (int64_t)cn * cn; idx += blockDim.x) {
+    const int i = idx % cn, j = idx / cn;
+    double v = 0.0;
+    if (i < c && j < c) v = (i >= j) ? src.L[(int64_t)j * src.ldl + i] : 0.0;
+    else if (i == c && j < c) v = lvec[j];
+    else if (i == c && j == c) v = s_misc[0];
+    dst.L[(int64_t)j * dst.ldl + i] = v;
+  }
+  // new W column for j = (x - Phi ell)/p in U-coordinates (length cn)
+  double* wj = sc.work + 3 * (int64_t)P.work_stride;
+  if (!dep) {
+    for (int a = threadIdx.x; a < cn; a += blockDim.x) {
+      double v;
+      if (a < c) v = appended ? (sc.gt[a] - sc.y[a]) / p : (sc.gt[a] - sc.y[a] + lvec[a]) / p;
+      else v = 1.0 / p;
+      wj[a] = v;
+    }
+  }
+  // ---- 2. the bordered core and its SVD ------------------------------------
+  double* QT = use_smem ? smem : sc.work + 4 * (int64_t)P.work_stride;
+  double* WB = QT + (int64_t)m * m;
+  for (int64_t idx = threadIdx.x; idx < (int64_t)m * m; idx += blockDim.x) {
+    const int i = idx % m, j = idx / m;  // QT(i, j) = Q(j, i)
+    double v = 0.0;
+    if (i < r && j == i) v = src.sigma[i];
+    else if (i == r && j < r) v = sc.ell[j];
+    else if (i == r && j == r) v = dep ? 0.0 : p;
+    QT[idx] = v;
+    WB[idx] = (i == j) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  cta_jacobi(QT, m, m, m, WB, m, m, &s_int[1]);
+  // singular values = column norms of Q^T W_bar = V_bar Sigma
+  double* sv = sc.work;  // m
+  int* perm = reinterpret_cast<int*>(sc.work + (int64_t)P.work_stride);
+  cta_col_norms(QT, m, m, m, sv);
+  cta_argsort_desc(sv, m, perm);
+  // sorted, sign-fixed W_bar (kept in QT's place after extracting V_bar)
+  double* vbar = sc.vbar;  // m x m, ld = m (global scratch, read by the V kernel)
+  for (int k = wid; k < m; k += nw) {
+    const int srcc = perm[k];
+    const double* wcol = WB + (int64_t)srcc * m;
+    const int at = warp_argmax_abs(wcol, m);
+    const double sg = (wcol[at] < 0.0) ? -1.0 : 1.0;
+    const double s = sv[srcc];
+    for (int i = lane; i < m; i += 32) {
+      const double vv = (s > 0.0) ? QT[(int64_t)srcc * m + i] / s : (i == srcc ? 1.0 : 0.0);
+      vbar[(int64_t)k * m + i] = sg * vv;
+    }
+  }
+  __syncthreads();
+  // move sorted signed W_bar into QT (QT is dead now)
+  for (int k = wid; k < m; k += nw) {
+    const int srcc = perm[k];
+    const double* wcol = WB + (int64_t)srcc * m;
+    const int at = warp_argmax_abs(wcol, m);
+    const double sg = (wcol[at] < 0.0) ? -1.0 : 1.0;
+    for (int i = lane; i < m; i += 32) QT[(int64_t)k * m + i] = sg * wcol[i];
+  }
+  __syncthreads();
+  double* WS = QT;  // sorted W_bar, m x m
+  // ---- 3. truncation (basis.py:160-168) ------------------------------------
+  int mk = dep ? r : m;
+  bool trunc = false;
+  if (mk > 0 && sv[perm[mk - 1]] < P.tol_sv) { mk -= 1; trunc = true; }
+  if (P.r_max >= 0 && mk > P.r_max) { mk = P.r_max; trunc = true; }
+  // ---- 4. W' = W_b W_bar[:, :mk] -------------------------------------------
+  for (int64_t idx = threadIdx.x; idx < (int64_t)cn * mk; idx += blockDim.x) {
+    const int a = idx % cn, k = idx / cn;
+    double s = 0.0;
+    if (a < c) {
+      for (int b = 0; b < r; ++b) s = fma(src.W[(int64_t)b * src.ldw + a], WS[(int64_t)k * m + b], s);
+    }
+    if (!dep) s = fma(wj[a], WS[(int64_t)k * m + r], s);
+    dst.W[(int64_t)k * dst.ldw + a] = s;
+  }
+  for (int k = threadIdx.x; k < mk; k += blockDim.x) dst.sigma[k] = sv[perm[k]];
+  __syncthreads();
+  // ---- 5. drift test and small-space QR (basis.py:170-174) -----------------
+  bool did_qr = false;
+  double drift = 0.0;
+  if (mk > 1) {
+    double part = 0.0;
+    for (int i = threadIdx.x; i < cn; i += blockDim.x) {
+      double a0 = 0.0, a1 = 0.0;
+      for (int j = i; j < cn; ++j) {
+        const double l = dst.L[(int64_t)i * dst.ldl + j];
+        a0 = fma(l, dst.W[j], a0);
+        a1 = fma(l, dst.W[(int64_t)(mk - 1) * dst.ldw + j], a1);
+      }
+      part = fma(a0, a1, part);
+    }
+    drift = fabs(block_sum(part, red));
+    const double thr = fmin(P.tol_svd, 2.220446049250313e-16 * (double)P.n);
+    if (drift > thr) {
+      did_qr = true;
+      double* M = use_smem ? smem : sc.work + 4 * (int64_t)P.work_stride;  // cn x mk
+      __syncthreads();
+      for (int64_t idx = threadIdx.x; idx < (int64_t)cn * mk; idx += blockDim.x) {
+        const int i = idx % cn, k = idx / cn;
+        double s = 0.0;
+        for (int j = i; j < cn; ++j) s = fma(dst.L[(int64_t)i * dst.ldl + j], dst.W[(int64_t)k * dst.ldw + j], s);
+        M[(int64_t)k * cn + i] = s;
+      }
+      __syncthreads();
+      double* tau = sc.work;
+      double* beta = sc.work + P.work_stride;
+      cta_householder_qr(M, cn, cn, mk, nullptr, 0, tau, beta, red);
+      // W <- L^{-T} Q_s, column by column (one warp per column)
+      for (int k = wid; k < mk; k += nw) {
+        double* wk = dst.W + (int64_t)k * dst.ldw;
+        for (int i = lane; i < cn; i += 32) wk[i] = M[(int64_t)k * cn + i];
+        __syncwarp();
+        warp_lower_t_solve(dst.L, dst.ldl, cn, wk);
+      }
+      __syncthreads();
+    }
+  }
+  if (threadIdx.x == 0) {
+    o.r = mk;
+    o.c = cn;
+    o.drift = drift;
+    o.n_dependent += dep ? 1 : 0;
+    o.n_truncated += trunc ? 1 : 0;
+    o.flags = (dep ? F_DEPENDENT : 0) | (trunc ? F_TRUNCATED : 0) | (did_qr ? F_QR : 0) |
+              (appended ? F_APPENDED : 0) | ((!dep && !appended) ? F_FOLDED : 0);
+    *dst.hdr = o;
+    st->m = m;
+    st->mkeep = mk;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// V' = [[V, 0], [0, 1]] V_bar[:, :mkeep]  (basis.py:147-158); restart/reject
+// produce the fresh e_k column (basis.py:83-91).  Thread per row of V'.
+// ---------------------------------------------------------------------------
+constexpr int kVCols = 16;
+__global__ void __launch_bounds__(128) k_vupdate(StateView src, StateView dst, Scratch sc, IsvdParams P) {
+  const IsvdStep* st = sc.step;
+  const int mode = st->mode;
+  const int64_t k = P.k_new;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int col0 = blockIdx.y * kVCols;
+  if (mode == M_ERROR || mode == M_REJECT) return;
+  if (mode == M_RESTART_ACCEPT) {
+    if (col0 == 0 && i < k) dst.V[i] = (i == k - 1) ? 1.0 : 0.0;
+    return;
+  }
+  const int m = st->m, mk = st->mkeep, r = m - 1;
+  if (col0 >= mk || i >= k) return;
+  const double* vb = sc.vbar;
+  double acc[kVCols];
+#pragma unroll
+  for (int q = 0; q < kVCols; ++q) acc[q] = 0.0;
+  if (i < k - 1) {
+    for (int b = 0; b < r; ++b) {
+      const double v = src.V[(int64_t)b * src.ldv + i];
+#pragma unroll
+      for (int q = 0; q < kVCols; ++q) {
+        const int col = col0 + q;
+        if (col < mk) acc[q] = fma(v, vb[(int64_t)col * m + b], acc[q]);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < kVCols; ++q) {
+      const int col = col0 + q;
+      if (col < mk) acc[q] = vb[(int64_t)col * m + r];
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < kVCols; ++q) {
+    const int col = col0 + q;
+    if (col < mk) dst.V[(int64_t)col * dst.ldv + i] = acc[q];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Compaction prep (one CTA): L^T W = Q_c R_c;  T = L^{-T} Q_c;  new W = R_c,
+// new L = I, c = r, base = 0.  Phi = U W = (U T) R_c exactly.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_compact_prep(StateView src, StateView dst, Scratch sc, IsvdParams P,
+                                                       int use_smem) {
+  extern __shared__ double smem[];
+  __shared__ double red[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const IsvdHdr h = *src.hdr;
+  const int r = h.r, c = h.c;
+  IsvdHdr o = h;
+  if (h.status != 0 || r == 0) {
+    if (threadIdx.x == 0) {
+      if (h.status == 0) { o.c = 0; o.base = 0; }
+      *dst.hdr = o;
+      sc.step->m = 0;
+    }
+    return;
+  }
+  double* M = use_smem ? smem : sc.work + 4 * (int64_t)P.work_stride;  // c x r
+  for (int64_t idx = threadIdx.x; idx < (int64_t)c * r; idx += blockDim.x) {
+    const int i = idx % c, k = idx / c;
+    double s = 0.0;
+    for (int j = i; j < c; ++j) s = fma(src.L[(int64_t)i * src.ldl + j], src.W[(int64_t)k * src.ldw + j], s);
+    M[(int64_t)k * c + i] = s;
+  }
+  __syncthreads();
+  cta_householder_qr(M, c, c, r, dst.W, dst.ldw, sc.work, sc.work + P.work_stride, red);
+  for (int k = wid; k < r; k += nw) {
+    double* tk = sc.T + (int64_t)k * P.ccap;
+    for (int i = lane; i < c; i += 32) tk[i] = M[(int64_t)k * c + i];
+    __syncwarp();
+    warp_lower_t_solve(src.L, src.ldl, c, tk);
+  }
+  for (int64_t idx = threadIdx.x; idx < (int64_t)r * r; idx += blockDim.x) {
+    const int i = idx % r, j = idx / r;
+    dst.L[(int64_t)j * dst.ldl + i] = (i == j) ? 1.0 : 0.0;
+  }
+  for (int k = threadIdx.x; k < r; k += blockDim.x) dst.sigma[k] = src.sigma[k];
+  if (threadIdx.x == 0) {
+    o.c = r;
+    o.base = 0;
+    *dst.hdr = o;
+    sc.step->m = c;  // number of source columns for the GEMM
+    sc.step->mkeep = r;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Tall-skinny GEMM:  out(n x q) = A(n x p) * T(p x q)   (fp64 FMA, register
+// blocked 4 rows x 8 cols per thread, T staged through shared memory).
+// A column-major (lda, first column a_col0); out column-major (ldo) or
+// row-major (ldo = row stride) when out_row_major.  p, q read from device.
+// ---------------------------------------------------------------------------
+constexpr int kGemmRows = 128;  // rows per CTA tile
+constexpr int kGemmKc = 32;     // T chunk (rows of T) per smem stage
+
+__global__ void __launch_bounds__(256) k_tall_gemm(const double* __restrict__ A, int64_t lda,
+                                                   const int32_t* a_col0_dev, int a_col0_add,
+                                                   const double* __restrict__ T, int64_t ldt,
+                                                   const int32_t* p_dev, const int32_t* q_dev,
+                                                   int q_max, double* __restrict__ out, int64_t ldo,
+                                                   int out_row_major, int64_t n, int64_t nrows_pad) {
+  extern __shared__ double ts[];  // kGemmKc x q_max
+  const int p = *p_dev, q = *q_dev;
+  const int col0 = (a_col0_dev ? *a_col0_dev : 0) + a_col0_add;
+  if (q <= 0) return;
+  const int tx = threadIdx.x & 31;   // row lane: rows tx, tx+32, tx+64, tx+96
+  const int ty = threadIdx.x >> 5;   // column group: cols ty*8 .. ty*8+7 (+64 per pass)
+  for (int64_t rt = blockIdx.x; rt * kGemmRows < nrows_pad; rt += gridDim.x) {
+    const int64_t r0 = rt * kGemmRows;
+    for (int cb = 0; cb < q; cb += 64) {
+      double acc[4][8];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 8; ++b) acc[a][b] = 0.0;
+      for (int k0 = 0; k0 < p; k0 += kGemmKc) {
+        const int kc = min(kGemmKc, p - k0);
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < kGemmKc * 64; idx += blockDim.x) {
+          const int kk = idx % kGemmKc, cc = idx / kGemmKc;
+          const int col = cb + cc;
+          ts[cc * kGemmKc + kk] = (kk < kc && col < q) ? T[(int64_t)col * ldt + k0 + kk] : 0.0;
+        }
+        __syncthreads();
+        for (int kk = 0; kk < kc; ++kk) {
+          const double* acol = A + (int64_t)(col0 + k0 + kk) * lda + r0;
+          double av[4];
+#pragma unroll
+          for (int a = 0; a < 4; ++a) av[a] = __ldg(acol + tx + 32 * a);
+#pragma unroll
+          for (int b = 0; b < 8; ++b) {
+            const double t = ts[(ty * 8 + b) * kGemmKc + kk];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) acc[a][b] = fma(av[a], t, acc[a][b]);
+          }
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        const int col = cb + ty * 8 + b;
+        if (col >= q) continue;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          const int64_t row = r0 + tx + 32 * a;
+          if (out_row_major) {
+            if (row < n) out[row * ldo + col] = acc[a][b];
+          } else if (row < nrows_pad) {
+            out[(int64_t)col * ldo + row] = acc[a][b];
+          }
+        }
+      }
+    }
+  }
+}
+
+}  // namespace strom

@@ -1,0 +1,216 @@
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "runtime.cuh"
+#include "../../include/strom_b200.h"
+
+namespace strom {
+
+static thread_local std::string g_last_error;
+
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+static void configure_pool_once() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~0ull;  // keep freed blocks cached in the pool
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  });
+}
+
+DevMem::DevMem(size_t b, cudaStream_t s) : bytes(b), stream(s) {
+  configure_pool_once();
+  if (b == 0) return;
+  cudaError_t e = cudaMallocAsync(&ptr, b, s);
+  if (e != cudaSuccess) {
+    ptr = nullptr;
+    throw Error(kCudaError, std::string("cudaMallocAsync(") + std::to_string(b) + "): " + cudaGetErrorString(e));
+  }
+}
+
+DevMem::~DevMem() {
+  if (ptr) cudaFreeAsync(ptr, stream);
+}
+
+DevMemPtr dev_alloc(size_t bytes, cudaStream_t s, bool zero) {
+  auto m = std::make_shared<DevMem>(bytes, s);
+  if (zero && bytes) STROM_CUDA(cudaMemsetAsync(m->ptr, 0, bytes, s));
+  return m;
+}
+
+int sm_count() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+
+size_t max_smem_optin() {
+  static size_t n = [] {
+    int dev = 0, v = 48 * 1024;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return (size_t)v;
+  }();
+  return n;
+}
+
+// ------------------------------------------------------------------ profiling
+namespace {
+struct ProfState {
+  std::mutex mu;
+  bool on = false;
+  long long launches[P_NKINDS] = {};
+  double host_bytes[P_NKINDS] = {};
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pairs;
+  cudaEvent_t open[P_NKINDS] = {};
+  unsigned long long* dev_bytes = nullptr;
+};
+ProfState& prof() {
+  static ProfState p;
+  return p;
+}
+}  // namespace
+
+unsigned long long* prof_dev_bytes() {
+  auto& p = prof();
+  std::lock_guard<std::mutex> g(p.mu);
+  if (!p.dev_bytes) {
+    if (cudaMalloc(&p.dev_bytes, sizeof(unsigned long long) * P_NKINDS) != cudaSuccess) {
+      p.dev_bytes = nullptr;
+      throw Error(kCudaError, "cannot allocate the profile counters");
+    }
+    cudaMemset(p.dev_bytes, 0, sizeof(unsigned long long) * P_NKINDS);
+  }
+  return p.dev_bytes;
+}
+
+void prof_begin(int kind, cudaStream_t s) {
+  auto& p = prof();
+  std::lock_guard<std::mutex> g(p.mu);
+  p.launches[kind] += 1;
+  if (!p.on) return;
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  cudaEventRecord(e, s);
+  p.open[kind] = e;
+}
+
+void prof_end(int kind, cudaStream_t s) {
+  auto& p = prof();
+  std::lock_guard<std::mutex> g(p.mu);
+  if (!p.on || !p.open[kind]) return;
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  cudaEventRecord(e, s);
+  p.pairs.push_back({kind, {p.open[kind], e}});
+  p.open[kind] = nullptr;
+}
+
+void prof_add_bytes(int kind, double bytes) {
+  auto& p = prof();
+  std::lock_guard<std::mutex> g(p.mu);
+  p.host_bytes[kind] += bytes;
+}
+
+}  // namespace strom
+
+namespace {
+// fp64 tensor-pipe probe: every warp issues `iters` x 8 independent DMMA.
+__global__ void __launch_bounds__(256) k_dmma_probe(int iters, double* sink) {
+  const int lane = threadIdx.x & 31;
+  double c[8][2];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) c[q][0] = c[q][1] = 0.0;
+  double a = 1.0 + 1e-3 * lane, b = 1.0 - 1e-3 * lane;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(c[q][0]), "+d"(c[q][1]) : "d"(a), "d"(b));
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) s += c[q][0] + c[q][1];
+  if (s == 12345.678) sink[0] = s;
+}
+}  // namespace
+
+extern "C" {
+
+const char* strom_last_error(void) { return strom::g_last_error.c_str(); }
+
+int strom_abi_version(void) { return STROM_B200_ABI_VERSION; }
+
+int strom_device_synchronize(void) {
+  return strom::guarded([] { STROM_CUDA(cudaDeviceSynchronize()); });
+}
+
+void strom_profile_enable(int32_t on) {
+  auto& p = strom::prof();
+  std::lock_guard<std::mutex> g(p.mu);
+  p.on = on != 0;
+}
+
+int strom_profile_reset(void) {
+  return strom::guarded([] {
+    unsigned long long* d = strom::prof_dev_bytes();
+    auto& p = strom::prof();
+    std::lock_guard<std::mutex> g(p.mu);
+    for (auto& pr : p.pairs) {
+      cudaEventDestroy(pr.second.first);
+      cudaEventDestroy(pr.second.second);
+    }
+    p.pairs.clear();
+    for (int k = 0; k < strom::P_NKINDS; ++k) {
+      p.launches[k] = 0;
+      p.host_bytes[k] = 0.0;
+      p.open[k] = nullptr;
+    }
+    STROM_CUDA(cudaMemset(d, 0, sizeof(unsigned long long) * strom::P_NKINDS));
+  });
+}
+
+int strom_profile_read(int32_t nkinds, int64_t* launches, double* ms, double* bytes) {
+  return strom::guarded([&] {
+    unsigned long long* d = strom::prof_dev_bytes();
+    STROM_CUDA(cudaDeviceSynchronize());
+    unsigned long long db[strom::P_NKINDS];
+    STROM_CUDA(cudaMemcpy(db, d, sizeof(db), cudaMemcpyDeviceToHost));
+    auto& p = strom::prof();
+    std::lock_guard<std::mutex> g(p.mu);
+    const int nk = nkinds < strom::P_NKINDS ? nkinds : strom::P_NKINDS;
+    for (int k = 0; k < nk; ++k) {
+      if (launches) launches[k] = p.launches[k];
+      if (bytes) bytes[k] = p.host_bytes[k] + (double)db[k];
+      if (ms) ms[k] = 0.0;
+    }
+    if (ms)
+      for (auto& pr : p.pairs) {
+        float t = 0.f;
+        if (pr.first < nk && cudaEventElapsedTime(&t, pr.second.first, pr.second.second) == cudaSuccess)
+          ms[pr.first] += t;
+      }
+  });
+}
+
+int strom_fp64_probe(int32_t iters, int32_t ctas_per_sm, void* stream, double* flops_out) {
+  return strom::guarded([&] {
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int grid = strom::sm_count() * (ctas_per_sm > 0 ? ctas_per_sm : 4);
+    auto sink = strom::dev_alloc(8, s, false);
+    k_dmma_probe<<<grid, 256, 0, s>>>(iters, sink->as<double>());
+    STROM_LAUNCH_CHECK();
+    // 8 DMMA (8x8x4 = 256 FMA = 512 flop) per warp per iteration
+    *flops_out = (double)grid * 8.0 * (double)iters * 8.0 * 512.0;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,257 @@
+// Single-CTA dense fp64 routines for the small matrices of the hot path:
+// the bordered (r+1)^2 iSVD core, the temporal snapshot blocks, the small-space
+// QR that replaces the reference's tall Householder QR, triangular solves.
+//
+// Every routine is called by ALL threads of the CTA (they contain
+// __syncthreads) and works on column-major arrays in shared or global memory.
+#pragma once
+
+#include "common.cuh"
+
+namespace strom {
+
+// ---------------------------------------------------------------------------
+// One-sided (Hestenes) Jacobi on the columns of A (rows x cols, col-major):
+// A <- A J, V <- V J until all column pairs are orthogonal to eps*sqrt(rows).
+// Parallel round-robin ordering: each round has ceil(cols/2) disjoint pairs,
+// one warp per pair (warps loop over pairs).  V may be nullptr.
+// `flag` is a shared int used for the convergence vote.
+// Returns the number of sweeps performed.
+// ---------------------------------------------------------------------------
+__device__ inline int cta_jacobi(double* A, int lda, int rows, int cols, double* V, int ldv,
+                                 int vrows, int* flag, int max_sweeps = 40) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (cols < 2) return 0;
+  const int ne = cols + (cols & 1);  // even number of players (one dummy if odd)
+  const int npairs = ne / 2;
+  const double tol = 2.220446049250313e-16 * sqrt((double)rows);
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    if (threadIdx.x == 0) *flag = 0;
+    __syncthreads();
+    for (int rnd = 0; rnd < ne - 1; ++rnd) {
+      for (int pk = wid; pk < npairs; pk += nw) {
+        int a, b;
+        if (pk == 0) {
+          a = rnd;
+          b = ne - 1;
+        } else {
+          a = (rnd + pk) % (ne - 1);
+          b = (rnd - pk + (ne - 1)) % (ne - 1);
+        }
+        if (a > b) { int t = a; a = b; b = t; }
+        if (b >= cols) continue;  // dummy player
+        double* ca = A + (int64_t)a * lda;
+        double* cb = A + (int64_t)b * lda;
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int i = lane; i < rows; i += 32) {
+          const double x = ca[i], y = cb[i];
+          al = fma(x, x, al);
+          be = fma(y, y, be);
+          ga = fma(x, y, ga);
+        }
+        al = warp_sum(al);
+        be = warp_sum(be);
+        ga = warp_sum(ga);
+        if (al == 0.0 || be == 0.0) continue;
+        if (fabs(ga) <= tol * sqrt(al) * sqrt(be)) continue;
+        const double zeta = (be - al) / (2.0 * ga);
+        const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+        const double c = 1.0 / sqrt(fma(t, t, 1.0));
+        const double s = c * t;
+        for (int i = lane; i < rows; i += 32) {
+          const double x = ca[i], y = cb[i];
+          ca[i] = c * x - s * y;
+          cb[i] = s * x + c * y;
+        }
+        if (V) {
+          double* va = V + (int64_t)a * ldv;
+          double* vb = V + (int64_t)b * ldv;
+          for (int i = lane; i < vrows; i += 32) {
+            const double x = va[i], y = vb[i];
+            va[i] = c * x - s * y;
+            vb[i] = s * x + c * y;
+          }
+        }
+        if (lane == 0) *flag = 1;
+      }
+      __syncthreads();
+    }
+    const int any = *flag;
+    __syncthreads();
+    if (!any) break;
+  }
+  return sweep;
+}
+
+// Column norms of A into out[cols] (one warp per column).
+__device__ inline void cta_col_norms(const double* A, int lda, int rows, int cols, double* out) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int j = wid; j < cols; j += nw) {
+    const double* cj = A + (int64_t)j * lda;
+    double s = 0.0;
+    for (int i = lane; i < rows; i += 32) s = fma(cj[i], cj[i], s);
+    s = warp_sum(s);
+    if (lane == 0) out[j] = sqrt(s);
+  }
+  __syncthreads();
+}
+
+// Stable descending argsort of vals[0..n) into perm (n <= blockDim.x).
+// Ties keep the lower index first (rank = #greater + #equal-with-lower-index).
+__device__ inline void cta_argsort_desc(const double* vals, int n, int* perm) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double v = vals[i];
+    int rank = 0;
+    for (int j = 0; j < n; ++j) {
+      const double u = vals[j];
+      rank += (u > v) || (u == v && j < i);
+    }
+    perm[rank] = i;
+  }
+  __syncthreads();
+}
+
+// Index of the largest |w[i]| (first on ties), computed by one warp.
+__device__ inline int warp_argmax_abs(const double* w, int n) {
+  const int lane = threadIdx.x & 31;
+  double best = -1.0;
+  int bi = 0x7fffffff;
+  for (int i = lane; i < n; i += 32) {
+    const double a = fabs(w[i]);
+    if (a > best) { best = a; bi = i; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+  }
+  return bi;
+}
+
+// ---------------------------------------------------------------------------
+// Householder QR of M (rows x cols, rows >= cols, col-major, ld), overwritten
+// by the explicit thin Q with diag(R) >= 0 (zero pivots count as +1), as
+// linalg.qr does (linalg.py:60-72).  If R != nullptr the upper triangle of R
+// (ldr) receives the matching R.  tau/beta: shared scratch of `cols` doubles.
+// ---------------------------------------------------------------------------
+__device__ inline void cta_householder_qr(double* M, int ld, int rows, int cols, double* R, int ldr,
+                                          double* tau, double* beta, double* red) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int j = 0; j < cols; ++j) {
+    double* x = M + (int64_t)j * ld;
+    double s = 0.0;
+    for (int i = j + 1 + threadIdx.x; i < rows; i += blockDim.x) s = fma(x[i], x[i], s);
+    s = block_sum(s, red);
+    const double x0 = x[j];
+    __syncthreads();
+    const double nrm = sqrt(fma(x0, x0, s));
+    double bt, tj, scal;
+    if (s == 0.0) {  // already upper-triangular in this column: H = I
+      bt = x0;
+      tj = 0.0;
+      scal = 0.0;
+    } else {
+      bt = (x0 >= 0.0) ? -nrm : nrm;
+      tj = (bt - x0) / bt;
+      scal = 1.0 / (x0 - bt);
+    }
+    for (int i = j + 1 + threadIdx.x; i < rows; i += blockDim.x) x[i] *= scal;
+    if (threadIdx.x == 0) {
+      tau[j] = tj;
+      beta[j] = bt;
+      x[j] = 1.0;  // implicit unit head of v
+    }
+    __syncthreads();
+    if (tj != 0.0) {
+      for (int k = j + 1 + wid; k < cols; k += nw) {
+        double* y = M + (int64_t)k * ld;
+        double d = 0.0;
+        for (int i = j + lane; i < rows; i += 32) d = fma(x[i], y[i], d);
+        d = warp_sum(d) * tj;
+        for (int i = j + lane; i < rows; i += 32) y[i] = fma(-d, x[i], y[i]);
+      }
+    }
+    __syncthreads();
+  }
+  // R (before sign fix) lives in the strict upper triangle of M plus beta.
+  if (R) {
+    for (int idx = threadIdx.x; idx < cols * cols; idx += blockDim.x) {
+      const int i = idx % cols, k = idx / cols;
+      double v = 0.0;
+      if (i < k) v = M[(int64_t)k * ld + i];
+      else if (i == k) v = beta[k];
+      R[(int64_t)k * ldr + i] = v;
+    }
+  }
+  __syncthreads();
+  // Form Q = H_0 ... H_{cols-1} [I; 0] by backward accumulation, in place:
+  // column j's Householder vector is consumed before column j becomes Q's.
+  for (int j = cols - 1; j >= 0; --j) {
+    double* v = M + (int64_t)j * ld;  // v[j] == 1, v[j+1..] stored, v[<j] = R part
+    const double tj = tau[j];
+    // columns k > j already hold Q entries (rows >= j+1 ... ), apply H_j to them
+    for (int k = j + 1 + wid; k < cols; k += nw) {
+      double* y = M + (int64_t)k * ld;
+      double d = 0.0;
+      for (int i = j + 1 + lane; i < rows; i += 32) d = fma(v[i], y[i], d);
+      // y[j] is 0 in [I;0] history (row j of columns k>j before applying H_j)
+      d = warp_sum(d) * tj;
+      for (int i = j + 1 + lane; i < rows; i += 32) y[i] = fma(-d, v[i], y[i]);
+      if (lane == 0) y[j] = -d;
+    }
+    __syncthreads();
+    // column j itself: H_j e_j = e_j - tau v  (v_j = 1)
+    for (int i = threadIdx.x; i < rows; i += blockDim.x) {
+      if (i < j) v[i] = 0.0;
+      else if (i == j) v[i] = 1.0 - tj;
+      else v[i] = -tj * v[i];
+    }
+    __syncthreads();
+  }
+  // diag(R) >= 0: flip Q column j (and R row j) where beta_j < 0.
+  for (int idx = threadIdx.x; idx < rows * cols; idx += blockDim.x) {
+    const int i = idx % rows, j = idx / rows;
+    if (beta[j] < 0.0) M[(int64_t)j * ld + i] = -M[(int64_t)j * ld + i];
+  }
+  if (R) {
+    for (int idx = threadIdx.x; idx < cols * cols; idx += blockDim.x) {
+      const int i = idx % cols, k = idx / cols;
+      if (beta[i] < 0.0) R[(int64_t)k * ldr + i] = -R[(int64_t)k * ldr + i];
+    }
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// Warp-level triangular solves with a lower-triangular L (n x n, col-major).
+// x holds b on entry and the solution on exit (global or shared); executed by
+// ONE warp.  n is small (<= a few hundred).
+// ---------------------------------------------------------------------------
+__device__ inline void warp_lower_solve(const double* L, int ld, int n, double* x) {
+  const int lane = threadIdx.x & 31;
+  for (int j = 0; j < n; ++j) {
+    double xj = 0.0;
+    if (lane == 0) xj = x[j] / L[(int64_t)j * ld + j];
+    xj = __shfl_sync(0xffffffffu, xj, 0);
+    if (lane == 0) x[j] = xj;
+    for (int i = j + 1 + lane; i < n; i += 32) x[i] = fma(-L[(int64_t)j * ld + i], xj, x[i]);
+    __syncwarp();
+  }
+}
+
+// Solve L^T x = b (backward), one warp.
+__device__ inline void warp_lower_t_solve(const double* L, int ld, int n, double* x) {
+  const int lane = threadIdx.x & 31;
+  for (int j = n - 1; j >= 0; --j) {
+    // x_j = (b_j - sum_{i>j} L[i,j] x_i) / L[j,j]
+    double s = 0.0;
+    for (int i = j + 1 + lane; i < n; i += 32) s = fma(L[(int64_t)j * ld + i], x[i], s);
+    s = warp_sum(s);
+    if (lane == 0) x[j] = (x[j] - s) / L[(int64_t)j * ld + j];
+    __syncwarp();
+  }
+}
+
+}  // namespace strom

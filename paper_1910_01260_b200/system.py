@@ -1,0 +1,120 @@
+"""Input containers of the hot path (reference system.py:30-103).
+
+``TimeGrid`` and ``LinearDynamicalSystem`` hold the same fields and validate
+them the same way as the reference; in addition they cache one device copy of
+their arrays (CSR A with int32/int64 indices, dense B, C, x0, dt) so repeated
+operator builds read HBM-resident operands.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Callable
+
+import numpy as np
+import scipy.sparse as sp
+import torch
+
+from ._tensors import F64, device
+
+InputSignal = Callable[[int], np.ndarray]
+
+
+@dataclass(frozen=True)
+class TimeGrid:
+    """Positive step sizes dt_k, k = 1..n_steps (system.py:30-62)."""
+
+    dt: np.ndarray
+
+    def __post_init__(self):
+        dt = self.dt
+        if isinstance(dt, torch.Tensor):
+            dt = dt.detach().cpu().numpy()
+        dt = np.atleast_1d(np.asarray(dt, dtype=float))
+        if dt.ndim != 1 or dt.size == 0:
+            raise ValueError("time grid needs at least one step")
+        if not np.all(dt > 0.0):
+            raise ValueError("all step sizes must be positive")
+        object.__setattr__(self, "dt", dt)
+        object.__setattr__(self, "_dev", None)
+
+    @classmethod
+    def uniform(cls, dt: float, n_steps: int) -> "TimeGrid":
+        return cls(np.full(n_steps, float(dt)))
+
+    @property
+    def n_steps(self) -> int:
+        return self.dt.size
+
+    @property
+    def total_time(self) -> float:
+        return float(self.dt.sum())
+
+    @property
+    def times(self) -> np.ndarray:
+        return np.cumsum(self.dt)
+
+    @property
+    def is_uniform(self) -> bool:
+        return bool(np.all(self.dt == self.dt[0]))
+
+    def dt_device(self) -> torch.Tensor:
+        if self._dev is None:
+            object.__setattr__(self, "_dev", torch.as_tensor(self.dt, dtype=F64, device=device()))
+        return self._dev
+
+
+@dataclass
+class LinearDynamicalSystem:
+    """Operators of one parameter instance of x' = A x + B f, y = C^T x (system.py:65-103)."""
+
+    a: sp.spmatrix
+    b: sp.spmatrix
+    c: np.ndarray
+    x0: np.ndarray
+    input_signal: InputSignal
+    constant_input: bool = False
+    param: dict = field(default_factory=dict)
+
+    def __post_init__(self):
+        self.a = sp.csr_array(self.a)
+        self.b = sp.csr_array(self.b)
+        self.c = np.atleast_2d(np.asarray(self.c, dtype=float))
+        self.x0 = np.asarray(self.x0, dtype=float)
+        n = self.a.shape[0]
+        if self.a.shape != (n, n):
+            raise ValueError(f"A must be square, got {self.a.shape}")
+        if self.b.shape[0] != n or self.c.shape[0] != n or self.x0.shape != (n,):
+            raise ValueError("operator dimensions are inconsistent")
+        self._dev = None
+
+    @property
+    def n_states(self) -> int:
+        return self.a.shape[0]
+
+    @property
+    def n_inputs(self) -> int:
+        return self.b.shape[1]
+
+    @property
+    def n_outputs(self) -> int:
+        return self.c.shape[1]
+
+    def device_arrays(self) -> dict:
+        """HBM-resident copies: CSR (indptr, indices, data, index_bits), B|C dense, x0."""
+        if self._dev is None:
+            dev = device()
+            a = self.a
+            a.sort_indices()
+            big = a.nnz >= 2**31 or a.shape[0] >= 2**31
+            it = np.int64 if big else np.int32
+            self._dev = dict(
+                indptr=torch.as_tensor(a.indptr.astype(it), device=dev),
+                indices=torch.as_tensor(a.indices.astype(it), device=dev),
+                data=torch.as_tensor(a.data.astype(np.float64), device=dev),
+                index_bits=64 if big else 32,
+                b=torch.as_tensor(self.b.toarray(), dtype=F64, device=dev),
+                c=torch.as_tensor(self.c, dtype=F64, device=dev),
+                x0=torch.as_tensor(self.x0, dtype=F64, device=dev),
+            )
+        return self._dev
