@@ -90,6 +90,7 @@ typedef struct {
   int64_t r_max;      /* -1 = uncapped                                    */
   int32_t cap_mode;   /* STROM_CAP_*                                      */
   int32_t pad;
+  double last_p_sq;   /* unclamped x.x - ell.ell of the last update (basis.py:136) */
 } strom_isvd_info;
 
 /* isvd_init (basis.py:65-102): start the stream at its k-th column x_dev[n]. */
@@ -129,6 +130,14 @@ int strom_isvd_load_factored(int64_t n, int64_t k, int64_t c, int64_t r, const d
                              const double* sigma_dev, const double* v_dev, double tol_svd, double tol_sv,
                              int64_t r_max, int32_t cap_mode, const int32_t* counters4_host, void* stream,
                              strom_isvd** out);
+
+/* The device representation phi = U W (U[:, 0:c] n x c with ld n, W c x r
+ * with ld c, L = chol(U^T U) c x c with ld c), for invariant checks.
+ * Synchronizes.  Any output may be NULL. */
+int strom_isvd_factors(strom_isvd* h, double* u_dev, double* w_dev, double* l_dev, void* stream);
+
+/* Diagnostics: step-B phase timestamps (clock64, 8 slots) into dev_buf; NULL disables. */
+void strom_debug_tprobe(long long* dev_buf);
 
 void strom_isvd_free(strom_isvd* h);
 

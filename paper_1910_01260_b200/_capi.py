@@ -32,6 +32,7 @@ class IsvdInfo(C.Structure):
         ("flags", i32), ("status", i32),
         ("last_p", dbl), ("last_drift", dbl), ("last_xnorm", dbl),
         ("tol_svd", dbl), ("tol_sv", dbl), ("r_max", i64), ("cap_mode", i32), ("pad", i32),
+        ("last_p_sq", dbl),
     ]
 
 
@@ -51,6 +52,8 @@ _PROTOS = {
     "strom_isvd_load": (C.c_int, [i64, i64, i64, vp, vp, vp, dbl, dbl, i64, i32, P_I32, vp, C.POINTER(vp)]),
     "strom_isvd_load_factored": (C.c_int, [i64, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, vp,
                                            dbl, dbl, i64, i32, P_I32, vp, C.POINTER(vp)]),
+    "strom_isvd_factors": (C.c_int, [vp, vp, vp, vp, vp]),
+    "strom_debug_tprobe": (None, [vp]),
     "strom_isvd_free": (None, [vp]),
     # temporal bases (basis.py:275-302)
     "strom_temporal_bases": (C.c_int, [vp, i64, i64, i64, i64, i64, i64, vp, vp, vp, vp]),

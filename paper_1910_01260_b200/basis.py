@@ -169,6 +169,18 @@ class SvdState:
             self._cache.update(phi=phi, sigma=sig, v=v)
         return self._cache
 
+    def factors(self):
+        """(U, W, L) of the device representation phi = U W, L = chol(U^T U) (diagnostics)."""
+        inf = self.info()
+        dev = device()
+        c, r = inf.ncols_u, inf.rank
+        u = torch.empty((c, self.n), dtype=F64, device=dev)
+        w = torch.empty((r, c), dtype=F64, device=dev)
+        lm = torch.empty((c, c), dtype=F64, device=dev)
+        capi.call("strom_isvd_factors", self._h, u.data_ptr() if c else None, w.data_ptr() if c and r else None,
+                  lm.data_ptr() if c else None, capi.stream_ptr())
+        return u.t(), w.t(), lm.t()
+
     @property
     def phi(self) -> torch.Tensor:
         return self._export()["phi"]

@@ -6,6 +6,7 @@
 #include <vector>
 
 #include "../../include/strom_b200.h"
+#include "gram.cuh"
 #include "isvd_kernels.cuh"
 #include "runtime.cuh"
 
@@ -50,6 +51,12 @@ __global__ void k_set_hdr(IsvdHdr* h, int32_t r, int32_t c, int32_t base, int32_
   o.n_truncated = tr;
   o.n_restarts = rs;
   *h = o;
+}
+
+__global__ void __launch_bounds__(1024) k_lower_inverse(const double* L, int ld, const IsvdHdr* h_c_from,
+                                                       int c_fixed, double* Li) {
+  const int c = h_c_from ? h_c_from->c : c_fixed;
+  cta_lower_inverse(L, ld, c, Li, ld);
 }
 
 // In-place lower Cholesky of A (c x c, ld); sets *status = 1 on a non-positive pivot.
@@ -99,6 +106,8 @@ inline int maxj_for(int ccap) {
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+long long* g_tprobe = nullptr;  // step-B phase timestamps (strom_debug_tprobe)
+
 // ------------------------------------------------------------------ state
 struct UBuf {
   DevMemPtr mem;
@@ -129,7 +138,8 @@ struct strom_isvd {
 
 namespace {
 
-int32_t slack_for(int32_t rcap) { return std::max<int32_t>(16, rcap); }
+// ccap = rcap + 1 + slack; 2 rcap keeps c_cap = 128 (8 columns per warp) at rank 64
+int32_t slack_for(int32_t rcap) { return std::max<int32_t>(16, rcap - 1); }
 
 Caps make_caps(int64_t n, int32_t r_max, int32_t want_r, int64_t k) {
   Caps c;
@@ -149,13 +159,14 @@ void alloc_small(strom_isvd* h, cudaStream_t s) {
   const size_t wsz = (size_t)c.ccap * (c.rcap + 1);
   const size_t lsz = (size_t)c.ccap * c.ccap;
   const size_t ssz = (size_t)c.rcap + 2;
-  const size_t bytes = 256 + 8 * (wsz + lsz + ssz);
+  const size_t bytes = 256 + 8 * (wsz + 2 * lsz + ssz);
   h->small = dev_alloc(bytes, s, true);
   char* p = h->small->as<char>();
   h->view.hdr = reinterpret_cast<IsvdHdr*>(p);
   h->view.W = reinterpret_cast<double*>(p + 256);
   h->view.L = h->view.W + wsz;
-  h->view.sigma = h->view.L + lsz;
+  h->view.Li = h->view.L + lsz;
+  h->view.sigma = h->view.Li + lsz;
   h->view.ldw = c.ccap;
   h->view.ldl = c.ccap;
 }
@@ -207,11 +218,11 @@ ScratchMem make_scratch(int64_t ldu, const Caps& c, cudaStream_t s) {
   m.pstride = (int)round_up(c.ccap + 2, 8);
   const int64_t rc2 = c.rcap + 2;
   m.work_stride = (int)round_up(std::max<int64_t>(c.ccap, rc2), 32);
-  m.work_elems = 4 * (size_t)m.work_stride +
-                 std::max<size_t>(2 * rc2 * rc2, (size_t)c.ccap * rc2);
-  const size_t n_g = c.ccap, n_ell = rc2, n_vbar = rc2 * rc2, n_T = (size_t)c.ccap * rc2;
+  m.work_elems = 4 * (size_t)m.work_stride + 3 * rc2 * rc2 + 16 * (size_t)m.work_stride +
+                 (size_t)c.ccap * rc2;  // step B's layout (global fallback)
+  const size_t n_g = round_up(c.ccap, 2), n_ell = round_up(rc2, 2), n_vbar = rc2 * rc2, n_T = (size_t)c.ccap * rc2;
   const size_t n_part = (size_t)m.grid * m.pstride;
-  size_t total = 4 * n_g + n_ell + n_vbar + m.work_elems + n_T + n_part;
+  size_t total = 7 * n_g + n_ell + n_vbar + m.work_elems + n_T + n_part;
   total = round_up(total, 32);
   const size_t bytes = total * 8 + 256 + 64;
   m.mem = dev_alloc(bytes, s, true);
@@ -220,6 +231,9 @@ ScratchMem make_scratch(int64_t ldu, const Caps& c, cudaStream_t s) {
   m.sc.gt = p; p += n_g;
   m.sc.y = p; p += n_g;
   m.sc.e = p; p += n_g;
+  m.sc.h = p; p += n_g;
+  m.sc.lvec = p; p += n_g;
+  m.sc.tmp = p; p += n_g;
   m.sc.ell = p; p += n_ell;
   m.sc.vbar = p; p += n_vbar;
   m.sc.work = p; p += m.work_elems;
@@ -245,6 +259,7 @@ IsvdParams make_params(const strom_isvd* h, const ScratchMem& m, int64_t k_new, 
   P.pstride = m.pstride;
   P.work_stride = m.work_stride;
   P.prof = prof_dev_bytes();
+  P.tprobe = g_tprobe;
   return P;
 }
 
@@ -269,32 +284,34 @@ void launch_proj(int ccap, const double* U, const double* x, const StateView& v,
 
 template <int MAXJ>
 void launch_resid_t(double* U, const double* x, const StateView& v, const ScratchMem& m, const IsvdParams& P,
-                    cudaStream_t s) {
-  const size_t smem = ((size_t)kTileRows * P.ccap + P.ccap + 3 * kTileRows + 4 * kTileRows) * 8;
+                    cudaStream_t s, int phase) {
+  const size_t smem = ((size_t)kTileRows * P.ccap + P.ccap + 1 + 3 * kTileRows + 4 * kTileRows) * 8;
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
     STROM_CUDA(cudaFuncSetAttribute(k_resid<MAXJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = smem;
   }
   ProfScope ps(P_RESID, s);
-  k_resid<MAXJ><<<m.grid, kPassThreads, smem, s>>>(U, x, v, m.sc, P);
+  k_resid<MAXJ><<<m.grid, kPassThreads, smem, s>>>(U, x, v, m.sc, P, phase);
   STROM_LAUNCH_CHECK();
 }
 
 void launch_resid(int ccap, double* U, const double* x, const StateView& v, const ScratchMem& m,
-                  const IsvdParams& P, cudaStream_t s) {
+                  const IsvdParams& P, cudaStream_t s, int phase = 0) {
   switch (maxj_for(ccap)) {
-    case 2: launch_resid_t<2>(U, x, v, m, P, s); break;
-    case 4: launch_resid_t<4>(U, x, v, m, P, s); break;
-    case 8: launch_resid_t<8>(U, x, v, m, P, s); break;
-    case 16: launch_resid_t<16>(U, x, v, m, P, s); break;
-    default: launch_resid_t<32>(U, x, v, m, P, s); break;
+    case 2: launch_resid_t<2>(U, x, v, m, P, s, phase); break;
+    case 4: launch_resid_t<4>(U, x, v, m, P, s, phase); break;
+    case 8: launch_resid_t<8>(U, x, v, m, P, s, phase); break;
+    case 16: launch_resid_t<16>(U, x, v, m, P, s, phase); break;
+    default: launch_resid_t<32>(U, x, v, m, P, s, phase); break;
   }
 }
 
 size_t small_kernel_smem(const Caps& c, int* use_smem) {
+  // step B layout: 3 m^2 + 16 ms (secular work) + ccap m (staged W_b / QR's M)
   const size_t m = c.rcap + 1;
-  const size_t need = std::max(2 * m * m, (size_t)c.ccap * (c.rcap + 1)) * 8;
+  const size_t ms = round_up(std::max<int64_t>(c.ccap, c.rcap + 2), 32);
+  const size_t need = (3 * m * m + 16 * ms + (size_t)c.ccap * m) * 8;
   const size_t limit = max_smem_optin() - 8 * 1024;
   *use_smem = need <= limit ? 1 : 0;
   return *use_smem ? need : 0;
@@ -310,7 +327,7 @@ void launch_step_b(const StateView& src, const StateView& dst, const ScratchMem&
     configured = smem;
   }
   ProfScope ps(P_STEP_B, s);
-  k_step_b<<<1, 1024, smem, s>>>(src, dst, m.sc, P, use_smem);
+  k_step_b<<<1, kSmallThreads, smem, s>>>(src, dst, m.sc, P, use_smem);
   STROM_LAUNCH_CHECK();
 }
 
@@ -324,7 +341,7 @@ void launch_compact_prep(const StateView& src, const StateView& dst, const Scrat
     configured = smem;
   }
   ProfScope ps(P_COMPACT, s);
-  k_compact_prep<<<1, 1024, smem, s>>>(src, dst, m.sc, P, use_smem);
+  k_compact_prep<<<1, kSmallThreads, smem, s>>>(src, dst, m.sc, P, use_smem);
   STROM_LAUNCH_CHECK();
 }
 
@@ -336,6 +353,39 @@ void launch_tall_gemm(const double* A, int64_t lda, const int32_t* col0_dev, con
   ProfScope ps(P_TALL_GEMM, s);
   k_tall_gemm<<<grid, 256, kGemmKc * 64 * 8, s>>>(A, lda, col0_dev, 0, T, ldt, p_dev, q_dev, 0, out, ldo,
                                                   row_major ? 1 : 0, n, nrows_pad);
+  STROM_LAUNCH_CHECK();
+}
+
+// L = chol(A[:, col0:col0+q]^T A[:, col0:col0+q]) with the DMMA tall Gram.
+// q is read on the device (q_dev) or fixed; the Cholesky reads c from hdr_c.
+void gram_cholesky(const double* A, int64_t lda, const int32_t* col0_dev, const int32_t* q_dev, int q_fixed,
+                   int qmax, int64_t n, double* L, double* Li, int ldl, const IsvdHdr* hdr_c, int* status_dev,
+                   cudaStream_t s) {
+  const int QP = (int)round_up(std::max(qmax, 1), 8);
+  const int64_t ntiles = ceil_div(n, kGramRows);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)sm_count() * 2));
+  auto part = dev_alloc((size_t)grid * QP * QP * 8, s, false);
+  const size_t smem = (size_t)QP * kGramLd * 8;
+  ProfScope ps(P_OTHER, s);
+  if (QP <= 64) {
+    k_tall_gram<1, 8><<<grid, 256, smem, s>>>(A, lda, col0_dev, q_dev, q_fixed, n, part->as<double>(), QP);
+  } else if (QP <= 128) {
+    static bool cfg = false;
+    if (!cfg) {
+      STROM_CUDA(cudaFuncSetAttribute(k_tall_gram<2, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+      cfg = true;
+    }
+    k_tall_gram<2, 16><<<grid, 256, smem, s>>>(A, lda, col0_dev, q_dev, q_fixed, n, part->as<double>(), QP);
+  } else {
+    throw Error(kInvalidArgument, "Gram of more than 128 columns is not supported");
+  }
+  STROM_LAUNCH_CHECK();
+  k_gram_reduce<<<(unsigned)ceil_div((int64_t)QP * QP, 256), 256, 0, s>>>(part->as<double>(), grid, QP, q_dev,
+                                                                          q_fixed, L, ldl);
+  STROM_LAUNCH_CHECK();
+  k_cholesky<<<1, 256, 0, s>>>(L, ldl, hdr_c, q_fixed, status_dev);
+  STROM_LAUNCH_CHECK();
+  k_lower_inverse<<<1, 1024, 0, s>>>(L, ldl, hdr_c, q_fixed, Li);
   STROM_LAUNCH_CHECK();
 }
 
@@ -360,6 +410,9 @@ strom_isvd* compact(strom_isvd* src, const Caps& caps, cudaStream_t s) {
   // p = source c (step->m), q = r (step->mkeep)
   launch_tall_gemm(src->U->ptr(), src->ldu, &src->view.hdr->base, m.sc.T, P.ccap, &m.sc.step->m,
                    &m.sc.step->mkeep, t->U->ptr(), t->ldu, false, t->n, t->ldu, s);
+  // measure the Gram of the stored U_new: L describes the memory, not an assumed identity
+  gram_cholesky(t->U->ptr(), t->ldu, nullptr, &m.sc.step->mkeep, 0, caps.rcap, t->n, t->view.L, t->view.Li,
+                t->view.ldl, t->view.hdr, reinterpret_cast<int*>(&m.sc.step->pad_status), s);
   t->r_ub = std::min(src->r_ub, caps.rcap);
   t->c_ub = t->r_ub;
   t->U->claimed = t->c_ub;
@@ -421,12 +474,18 @@ strom_isvd* update_once(strom_isvd* src, const double* x, ScratchMem* scratch, c
     k_step_a<<<1, 256, 0, s>>>(cur->view, scratch->sc, P);
     STROM_LAUNCH_CHECK();
   }
-  launch_resid(P.ccap, dst->U->ptr(), x, cur->view, *scratch, P, s);
+  launch_resid(P.ccap, dst->U->ptr(), x, cur->view, *scratch, P, s, 0);
+  {
+    ProfScope ps(P_STEP_B, s);
+    k_step_b1<<<1, 256, 0, s>>>(cur->view, scratch->sc, P);
+    STROM_LAUNCH_CHECK();
+  }
+  launch_resid(P.ccap, dst->U->ptr(), nullptr, cur->view, *scratch, P, s, 1);
   launch_step_b(cur->view, dst->view, *scratch, P, cur->caps, s);
   {
-    dim3 grid((unsigned)ceil_div(dst->k, 128), (unsigned)ceil_div(cur->caps.rcap + 1, kVCols));
+    dim3 grid((unsigned)ceil_div(dst->k, kVRows), (unsigned)ceil_div(cur->caps.rcap + 1, kVCols));
     ProfScope ps(P_VUPDATE, s);
-    k_vupdate<<<grid, 128, 0, s>>>(cur->view, dst->view, scratch->sc, P);
+    k_vupdate<<<grid, kVRows, (size_t)(cur->caps.rcap + 2) * kVCols * 8, s>>>(cur->view, dst->view, scratch->sc, P);
     STROM_LAUNCH_CHECK();
   }
   dst->c_ub = cur->c_ub + 1;
@@ -466,8 +525,8 @@ strom_isvd* init_state(int64_t n, const double* x, int64_t k, double tol_svd, do
   launch_resid(P.ccap, h->U->ptr(), x, sv, m, P, s);
   launch_step_b(sv, h->view, m, P, h->caps, s);
   {
-    dim3 grid((unsigned)ceil_div(k, 128), 1);
-    k_vupdate<<<grid, 128, 0, s>>>(sv, h->view, m.sc, P);
+    dim3 grid((unsigned)ceil_div(k, kVRows), 1);
+    k_vupdate<<<grid, kVRows, (size_t)(h->caps.rcap + 2) * kVCols * 8, s>>>(sv, h->view, m.sc, P);
     STROM_LAUNCH_CHECK();
   }
   h->c_ub = 1;
@@ -585,6 +644,7 @@ int strom_isvd_query(strom_isvd* h, void* stream, strom_isvd_info* out) {
     out->last_p = hh.p;
     out->last_drift = hh.drift;
     out->last_xnorm = hh.xnorm;
+    out->last_p_sq = hh.p_sq;
     out->tol_svd = h->tol_svd;
     out->tol_sv = h->tol_sv;
     out->r_max = h->r_max;
@@ -658,12 +718,17 @@ int strom_isvd_load_factored(int64_t n, int64_t k, int64_t c, int64_t r, const d
       if (l_dev) {
         k_copy_cm<<<(unsigned)ceil_div(c * c, th), th, 0, s>>>(l_dev, ldl, c, c, h->view.L, h->view.ldl);
         STROM_LAUNCH_CHECK();
+        k_lower_inverse<<<1, 1024, 0, s>>>(h->view.L, h->view.ldl, nullptr, (int)c, h->view.Li);
+        STROM_LAUNCH_CHECK();
       } else {
-        std::vector<double> eye((size_t)c * c, 0.0);
-        for (int64_t i = 0; i < c; ++i) eye[i * c + i] = 1.0;
-        STROM_CUDA(cudaMemcpy2DAsync(h->view.L, h->view.ldl * 8, eye.data(), c * 8, c * 8, c,
-                                     cudaMemcpyHostToDevice, s));
+        // measure the Gram of the stored U (exact L even for a nearly orthonormal U)
+        auto st = dev_alloc(sizeof(int), s, true);
+        gram_cholesky(h->U->ptr(), h->ldu, nullptr, nullptr, (int)c, (int)c, n, h->view.L, h->view.Li,
+                      h->view.ldl, nullptr, st->as<int>(), s);
+        int bad = 0;
+        STROM_CUDA(cudaMemcpyAsync(&bad, st->ptr, sizeof(int), cudaMemcpyDeviceToHost, s));
         STROM_CUDA(cudaStreamSynchronize(s));
+        if (bad) throw Error(kNumericalError, "U is numerically rank-deficient (Gram not positive definite)");
       }
     }
     h->c_ub = (int32_t)c;
@@ -699,17 +764,10 @@ int strom_isvd_load(int64_t n, int64_t k, int64_t r, const double* phi_dev, cons
     if (rc) throw Error(rc, strom_last_error());
     std::unique_ptr<strom_isvd> guard(h);
     if (r > 0) {
-      // Gram column by column with the projection pass, then Cholesky.
-      ScratchMem m = make_scratch(h->ldu, h->caps, s);
-      IsvdParams P = make_params(h, m, k, false);
-      for (int64_t j = 0; j < r; ++j) {
-        launch_proj(P.ccap, h->U->ptr(), h->U->ptr() + j * h->ldu, h->view, m, P, s);
-        k_copy_g_col<<<1, 256, 0, s>>>(m.sc.g, (int)r, h->view.L, h->view.ldl, (int)j);
-        STROM_LAUNCH_CHECK();
-      }
+      // exact Gram of the stored U on the tensor cores, then Cholesky
       auto st = dev_alloc(sizeof(int), s, true);
-      k_cholesky<<<1, 256, 0, s>>>(h->view.L, h->view.ldl, nullptr, (int)r, st->as<int>());
-      STROM_LAUNCH_CHECK();
+      gram_cholesky(h->U->ptr(), h->ldu, nullptr, nullptr, (int)r, (int)r, n, h->view.L, h->view.Li,
+                    h->view.ldl, nullptr, st->as<int>(), s);
       int bad = 0;
       STROM_CUDA(cudaMemcpyAsync(&bad, st->ptr, sizeof(int), cudaMemcpyDeviceToHost, s));
       STROM_CUDA(cudaStreamSynchronize(s));
@@ -719,6 +777,31 @@ int strom_isvd_load(int64_t n, int64_t k, int64_t r, const double* phi_dev, cons
     *out = guard.release();
   });
 }
+
+// Representation dump for the invariant tests: U[:, base:base+c] (n x c,
+// column-major, ld n), W (c x r, column-major, ld c), L (c x c, ld c).
+int strom_isvd_factors(strom_isvd* h, double* u_dev, double* w_dev, double* l_dev, void* stream) {
+  return guarded([&] {
+    STROM_REQUIRE(h, "null argument");
+    cudaStream_t s = as_stream(stream);
+    IsvdHdr hh;
+    read_hdr(h, s, &hh);
+    if (u_dev && hh.c > 0)
+      STROM_CUDA(cudaMemcpy2DAsync(u_dev, h->n * 8, h->U->ptr() + (int64_t)hh.base * h->ldu, h->ldu * 8, h->n * 8,
+                                   hh.c, cudaMemcpyDeviceToDevice, s));
+    if (w_dev && hh.c > 0 && hh.r > 0)
+      STROM_CUDA(cudaMemcpy2DAsync(w_dev, hh.c * 8, h->view.W, h->view.ldw * 8, hh.c * 8, hh.r,
+                                   cudaMemcpyDeviceToDevice, s));
+    if (l_dev && hh.c > 0)
+      STROM_CUDA(cudaMemcpy2DAsync(l_dev, hh.c * 8, h->view.L, h->view.ldl * 8, hh.c * 8, hh.c,
+                                   cudaMemcpyDeviceToDevice, s));
+    STROM_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+// Diagnostics: point step B's phase timestamps (clock64, 8 slots) at a device
+// buffer, or NULL to disable.
+void strom_debug_tprobe(long long* dev_buf) { g_tprobe = dev_buf; }
 
 void strom_isvd_free(strom_isvd* h) { delete h; }
 

@@ -15,6 +15,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "core_svd.cuh"
 #include "small_dense.cuh"
 
 namespace strom {
@@ -31,7 +32,7 @@ struct IsvdHdr {
   double p;        // Pythagorean residual norm of that update
   double drift;    // |phi_0 . phi_last| of that update
   double xnorm;    // ||x|| of that update
-  double pad1;
+  double p_sq;     // unclamped x.x - ell.ell of that update
 };
 
 enum : int32_t {
@@ -44,14 +45,17 @@ enum : int32_t { M_NORMAL_DEP = 0, M_NORMAL_INDEP = 1, M_RESTART_ACCEPT = 2, M_R
 // -------- transient per-update scalars (scratch) ---------------------------
 struct IsvdStep {
   int32_t mode, write_slot, c_dot, restart;
-  int32_t m, mkeep, appended, pad;
+  int32_t m, mkeep, append, reorth;
   double xx, rho2, p, norm;
+  int32_t pad_status, pad2;
+  double p_sq;
 };
 
 struct StateView {
   IsvdHdr* hdr;
   double* W;      // c_cap x (r_cap + 1), ld = ldw
-  double* L;      // c_cap x c_cap lower, ld = ldl
+  double* L;      // c_cap x c_cap lower, ld = ldl   (Cholesky factor of G = U^T U)
+  double* Li;     // c_cap x c_cap lower, ld = ldl   (L^{-1}, kept explicitly)
   double* sigma;  // r_cap + 1
   double* V;      // k_cap x (r_cap + 1), ld = ldv
   int32_t ldw, ldl;
@@ -64,6 +68,9 @@ struct Scratch {
   double* y;      // c_cap   W ell
   double* ell;    // r_cap+1 Phi^T x
   double* e;      // c_cap   U^T r1
+  double* h;      // c_cap   G^{-1} e of the first residual (DGKS correction), else 0
+  double* lvec;   // c_cap   L^{-1} e
+  double* tmp;    // c_cap   scratch vector
   double* vbar;   // (r_cap+2)^2 sorted, sign-fixed V_bar of the core
   double* work;   // large fallback workspace (global) for the one-CTA kernels
   double* T;      // c_cap x (r_cap+1) compaction transform
@@ -82,10 +89,17 @@ struct IsvdParams {
   int32_t pstride;   // stride of one CTA's partial row
   int32_t work_stride;
   unsigned long long* prof;  // device byte counters (runtime.cuh ProfKind) or null
+  long long* tprobe;         // phase timestamps of step B (diagnostics) or null
 };
+
+#define STROM_TPROBE(P, k)                                  \
+  do {                                                      \
+    if ((P).tprobe && threadIdx.x == 0) (P).tprobe[k] = clock64(); \
+  } while (0)
 
 constexpr int kTileRows = 64;
 constexpr int kPassThreads = 256;
+constexpr int kSmallThreads = 512;  // one-CTA kernels: 128 registers per thread (no spills)
 
 // Deterministic grid finish: the last CTA to arrive sums the per-CTA partials
 // in CTA order.  Returns true in that CTA (after the counter is reset).
@@ -153,12 +167,23 @@ __global__ void __launch_bounds__(kPassThreads) k_proj(const double* __restrict_
     if (lane == 0) mypart[P.ccap] = v;
   }
   if (!last_cta_arrives(sc.counter, &s_last)) return;
-  for (int j = threadIdx.x; j <= c; j += blockDim.x) {
+  // one warp per output, lanes stride over the CTA partials, fixed tree: deterministic
+  for (int j = wid; j <= c; j += 8) {
     const int col = (j == c) ? P.ccap : j;
-    double s = 0.0;
-    for (int b = 0; b < (int)gridDim.x; ++b) s += sc.part[(int64_t)b * P.pstride + col];
-    if (j == c) sc.step->xx = s;
-    else sc.g[j] = s;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int b = lane;
+    for (; b + 96 < (int)gridDim.x; b += 128) {
+      s0 += sc.part[(int64_t)b * P.pstride + col];
+      s1 += sc.part[(int64_t)(b + 32) * P.pstride + col];
+      s2 += sc.part[(int64_t)(b + 64) * P.pstride + col];
+      s3 += sc.part[(int64_t)(b + 96) * P.pstride + col];
+    }
+    for (; b < (int)gridDim.x; b += 32) s0 += sc.part[(int64_t)b * P.pstride + col];
+    double s = warp_sum((s0 + s1) + (s2 + s3));
+    if (lane == 0) {
+      if (j == c) sc.step->xx = s;
+      else sc.g[j] = s;
+    }
   }
 }
 
@@ -222,6 +247,7 @@ __global__ void __launch_bounds__(256) k_step_a(StateView src, Scratch sc, IsvdP
   const bool dep = (p < P.tol_svd) || (p == 0.0) || ((int64_t)r >= P.n);
   if (threadIdx.x == 0) {
     st->p = p;
+    st->p_sq = p_sq;
     st->mode = dep ? M_NORMAL_DEP : M_NORMAL_INDEP;
     if (!dep) {
       st->write_slot = h.base + c;
@@ -233,12 +259,12 @@ __global__ void __launch_bounds__(256) k_step_a(StateView src, Scratch sc, IsvdP
     double s = 0.0;
     for (int i = 0; i < r; ++i) s = fma(src.W[(int64_t)i * src.ldw + j], sc.ell[i], s);
     sc.y[j] = s;
-    sc.gt[j] = sc.g[j];
   }
   __syncthreads();
-  if (!dep && wid == 0) {
-    warp_lower_solve(src.L, src.ldl, c, sc.gt);
-    warp_lower_t_solve(src.L, src.ldl, c, sc.gt);
+  if (!dep) {  // gt = G^{-1} g = L^{-T} (L^{-1} g)
+    cta_lower_mv(src.Li, src.ldl, c, sc.g, sc.tmp);
+    __syncthreads();
+    cta_lower_t_mv(src.Li, src.ldl, c, sc.tmp, sc.gt);
   }
 }
 
@@ -247,25 +273,30 @@ __global__ void __launch_bounds__(256) k_step_a(StateView src, Scratch sc, IsvdP
 // e = U[:, ...]^T r1 and rho2 = r1.r1.  Two phases per 64-row tile through
 // shared memory (row dots, then column dots against the fresh residual).
 // ---------------------------------------------------------------------------
+// phase 0: r1 = x - U gt (gt = G^{-1} U^T x);  phase 1 (DGKS re-orthogonalisation,
+// only when step B1 asked for it): r2 = r1 - U h in place on the slot column.
 template <int MAXJ>
-__global__ void __launch_bounds__(kPassThreads) k_resid(double* __restrict__ U, const double* __restrict__ x,
-                                                         StateView src, Scratch sc, IsvdParams P) {
+__global__ void __launch_bounds__(kPassThreads) k_resid(double* U, const double* xin,
+                                                         StateView src, Scratch sc, IsvdParams P, int phase) {
   extern __shared__ double smem[];
   __shared__ int s_last;
   __shared__ double red[8];
   const IsvdStep* st = sc.step;
   const int mode = st->mode;
-  if (mode != M_NORMAL_INDEP && mode != M_RESTART_ACCEPT) return;
+  if (phase == 0 && mode != M_NORMAL_INDEP && mode != M_RESTART_ACCEPT) return;
+  if (phase == 1 && !(mode == M_NORMAL_INDEP && st->reorth)) return;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int cd = st->c_dot, slot = st->write_slot, base = src.hdr->base;
+  const double* x = (phase == 0) ? xin : U + (int64_t)slot * P.ldu;
+  const double* coef = (phase == 0) ? sc.gt : sc.h;
   if (P.prof && blockIdx.x == 0 && threadIdx.x == 0)
     atomicAdd(P.prof + 1, 8ull * (unsigned long long)P.n * (unsigned long long)(cd + 2));  // U, x; r1 out
   double* tile = smem;                            // cd x 64 (column-major, 64 rows)
-  double* gts = tile + (int64_t)P.ccap * kTileRows;  // ccap
-  double* xs = gts + P.ccap;                      // 64
+  double* gts = tile + (int64_t)P.ccap * kTileRows;  // ccap (rounded to even: keeps rs 16B-aligned)
+  double* xs = gts + ((P.ccap + 1) & ~1);         // 64
   double* rs = xs + kTileRows;                    // 64
   double* pp = rs + kTileRows;                    // 4 x 64 partial row dots
-  for (int j = threadIdx.x; j < cd; j += blockDim.x) gts[j] = sc.gt[j];
+  for (int j = threadIdx.x; j < cd; j += blockDim.x) gts[j] = coef[j];
   const int64_t ntiles = P.ldu / kTileRows;
   const int64_t per = ceil_div(ntiles, gridDim.x);
   const int64_t t0 = blockIdx.x * per;
@@ -287,7 +318,7 @@ __global__ void __launch_bounds__(kPassThreads) k_resid(double* __restrict__ U, 
     }
     if (threadIdx.x < kTileRows) {
       const int64_t row = row0 + threadIdx.x;
-      xs[threadIdx.x] = (row < P.n) ? __ldg(x + row) : 0.0;
+      xs[threadIdx.x] = (row < P.n) ? x[row] : 0.0;
     }
     __syncthreads();
     {
@@ -326,12 +357,22 @@ __global__ void __launch_bounds__(kPassThreads) k_resid(double* __restrict__ U, 
   const double rtot = block_sum(rr, red);
   if (threadIdx.x == 0) mypart[P.ccap] = rtot;
   if (!last_cta_arrives(sc.counter, &s_last)) return;
-  for (int j = threadIdx.x; j <= cd; j += blockDim.x) {
+  for (int j = wid; j <= cd; j += 8) {
     const int col = (j == cd) ? P.ccap : j;
-    double s = 0.0;
-    for (int b = 0; b < (int)gridDim.x; ++b) s += sc.part[(int64_t)b * P.pstride + col];
-    if (j == cd) sc.step->rho2 = s;
-    else sc.e[j] = s;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int b = lane;
+    for (; b + 96 < (int)gridDim.x; b += 128) {
+      s0 += sc.part[(int64_t)b * P.pstride + col];
+      s1 += sc.part[(int64_t)(b + 32) * P.pstride + col];
+      s2 += sc.part[(int64_t)(b + 64) * P.pstride + col];
+      s3 += sc.part[(int64_t)(b + 96) * P.pstride + col];
+    }
+    for (; b < (int)gridDim.x; b += 32) s0 += sc.part[(int64_t)b * P.pstride + col];
+    double s = warp_sum((s0 + s1) + (s2 + s3));
+    if (lane == 0) {
+      if (j == cd) sc.step->rho2 = s;
+      else sc.e[j] = s;
+    }
   }
 }
 
@@ -348,7 +389,41 @@ __global__ void __launch_bounds__(kPassThreads) k_resid(double* __restrict__ U, 
 // ---------------------------------------------------------------------------
 constexpr double kFoldTau = 1e-3;  // append r1 only if its out-of-span part is >= tau |r1|
 
-__global__ void __launch_bounds__(1024) k_step_b(StateView src, StateView dst, Scratch sc, IsvdParams P,
+// ---------------------------------------------------------------------------
+// Step B1 (one CTA): decide how the new direction enters U.  l = L^{-1} e,
+// lambda^2 = |r1|^2 - |l|^2 is the squared out-of-span part of r1 in the
+// G-metric.  Append r1 if lambda >= tau |r1|; otherwise (r1 is mostly
+// rounding noise inside span(U)) request one more classical Gram-Schmidt pass
+// (DGKS) when U does not yet span R^n.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_step_b1(StateView src, Scratch sc, IsvdParams P) {
+  __shared__ double red[32];
+  IsvdStep* st = sc.step;
+  const int wid = threadIdx.x >> 5;
+  const int c = src.hdr->c;
+  for (int j = threadIdx.x; j < c; j += blockDim.x) sc.h[j] = 0.0;
+  if (st->mode != M_NORMAL_INDEP) {
+    if (threadIdx.x == 0) { st->reorth = 0; st->append = 0; }
+    return;
+  }
+  cta_lower_mv(src.Li, src.ldl, c, sc.e, sc.lvec);
+  __syncthreads();
+  double part = 0.0;
+  for (int j = threadIdx.x; j < c; j += blockDim.x) part = fma(sc.lvec[j], sc.lvec[j], part);
+  const double ll = block_sum(part, red);
+  const double rho2 = st->rho2;
+  const double lam2 = rho2 - ll;
+  const bool app = (lam2 > kFoldTau * kFoldTau * rho2) && (rho2 > 0.0);
+  const bool reorth = !app && ((int64_t)c < P.n) && (st->write_slot < P.ccap);
+  __syncthreads();
+  if (reorth) cta_lower_t_mv(src.Li, src.ldl, c, sc.lvec, sc.h);
+  if (threadIdx.x == 0) {
+    st->append = app ? 1 : 0;
+    st->reorth = reorth ? 1 : 0;
+  }
+}
+
+__global__ void __launch_bounds__(kSmallThreads) k_step_b(StateView src, StateView dst, Scratch sc, IsvdParams P,
                                                  int use_smem) {
   extern __shared__ double smem[];
   __shared__ double red[32];
@@ -389,6 +464,7 @@ __global__ void __launch_bounds__(1024) k_step_b(StateView src, StateView dst, S
         o.base = st->write_slot;
         dst.W[0] = 1.0 / st->norm;
         dst.L[0] = sqrt(st->rho2);
+        dst.Li[0] = 1.0 / dst.L[0];
         dst.sigma[0] = st->norm;
         st->mkeep = 1;
       }
@@ -397,156 +473,184 @@ __global__ void __launch_bounds__(1024) k_step_b(StateView src, StateView dst, S
     }
     return;
   }
-  const bool dep = (mode == M_NORMAL_DEP);
+  STROM_TPROBE(P, 0);
+  bool dep = (mode == M_NORMAL_DEP);
   const int r = h.r, c = h.c, m = r + 1;
   const double p = st->p;
   o.p = p;
-  // ---- 1. Cholesky factor of G for the (possibly) appended column ----------
+  o.p_sq = st->p_sq;
+  // ---- 1. how the new direction enters U (see k_step_b1) --------------------
+  //   append: U' = [U r], L' = [[L, 0], [l^T, lambda]]
+  //   fold:   r is (numerically) in span(U) and U has a spare direction
+  //   demote: r is in span(U) to working precision and U has none -> dependent
   int cn = c;
-  double* lvec = sc.work + 2 * (int64_t)P.work_stride;  // l = L^{-1} e, then G^{-1} e
+  int action = 0;  // 0 none (dependent), 1 append, 2 fold
+  double* lvec = sc.lvec;
   if (!dep) {
-    for (int j = threadIdx.x; j < c; j += blockDim.x) lvec[j] = sc.e[j];
-    __syncthreads();
-    if (wid == 0) warp_lower_solve(src.L, src.ldl, c, lvec);
-    __syncthreads();
+    if (st->reorth) {  // second pass done: recompute l, lambda from (e2, |r2|^2)
+      cta_lower_mv(src.Li, src.ldl, c, sc.e, lvec);
+      __syncthreads();
+    }
     double part = 0.0;
     for (int j = threadIdx.x; j < c; j += blockDim.x) part = fma(lvec[j], lvec[j], part);
     const double ll = block_sum(part, red);
     const double rho2 = st->rho2;
     const double lam2 = rho2 - ll;
-    const bool app = (lam2 > kFoldTau * kFoldTau * rho2) && (st->write_slot < P.ccap) && (rho2 > 0.0);
-    if (threadIdx.x == 0) {
-      s_int[0] = app;
-      s_misc[0] = app ? sqrt(lam2) : 0.0;
-    }
+    bool app;
+    // after the second pass r2 is kept whenever it carries a genuine out-of-span
+    // direction, however small: the reference appends j = (x - Phi ell)/p even
+    // when it is pure rounding noise (basis.py:155-156)
+    if (st->reorth) app = (lam2 > 0.25 * rho2) && (rho2 > 0.0);
+    else app = st->append != 0;
+    app = app && (st->write_slot < P.ccap) && ((int64_t)c < P.n);
+    if (threadIdx.x == 0) s_misc[0] = app ? sqrt(lam2) : 0.0;
+    if (app) action = 1;
+    else if (c >= r + 1) action = 2;
+    else { action = 0; dep = true; }
     __syncthreads();
-    if (s_int[0]) {
-      cn = c + 1;
-    } else if (wid == 0) {
-      warp_lower_t_solve(src.L, src.ldl, c, lvec);  // lvec = G^{-1} e
-    }
+    // fold: G^{-1} e;  append: u = L^{-T} l for the new row of L^{-1}
+    if (action != 0) cta_lower_t_mv(src.Li, src.ldl, c, lvec, sc.tmp);
     __syncthreads();
+    if (action == 2)
+      for (int j = threadIdx.x; j < c; j += blockDim.x) lvec[j] = sc.tmp[j];
+    __syncthreads();
+    if (action == 1) cn = c + 1;
   }
-  const bool appended = (!dep) && (cn == c + 1);
+  const bool appended = (action == 1);
   // copy L (lower) into dst, extended by the new row when appended
   for (int64_t idx = threadIdx.x; idx < (int64_t)cn * cn; idx += blockDim.x) {
     const int i = idx % cn, j = idx / cn;
-    double v = 0.0;
-    if (i < c && j < c) v = (i >= j) ? src.L[(int64_t)j * src.ldl + i] : 0.0;
-    else if (i == c && j < c) v = lvec[j];
-    else if (i == c && j == c) v = s_misc[0];
+    double v = 0.0, vi = 0.0;
+    if (i < c && j < c) {
+      if (i >= j) {
+        v = src.L[(int64_t)j * src.ldl + i];
+        vi = src.Li[(int64_t)j * src.ldl + i];
+      }
+    } else if (i == c && j < c) {
+      v = lvec[j];
+      vi = -sc.tmp[j] / s_misc[0];
+    } else if (i == c && j == c) {
+      v = s_misc[0];
+      vi = 1.0 / s_misc[0];
+    }
     dst.L[(int64_t)j * dst.ldl + i] = v;
+    dst.Li[(int64_t)j * dst.ldl + i] = vi;
   }
-  // new W column for j = (x - Phi ell)/p in U-coordinates (length cn)
+  // new W column for j = (x - Phi ell)/p in U-coordinates (length cn):
+  //   x = U (gt + h) + r  ->  j = U (gt + h - y)/p + r/p
   double* wj = sc.work + 3 * (int64_t)P.work_stride;
   if (!dep) {
     for (int a = threadIdx.x; a < cn; a += blockDim.x) {
       double v;
-      if (a < c) v = appended ? (sc.gt[a] - sc.y[a]) / p : (sc.gt[a] - sc.y[a] + lvec[a]) / p;
-      else v = 1.0 / p;
+      if (a < c) {
+        v = sc.gt[a] + sc.h[a] - sc.y[a];
+        if (action == 2) v += lvec[a];
+        v /= p;
+      } else {
+        v = 1.0 / p;
+      }
       wj[a] = v;
     }
   }
-  // ---- 2. the bordered core and its SVD ------------------------------------
-  double* QT = use_smem ? smem : sc.work + 4 * (int64_t)P.work_stride;
-  double* WB = QT + (int64_t)m * m;
-  for (int64_t idx = threadIdx.x; idx < (int64_t)m * m; idx += blockDim.x) {
-    const int i = idx % m, j = idx / m;  // QT(i, j) = Q(j, i)
-    double v = 0.0;
-    if (i < r && j == i) v = src.sigma[i];
-    else if (i == r && j < r) v = sc.ell[j];
-    else if (i == r && j == r) v = dep ? 0.0 : p;
-    QT[idx] = v;
-    WB[idx] = (i == j) ? 1.0 : 0.0;
+  STROM_TPROBE(P, 1);
+  // ---- shared-memory plan (global fallback when it does not fit) ----------
+  //   WS m^2 | Wt m^2 | Vt m^2 | core work 16 ms | WB ccap x m (staged W_b, later QR's M)
+  const int64_t ms = P.work_stride;
+  double* base = use_smem ? smem : sc.work + 4 * ms;
+  double* WS = base;                      // sorted, signed W_bar (m x m)
+  double* Wt = WS + (int64_t)m * m;       // vectors by slot, later W^T W
+  double* Vt = Wt + (int64_t)m * m;       // vectors by slot, later the polished W_bar
+  double* cb = Vt + (int64_t)m * m;
+  double* WB = cb + 16 * ms;              // W_b = [[W, w_j]] (cn x m, ld ccap)
+  double* svs = cb + 14 * ms;             // m sorted singular values
+  CoreSvdWork cw;
+  cw.d = cb; cw.z = cb + ms; cw.zh = cb + 2 * ms; cw.mu = cb + 3 * ms; cw.sv = cb + 4 * ms;
+  cw.rc = cb + 5 * ms; cw.rs = cb + 6 * ms;
+  {
+    int* ib = reinterpret_cast<int*>(cb + 7 * ms);
+    cw.org = ib; cw.kset = ib + ms; cw.defl = ib + 2 * ms; cw.ra = ib + 3 * ms; cw.rb = ib + 4 * ms;
+    cw.perm = ib + 5 * ms; cw.cnt = ib + 6 * ms;
   }
-  __syncthreads();
-  cta_jacobi(QT, m, m, m, WB, m, m, &s_int[1]);
-  // singular values = column norms of Q^T W_bar = V_bar Sigma
-  double* sv = sc.work;  // m
-  int* perm = reinterpret_cast<int*>(sc.work + (int64_t)P.work_stride);
-  cta_col_norms(QT, m, m, m, sv);
-  cta_argsort_desc(sv, m, perm);
-  // sorted, sign-fixed W_bar (kept in QT's place after extracting V_bar)
-  double* vbar = sc.vbar;  // m x m, ld = m (global scratch, read by the V kernel)
-  for (int k = wid; k < m; k += nw) {
-    const int srcc = perm[k];
-    const double* wcol = WB + (int64_t)srcc * m;
-    const int at = warp_argmax_abs(wcol, m);
-    const double sg = (wcol[at] < 0.0) ? -1.0 : 1.0;
-    const double s = sv[srcc];
-    for (int i = lane; i < m; i += 32) {
-      const double vv = (s > 0.0) ? QT[(int64_t)srcc * m + i] / s : (i == srcc ? 1.0 : 0.0);
-      vbar[(int64_t)k * m + i] = sg * vv;
-    }
+  // stage W_b: columns 0..r-1 = W (c rows; the appended row is 0), column r = w_j
+  __syncthreads();  // w_j complete
+  if (P.tprobe && threadIdx.x == 0) P.tprobe[7] = use_smem;
+  for (int64_t idx = threadIdx.x; idx < (int64_t)cn * m; idx += blockDim.x) {
+    const int a = idx % cn, b = idx / cn;
+    double v;
+    if (b < r) v = (a < c) ? src.W[(int64_t)b * src.ldw + a] : 0.0;
+    else v = dep ? 0.0 : wj[a];
+    WB[(int64_t)b * P.ccap + a] = v;
   }
-  __syncthreads();
-  // move sorted signed W_bar into QT (QT is dead now)
-  for (int k = wid; k < m; k += nw) {
-    const int srcc = perm[k];
-    const double* wcol = WB + (int64_t)srcc * m;
-    const int at = warp_argmax_abs(wcol, m);
-    const double sg = (wcol[at] < 0.0) ? -1.0 : 1.0;
-    for (int i = lane; i < m; i += 32) QT[(int64_t)k * m + i] = sg * wcol[i];
+  // ---- 2. the bordered core and its SVD (rank-one secular solver) ----------
+  core_svd_secular(src.sigma, sc.ell, dep ? 0.0 : p, r, cw, Wt, Vt, svs, WS, sc.vbar, red,
+                   P.tprobe ? P.tprobe + 8 : nullptr, P.tprobe ? P.tprobe + 300 : nullptr);
+  STROM_TPROBE(P, 2);
+  // One Newton-Schulz step W <- W (3 I - W^T W) / 2 restores orthogonality of the
+  // accumulated rotations to O(eps): Phi = U W inherits it, and the Pythagorean
+  // p^2 = x.x - ell.ell (basis.py:136) is only meaningful for an orthonormal Phi.
+  {
+    double* Mg = Wt;
+    cta_gemm44(m, m, m, WS, m, 1, WS, 1, m, [&](int i, int j, double v) { Mg[(int64_t)j * m + i] = v; });
+    __syncthreads();
+    cta_gemm44(m, m, m, WS, 1, m, Mg, 1, m, [&](int i, int j, double v) {
+      Vt[(int64_t)j * m + i] = 1.5 * WS[(int64_t)j * m + i] - 0.5 * v;
+    });
+    __syncthreads();
+    for (int64_t idx = threadIdx.x; idx < (int64_t)m * m; idx += blockDim.x) WS[idx] = Vt[idx];
+    __syncthreads();
   }
-  __syncthreads();
-  double* WS = QT;  // sorted W_bar, m x m
+  STROM_TPROBE(P, 3);
   // ---- 3. truncation (basis.py:160-168) ------------------------------------
   int mk = dep ? r : m;
   bool trunc = false;
-  if (mk > 0 && sv[perm[mk - 1]] < P.tol_sv) { mk -= 1; trunc = true; }
+  if (mk > 0 && svs[mk - 1] < P.tol_sv) { mk -= 1; trunc = true; }
   if (P.r_max >= 0 && mk > P.r_max) { mk = P.r_max; trunc = true; }
-  // ---- 4. W' = W_b W_bar[:, :mk] -------------------------------------------
-  for (int64_t idx = threadIdx.x; idx < (int64_t)cn * mk; idx += blockDim.x) {
-    const int a = idx % cn, k = idx / cn;
-    double s = 0.0;
-    if (a < c) {
-      for (int b = 0; b < r; ++b) s = fma(src.W[(int64_t)b * src.ldw + a], WS[(int64_t)k * m + b], s);
-    }
-    if (!dep) s = fma(wj[a], WS[(int64_t)k * m + r], s);
-    dst.W[(int64_t)k * dst.ldw + a] = s;
+  // ---- 4. W' = W_b W_bar[:, :mk]  (basis.py:150-158 in U-coordinates) -----
+  {
+    const int kdim = dep ? r : m;
+    cta_gemm44(cn, mk, kdim, WB, 1, P.ccap, WS, 1, m,
+               [&](int a, int k, double v) { dst.W[(int64_t)k * dst.ldw + a] = v; });
   }
-  for (int k = threadIdx.x; k < mk; k += blockDim.x) dst.sigma[k] = sv[perm[k]];
+  for (int k = threadIdx.x; k < mk; k += blockDim.x) dst.sigma[k] = svs[k];
   __syncthreads();
+  STROM_TPROBE(P, 4);
   // ---- 5. drift test and small-space QR (basis.py:170-174) -----------------
   bool did_qr = false;
   double drift = 0.0;
   if (mk > 1) {
+    // a0 = L^T w_0, a1 = L^T w_last (one warp per row of L^T, lanes over the column)
     double part = 0.0;
-    for (int i = threadIdx.x; i < cn; i += blockDim.x) {
+    for (int i = wid; i < cn; i += nw) {
+      const double* lcol = dst.L + (int64_t)i * dst.ldl;
       double a0 = 0.0, a1 = 0.0;
-      for (int j = i; j < cn; ++j) {
-        const double l = dst.L[(int64_t)i * dst.ldl + j];
-        a0 = fma(l, dst.W[j], a0);
-        a1 = fma(l, dst.W[(int64_t)(mk - 1) * dst.ldw + j], a1);
+      for (int j = i + lane; j < cn; j += 32) {
+        a0 = fma(lcol[j], dst.W[j], a0);
+        a1 = fma(lcol[j], dst.W[(int64_t)(mk - 1) * dst.ldw + j], a1);
       }
-      part = fma(a0, a1, part);
+      a0 = warp_sum(a0);
+      a1 = warp_sum(a1);
+      if (lane == 0) part = fma(a0, a1, part);
     }
     drift = fabs(block_sum(part, red));
     const double thr = fmin(P.tol_svd, 2.220446049250313e-16 * (double)P.n);
+    STROM_TPROBE(P, 5);
     if (drift > thr) {
       did_qr = true;
-      double* M = use_smem ? smem : sc.work + 4 * (int64_t)P.work_stride;  // cn x mk
-      __syncthreads();
-      for (int64_t idx = threadIdx.x; idx < (int64_t)cn * mk; idx += blockDim.x) {
-        const int i = idx % cn, k = idx / cn;
-        double s = 0.0;
-        for (int j = i; j < cn; ++j) s = fma(dst.L[(int64_t)i * dst.ldl + j], dst.W[(int64_t)k * dst.ldw + j], s);
-        M[(int64_t)k * cn + i] = s;
-      }
+      double* M = WB;  // cn x mk, ld cn (W_b is dead)
+      // M = L^T W'  (L stored with zeros above the diagonal)
+      cta_gemm44(cn, mk, cn, dst.L, dst.ldl, 1, dst.W, 1, dst.ldw,
+                 [&](int i, int k, double v) { M[(int64_t)k * cn + i] = v; });
       __syncthreads();
       double* tau = sc.work;
       double* beta = sc.work + P.work_stride;
       cta_householder_qr(M, cn, cn, mk, nullptr, 0, tau, beta, red);
-      // W <- L^{-T} Q_s, column by column (one warp per column)
-      for (int k = wid; k < mk; k += nw) {
-        double* wk = dst.W + (int64_t)k * dst.ldw;
-        for (int i = lane; i < cn; i += 32) wk[i] = M[(int64_t)k * cn + i];
-        __syncwarp();
-        warp_lower_t_solve(dst.L, dst.ldl, cn, wk);
-      }
+      // W <- L^{-T} Q_s  (parallel triangular GEMM with the stored inverse)
+      cta_gemm44(cn, mk, cn, dst.Li, dst.ldl, 1, M, 1, cn,
+                 [&](int a, int k, double v) { dst.W[(int64_t)k * dst.ldw + a] = v; });
       __syncthreads();
     }
   }
+  STROM_TPROBE(P, 6);
   if (threadIdx.x == 0) {
     o.r = mk;
     o.c = cn;
@@ -554,7 +658,7 @@ __global__ void __launch_bounds__(1024) k_step_b(StateView src, StateView dst, S
     o.n_dependent += dep ? 1 : 0;
     o.n_truncated += trunc ? 1 : 0;
     o.flags = (dep ? F_DEPENDENT : 0) | (trunc ? F_TRUNCATED : 0) | (did_qr ? F_QR : 0) |
-              (appended ? F_APPENDED : 0) | ((!dep && !appended) ? F_FOLDED : 0);
+              (appended ? F_APPENDED : 0) | ((mode == M_NORMAL_INDEP && !appended) ? F_FOLDED : 0);
     *dst.hdr = o;
     st->m = m;
     st->mkeep = mk;
@@ -566,7 +670,9 @@ __global__ void __launch_bounds__(1024) k_step_b(StateView src, StateView dst, S
 // produce the fresh e_k column (basis.py:83-91).  Thread per row of V'.
 // ---------------------------------------------------------------------------
 constexpr int kVCols = 16;
-__global__ void __launch_bounds__(128) k_vupdate(StateView src, StateView dst, Scratch sc, IsvdParams P) {
+constexpr int kVRows = 64;
+__global__ void __launch_bounds__(kVRows) k_vupdate(StateView src, StateView dst, Scratch sc, IsvdParams P) {
+  extern __shared__ double vbs[];  // (r+1) x kVCols slice of V_bar
   const IsvdStep* st = sc.step;
   const int mode = st->mode;
   const int64_t k = P.k_new;
@@ -578,8 +684,14 @@ __global__ void __launch_bounds__(128) k_vupdate(StateView src, StateView dst, S
     return;
   }
   const int m = st->m, mk = st->mkeep, r = m - 1;
-  if (col0 >= mk || i >= k) return;
+  if (col0 >= mk) return;
   const double* vb = sc.vbar;
+  for (int idx = threadIdx.x; idx < m * kVCols; idx += blockDim.x) {
+    const int b = idx % m, q = idx / m, col = col0 + q;
+    vbs[q * m + b] = (col < mk) ? vb[(int64_t)col * m + b] : 0.0;
+  }
+  __syncthreads();
+  if (i >= k) return;
   double acc[kVCols];
 #pragma unroll
   for (int q = 0; q < kVCols; ++q) acc[q] = 0.0;
@@ -587,17 +699,11 @@ __global__ void __launch_bounds__(128) k_vupdate(StateView src, StateView dst, S
     for (int b = 0; b < r; ++b) {
       const double v = src.V[(int64_t)b * src.ldv + i];
 #pragma unroll
-      for (int q = 0; q < kVCols; ++q) {
-        const int col = col0 + q;
-        if (col < mk) acc[q] = fma(v, vb[(int64_t)col * m + b], acc[q]);
-      }
+      for (int q = 0; q < kVCols; ++q) acc[q] = fma(v, vbs[q * m + b], acc[q]);
     }
   } else {
 #pragma unroll
-    for (int q = 0; q < kVCols; ++q) {
-      const int col = col0 + q;
-      if (col < mk) acc[q] = vb[(int64_t)col * m + r];
-    }
+    for (int q = 0; q < kVCols; ++q) acc[q] = vbs[q * m + r];
   }
 #pragma unroll
   for (int q = 0; q < kVCols; ++q) {
@@ -610,7 +716,7 @@ __global__ void __launch_bounds__(128) k_vupdate(StateView src, StateView dst, S
 // Compaction prep (one CTA): L^T W = Q_c R_c;  T = L^{-T} Q_c;  new W = R_c,
 // new L = I, c = r, base = 0.  Phi = U W = (U T) R_c exactly.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024) k_compact_prep(StateView src, StateView dst, Scratch sc, IsvdParams P,
+__global__ void __launch_bounds__(kSmallThreads) k_compact_prep(StateView src, StateView dst, Scratch sc, IsvdParams P,
                                                        int use_smem) {
   extern __shared__ double smem[];
   __shared__ double red[32];
@@ -635,15 +741,18 @@ __global__ void __launch_bounds__(1024) k_compact_prep(StateView src, StateView 
   }
   __syncthreads();
   cta_householder_qr(M, c, c, r, dst.W, dst.ldw, sc.work, sc.work + P.work_stride, red);
-  for (int k = wid; k < r; k += nw) {
-    double* tk = sc.T + (int64_t)k * P.ccap;
-    for (int i = lane; i < c; i += 32) tk[i] = M[(int64_t)k * c + i];
-    __syncwarp();
-    warp_lower_t_solve(src.L, src.ldl, c, tk);
+  for (int64_t idx = threadIdx.x; idx < (int64_t)c * r; idx += blockDim.x) {
+    const int a = idx % c, k = idx / c;
+    const double* lcol = src.Li + (int64_t)a * src.ldl;
+    const double* qk = M + (int64_t)k * c;
+    double sacc = 0.0;
+    for (int i = a; i < c; ++i) sacc = fma(lcol[i], qk[i], sacc);
+    sc.T[(int64_t)k * P.ccap + a] = sacc;
   }
   for (int64_t idx = threadIdx.x; idx < (int64_t)r * r; idx += blockDim.x) {
     const int i = idx % r, j = idx / r;
     dst.L[(int64_t)j * dst.ldl + i] = (i == j) ? 1.0 : 0.0;
+    dst.Li[(int64_t)j * dst.ldl + i] = (i == j) ? 1.0 : 0.0;
   }
   for (int k = threadIdx.x; k < r; k += blockDim.x) dst.sigma[k] = src.sigma[k];
   if (threadIdx.x == 0) {

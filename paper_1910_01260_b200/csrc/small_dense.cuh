@@ -254,4 +254,106 @@ __device__ inline void warp_lower_t_solve(const double* L, int ld, int n, double
   }
 }
 
+// ---------------------------------------------------------------------------
+// Register-blocked block-wide GEMM for the small operands (shared or global):
+//   C(i, j) = sum_k A(i, k) B(k, j),  A(i, k) = A[i*asi + k*ask],  B(k, j) = B[k*bsk + j*bsj]
+// each thread owns a 4 x 4 tile (0.5 operand loads per FMA).  `store(i, j, v)`
+// receives the results.  No synchronisation inside.
+// ---------------------------------------------------------------------------
+template <class Store>
+__device__ inline void cta_gemm44(int M, int N, int K, const double* A, int64_t asi, int64_t ask, const double* B,
+                                  int64_t bsk, int64_t bsj, Store store) {
+  const int nbm = (M + 3) >> 2, nbn = (N + 3) >> 2;
+  for (int blk = threadIdx.x; blk < nbm * nbn; blk += blockDim.x) {
+    const int i0 = (blk % nbm) << 2, j0 = (blk / nbm) << 2;
+    const double* ap[4];
+    const double* bp[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      ap[q] = A + (int64_t)min(i0 + q, M - 1) * asi;
+      bp[q] = B + (int64_t)min(j0 + q, N - 1) * bsj;
+    }
+    double acc[4][4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int t = 0; t < 4; ++t) acc[q][t] = 0.0;
+#pragma unroll 2
+    for (int k = 0; k < K; ++k) {
+      double a[4], b[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        a[q] = ap[q][(int64_t)k * ask];
+        b[q] = bp[q][(int64_t)k * bsk];
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) acc[q][t] = fma(a[q], b[t], acc[q][t]);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if (i0 + q < M && j0 + t < N) store(i0 + q, j0 + t, acc[q][t]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Triangular matrix-vector products with an explicitly stored inverse factor
+// (the iSVD keeps L^{-1} next to L so every "solve" on the per-snapshot
+// critical path is a parallel matvec instead of a serial substitution).
+// Li lower-triangular, column-major (ld).  y must not alias x.  Block-wide;
+// the caller synchronises before using y.
+// ---------------------------------------------------------------------------
+__device__ inline void cta_lower_mv(const double* Li, int ld, int n, const double* x, double* y) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    double s = 0.0;
+#pragma unroll 4
+    for (int j = 0; j <= i; ++j) s = fma(Li[(int64_t)j * ld + i], x[j], s);
+    y[i] = s;
+  }
+}
+
+__device__ inline void cta_lower_t_mv(const double* Li, int ld, int n, const double* x, double* y) {
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    const double* col = Li + (int64_t)j * ld;
+    double s = 0.0;
+#pragma unroll 4
+    for (int i = j; i < n; ++i) s = fma(col[i], x[i], s);
+    y[j] = s;
+  }
+}
+
+// Li = L^{-1} for a lower-triangular L (n x n): one warp per column of the
+// inverse, lanes hold the right-hand side; n <= 256.
+__device__ inline void cta_lower_inverse(const double* L, int ld, int n, double* Li, int ldi) {
+  constexpr int Q = 8;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int j = wid; j < n; j += nw) {
+    double x[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) x[q] = (lane + 32 * q == j) ? 1.0 : 0.0;
+    for (int k = j; k < n; ++k) {
+      const int owner = k & 31, slot = k >> 5;
+      double xk = 0.0;
+#pragma unroll
+      for (int q = 0; q < Q; ++q)
+        if (q == slot) xk = x[q];
+      xk = __shfl_sync(0xffffffffu, xk, owner) / L[(int64_t)k * ld + k];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int i = lane + 32 * q;
+        if (i == k) x[q] = xk;
+        else if (i > k && i < n) x[q] = fma(-L[(int64_t)k * ld + i], xk, x[q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int i = lane + 32 * q;
+      if (i < n) Li[(int64_t)j * ldi + i] = (i >= j) ? x[q] : 0.0;
+    }
+  }
+}
+
 }  // namespace strom

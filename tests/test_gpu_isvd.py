@@ -270,19 +270,42 @@ class TestLockstep:
 
 
 # ---------------------------------------------------------------- free-running (P3) on config 1
+def cfg1_snapshots():
+    dt = wl.cfg1_dt()
+    return np.hstack([so.fom_march(d.a, d.b, d.x0, dt, d.inputs) for d in map(wl.cfg1_system, wl.CFG1_TRAIN_NU)])
+
+
+def reference_envelope(u, seeds=(0, 1, 2)):
+    """The reference against itself under a summation-order change (row permutation of the
+    snapshots: mathematically the same problem).  SURVEY 8(c) P3 compares the device with
+    10x this envelope."""
+    ref = so.stream(u, wl.CFG1_TOL, tol_sv=wl.CFG1_TOL)
+    env = np.zeros(8)
+    for sd in seeds:
+        perm = np.random.default_rng(sd).permutation(u.shape[0])
+        r = so.stream(u[perm], wl.CFG1_TOL, tol_sv=wl.CFG1_TOL)
+        env = np.maximum(env, np.abs(r.sigma[:8] - ref.sigma[:8]) / ref.sigma[:8])
+    return ref, env
+
+
 class TestCfg1FreeRunning:
-    def test_pipeline_vs_golden(self, cuda):
+    def test_pipeline_vs_reference_envelope(self, cuda):
         g = load_golden("golden_cfg1.npz")
-        dt = wl.cfg1_dt()
-        mats = [so.fom_march(d.a, d.b, d.x0, dt, d.inputs) for d in map(wl.cfg1_system, wl.CFG1_TRAIN_NU)]
-        u = np.hstack(mats)
+        u = cfg1_snapshots()
+        ref, env = reference_envelope(u)
+        assert np.array_equal(ref.sigma, g["sigma"])
         st = basis.isvd_init(u[:, 0], wl.CFG1_TOL, tol_sv=wl.CFG1_TOL)
         st = basis.ingest_simulation(st, torch.as_tensor(u[:, 1:], device="cuda"))
-        s = npy(st.sigma)
-        ref = g["sigma"]
-        # sigma_i >= 1e-2 sigma_0 (i <= 6): north-star 1e-10 bar, measured reference
-        # 1-ulp envelope 8.4e-11 -> allow 10x the envelope
-        lead = ref >= 1e-2 * ref[0]
-        assert np.max(sigma_rel(s[: lead.sum()], ref[lead])) <= 8.4e-10
-        # leading-5 subspace: reference envelope 3.7e-8
+        s = npy(st.sigma)[:8]
+        lead = ref.sigma[:8] >= 1e-2 * ref.sigma[0]  # i <= 6
+        dev_err = np.abs(s - ref.sigma[:8]) / ref.sigma[:8]
+        print("cfg1 sigma rel vs reference", dev_err[lead], "reference reduction-order envelope", env[lead])
+        assert np.all(dev_err[lead] <= np.maximum(10 * env[lead], 1e-10))
+        # and no less accurate than the reference against the batch SVD (the truth)
+        sb = np.linalg.svd(u, compute_uv=False)[:8]
+        err_dev = np.abs(s - sb) / sb
+        err_ref = np.abs(ref.sigma[:8] - sb) / sb
+        print("vs batch: device", err_dev[lead], "reference", err_ref[lead])
+        assert np.all(err_dev[lead] <= np.maximum(10 * err_ref[lead], 1e-10))
+        # leading-5 subspace: reference envelope 3.7e-8 (SURVEY App. A)
         assert principal_sine(npy(st.phi)[:, :5], g["phi10"][:, :5]) <= 3.7e-7
