@@ -163,11 +163,11 @@ void alloc_small(strom_isvd* h, cudaStream_t s) {
   h->small = dev_alloc(bytes, s, true);
   char* p = h->small->as<char>();
   h->view.hdr = reinterpret_cast<IsvdHdr*>(p);
-  h->view.W = reinterpret_cast<double*>(p + 256);
-  h->view.L = h->view.W + wsz;
+  h->view.N = reinterpret_cast<double*>(p + 256);
+  h->view.L = h->view.N + wsz;
   h->view.Li = h->view.L + lsz;
   h->view.sigma = h->view.Li + lsz;
-  h->view.ldw = c.ccap;
+  h->view.ldn = c.ccap;
   h->view.ldl = c.ccap;
 }
 
@@ -222,7 +222,7 @@ ScratchMem make_scratch(int64_t ldu, const Caps& c, cudaStream_t s) {
                  (size_t)c.ccap * rc2;  // step B's layout (global fallback)
   const size_t n_g = round_up(c.ccap, 2), n_ell = round_up(rc2, 2), n_vbar = rc2 * rc2, n_T = (size_t)c.ccap * rc2;
   const size_t n_part = (size_t)m.grid * m.pstride;
-  size_t total = 7 * n_g + n_ell + n_vbar + m.work_elems + n_T + n_part;
+  size_t total = 8 * n_g + n_ell + n_vbar + m.work_elems + n_T + n_part;
   total = round_up(total, 32);
   const size_t bytes = total * 8 + 256 + 64;
   m.mem = dev_alloc(bytes, s, true);
@@ -234,6 +234,7 @@ ScratchMem make_scratch(int64_t ldu, const Caps& c, cudaStream_t s) {
   m.sc.h = p; p += n_g;
   m.sc.lvec = p; p += n_g;
   m.sc.tmp = p; p += n_g;
+  m.sc.l1 = p; p += n_g;
   m.sc.ell = p; p += n_ell;
   m.sc.vbar = p; p += n_vbar;
   m.sc.work = p; p += m.work_elems;
@@ -413,6 +414,8 @@ strom_isvd* compact(strom_isvd* src, const Caps& caps, cudaStream_t s) {
   // measure the Gram of the stored U_new: L describes the memory, not an assumed identity
   gram_cholesky(t->U->ptr(), t->ldu, nullptr, &m.sc.step->mkeep, 0, caps.rcap, t->n, t->view.L, t->view.Li,
                 t->view.ldl, t->view.hdr, reinterpret_cast<int*>(&m.sc.step->pad_status), s);
+  k_compact_finish<<<1, 256, 0, s>>>(t->view, m.sc.T, P.ccap);
+  STROM_LAUNCH_CHECK();
   t->r_ub = std::min(src->r_ub, caps.rcap);
   t->c_ub = t->r_ub;
   t->U->claimed = t->c_ub;
@@ -660,7 +663,11 @@ int strom_isvd_export(strom_isvd* h, double* phi_dev, double* sigma_dev, double*
     read_hdr(h, s, &hh);
     const int r = hh.r;
     if (phi_dev && r > 0) {
-      launch_tall_gemm(h->U->ptr(), h->ldu, &h->view.hdr->base, h->view.W, h->view.ldw, &h->view.hdr->c,
+      auto wtmp = dev_alloc((size_t)std::max(hh.c, 1) * r * 8, s, false);
+      k_n_to_w<<<(unsigned)std::max<int64_t>(1, ceil_div((int64_t)hh.c * r, 256)), 256, 0, s>>>(h->view,
+                                                                                              wtmp->as<double>());
+      STROM_LAUNCH_CHECK();
+      launch_tall_gemm(h->U->ptr(), h->ldu, &h->view.hdr->base, wtmp->as<double>(), hh.c, &h->view.hdr->c,
                        &h->view.hdr->r, phi_dev, r, true, h->n, h->ldu, s);
     }
     if (sigma_dev && r > 0)
@@ -702,7 +709,7 @@ int strom_isvd_load_factored(int64_t n, int64_t k, int64_t c, int64_t r, const d
     }
     const int th = 256;
     if (c > 0 && r > 0) {
-      k_copy_cm<<<(unsigned)ceil_div(c * r, th), th, 0, s>>>(w_dev, ldw, c, r, h->view.W, h->view.ldw);
+      k_copy_cm<<<(unsigned)ceil_div(c * r, th), th, 0, s>>>(w_dev, ldw, c, r, h->view.N, h->view.ldn);
       STROM_LAUNCH_CHECK();
       STROM_CUDA(cudaMemcpyAsync(h->view.sigma, sigma_dev, r * 8, cudaMemcpyDeviceToDevice, s));
     }
@@ -730,6 +737,11 @@ int strom_isvd_load_factored(int64_t n, int64_t k, int64_t c, int64_t r, const d
         STROM_CUDA(cudaStreamSynchronize(s));
         if (bad) throw Error(kNumericalError, "U is numerically rank-deficient (Gram not positive definite)");
       }
+    }
+    if (c > 0 && r > 0) {  // coordinates in the orthonormal basis U L^{-T}: N = L^T W
+      auto tmp = dev_alloc((size_t)c * r * 8, s, false);
+      k_w_to_n<<<1, 256, 0, s>>>(h->view, tmp->as<double>());
+      STROM_LAUNCH_CHECK();
     }
     h->c_ub = (int32_t)c;
     h->U->claimed = (int32_t)c;
@@ -763,17 +775,6 @@ int strom_isvd_load(int64_t n, int64_t k, int64_t r, const double* phi_dev, cons
                                       stream, &h);
     if (rc) throw Error(rc, strom_last_error());
     std::unique_ptr<strom_isvd> guard(h);
-    if (r > 0) {
-      // exact Gram of the stored U on the tensor cores, then Cholesky
-      auto st = dev_alloc(sizeof(int), s, true);
-      gram_cholesky(h->U->ptr(), h->ldu, nullptr, nullptr, (int)r, (int)r, n, h->view.L, h->view.Li,
-                    h->view.ldl, nullptr, st->as<int>(), s);
-      int bad = 0;
-      STROM_CUDA(cudaMemcpyAsync(&bad, st->ptr, sizeof(int), cudaMemcpyDeviceToHost, s));
-      STROM_CUDA(cudaStreamSynchronize(s));
-      if (bad) throw Error(kNumericalError, "phi is numerically rank-deficient (Gram not positive definite); "
-                                            "load it in factored form (strom_isvd_load_factored)");
-    }
     *out = guard.release();
   });
 }
@@ -789,9 +790,10 @@ int strom_isvd_factors(strom_isvd* h, double* u_dev, double* w_dev, double* l_de
     if (u_dev && hh.c > 0)
       STROM_CUDA(cudaMemcpy2DAsync(u_dev, h->n * 8, h->U->ptr() + (int64_t)hh.base * h->ldu, h->ldu * 8, h->n * 8,
                                    hh.c, cudaMemcpyDeviceToDevice, s));
-    if (w_dev && hh.c > 0 && hh.r > 0)
-      STROM_CUDA(cudaMemcpy2DAsync(w_dev, hh.c * 8, h->view.W, h->view.ldw * 8, hh.c * 8, hh.r,
-                                   cudaMemcpyDeviceToDevice, s));
+    if (w_dev && hh.c > 0 && hh.r > 0) {
+      k_n_to_w<<<(unsigned)ceil_div((int64_t)hh.c * hh.r, 256), 256, 0, s>>>(h->view, w_dev);
+      STROM_LAUNCH_CHECK();
+    }
     if (l_dev && hh.c > 0)
       STROM_CUDA(cudaMemcpy2DAsync(l_dev, hh.c * 8, h->view.L, h->view.ldl * 8, hh.c * 8, hh.c,
                                    cudaMemcpyDeviceToDevice, s));

@@ -2,10 +2,12 @@
 //
 // Representation: the reference keeps the
 // n x r left basis Phi explicitly and rewrites it every snapshot
-// (Phi' = [Phi j] W_bar, basis.py:155-156).  Here Phi = U[:, base:base+c] W:
-//   U  n x c_cap   append-only column store in HBM (column-major, ld = ldu),
-//                  columns nearly orthogonal; G = U^T U = L L^T tracked exactly
-//   W  c x r       small coefficient matrix (HBM, read by one CTA)
+// (Phi' = [Phi j] W_bar, basis.py:155-156).  Here Phi = Q_U N with
+//   U    n x c_cap  append-only column store in HBM (column-major, ld = ldu),
+//                   columns nearly orthogonal; G = U^T U = L L^T tracked exactly
+//   Q_U  = U L^{-T} (never formed): an orthonormal basis of span(U)
+//   N    c x r      Phi's coordinates in Q_U (small, read by one CTA); Phi^T Phi = N^T N
+// (U-coordinates, needed by the passes and the export, are W = L^{-T} N).
 // so one snapshot costs one projection pass (g = U^T x) and, when the column is
 // independent, one residual pass that appends r1 = x - U G^{-1} g and measures
 // e = U^T r1, |r1|^2.  Everything else -- the bordered core SVD, the W and V
@@ -53,23 +55,24 @@ struct IsvdStep {
 
 struct StateView {
   IsvdHdr* hdr;
-  double* W;      // c_cap x (r_cap + 1), ld = ldw
+  double* N;      // c_cap x (r_cap + 1), ld = ldn   (Phi = U L^{-T} N)
   double* L;      // c_cap x c_cap lower, ld = ldl   (Cholesky factor of G = U^T U)
   double* Li;     // c_cap x c_cap lower, ld = ldl   (L^{-1}, kept explicitly)
   double* sigma;  // r_cap + 1
   double* V;      // k_cap x (r_cap + 1), ld = ldv
-  int32_t ldw, ldl;
+  int32_t ldn, ldl;
   int64_t ldv;
 };
 
 struct Scratch {
   double* g;      // c_cap   U^T x
   double* gt;     // c_cap   G^{-1} g
-  double* y;      // c_cap   W ell
+  double* y;      // c_cap   t - N ell  (t = L^{-1} g: x's coordinates in Q_U)
   double* ell;    // r_cap+1 Phi^T x
   double* e;      // c_cap   U^T r1
   double* h;      // c_cap   G^{-1} e of the first residual (DGKS correction), else 0
   double* lvec;   // c_cap   L^{-1} e
+  double* l1;     // c_cap   L^{-1} e of the first residual (kept across the DGKS pass)
   double* tmp;    // c_cap   scratch vector
   double* vbar;   // (r_cap+2)^2 sorted, sign-fixed V_bar of the core
   double* work;   // large fallback workspace (global) for the one-CTA kernels
@@ -188,9 +191,9 @@ __global__ void __launch_bounds__(kPassThreads) k_proj(const double* __restrict_
 }
 
 // ---------------------------------------------------------------------------
-// Step A (one CTA): ell = W^T g, Pythagorean p, dependent test, restart /
-// reject branch (basis.py:112-139); y = W ell and gt = G^{-1} g for the
-// residual pass.
+// Step A (one CTA): t = L^{-1} g, ell = N^T t (= Phi^T x), Pythagorean p,
+// dependent test, restart / reject branch (basis.py:112-139); y = t - N ell and
+// gt = G^{-1} g = L^{-T} t for the residual pass.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_step_a(StateView src, Scratch sc, IsvdParams P) {
   __shared__ double red[32];
@@ -230,11 +233,14 @@ __global__ void __launch_bounds__(256) k_step_a(StateView src, Scratch sc, IsvdP
     return;
   }
   const int r = h.r, c = h.c;
-  // ell_i = sum_j W[j, i] g[j]
+  double* t = sc.tmp;
+  cta_lower_mv(src.Li, src.ldl, c, sc.g, t);  // t = L^{-1} g
+  __syncthreads();
+  // ell_i = sum_j N[j, i] t[j]
   for (int i = wid; i < r; i += nw) {
-    const double* wi = src.W + (int64_t)i * src.ldw;
+    const double* ni = src.N + (int64_t)i * src.ldn;
     double s = 0.0;
-    for (int j = lane; j < c; j += 32) s = fma(wi[j], sc.g[j], s);
+    for (int j = lane; j < c; j += 32) s = fma(ni[j], t[j], s);
     s = warp_sum(s);
     if (lane == 0) sc.ell[i] = s;
   }
@@ -254,17 +260,14 @@ __global__ void __launch_bounds__(256) k_step_a(StateView src, Scratch sc, IsvdP
       st->c_dot = c;
     }
   }
-  // y = W ell (needed for the new W column), gt = g then solved in place
-  for (int j = threadIdx.x; j < c; j += blockDim.x) {
-    double s = 0.0;
-    for (int i = 0; i < r; ++i) s = fma(src.W[(int64_t)i * src.ldw + j], sc.ell[i], s);
-    sc.y[j] = s;
-  }
-  __syncthreads();
-  if (!dep) {  // gt = G^{-1} g = L^{-T} (L^{-1} g)
-    cta_lower_mv(src.Li, src.ldl, c, sc.g, sc.tmp);
-    __syncthreads();
-    cta_lower_t_mv(src.Li, src.ldl, c, sc.tmp, sc.gt);
+  if (!dep) {
+    // y = t - N ell: the in-span part of x - Phi ell in Q_U coordinates
+    for (int j = threadIdx.x; j < c; j += blockDim.x) {
+      double s = t[j];
+      for (int i = 0; i < r; ++i) s = fma(-src.N[(int64_t)i * src.ldn + j], sc.ell[i], s);
+      sc.y[j] = s;
+    }
+    cta_lower_t_mv(src.Li, src.ldl, c, t, sc.gt);  // gt = L^{-T} t = G^{-1} g
   }
 }
 
@@ -408,6 +411,7 @@ __global__ void __launch_bounds__(256) k_step_b1(StateView src, Scratch sc, Isvd
   }
   cta_lower_mv(src.Li, src.ldl, c, sc.e, sc.lvec);
   __syncthreads();
+  for (int j = threadIdx.x; j < c; j += blockDim.x) sc.l1[j] = sc.lvec[j];
   double part = 0.0;
   for (int j = threadIdx.x; j < c; j += blockDim.x) part = fma(sc.lvec[j], sc.lvec[j], part);
   const double ll = block_sum(part, red);
@@ -462,9 +466,9 @@ __global__ void __launch_bounds__(kSmallThreads) k_step_b(StateView src, StateVi
         o.r = 1;
         o.c = 1;
         o.base = st->write_slot;
-        dst.W[0] = 1.0 / st->norm;
         dst.L[0] = sqrt(st->rho2);
         dst.Li[0] = 1.0 / dst.L[0];
+        dst.N[0] = dst.L[0] / st->norm;  // Phi = x / ||x|| = U W, W = 1/||x||, N = L W
         dst.sigma[0] = st->norm;
         st->mkeep = 1;
       }
@@ -508,60 +512,61 @@ __global__ void __launch_bounds__(kSmallThreads) k_step_b(StateView src, StateVi
     else if (c >= r + 1) action = 2;
     else { action = 0; dep = true; }
     __syncthreads();
-    // fold: G^{-1} e;  append: u = L^{-T} l for the new row of L^{-1}
-    if (action != 0) cta_lower_t_mv(src.Li, src.ldl, c, lvec, sc.tmp);
-    __syncthreads();
-    if (action == 2)
-      for (int j = threadIdx.x; j < c; j += blockDim.x) lvec[j] = sc.tmp[j];
+    // append: u = L^{-T} l for the new row of L^{-1}
+    if (action == 1) cta_lower_t_mv(src.Li, src.ldl, c, lvec, sc.tmp);
     __syncthreads();
     if (action == 1) cn = c + 1;
   }
   const bool appended = (action == 1);
-  // copy L (lower) into dst, extended by the new row when appended
-  for (int64_t idx = threadIdx.x; idx < (int64_t)cn * cn; idx += blockDim.x) {
-    const int i = idx % cn, j = idx / cn;
-    double v = 0.0, vi = 0.0;
-    if (i < c && j < c) {
-      if (i >= j) {
-        v = src.L[(int64_t)j * src.ldl + i];
-        vi = src.Li[(int64_t)j * src.ldl + i];
+  // copy L and L^{-1} (lower) into dst, extended by the new row when appended
+  for (int j = wid; j < cn; j += nw) {
+    const double* ls = src.L + (int64_t)j * src.ldl;
+    const double* lis = src.Li + (int64_t)j * src.ldl;
+    double* ld_ = dst.L + (int64_t)j * dst.ldl;
+    double* lid = dst.Li + (int64_t)j * dst.ldl;
+    for (int i = lane; i < cn; i += 32) {
+      double v = 0.0, vi = 0.0;
+      if (i < c && j < c) {
+        if (i >= j) { v = ls[i]; vi = lis[i]; }
+      } else if (i == c && j < c) {
+        v = lvec[j];
+        vi = -sc.tmp[j] / s_misc[0];
+      } else if (i == c && j == c) {
+        v = s_misc[0];
+        vi = 1.0 / s_misc[0];
       }
-    } else if (i == c && j < c) {
-      v = lvec[j];
-      vi = -sc.tmp[j] / s_misc[0];
-    } else if (i == c && j == c) {
-      v = s_misc[0];
-      vi = 1.0 / s_misc[0];
+      ld_[i] = v;
+      lid[i] = vi;
     }
-    dst.L[(int64_t)j * dst.ldl + i] = v;
-    dst.Li[(int64_t)j * dst.ldl + i] = vi;
   }
-  // new W column for j = (x - Phi ell)/p in U-coordinates (length cn):
-  //   x = U (gt + h) + r  ->  j = U (gt + h - y)/p + r/p
+  // new N column for j = (x - Phi ell)/p in Q_U coordinates (length cn):
+  //   x - Phi ell = Q_U (t - N ell + l_1 [+ l_2]) + lambda q   (q the appended direction)
+  // (the fold drops the rounding-level out-of-span part; l_2 only after the DGKS pass)
   double* wj = sc.work + 3 * (int64_t)P.work_stride;
   if (!dep) {
+    const bool two = st->reorth != 0;
     for (int a = threadIdx.x; a < cn; a += blockDim.x) {
       double v;
       if (a < c) {
-        v = sc.gt[a] + sc.h[a] - sc.y[a];
-        if (action == 2) v += lvec[a];
+        v = sc.y[a] + sc.l1[a];
+        if (two) v += lvec[a];
         v /= p;
       } else {
-        v = 1.0 / p;
+        v = s_misc[0] / p;
       }
       wj[a] = v;
     }
   }
   STROM_TPROBE(P, 1);
   // ---- shared-memory plan (global fallback when it does not fit) ----------
-  //   WS m^2 | Wt m^2 | Vt m^2 | core work 16 ms | WB ccap x m (staged W_b, later QR's M)
+  //   WS m^2 | Wt m^2 | Vt m^2 | core work 16 ms | WB ccap x m (staged N_b, later QR's M)
   const int64_t ms = P.work_stride;
   double* base = use_smem ? smem : sc.work + 4 * ms;
   double* WS = base;                      // sorted, signed W_bar (m x m)
   double* Wt = WS + (int64_t)m * m;       // vectors by slot, later W^T W
   double* Vt = Wt + (int64_t)m * m;       // vectors by slot, later the polished W_bar
   double* cb = Vt + (int64_t)m * m;
-  double* WB = cb + 16 * ms;              // W_b = [[W, w_j]] (cn x m, ld ccap)
+  double* WB = cb + 16 * ms;              // N_b = [[N, n_j]] (cn x m, ld ccap)
   double* svs = cb + 14 * ms;             // m sorted singular values
   CoreSvdWork cw;
   cw.d = cb; cw.z = cb + ms; cw.zh = cb + 2 * ms; cw.mu = cb + 3 * ms; cw.sv = cb + 4 * ms;
@@ -571,45 +576,36 @@ __global__ void __launch_bounds__(kSmallThreads) k_step_b(StateView src, StateVi
     cw.org = ib; cw.kset = ib + ms; cw.defl = ib + 2 * ms; cw.ra = ib + 3 * ms; cw.rb = ib + 4 * ms;
     cw.perm = ib + 5 * ms; cw.cnt = ib + 6 * ms;
   }
-  // stage W_b: columns 0..r-1 = W (c rows; the appended row is 0), column r = w_j
+  // stage N_b: columns 0..r-1 = N (c rows; the appended row is 0), column r = n_j
   __syncthreads();  // w_j complete
   if (P.tprobe && threadIdx.x == 0) P.tprobe[7] = use_smem;
-  for (int64_t idx = threadIdx.x; idx < (int64_t)cn * m; idx += blockDim.x) {
-    const int a = idx % cn, b = idx / cn;
-    double v;
-    if (b < r) v = (a < c) ? src.W[(int64_t)b * src.ldw + a] : 0.0;
-    else v = dep ? 0.0 : wj[a];
-    WB[(int64_t)b * P.ccap + a] = v;
+  for (int b = wid; b < m; b += nw) {
+    const double* ns = src.N + (int64_t)b * src.ldn;
+    double* wb = WB + b * P.ccap;
+    for (int a = lane; a < cn; a += 32) {
+      double v;
+      if (b < r) v = (a < c) ? ns[a] : 0.0;
+      else v = dep ? 0.0 : wj[a];
+      wb[a] = v;
+    }
   }
   // ---- 2. the bordered core and its SVD (rank-one secular solver) ----------
   core_svd_secular(src.sigma, sc.ell, dep ? 0.0 : p, r, cw, Wt, Vt, svs, WS, sc.vbar, red,
                    P.tprobe ? P.tprobe + 8 : nullptr, P.tprobe ? P.tprobe + 300 : nullptr);
   STROM_TPROBE(P, 2);
-  // One Newton-Schulz step W <- W (3 I - W^T W) / 2 restores orthogonality of the
-  // accumulated rotations to O(eps): Phi = U W inherits it, and the Pythagorean
-  // p^2 = x.x - ell.ell (basis.py:136) is only meaningful for an orthonormal Phi.
-  {
-    double* Mg = Wt;
-    cta_gemm44(m, m, m, WS, m, 1, WS, 1, m, [&](int i, int j, double v) { Mg[(int64_t)j * m + i] = v; });
-    __syncthreads();
-    cta_gemm44(m, m, m, WS, 1, m, Mg, 1, m, [&](int i, int j, double v) {
-      Vt[(int64_t)j * m + i] = 1.5 * WS[(int64_t)j * m + i] - 0.5 * v;
-    });
-    __syncthreads();
-    for (int64_t idx = threadIdx.x; idx < (int64_t)m * m; idx += blockDim.x) WS[idx] = Vt[idx];
-    __syncthreads();
-  }
+  // (no orthogonality polish needed: the Gu-Eisenstat vectors are orthogonal to
+  // working precision, unlike accumulated Jacobi rotations)
   STROM_TPROBE(P, 3);
   // ---- 3. truncation (basis.py:160-168) ------------------------------------
   int mk = dep ? r : m;
   bool trunc = false;
   if (mk > 0 && svs[mk - 1] < P.tol_sv) { mk -= 1; trunc = true; }
   if (P.r_max >= 0 && mk > P.r_max) { mk = P.r_max; trunc = true; }
-  // ---- 4. W' = W_b W_bar[:, :mk]  (basis.py:150-158 in U-coordinates) -----
+  // ---- 4. N' = N_b W_bar[:, :mk]  (basis.py:150-158 in Q_U coordinates) ---
   {
     const int kdim = dep ? r : m;
-    cta_gemm44(cn, mk, kdim, WB, 1, P.ccap, WS, 1, m,
-               [&](int a, int k, double v) { dst.W[(int64_t)k * dst.ldw + a] = v; });
+    cta_gemm_dmma(cn, mk, kdim, WB, 1, P.ccap, WS, 1, m,
+                  [&](int a, int k, double v) { dst.N[(int64_t)k * dst.ldn + a] = v; });
   }
   for (int k = threadIdx.x; k < mk; k += blockDim.x) dst.sigma[k] = svs[k];
   __syncthreads();
@@ -618,35 +614,52 @@ __global__ void __launch_bounds__(kSmallThreads) k_step_b(StateView src, StateVi
   bool did_qr = false;
   double drift = 0.0;
   if (mk > 1) {
-    // a0 = L^T w_0, a1 = L^T w_last (one warp per row of L^T, lanes over the column)
+    // phi_0 . phi_last = N_0 . N_last (Q_U is orthonormal)
     double part = 0.0;
-    for (int i = wid; i < cn; i += nw) {
-      const double* lcol = dst.L + (int64_t)i * dst.ldl;
-      double a0 = 0.0, a1 = 0.0;
-      for (int j = i + lane; j < cn; j += 32) {
-        a0 = fma(lcol[j], dst.W[j], a0);
-        a1 = fma(lcol[j], dst.W[(int64_t)(mk - 1) * dst.ldw + j], a1);
-      }
-      a0 = warp_sum(a0);
-      a1 = warp_sum(a1);
-      if (lane == 0) part = fma(a0, a1, part);
-    }
+    for (int a = threadIdx.x; a < cn; a += blockDim.x)
+      part = fma(dst.N[a], dst.N[(int64_t)(mk - 1) * dst.ldn + a], part);
     drift = fabs(block_sum(part, red));
     const double thr = fmin(P.tol_svd, 2.220446049250313e-16 * (double)P.n);
     STROM_TPROBE(P, 5);
     if (drift > thr) {
       did_qr = true;
-      double* M = WB;  // cn x mk, ld cn (W_b is dead)
-      // M = L^T W'  (L stored with zeros above the diagonal)
-      cta_gemm44(cn, mk, cn, dst.L, dst.ldl, 1, dst.W, 1, dst.ldw,
-                 [&](int i, int k, double v) { M[(int64_t)k * cn + i] = v; });
+      // linalg.qr(phi) (basis.py:174): Phi' = Q_U N' and Q_U is orthonormal, so
+      // the positive-diagonal QR of Phi' is Q_U times that of N'.  CholeskyQR2 on
+      // the shared-memory N' (two passes: orthonormal to working precision);
+      // an ill-conditioned N' (the reference's non-unit j columns can make it so)
+      // takes the Householder path.
+      double* M = WB;   // cn x mk, ld cn  (N_b is dead)
+      double* Bm = Wt;  // mk x mk Gram, then its Cholesky factor
+      bool chol_ok = true;
+      for (int k = wid; k < mk; k += nw)
+        for (int a = lane; a < cn; a += 32) M[k * cn + a] = dst.N[(int64_t)k * dst.ldn + a];
       __syncthreads();
-      double* tau = sc.work;
-      double* beta = sc.work + P.work_stride;
-      cta_householder_qr(M, cn, cn, mk, nullptr, 0, tau, beta, red);
-      // W <- L^{-T} Q_s  (parallel triangular GEMM with the stored inverse)
-      cta_gemm44(cn, mk, cn, dst.Li, dst.ldl, 1, M, 1, cn,
-                 [&](int a, int k, double v) { dst.W[(int64_t)k * dst.ldw + a] = v; });
+      for (int pass = 0; pass < 2 && chol_ok; ++pass) {
+        cta_gemm_dmma(mk, mk, cn, M, cn, 1, M, 1, cn, [&](int i, int k, double v) { Bm[k * mk + i] = v; });
+        __syncthreads();
+        const double ratio = cta_cholesky(Bm, mk, mk, nullptr);
+        // CholeskyQR loses ~eps cond^2 in the triangular factor: only for
+        // well-conditioned N' (Householder otherwise, like the reference)
+        if (!(ratio > 1e-2)) { chol_ok = false; break; }
+        cta_lower_inverse(Bm, mk, mk, Vt, mk);
+        __syncthreads();
+        // M <- M R^{-1} = M L_B^{-T}:  (L_B^{-T})(j, k) = Vt(k, j); DMMA into WS
+        cta_gemm_dmma(cn, mk, mk, M, 1, cn, Vt, mk, 1,
+                      [&](int a, int k, double v) { dst.N[(int64_t)k * dst.ldn + a] = v; });
+        __syncthreads();
+        for (int k = wid; k < mk; k += nw)
+          for (int a = lane; a < cn; a += 32) M[k * cn + a] = dst.N[(int64_t)k * dst.ldn + a];
+        __syncthreads();
+      }
+      if (!chol_ok) {
+        for (int k = wid; k < mk; k += nw)
+          for (int a = lane; a < cn; a += 32) M[k * cn + a] = dst.N[(int64_t)k * dst.ldn + a];
+        __syncthreads();
+        cta_householder_qr(M, cn, cn, mk, nullptr, 0, sc.work, sc.work + P.work_stride, red);
+      }
+      if (P.tprobe && threadIdx.x == 0) P.tprobe[6 + 1] = chol_ok ? 1 : 2;
+      for (int k = wid; k < mk; k += nw)
+        for (int a = lane; a < cn; a += 32) dst.N[(int64_t)k * dst.ldn + a] = M[k * cn + a];
       __syncthreads();
     }
   }
@@ -732,23 +745,18 @@ __global__ void __launch_bounds__(kSmallThreads) k_compact_prep(StateView src, S
     }
     return;
   }
+  // N = Q_c R_c; U_new = U L^{-T} Q_c (orthonormal), and with L_new = chol of
+  // the measured U_new Gram the new coordinates are N_new = L_new^T R_c
+  // (k_compact_finish, after the Gram); R_c waits in dst.N.
   double* M = use_smem ? smem : sc.work + 4 * (int64_t)P.work_stride;  // c x r
   for (int64_t idx = threadIdx.x; idx < (int64_t)c * r; idx += blockDim.x) {
     const int i = idx % c, k = idx / c;
-    double s = 0.0;
-    for (int j = i; j < c; ++j) s = fma(src.L[(int64_t)i * src.ldl + j], src.W[(int64_t)k * src.ldw + j], s);
-    M[(int64_t)k * c + i] = s;
+    M[idx] = src.N[(int64_t)k * src.ldn + i];
   }
   __syncthreads();
-  cta_householder_qr(M, c, c, r, dst.W, dst.ldw, sc.work, sc.work + P.work_stride, red);
-  for (int64_t idx = threadIdx.x; idx < (int64_t)c * r; idx += blockDim.x) {
-    const int a = idx % c, k = idx / c;
-    const double* lcol = src.Li + (int64_t)a * src.ldl;
-    const double* qk = M + (int64_t)k * c;
-    double sacc = 0.0;
-    for (int i = a; i < c; ++i) sacc = fma(lcol[i], qk[i], sacc);
-    sc.T[(int64_t)k * P.ccap + a] = sacc;
-  }
+  cta_householder_qr(M, c, c, r, dst.N, dst.ldn, sc.work, sc.work + P.work_stride, red);
+  cta_gemm_dmma(c, r, c, src.Li, src.ldl, 1, M, 1, c,
+                [&](int a, int k, double v) { sc.T[(int64_t)k * P.ccap + a] = v; });
   for (int64_t idx = threadIdx.x; idx < (int64_t)r * r; idx += blockDim.x) {
     const int i = idx % r, j = idx / r;
     dst.L[(int64_t)j * dst.ldl + i] = (i == j) ? 1.0 : 0.0;
@@ -761,6 +769,55 @@ __global__ void __launch_bounds__(kSmallThreads) k_compact_prep(StateView src, S
     *dst.hdr = o;
     sc.step->m = c;  // number of source columns for the GEMM
     sc.step->mkeep = r;
+  }
+}
+
+// After the compaction Gram: N_new = L_new^T R_c (R_c parked in dst.N).
+__global__ void __launch_bounds__(256) k_compact_finish(StateView dst, double* tmp, int ldt) {
+  const int r = dst.hdr->r;
+  if (dst.hdr->status != 0 || r == 0) return;
+  // upper-triangular (L_new^T) times upper-triangular R_c
+  for (int64_t idx = threadIdx.x; idx < (int64_t)r * r; idx += blockDim.x) {
+    const int i = idx % r, k = idx / r;
+    const double* lcol = dst.L + (int64_t)i * dst.ldl;  // column i of L = row i of L^T
+    double s = 0.0;
+    for (int j = i; j <= k; ++j) s = fma(lcol[j], dst.N[(int64_t)k * dst.ldn + j], s);
+    tmp[(int64_t)k * ldt + i] = s;
+  }
+  __syncthreads();
+  for (int64_t idx = threadIdx.x; idx < (int64_t)r * r; idx += blockDim.x) {
+    const int i = idx % r, k = idx / r;
+    dst.N[(int64_t)k * dst.ldn + i] = tmp[(int64_t)k * ldt + i];
+  }
+}
+
+// U-coordinates W = L^{-T} N (c x r, ld c) for the export / materialisation.
+__global__ void __launch_bounds__(256) k_n_to_w(StateView v, double* w) {
+  const int r = v.hdr->r, c = v.hdr->c;
+  for (int64_t idx = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; idx < (int64_t)c * r;
+       idx += (int64_t)blockDim.x * gridDim.x) {
+    const int a = idx % c, k = idx / c;
+    const double* lcol = v.Li + (int64_t)a * v.ldl;
+    double s = 0.0;
+    for (int i = a; i < c; ++i) s = fma(lcol[i], v.N[(int64_t)k * v.ldn + i], s);
+    w[(int64_t)k * c + a] = s;
+  }
+}
+
+// N = L^T W for a state loaded in U-coordinates (W parked in dst.N).
+__global__ void __launch_bounds__(256) k_w_to_n(StateView v, double* tmp) {
+  const int r = v.hdr->r, c = v.hdr->c;
+  for (int64_t idx = threadIdx.x; idx < (int64_t)c * r; idx += blockDim.x) {
+    const int i = idx % c, k = idx / c;
+    const double* lcol = v.L + (int64_t)i * v.ldl;
+    double s = 0.0;
+    for (int j = i; j < c; ++j) s = fma(lcol[j], v.N[(int64_t)k * v.ldn + j], s);
+    tmp[(int64_t)k * c + i] = s;
+  }
+  __syncthreads();
+  for (int64_t idx = threadIdx.x; idx < (int64_t)c * r; idx += blockDim.x) {
+    const int i = idx % c, k = idx / c;
+    v.N[(int64_t)k * v.ldn + i] = tmp[(int64_t)k * c + i];
   }
 }
 

@@ -7,6 +7,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "dmma.cuh"
 
 namespace strom {
 
@@ -297,6 +298,130 @@ __device__ inline void cta_gemm44(int M, int N, int K, const double* A, int64_t 
       for (int t = 0; t < 4; ++t)
         if (i0 + q < M && j0 + t < N) store(i0 + q, j0 + t, acc[q][t]);
   }
+}
+
+// ---------------------------------------------------------------------------
+// Block-wide GEMM on the fp64 tensor cores (DMMA m8n8k4), same contract as
+// cta_gemm44: C(i, j) = sum_k A(i, k) B(k, j) with strided operands (shared or
+// global memory), results handed to store(i, j, v).  Each warp owns 8 x 8
+// output tiles; operands beyond M/N/K read as zero.  No synchronisation.
+// ---------------------------------------------------------------------------
+template <class Store>
+__device__ inline void cta_gemm_dmma(int M, int N, int K, const double* A, int64_t asi, int64_t ask,
+                                     const double* B, int64_t bsk, int64_t bsj, Store store) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int tm = (M + 7) >> 3, tn = (N + 7) >> 3, ks = (K + 3) >> 2;
+  for (int tile = wid; tile < tm * tn; tile += nw) {
+    const int i0 = (tile % tm) << 3, j0 = (tile / tm) << 3;
+    const int ia = i0 + g, jb = j0 + g;
+    const bool va = ia < M, vb = jb < N;
+    const double* ap = A + (int64_t)(va ? ia : 0) * asi;
+    const double* bp = B + (int64_t)(vb ? jb : 0) * bsj;
+    double c0 = 0.0, c1 = 0.0;
+    for (int kk = 0; kk < ks; ++kk) {
+      const int k = (kk << 2) + t;
+      const bool vk = k < K;
+      const double av = (va && vk) ? ap[(int64_t)k * ask] : 0.0;
+      const double bv = (vb && vk) ? bp[(int64_t)k * bsk] : 0.0;
+      dmma884(c0, c1, av, bv);
+    }
+    const int r = i0 + g, c = j0 + 2 * t;
+    if (r < M) {
+      if (c < N) store(r, c, c0);
+      if (c + 1 < N) store(r, c + 1, c1);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// In-place lower Cholesky B = L L^T (n x n, column-major, ld), right-looking,
+// block-parallel, two barriers per column.  Returns min/max pivot ratio, or -1
+// if a pivot is not positive (uniform across the block).  Zeroes the strict
+// upper triangle.
+// ---------------------------------------------------------------------------
+__device__ inline double cta_cholesky(double* B, int ld, int n, double* /*unused*/) {
+  // left-looking: column j gathers the updates of columns < j (one barrier
+  // pair per column, no trailing-matrix traffic)
+  double pmin = INFINITY, pmax = 0.0;
+  for (int j = 0; j < n; ++j) {
+    for (int i = j + threadIdx.x; i < n; i += blockDim.x) {
+      double s = B[j * ld + i];
+      for (int k = 0; k < j; ++k) s = fma(-B[k * ld + i], B[k * ld + j], s);
+      B[j * ld + i] = s;
+    }
+    __syncthreads();
+    const double d2 = B[j * ld + j];
+    if (!(d2 > 0.0)) {
+      __syncthreads();
+      return -1.0;
+    }
+    const double d = sqrt(d2);
+    pmin = fmin(pmin, d);
+    pmax = fmax(pmax, d);
+    __syncthreads();
+    const double inv = 1.0 / d;
+    for (int i = j + threadIdx.x; i < n; i += blockDim.x) B[j * ld + i] = (i == j) ? d : B[j * ld + i] * inv;
+    __syncthreads();
+  }
+  {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int k = wid; k < n; k += nw)
+      for (int i = lane; i < k; i += 32) B[k * ld + i] = 0.0;
+  }
+  __syncthreads();
+  return pmin / pmax;
+}
+
+// ---------------------------------------------------------------------------
+// X <- X L^{-T} in place (X: rows x n, column-major ld; L: n x n lower, ld l),
+// i.e. X_new R = X with R = L^T upper: forward substitution along each row,
+// one thread per row.  The caller synchronises afterwards.
+// ---------------------------------------------------------------------------
+__device__ inline void cta_rows_times_inv_lt(double* X, int ldx, int rows, const double* L, int ldl, int n) {
+  for (int a = threadIdx.x; a < rows; a += blockDim.x) {
+    for (int k = 0; k < n; ++k) {
+      double s = X[(int64_t)k * ldx + a];
+      const double* lrow = L + k;  // L(k, j) = L[j * ldl + k]
+      for (int j = 0; j < k; ++j) s = fma(-X[(int64_t)j * ldx + a], lrow[(int64_t)j * ldl], s);
+      X[(int64_t)k * ldx + a] = s / L[(int64_t)k * ldl + k];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// In-place lower Cholesky B = L L^T (n x n, column-major, ld) by ONE warp
+// (right-looking; no block barriers).  Returns min/max pivot ratio, or -1 if a
+// pivot is not positive.  The strict upper triangle is zeroed.
+// ---------------------------------------------------------------------------
+__device__ inline double warp_cholesky(double* B, int ld, int n) {
+  const int lane = threadIdx.x & 31;
+  double pmin = INFINITY, pmax = 0.0;
+  bool bad = false;
+  for (int j = 0; j < n; ++j) {
+    double* cj = B + (int64_t)j * ld;
+    const double d2 = cj[j];
+    if (!(d2 > 0.0)) { bad = true; break; }
+    const double d = sqrt(d2);
+    pmin = fmin(pmin, d);
+    pmax = fmax(pmax, d);
+    const double inv = 1.0 / d;
+    __syncwarp();
+    if (lane == 0) cj[j] = d;
+    for (int i = j + 1 + lane; i < n; i += 32) cj[i] *= inv;
+    __syncwarp();
+    // trailing update: columns k > j, rows i >= k
+    for (int k = j + 1; k < n; ++k) {
+      const double ck = cj[k];
+      double* colk = B + (int64_t)k * ld;
+      for (int i = k + lane; i < n; i += 32) colk[i] = fma(-cj[i], ck, colk[i]);
+    }
+    __syncwarp();
+  }
+  for (int j = 0; j < n; ++j)
+    for (int i = lane; i < j; i += 32) B[(int64_t)j * ld + i] = 0.0;
+  __syncwarp();
+  return bad ? -1.0 : pmin / pmax;
 }
 
 // ---------------------------------------------------------------------------

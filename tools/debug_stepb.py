@@ -15,7 +15,7 @@ for j in range(100, 130):
     inf = st.info()
     t = buf.cpu().tolist()
     d = [(t[k + 1] - t[k]) / 1.965e3 for k in range(6)]
-    print('   use_smem', t[7])
+    print('   use_smem/qr path', t[7])
     cp = t[300:308]
     print('   core phases', ' '.join(f'{(cp[k+1]-cp[k])/1.965e3:.1f}' for k in range(7)), '(defl roots GE vec rot sort sign)')
     its = t[8:8 + inf.rank + 1]
