@@ -107,17 +107,19 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------- dist
-def dist_setup(want_gpus):
+def dist_setup(want_gpus, backend=None):
+    """One process per GPU (torchrun env).  backend defaults to nccl; the CPU
+    tests drive the same helpers over gloo."""
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if ws > 1:
+        import torch
         import torch.distributed as dist
 
-        backend = "nccl"
-        import torch
-
-        torch.cuda.set_device(local)
+        backend = backend or "nccl"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
         dist.init_process_group(backend=backend)
     return ws, rank, local
 
@@ -130,14 +132,26 @@ def barrier(ws):
 
 
 def allmax(ws, x):
+    """Max over ranks (the timing rule: the slowest rank's device time)."""
     if ws == 1:
         return x
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def whole_job_rate(units_per_rank_step, steps, ws, ms_max):
+    """value: units processed by ALL ranks / the slowest rank's device time."""
+    return units_per_rank_step * steps * ws / (ms_max / 1e3)
+
+
+def replica_seed(rank):
+    """Replicas only: rank r ingests its own independent cfg2 stream (seed r)."""
+    return rank
 
 
 # --------------------------------------------------------------------------- device arm
@@ -147,7 +161,7 @@ def bench_isvd_device(args, ws, rank):
     from paper_1910_01260_b200 import _capi, basis, workloads as wl
 
     dev = torch.device("cuda", torch.cuda.current_device())
-    xt, _, _, _ = wl.cfg2_stream_torch(n=N_S, cols=COLS, rank=RANK, seed=rank, device=dev)
+    xt, _, _, _ = wl.cfg2_stream_torch(n=N_S, cols=COLS, rank=RANK, seed=replica_seed(rank), device=dev)
     torch.cuda.synchronize()
     st0 = basis.isvd_init(xt[0], TOL, tol_sv=TOL, r_max=RANK, cap_mode="truncate")
     st100 = basis.ingest_simulation(st0, xt[1:WARM_COLS].T)
@@ -178,7 +192,7 @@ def bench_isvd_device(args, ws, rank):
     lib.strom_profile_read(16, launches, None, None)
     gpu_launches = int(sum(launches[k] for k in range(len(PROF_KINDS))))
     ms_max = allmax(ws, ms)
-    value = nsnap * args.steps * ws / (ms_max / 1e3)
+    value = whole_job_rate(nsnap, args.steps, ws, ms_max)
     # ---- profiled repetition: per-kernel CUDA-event durations + algorithmic bytes
     lib.strom_profile_reset()
     lib.strom_profile_enable(1)
