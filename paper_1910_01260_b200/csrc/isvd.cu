@@ -1,9 +1,13 @@
 // Host orchestration + C ABI of the streaming incremental SVD
 // (reference basis.py:30-194).  See isvd_kernels.cuh for the representation.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <vector>
+
+#include <cudaTypedefs.h>
 
 #include "../../include/strom_b200.h"
 #include "gram.cuh"
@@ -95,26 +99,38 @@ __global__ void k_copy_g_col(const double* g, int c, double* G, int ld, int j) {
   for (int i = threadIdx.x; i < c; i += blockDim.x) G[(int64_t)j * ld + i] = g[i];
 }
 
-inline int maxj_for(int ccap) {
-  const int need = (ccap + 7) / 8;
-  if (need <= 2) return 2;
-  if (need <= 4) return 4;
-  if (need <= 8) return 8;
-  if (need <= 16) return 16;
-  return 32;
-}
-
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// diagnostics: STROM_TRACE=1 synchronises and names every launch of the update
+void trace_point(const char* what, cudaStream_t s) {
+  static const bool on = [] {
+    const char* e = getenv("STROM_TRACE");
+    return e && atoi(e) != 0;
+  }();
+  if (!on) return;
+  fprintf(stderr, "[strom] %s ...", what);
+  fflush(stderr);
+  cudaError_t e = cudaStreamSynchronize(s);
+  fprintf(stderr, " %s\n", cudaGetErrorString(e));
+}
 
 long long* g_tprobe = nullptr;  // step-B phase timestamps (strom_debug_tprobe)
 
 // ------------------------------------------------------------------ state
-struct UBuf {
-  DevMemPtr mem;
+// The append-only store shared by a state and its successors: U (n x ccap,
+// column-major, ld ldu) and the exact factors L, L^{-1} of G = U^T U, indexed
+// by physical column.  `claimed` bounds the physical columns any live state
+// may have written: a successor that would append past a state whose c_ub is
+// below `claimed` copies the store first (copy-on-write).
+struct Store {
+  DevMemPtr umem, lmem;
   int64_t ldu = 0;
   int32_t ccap = 0;
-  int32_t claimed = 0;  // host bound: no live state uses a physical column >= claimed
-  double* ptr() const { return mem->as<double>(); }
+  int32_t claimed = 0;
+  CUtensorMap umap{};  // 2D TMA descriptor of U (rows x ccap), box kStageRows x 8
+  double* U() const { return umem->as<double>(); }
+  double* L() const { return lmem->as<double>(); }
+  double* Li() const { return L() + (size_t)ccap * ccap; }
 };
 
 struct Caps {
@@ -131,14 +147,14 @@ struct strom_isvd {
   Caps caps;
   int32_t c_ub = 0;  // bound on base + c (physical end of used columns)
   int32_t r_ub = 0;  // bound on rank
-  std::shared_ptr<UBuf> U;
+  std::shared_ptr<Store> store;
   DevMemPtr small, vmem;
   StateView view{};
 };
 
 namespace {
 
-// ccap = rcap + 1 + slack; 2 rcap keeps c_cap = 128 (8 columns per warp) at rank 64
+// ccap = rcap + 1 + slack; 2 rcap keeps c_cap = 128 at rank 64
 int32_t slack_for(int32_t rcap) { return std::max<int32_t>(16, rcap - 1); }
 
 Caps make_caps(int64_t n, int32_t r_max, int32_t want_r, int64_t k) {
@@ -154,35 +170,76 @@ Caps make_caps(int64_t n, int32_t r_max, int32_t want_r, int64_t k) {
   return c;
 }
 
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  if (!fn) throw Error(kCudaError, "cuTensorMapEncodeTiled is unavailable");
+  return fn;
+}
+
+void encode_umap(Store* st) {
+  cuuint64_t dims[2] = {(cuuint64_t)st->ldu, (cuuint64_t)st->ccap};
+  cuuint64_t strides[1] = {(cuuint64_t)st->ldu * 8};
+  cuuint32_t box[2] = {(cuuint32_t)kStageRows, (cuuint32_t)kBoxCols};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = tensor_map_encoder()(&st->umap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, st->umem->ptr, dims, strides, box,
+                                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(kCudaError, "cuTensorMapEncodeTiled failed for the U store");
+}
+
+std::shared_ptr<Store> alloc_store(int64_t n, int64_t ldu, int32_t ccap, cudaStream_t s) {
+  auto st = std::make_shared<Store>();
+  st->umem = dev_alloc((size_t)ldu * ccap * 8, s, false);
+  if (ldu > n)  // padding rows are read by the passes: keep them zero (never NaN)
+    STROM_CUDA(cudaMemset2DAsync(st->umem->as<double>() + n, ldu * 8, 0, (ldu - n) * 8, ccap, s));
+  st->lmem = dev_alloc((size_t)2 * ccap * ccap * 8, s, true);
+  st->ldu = ldu;
+  st->ccap = ccap;
+  encode_umap(st.get());
+  return st;
+}
+
+void set_store(strom_isvd* h, const std::shared_ptr<Store>& st) {
+  h->store = st;
+  h->view.L = st->L();
+  h->view.Li = st->Li();
+  h->view.ldl = st->ccap;
+}
+
+// copy-on-write: a private store holding the first c_ub physical columns
+std::shared_ptr<Store> clone_store(const Store& src, int64_t n, int32_t c_ub, cudaStream_t s) {
+  auto st = alloc_store(n, src.ldu, src.ccap, s);
+  if (c_ub > 0)
+    STROM_CUDA(cudaMemcpyAsync(st->U(), src.U(), (size_t)src.ldu * c_ub * 8, cudaMemcpyDeviceToDevice, s));
+  STROM_CUDA(cudaMemcpyAsync(st->L(), src.L(), (size_t)2 * src.ccap * src.ccap * 8, cudaMemcpyDeviceToDevice, s));
+  st->claimed = c_ub;
+  return st;
+}
+
 void alloc_small(strom_isvd* h, cudaStream_t s) {
   const Caps& c = h->caps;
   const size_t wsz = (size_t)c.ccap * (c.rcap + 1);
-  const size_t lsz = (size_t)c.ccap * c.ccap;
   const size_t ssz = (size_t)c.rcap + 2;
-  const size_t bytes = 256 + 8 * (wsz + 2 * lsz + ssz);
+  const size_t bytes = 256 + 8 * (wsz + ssz);
   h->small = dev_alloc(bytes, s, true);
   char* p = h->small->as<char>();
   h->view.hdr = reinterpret_cast<IsvdHdr*>(p);
   h->view.N = reinterpret_cast<double*>(p + 256);
-  h->view.L = h->view.N + wsz;
-  h->view.Li = h->view.L + lsz;
-  h->view.sigma = h->view.Li + lsz;
+  h->view.sigma = h->view.N + wsz;
   h->view.ldn = c.ccap;
-  h->view.ldl = c.ccap;
 }
 
 void alloc_v(strom_isvd* h, cudaStream_t s) {
   h->vmem = dev_alloc((size_t)h->caps.kcap * (h->caps.rcap + 1) * 8, s, false);
   h->view.V = h->vmem->as<double>();
   h->view.ldv = h->caps.kcap;
-}
-
-std::shared_ptr<UBuf> alloc_u(int64_t ldu, int32_t ccap, cudaStream_t s) {
-  auto u = std::make_shared<UBuf>();
-  u->mem = dev_alloc((size_t)ldu * ccap * 8, s, true);
-  u->ldu = ldu;
-  u->ccap = ccap;
-  return u;
 }
 
 strom_isvd* new_like(const strom_isvd* src, const Caps& caps) {
@@ -198,55 +255,58 @@ strom_isvd* new_like(const strom_isvd* src, const Caps& caps) {
   return h;
 }
 
-// per-call scratch
-struct ScratchMem {
+// ------------------------------------------------------------------ pipeline scratch
+struct PipeMem {
   DevMemPtr mem;
-  Scratch sc{};
-  int grid = 0;
-  int pstride = 0, work_stride = 0;
-  size_t work_elems = 0;
+  Pipe pp{};
+  int32_t ccap = 0, rcap = 0;
+  int pstride = 0, work_stride = 0, max_grid = 0;
 };
 
-int pass_grid(int64_t ldu) {
-  const int64_t ntiles = ldu / kTileRows;
-  return (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)sm_count() * 4));
-}
-
-ScratchMem make_scratch(int64_t ldu, const Caps& c, cudaStream_t s) {
-  ScratchMem m;
-  m.grid = pass_grid(ldu);
-  m.pstride = (int)round_up(c.ccap + 2, 8);
+PipeMem make_pipe(const Caps& c, cudaStream_t s) {
+  PipeMem m;
+  m.ccap = c.ccap;
+  m.rcap = c.rcap;
+  m.max_grid = sm_count() * 8;
+  m.pstride = (int)(2 * round_up(c.ccap + 1, 4) + 8);
   const int64_t rc2 = c.rcap + 2;
   m.work_stride = (int)round_up(std::max<int64_t>(c.ccap, rc2), 32);
-  m.work_elems = 4 * (size_t)m.work_stride + 3 * rc2 * rc2 + 16 * (size_t)m.work_stride +
-                 (size_t)c.ccap * rc2;  // step B's layout (global fallback)
-  const size_t n_g = round_up(c.ccap, 2), n_ell = round_up(rc2, 2), n_vbar = rc2 * rc2, n_T = (size_t)c.ccap * rc2;
-  const size_t n_part = (size_t)m.grid * m.pstride;
-  size_t total = 8 * n_g + n_ell + n_vbar + m.work_elems + n_T + n_part;
+  const size_t work_elems = 4 * (size_t)m.work_stride + 3 * rc2 * rc2 + 16 * (size_t)m.work_stride +
+                            (size_t)c.ccap * rc2;  // step B's layout (global fallback)
+  const size_t nv = round_up(c.ccap + 2, 4), nell = round_up(rc2, 4);
+  const size_t n_part = (size_t)m.max_grid * m.pstride;
+  size_t total = 2 * nell + 2 * nv + 6 * nv + 2 * (2 * nv + 8) + rc2 * rc2 + work_elems + (size_t)c.ccap * rc2 + n_part;
   total = round_up(total, 32);
-  const size_t bytes = total * 8 + 256 + 64;
+  const size_t bytes = total * 8 + 512;
   m.mem = dev_alloc(bytes, s, true);
   double* p = m.mem->as<double>();
-  m.sc.g = p; p += n_g;
-  m.sc.gt = p; p += n_g;
-  m.sc.y = p; p += n_g;
-  m.sc.e = p; p += n_g;
-  m.sc.h = p; p += n_g;
-  m.sc.lvec = p; p += n_g;
-  m.sc.tmp = p; p += n_g;
-  m.sc.l1 = p; p += n_g;
-  m.sc.ell = p; p += n_ell;
-  m.sc.vbar = p; p += n_vbar;
-  m.sc.work = p; p += m.work_elems;
-  m.sc.T = p; p += n_T;
-  m.sc.part = p; p += n_part;
+  for (int i = 0; i < 2; ++i) { m.pp.ell[i] = p; p += nell; }
+  for (int i = 0; i < 2; ++i) { m.pp.nj[i] = p; p += nv; }
+  m.pp.tvec = p; p += nv;
+  m.pp.gt = p; p += nv;
+  m.pp.y = p; p += nv;
+  m.pp.l1 = p; p += nv;
+  m.pp.h = p; p += nv;
+  m.pp.tmp = p; p += nv;
+  m.pp.fo.e = p; p += nv;
+  m.pp.fo.gn = p; p += nv;
+  m.pp.fo.scal = p; p += 8;
+  m.pp.ro.e = p; p += nv;
+  m.pp.ro.gn = p; p += nv;
+  m.pp.ro.scal = p; p += 8;
+  m.pp.vbar = p; p += rc2 * rc2;
+  m.pp.work = p; p += work_elems;
+  m.pp.T = p; p += (size_t)c.ccap * rc2;
+  m.pp.part = p; p += n_part;
   char* q = m.mem->as<char>() + total * 8;
-  m.sc.step = reinterpret_cast<IsvdStep*>(q);
-  m.sc.counter = reinterpret_cast<unsigned*>(q + 256);
+  m.pp.ctl = reinterpret_cast<PipeCtl*>(q);
+  m.pp.step[0] = reinterpret_cast<IsvdStep*>(q + 64);
+  m.pp.step[1] = reinterpret_cast<IsvdStep*>(q + 192);
+  m.pp.counter = reinterpret_cast<unsigned*>(q + 384);
   return m;
 }
 
-IsvdParams make_params(const strom_isvd* h, const ScratchMem& m, int64_t k_new, bool init_call) {
+IsvdParams make_params(const strom_isvd* h, const PipeMem& m, int64_t k_new, bool init_call) {
   IsvdParams P;
   P.n = h->n;
   P.ldu = h->ldu;
@@ -259,57 +319,133 @@ IsvdParams make_params(const strom_isvd* h, const ScratchMem& m, int64_t k_new, 
   P.k_new = k_new;
   P.pstride = m.pstride;
   P.work_stride = m.work_stride;
+  P.parity = 0;
+  P.has_next = 0;
+  P.L = h->store->L();
+  P.Li = h->store->Li();
   P.prof = prof_dev_bytes();
   P.tprobe = g_tprobe;
   return P;
 }
 
+// ------------------------------------------------------------------ launchers
+template <class K>
+void set_smem_attr(K kernel, size_t smem, size_t* configured) {
+  // the default cap counts static shared memory too: raise it whenever a launch
+  // asks for more dynamic shared memory than any earlier one
+  if (smem > 32 * 1024 && smem > *configured) {
+    STROM_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    *configured = smem;
+  }
+}
+
+inline int pass_maxj(int cols) {
+  const int need = (cols + kPassConsumers - 1) / kPassConsumers;
+  if (need <= 1) return 1;
+  if (need <= 2) return 2;
+  if (need <= 4) return 4;
+  if (need <= 8) return 8;
+  if (need <= 12) return 12;
+  if (need <= 16) return 16;
+  if (need <= 24) return 24;
+  return 32;
+}
+
+// pipeline depth: stages of kStageRows x cols within ~180 KB (2 .. kPassMaxStages)
+inline int pass_stages(int cols) {
+  const size_t per = (size_t)kStageRows * std::max(cols, 1) * 8;
+  return (int)std::max<size_t>(2, std::min<size_t>(kPassMaxStages, (180u * 1024u) / per));
+}
+
 template <int MAXJ>
-void launch_proj_t(const double* U, const double* x, const StateView& v, const ScratchMem& m, const IsvdParams& P,
+void launch_pass_t(const CUtensorMap& umap, const PassArgs& a, int cols_ub, int reserve, int kind_prof,
                    cudaStream_t s) {
-  ProfScope ps(P_PROJ, s);
-  k_proj<MAXJ><<<m.grid, kPassThreads, 0, s>>>(U, x, v, m.sc, P);
+  const int cols = (int)round_up(std::max(cols_ub, 1), kBoxCols);
+  const int nst = pass_stages(cols);
+  const size_t smem = (size_t)nst * kStageRows * cols * 8;
+  static size_t cfg = 0;
+  set_smem_attr(k_pass<MAXJ>, smem, &cfg);
+  const int64_t ntiles = a.ldu / kStageRows;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, std::max(1, sm_count() - reserve)));
+  ProfScope ps(kind_prof, s);
+  k_pass<MAXJ><<<grid, kPassThreads, smem, s>>>(umap, a, nst);
+  {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      cudaFuncAttributes fa{};
+      cudaFuncGetAttributes(&fa, k_pass<MAXJ>);
+      char buf[256];
+      snprintf(buf, sizeof buf, "k_pass<%d> launch (grid %d, smem %zu + static %zu, max dyn %d, regs %d, stages %d): %s",
+               MAXJ, grid, smem, (size_t)fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes, fa.numRegs, nst,
+               cudaGetErrorString(e));
+      throw Error(kCudaError, buf);
+    }
+  }
+}
+
+// kind PASS_*; cols_ub bounds the U columns the pass may read
+void launch_pass(int kind, int cols_ub, const strom_isvd* h, const PipeMem& m, const double* x, const double* xn,
+                 int reserve, cudaStream_t s) {
+  PassArgs a;
+  a.U = h->store->U();
+  a.ldu = h->ldu;
+  a.n = h->n;
+  a.ctl = m.pp.ctl;
+  a.kind = kind;
+  a.pstride = m.pstride;
+  a.x = x;
+  a.coef = (kind == PASS_FUSED) ? m.pp.gt : (kind == PASS_SECOND ? m.pp.h : nullptr);
+  a.xn = xn;
+  a.out = (kind == PASS_SECOND) ? m.pp.ro : m.pp.fo;
+  a.part = m.pp.part;
+  a.counter = m.pp.counter;
+  a.prof = prof_dev_bytes();
+  const int pk = (kind == PASS_SECOND) ? P_RESID : P_PROJ;
+  const int cu = std::max(cols_ub, 1);
+  switch (pass_maxj(cu)) {
+    case 1: launch_pass_t<1>(h->store->umap, a, cu, reserve, pk, s); break;
+    case 2: launch_pass_t<2>(h->store->umap, a, cu, reserve, pk, s); break;
+    case 4: launch_pass_t<4>(h->store->umap, a, cu, reserve, pk, s); break;
+    case 8: launch_pass_t<8>(h->store->umap, a, cu, reserve, pk, s); break;
+    case 12: launch_pass_t<12>(h->store->umap, a, cu, reserve, pk, s); break;
+    case 16: launch_pass_t<16>(h->store->umap, a, cu, reserve, pk, s); break;
+    case 24: launch_pass_t<24>(h->store->umap, a, cu, reserve, pk, s); break;
+    default: launch_pass_t<32>(h->store->umap, a, cu, reserve, pk, s); break;
+  }
+}
+
+size_t decide_smem(const PipeMem& m) { return (size_t)(kDecideThreads / 32) * round_up(m.ccap, 32) * 8; }
+
+
+void launch_prep(const PipeMem& m, const IsvdParams& P, cudaStream_t s) {
+  static size_t cfg = 0;
+  const size_t smem = decide_smem(m);
+  set_smem_attr(k_prep, smem, &cfg);
+  ProfScope ps(P_STEP_A, s);
+  k_prep<<<1, kDecideThreads, smem, s>>>(m.pp, P);
   STROM_LAUNCH_CHECK();
 }
 
-void launch_proj(int ccap, const double* U, const double* x, const StateView& v, const ScratchMem& m,
-                 const IsvdParams& P, cudaStream_t s) {
-  switch (maxj_for(ccap)) {
-    case 2: launch_proj_t<2>(U, x, v, m, P, s); break;
-    case 4: launch_proj_t<4>(U, x, v, m, P, s); break;
-    case 8: launch_proj_t<8>(U, x, v, m, P, s); break;
-    case 16: launch_proj_t<16>(U, x, v, m, P, s); break;
-    default: launch_proj_t<32>(U, x, v, m, P, s); break;
-  }
-}
-
-template <int MAXJ>
-void launch_resid_t(double* U, const double* x, const StateView& v, const ScratchMem& m, const IsvdParams& P,
-                    cudaStream_t s, int phase) {
-  const size_t smem = ((size_t)kTileRows * P.ccap + P.ccap + 1 + 3 * kTileRows + 4 * kTileRows) * 8;
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    STROM_CUDA(cudaFuncSetAttribute(k_resid<MAXJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = smem;
-  }
-  ProfScope ps(P_RESID, s);
-  k_resid<MAXJ><<<m.grid, kPassThreads, smem, s>>>(U, x, v, m.sc, P, phase);
+void launch_decide(const StateView& src, const PipeMem& m, const IsvdParams& P, cudaStream_t s) {
+  static size_t cfg = 0;
+  const size_t smem = decide_smem(m);
+  set_smem_attr(k_decide, smem, &cfg);
+  ProfScope ps(P_STEP_A, s);
+  k_decide<<<1, kDecideThreads, smem, s>>>(src, m.pp, P);
   STROM_LAUNCH_CHECK();
 }
 
-void launch_resid(int ccap, double* U, const double* x, const StateView& v, const ScratchMem& m,
-                  const IsvdParams& P, cudaStream_t s, int phase = 0) {
-  switch (maxj_for(ccap)) {
-    case 2: launch_resid_t<2>(U, x, v, m, P, s, phase); break;
-    case 4: launch_resid_t<4>(U, x, v, m, P, s, phase); break;
-    case 8: launch_resid_t<8>(U, x, v, m, P, s, phase); break;
-    case 16: launch_resid_t<16>(U, x, v, m, P, s, phase); break;
-    default: launch_resid_t<32>(U, x, v, m, P, s, phase); break;
-  }
+void launch_decide2(const StateView& src, const PipeMem& m, const IsvdParams& P, cudaStream_t s) {
+  static size_t cfg = 0;
+  const size_t smem = decide_smem(m);
+  set_smem_attr(k_decide2, smem, &cfg);
+  ProfScope ps(P_STEP_A, s);
+  k_decide2<<<1, kDecideThreads, smem, s>>>(src, m.pp, P);
+  STROM_LAUNCH_CHECK();
 }
 
 size_t small_kernel_smem(const Caps& c, int* use_smem) {
-  // step B layout: 3 m^2 + 16 ms (secular work) + ccap m (staged W_b / QR's M)
+  // step B layout: 3 m^2 + 16 ms (secular work) + ccap m (staged N_b / QR's M)
   const size_t m = c.rcap + 1;
   const size_t ms = round_up(std::max<int64_t>(c.ccap, c.rcap + 2), 32);
   const size_t need = (3 * m * m + 16 * ms + (size_t)c.ccap * m) * 8;
@@ -318,31 +454,33 @@ size_t small_kernel_smem(const Caps& c, int* use_smem) {
   return *use_smem ? need : 0;
 }
 
-void launch_step_b(const StateView& src, const StateView& dst, const ScratchMem& m, const IsvdParams& P,
+void launch_step_b(const StateView& src, const StateView& dst, const PipeMem& m, const IsvdParams& P,
                    const Caps& caps, cudaStream_t s) {
   int use_smem = 0;
   const size_t smem = small_kernel_smem(caps, &use_smem);
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    STROM_CUDA(cudaFuncSetAttribute(k_step_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = smem;
-  }
+  static size_t cfg = 0;
+  set_smem_attr(k_step_b, smem, &cfg);
   ProfScope ps(P_STEP_B, s);
-  k_step_b<<<1, kSmallThreads, smem, s>>>(src, dst, m.sc, P, use_smem);
+  k_step_b<<<1, kSmallThreads, smem, s>>>(src, dst, m.pp, P, use_smem);
   STROM_LAUNCH_CHECK();
 }
 
-void launch_compact_prep(const StateView& src, const StateView& dst, const ScratchMem& m, const IsvdParams& P,
+void launch_vupdate(const StateView& src, const StateView& dst, const PipeMem& m, const IsvdParams& P, int rcap,
+                    cudaStream_t s) {
+  dim3 grid((unsigned)ceil_div(P.k_new, kVRows), (unsigned)ceil_div(rcap + 1, kVCols));
+  ProfScope ps(P_VUPDATE, s);
+  k_vupdate<<<grid, kVRows, (size_t)(rcap + 2) * kVCols * 8, s>>>(src, dst, m.pp, P);
+  STROM_LAUNCH_CHECK();
+}
+
+void launch_compact_prep(const StateView& src, const StateView& dst, const PipeMem& m, const IsvdParams& P,
                          const Caps& caps, cudaStream_t s) {
   int use_smem = 0;
   const size_t smem = small_kernel_smem(caps, &use_smem);
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    STROM_CUDA(cudaFuncSetAttribute(k_compact_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = smem;
-  }
+  static size_t cfg = 0;
+  set_smem_attr(k_compact_prep, smem, &cfg);
   ProfScope ps(P_COMPACT, s);
-  k_compact_prep<<<1, kSmallThreads, smem, s>>>(src, dst, m.sc, P, use_smem);
+  k_compact_prep<<<1, kSmallThreads, smem, s>>>(src, dst, m.pp, P, use_smem);
   STROM_LAUNCH_CHECK();
 }
 
@@ -390,36 +528,36 @@ void gram_cholesky(const double* A, int64_t lda, const int32_t* col0_dev, const 
   STROM_LAUNCH_CHECK();
 }
 
-// Compaction into fresh buffers (also used to grow capacities):
-// U_new = U[:, base:base+c] L^{-T} Q_c,  W_new = R_c,  L_new = I.
+// Compaction into a fresh store (also used to grow capacities):
+// U_new = U[:, base:base+c] L^{-T} Q_c, N_new = L_new^T R_c, L_new measured.
 strom_isvd* compact(strom_isvd* src, const Caps& caps, cudaStream_t s) {
   strom_isvd* t = new_like(src, caps);
+  std::unique_ptr<strom_isvd> guard(t);
   alloc_small(t, s);
   t->vmem = src->vmem;  // V is immutable: share it
   t->view.V = src->view.V;
   t->view.ldv = src->view.ldv;
   t->caps.kcap = src->caps.kcap;
-  t->U = alloc_u(src->ldu, caps.ccap, s);
-  ScratchMem m = make_scratch(src->ldu, caps.ccap >= src->caps.ccap ? caps : src->caps, s);
-  IsvdParams P = make_params(src, m, src->k, false);
-  P.ccap = std::max(caps.ccap, src->caps.ccap);
-  P.work_stride = m.work_stride;
+  set_store(t, alloc_store(src->n, src->ldu, caps.ccap, s));
   Caps kc = caps;
   kc.ccap = std::max(caps.ccap, src->caps.ccap);
   kc.rcap = std::max(caps.rcap, src->caps.rcap);
+  PipeMem m = make_pipe(kc, s);
+  IsvdParams P = make_params(src, m, src->k, false);
+  P.ccap = kc.ccap;
   launch_compact_prep(src->view, t->view, m, P, kc, s);
-  // p = source c (step->m), q = r (step->mkeep)
-  launch_tall_gemm(src->U->ptr(), src->ldu, &src->view.hdr->base, m.sc.T, P.ccap, &m.sc.step->m,
-                   &m.sc.step->mkeep, t->U->ptr(), t->ldu, false, t->n, t->ldu, s);
+  // p = source c (step->m), q = r (step->mkeep); source columns start at base
+  launch_tall_gemm(src->store->U(), src->ldu, &src->view.hdr->base, m.pp.T, P.ccap, &m.pp.step[0]->m,
+                   &m.pp.step[0]->mkeep, t->store->U(), t->ldu, false, t->n, t->ldu, s);
   // measure the Gram of the stored U_new: L describes the memory, not an assumed identity
-  gram_cholesky(t->U->ptr(), t->ldu, nullptr, &m.sc.step->mkeep, 0, caps.rcap, t->n, t->view.L, t->view.Li,
-                t->view.ldl, t->view.hdr, reinterpret_cast<int*>(&m.sc.step->pad_status), s);
-  k_compact_finish<<<1, 256, 0, s>>>(t->view, m.sc.T, P.ccap);
+  gram_cholesky(t->store->U(), t->ldu, nullptr, &m.pp.step[0]->mkeep, 0, caps.rcap, t->n, t->view.L, t->view.Li,
+                t->view.ldl, t->view.hdr, &m.pp.step[0]->pad0, s);
+  k_compact_finish<<<1, 256, 0, s>>>(t->view, m.pp.T, P.ccap);
   STROM_LAUNCH_CHECK();
   t->r_ub = std::min(src->r_ub, caps.rcap);
   t->c_ub = t->r_ub;
-  t->U->claimed = t->c_ub;
-  return t;
+  t->store->claimed = t->c_ub;
+  return guard.release();
 }
 
 void read_hdr(const strom_isvd* h, cudaStream_t s, IsvdHdr* out) {
@@ -427,12 +565,10 @@ void read_hdr(const strom_isvd* h, cudaStream_t s, IsvdHdr* out) {
   STROM_CUDA(cudaStreamSynchronize(s));
 }
 
-// One functional update cur -> new state (all device-side decisions).
-strom_isvd* update_once(strom_isvd* src, const double* x, ScratchMem* scratch, cudaStream_t s,
-                        std::shared_ptr<strom_isvd>* keep) {
-  strom_isvd* cur = src;
-  std::unique_ptr<strom_isvd> tmp;
-  // rank capacity (uncapped streams grow; capped streams are sized by r_max)
+// Capacity management before an update of `cur` (host side; synchronises only
+// when a bound says it might be needed).  Returns the state to update from
+// (cur itself, or a compacted copy owned by *hold).
+strom_isvd* ensure_capacity(strom_isvd* cur, std::unique_ptr<strom_isvd>* hold, cudaStream_t s) {
   if (cur->r_max < 0 && cur->r_ub + 1 > cur->caps.rcap && cur->caps.rcap < cur->n) {
     IsvdHdr hh;
     read_hdr(cur, s, &hh);
@@ -441,61 +577,254 @@ strom_isvd* update_once(strom_isvd* src, const double* x, ScratchMem* scratch, c
     if (hh.r + 1 > cur->caps.rcap) {
       Caps nc = make_caps(cur->n, -1, std::min<int64_t>(cur->n, 2 * (int64_t)cur->caps.rcap), cur->k);
       nc.kcap = cur->caps.kcap;
-      tmp.reset(compact(cur, nc, s));
-      cur = tmp.get();
-      *scratch = ScratchMem();
+      hold->reset(compact(cur, nc, s));
+      cur = hold->get();
     }
   }
-  // physical column capacity: host-scheduled compaction
   if (cur->c_ub + 1 > cur->caps.ccap) {
-    strom_isvd* t = compact(cur, cur->caps, s);
-    tmp.reset(t);
-    cur = t;
+    IsvdHdr hh;
+    read_hdr(cur, s, &hh);  // refine the bound: dependent updates did not append
+    cur->c_ub = hh.base + hh.c;
+    cur->r_ub = hh.r;
+    if (cur->c_ub + 1 > cur->caps.ccap) {
+      hold->reset(compact(cur, cur->caps, s));
+      cur = hold->get();
+    }
   }
-  if (!scratch->mem || scratch->pstride != (int)round_up(cur->caps.ccap + 2, 8)) {
-    *scratch = make_scratch(cur->ldu, cur->caps, s);
-  }
+  return cur;
+}
+
+// The store a successor of `cur` may append to (shared, or a private copy).
+std::shared_ptr<Store> successor_store(const strom_isvd* cur, cudaStream_t s) {
+  if (cur->store->claimed != cur->c_ub) return clone_store(*cur->store, cur->n, cur->c_ub, s);
+  return cur->store;
+}
+
+// One functional update cur -> new state (all device-side decisions), on one stream.
+strom_isvd* update_once(strom_isvd* src, const double* x, cudaStream_t s, bool init_call = false) {
+  std::unique_ptr<strom_isvd> hold;
+  strom_isvd* cur = ensure_capacity(src, &hold, s);
   Caps nc = cur->caps;
   if (cur->k + 1 > nc.kcap) nc.kcap = round_up((cur->k + 1) * 2, 64);
   strom_isvd* dst = new_like(cur, nc);
+  std::unique_ptr<strom_isvd> dguard(dst);
   dst->k = cur->k + 1;
   alloc_small(dst, s);
   alloc_v(dst, s);
-  // append-only store: share unless another state already claimed beyond cur
-  if (cur->U->claimed != cur->c_ub) {
-    auto u = alloc_u(cur->ldu, cur->caps.ccap, s);
-    STROM_CUDA(cudaMemcpyAsync(u->ptr(), cur->U->ptr(), (size_t)cur->ldu * cur->c_ub * 8,
-                               cudaMemcpyDeviceToDevice, s));
-    dst->U = u;
-  } else {
-    dst->U = cur->U;
-  }
-  IsvdParams P = make_params(cur, *scratch, dst->k, false);
-  launch_proj(P.ccap, dst->U->ptr(), x, cur->view, *scratch, P, s);
-  {
-    ProfScope ps(P_STEP_A, s);
-    k_step_a<<<1, 256, 0, s>>>(cur->view, scratch->sc, P);
-    STROM_LAUNCH_CHECK();
-  }
-  launch_resid(P.ccap, dst->U->ptr(), x, cur->view, *scratch, P, s, 0);
-  {
-    ProfScope ps(P_STEP_B, s);
-    k_step_b1<<<1, 256, 0, s>>>(cur->view, scratch->sc, P);
-    STROM_LAUNCH_CHECK();
-  }
-  launch_resid(P.ccap, dst->U->ptr(), nullptr, cur->view, *scratch, P, s, 1);
-  launch_step_b(cur->view, dst->view, *scratch, P, cur->caps, s);
-  {
-    dim3 grid((unsigned)ceil_div(dst->k, kVRows), (unsigned)ceil_div(cur->caps.rcap + 1, kVCols));
-    ProfScope ps(P_VUPDATE, s);
-    k_vupdate<<<grid, kVRows, (size_t)(cur->caps.rcap + 2) * kVCols * 8, s>>>(cur->view, dst->view, scratch->sc, P);
-    STROM_LAUNCH_CHECK();
-  }
+  set_store(dst, successor_store(cur, s));
+  PipeMem m = make_pipe(cur->caps, s);
+  IsvdParams P = make_params(dst, m, dst->k, init_call);
+  const int cols = cur->c_ub;
+  k_init_ctl<<<1, 1, 0, s>>>(m.pp.ctl, cur->view.hdr);
+  STROM_LAUNCH_CHECK();
+  launch_pass(PASS_PROJ, cols, dst, m, nullptr, x, 0, s);
+  trace_point("proj", s);
+  launch_prep(m, P, s);
+  trace_point("prep", s);
+  launch_pass(PASS_FUSED, cols, dst, m, x, nullptr, 0, s);
+  trace_point("fused", s);
+  launch_decide(cur->view, m, P, s);
+  trace_point("decide", s);
+  launch_pass(PASS_SECOND, cols, dst, m, x, nullptr, 0, s);
+  trace_point("second", s);
+  launch_decide2(cur->view, m, P, s);
+  trace_point("decide2", s);
+  launch_step_b(cur->view, dst->view, m, P, cur->caps, s);
+  trace_point("step_b", s);
+  launch_vupdate(cur->view, dst->view, m, P, cur->caps.rcap, s);
+  trace_point("vupdate", s);
   dst->c_ub = cur->c_ub + 1;
-  dst->U->claimed = std::max(dst->U->claimed, dst->c_ub);
+  dst->store->claimed = std::max(dst->store->claimed, dst->c_ub);
   dst->r_ub = std::min(cur->r_ub + 1, cur->caps.rcap);
-  (void)keep;
-  return dst;
+  return dguard.release();
+}
+
+// ------------------------------------------------------------------ ingestion
+// Columns of an ingest call: device pointers, or host columns staged through a
+// ring of device chunks on a copy stream.
+struct ColumnSource {
+  const double* X = nullptr;
+  int64_t ldx = 0, n = 0, ncols = 0;
+  bool host = false;
+  cudaStream_t s = nullptr, cs = nullptr;
+  static constexpr int64_t kChunk = 16;
+  static constexpr int kRing = 3;
+  std::vector<DevMemPtr> ring;
+  std::vector<cudaEvent_t> ready, freed;
+  int64_t issued = 0, waited = -1;
+
+  void open(const double* X_, int64_t ldx_, int64_t n_, int64_t ncols_, bool host_, cudaStream_t s_) {
+    X = X_; ldx = ldx_; n = n_; ncols = ncols_; host = host_; s = s_;
+    if (!host) return;
+    STROM_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    ring.resize(kRing);
+    ready.resize(kRing);
+    freed.resize(kRing);
+    for (int i = 0; i < kRing; ++i) {
+      ring[i] = dev_alloc((size_t)n * kChunk * 8, s, false);
+      STROM_CUDA(cudaEventCreateWithFlags(&ready[i], cudaEventDisableTiming));
+      STROM_CUDA(cudaEventCreateWithFlags(&freed[i], cudaEventDisableTiming));
+      STROM_CUDA(cudaEventRecord(freed[i], s));
+    }
+    const int64_t nchunks = ceil_div(ncols, kChunk);
+    while (issued < std::min<int64_t>(kRing, nchunks)) issue(issued++);
+  }
+  void issue(int64_t q) {
+    const int slot = (int)(q % kRing);
+    const int64_t c0 = q * kChunk, cn = std::min(kChunk, ncols - c0);
+    STROM_CUDA(cudaStreamWaitEvent(cs, freed[slot], 0));
+    STROM_CUDA(cudaMemcpy2DAsync(ring[slot]->ptr, n * 8, X + c0 * ldx, ldx * 8, n * 8, cn, cudaMemcpyHostToDevice,
+                                 cs));
+    STROM_CUDA(cudaEventRecord(ready[slot], cs));
+  }
+  // device pointer of column t; the compute stream waits for its chunk once
+  const double* col(int64_t t) {
+    if (t < 0 || t >= ncols) return nullptr;
+    if (!host) return X + t * ldx;
+    const int64_t q = t / kChunk;
+    if (q > waited) {
+      for (int64_t w = waited + 1; w <= q; ++w) STROM_CUDA(cudaStreamWaitEvent(s, ready[w % kRing], 0));
+      waited = q;
+    }
+    return ring[q % kRing]->as<double>() + (t - q * kChunk) * n;
+  }
+  // every kernel reading columns <= t has been queued on s
+  void release(int64_t t) {
+    if (!host) return;
+    if ((t + 1) % kChunk != 0 && t + 1 != ncols) return;
+    const int64_t q = t / kChunk;
+    STROM_CUDA(cudaEventRecord(freed[q % kRing], s));
+    const int64_t nchunks = ceil_div(ncols, kChunk);
+    if (issued < nchunks && issued <= q + kRing) issue(issued++);
+  }
+  void close() {
+    if (!host) return;
+    STROM_CUDA(cudaStreamSynchronize(cs));
+    for (int i = 0; i < kRing; ++i) {
+      cudaEventDestroy(ready[i]);
+      cudaEventDestroy(freed[i]);
+    }
+    cudaStreamDestroy(cs);
+    cs = nullptr;
+  }
+};
+
+// Pipelined ingestion of ncols snapshots (basis.py:187-194): stream s carries
+// the passes and the decisions, stream s2 the core step and V update of update
+// t while s already runs the pass of update t+1.
+strom_isvd* ingest_pipelined(strom_isvd* src, ColumnSource& cols, cudaStream_t s) {
+  const int64_t ncols = cols.ncols;
+  static const int dbg = [] {
+    const char* e = getenv("STROM_PIPE_DEBUG");
+    return e ? atoi(e) : 0;
+  }();
+  cudaStream_t s2;
+  STROM_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+  cudaStream_t s2_created = s2;
+  if (dbg & 1) s2 = s;  // diagnostics: one stream
+  cudaEvent_t evD, evB, evV;
+  STROM_CUDA(cudaEventCreateWithFlags(&evD, cudaEventDisableTiming));
+  STROM_CUDA(cudaEventCreateWithFlags(&evB, cudaEventDisableTiming));
+  STROM_CUDA(cudaEventCreateWithFlags(&evV, cudaEventDisableTiming));
+  // s2 starts after everything queued on s so far
+  STROM_CUDA(cudaEventRecord(evV, s));
+  STROM_CUDA(cudaStreamWaitEvent(s2, evV, 0));
+  std::unique_ptr<strom_isvd> slot[2];
+  std::unique_ptr<strom_isvd> hold;  // a compacted state
+  strom_isvd* prev = src;
+  const int64_t kfinal = src->k + ncols;
+  PipeMem m;
+  bool need_prep = true;
+  auto join = [&]() {  // s waits for all of s2
+    STROM_CUDA(cudaEventRecord(evV, s2));
+    STROM_CUDA(cudaStreamWaitEvent(s, evV, 0));
+  };
+  for (int64_t t = 0; t < ncols; ++t) {
+    // ---- capacity (host bounds; synchronises only when a bound is hit)
+    {
+      const bool rank_hit = prev->r_max < 0 && prev->r_ub + 1 > prev->caps.rcap && prev->caps.rcap < prev->n;
+      const bool col_hit = prev->c_ub + 1 > prev->caps.ccap;
+      if (rank_hit || col_hit) {
+        join();
+        std::unique_ptr<strom_isvd> h2;
+        strom_isvd* nx = ensure_capacity(prev, &h2, s);
+        if (nx != prev) {
+          hold = std::move(h2);
+          prev = nx;
+          need_prep = true;
+        }
+        STROM_CUDA(cudaEventRecord(evB, s));  // s2 may not run ahead of the compaction
+        STROM_CUDA(cudaStreamWaitEvent(s2, evB, 0));
+      }
+    }
+    if (t == 0) {
+      if (prev->store->claimed != prev->c_ub) {
+        // copy-on-write once for the whole sequence: intermediate states are private
+        std::shared_ptr<Store> st = successor_store(prev, s);
+        auto* cp = new strom_isvd(*prev);
+        set_store(cp, st);
+        hold.reset(cp);
+        prev = cp;
+      }
+    }
+    // ---- destination state of update t (ping-pong blocks, V sized for the whole call)
+    std::unique_ptr<strom_isvd>& dslot = slot[t & 1];
+    if (!dslot || dslot->caps.rcap != prev->caps.rcap || dslot->caps.ccap != prev->caps.ccap) {
+      Caps nc = prev->caps;
+      nc.kcap = std::max<int64_t>(prev->caps.kcap, round_up(kfinal, 64));
+      if (dslot) join();  // the old block may still be read by s2
+      dslot.reset(new_like(prev, nc));
+      alloc_small(dslot.get(), s);
+      alloc_v(dslot.get(), s);
+    }
+    strom_isvd* dst = dslot.get();
+    dst->k = prev->k + 1;
+    set_store(dst, prev->store);
+    if (!m.mem || m.ccap != prev->caps.ccap || m.rcap != prev->caps.rcap) {
+      join();
+      m = make_pipe(prev->caps, s);
+      need_prep = true;
+    }
+    IsvdParams P = make_params(dst, m, dst->k, false);
+    P.parity = (int)(t & 1);
+    P.has_next = (t + 1 < ncols && !(dbg & 2)) ? 1 : 0;
+    if (dbg & 2) need_prep = true;  // diagnostics: re-project every snapshot
+    const int cols_ub = prev->c_ub;
+    const double* xt = cols.col(t);
+    const double* xn = cols.col(t + 1);
+    if (need_prep) {
+      if (t > 0) STROM_CUDA(cudaStreamWaitEvent(s, evB, 0));  // prev's header comes from s2
+      k_init_ctl<<<1, 1, 0, s>>>(m.pp.ctl, prev->view.hdr);
+      STROM_LAUNCH_CHECK();
+      launch_pass(PASS_PROJ, cols_ub, dst, m, nullptr, xt, 0, s);
+      launch_prep(m, P, s);
+      need_prep = false;
+    }
+    launch_pass(PASS_FUSED, cols_ub, dst, m, xt, (dbg & 2) ? nullptr : xn, 1, s);
+    if (t > 0) STROM_CUDA(cudaStreamWaitEvent(s, evB, 0));  // D(t) reads the state B(t-1) wrote
+    launch_decide(prev->view, m, P, s);
+    launch_pass(PASS_SECOND, cols_ub, dst, m, xt, xn, 1, s);
+    launch_decide2(prev->view, m, P, s);
+    cols.release(t);
+    STROM_CUDA(cudaEventRecord(evD, s));
+    STROM_CUDA(cudaStreamWaitEvent(s2, evD, 0));
+    launch_step_b(prev->view, dst->view, m, P, prev->caps, s2);
+    STROM_CUDA(cudaEventRecord(evB, s2));
+    launch_vupdate(prev->view, dst->view, m, P, prev->caps.rcap, s2);
+    dst->c_ub = prev->c_ub + 1;
+    dst->store->claimed = std::max(dst->store->claimed, dst->c_ub);
+    dst->r_ub = std::min(prev->r_ub + 1, prev->caps.rcap);
+    prev = dst;
+  }
+  join();
+  // the result owns its block; the other ping-pong block dies here (stream-ordered free)
+  strom_isvd* out = slot[(ncols - 1) & 1].release();
+  STROM_CUDA(cudaStreamSynchronize(s2));
+  cudaEventDestroy(evD);
+  cudaEventDestroy(evB);
+  cudaEventDestroy(evV);
+  cudaStreamDestroy(s2_created);
+  return out;
 }
 
 strom_isvd* init_state(int64_t n, const double* x, int64_t k, double tol_svd, double tol_sv, int64_t r_max,
@@ -503,39 +832,23 @@ strom_isvd* init_state(int64_t n, const double* x, int64_t k, double tol_svd, do
   STROM_REQUIRE(n >= 1, "need n >= 1");
   STROM_REQUIRE(k >= 1, "need k >= 1");
   STROM_REQUIRE(cap_mode == 0 || cap_mode == 1, "unknown cap_mode");
-  auto* h = new strom_isvd();
-  h->n = n;
-  h->ldu = round_up(n, kGemmRows);
-  h->k = k;
-  h->tol_svd = tol_svd;
-  h->tol_sv = tol_sv;
-  h->r_max = (int32_t)r_max;
-  h->cap_mode = cap_mode;
-  h->caps = make_caps(n, h->r_max, 1, k);
-  alloc_small(h, s);
-  alloc_v(h, s);
-  h->U = alloc_u(h->ldu, h->caps.ccap, s);
-  ScratchMem m = make_scratch(h->ldu, h->caps, s);
-  // fresh header: r = c = base = 0 (zeroed allocation) -> the restart path
-  IsvdParams P = make_params(h, m, k, true);
-  // run the update machinery from an empty source state into h itself
-  auto src_small = dev_alloc(256, s, true);
-  StateView sv = h->view;
-  sv.hdr = src_small->as<IsvdHdr>();
-  launch_proj(P.ccap, h->U->ptr(), x, sv, m, P, s);
-  k_step_a<<<1, 256, 0, s>>>(sv, m.sc, P);
-  STROM_LAUNCH_CHECK();
-  launch_resid(P.ccap, h->U->ptr(), x, sv, m, P, s);
-  launch_step_b(sv, h->view, m, P, h->caps, s);
-  {
-    dim3 grid((unsigned)ceil_div(k, kVRows), 1);
-    k_vupdate<<<grid, kVRows, (size_t)(h->caps.rcap + 2) * kVCols * 8, s>>>(sv, h->view, m.sc, P);
-    STROM_LAUNCH_CHECK();
-  }
-  h->c_ub = 1;
-  h->U->claimed = 1;
-  h->r_ub = 1;
-  return h;
+  // an empty state (r = c = base = 0) at column k - 1; the update machinery's
+  // restart branch then implements isvd_init (basis.py:65-102)
+  strom_isvd e;
+  e.n = n;
+  e.ldu = round_up(n, kGemmRows);
+  e.k = k - 1;
+  e.tol_svd = tol_svd;
+  e.tol_sv = tol_sv;
+  e.r_max = (int32_t)r_max;
+  e.cap_mode = cap_mode;
+  e.caps = make_caps(n, e.r_max, 1, k);
+  alloc_small(&e, s);
+  alloc_v(&e, s);
+  set_store(&e, alloc_store(n, e.ldu, e.caps.ccap, s));
+  e.c_ub = 0;
+  e.r_ub = 0;
+  return update_once(&e, x, s, true);
 }
 
 }  // namespace
@@ -553,9 +866,8 @@ int strom_isvd_init(int64_t n, const double* x_dev, int64_t k, double tol_svd, d
 
 int strom_isvd_update(strom_isvd* src, const double* x_dev, void* stream, strom_isvd** out) {
   return guarded([&] {
-    STROM_REQUIRE(src && out && x_dev, "null argument");
-    ScratchMem m;
-    *out = update_once(src, x_dev, &m, as_stream(stream), nullptr);
+    STROM_REQUIRE(src && x_dev && out, "null argument");
+    *out = update_once(src, x_dev, as_stream(stream));
   });
 }
 
@@ -565,65 +877,21 @@ int strom_isvd_ingest(strom_isvd* src, const double* X, int64_t ldx, int64_t nco
     STROM_REQUIRE(src && out, "null argument");
     STROM_REQUIRE(ncols >= 0 && ldx >= src->n, "bad ingest shape");
     cudaStream_t s = as_stream(stream);
-    ScratchMem m;
-    std::unique_ptr<strom_isvd> cur;
-    strom_isvd* c0 = src;
     if (ncols == 0) {
-      // a copy of the state (new handle sharing immutable buffers)
-      auto* h = new strom_isvd(*src);
-      *out = h;
+      *out = new strom_isvd(*src);  // a copy of the state (new handle sharing immutable buffers)
       return;
     }
-    if (!x_on_host) {
-      for (int64_t t = 0; t < ncols; ++t) {
-        strom_isvd* nx = update_once(cur ? cur.get() : c0, X + t * ldx, &m, s, nullptr);
-        cur.reset(nx);
-      }
-      *out = cur.release();
-      return;
+    ColumnSource cols;
+    cols.open(X, ldx, src->n, ncols, x_on_host != 0, s);
+    strom_isvd* res = nullptr;
+    try {
+      res = ingest_pipelined(src, cols, s);
+    } catch (...) {
+      cols.close();
+      throw;
     }
-    // host columns: chunked H2D on a copy stream, overlapped with the updates
-    const int64_t chunk = 16;
-    const int nring = 3;
-    const int64_t n = src->n;
-    cudaStream_t cs;
-    STROM_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-    std::vector<DevMemPtr> ring(nring);
-    std::vector<cudaEvent_t> ready(nring), freed(nring);
-    for (int i = 0; i < nring; ++i) {
-      ring[i] = dev_alloc((size_t)n * chunk * 8, s, false);
-      STROM_CUDA(cudaEventCreateWithFlags(&ready[i], cudaEventDisableTiming));
-      STROM_CUDA(cudaEventCreateWithFlags(&freed[i], cudaEventDisableTiming));
-      STROM_CUDA(cudaEventRecord(freed[i], s));
-    }
-    const int64_t nchunks = ceil_div(ncols, chunk);
-    auto issue = [&](int64_t q) {
-      const int slot = (int)(q % nring);
-      const int64_t c0i = q * chunk, cn = std::min(chunk, ncols - c0i);
-      STROM_CUDA(cudaStreamWaitEvent(cs, freed[slot], 0));
-      STROM_CUDA(cudaMemcpy2DAsync(ring[slot]->ptr, n * 8, X + c0i * ldx, ldx * 8, n * 8, cn,
-                                   cudaMemcpyHostToDevice, cs));
-      STROM_CUDA(cudaEventRecord(ready[slot], cs));
-    };
-    for (int64_t q = 0; q < std::min<int64_t>(nring, nchunks); ++q) issue(q);
-    for (int64_t q = 0; q < nchunks; ++q) {
-      const int slot = (int)(q % nring);
-      STROM_CUDA(cudaStreamWaitEvent(s, ready[slot], 0));
-      const int64_t c0i = q * chunk, cn = std::min(chunk, ncols - c0i);
-      for (int64_t t = 0; t < cn; ++t) {
-        strom_isvd* nx = update_once(cur ? cur.get() : c0, ring[slot]->as<double>() + t * n, &m, s, nullptr);
-        cur.reset(nx);
-      }
-      STROM_CUDA(cudaEventRecord(freed[slot], s));
-      if (q + nring < nchunks) issue(q + nring);
-    }
-    STROM_CUDA(cudaStreamSynchronize(cs));
-    for (int i = 0; i < nring; ++i) {
-      cudaEventDestroy(ready[i]);
-      cudaEventDestroy(freed[i]);
-    }
-    cudaStreamDestroy(cs);
-    *out = cur.release();
+    cols.close();
+    *out = res;
   });
 }
 
@@ -667,7 +935,7 @@ int strom_isvd_export(strom_isvd* h, double* phi_dev, double* sigma_dev, double*
       k_n_to_w<<<(unsigned)std::max<int64_t>(1, ceil_div((int64_t)hh.c * r, 256)), 256, 0, s>>>(h->view,
                                                                                               wtmp->as<double>());
       STROM_LAUNCH_CHECK();
-      launch_tall_gemm(h->U->ptr(), h->ldu, &h->view.hdr->base, wtmp->as<double>(), hh.c, &h->view.hdr->c,
+      launch_tall_gemm(h->store->U(), h->ldu, &h->view.hdr->base, wtmp->as<double>(), hh.c, &h->view.hdr->c,
                        &h->view.hdr->r, phi_dev, r, true, h->n, h->ldu, s);
     }
     if (sigma_dev && r > 0)
@@ -703,9 +971,9 @@ int strom_isvd_load_factored(int64_t n, int64_t k, int64_t c, int64_t r, const d
     STROM_REQUIRE(c + 1 <= h->caps.ccap, "too many factored columns for this capacity");
     alloc_small(h, s);
     alloc_v(h, s);
-    h->U = alloc_u(h->ldu, h->caps.ccap, s);
+    set_store(h, alloc_store(n, h->ldu, h->caps.ccap, s));
     if (c > 0) {
-      STROM_CUDA(cudaMemcpy2DAsync(h->U->ptr(), h->ldu * 8, u_dev, ldu * 8, n * 8, c, cudaMemcpyDeviceToDevice, s));
+      STROM_CUDA(cudaMemcpy2DAsync(h->store->U(), h->ldu * 8, u_dev, ldu * 8, n * 8, c, cudaMemcpyDeviceToDevice, s));
     }
     const int th = 256;
     if (c > 0 && r > 0) {
@@ -730,7 +998,7 @@ int strom_isvd_load_factored(int64_t n, int64_t k, int64_t c, int64_t r, const d
       } else {
         // measure the Gram of the stored U (exact L even for a nearly orthonormal U)
         auto st = dev_alloc(sizeof(int), s, true);
-        gram_cholesky(h->U->ptr(), h->ldu, nullptr, nullptr, (int)c, (int)c, n, h->view.L, h->view.Li,
+        gram_cholesky(h->store->U(), h->ldu, nullptr, nullptr, (int)c, (int)c, n, h->view.L, h->view.Li,
                       h->view.ldl, nullptr, st->as<int>(), s);
         int bad = 0;
         STROM_CUDA(cudaMemcpyAsync(&bad, st->ptr, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -744,7 +1012,7 @@ int strom_isvd_load_factored(int64_t n, int64_t k, int64_t c, int64_t r, const d
       STROM_LAUNCH_CHECK();
     }
     h->c_ub = (int32_t)c;
-    h->U->claimed = (int32_t)c;
+    h->store->claimed = (int32_t)c;
     h->r_ub = (int32_t)r;
     *out = guard.release();
   });
@@ -788,14 +1056,15 @@ int strom_isvd_factors(strom_isvd* h, double* u_dev, double* w_dev, double* l_de
     IsvdHdr hh;
     read_hdr(h, s, &hh);
     if (u_dev && hh.c > 0)
-      STROM_CUDA(cudaMemcpy2DAsync(u_dev, h->n * 8, h->U->ptr() + (int64_t)hh.base * h->ldu, h->ldu * 8, h->n * 8,
+      STROM_CUDA(cudaMemcpy2DAsync(u_dev, h->n * 8, h->store->U() + (int64_t)hh.base * h->ldu, h->ldu * 8, h->n * 8,
                                    hh.c, cudaMemcpyDeviceToDevice, s));
     if (w_dev && hh.c > 0 && hh.r > 0) {
       k_n_to_w<<<(unsigned)ceil_div((int64_t)hh.c * hh.r, 256), 256, 0, s>>>(h->view, w_dev);
       STROM_LAUNCH_CHECK();
     }
     if (l_dev && hh.c > 0)
-      STROM_CUDA(cudaMemcpy2DAsync(l_dev, hh.c * 8, h->view.L, h->view.ldl * 8, hh.c * 8, hh.c,
+      STROM_CUDA(cudaMemcpy2DAsync(l_dev, hh.c * 8, h->view.L + (int64_t)hh.base * (h->view.ldl + 1),
+                                   h->view.ldl * 8, hh.c * 8, hh.c,
                                    cudaMemcpyDeviceToDevice, s));
     STROM_CUDA(cudaStreamSynchronize(s));
   });

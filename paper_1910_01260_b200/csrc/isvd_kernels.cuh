@@ -1,20 +1,25 @@
 // Device kernels of the streaming incremental SVD (reference basis.py:105-184).
 //
-// Representation: the reference keeps the
-// n x r left basis Phi explicitly and rewrites it every snapshot
-// (Phi' = [Phi j] W_bar, basis.py:155-156).  Here Phi = Q_U N with
-//   U    n x c_cap  append-only column store in HBM (column-major, ld = ldu),
-//                   columns nearly orthogonal; G = U^T U = L L^T tracked exactly
+// Representation: the reference keeps the n x r left
+// basis Phi explicitly and rewrites it every snapshot (Phi' = [Phi j] W_bar,
+// basis.py:155-156).  Here Phi = Q_U N with
+//   U    n x c_cap  append-only column store in HBM (column-major, ld = ldu)
+//   G  = U^T U = L L^T, L and L^{-1} kept exactly, indexed by PHYSICAL column
+//        (the live block of a state starts at (base, base)); append-only like U
 //   Q_U  = U L^{-T} (never formed): an orthonormal basis of span(U)
-//   N    c x r      Phi's coordinates in Q_U (small, read by one CTA); Phi^T Phi = N^T N
-// (U-coordinates, needed by the passes and the export, are W = L^{-T} N).
-// so one snapshot costs one projection pass (g = U^T x) and, when the column is
-// independent, one residual pass that appends r1 = x - U G^{-1} g and measures
-// e = U^T r1, |r1|^2.  Everything else -- the bordered core SVD, the W and V
-// rotations, truncation, drift test, re-orthogonalisation -- is small-space
-// work on one CTA.  The reference's tall QR (basis.py:174) becomes a QR of the
-// (c x r) matrix L^T W; its Q is the same unique positive-diagonal Q.
+//   N    c x r      Phi's coordinates in Q_U (small); Phi^T Phi = N^T N.
+//
+// One snapshot x_t costs ONE pass over U (k_pass, kind FUSED): it forms the
+// residual r1 = x_t - U G^{-1} U^T x_t into the next free column, measures
+// e = U^T r1 and |r1|^2 for the exact Gram extension, and -- reading the same
+// U tile -- the projection U^T x_{t+1} of the NEXT snapshot.  The decision
+// chain (k_decide, optional re-orthogonalisation pass + k_decide2) is a few
+// microseconds of one-CTA work; the bordered core SVD, N rotation, truncation
+// and drift QR (k_step_b) and the V update run on a second stream, overlapped
+// with the next snapshot's pass.
 #pragma once
+
+#include <cuda.h>
 
 #include "common.cuh"
 #include "core_svd.cuh"
@@ -44,42 +49,62 @@ enum : int32_t {
 
 enum : int32_t { M_NORMAL_DEP = 0, M_NORMAL_INDEP = 1, M_RESTART_ACCEPT = 2, M_REJECT = 3, M_ERROR = 4 };
 
-// -------- transient per-update scalars (scratch) ---------------------------
+// -------- pipeline control (device) ----------------------------------------
+// The columns (c, base) of the most recently DECIDED state: the passes read
+// them, so the host never needs to know the device-side decisions.
+struct PipeCtl {
+  int32_t c, base;
+  int32_t reorth;  // 0 none, 1 DGKS pass requested, 2 restart copy requested
+  int32_t pad;
+  double xx;       // x.x of the snapshot about to be decided
+};
+
+// One update's decisions (double-buffered by update parity: k_step_b of update
+// t reads record t%2 while the decision kernels of t+1 write the other one).
 struct IsvdStep {
-  int32_t mode, write_slot, c_dot, restart;
-  int32_t m, mkeep, append, reorth;
-  double xx, rho2, p, norm;
-  int32_t pad_status, pad2;
-  double p_sq;
+  int32_t mode, restart, action, dep;  // action: 0 none (dependent), 1 append, 2 fold
+  int32_t c, cn, base_new, slot;       // U columns before / after, new base, write slot
+  int32_t m, mkeep, pad0, pad1;        // set by k_step_b for k_vupdate
+  double xx, rho2, p, p_sq, norm, lam;
+};
+
+// Outputs of one pass: e (c), gn (c + 1: U^T x_next, [c] = r . x_next),
+// scal[0] = r.r, scal[1] = x_next.x_next, scal[2] = r.x_next
+struct PassOut {
+  double* e;
+  double* gn;
+  double* scal;
+};
+
+struct Pipe {
+  PipeCtl* ctl;
+  IsvdStep* step[2];
+  double* ell[2];  // r_cap + 2: Phi^T x
+  double* nj[2];   // c_cap + 1: the new N column (x - Phi ell)/p in Q_U coordinates
+  double* tvec;    // L^{-1} g: x's coordinates in Q_U
+  double* gt;      // G^{-1} g = L^{-T} tvec
+  double* y;       // tvec - N ell
+  double* l1;      // L^{-1} e of the first residual
+  double* h;       // DGKS coefficients G^{-1} e, later l2
+  double* tmp;     // c_cap scratch
+  PassOut fo;      // the fused pass
+  PassOut ro;      // the second (re-orthogonalisation / restart) pass
+  double* vbar;    // (r_cap+2)^2 sorted, sign-fixed V_bar of the core
+  double* work;    // global fallback workspace of the one-CTA kernels
+  double* T;       // c_cap x (r_cap+1) compaction transform
+  double* part;    // per-CTA partial sums of the passes
+  unsigned* counter;
 };
 
 struct StateView {
   IsvdHdr* hdr;
   double* N;      // c_cap x (r_cap + 1), ld = ldn   (Phi = U L^{-T} N)
-  double* L;      // c_cap x c_cap lower, ld = ldl   (Cholesky factor of G = U^T U)
-  double* Li;     // c_cap x c_cap lower, ld = ldl   (L^{-1}, kept explicitly)
   double* sigma;  // r_cap + 1
   double* V;      // k_cap x (r_cap + 1), ld = ldv
+  double* L;      // store: c_cap x c_cap lower (physical columns), ld = ldl
+  double* Li;     // store: L^{-1}
   int32_t ldn, ldl;
   int64_t ldv;
-};
-
-struct Scratch {
-  double* g;      // c_cap   U^T x
-  double* gt;     // c_cap   G^{-1} g
-  double* y;      // c_cap   t - N ell  (t = L^{-1} g: x's coordinates in Q_U)
-  double* ell;    // r_cap+1 Phi^T x
-  double* e;      // c_cap   U^T r1
-  double* h;      // c_cap   G^{-1} e of the first residual (DGKS correction), else 0
-  double* lvec;   // c_cap   L^{-1} e
-  double* l1;     // c_cap   L^{-1} e of the first residual (kept across the DGKS pass)
-  double* tmp;    // c_cap   scratch vector
-  double* vbar;   // (r_cap+2)^2 sorted, sign-fixed V_bar of the core
-  double* work;   // large fallback workspace (global) for the one-CTA kernels
-  double* T;      // c_cap x (r_cap+1) compaction transform
-  double* part;   // per-CTA partial sums
-  unsigned* counter;
-  IsvdStep* step;
 };
 
 struct IsvdParams {
@@ -91,6 +116,10 @@ struct IsvdParams {
   int64_t k_new;     // column counter after this update
   int32_t pstride;   // stride of one CTA's partial row
   int32_t work_stride;
+  int32_t parity;    // which IsvdStep / ell / nj record this update uses
+  int32_t has_next;  // the fused pass also projected the next snapshot
+  double* L;         // store pointers (physical indexing), ld = ccap
+  double* Li;
   unsigned long long* prof;  // device byte counters (runtime.cuh ProfKind) or null
   long long* tprobe;         // phase timestamps of step B (diagnostics) or null
 };
@@ -100,9 +129,13 @@ struct IsvdParams {
     if ((P).tprobe && threadIdx.x == 0) (P).tprobe[k] = clock64(); \
   } while (0)
 
-constexpr int kTileRows = 64;
-constexpr int kPassThreads = 256;
+constexpr int kPassRows = 32;       // rows per pass tile (one per lane)
+constexpr int kPassConsumers = 8;                        // consumer warps of the pass
+constexpr int kPassThreads = 32 * (kPassConsumers + 1);  // + one TMA producer warp; one CTA per SM
+constexpr int kStageRows = 64;                           // rows per pipeline stage (2 per lane)
 constexpr int kSmallThreads = 512;  // one-CTA kernels: 128 registers per thread (no spills)
+constexpr int kDecideThreads = 512;
+constexpr int kTileRows = 64;       // legacy tile of the helpers below
 
 // Deterministic grid finish: the last CTA to arrive sums the per-CTA partials
 // in CTA order.  Returns true in that CTA (after the counter is reset).
@@ -123,319 +156,537 @@ __device__ inline bool last_cta_arrives(unsigned* counter, int* s_is_last) {
 }
 
 // ---------------------------------------------------------------------------
-// Projection pass: g = U[:, base:base+c]^T x and xx = x.x  (basis.py:135-136)
-// Warp w owns columns w, w+8, ...; lane l owns rows 2l, 2l+1 of each 64-row
-// tile (128-bit loads of U).  Contiguous tile ranges per CTA.
+// The pass over U (HBM-bound; one per snapshot).
+//   PROJ   : gn = U^T xn, scal[1] = xn.xn                           (first snapshot)
+//   FUSED  : r = x - U coef -> U[:, base + c]; e = U^T r; scal[0] = r.r;
+//            gn[0..c) = U^T xn, gn[c] = r.xn, scal[1] = xn.xn, scal[2] = r.xn
+//   SECOND : only if ctl->reorth: 1 = DGKS, r = r1 - U h in place; 2 = restart
+//            copy, r = x (no U columns read); e, scal[0], scal[2]
+// 32-row tiles, lane = row; warp w owns columns w + 8q.  U streams through a
+// multi-stage shared-memory ring filled by bulk async copies (mbarrier tx).  Row dots of r reduce
+// across warps through a double-buffered shared array (one barrier per tile);
+// column dots stay in registers until a deterministic last-CTA reduction.
+// Reference: basis.py:135-139 (projection, Pythagorean p) and 150-156 (j).
 // ---------------------------------------------------------------------------
-template <int MAXJ>
-__global__ void __launch_bounds__(kPassThreads) k_proj(const double* __restrict__ U,
-                                                        const double* __restrict__ x,
-                                                        StateView src, Scratch sc, IsvdParams P) {
-  __shared__ int s_last;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int c = src.hdr->c, base = src.hdr->base;
-  if (P.prof && blockIdx.x == 0 && threadIdx.x == 0)
-    atomicAdd(P.prof + 0, 8ull * (unsigned long long)P.n * (unsigned long long)(c + 1));  // U cols + x
-  const int64_t ntiles = P.ldu / kTileRows;
-  const int64_t per = ceil_div(ntiles, gridDim.x);
-  const int64_t t0 = blockIdx.x * per;
-  const int64_t t1 = min(ntiles, t0 + per);
-  double acc[MAXJ];
-#pragma unroll
-  for (int q = 0; q < MAXJ; ++q) acc[q] = 0.0;
-  double xx = 0.0;
-  for (int64_t t = t0; t < t1; ++t) {
-    const int64_t row = t * kTileRows + 2 * lane;
-    const double x0 = (row < P.n) ? __ldg(x + row) : 0.0;
-    const double x1 = (row + 1 < P.n) ? __ldg(x + row + 1) : 0.0;
-    if (wid == 0) xx = fma(x1, x1, fma(x0, x0, xx));
-#pragma unroll
-    for (int q = 0; q < MAXJ; ++q) {
-      const int j = wid + 8 * q;
-      if (j < c) {
-        const double2 u = __ldg(reinterpret_cast<const double2*>(U + (int64_t)(base + j) * P.ldu + row));
-        acc[q] = fma(u.y, x1, fma(u.x, x0, acc[q]));
-      }
-    }
-  }
-  double* mypart = sc.part + (int64_t)blockIdx.x * P.pstride;
-#pragma unroll
-  for (int q = 0; q < MAXJ; ++q) {
-    const int j = wid + 8 * q;
-    const double v = warp_sum(acc[q]);
-    if (lane == 0 && j < c) mypart[j] = v;
-  }
-  if (wid == 0) {
-    const double v = warp_sum(xx);
-    if (lane == 0) mypart[P.ccap] = v;
-  }
-  if (!last_cta_arrives(sc.counter, &s_last)) return;
-  // one warp per output, lanes stride over the CTA partials, fixed tree: deterministic
-  for (int j = wid; j <= c; j += 8) {
-    const int col = (j == c) ? P.ccap : j;
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    int b = lane;
-    for (; b + 96 < (int)gridDim.x; b += 128) {
-      s0 += sc.part[(int64_t)b * P.pstride + col];
-      s1 += sc.part[(int64_t)(b + 32) * P.pstride + col];
-      s2 += sc.part[(int64_t)(b + 64) * P.pstride + col];
-      s3 += sc.part[(int64_t)(b + 96) * P.pstride + col];
-    }
-    for (; b < (int)gridDim.x; b += 32) s0 += sc.part[(int64_t)b * P.pstride + col];
-    double s = warp_sum((s0 + s1) + (s2 + s3));
-    if (lane == 0) {
-      if (j == c) sc.step->xx = s;
-      else sc.g[j] = s;
-    }
-  }
+enum : int32_t { PASS_PROJ = 0, PASS_FUSED = 1, PASS_SECOND = 2 };
+
+struct PassArgs {
+  double* U;
+  int64_t ldu, n;
+  const PipeCtl* ctl;
+  int32_t kind;
+  int32_t pstride;
+  const double* x;
+  const double* coef;
+  const double* xn;
+  PassOut out;
+  double* part;
+  unsigned* counter;
+  unsigned long long* prof;
+};
+
+// -------- bulk-copy (TMA) + mbarrier primitives ---------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
 }
 
-// ---------------------------------------------------------------------------
-// Step A (one CTA): t = L^{-1} g, ell = N^T t (= Phi^T x), Pythagorean p,
-// dependent test, restart / reject branch (basis.py:112-139); y = t - N ell and
-// gt = G^{-1} g = L^{-T} t for the residual pass.
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_step_a(StateView src, Scratch sc, IsvdParams P) {
-  __shared__ double red[32];
-  __shared__ int s_mode;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const IsvdHdr h = *src.hdr;
-  IsvdStep* st = sc.step;
-  const double xx = st->xx;
-  if (threadIdx.x == 0) {
-    int mode;
-    st->restart = 0;
-    st->write_slot = -1;
-    st->c_dot = 0;
-    st->norm = sqrt(xx);
-    if (h.status != 0 || !isfinite(xx)) {
-      mode = M_ERROR;
+// 2D tensor TMA: box (kPassRows rows x kBoxCols columns) of U at (row, col)
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int row, int col, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(row), "r"(col), "r"(smem_u32(bar))
+      : "memory");
+}
+
+constexpr int kPassMaxStages = 8;
+constexpr int kBoxCols = 8;  // columns per TMA box (2 KB with 32 rows)
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// The pass: warp 0 streams U (kStageRows rows x c columns per stage, 2D TMA
+// boxes of kStageRows x 8) into a ring of shared-memory stages (full/empty
+// mbarriers); the kPassConsumers consumer warps process every stage together
+// -- warp w owns columns w + 8q, lane l rows 2l, 2l+1 -- and exchange row-dot
+// partials through a double-buffered shared array with ONE consumer-only named
+// barrier per stage.  Column dots stay in registers until a deterministic
+// last-CTA reduction.
+template <int MAXJ>
+__global__ void __launch_bounds__(kPassThreads, 1) k_pass(const __grid_constant__ CUtensorMap umap, PassArgs a,
+                                                         int nstages) {
+  extern __shared__ __align__(128) double stg[];  // nstages x (kStageRows x cs), column segments
+  __shared__ __align__(8) uint64_t full[kPassMaxStages];
+  __shared__ __align__(8) uint64_t empty[kPassMaxStages];
+  __shared__ double gts[kPassConsumers * MAXJ];
+  __shared__ __align__(16) double red[2][kPassConsumers][kStageRows];
+  __shared__ double wsc[3];
+  __shared__ int s_last;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int c = a.ctl->c;
+  const int base = a.ctl->base;
+  const int slot = base + c;
+  const double* x = a.x;
+  const double* coef = a.coef;
+  bool do_e = false, do_gn = false;
+  if (a.kind == PASS_SECOND) {
+    const int ro = a.ctl->reorth;
+    if (ro == 0) return;
+    if (ro == 1) {
+      x = a.U + (int64_t)slot * a.ldu;  // r2 = r1 - U h, in place
+      do_e = true;
     } else {
-      const bool at_cap = P.r_max >= 0 && h.r >= P.r_max;
-      if (h.r == 0 || (at_cap && P.cap_mode == 0)) {
-        st->restart = at_cap ? 1 : 0;
-        if (sqrt(xx) > P.tol_svd) {
-          mode = M_RESTART_ACCEPT;
-          st->write_slot = h.base + h.c;
-          st->c_dot = 0;
-        } else {
-          mode = M_REJECT;
-        }
-      } else {
-        mode = -1;  // decided below
-      }
+      coef = nullptr;  // slot <- x
+      c = 0;
     }
-    s_mode = mode;
+  } else if (a.kind == PASS_FUSED) {
+    do_e = true;
+    do_gn = a.xn != nullptr;
+  } else {
+    x = nullptr;
+    do_gn = true;
   }
-  __syncthreads();
-  if (s_mode != -1) {
-    if (threadIdx.x == 0) st->mode = s_mode;
-    return;
-  }
-  const int r = h.r, c = h.c;
-  double* t = sc.tmp;
-  cta_lower_mv(src.Li, src.ldl, c, sc.g, t);  // t = L^{-1} g
-  __syncthreads();
-  // ell_i = sum_j N[j, i] t[j]
-  for (int i = wid; i < r; i += nw) {
-    const double* ni = src.N + (int64_t)i * src.ldn;
-    double s = 0.0;
-    for (int j = lane; j < c; j += 32) s = fma(ni[j], t[j], s);
-    s = warp_sum(s);
-    if (lane == 0) sc.ell[i] = s;
-  }
-  __syncthreads();
-  double part = 0.0;
-  for (int i = threadIdx.x; i < r; i += blockDim.x) part = fma(sc.ell[i], sc.ell[i], part);
-  const double ll = block_sum(part, red);
-  const double p_sq = xx - ll;
-  const double p = (p_sq > 0.0) ? sqrt(p_sq) : 0.0;
-  const bool dep = (p < P.tol_svd) || (p == 0.0) || ((int64_t)r >= P.n);
-  if (threadIdx.x == 0) {
-    st->p = p;
-    st->p_sq = p_sq;
-    st->mode = dep ? M_NORMAL_DEP : M_NORMAL_INDEP;
-    if (!dep) {
-      st->write_slot = h.base + c;
-      st->c_dot = c;
-    }
-  }
-  if (!dep) {
-    // y = t - N ell: the in-span part of x - Phi ell in Q_U coordinates
-    for (int j = threadIdx.x; j < c; j += blockDim.x) {
-      double s = t[j];
-      for (int i = 0; i < r; ++i) s = fma(-src.N[(int64_t)i * src.ldn + j], sc.ell[i], s);
-      sc.y[j] = s;
-    }
-    cta_lower_t_mv(src.Li, src.ldl, c, t, sc.gt);  // gt = L^{-T} t = G^{-1} g
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Residual pass: r1 = x - U[:, base:base+c_dot] gt written to U[:, slot];
-// e = U[:, ...]^T r1 and rho2 = r1.r1.  Two phases per 64-row tile through
-// shared memory (row dots, then column dots against the fresh residual).
-// ---------------------------------------------------------------------------
-// phase 0: r1 = x - U gt (gt = G^{-1} U^T x);  phase 1 (DGKS re-orthogonalisation,
-// only when step B1 asked for it): r2 = r1 - U h in place on the slot column.
-template <int MAXJ>
-__global__ void __launch_bounds__(kPassThreads) k_resid(double* U, const double* xin,
-                                                         StateView src, Scratch sc, IsvdParams P, int phase) {
-  extern __shared__ double smem[];
-  __shared__ int s_last;
-  __shared__ double red[8];
-  const IsvdStep* st = sc.step;
-  const int mode = st->mode;
-  if (phase == 0 && mode != M_NORMAL_INDEP && mode != M_RESTART_ACCEPT) return;
-  if (phase == 1 && !(mode == M_NORMAL_INDEP && st->reorth)) return;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int cd = st->c_dot, slot = st->write_slot, base = src.hdr->base;
-  const double* x = (phase == 0) ? xin : U + (int64_t)slot * P.ldu;
-  const double* coef = (phase == 0) ? sc.gt : sc.h;
-  if (P.prof && blockIdx.x == 0 && threadIdx.x == 0)
-    atomicAdd(P.prof + 1, 8ull * (unsigned long long)P.n * (unsigned long long)(cd + 2));  // U, x; r1 out
-  double* tile = smem;                            // cd x 64 (column-major, 64 rows)
-  double* gts = tile + (int64_t)P.ccap * kTileRows;  // ccap (rounded to even: keeps rs 16B-aligned)
-  double* xs = gts + ((P.ccap + 1) & ~1);         // 64
-  double* rs = xs + kTileRows;                    // 64
-  double* pp = rs + kTileRows;                    // 4 x 64 partial row dots
-  for (int j = threadIdx.x; j < cd; j += blockDim.x) gts[j] = coef[j];
-  const int64_t ntiles = P.ldu / kTileRows;
+  const bool do_r = x != nullptr;
+  const bool do_coef = do_r && coef != nullptr && c > 0;
+  const bool do_xn = a.xn != nullptr;
+  if (a.prof && blockIdx.x == 0 && threadIdx.x == 0)
+    atomicAdd(a.prof + (a.kind == PASS_SECOND ? 1 : 0),
+              8ull * (unsigned long long)a.n * (unsigned long long)(c + (do_r ? 2 : 0) + (do_xn ? 1 : 0)));
+  for (int j = threadIdx.x; j < kPassConsumers * MAXJ; j += blockDim.x) gts[j] = (do_coef && j < c) ? coef[j] : 0.0;
+  const int64_t ntiles = a.ldu / kStageRows;
   const int64_t per = ceil_div(ntiles, gridDim.x);
   const int64_t t0 = blockIdx.x * per;
-  const int64_t t1 = min(ntiles, t0 + per);
-  double acc[MAXJ];
-#pragma unroll
-  for (int q = 0; q < MAXJ; ++q) acc[q] = 0.0;
-  double rr = 0.0;
-  for (int64_t t = t0; t < t1; ++t) {
-    const int64_t row0 = t * kTileRows;
-    __syncthreads();  // previous tile fully consumed
-#pragma unroll
-    for (int q = 0; q < MAXJ; ++q) {
-      const int j = wid + 8 * q;
-      if (j < cd) {
-        const double2 u = __ldg(reinterpret_cast<const double2*>(U + (int64_t)(base + j) * P.ldu + row0 + 2 * lane));
-        reinterpret_cast<double2*>(tile + (int64_t)j * kTileRows)[lane] = u;
+  const int64_t nt = max((int64_t)0, min(ntiles, t0 + per) - t0);
+  const int nbox = (c + kBoxCols - 1) / kBoxCols;
+  const int cs = nbox * kBoxCols;
+  const unsigned stage_elems = (unsigned)(kStageRows * cs);
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < nstages; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], kPassConsumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (wid == 0) {
+    // ---------------- producer ----------------
+    if (lane == 0 && cs > 0) {
+      for (int64_t i = 0; i < nt; ++i) {
+        const int st = (int)(i % nstages);
+        const int64_t use = i / nstages;
+        if (use > 0) mbar_wait(&empty[st], (unsigned)((use - 1) & 1));
+        mbar_expect_tx(&full[st], stage_elems * 8u);
+        double* dst = stg + (size_t)st * stage_elems;
+        const int row0 = (int)((t0 + i) * kStageRows);
+        for (int b = 0; b < nbox; ++b)
+          tma_load_2d(dst + b * kBoxCols * kStageRows, &umap, row0, base + b * kBoxCols, &full[st]);
       }
     }
-    if (threadIdx.x < kTileRows) {
-      const int64_t row = row0 + threadIdx.x;
-      xs[threadIdx.x] = (row < P.n) ? x[row] : 0.0;
+  } else {
+    // ---------------- consumers ----------------
+    const int cw = wid - 1;
+    double ae[MAXJ], ag[MAXJ];
+#pragma unroll
+    for (int q = 0; q < MAXJ; ++q) { ae[q] = 0.0; ag[q] = 0.0; }
+    double rr = 0.0, gs = 0.0, xq = 0.0;
+    double* scol = a.U + (int64_t)slot * a.ldu;
+    for (int64_t i = 0; i < nt; ++i) {
+      const int64_t row = (t0 + i) * kStageRows + 2 * lane;
+      const bool live0 = row < a.n, live1 = row + 1 < a.n;
+      double2 xv = make_double2(0.0, 0.0), xnv = make_double2(0.0, 0.0);
+      if (do_r) {
+        xv.x = live0 ? x[row] : 0.0;
+        xv.y = live1 ? x[row + 1] : 0.0;
+      }
+      if (do_xn) {
+        xnv.x = live0 ? __ldg(a.xn + row) : 0.0;
+        xnv.y = live1 ? __ldg(a.xn + row + 1) : 0.0;
+      }
+      const int st = (int)(i % nstages);
+      const int64_t use = i / nstages;
+      double2 u[MAXJ];
+      if (cs > 0) {
+        mbar_wait(&full[st], (unsigned)(use & 1));
+        const double* tile = stg + (size_t)st * stage_elems;
+#pragma unroll
+        for (int q = 0; q < MAXJ; ++q) {
+          const int j = cw + kPassConsumers * q;
+          u[q] = (j < c) ? reinterpret_cast<const double2*>(tile + j * kStageRows)[lane] : make_double2(0.0, 0.0);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);  // the stage is in registers
+      } else {
+#pragma unroll
+        for (int q = 0; q < MAXJ; ++q) u[q] = make_double2(0.0, 0.0);
+      }
+      double2 r = xv;
+      if (do_coef) {
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int q = 0; q < MAXJ; ++q) {
+          const double gq = gts[cw + kPassConsumers * q];
+          s0 = fma(u[q].x, gq, s0);
+          s1 = fma(u[q].y, gq, s1);
+        }
+        reinterpret_cast<double2*>(&red[i & 1][cw][0])[lane] = make_double2(s0, s1);
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kPassConsumers) : "memory");
+        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+        for (int w = 0; w < kPassConsumers; ++w) {
+          const double2 p = reinterpret_cast<const double2*>(&red[i & 1][w][0])[lane];
+          d0 += p.x;
+          d1 += p.y;
+        }
+        r.x = xv.x - d0;
+        r.y = xv.y - d1;
+      }
+      if (!live0) r.x = 0.0;
+      if (!live1) r.y = 0.0;
+      if (do_r) {
+        if (cw == kPassConsumers - 1) {
+          reinterpret_cast<double2*>(scol + (t0 + i) * kStageRows)[lane] = r;
+          rr = fma(r.y, r.y, fma(r.x, r.x, rr));
+          gs = fma(r.y, xnv.y, fma(r.x, xnv.x, gs));
+        }
+        if (do_e) {
+#pragma unroll
+          for (int q = 0; q < MAXJ; ++q) ae[q] = fma(u[q].y, r.y, fma(u[q].x, r.x, ae[q]));
+        }
+      }
+      if (do_gn) {
+#pragma unroll
+        for (int q = 0; q < MAXJ; ++q) ag[q] = fma(u[q].y, xnv.y, fma(u[q].x, xnv.x, ag[q]));
+        if (cw == kPassConsumers - 1) xq = fma(xnv.y, xnv.y, fma(xnv.x, xnv.x, xq));
+      }
     }
-    __syncthreads();
-    {
-      const int rrow = threadIdx.x & (kTileRows - 1), quarter = threadIdx.x >> 6;
-      double s = 0.0;
-      for (int j = quarter; j < cd; j += 4) s = fma(tile[(int64_t)j * kTileRows + rrow], gts[j], s);
-      pp[quarter * kTileRows + rrow] = s;
-    }
-    __syncthreads();
-    if (threadIdx.x < kTileRows) {
-      const int i = threadIdx.x;
-      const double dot = (pp[i] + pp[kTileRows + i]) + (pp[2 * kTileRows + i] + pp[3 * kTileRows + i]);
-      const double r1 = (row0 + i < P.n) ? xs[i] - dot : 0.0;
-      rs[i] = r1;
-      U[(int64_t)slot * P.ldu + row0 + i] = r1;
-      rr = fma(r1, r1, rr);
-    }
-    __syncthreads();
-    const double2 r2 = reinterpret_cast<const double2*>(rs)[lane];
+    // per-CTA partials: [0, PG) e | [PG, 2 PG) gn | 2 PG + {0: r.r, 1: xn.xn, 2: r.xn}
+    const int PG = (a.pstride - 8) / 2;
+    double* mypart = a.part + (int64_t)blockIdx.x * a.pstride;
 #pragma unroll
     for (int q = 0; q < MAXJ; ++q) {
-      const int j = wid + 8 * q;
-      if (j < cd) {
-        const double2 u = reinterpret_cast<const double2*>(tile + (int64_t)j * kTileRows)[lane];
-        acc[q] = fma(u.y, r2.y, fma(u.x, r2.x, acc[q]));
+      const int j = cw + kPassConsumers * q;
+      if (do_e) {
+        const double v = warp_sum(ae[q]);
+        if (lane == 0 && j < c) mypart[j] = v;
+      }
+      if (do_gn) {
+        const double v = warp_sum(ag[q]);
+        if (lane == 0 && j < c) mypart[PG + j] = v;
+      }
+    }
+    if (cw == kPassConsumers - 1) {
+      rr = warp_sum(rr);
+      gs = warp_sum(gs);
+      xq = warp_sum(xq);
+      if (lane == 0) {
+        mypart[2 * PG] = rr;
+        mypart[2 * PG + 1] = xq;
+        mypart[2 * PG + 2] = gs;
       }
     }
   }
-  double* mypart = sc.part + (int64_t)blockIdx.x * P.pstride;
-#pragma unroll
-  for (int q = 0; q < MAXJ; ++q) {
-    const int j = wid + 8 * q;
-    const double v = warp_sum(acc[q]);
-    if (lane == 0 && j < cd) mypart[j] = v;
-  }
-  const double rtot = block_sum(rr, red);
-  if (threadIdx.x == 0) mypart[P.ccap] = rtot;
-  if (!last_cta_arrives(sc.counter, &s_last)) return;
-  for (int j = wid; j <= cd; j += 8) {
-    const int col = (j == cd) ? P.ccap : j;
+  if (!last_cta_arrives(a.counter, &s_last)) return;
+  // one warp per output, lanes stride over the CTA partials, fixed tree: deterministic
+  const int PG = (a.pstride - 8) / 2;
+  const int nwarps = blockDim.x >> 5;
+  const int ne = do_e ? c : 0, ng = do_gn ? c : 0;
+  const int nout = ne + ng + 3;
+  for (int o = wid; o < nout; o += nwarps) {
+    int col;
+    if (o < ne) col = o;
+    else if (o < ne + ng) col = PG + (o - ne);
+    else col = 2 * PG + (o - ne - ng);
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
     int b = lane;
     for (; b + 96 < (int)gridDim.x; b += 128) {
-      s0 += sc.part[(int64_t)b * P.pstride + col];
-      s1 += sc.part[(int64_t)(b + 32) * P.pstride + col];
-      s2 += sc.part[(int64_t)(b + 64) * P.pstride + col];
-      s3 += sc.part[(int64_t)(b + 96) * P.pstride + col];
+      s0 += a.part[(int64_t)b * a.pstride + col];
+      s1 += a.part[(int64_t)(b + 32) * a.pstride + col];
+      s2 += a.part[(int64_t)(b + 64) * a.pstride + col];
+      s3 += a.part[(int64_t)(b + 96) * a.pstride + col];
     }
-    for (; b < (int)gridDim.x; b += 32) s0 += sc.part[(int64_t)b * P.pstride + col];
-    double s = warp_sum((s0 + s1) + (s2 + s3));
+    for (; b < (int)gridDim.x; b += 32) s0 += a.part[(int64_t)b * a.pstride + col];
+    const double sum = warp_sum((s0 + s1) + (s2 + s3));
     if (lane == 0) {
-      if (j == cd) sc.step->rho2 = s;
-      else sc.e[j] = s;
+      if (o < ne) a.out.e[o] = sum;
+      else if (o < ne + ng) a.out.gn[o - ne] = sum;
+      else {
+        const int k = o - ne - ng;
+        a.out.scal[k] = sum;
+        if (k == 2 && a.kind == PASS_FUSED && do_gn) a.out.gn[c] = sum;  // r . x_next
+      }
     }
   }
 }
 
 // ---------------------------------------------------------------------------
-// Step B (one CTA, 1024 threads): everything in small space.
-//   * extend the Cholesky factor of G with the appended column (or fold an
-//     in-span residual back into U's existing columns)
-//   * bordered core Q = [[diag(sigma), ell], [0, p]] (basis.py:141-144) and its
-//     SVD by one-sided Jacobi on Q^T (accumulated rotations give W_bar)
-//   * sort descending + sign rule (linalg.py:31-38, 53)
-//   * W' = [W w_j] W_bar  (basis.py:150-158), truncation (basis.py:160-168)
-//   * drift |phi_0 . phi_last| = |(L^T w_0) . (L^T w_last)|, and on drift the
-//     small-space QR replacing linalg.qr(phi) (basis.py:170-174)
+// Small-space helpers of the decision kernels
 // ---------------------------------------------------------------------------
+// Bordered extension of G's factors by the appended column (physical row c of
+// the block at (base, base)):  L' = [[L, 0], [l^T, lam]],
+// L'^{-1} = [[L^{-1}, 0], [-(L^{-T} l)^T / lam, 1 / lam]].
+__device__ inline void append_factor_row(double* Lb, double* Lib, int ldl, int c, const double* l, double lam,
+                                         double* tmpv) {
+  cta_gemv_t_cm(Lib, ldl, c, c, l, tmpv, true);  // tmpv = L^{-T} l
+  for (int j = threadIdx.x; j < c; j += blockDim.x) {
+    Lb[(int64_t)j * ldl + c] = l[j];
+    Lib[(int64_t)j * ldl + c] = -tmpv[j] / lam;
+  }
+  if (threadIdx.x == 0) {
+    Lb[(int64_t)c * ldl + c] = lam;
+    Lib[(int64_t)c * ldl + c] = 1.0 / lam;
+  }
+  __syncthreads();
+}
+
+// Coefficients of the next snapshot's residual: tvec = L^{-1} g, gt = L^{-T} tvec.
+__device__ inline void prep_next(const IsvdParams& P, const Pipe& pp, double* part) {
+  __syncthreads();  // ctl may have been written by thread 0 of this CTA
+  const int c = *(volatile const int32_t*)&pp.ctl->c, base = *(volatile const int32_t*)&pp.ctl->base;
+  const double* Lib = P.Li + (int64_t)base * (P.ccap + 1);
+  if (c > 0) {
+    cta_gemv_cm<8>(Lib, P.ccap, c, c, pp.fo.gn, 1.0, nullptr, pp.tvec, part, true);
+    cta_gemv_t_cm(Lib, P.ccap, c, c, pp.tvec, pp.gt, true);
+  }
+  if (threadIdx.x == 0) pp.ctl->xx = pp.fo.scal[1];
+}
+
+// A (first snapshot of a sequence, or after a compaction): prepare from a PROJ pass.
+__global__ void __launch_bounds__(kDecideThreads) k_prep(Pipe pp, IsvdParams P) {
+  extern __shared__ double part[];
+  prep_next(P, pp, part);
+}
+
+// ctl <- the columns of a state (start of a sequence / after a compaction)
+__global__ void k_init_ctl(PipeCtl* ctl, const IsvdHdr* h) {
+  ctl->c = h->c;
+  ctl->base = h->base;
+  ctl->reorth = 0;
+}
+
 constexpr double kFoldTau = 1e-3;  // append r1 only if its out-of-span part is >= tau |r1|
 
 // ---------------------------------------------------------------------------
-// Step B1 (one CTA): decide how the new direction enters U.  l = L^{-1} e,
-// lambda^2 = |r1|^2 - |l|^2 is the squared out-of-span part of r1 in the
-// G-metric.  Append r1 if lambda >= tau |r1|; otherwise (r1 is mostly
-// rounding noise inside span(U)) request one more classical Gram-Schmidt pass
-// (DGKS) when U does not yet span R^n.
+// D: every decision of update t (basis.py:112-139 and the U bookkeeping):
+//   restart / reject (basis.py:112-133), ell = Phi^T x = N^T L^{-1} g, the
+//   Pythagorean p (basis.py:136-138), the dependent test, and for an
+//   independent snapshot how r1 enters U: l = L^{-1} e, lambda^2 = |r1|^2 -
+//   |l|^2 (its out-of-span part in the G metric); append when lambda >= tau |r1|
+//   (extending L, L^{-1} in the store), else request one DGKS pass (k_decide2
+//   finishes).  Without a follow-up pass it also prepares the next snapshot.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_step_b1(StateView src, Scratch sc, IsvdParams P) {
+__global__ void __launch_bounds__(kDecideThreads) k_decide(StateView src, Pipe pp, IsvdParams P) {
+  extern __shared__ double part[];  // nw * c_cap
   __shared__ double red[32];
-  IsvdStep* st = sc.step;
-  const int wid = threadIdx.x >> 5;
-  const int c = src.hdr->c;
-  for (int j = threadIdx.x; j < c; j += blockDim.x) sc.h[j] = 0.0;
-  if (st->mode != M_NORMAL_INDEP) {
-    if (threadIdx.x == 0) { st->reorth = 0; st->append = 0; }
-    return;
+  const IsvdHdr h = *src.hdr;
+  IsvdStep* st = pp.step[P.parity];
+  double* ell = pp.ell[P.parity];
+  double* nj = pp.nj[P.parity];
+  const int c = h.c, base = h.base, r = h.r;
+  const int ldl = P.ccap;
+  double* Lb = P.L + (int64_t)base * (ldl + 1);
+  double* Lib = P.Li + (int64_t)base * (ldl + 1);
+  const double xx = pp.ctl->xx;
+  const double rho2 = pp.fo.scal[0];
+  const int slot = base + c;
+  int mode = -1, restart = 0, action = 0, dep = 0, cn = c, base_new = base, reorth = 0;
+  double p = 0.0, p_sq = 0.0, lam = 0.0;
+  if (h.status != 0 || !isfinite(xx)) {
+    mode = M_ERROR;
+  } else {
+    const bool at_cap = P.r_max >= 0 && h.r >= P.r_max;
+    if (r == 0 || (at_cap && P.cap_mode == 0)) {
+      restart = at_cap ? 1 : 0;
+      if (sqrt(xx) > P.tol_svd) {
+        mode = M_RESTART_ACCEPT;
+        if (c == 0) {  // the pass read no U columns: the slot already holds x
+          lam = sqrt(rho2);
+          cn = 1;
+          base_new = slot;
+        } else {
+          reorth = 2;  // copy x into the slot (second pass), k_decide2 finishes
+        }
+      } else {
+        mode = M_REJECT;
+        cn = 0;
+        base_new = base + c;
+      }
+    }
   }
-  cta_lower_mv(src.Li, src.ldl, c, sc.e, sc.lvec);
-  __syncthreads();
-  for (int j = threadIdx.x; j < c; j += blockDim.x) sc.l1[j] = sc.lvec[j];
-  double part = 0.0;
-  for (int j = threadIdx.x; j < c; j += blockDim.x) part = fma(sc.lvec[j], sc.lvec[j], part);
-  const double ll = block_sum(part, red);
-  const double rho2 = st->rho2;
-  const double lam2 = rho2 - ll;
-  const bool app = (lam2 > kFoldTau * kFoldTau * rho2) && (rho2 > 0.0);
-  const bool reorth = !app && ((int64_t)c < P.n) && (st->write_slot < P.ccap);
-  __syncthreads();
-  if (reorth) cta_lower_t_mv(src.Li, src.ldl, c, sc.lvec, sc.h);
+  if (mode == -1) {
+    cta_gemv_t_cm(src.N, src.ldn, c, r, pp.tvec, ell, false);  // ell = N^T tvec
+    double pl = 0.0;
+    for (int i = threadIdx.x; i < r; i += blockDim.x) pl = fma(ell[i], ell[i], pl);
+    const double ll = block_sum(pl, red);
+    p_sq = xx - ll;
+    p = (p_sq > 0.0) ? sqrt(p_sq) : 0.0;
+    dep = (p < P.tol_svd) || (p == 0.0) || ((int64_t)r >= P.n);
+    mode = dep ? M_NORMAL_DEP : M_NORMAL_INDEP;
+    if (!dep) {
+      cta_gemv_cm<8>(src.N, src.ldn, c, r, ell, -1.0, pp.tvec, pp.y, part, false);  // y = tvec - N ell
+      cta_gemv_cm<8>(Lib, ldl, c, c, pp.fo.e, 1.0, nullptr, pp.l1, part, true);      // l1 = L^{-1} e
+      double pq = 0.0;
+      for (int j = threadIdx.x; j < c; j += blockDim.x) pq = fma(pp.l1[j], pp.l1[j], pq);
+      const double ll1 = block_sum(pq, red);
+      const double lam2 = rho2 - ll1;
+      const bool room = (slot < P.ccap) && ((int64_t)c < P.n);
+      const bool app = room && (lam2 > kFoldTau * kFoldTau * rho2) && (rho2 > 0.0);
+      if (app) {
+        lam = sqrt(lam2);
+        append_factor_row(Lb, Lib, ldl, c, pp.l1, lam, pp.tmp);
+        for (int a = threadIdx.x; a <= c; a += blockDim.x) nj[a] = (a < c) ? (pp.y[a] + pp.l1[a]) / p : lam / p;
+        cn = c + 1;
+        action = 1;
+      } else if (room) {
+        reorth = 1;
+        cta_gemv_t_cm(Lib, ldl, c, c, pp.l1, pp.h, true);  // h = L^{-T} l1 = G^{-1} e
+      } else if (c >= r + 1) {
+        for (int a = threadIdx.x; a < c; a += blockDim.x) nj[a] = (pp.y[a] + pp.l1[a]) / p;
+        action = 2;
+      } else {
+        dep = 1;
+      }
+    }
+  }
+  if (mode == M_RESTART_ACCEPT && reorth == 0 && threadIdx.x == 0) {
+    P.L[(int64_t)slot * (ldl + 1)] = lam;
+    P.Li[(int64_t)slot * (ldl + 1)] = 1.0 / lam;
+  }
   if (threadIdx.x == 0) {
-    st->append = app ? 1 : 0;
-    st->reorth = reorth ? 1 : 0;
+    st->mode = mode;
+    st->restart = restart;
+    st->action = action;
+    st->dep = (mode == M_NORMAL_DEP) ? 1 : dep;
+    st->c = c;
+    st->cn = cn;
+    st->base_new = base_new;
+    st->slot = slot;
+    st->xx = xx;
+    st->rho2 = rho2;
+    st->p = p;
+    st->p_sq = p_sq;
+    st->norm = sqrt(xx);
+    st->lam = lam;
+    pp.ctl->reorth = reorth;
+    if (reorth == 0) {
+      pp.ctl->c = cn;
+      pp.ctl->base = base_new;
+    }
   }
+  if (reorth == 0 && P.has_next) prep_next(P, pp, part);
 }
 
-__global__ void __launch_bounds__(kSmallThreads) k_step_b(StateView src, StateView dst, Scratch sc, IsvdParams P,
-                                                 int use_smem) {
+// ---------------------------------------------------------------------------
+// D2: after the second pass.  DGKS: l2 = L^{-1} e2, lambda2^2 = |r2|^2 - |l2|^2;
+// append r2 whenever it carries a genuine out-of-span direction (the reference
+// appends j = (x - Phi ell)/p even when it is rounding noise, basis.py:155-156),
+// else fold it back (U keeps a spare direction) or demote the update to
+// dependent.  Restart copy: the new one-column state.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kDecideThreads) k_decide2(StateView src, Pipe pp, IsvdParams P) {
+  extern __shared__ double part[];
+  __shared__ double red[32];
+  const int ro = pp.ctl->reorth;
+  if (ro == 0) return;
+  IsvdStep* st = pp.step[P.parity];
+  double* nj = pp.nj[P.parity];
+  const int c = st->c, slot = st->slot, r = src.hdr->r, base = src.hdr->base;
+  const int ldl = P.ccap;
+  double* Lb = P.L + (int64_t)base * (ldl + 1);
+  double* Lib = P.Li + (int64_t)base * (ldl + 1);
+  __syncthreads();
+  int cn = c, action = 0, dep = 0, base_new = base;
+  double lam = 0.0;
+  if (ro == 1) {
+    const double p = st->p;
+    double* l2 = pp.h;  // h is spent
+    cta_gemv_cm<8>(Lib, ldl, c, c, pp.ro.e, 1.0, nullptr, l2, part, true);
+    double pq = 0.0;
+    for (int j = threadIdx.x; j < c; j += blockDim.x) pq = fma(l2[j], l2[j], pq);
+    const double ll2 = block_sum(pq, red);
+    const double rho2b = pp.ro.scal[0];
+    const double lam2 = rho2b - ll2;
+    if ((lam2 > 0.25 * rho2b) && (rho2b > 0.0)) {
+      lam = sqrt(lam2);
+      append_factor_row(Lb, Lib, ldl, c, l2, lam, pp.tmp);
+      for (int a = threadIdx.x; a <= c; a += blockDim.x)
+        nj[a] = (a < c) ? (pp.y[a] + pp.l1[a] + l2[a]) / p : lam / p;
+      if (threadIdx.x == 0) pp.fo.gn[c] = pp.ro.scal[2];  // r2 . x_next
+      cn = c + 1;
+      action = 1;
+    } else if (c >= r + 1) {
+      for (int a = threadIdx.x; a < c; a += blockDim.x) nj[a] = (pp.y[a] + pp.l1[a] + l2[a]) / p;
+      action = 2;
+    } else {
+      dep = 1;
+    }
+  } else {
+    lam = sqrt(pp.ro.scal[0]);
+    if (threadIdx.x == 0) {
+      P.L[(int64_t)slot * (ldl + 1)] = lam;
+      P.Li[(int64_t)slot * (ldl + 1)] = 1.0 / lam;
+      pp.fo.gn[0] = pp.ro.scal[2];  // x . x_next
+      st->rho2 = pp.ro.scal[0];
+    }
+    cn = 1;
+    base_new = slot;
+  }
+  if (threadIdx.x == 0) {
+    if (ro == 1) {
+      st->action = action;
+      st->dep = dep;
+    }
+    st->cn = cn;
+    st->base_new = base_new;
+    st->lam = lam;
+    pp.ctl->c = cn;
+    pp.ctl->base = base_new;
+    pp.ctl->reorth = 0;
+  }
+  if (P.has_next) prep_next(P, pp, part);
+}
+
+// ---------------------------------------------------------------------------
+// B (one CTA; second stream): everything of update t that the next snapshot's
+// pass does not depend on.
+//   * bordered core Q = [[diag(sigma), ell], [0, p]] (basis.py:141-144) and its
+//     SVD by the rank-one secular solver, sort + sign rule (linalg.py:31-38, 53)
+//   * N' = [N n_j] W_bar (basis.py:150-158 in Q_U coordinates), truncation
+//     (basis.py:160-168), drift |phi_0 . phi_last| = |N_0 . N_last| and the QR
+//     of basis.py:170-174 on N' (Q_U is orthonormal: QR(Phi') = Q_U QR(N'))
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kSmallThreads) k_step_b(StateView src, StateView dst, Pipe pp, IsvdParams P,
+                                                          int use_smem) {
   extern __shared__ double smem[];
   __shared__ double red[32];
-  __shared__ double s_misc[4];
-  __shared__ int s_int[8];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const IsvdHdr h = *src.hdr;
-  IsvdStep* st = sc.step;
+  IsvdStep* st = pp.step[P.parity];
+  const double* ell = pp.ell[P.parity];
+  const double* wj = pp.nj[P.parity];
   const int mode = st->mode;
   IsvdHdr o = h;
   o.flags = 0;
@@ -455,20 +706,16 @@ __global__ void __launch_bounds__(kSmallThreads) k_step_b(StateView src, StateVi
   if (mode == M_REJECT || mode == M_RESTART_ACCEPT) {
     if (threadIdx.x == 0) {
       if (st->restart) { o.n_restarts += 1; o.flags |= F_RESTART; }
+      o.c = st->cn;
+      o.base = st->base_new;
       if (mode == M_REJECT) {
         o.r = 0;
-        o.c = 0;
-        o.base = h.base + h.c;
         o.n_rejected += 1;
         o.flags |= F_REJECTED;
         st->mkeep = 0;
       } else {
         o.r = 1;
-        o.c = 1;
-        o.base = st->write_slot;
-        dst.L[0] = sqrt(st->rho2);
-        dst.Li[0] = 1.0 / dst.L[0];
-        dst.N[0] = dst.L[0] / st->norm;  // Phi = x / ||x|| = U W, W = 1/||x||, N = L W
+        dst.N[0] = st->lam / st->norm;  // Phi = x / ||x|| = Q_U N with Q_U = x / lam
         dst.sigma[0] = st->norm;
         st->mkeep = 1;
       }
@@ -478,90 +725,19 @@ __global__ void __launch_bounds__(kSmallThreads) k_step_b(StateView src, StateVi
     return;
   }
   STROM_TPROBE(P, 0);
-  bool dep = (mode == M_NORMAL_DEP);
-  const int r = h.r, c = h.c, m = r + 1;
+  const bool dep = st->dep != 0;
+  const int r = h.r, c = st->c, m = r + 1;
+  const int cn = st->cn;
+  const int action = st->action;
   const double p = st->p;
   o.p = p;
   o.p_sq = st->p_sq;
-  // ---- 1. how the new direction enters U (see k_step_b1) --------------------
-  //   append: U' = [U r], L' = [[L, 0], [l^T, lambda]]
-  //   fold:   r is (numerically) in span(U) and U has a spare direction
-  //   demote: r is in span(U) to working precision and U has none -> dependent
-  int cn = c;
-  int action = 0;  // 0 none (dependent), 1 append, 2 fold
-  double* lvec = sc.lvec;
-  if (!dep) {
-    if (st->reorth) {  // second pass done: recompute l, lambda from (e2, |r2|^2)
-      cta_lower_mv(src.Li, src.ldl, c, sc.e, lvec);
-      __syncthreads();
-    }
-    double part = 0.0;
-    for (int j = threadIdx.x; j < c; j += blockDim.x) part = fma(lvec[j], lvec[j], part);
-    const double ll = block_sum(part, red);
-    const double rho2 = st->rho2;
-    const double lam2 = rho2 - ll;
-    bool app;
-    // after the second pass r2 is kept whenever it carries a genuine out-of-span
-    // direction, however small: the reference appends j = (x - Phi ell)/p even
-    // when it is pure rounding noise (basis.py:155-156)
-    if (st->reorth) app = (lam2 > 0.25 * rho2) && (rho2 > 0.0);
-    else app = st->append != 0;
-    app = app && (st->write_slot < P.ccap) && ((int64_t)c < P.n);
-    if (threadIdx.x == 0) s_misc[0] = app ? sqrt(lam2) : 0.0;
-    if (app) action = 1;
-    else if (c >= r + 1) action = 2;
-    else { action = 0; dep = true; }
-    __syncthreads();
-    // append: u = L^{-T} l for the new row of L^{-1}
-    if (action == 1) cta_lower_t_mv(src.Li, src.ldl, c, lvec, sc.tmp);
-    __syncthreads();
-    if (action == 1) cn = c + 1;
-  }
   const bool appended = (action == 1);
-  // copy L and L^{-1} (lower) into dst, extended by the new row when appended
-  for (int j = wid; j < cn; j += nw) {
-    const double* ls = src.L + (int64_t)j * src.ldl;
-    const double* lis = src.Li + (int64_t)j * src.ldl;
-    double* ld_ = dst.L + (int64_t)j * dst.ldl;
-    double* lid = dst.Li + (int64_t)j * dst.ldl;
-    for (int i = lane; i < cn; i += 32) {
-      double v = 0.0, vi = 0.0;
-      if (i < c && j < c) {
-        if (i >= j) { v = ls[i]; vi = lis[i]; }
-      } else if (i == c && j < c) {
-        v = lvec[j];
-        vi = -sc.tmp[j] / s_misc[0];
-      } else if (i == c && j == c) {
-        v = s_misc[0];
-        vi = 1.0 / s_misc[0];
-      }
-      ld_[i] = v;
-      lid[i] = vi;
-    }
-  }
-  // new N column for j = (x - Phi ell)/p in Q_U coordinates (length cn):
-  //   x - Phi ell = Q_U (t - N ell + l_1 [+ l_2]) + lambda q   (q the appended direction)
-  // (the fold drops the rounding-level out-of-span part; l_2 only after the DGKS pass)
-  double* wj = sc.work + 3 * (int64_t)P.work_stride;
-  if (!dep) {
-    const bool two = st->reorth != 0;
-    for (int a = threadIdx.x; a < cn; a += blockDim.x) {
-      double v;
-      if (a < c) {
-        v = sc.y[a] + sc.l1[a];
-        if (two) v += lvec[a];
-        v /= p;
-      } else {
-        v = s_misc[0] / p;
-      }
-      wj[a] = v;
-    }
-  }
   STROM_TPROBE(P, 1);
   // ---- shared-memory plan (global fallback when it does not fit) ----------
   //   WS m^2 | Wt m^2 | Vt m^2 | core work 16 ms | WB ccap x m (staged N_b, later QR's M)
   const int64_t ms = P.work_stride;
-  double* base = use_smem ? smem : sc.work + 4 * ms;
+  double* base = use_smem ? smem : pp.work + 4 * ms;
   double* WS = base;                      // sorted, signed W_bar (m x m)
   double* Wt = WS + (int64_t)m * m;       // vectors by slot, later W^T W
   double* Vt = Wt + (int64_t)m * m;       // vectors by slot, later the polished W_bar
@@ -577,8 +753,6 @@ __global__ void __launch_bounds__(kSmallThreads) k_step_b(StateView src, StateVi
     cw.perm = ib + 5 * ms; cw.cnt = ib + 6 * ms;
   }
   // stage N_b: columns 0..r-1 = N (c rows; the appended row is 0), column r = n_j
-  __syncthreads();  // w_j complete
-  if (P.tprobe && threadIdx.x == 0) P.tprobe[7] = use_smem;
   for (int b = wid; b < m; b += nw) {
     const double* ns = src.N + (int64_t)b * src.ldn;
     double* wb = WB + b * P.ccap;
@@ -590,7 +764,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_step_b(StateView src, StateVi
     }
   }
   // ---- 2. the bordered core and its SVD (rank-one secular solver) ----------
-  core_svd_secular(src.sigma, sc.ell, dep ? 0.0 : p, r, cw, Wt, Vt, svs, WS, sc.vbar, red,
+  core_svd_secular(src.sigma, ell, dep ? 0.0 : p, r, cw, Wt, Vt, svs, WS, pp.vbar, red,
                    P.tprobe ? P.tprobe + 8 : nullptr, P.tprobe ? P.tprobe + 300 : nullptr);
   STROM_TPROBE(P, 2);
   // (no orthogonality polish needed: the Gu-Eisenstat vectors are orthogonal to
@@ -655,7 +829,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_step_b(StateView src, StateVi
         for (int k = wid; k < mk; k += nw)
           for (int a = lane; a < cn; a += 32) M[k * cn + a] = dst.N[(int64_t)k * dst.ldn + a];
         __syncthreads();
-        cta_householder_qr(M, cn, cn, mk, nullptr, 0, sc.work, sc.work + P.work_stride, red);
+        cta_householder_qr(M, cn, cn, mk, nullptr, 0, pp.work, pp.work + P.work_stride, red);
       }
       if (P.tprobe && threadIdx.x == 0) P.tprobe[6 + 1] = chol_ok ? 1 : 2;
       for (int k = wid; k < mk; k += nw)
@@ -671,7 +845,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_step_b(StateView src, StateVi
     o.n_dependent += dep ? 1 : 0;
     o.n_truncated += trunc ? 1 : 0;
     o.flags = (dep ? F_DEPENDENT : 0) | (trunc ? F_TRUNCATED : 0) | (did_qr ? F_QR : 0) |
-              (appended ? F_APPENDED : 0) | ((mode == M_NORMAL_INDEP && !appended) ? F_FOLDED : 0);
+              (appended ? F_APPENDED : 0) | ((mode == M_NORMAL_INDEP && action == 2) ? F_FOLDED : 0);
     *dst.hdr = o;
     st->m = m;
     st->mkeep = mk;
@@ -684,9 +858,9 @@ __global__ void __launch_bounds__(kSmallThreads) k_step_b(StateView src, StateVi
 // ---------------------------------------------------------------------------
 constexpr int kVCols = 16;
 constexpr int kVRows = 64;
-__global__ void __launch_bounds__(kVRows) k_vupdate(StateView src, StateView dst, Scratch sc, IsvdParams P) {
+__global__ void __launch_bounds__(kVRows) k_vupdate(StateView src, StateView dst, Pipe pp, IsvdParams P) {
   extern __shared__ double vbs[];  // (r+1) x kVCols slice of V_bar
-  const IsvdStep* st = sc.step;
+  const IsvdStep* st = pp.step[P.parity];
   const int mode = st->mode;
   const int64_t k = P.k_new;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -698,7 +872,7 @@ __global__ void __launch_bounds__(kVRows) k_vupdate(StateView src, StateView dst
   }
   const int m = st->m, mk = st->mkeep, r = m - 1;
   if (col0 >= mk) return;
-  const double* vb = sc.vbar;
+  const double* vb = pp.vbar;
   for (int idx = threadIdx.x; idx < m * kVCols; idx += blockDim.x) {
     const int b = idx % m, q = idx / m, col = col0 + q;
     vbs[q * m + b] = (col < mk) ? vb[(int64_t)col * m + b] : 0.0;
@@ -726,89 +900,80 @@ __global__ void __launch_bounds__(kVRows) k_vupdate(StateView src, StateView dst
 }
 
 // ---------------------------------------------------------------------------
-// Compaction prep (one CTA): L^T W = Q_c R_c;  T = L^{-T} Q_c;  new W = R_c,
-// new L = I, c = r, base = 0.  Phi = U W = (U T) R_c exactly.
+// Compaction prep (one CTA): N = Q_c R_c (Householder);  T = L^{-T} Q_c, so
+// U_new = U T has orthonormal columns in exact arithmetic and Phi = U_new R_c.
+// The new store's L is then MEASURED (Gram of the stored U_new) and
+// k_compact_finish sets N_new = L_new^T R_c.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kSmallThreads) k_compact_prep(StateView src, StateView dst, Scratch sc, IsvdParams P,
-                                                       int use_smem) {
+__global__ void __launch_bounds__(kSmallThreads) k_compact_prep(StateView src, StateView dst, Pipe pp, IsvdParams P,
+                                                                int use_smem) {
   extern __shared__ double smem[];
   __shared__ double red[32];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const IsvdHdr h = *src.hdr;
   const int r = h.r, c = h.c;
   IsvdHdr o = h;
+  IsvdStep* st = pp.step[0];
   if (h.status != 0 || r == 0) {
     if (threadIdx.x == 0) {
       if (h.status == 0) { o.c = 0; o.base = 0; }
       *dst.hdr = o;
-      sc.step->m = 0;
+      st->m = 0;
+      st->mkeep = 0;
     }
     return;
   }
-  // N = Q_c R_c; U_new = U L^{-T} Q_c (orthonormal), and with L_new = chol of
-  // the measured U_new Gram the new coordinates are N_new = L_new^T R_c
-  // (k_compact_finish, after the Gram); R_c waits in dst.N.
-  double* M = use_smem ? smem : sc.work + 4 * (int64_t)P.work_stride;  // c x r
-  for (int64_t idx = threadIdx.x; idx < (int64_t)c * r; idx += blockDim.x) {
-    const int i = idx % c, k = idx / c;
-    M[idx] = src.N[(int64_t)k * src.ldn + i];
-  }
+  double* M = use_smem ? smem : pp.work + 4 * (int64_t)P.work_stride;  // c x r
+  for (int k = threadIdx.x >> 5; k < r; k += blockDim.x >> 5)
+    for (int i = threadIdx.x & 31; i < c; i += 32) M[k * c + i] = src.N[(int64_t)k * src.ldn + i];
   __syncthreads();
-  cta_householder_qr(M, c, c, r, dst.N, dst.ldn, sc.work, sc.work + P.work_stride, red);
-  cta_gemm_dmma(c, r, c, src.Li, src.ldl, 1, M, 1, c,
-                [&](int a, int k, double v) { sc.T[(int64_t)k * P.ccap + a] = v; });
-  for (int64_t idx = threadIdx.x; idx < (int64_t)r * r; idx += blockDim.x) {
-    const int i = idx % r, j = idx / r;
-    dst.L[(int64_t)j * dst.ldl + i] = (i == j) ? 1.0 : 0.0;
-    dst.Li[(int64_t)j * dst.ldl + i] = (i == j) ? 1.0 : 0.0;
-  }
+  cta_householder_qr(M, c, c, r, dst.N, dst.ldn, pp.work, pp.work + P.work_stride, red);
+  const double* Lib = src.Li + (int64_t)h.base * (src.ldl + 1);
+  cta_gemm_dmma(c, r, c, Lib, src.ldl, 1, M, 1, c, [&](int a, int k, double v) { pp.T[(int64_t)k * P.ccap + a] = v; });
   for (int k = threadIdx.x; k < r; k += blockDim.x) dst.sigma[k] = src.sigma[k];
   if (threadIdx.x == 0) {
     o.c = r;
     o.base = 0;
     *dst.hdr = o;
-    sc.step->m = c;  // number of source columns for the GEMM
-    sc.step->mkeep = r;
+    st->m = c;  // number of source columns for the GEMM
+    st->mkeep = r;
   }
 }
 
-// After the compaction Gram: N_new = L_new^T R_c (R_c parked in dst.N).
+// After the compaction Gram: N_new = L_new^T R_c (R_c parked in dst.N; base 0).
 __global__ void __launch_bounds__(256) k_compact_finish(StateView dst, double* tmp, int ldt) {
   const int r = dst.hdr->r;
   if (dst.hdr->status != 0 || r == 0) return;
-  // upper-triangular (L_new^T) times upper-triangular R_c
-  for (int64_t idx = threadIdx.x; idx < (int64_t)r * r; idx += blockDim.x) {
-    const int i = idx % r, k = idx / r;
-    const double* lcol = dst.L + (int64_t)i * dst.ldl;  // column i of L = row i of L^T
-    double s = 0.0;
-    for (int j = i; j <= k; ++j) s = fma(lcol[j], dst.N[(int64_t)k * dst.ldn + j], s);
-    tmp[(int64_t)k * ldt + i] = s;
-  }
+  for (int k = 0; k < r; ++k)
+    for (int i = threadIdx.x; i <= k; i += blockDim.x) {
+      const double* lcol = dst.L + (int64_t)i * dst.ldl;  // column i of L = row i of L^T
+      double s = 0.0;
+      for (int j = i; j <= k; ++j) s = fma(lcol[j], dst.N[(int64_t)k * dst.ldn + j], s);
+      tmp[(int64_t)k * ldt + i] = s;
+    }
   __syncthreads();
-  for (int64_t idx = threadIdx.x; idx < (int64_t)r * r; idx += blockDim.x) {
-    const int i = idx % r, k = idx / r;
-    dst.N[(int64_t)k * dst.ldn + i] = tmp[(int64_t)k * ldt + i];
-  }
+  for (int k = 0; k < r; ++k)
+    for (int i = threadIdx.x; i < r; i += blockDim.x) dst.N[(int64_t)k * dst.ldn + i] = (i <= k) ? tmp[(int64_t)k * ldt + i] : 0.0;
 }
 
 // U-coordinates W = L^{-T} N (c x r, ld c) for the export / materialisation.
 __global__ void __launch_bounds__(256) k_n_to_w(StateView v, double* w) {
-  const int r = v.hdr->r, c = v.hdr->c;
+  const int r = v.hdr->r, c = v.hdr->c, base = v.hdr->base;
+  const double* Lib = v.Li + (int64_t)base * (v.ldl + 1);
   for (int64_t idx = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; idx < (int64_t)c * r;
        idx += (int64_t)blockDim.x * gridDim.x) {
-    const int a = idx % c, k = idx / c;
-    const double* lcol = v.Li + (int64_t)a * v.ldl;
+    const int a = (int)(idx % c), k = (int)(idx / c);
+    const double* lcol = Lib + (int64_t)a * v.ldl;
     double s = 0.0;
     for (int i = a; i < c; ++i) s = fma(lcol[i], v.N[(int64_t)k * v.ldn + i], s);
     w[(int64_t)k * c + a] = s;
   }
 }
 
-// N = L^T W for a state loaded in U-coordinates (W parked in dst.N).
+// N = L^T W for a state loaded in U-coordinates (W parked in v.N; base 0).
 __global__ void __launch_bounds__(256) k_w_to_n(StateView v, double* tmp) {
   const int r = v.hdr->r, c = v.hdr->c;
   for (int64_t idx = threadIdx.x; idx < (int64_t)c * r; idx += blockDim.x) {
-    const int i = idx % c, k = idx / c;
+    const int i = (int)(idx % c), k = (int)(idx / c);
     const double* lcol = v.L + (int64_t)i * v.ldl;
     double s = 0.0;
     for (int j = i; j < c; ++j) s = fma(lcol[j], v.N[(int64_t)k * v.ldn + j], s);
@@ -816,7 +981,7 @@ __global__ void __launch_bounds__(256) k_w_to_n(StateView v, double* tmp) {
   }
   __syncthreads();
   for (int64_t idx = threadIdx.x; idx < (int64_t)c * r; idx += blockDim.x) {
-    const int i = idx % c, k = idx / c;
+    const int i = (int)(idx % c), k = (int)(idx / c);
     v.N[(int64_t)k * v.ldn + i] = tmp[(int64_t)k * c + i];
   }
 }

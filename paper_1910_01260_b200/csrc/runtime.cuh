@@ -36,7 +36,16 @@ void set_last_error(const std::string& msg);
                                                     cudaGetErrorString(_e));              \
   } while (0)
 
-#define STROM_LAUNCH_CHECK() STROM_CUDA(cudaGetLastError())
+#define STROM_STR2(x) #x
+#define STROM_STR(x) STROM_STR2(x)
+#define STROM_LAUNCH_CHECK()                                                              \
+  do {                                                                                    \
+    cudaError_t _e = cudaGetLastError();                                                  \
+    if (_e != cudaSuccess)                                                                \
+      throw ::strom::Error(::strom::kCudaError, std::string("kernel launch at " __FILE__   \
+                                                            ":" STROM_STR(__LINE__) ": ") + \
+                                                    cudaGetErrorString(_e));              \
+  } while (0)
 
 #define STROM_REQUIRE(cond, msg)                                                          \
   do {                                                                                    \

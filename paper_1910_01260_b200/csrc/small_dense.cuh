@@ -431,6 +431,57 @@ __device__ inline double warp_cholesky(double* B, int ld, int n) {
 // Li lower-triangular, column-major (ld).  y must not alias x.  Block-wide;
 // the caller synchronises before using y.
 // ---------------------------------------------------------------------------
+// y[i] = (base ? base[i] : 0) + sgn * sum_j A(i, j) x[j] for i < rows, j < cols
+// (A column-major, ld; lower: only j <= i).  Warp w takes columns j = w mod nw,
+// lanes take rows (coalesced), and the per-warp partials are reduced in a fixed
+// order through `part` (nw * rows doubles of shared memory): deterministic, and
+// every load of A is independent (no serial dependence chain through memory).
+// rows <= 32 * K.  x must not alias y.  Ends with __syncthreads.
+template <int K>
+__device__ inline void cta_gemv_cm(const double* A, int ld, int rows, int cols, const double* x, double sgn,
+                                   const double* base, double* y, double* part, bool lower) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double acc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc[k] = 0.0;
+  for (int j = wid; j < cols; j += nw) {
+    const double xj = x[j];
+    const double* col = A + (int64_t)j * ld;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int i = lane + 32 * k;
+      if (i < rows && (!lower || i >= j)) acc[k] = fma(col[i], xj, acc[k]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int i = lane + 32 * k;
+    if (i < rows) part[wid * rows + i] = acc[k];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < rows; i += blockDim.x) {
+    double s = 0.0;
+    for (int w = 0; w < nw; ++w) s += part[w * rows + i];
+    y[i] = (base ? base[i] : 0.0) + sgn * s;
+  }
+  __syncthreads();
+}
+
+// y[j] = sum_i A(i, j) x[i] over i < rows (lower: i >= j), j < cols: one warp
+// per column, lanes over rows.  Ends with __syncthreads.
+__device__ inline void cta_gemv_t_cm(const double* A, int ld, int rows, int cols, const double* x, double* y,
+                                     bool lower) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int j = wid; j < cols; j += nw) {
+    const double* col = A + (int64_t)j * ld;
+    double s = 0.0;
+    for (int i = (lower ? j : 0) + lane; i < rows; i += 32) s = fma(col[i], x[i], s);
+    s = warp_sum(s);
+    if (lane == 0) y[j] = s;
+  }
+  __syncthreads();
+}
+
 __device__ inline void cta_lower_mv(const double* Li, int ld, int n, const double* x, double* y) {
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     double s = 0.0;
