@@ -136,6 +136,9 @@ int strom_isvd_load_factored(int64_t n, int64_t k, int64_t c, int64_t r, const d
  * Synchronizes.  Any output may be NULL. */
 int strom_isvd_factors(strom_isvd* h, double* u_dev, double* w_dev, double* l_dev, void* stream);
 
+/* Diagnostics: mean ms of `iters` fused passes over a synthetic n x c store. */
+int strom_debug_pass_bw(int64_t n, int32_t c, int32_t iters, int32_t reserve, double* ms_out);
+
 /* Diagnostics: step-B phase timestamps (clock64, 8 slots) into dev_buf; NULL disables. */
 void strom_debug_tprobe(long long* dev_buf);
 

@@ -1,4 +1,4 @@
-// Tall-skinny Gram G = A^T A (A: n x q column-major, q <= 128) on the fp64
+// Tall-skinny Gram G = A^T A (A: n x q, column-major or row-tiled, q <= 128) on the fp64
 // tensor cores (DMMA m8n8k4).  Used to measure the exact Gram of a freshly
 // compacted U (so the small-space Cholesky factor L describes the stored U,
 // not an assumed identity) and when loading a state from an explicit phi.
@@ -13,8 +13,7 @@ constexpr int kGramRows = 32;
 constexpr int kGramLd = kGramRows + 4;
 
 template <int TAW, int TBM>
-__global__ void __launch_bounds__(256) k_tall_gram(const double* __restrict__ A, int64_t lda,
-                                                   const int32_t* col0_dev, const int32_t* q_dev, int q_fixed,
+__global__ void __launch_bounds__(256) k_tall_gram(Tall A, const int32_t* col0_dev, const int32_t* q_dev, int q_fixed,
                                                    int64_t n, double* __restrict__ part, int QP) {
   extern __shared__ double gsm[];  // QP x kGramLd
   const int q = q_dev ? *q_dev : q_fixed;
@@ -36,7 +35,7 @@ __global__ void __launch_bounds__(256) k_tall_gram(const double* __restrict__ A,
     for (int idx = threadIdx.x; idx < kGramRows * T8 * 8; idx += blockDim.x) {
       const int i = idx % kGramRows, a = idx / kGramRows;
       const int64_t row = row0 + i;
-      gsm[a * kGramLd + i] = (row < n && a < q) ? __ldg(A + (int64_t)(col0 + a) * lda + row) : 0.0;
+      gsm[a * kGramLd + i] = (row < n && a < q) ? __ldg(A.p + A.off(row, col0 + a)) : 0.0;
     }
     __syncthreads();
 #pragma unroll

@@ -7,8 +7,6 @@
 #include <memory>
 #include <vector>
 
-#include <cudaTypedefs.h>
-
 #include "../../include/strom_b200.h"
 #include "gram.cuh"
 #include "isvd_kernels.cuh"
@@ -41,6 +39,14 @@ __global__ void k_copy_cm(const double* __restrict__ src, int64_t lds, int64_t r
   if (idx >= rows * cols) return;
   const int64_t i = idx % rows, j = idx / rows;
   dst[j * ldd + i] = src[j * lds + i];
+}
+
+// out(i, j) = in(i, j) for i < rows, j < cols (layout conversion between Tall views)
+__global__ void k_copy_tall(Tall in, int64_t rows, int64_t cols, Tall out) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= rows * cols) return;
+  const int64_t i = idx % rows, j = idx / rows;
+  out.p[out.off(i, j)] = in.p[in.off(i, j)];
 }
 
 __global__ void k_set_hdr(IsvdHdr* h, int32_t r, int32_t c, int32_t base, int32_t rej, int32_t dep, int32_t tr,
@@ -117,8 +123,9 @@ void trace_point(const char* what, cudaStream_t s) {
 long long* g_tprobe = nullptr;  // step-B phase timestamps (strom_debug_tprobe)
 
 // ------------------------------------------------------------------ state
-// The append-only store shared by a state and its successors: U (n x ccap,
-// column-major, ld ldu) and the exact factors L, L^{-1} of G = U^T U, indexed
+// The append-only store shared by a state and its successors: U (ldu x ccap,
+// row-tiled: kUTile-row tiles, each holding its ccap column segments
+// contiguously, so one pass stage is one contiguous bulk copy) and the exact factors L, L^{-1} of G = U^T U, indexed
 // by physical column.  `claimed` bounds the physical columns any live state
 // may have written: a successor that would append past a state whose c_ub is
 // below `claimed` copies the store first (copy-on-write).
@@ -127,7 +134,6 @@ struct Store {
   int64_t ldu = 0;
   int32_t ccap = 0;
   int32_t claimed = 0;
-  CUtensorMap umap{};  // 2D TMA descriptor of U (rows x ccap), box kStageRows x 8
   double* U() const { return umem->as<double>(); }
   double* L() const { return lmem->as<double>(); }
   double* Li() const { return L() + (size_t)ccap * ccap; }
@@ -170,39 +176,18 @@ Caps make_caps(int64_t n, int32_t r_max, int32_t want_r, int64_t k) {
   return c;
 }
 
-PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      p = nullptr;
-    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }();
-  if (!fn) throw Error(kCudaError, "cuTensorMapEncodeTiled is unavailable");
-  return fn;
-}
-
-void encode_umap(Store* st) {
-  cuuint64_t dims[2] = {(cuuint64_t)st->ldu, (cuuint64_t)st->ccap};
-  cuuint64_t strides[1] = {(cuuint64_t)st->ldu * 8};
-  cuuint32_t box[2] = {(cuuint32_t)kStageRows, (cuuint32_t)kBoxCols};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = tensor_map_encoder()(&st->umap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, st->umem->ptr, dims, strides, box,
-                                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) throw Error(kCudaError, "cuTensorMapEncodeTiled failed for the U store");
-}
-
 std::shared_ptr<Store> alloc_store(int64_t n, int64_t ldu, int32_t ccap, cudaStream_t s) {
   auto st = std::make_shared<Store>();
   st->umem = dev_alloc((size_t)ldu * ccap * 8, s, false);
-  if (ldu > n)  // padding rows are read by the passes: keep them zero (never NaN)
-    STROM_CUDA(cudaMemset2DAsync(st->umem->as<double>() + n, ldu * 8, 0, (ldu - n) * 8, ccap, s));
+  // tiles holding padding rows (>= n) are read by the passes: keep them zero (never NaN)
+  const int64_t first_pad_tile = n / kUTile;
+  const int64_t ntile = ldu / kUTile;
+  if (first_pad_tile < ntile)
+    STROM_CUDA(cudaMemsetAsync(st->umem->as<double>() + first_pad_tile * kUTile * ccap, 0,
+                               (size_t)(ntile - first_pad_tile) * kUTile * ccap * 8, s));
   st->lmem = dev_alloc((size_t)2 * ccap * ccap * 8, s, true);
   st->ldu = ldu;
   st->ccap = ccap;
-  encode_umap(st.get());
   return st;
 }
 
@@ -216,8 +201,9 @@ void set_store(strom_isvd* h, const std::shared_ptr<Store>& st) {
 // copy-on-write: a private store holding the first c_ub physical columns
 std::shared_ptr<Store> clone_store(const Store& src, int64_t n, int32_t c_ub, cudaStream_t s) {
   auto st = alloc_store(n, src.ldu, src.ccap, s);
-  if (c_ub > 0)
-    STROM_CUDA(cudaMemcpyAsync(st->U(), src.U(), (size_t)src.ldu * c_ub * 8, cudaMemcpyDeviceToDevice, s));
+  if (c_ub > 0)  // the first c_ub column segments of every tile
+    STROM_CUDA(cudaMemcpy2DAsync(st->U(), (size_t)kUTile * src.ccap * 8, src.U(), (size_t)kUTile * src.ccap * 8,
+                                 (size_t)kUTile * c_ub * 8, src.ldu / kUTile, cudaMemcpyDeviceToDevice, s));
   STROM_CUDA(cudaMemcpyAsync(st->L(), src.L(), (size_t)2 * src.ccap * src.ccap * 8, cudaMemcpyDeviceToDevice, s));
   st->claimed = c_ub;
   return st;
@@ -351,24 +337,31 @@ inline int pass_maxj(int cols) {
   return 32;
 }
 
-// pipeline depth: stages of kStageRows x cols within ~180 KB (2 .. kPassMaxStages)
+// pipeline depth: stages of kStageRows x cols within ~140 KB (2 .. kPassMaxStages)
+size_t pass_stage_budget() {
+  static size_t v = [] {
+    const char* e = getenv("STROM_STAGE_KB");
+    const int kb = e ? atoi(e) : 140;
+    return (size_t)std::max(16, std::min(200, kb)) * 1024;
+  }();
+  return v;
+}
 inline int pass_stages(int cols) {
-  const size_t per = (size_t)kStageRows * std::max(cols, 1) * 8;
-  return (int)std::max<size_t>(2, std::min<size_t>(kPassMaxStages, (180u * 1024u) / per));
+  const size_t per = (size_t)kStageRows * (std::max(cols, 1) + 2) * 8;
+  return (int)std::max<size_t>(2, std::min<size_t>(kPassMaxStages, pass_stage_budget() / per));
 }
 
 template <int MAXJ>
-void launch_pass_t(const CUtensorMap& umap, const PassArgs& a, int cols_ub, int reserve, int kind_prof,
-                   cudaStream_t s) {
-  const int cols = (int)round_up(std::max(cols_ub, 1), kBoxCols);
+void launch_pass_t(const PassArgs& a, int cols_ub, int reserve, int kind_prof, cudaStream_t s) {
+  const int cols = std::max(cols_ub, 1);
   const int nst = pass_stages(cols);
-  const size_t smem = (size_t)nst * kStageRows * cols * 8;
+  const size_t smem = (size_t)nst * kStageRows * (cols + 2) * 8;  // + x and x_next segments
   static size_t cfg = 0;
   set_smem_attr(k_pass<MAXJ>, smem, &cfg);
   const int64_t ntiles = a.ldu / kStageRows;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, std::max(1, sm_count() - reserve)));
   ProfScope ps(kind_prof, s);
-  k_pass<MAXJ><<<grid, kPassThreads, smem, s>>>(umap, a, nst);
+  k_pass<MAXJ><<<grid, kPassThreads, smem, s>>>(a, nst);
   {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
@@ -390,6 +383,19 @@ void launch_pass(int kind, int cols_ub, const strom_isvd* h, const PipeMem& m, c
   a.U = h->store->U();
   a.ldu = h->ldu;
   a.n = h->n;
+  a.ccap = h->store->ccap;
+  {
+    static const int dbg = [] {
+      const char* e = getenv("STROM_PASS_DBG");
+      return e ? atoi(e) : 0;
+    }();
+    a.dbg = dbg;
+  }
+  auto bulk_ok = [&](const double* v) {
+    return v && (reinterpret_cast<uintptr_t>(v) % 16 == 0) && (h->n % 2 == 0);
+  };
+  a.x_bulk = bulk_ok(x) ? 1 : 0;
+  a.xn_bulk = bulk_ok(xn) ? 1 : 0;
   a.ctl = m.pp.ctl;
   a.kind = kind;
   a.pstride = m.pstride;
@@ -403,14 +409,14 @@ void launch_pass(int kind, int cols_ub, const strom_isvd* h, const PipeMem& m, c
   const int pk = (kind == PASS_SECOND) ? P_RESID : P_PROJ;
   const int cu = std::max(cols_ub, 1);
   switch (pass_maxj(cu)) {
-    case 1: launch_pass_t<1>(h->store->umap, a, cu, reserve, pk, s); break;
-    case 2: launch_pass_t<2>(h->store->umap, a, cu, reserve, pk, s); break;
-    case 4: launch_pass_t<4>(h->store->umap, a, cu, reserve, pk, s); break;
-    case 8: launch_pass_t<8>(h->store->umap, a, cu, reserve, pk, s); break;
-    case 12: launch_pass_t<12>(h->store->umap, a, cu, reserve, pk, s); break;
-    case 16: launch_pass_t<16>(h->store->umap, a, cu, reserve, pk, s); break;
-    case 24: launch_pass_t<24>(h->store->umap, a, cu, reserve, pk, s); break;
-    default: launch_pass_t<32>(h->store->umap, a, cu, reserve, pk, s); break;
+    case 1: launch_pass_t<1>(a, cu, reserve, pk, s); break;
+    case 2: launch_pass_t<2>(a, cu, reserve, pk, s); break;
+    case 4: launch_pass_t<4>(a, cu, reserve, pk, s); break;
+    case 8: launch_pass_t<8>(a, cu, reserve, pk, s); break;
+    case 12: launch_pass_t<12>(a, cu, reserve, pk, s); break;
+    case 16: launch_pass_t<16>(a, cu, reserve, pk, s); break;
+    case 24: launch_pass_t<24>(a, cu, reserve, pk, s); break;
+    default: launch_pass_t<32>(a, cu, reserve, pk, s); break;
   }
 }
 
@@ -484,20 +490,20 @@ void launch_compact_prep(const StateView& src, const StateView& dst, const PipeM
   STROM_LAUNCH_CHECK();
 }
 
-void launch_tall_gemm(const double* A, int64_t lda, const int32_t* col0_dev, const double* T, int64_t ldt,
-                      const int32_t* p_dev, const int32_t* q_dev, double* out, int64_t ldo, bool row_major,
-                      int64_t n, int64_t nrows_pad, cudaStream_t s) {
+void launch_tall_gemm(const Tall& A, const int32_t* col0_dev, const double* T, int64_t ldt, const int32_t* p_dev,
+                      const int32_t* q_dev, const Tall& out, bool row_major, int64_t n, int64_t nrows_pad,
+                      cudaStream_t s) {
   const int64_t tiles = ceil_div(nrows_pad, kGemmRows);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)sm_count() * 4));
   ProfScope ps(P_TALL_GEMM, s);
-  k_tall_gemm<<<grid, 256, kGemmKc * 64 * 8, s>>>(A, lda, col0_dev, 0, T, ldt, p_dev, q_dev, 0, out, ldo,
-                                                  row_major ? 1 : 0, n, nrows_pad);
+  k_tall_gemm<<<grid, 256, kGemmKc * 64 * 8, s>>>(A, col0_dev, 0, T, ldt, p_dev, q_dev, 0, out, row_major ? 1 : 0, n,
+                                                  nrows_pad);
   STROM_LAUNCH_CHECK();
 }
 
 // L = chol(A[:, col0:col0+q]^T A[:, col0:col0+q]) with the DMMA tall Gram.
 // q is read on the device (q_dev) or fixed; the Cholesky reads c from hdr_c.
-void gram_cholesky(const double* A, int64_t lda, const int32_t* col0_dev, const int32_t* q_dev, int q_fixed,
+void gram_cholesky(const Tall& A, const int32_t* col0_dev, const int32_t* q_dev, int q_fixed,
                    int qmax, int64_t n, double* L, double* Li, int ldl, const IsvdHdr* hdr_c, int* status_dev,
                    cudaStream_t s) {
   const int QP = (int)round_up(std::max(qmax, 1), 8);
@@ -507,14 +513,14 @@ void gram_cholesky(const double* A, int64_t lda, const int32_t* col0_dev, const 
   const size_t smem = (size_t)QP * kGramLd * 8;
   ProfScope ps(P_OTHER, s);
   if (QP <= 64) {
-    k_tall_gram<1, 8><<<grid, 256, smem, s>>>(A, lda, col0_dev, q_dev, q_fixed, n, part->as<double>(), QP);
+    k_tall_gram<1, 8><<<grid, 256, smem, s>>>(A, col0_dev, q_dev, q_fixed, n, part->as<double>(), QP);
   } else if (QP <= 128) {
     static bool cfg = false;
     if (!cfg) {
       STROM_CUDA(cudaFuncSetAttribute(k_tall_gram<2, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
       cfg = true;
     }
-    k_tall_gram<2, 16><<<grid, 256, smem, s>>>(A, lda, col0_dev, q_dev, q_fixed, n, part->as<double>(), QP);
+    k_tall_gram<2, 16><<<grid, 256, smem, s>>>(A, col0_dev, q_dev, q_fixed, n, part->as<double>(), QP);
   } else {
     throw Error(kInvalidArgument, "Gram of more than 128 columns is not supported");
   }
@@ -547,10 +553,12 @@ strom_isvd* compact(strom_isvd* src, const Caps& caps, cudaStream_t s) {
   P.ccap = kc.ccap;
   launch_compact_prep(src->view, t->view, m, P, kc, s);
   // p = source c (step->m), q = r (step->mkeep); source columns start at base
-  launch_tall_gemm(src->store->U(), src->ldu, &src->view.hdr->base, m.pp.T, P.ccap, &m.pp.step[0]->m,
-                   &m.pp.step[0]->mkeep, t->store->U(), t->ldu, false, t->n, t->ldu, s);
+  launch_tall_gemm(tall_tiled(src->store->U(), src->store->ccap), &src->view.hdr->base, m.pp.T, P.ccap,
+                   &m.pp.step[0]->m, &m.pp.step[0]->mkeep, tall_tiled(t->store->U(), t->store->ccap), false, t->n,
+                   t->ldu, s);
   // measure the Gram of the stored U_new: L describes the memory, not an assumed identity
-  gram_cholesky(t->store->U(), t->ldu, nullptr, &m.pp.step[0]->mkeep, 0, caps.rcap, t->n, t->view.L, t->view.Li,
+  gram_cholesky(tall_tiled(t->store->U(), t->store->ccap), nullptr, &m.pp.step[0]->mkeep, 0, caps.rcap, t->n,
+                t->view.L, t->view.Li,
                 t->view.ldl, t->view.hdr, &m.pp.step[0]->pad0, s);
   k_compact_finish<<<1, 256, 0, s>>>(t->view, m.pp.T, P.ccap);
   STROM_LAUNCH_CHECK();
@@ -935,8 +943,8 @@ int strom_isvd_export(strom_isvd* h, double* phi_dev, double* sigma_dev, double*
       k_n_to_w<<<(unsigned)std::max<int64_t>(1, ceil_div((int64_t)hh.c * r, 256)), 256, 0, s>>>(h->view,
                                                                                               wtmp->as<double>());
       STROM_LAUNCH_CHECK();
-      launch_tall_gemm(h->store->U(), h->ldu, &h->view.hdr->base, wtmp->as<double>(), hh.c, &h->view.hdr->c,
-                       &h->view.hdr->r, phi_dev, r, true, h->n, h->ldu, s);
+      launch_tall_gemm(tall_tiled(h->store->U(), h->store->ccap), &h->view.hdr->base, wtmp->as<double>(), hh.c,
+                       &h->view.hdr->c, &h->view.hdr->r, tall_cm(phi_dev, r), true, h->n, h->ldu, s);
     }
     if (sigma_dev && r > 0)
       STROM_CUDA(cudaMemcpyAsync(sigma_dev, h->view.sigma, r * 8, cudaMemcpyDeviceToDevice, s));
@@ -973,7 +981,9 @@ int strom_isvd_load_factored(int64_t n, int64_t k, int64_t c, int64_t r, const d
     alloc_v(h, s);
     set_store(h, alloc_store(n, h->ldu, h->caps.ccap, s));
     if (c > 0) {
-      STROM_CUDA(cudaMemcpy2DAsync(h->store->U(), h->ldu * 8, u_dev, ldu * 8, n * 8, c, cudaMemcpyDeviceToDevice, s));
+      k_copy_tall<<<(unsigned)ceil_div(n * c, 256), 256, 0, s>>>(tall_cm(u_dev, ldu), n, c,
+                                                                tall_tiled(h->store->U(), h->store->ccap));
+      STROM_LAUNCH_CHECK();
     }
     const int th = 256;
     if (c > 0 && r > 0) {
@@ -998,7 +1008,8 @@ int strom_isvd_load_factored(int64_t n, int64_t k, int64_t c, int64_t r, const d
       } else {
         // measure the Gram of the stored U (exact L even for a nearly orthonormal U)
         auto st = dev_alloc(sizeof(int), s, true);
-        gram_cholesky(h->store->U(), h->ldu, nullptr, nullptr, (int)c, (int)c, n, h->view.L, h->view.Li,
+        gram_cholesky(tall_tiled(h->store->U(), h->store->ccap), nullptr, nullptr, (int)c, (int)c, n, h->view.L,
+                      h->view.Li,
                       h->view.ldl, nullptr, st->as<int>(), s);
         int bad = 0;
         STROM_CUDA(cudaMemcpyAsync(&bad, st->ptr, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -1055,9 +1066,12 @@ int strom_isvd_factors(strom_isvd* h, double* u_dev, double* w_dev, double* l_de
     cudaStream_t s = as_stream(stream);
     IsvdHdr hh;
     read_hdr(h, s, &hh);
-    if (u_dev && hh.c > 0)
-      STROM_CUDA(cudaMemcpy2DAsync(u_dev, h->n * 8, h->store->U() + (int64_t)hh.base * h->ldu, h->ldu * 8, h->n * 8,
-                                   hh.c, cudaMemcpyDeviceToDevice, s));
+    if (u_dev && hh.c > 0) {
+      Tall src = tall_tiled(h->store->U(), h->store->ccap);
+      src.p += (int64_t)hh.base * kUTile;  // logical column 0 = physical column base
+      k_copy_tall<<<(unsigned)ceil_div(h->n * hh.c, 256), 256, 0, s>>>(src, h->n, hh.c, tall_cm(u_dev, h->n));
+      STROM_LAUNCH_CHECK();
+    }
     if (w_dev && hh.c > 0 && hh.r > 0) {
       k_n_to_w<<<(unsigned)ceil_div((int64_t)hh.c * hh.r, 256), 256, 0, s>>>(h->view, w_dev);
       STROM_LAUNCH_CHECK();
@@ -1066,6 +1080,39 @@ int strom_isvd_factors(strom_isvd* h, double* u_dev, double* w_dev, double* l_de
       STROM_CUDA(cudaMemcpy2DAsync(l_dev, hh.c * 8, h->view.L + (int64_t)hh.base * (h->view.ldl + 1),
                                    h->view.ldl * 8, hh.c * 8, hh.c,
                                    cudaMemcpyDeviceToDevice, s));
+    STROM_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+// Diagnostics: time `iters` FUSED passes over a synthetic n x c store (random
+// values), reserve SMs left idle; writes the mean ms per pass.
+int strom_debug_pass_bw(int64_t n, int32_t c, int32_t iters, int32_t reserve, double* ms_out) {
+  return guarded([&] {
+    cudaStream_t s = nullptr;  // legacy stream: outlives every stream-ordered free below
+    strom_isvd h;
+    h.n = n;
+    h.ldu = round_up(n, kGemmRows);
+    h.caps = make_caps(n, -1, std::max(c, 1), 1);
+    STROM_REQUIRE(c + 1 <= h.caps.ccap, "c too large for the capacity");
+    set_store(&h, alloc_store(n, h.ldu, h.caps.ccap, s));
+    STROM_CUDA(cudaMemsetAsync(h.store->U(), 0, (size_t)h.ldu * h.caps.ccap * 8, s));
+    auto xs = dev_alloc((size_t)n * 2 * 8, s, true);
+    PipeMem m = make_pipe(h.caps, s);
+    std::vector<int32_t> ctl = {c, 0, 0, 0};
+    STROM_CUDA(cudaMemcpyAsync(m.pp.ctl, ctl.data(), 16, cudaMemcpyHostToDevice, s));
+    cudaEvent_t e0, e1;
+    STROM_CUDA(cudaEventCreate(&e0));
+    STROM_CUDA(cudaEventCreate(&e1));
+    launch_pass(PASS_FUSED, c, &h, m, xs->as<double>(), xs->as<double>() + n, reserve, s);
+    STROM_CUDA(cudaEventRecord(e0, s));
+    for (int i = 0; i < iters; ++i) launch_pass(PASS_FUSED, c, &h, m, xs->as<double>(), xs->as<double>() + n, reserve, s);
+    STROM_CUDA(cudaEventRecord(e1, s));
+    STROM_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    STROM_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    *ms_out = ms / std::max(iters, 1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
     STROM_CUDA(cudaStreamSynchronize(s));
   });
 }

@@ -19,8 +19,6 @@
 // with the next snapshot's pass.
 #pragma once
 
-#include <cuda.h>
-
 #include "common.cuh"
 #include "core_svd.cuh"
 #include "small_dense.cuh"
@@ -132,7 +130,8 @@ struct IsvdParams {
 constexpr int kPassRows = 32;       // rows per pass tile (one per lane)
 constexpr int kPassConsumers = 8;                        // consumer warps of the pass
 constexpr int kPassThreads = 32 * (kPassConsumers + 1);  // + one TMA producer warp; one CTA per SM
-constexpr int kStageRows = 64;                           // rows per pipeline stage (2 per lane)
+constexpr int kStageRows = kUTile;                       // rows per pipeline stage = one U tile
+constexpr int kSubRows = kUTile;                         // rows per consumer step (2 per lane)
 constexpr int kSmallThreads = 512;  // one-CTA kernels: 128 registers per thread (no spills)
 constexpr int kDecideThreads = 512;
 constexpr int kTileRows = 64;       // legacy tile of the helpers below
@@ -171,8 +170,11 @@ __device__ inline bool last_cta_arrives(unsigned* counter, int* s_is_last) {
 enum : int32_t { PASS_PROJ = 0, PASS_FUSED = 1, PASS_SECOND = 2 };
 
 struct PassArgs {
-  double* U;
+  double* U;  // row-tiled store (kUTile-row tiles of ccap column segments)
   int64_t ldu, n;
+  int64_t ccap;
+  int32_t dbg;  // diagnostics: 1 = consumers only wait/release (bandwidth probe)
+  int32_t x_bulk, xn_bulk;  // x / xn may be staged by bulk copy (16-byte aligned, n even)
   const PipeCtl* ctl;
   int32_t kind;
   int32_t pstride;
@@ -213,17 +215,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                : "memory");
 }
 
-// 2D tensor TMA: box (kPassRows rows x kBoxCols columns) of U at (row, col)
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int row, int col, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(row), "r"(col), "r"(smem_u32(bar))
-      : "memory");
-}
-
 constexpr int kPassMaxStages = 8;
-constexpr int kBoxCols = 8;  // columns per TMA box (2 KB with 32 rows)
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -237,13 +229,12 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // barrier per stage.  Column dots stay in registers until a deterministic
 // last-CTA reduction.
 template <int MAXJ>
-__global__ void __launch_bounds__(kPassThreads, 1) k_pass(const __grid_constant__ CUtensorMap umap, PassArgs a,
-                                                         int nstages) {
+__global__ void __launch_bounds__(kPassThreads, 1) k_pass(PassArgs a, int nstages) {
   extern __shared__ __align__(128) double stg[];  // nstages x (kStageRows x cs), column segments
   __shared__ __align__(8) uint64_t full[kPassMaxStages];
   __shared__ __align__(8) uint64_t empty[kPassMaxStages];
   __shared__ double gts[kPassConsumers * MAXJ];
-  __shared__ __align__(16) double red[2][kPassConsumers][kStageRows];
+  __shared__ __align__(16) double red[2][kPassConsumers][kSubRows];
   __shared__ double wsc[3];
   __shared__ int s_last;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -252,12 +243,13 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(const __grid_constant_
   const int slot = base + c;
   const double* x = a.x;
   const double* coef = a.coef;
-  bool do_e = false, do_gn = false;
+  bool do_e = false, do_gn = false, x_is_slot = false;
   if (a.kind == PASS_SECOND) {
     const int ro = a.ctl->reorth;
     if (ro == 0) return;
     if (ro == 1) {
-      x = a.U + (int64_t)slot * a.ldu;  // r2 = r1 - U h, in place
+      x_is_slot = true;  // r2 = r1 - U h, in place on the slot column
+      x = a.U;
       do_e = true;
     } else {
       coef = nullptr;  // slot <- x
@@ -270,6 +262,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(const __grid_constant_
     x = nullptr;
     do_gn = true;
   }
+  const int64_t tstride = (int64_t)kUTile * a.ccap;  // one U tile: kUTile rows x ccap columns
   const bool do_r = x != nullptr;
   const bool do_coef = do_r && coef != nullptr && c > 0;
   const bool do_xn = a.xn != nullptr;
@@ -281,10 +274,16 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(const __grid_constant_
   const int64_t per = ceil_div(ntiles, gridDim.x);
   const int64_t t0 = blockIdx.x * per;
   const int64_t nt = max((int64_t)0, min(ntiles, t0 + per) - t0);
-  const int nbox = (c + kBoxCols - 1) / kBoxCols;
-  const int cs = nbox * kBoxCols;
-  const unsigned stage_elems = (unsigned)(kStageRows * cs);
-  if (threadIdx.x == 0) {
+  // stage layout: [U column segments base .. base+cu) [x segment] [xn segment], kStageRows rows each.
+  // DGKS reads the slot column as x: it is U column c of the stage.
+  const int cu = c + (x_is_slot ? 1 : 0);
+  const bool x_stage = x_is_slot || (do_r && a.x_bulk);
+  const bool x_own = do_r && !x_is_slot && a.x_bulk;  // x has its own segment
+  const bool xn_stage = do_xn && a.xn_bulk;
+  const int x_col = x_is_slot ? c : cu;
+  const int xn_col = cu + (x_own ? 1 : 0);
+  const int cs = cu + (x_own ? 1 : 0) + (xn_stage ? 1 : 0);
+  const unsigned stage_elems = (unsigned)(kStageRows * cs);  if (threadIdx.x == 0) {
     for (int st = 0; st < nstages; ++st) {
       mbar_init(&full[st], 1);
       mbar_init(&empty[st], kPassConsumers);
@@ -299,11 +298,15 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(const __grid_constant_
         const int st = (int)(i % nstages);
         const int64_t use = i / nstages;
         if (use > 0) mbar_wait(&empty[st], (unsigned)((use - 1) & 1));
-        mbar_expect_tx(&full[st], stage_elems * 8u);
+        const int64_t row0 = (t0 + i) * kStageRows;
+        const int valid = (int)max((int64_t)0, min((int64_t)kStageRows, a.n - row0));
+        const unsigned bu = (unsigned)(kStageRows * cu) * 8u, bv = (unsigned)valid * 8u;
+        mbar_expect_tx(&full[st], bu + (x_own ? bv : 0u) + (xn_stage ? bv : 0u));
         double* dst = stg + (size_t)st * stage_elems;
-        const int row0 = (int)((t0 + i) * kStageRows);
-        for (int b = 0; b < nbox; ++b)
-          tma_load_2d(dst + b * kBoxCols * kStageRows, &umap, row0, base + b * kBoxCols, &full[st]);
+        // the live column segments of U tile t0 + i are one contiguous run
+        if (bu) bulk_g2s(dst, a.U + (t0 + i) * tstride + (int64_t)base * kUTile, bu, &full[st]);
+        if (x_own && bv) bulk_g2s(dst + x_col * kStageRows, x + row0, bv, &full[st]);
+        if (xn_stage && bv) bulk_g2s(dst + xn_col * kStageRows, a.xn + row0, bv, &full[st]);
       }
     }
   } else {
@@ -313,74 +316,87 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(const __grid_constant_
 #pragma unroll
     for (int q = 0; q < MAXJ; ++q) { ae[q] = 0.0; ag[q] = 0.0; }
     double rr = 0.0, gs = 0.0, xq = 0.0;
-    double* scol = a.U + (int64_t)slot * a.ldu;
     for (int64_t i = 0; i < nt; ++i) {
-      const int64_t row = (t0 + i) * kStageRows + 2 * lane;
-      const bool live0 = row < a.n, live1 = row + 1 < a.n;
-      double2 xv = make_double2(0.0, 0.0), xnv = make_double2(0.0, 0.0);
-      if (do_r) {
-        xv.x = live0 ? x[row] : 0.0;
-        xv.y = live1 ? x[row + 1] : 0.0;
-      }
-      if (do_xn) {
-        xnv.x = live0 ? __ldg(a.xn + row) : 0.0;
-        xnv.y = live1 ? __ldg(a.xn + row + 1) : 0.0;
-      }
       const int st = (int)(i % nstages);
       const int64_t use = i / nstages;
-      double2 u[MAXJ];
-      if (cs > 0) {
-        mbar_wait(&full[st], (unsigned)(use & 1));
-        const double* tile = stg + (size_t)st * stage_elems;
+      if (cs > 0) mbar_wait(&full[st], (unsigned)(use & 1));
+      if (a.dbg & 1) {
+        __syncwarp();
+        if (lane == 0 && cs > 0) mbar_arrive(&empty[st]);
+        continue;
+      }
+      const double* tile = stg + (size_t)st * stage_elems;
+#pragma unroll 1
+      for (int hh = 0; hh < kStageRows / kSubRows; ++hh) {
+        const int64_t sub = (t0 + i) * (kStageRows / kSubRows) + hh;  // global sub-tile index
+        const int64_t row = sub * kSubRows + 2 * lane;
+        const bool live0 = row < a.n, live1 = row + 1 < a.n;
+        double2 xv = make_double2(0.0, 0.0), xnv = make_double2(0.0, 0.0);
+        double* scol = a.U + sub * tstride + (int64_t)slot * kUTile;  // this tile's slot segment
+        if (x_stage) {
+          xv = reinterpret_cast<const double2*>(tile + x_col * kStageRows + hh * kSubRows)[lane];
+        } else if (do_r) {
+          xv.x = live0 ? x[row] : 0.0;
+          xv.y = live1 ? x[row + 1] : 0.0;
+        }
+        if (xn_stage) {
+          xnv = reinterpret_cast<const double2*>(tile + xn_col * kStageRows + hh * kSubRows)[lane];
+        } else if (do_xn) {
+          xnv.x = live0 ? __ldg(a.xn + row) : 0.0;
+          xnv.y = live1 ? __ldg(a.xn + row + 1) : 0.0;
+        }
+        if (!live0) { xv.x = 0.0; xnv.x = 0.0; }
+        if (!live1) { xv.y = 0.0; xnv.y = 0.0; }
+        double2 u[MAXJ];
 #pragma unroll
         for (int q = 0; q < MAXJ; ++q) {
           const int j = cw + kPassConsumers * q;
-          u[q] = (j < c) ? reinterpret_cast<const double2*>(tile + j * kStageRows)[lane] : make_double2(0.0, 0.0);
+          u[q] = (j < c) ? reinterpret_cast<const double2*>(tile + j * kStageRows + hh * kSubRows)[lane]
+                         : make_double2(0.0, 0.0);
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[st]);  // the stage is in registers
-      } else {
-#pragma unroll
-        for (int q = 0; q < MAXJ; ++q) u[q] = make_double2(0.0, 0.0);
-      }
-      double2 r = xv;
-      if (do_coef) {
-        double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-        for (int q = 0; q < MAXJ; ++q) {
-          const double gq = gts[cw + kPassConsumers * q];
-          s0 = fma(u[q].x, gq, s0);
-          s1 = fma(u[q].y, gq, s1);
+        if (hh == kStageRows / kSubRows - 1 && cs > 0) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[st]);  // the stage is in registers
         }
-        reinterpret_cast<double2*>(&red[i & 1][cw][0])[lane] = make_double2(s0, s1);
-        asm volatile("bar.sync 1, %0;" ::"n"(32 * kPassConsumers) : "memory");
-        double d0 = 0.0, d1 = 0.0;
+        double2 r = xv;
+        if (do_coef) {
+          double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-        for (int w = 0; w < kPassConsumers; ++w) {
-          const double2 p = reinterpret_cast<const double2*>(&red[i & 1][w][0])[lane];
-          d0 += p.x;
-          d1 += p.y;
-        }
-        r.x = xv.x - d0;
-        r.y = xv.y - d1;
-      }
-      if (!live0) r.x = 0.0;
-      if (!live1) r.y = 0.0;
-      if (do_r) {
-        if (cw == kPassConsumers - 1) {
-          reinterpret_cast<double2*>(scol + (t0 + i) * kStageRows)[lane] = r;
-          rr = fma(r.y, r.y, fma(r.x, r.x, rr));
-          gs = fma(r.y, xnv.y, fma(r.x, xnv.x, gs));
-        }
-        if (do_e) {
+          for (int q = 0; q < MAXJ; ++q) {
+            const double gq = gts[cw + kPassConsumers * q];
+            s0 = fma(u[q].x, gq, s0);
+            s1 = fma(u[q].y, gq, s1);
+          }
+          reinterpret_cast<double2*>(&red[sub & 1][cw][0])[lane] = make_double2(s0, s1);
+          asm volatile("bar.sync 1, %0;" ::"n"(32 * kPassConsumers) : "memory");
+          double d0 = 0.0, d1 = 0.0;
 #pragma unroll
-          for (int q = 0; q < MAXJ; ++q) ae[q] = fma(u[q].y, r.y, fma(u[q].x, r.x, ae[q]));
+          for (int w = 0; w < kPassConsumers; ++w) {
+            const double2 p = reinterpret_cast<const double2*>(&red[sub & 1][w][0])[lane];
+            d0 += p.x;
+            d1 += p.y;
+          }
+          r.x = xv.x - d0;
+          r.y = xv.y - d1;
         }
-      }
-      if (do_gn) {
+        if (!live0) r.x = 0.0;
+        if (!live1) r.y = 0.0;
+        if (do_r) {
+          if (cw == kPassConsumers - 1) {
+            reinterpret_cast<double2*>(scol)[lane] = r;
+            rr = fma(r.y, r.y, fma(r.x, r.x, rr));
+            gs = fma(r.y, xnv.y, fma(r.x, xnv.x, gs));
+          }
+          if (do_e) {
 #pragma unroll
-        for (int q = 0; q < MAXJ; ++q) ag[q] = fma(u[q].y, xnv.y, fma(u[q].x, xnv.x, ag[q]));
-        if (cw == kPassConsumers - 1) xq = fma(xnv.y, xnv.y, fma(xnv.x, xnv.x, xq));
+            for (int q = 0; q < MAXJ; ++q) ae[q] = fma(u[q].y, r.y, fma(u[q].x, r.x, ae[q]));
+          }
+        }
+        if (do_gn) {
+#pragma unroll
+          for (int q = 0; q < MAXJ; ++q) ag[q] = fma(u[q].y, xnv.y, fma(u[q].x, xnv.x, ag[q]));
+          if (cw == kPassConsumers - 1) xq = fma(xnv.y, xnv.y, fma(xnv.x, xnv.x, xq));
+        }
       }
     }
     // per-CTA partials: [0, PG) e | [PG, 2 PG) gn | 2 PG + {0: r.r, 1: xn.xn, 2: r.xn}
@@ -989,18 +1005,17 @@ __global__ void __launch_bounds__(256) k_w_to_n(StateView v, double* tmp) {
 // ---------------------------------------------------------------------------
 // Tall-skinny GEMM:  out(n x q) = A(n x p) * T(p x q)   (fp64 FMA, register
 // blocked 4 rows x 8 cols per thread, T staged through shared memory).
-// A column-major (lda, first column a_col0); out column-major (ldo) or
-// row-major (ldo = row stride) when out_row_major.  p, q read from device.
+// A and out are Tall views (column-major or row-tiled; first A column a_col0);
+// out row-major (row stride out.cs) when out_row_major.  p, q read from device.
 // ---------------------------------------------------------------------------
 constexpr int kGemmRows = 128;  // rows per CTA tile
 constexpr int kGemmKc = 32;     // T chunk (rows of T) per smem stage
 
-__global__ void __launch_bounds__(256) k_tall_gemm(const double* __restrict__ A, int64_t lda,
-                                                   const int32_t* a_col0_dev, int a_col0_add,
+__global__ void __launch_bounds__(256) k_tall_gemm(Tall A, const int32_t* a_col0_dev, int a_col0_add,
                                                    const double* __restrict__ T, int64_t ldt,
                                                    const int32_t* p_dev, const int32_t* q_dev,
-                                                   int q_max, double* __restrict__ out, int64_t ldo,
-                                                   int out_row_major, int64_t n, int64_t nrows_pad) {
+                                                   int q_max, Tall out, int out_row_major, int64_t n,
+                                                   int64_t nrows_pad) {
   extern __shared__ double ts[];  // kGemmKc x q_max
   const int p = *p_dev, q = *q_dev;
   const int col0 = (a_col0_dev ? *a_col0_dev : 0) + a_col0_add;
@@ -1025,10 +1040,9 @@ __global__ void __launch_bounds__(256) k_tall_gemm(const double* __restrict__ A,
         }
         __syncthreads();
         for (int kk = 0; kk < kc; ++kk) {
-          const double* acol = A + (int64_t)(col0 + k0 + kk) * lda + r0;
           double av[4];
 #pragma unroll
-          for (int a = 0; a < 4; ++a) av[a] = __ldg(acol + tx + 32 * a);
+          for (int a = 0; a < 4; ++a) av[a] = __ldg(A.p + A.off(r0 + tx + 32 * a, col0 + k0 + kk));
 #pragma unroll
           for (int b = 0; b < 8; ++b) {
             const double t = ts[(ty * 8 + b) * kGemmKc + kk];
@@ -1045,9 +1059,9 @@ __global__ void __launch_bounds__(256) k_tall_gemm(const double* __restrict__ A,
         for (int a = 0; a < 4; ++a) {
           const int64_t row = r0 + tx + 32 * a;
           if (out_row_major) {
-            if (row < n) out[row * ldo + col] = acc[a][b];
+            if (row < n) out.p[row * out.cs + col] = acc[a][b];
           } else if (row < nrows_pad) {
-            out[(int64_t)col * ldo + row] = acc[a][b];
+            out.p[out.off(row, col)] = acc[a][b];
           }
         }
       }
