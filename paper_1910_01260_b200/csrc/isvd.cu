@@ -160,8 +160,17 @@ struct strom_isvd {
 
 namespace {
 
-// ccap = rcap + 1 + slack; 2 rcap keeps c_cap = 128 at rank 64
-int32_t slack_for(int32_t rcap) { return std::max<int32_t>(16, rcap - 1); }
+// ccap = rcap + 1 + slack
+int32_t slack_for(int32_t rcap) {
+  static const int env = [] {
+    const char* e = getenv("STROM_SLACK");
+    return e ? atoi(e) : 0;
+  }();
+  if (env > 0) return env;  // diagnostics
+  // passes read ~r + slack/2 columns; a compaction (one DMMA sweep) costs about
+  // as much as ~1000 column reads and recurs every ~3 slack updates at cfg2
+  return std::max<int32_t>(16, rcap / 2);
+}
 
 Caps make_caps(int64_t n, int32_t r_max, int32_t want_r, int64_t k) {
   Caps c;
@@ -501,6 +510,31 @@ void launch_tall_gemm(const Tall& A, const int32_t* col0_dev, const double* T, i
   STROM_LAUNCH_CHECK();
 }
 
+// Gram from per-CTA partials (QP x QP each, summed in CTA order) -> L = chol, Li = L^{-1}
+void gram_finish(const double* part, int nparts, int QP, const int32_t* q_dev, int q_fixed, double* L, double* Li,
+                 int ldl, const IsvdHdr* hdr_c, int* status_dev, cudaStream_t s) {
+  k_gram_reduce<<<(unsigned)ceil_div((int64_t)QP * QP, 256), 256, 0, s>>>(part, nparts, QP, q_dev, q_fixed, L, ldl);
+  STROM_LAUNCH_CHECK();
+  k_cholesky<<<1, 256, 0, s>>>(L, ldl, hdr_c, q_fixed, status_dev);
+  STROM_LAUNCH_CHECK();
+  k_lower_inverse<<<1, 1024, 0, s>>>(L, ldl, hdr_c, q_fixed, Li);
+  STROM_LAUNCH_CHECK();
+}
+
+template <int GB>
+void launch_compact_pass(const Store& src, const int32_t* base_dev, const int32_t* c_dev, const int32_t* r_dev,
+                         const double* T, int64_t ldt, int cmax, int rmax, const Store& dst, double* part, int QP,
+                         cudaStream_t s) {
+  const int c4 = (cmax + 3) & ~3, RP = (rmax + 31) & ~31;
+  const size_t smem = ((size_t)c4 * (RP + 4) + (size_t)c4 * (kUTile + 4) + (size_t)RP * (kUTile + 4)) * 8;
+  static size_t cfg = 0;
+  set_smem_attr(k_compact_pass<GB>, smem, &cfg);
+  ProfScope ps(P_TALL_GEMM, s);
+  k_compact_pass<GB><<<sm_count(), kCompactThreads, smem, s>>>(src.U(), src.ccap, base_dev, c_dev, r_dev, T, ldt,
+                                                               dst.U(), dst.ccap, src.ldu / kUTile, part, QP);
+  STROM_LAUNCH_CHECK();
+}
+
 // L = chol(A[:, col0:col0+q]^T A[:, col0:col0+q]) with the DMMA tall Gram.
 // q is read on the device (q_dev) or fixed; the Cholesky reads c from hdr_c.
 void gram_cholesky(const Tall& A, const int32_t* col0_dev, const int32_t* q_dev, int q_fixed,
@@ -525,13 +559,7 @@ void gram_cholesky(const Tall& A, const int32_t* col0_dev, const int32_t* q_dev,
     throw Error(kInvalidArgument, "Gram of more than 128 columns is not supported");
   }
   STROM_LAUNCH_CHECK();
-  k_gram_reduce<<<(unsigned)ceil_div((int64_t)QP * QP, 256), 256, 0, s>>>(part->as<double>(), grid, QP, q_dev,
-                                                                          q_fixed, L, ldl);
-  STROM_LAUNCH_CHECK();
-  k_cholesky<<<1, 256, 0, s>>>(L, ldl, hdr_c, q_fixed, status_dev);
-  STROM_LAUNCH_CHECK();
-  k_lower_inverse<<<1, 1024, 0, s>>>(L, ldl, hdr_c, q_fixed, Li);
-  STROM_LAUNCH_CHECK();
+  gram_finish(part->as<double>(), grid, QP, q_dev, q_fixed, L, Li, ldl, hdr_c, status_dev, s);
 }
 
 // Compaction into a fresh store (also used to grow capacities):
@@ -553,13 +581,32 @@ strom_isvd* compact(strom_isvd* src, const Caps& caps, cudaStream_t s) {
   P.ccap = kc.ccap;
   launch_compact_prep(src->view, t->view, m, P, kc, s);
   // p = source c (step->m), q = r (step->mkeep); source columns start at base
-  launch_tall_gemm(tall_tiled(src->store->U(), src->store->ccap), &src->view.hdr->base, m.pp.T, P.ccap,
-                   &m.pp.step[0]->m, &m.pp.step[0]->mkeep, tall_tiled(t->store->U(), t->store->ccap), false, t->n,
-                   t->ldu, s);
-  // measure the Gram of the stored U_new: L describes the memory, not an assumed identity
-  gram_cholesky(tall_tiled(t->store->U(), t->store->ccap), nullptr, &m.pp.step[0]->mkeep, 0, caps.rcap, t->n,
-                t->view.L, t->view.Li,
-                t->view.ldl, t->view.hdr, &m.pp.step[0]->pad0, s);
+  if (kc.rcap <= 128) {
+    // one fused DMMA sweep: U_new = U T and the measured Gram of the stored U_new
+    const int RP = (int)round_up(kc.rcap, 32);
+    auto part = dev_alloc((size_t)sm_count() * RP * RP * 8, s, false);
+    const int nbg = (RP / 16) * (RP / 32);
+    const int gb = (nbg + 7) / 8;
+    const int32_t* bptr = &src->view.hdr->base;
+    const int32_t* cptr = &m.pp.step[0]->m;
+    const int32_t* rptr = &m.pp.step[0]->mkeep;
+    const int cmax = src->caps.ccap;
+    switch (gb) {
+      case 1: launch_compact_pass<1>(*src->store, bptr, cptr, rptr, m.pp.T, P.ccap, cmax, kc.rcap, *t->store, part->as<double>(), RP, s); break;
+      case 2: launch_compact_pass<2>(*src->store, bptr, cptr, rptr, m.pp.T, P.ccap, cmax, kc.rcap, *t->store, part->as<double>(), RP, s); break;
+      case 3: launch_compact_pass<3>(*src->store, bptr, cptr, rptr, m.pp.T, P.ccap, cmax, kc.rcap, *t->store, part->as<double>(), RP, s); break;
+      default: launch_compact_pass<4>(*src->store, bptr, cptr, rptr, m.pp.T, P.ccap, cmax, kc.rcap, *t->store, part->as<double>(), RP, s); break;
+    }
+    gram_finish(part->as<double>(), sm_count(), RP, rptr, 0, t->view.L, t->view.Li, t->view.ldl, t->view.hdr,
+                &m.pp.step[0]->pad0, s);
+  } else {
+    launch_tall_gemm(tall_tiled(src->store->U(), src->store->ccap), &src->view.hdr->base, m.pp.T, P.ccap,
+                     &m.pp.step[0]->m, &m.pp.step[0]->mkeep, tall_tiled(t->store->U(), t->store->ccap), false, t->n,
+                     t->ldu, s);
+    // measure the Gram of the stored U_new: L describes the memory, not an assumed identity
+    gram_cholesky(tall_tiled(t->store->U(), t->store->ccap), nullptr, &m.pp.step[0]->mkeep, 0, caps.rcap, t->n,
+                  t->view.L, t->view.Li, t->view.ldl, t->view.hdr, &m.pp.step[0]->pad0, s);
+  }
   k_compact_finish<<<1, 256, 0, s>>>(t->view, m.pp.T, P.ccap);
   STROM_LAUNCH_CHECK();
   t->r_ub = std::min(src->r_ub, caps.rcap);

@@ -21,6 +21,7 @@
 
 #include "common.cuh"
 #include "core_svd.cuh"
+#include "dmma.cuh"
 #include "small_dense.cuh"
 
 namespace strom {
@@ -999,6 +1000,137 @@ __global__ void __launch_bounds__(256) k_w_to_n(StateView v, double* tmp) {
   for (int64_t idx = threadIdx.x; idx < (int64_t)c * r; idx += blockDim.x) {
     const int i = (int)(idx % c), k = (int)(idx / c);
     v.N[(int64_t)k * v.ldn + i] = tmp[(int64_t)k * c + i];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Fused compaction pass on the fp64 tensor cores (DMMA m8n8k4): for every
+// 64-row tile of the row-tiled store,
+//     U_new tile = U tile (64 x c, columns base..) * T (c x r)      -> new store
+//     G         += U_new tile^T U_new tile                          (registers)
+// so the Gram of the STORED U_new is measured in the same sweep (one read of
+// U, one write of U_new).  c, r are read on the device; r <= 32 * GB * 2 / ...
+// Each warp owns 16 x 32 blocks (2 x 4 fragments): of C per tile, and GB
+// persistent blocks of G.  Per-CTA Gram partials (QP x QP) go to `part`.
+// ---------------------------------------------------------------------------
+constexpr int kCompactThreads = 256;
+template <int GB>
+__global__ void __launch_bounds__(kCompactThreads, 1) k_compact_pass(const double* __restrict__ U, int64_t src_ccap,
+                                                                     const int32_t* base_dev, const int32_t* c_dev,
+                                                                     const int32_t* r_dev, const double* __restrict__ T,
+                                                                     int64_t ldt, double* __restrict__ Unew,
+                                                                     int64_t dst_ccap, int64_t ntiles,
+                                                                     double* __restrict__ part, int QP) {
+  extern __shared__ __align__(16) double csm[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int base = *base_dev, c = *c_dev, r = *r_dev;
+  const int c4 = (c + 3) & ~3;   // K padded to the DMMA k-step
+  const int RP = (r + 31) & ~31;  // C / G columns padded to 32-wide blocks
+  // leading dimensions = 4 (mod 16) doubles: the 16 lanes of a half-warp that
+  // load one DMMA fragment (lane = 4 g + t, address t ld + g) hit 16 distinct banks
+  const int LT = RP + 4, LA = kUTile + 4, LC = kUTile + 4;
+  double* Ts = csm;                       // c4 x LT, T(k, j) at Ts[k * LT + j]
+  double* At = Ts + (size_t)c4 * LT;      // c4 x LA, U(i, k) at At[k * LA + i]
+  double* Cs = At + (size_t)c4 * LA;      // RP x LC, C(i, j) at Cs[j * LC + i]
+  for (int idx = threadIdx.x; idx < c4 * RP; idx += blockDim.x) {
+    const int k = idx / RP, j = idx % RP;
+    Ts[k * LT + j] = (k < c && j < r) ? T[(int64_t)j * ldt + k] : 0.0;
+  }
+  for (int idx = threadIdx.x; idx < (c4 - c) * kUTile; idx += blockDim.x)
+    At[(size_t)(c + idx / kUTile) * LA + idx % kUTile] = 0.0;
+  const int nbc = (kUTile / 16) * (RP / 32);     // C blocks per tile
+  const int nbg = (RP / 16) * (RP / 32);          // G blocks
+  double gacc[GB][2][4][2];
+#pragma unroll
+  for (int b = 0; b < GB; ++b)
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) gacc[b][x][y][0] = gacc[b][x][y][1] = 0.0;
+  const int64_t per = ceil_div(ntiles, gridDim.x);
+  const int64_t tt0 = blockIdx.x * per, tt1 = min(ntiles, tt0 + per);
+  for (int64_t tile = tt0; tile < tt1; ++tile) {
+    __syncthreads();  // previous tile's At / Cs fully consumed
+    {
+      const double2* src = reinterpret_cast<const double2*>(U + tile * kUTile * src_ccap + (int64_t)base * kUTile);
+      for (int idx = threadIdx.x; idx < c * kUTile / 2; idx += blockDim.x) {
+        const int k = idx / (kUTile / 2), i2 = idx % (kUTile / 2);
+        reinterpret_cast<double2*>(At + (size_t)k * LA)[i2] = __ldg(src + idx);
+      }
+    }
+    __syncthreads();
+    // C(i, j) = sum_k U(i, k) T(k, j)
+    for (int blk = wid; blk < nbc; blk += kCompactThreads / 32) {
+      const int i0 = (blk % (kUTile / 16)) * 16, j0 = (blk / (kUTile / 16)) * 32;
+      double acc[2][4][2];
+#pragma unroll
+      for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+      for (int k0 = 0; k0 < c4; k0 += 4) {
+        const int k = k0 + t;
+        double av[2], bv[4];
+#pragma unroll
+        for (int x = 0; x < 2; ++x) av[x] = At[k * LA + i0 + 8 * x + g];
+#pragma unroll
+        for (int y = 0; y < 4; ++y) bv[y] = Ts[k * LT + j0 + 8 * y + g];
+#pragma unroll
+        for (int x = 0; x < 2; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) dmma884(acc[x][y][0], acc[x][y][1], av[x], bv[y]);
+      }
+#pragma unroll
+      for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) {
+          const int i = i0 + 8 * x + g, j = j0 + 8 * y + 2 * t;
+          Cs[(size_t)j * LC + i] = acc[x][y][0];
+          Cs[(size_t)(j + 1) * LC + i] = acc[x][y][1];
+        }
+    }
+    __syncthreads();
+    {  // the r live column segments of the new tile are one contiguous run
+      double2* dst = reinterpret_cast<double2*>(Unew + tile * kUTile * dst_ccap);
+      for (int idx = threadIdx.x; idx < r * kUTile / 2; idx += blockDim.x) {
+        const int j = idx / (kUTile / 2), i2 = idx % (kUTile / 2);
+        dst[idx] = reinterpret_cast<const double2*>(Cs + (size_t)j * LC)[i2];
+      }
+    }
+    // G += C^T C: G(a, b) = sum_i C(i, a) C(i, b)
+#pragma unroll
+    for (int bb = 0; bb < GB; ++bb) {
+      const int blk = wid + bb * (kCompactThreads / 32);
+      if (blk >= nbg) break;
+      const int a0 = (blk % (RP / 16)) * 16, b0 = (blk / (RP / 16)) * 32;
+      for (int k0 = 0; k0 < kUTile; k0 += 4) {
+        const int k = k0 + t;
+        double av[2], bv[4];
+#pragma unroll
+        for (int x = 0; x < 2; ++x) av[x] = Cs[(size_t)(a0 + 8 * x + g) * LC + k];
+#pragma unroll
+        for (int y = 0; y < 4; ++y) bv[y] = Cs[(size_t)(b0 + 8 * y + g) * LC + k];
+#pragma unroll
+        for (int x = 0; x < 2; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) dmma884(gacc[bb][x][y][0], gacc[bb][x][y][1], av[x], bv[y]);
+      }
+    }
+  }
+  double* mp = part + (int64_t)blockIdx.x * QP * QP;
+#pragma unroll
+  for (int bb = 0; bb < GB; ++bb) {
+    const int blk = wid + bb * (kCompactThreads / 32);
+    if (blk >= nbg) break;
+    const int a0 = (blk % (RP / 16)) * 16, b0 = (blk / (RP / 16)) * 32;
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) {
+        const int a = a0 + 8 * x + g, b = b0 + 8 * y + 2 * t;
+        if (a < QP && b < QP) mp[a * QP + b] = gacc[bb][x][y][0];
+        if (a < QP && b + 1 < QP) mp[a * QP + b + 1] = gacc[bb][x][y][1];
+      }
   }
 }
 
