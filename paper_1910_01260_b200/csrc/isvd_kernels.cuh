@@ -826,21 +826,23 @@ __global__ void __launch_bounds__(kSmallThreads) k_step_b(StateView src, StateVi
         for (int a = lane; a < cn; a += 32) M[k * cn + a] = dst.N[(int64_t)k * dst.ldn + a];
       __syncthreads();
       for (int pass = 0; pass < 2 && chol_ok; ++pass) {
+        STROM_TPROBE(P, 280 + 6 * pass);
         cta_gemm_dmma(mk, mk, cn, M, cn, 1, M, 1, cn, [&](int i, int k, double v) { Bm[k * mk + i] = v; });
         __syncthreads();
+        STROM_TPROBE(P, 281 + 6 * pass);
         const double ratio = cta_cholesky(Bm, mk, mk, nullptr);
-        // CholeskyQR loses ~eps cond^2 in the triangular factor: only for
-        // well-conditioned N' (Householder otherwise, like the reference)
+        STROM_TPROBE(P, 282 + 6 * pass);
+        // CholeskyQR loses ~eps cond^2: only for well-conditioned N' (Householder
+        // otherwise, like the reference); one pass suffices when cond <= 2
         if (!(ratio > 1e-2)) { chol_ok = false; break; }
-        cta_lower_inverse(Bm, mk, mk, Vt, mk);
+        for (int k = threadIdx.x; k < mk; k += blockDim.x) Vt[k] = 1.0 / Bm[k * mk + k];
         __syncthreads();
-        // M <- M R^{-1} = M L_B^{-T}:  (L_B^{-T})(j, k) = Vt(k, j); DMMA into WS
-        cta_gemm_dmma(cn, mk, mk, M, 1, cn, Vt, mk, 1,
-                      [&](int a, int k, double v) { dst.N[(int64_t)k * dst.ldn + a] = v; });
+        STROM_TPROBE(P, 283 + 6 * pass);
+        cta_rows_times_inv_lt(M, cn, cn, Bm, mk, mk, Vt);  // M <- M R^{-1}
         __syncthreads();
-        for (int k = wid; k < mk; k += nw)
-          for (int a = lane; a < cn; a += 32) M[k * cn + a] = dst.N[(int64_t)k * dst.ldn + a];
-        __syncthreads();
+        STROM_TPROBE(P, 284 + 6 * pass);
+        STROM_TPROBE(P, 285 + 6 * pass);
+        if (ratio > 0.5) break;
       }
       if (!chol_ok) {
         for (int k = wid; k < mk; k += nw)
@@ -939,11 +941,41 @@ __global__ void __launch_bounds__(kSmallThreads) k_compact_prep(StateView src, S
     }
     return;
   }
-  double* M = use_smem ? smem : pp.work + 4 * (int64_t)P.work_stride;  // c x r
-  for (int k = threadIdx.x >> 5; k < r; k += blockDim.x >> 5)
-    for (int i = threadIdx.x & 31; i < c; i += 32) M[k * c + i] = src.N[(int64_t)k * src.ldn + i];
+  // shared plan (step B's footprint): Bm r^2 | Bi r^2 | spare m^2 | ... | M (c x r, ld c)
+  const int m = r + 1;
+  double* sbase = use_smem ? smem : pp.work + 4 * (int64_t)P.work_stride;
+  double* Bm = sbase;
+  double* Bi = Bm + (int64_t)m * m;
+  double* M = sbase + 3 * (int64_t)m * m + 16 * (int64_t)P.work_stride;  // c x r
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int k = wid; k < r; k += nw)
+    for (int i = lane; i < c; i += 32) M[k * c + i] = src.N[(int64_t)k * src.ldn + i];
   __syncthreads();
-  cta_householder_qr(M, c, c, r, dst.N, dst.ldn, pp.work, pp.work + P.work_stride, red);
+  // N = Q_c R_c by CholeskyQR2 (N has orthonormal columns up to the drift the
+  // reference's QR trigger allows); Householder when its Gram is ill-conditioned
+  bool chol_ok = true;
+  for (int pass = 0; pass < 2 && chol_ok; ++pass) {
+    cta_gemm_dmma(r, r, c, M, c, 1, M, 1, c, [&](int i, int k, double v) { Bm[k * r + i] = v; });
+    __syncthreads();
+    const double ratio = cta_cholesky(Bm, r, r, nullptr);
+    if (!(ratio > 1e-2)) { chol_ok = false; break; }
+    for (int k = threadIdx.x; k < r; k += blockDim.x) Bi[k] = 1.0 / Bm[k * r + k];
+    __syncthreads();
+    cta_rows_times_inv_lt(M, c, c, Bm, r, r, Bi);  // M <- M Bm^{-T}
+    __syncthreads();
+    if (ratio > 0.5) break;  // cond <= 2: one CholeskyQR pass is orthogonal to ~eps cond^2
+  }
+  if (chol_ok) {
+    // R_c = Q_c^T N (upper triangular up to rounding; used in full)
+    cta_gemm_dmma(r, r, c, M, c, 1, src.N, 1, src.ldn,
+                  [&](int i, int k, double v) { dst.N[(int64_t)k * dst.ldn + i] = v; });
+  } else {
+    for (int k = wid; k < r; k += nw)
+      for (int i = lane; i < c; i += 32) M[k * c + i] = src.N[(int64_t)k * src.ldn + i];
+    __syncthreads();
+    cta_householder_qr(M, c, c, r, dst.N, dst.ldn, pp.work, pp.work + P.work_stride, red);
+  }
+  __syncthreads();
   const double* Lib = src.Li + (int64_t)h.base * (src.ldl + 1);
   cta_gemm_dmma(c, r, c, Lib, src.ldl, 1, M, 1, c, [&](int a, int k, double v) { pp.T[(int64_t)k * P.ccap + a] = v; });
   for (int k = threadIdx.x; k < r; k += blockDim.x) dst.sigma[k] = src.sigma[k];
@@ -956,20 +988,23 @@ __global__ void __launch_bounds__(kSmallThreads) k_compact_prep(StateView src, S
   }
 }
 
-// After the compaction Gram: N_new = L_new^T R_c (R_c parked in dst.N; base 0).
+// After the compaction Gram: N_new = L_new^T R_c (R_c parked in dst.N; base 0;
+// R_c is used in full -- CholeskyQR's R_c = Q_c^T N is triangular only up to rounding).
 __global__ void __launch_bounds__(256) k_compact_finish(StateView dst, double* tmp, int ldt) {
   const int r = dst.hdr->r;
   if (dst.hdr->status != 0 || r == 0) return;
-  for (int k = 0; k < r; ++k)
-    for (int i = threadIdx.x; i <= k; i += blockDim.x) {
-      const double* lcol = dst.L + (int64_t)i * dst.ldl;  // column i of L = row i of L^T
-      double s = 0.0;
-      for (int j = i; j <= k; ++j) s = fma(lcol[j], dst.N[(int64_t)k * dst.ldn + j], s);
-      tmp[(int64_t)k * ldt + i] = s;
-    }
+  for (int idx = threadIdx.x; idx < r * r; idx += blockDim.x) {
+    const int i = idx % r, k = idx / r;
+    const double* lcol = dst.L + (int64_t)i * dst.ldl;  // column i of L = row i of L^T
+    double s = 0.0;
+    for (int j = i; j < r; ++j) s = fma(lcol[j], dst.N[(int64_t)k * dst.ldn + j], s);
+    tmp[(int64_t)k * ldt + i] = s;
+  }
   __syncthreads();
-  for (int k = 0; k < r; ++k)
-    for (int i = threadIdx.x; i < r; i += blockDim.x) dst.N[(int64_t)k * dst.ldn + i] = (i <= k) ? tmp[(int64_t)k * ldt + i] : 0.0;
+  for (int idx = threadIdx.x; idx < r * r; idx += blockDim.x) {
+    const int i = idx % r, k = idx / r;
+    dst.N[(int64_t)k * dst.ldn + i] = tmp[(int64_t)k * ldt + i];
+  }
 }
 
 // U-coordinates W = L^{-T} N (c x r, ld c) for the export / materialisation.

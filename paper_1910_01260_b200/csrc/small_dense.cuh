@@ -341,34 +341,42 @@ __device__ inline void cta_gemm_dmma(int M, int N, int K, const double* A, int64
 // upper triangle.
 // ---------------------------------------------------------------------------
 __device__ inline double cta_cholesky(double* B, int ld, int n, double* /*unused*/) {
-  // left-looking: column j gathers the updates of columns < j (one barrier
-  // pair per column, no trailing-matrix traffic)
+  // right-looking with ONE barrier per column: column j's rank-1 update uses the
+  // unscaled column (B(i,j) B(k,j) / B(j,j)), and column j is scaled in the
+  // next column's phase, when nobody reads it any more
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   double pmin = INFINITY, pmax = 0.0;
+  double prev_inv = 0.0;
   for (int j = 0; j < n; ++j) {
-    for (int i = j + threadIdx.x; i < n; i += blockDim.x) {
-      double s = B[j * ld + i];
-      for (int k = 0; k < j; ++k) s = fma(-B[k * ld + i], B[k * ld + j], s);
-      B[j * ld + i] = s;
-    }
-    __syncthreads();
-    const double d2 = B[j * ld + j];
+    __syncthreads();  // column j is final (updated by all earlier columns)
+    const double* cj = B + j * ld;
+    const double d2 = cj[j];
     if (!(d2 > 0.0)) {
       __syncthreads();
       return -1.0;
     }
-    const double d = sqrt(d2);
-    pmin = fmin(pmin, d);
-    pmax = fmax(pmax, d);
-    __syncthreads();
-    const double inv = 1.0 / d;
-    for (int i = j + threadIdx.x; i < n; i += blockDim.x) B[j * ld + i] = (i == j) ? d : B[j * ld + i] * inv;
-    __syncthreads();
+    const double rd2 = 1.0 / d2;
+    const double inv = rsqrt(d2);
+    pmin = fmin(pmin, d2 * inv);
+    pmax = fmax(pmax, d2 * inv);
+    if (j > 0) {  // scale the previous column (nobody reads it in this phase)
+      double* cp = B + (j - 1) * ld;
+      for (int i = j - 1 + threadIdx.x; i < n; i += blockDim.x) cp[i] = (i == j - 1) ? 1.0 / prev_inv : cp[i] * prev_inv;
+    }
+    for (int k = j + 1 + wid; k < n; k += nw) {
+      const double ck = cj[k] * rd2;
+      double* colk = B + k * ld;
+      for (int i = k + lane; i < n; i += 32) colk[i] = fma(-cj[i], ck, colk[i]);
+    }
+    prev_inv = inv;
   }
-  {
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int k = wid; k < n; k += nw)
-      for (int i = lane; i < k; i += 32) B[k * ld + i] = 0.0;
+  __syncthreads();
+  if (n > 0) {
+    double* cp = B + (n - 1) * ld;
+    if (threadIdx.x == 0) cp[n - 1] = 1.0 / prev_inv;
   }
+  for (int k = wid; k < n; k += nw)
+    for (int i = lane; i < k; i += 32) B[k * ld + i] = 0.0;
   __syncthreads();
   return pmin / pmax;
 }
@@ -378,13 +386,22 @@ __device__ inline double cta_cholesky(double* B, int ld, int n, double* /*unused
 // i.e. X_new R = X with R = L^T upper: forward substitution along each row,
 // one thread per row.  The caller synchronises afterwards.
 // ---------------------------------------------------------------------------
-__device__ inline void cta_rows_times_inv_lt(double* X, int ldx, int rows, const double* L, int ldl, int n) {
+__device__ inline void cta_rows_times_inv_lt(double* X, int ldx, int rows, const double* L, int ldl, int n,
+                                             const double* dinv) {
+  // dinv[k] = 1 / L(k, k) (precomputed: no division on the dependency chain)
   for (int a = threadIdx.x; a < rows; a += blockDim.x) {
     for (int k = 0; k < n; ++k) {
-      double s = X[(int64_t)k * ldx + a];
       const double* lrow = L + k;  // L(k, j) = L[j * ldl + k]
-      for (int j = 0; j < k; ++j) s = fma(-X[(int64_t)j * ldx + a], lrow[(int64_t)j * ldl], s);
-      X[(int64_t)k * ldx + a] = s / L[(int64_t)k * ldl + k];
+      double s0 = X[(int64_t)k * ldx + a], s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int j = 0;
+      for (; j + 3 < k; j += 4) {
+        s0 = fma(-X[(int64_t)j * ldx + a], lrow[(int64_t)j * ldl], s0);
+        s1 = fma(-X[(int64_t)(j + 1) * ldx + a], lrow[(int64_t)(j + 1) * ldl], s1);
+        s2 = fma(-X[(int64_t)(j + 2) * ldx + a], lrow[(int64_t)(j + 2) * ldl], s2);
+        s3 = fma(-X[(int64_t)(j + 3) * ldx + a], lrow[(int64_t)(j + 3) * ldl], s3);
+      }
+      for (; j < k; ++j) s0 = fma(-X[(int64_t)j * ldx + a], lrow[(int64_t)j * ldl], s0);
+      X[(int64_t)k * ldx + a] = ((s0 + s1) + (s2 + s3)) * dinv[k];
     }
   }
 }
@@ -503,8 +520,12 @@ __device__ inline void cta_lower_t_mv(const double* Li, int ld, int n, const dou
 
 // Li = L^{-1} for a lower-triangular L (n x n): one warp per column of the
 // inverse, lanes hold the right-hand side; n <= 256.
-__device__ inline void cta_lower_inverse(const double* L, int ld, int n, double* Li, int ldi) {
-  constexpr int Q = 8;
+template <int Q>
+__device__ inline void cta_lower_inverse_q(const double* L, int ld, int n, double* Li, int ldi) {
+  // warp per column of the inverse: forward substitution L x = e_j with the
+  // right-hand side distributed over the lanes (rows lane + 32 q); the
+  // reciprocal pivots are taken from Li's diagonal (precomputed below), so the
+  // serial chain per step is one shuffle and one multiply
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int j = wid; j < n; j += nw) {
     double x[Q];
@@ -516,20 +537,32 @@ __device__ inline void cta_lower_inverse(const double* L, int ld, int n, double*
 #pragma unroll
       for (int q = 0; q < Q; ++q)
         if (q == slot) xk = x[q];
-      xk = __shfl_sync(0xffffffffu, xk, owner) / L[(int64_t)k * ld + k];
+      xk = __shfl_sync(0xffffffffu, xk, owner) * Li[(int64_t)k * ldi + k];
+      const double* lk = L + (int64_t)k * ld;
 #pragma unroll
       for (int q = 0; q < Q; ++q) {
         const int i = lane + 32 * q;
         if (i == k) x[q] = xk;
-        else if (i > k && i < n) x[q] = fma(-L[(int64_t)k * ld + i], xk, x[q]);
+        else if (i > k && i < n) x[q] = fma(-lk[i], xk, x[q]);
       }
     }
+    __syncwarp();
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       const int i = lane + 32 * q;
-      if (i < n) Li[(int64_t)j * ldi + i] = (i >= j) ? x[q] : 0.0;
+      if (i < n && i != j) Li[(int64_t)j * ldi + i] = (i > j) ? x[q] : 0.0;
     }
   }
+}
+
+// Li = L^{-1} for a lower-triangular L (n x n), n <= 256.  Li must not alias L.
+__device__ inline void cta_lower_inverse(const double* L, int ld, int n, double* Li, int ldi) {
+  for (int k = threadIdx.x; k < n; k += blockDim.x) Li[(int64_t)k * ldi + k] = 1.0 / L[(int64_t)k * ld + k];
+  __syncthreads();
+  if (n <= 32) cta_lower_inverse_q<1>(L, ld, n, Li, ldi);
+  else if (n <= 64) cta_lower_inverse_q<2>(L, ld, n, Li, ldi);
+  else if (n <= 128) cta_lower_inverse_q<4>(L, ld, n, Li, ldi);
+  else cta_lower_inverse_q<8>(L, ld, n, Li, ldi);
 }
 
 }  // namespace strom

@@ -20,5 +20,8 @@ for j in range(100, 130):
     print('   core phases', ' '.join(f'{(cp[k+1]-cp[k])/1.965e3:.1f}' for k in range(7)), '(defl roots GE vec rot sort sign)')
     its = t[8:8 + inf.rank + 1]
     print('   iters max', max(its), 'mean', sum(its) / len(its), 'n>=99', sum(1 for v in its if v >= 99))
+    q = t[280:292]
+    if q[5] > 0:
+        print('   qr phases', ' '.join(f'{(q[k+1]-q[k])/1.965e3:.1f}' for k in range(11)), '(gram chol inv gemm copy | ...)')
     print('upd', j, 'flags', inf.flags, 'c', inf.ncols_u, ' '.join(f'{n}={v:.1f}us' for n, v in zip(names, d) if v > 0))
 _capi.lib.strom_debug_tprobe(None)
