@@ -270,7 +270,7 @@ PipeMem make_pipe(const Caps& c, cudaStream_t s) {
                             (size_t)c.ccap * rc2;  // step B's layout (global fallback)
   const size_t nv = round_up(c.ccap + 2, 4), nell = round_up(rc2, 4);
   const size_t n_part = (size_t)m.max_grid * m.pstride;
-  size_t total = 2 * nell + 2 * nv + 6 * nv + 2 * (2 * nv + 8) + rc2 * rc2 + work_elems + (size_t)c.ccap * rc2 + n_part;
+  size_t total = 2 * nell + 2 * nv + 7 * nv + 2 * (2 * nv + 8) + rc2 * rc2 + work_elems + (size_t)c.ccap * rc2 + n_part;
   total = round_up(total, 32);
   const size_t bytes = total * 8 + 512;
   m.mem = dev_alloc(bytes, s, true);
@@ -283,6 +283,7 @@ PipeMem make_pipe(const Caps& c, cudaStream_t s) {
   m.pp.l1 = p; p += nv;
   m.pp.h = p; p += nv;
   m.pp.tmp = p; p += nv;
+  m.pp.w = p; p += nv;
   m.pp.fo.e = p; p += nv;
   m.pp.fo.gn = p; p += nv;
   m.pp.fo.scal = p; p += 8;
@@ -364,7 +365,9 @@ template <int MAXJ>
 void launch_pass_t(const PassArgs& a, int cols_ub, int reserve, int kind_prof, cudaStream_t s) {
   const int cols = std::max(cols_ub, 1);
   const int nst = pass_stages(cols);
-  const size_t smem = (size_t)nst * kStageRows * (cols + 2) * 8;  // + x and x_next segments
+  // stages (+ x and x_next segments); the decision tail reuses them as its workspace
+  const size_t smem = std::max((size_t)nst * kStageRows * (cols + 2) * 8,
+                               (size_t)2 * (kPassThreads / 32) * round_up(a.ccap, 32) * 8);
   static size_t cfg = 0;
   set_smem_attr(k_pass<MAXJ>, smem, &cfg);
   const int64_t ntiles = a.ldu / kStageRows;
@@ -385,9 +388,16 @@ void launch_pass_t(const PassArgs& a, int cols_ub, int reserve, int kind_prof, c
   }
 }
 
-// kind PASS_*; cols_ub bounds the U columns the pass may read
+// kind PASS_*; cols_ub bounds the U columns the pass may read.  tail: the
+// decision run by the last CTA (1 decide after FUSED, 2 decide2 after SECOND)
+struct PassTail {
+  int32_t tail = 0, b_expect = -1;
+  const StateView* src = nullptr;
+  const IsvdParams* P = nullptr;
+};
+
 void launch_pass(int kind, int cols_ub, const strom_isvd* h, const PipeMem& m, const double* x, const double* xn,
-                 int reserve, cudaStream_t s) {
+                 int reserve, cudaStream_t s, const PassTail& tl = PassTail()) {
   PassArgs a;
   a.U = h->store->U();
   a.ldu = h->ldu;
@@ -415,6 +425,11 @@ void launch_pass(int kind, int cols_ub, const strom_isvd* h, const PipeMem& m, c
   a.part = m.pp.part;
   a.counter = m.pp.counter;
   a.prof = prof_dev_bytes();
+  a.tail = tl.tail;
+  a.b_expect = tl.b_expect;
+  a.dpp = m.pp;
+  if (tl.src) a.dsrc = *tl.src;
+  if (tl.P) a.dP = *tl.P;
   const int pk = (kind == PASS_SECOND) ? P_RESID : P_PROJ;
   const int cu = std::max(cols_ub, 1);
   switch (pass_maxj(cu)) {
@@ -429,7 +444,7 @@ void launch_pass(int kind, int cols_ub, const strom_isvd* h, const PipeMem& m, c
   }
 }
 
-size_t decide_smem(const PipeMem& m) { return (size_t)(kDecideThreads / 32) * round_up(m.ccap, 32) * 8; }
+size_t decide_smem(const PipeMem& m) { return (size_t)2 * (kDecideThreads / 32) * round_up(m.ccap, 32) * 8; }
 
 
 void launch_prep(const PipeMem& m, const IsvdParams& P, cudaStream_t s) {
@@ -441,22 +456,29 @@ void launch_prep(const PipeMem& m, const IsvdParams& P, cudaStream_t s) {
   STROM_LAUNCH_CHECK();
 }
 
-void launch_decide(const StateView& src, const PipeMem& m, const IsvdParams& P, cudaStream_t s) {
-  static size_t cfg = 0;
+void launch_decide_kernel(bool second, const StateView& src, const PipeMem& m, const IsvdParams& P,
+                          cudaStream_t s) {
+  static size_t cfg1 = 0, cfg2 = 0;
   const size_t smem = decide_smem(m);
-  set_smem_attr(k_decide, smem, &cfg);
   ProfScope ps(P_STEP_A, s);
-  k_decide<<<1, kDecideThreads, smem, s>>>(src, m.pp, P);
+  if (!second) {
+    set_smem_attr(k_decide, smem, &cfg1);
+    k_decide<<<1, kDecideThreads, smem, s>>>(src, m.pp, P);
+  } else {
+    set_smem_attr(k_decide2, smem, &cfg2);
+    k_decide2<<<1, kDecideThreads, smem, s>>>(src, m.pp, P);
+  }
   STROM_LAUNCH_CHECK();
 }
 
-void launch_decide2(const StateView& src, const PipeMem& m, const IsvdParams& P, cudaStream_t s) {
-  static size_t cfg = 0;
-  const size_t smem = decide_smem(m);
-  set_smem_attr(k_decide2, smem, &cfg);
-  ProfScope ps(P_STEP_A, s);
-  k_decide2<<<1, kDecideThreads, smem, s>>>(src, m.pp, P);
-  STROM_LAUNCH_CHECK();
+// The decisions as their own 512-thread kernels (default; measured faster than
+// running them in the pass's last CTA, STROM_DECIDE_TAIL=1, at cfg2).
+bool decide_as_kernel() {
+  static const bool v = [] {
+    const char* e = getenv("STROM_DECIDE_TAIL");
+    return !(e && atoi(e) != 0);
+  }();
+  return v;
 }
 
 size_t small_kernel_smem(const Caps& c, int* use_smem) {
@@ -676,14 +698,17 @@ strom_isvd* update_once(strom_isvd* src, const double* x, cudaStream_t s, bool i
   trace_point("proj", s);
   launch_prep(m, P, s);
   trace_point("prep", s);
-  launch_pass(PASS_FUSED, cols, dst, m, x, nullptr, 0, s);
-  trace_point("fused", s);
-  launch_decide(cur->view, m, P, s);
-  trace_point("decide", s);
-  launch_pass(PASS_SECOND, cols, dst, m, x, nullptr, 0, s);
-  trace_point("second", s);
-  launch_decide2(cur->view, m, P, s);
-  trace_point("decide2", s);
+  {
+    PassTail tl;
+    tl.tail = 1;  // decide (basis.py:112-139) in the pass's last CTA
+    tl.src = &cur->view;
+    tl.P = &P;
+    launch_pass(PASS_FUSED, cols, dst, m, x, nullptr, 0, s, tl);
+    trace_point("fused+decide", s);
+    tl.tail = 2;  // re-orthogonalisation / restart copy, only when requested
+    launch_pass(PASS_SECOND, cols, dst, m, x, nullptr, 0, s, tl);
+    trace_point("second+decide2", s);
+  }
   launch_step_b(cur->view, dst->view, m, P, cur->caps, s);
   trace_point("step_b", s);
   launch_vupdate(cur->view, dst->view, m, P, cur->caps.rcap, s);
@@ -790,6 +815,7 @@ strom_isvd* ingest_pipelined(strom_isvd* src, ColumnSource& cols, cudaStream_t s
   const int64_t kfinal = src->k + ncols;
   PipeMem m;
   bool need_prep = true;
+  int64_t b_launched = 0;  // core steps queued on s2 since the last k_init_ctl
   auto join = [&]() {  // s waits for all of s2
     STROM_CUDA(cudaEventRecord(evV, s2));
     STROM_CUDA(cudaStreamWaitEvent(s, evV, 0));
@@ -849,21 +875,34 @@ strom_isvd* ingest_pipelined(strom_isvd* src, ColumnSource& cols, cudaStream_t s
     const double* xn = cols.col(t + 1);
     if (need_prep) {
       if (t > 0) STROM_CUDA(cudaStreamWaitEvent(s, evB, 0));  // prev's header comes from s2
-      k_init_ctl<<<1, 1, 0, s>>>(m.pp.ctl, prev->view.hdr);
+      k_init_ctl<<<1, 1, 0, s>>>(m.pp.ctl, prev->view.hdr);    // also resets the B counter
       STROM_LAUNCH_CHECK();
+      b_launched = 0;
       launch_pass(PASS_PROJ, cols_ub, dst, m, nullptr, xt, 0, s);
       launch_prep(m, P, s);
       need_prep = false;
     }
-    launch_pass(PASS_FUSED, cols_ub, dst, m, xt, (dbg & 2) ? nullptr : xn, 1, s);
-    if (t > 0) STROM_CUDA(cudaStreamWaitEvent(s, evB, 0));  // D(t) reads the state B(t-1) wrote
-    launch_decide(prev->view, m, P, s);
-    launch_pass(PASS_SECOND, cols_ub, dst, m, xt, xn, 1, s);
-    launch_decide2(prev->view, m, P, s);
+    if (decide_as_kernel()) {
+      launch_pass(PASS_FUSED, cols_ub, dst, m, xt, (dbg & 2) ? nullptr : xn, 1, s);
+      if (t > 0) STROM_CUDA(cudaStreamWaitEvent(s, evB, 0));
+      launch_decide_kernel(false, prev->view, m, P, s);
+      launch_pass(PASS_SECOND, cols_ub, dst, m, xt, xn, 1, s);
+      launch_decide_kernel(true, prev->view, m, P, s);
+    } else {
+      PassTail tl;
+      tl.tail = 1;
+      tl.b_expect = (int32_t)b_launched;  // D(t) needs B(t-1): the pass's last CTA waits for it
+      tl.src = &prev->view;
+      tl.P = &P;
+      launch_pass(PASS_FUSED, cols_ub, dst, m, xt, (dbg & 2) ? nullptr : xn, 1, s, tl);
+      tl.tail = 2;
+      launch_pass(PASS_SECOND, cols_ub, dst, m, xt, xn, 1, s, tl);
+    }
     cols.release(t);
     STROM_CUDA(cudaEventRecord(evD, s));
     STROM_CUDA(cudaStreamWaitEvent(s2, evD, 0));
     launch_step_b(prev->view, dst->view, m, P, prev->caps, s2);
+    ++b_launched;
     STROM_CUDA(cudaEventRecord(evB, s2));
     launch_vupdate(prev->view, dst->view, m, P, prev->caps.rcap, s2);
     dst->c_ub = prev->c_ub + 1;

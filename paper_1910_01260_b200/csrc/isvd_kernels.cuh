@@ -54,7 +54,7 @@ enum : int32_t { M_NORMAL_DEP = 0, M_NORMAL_INDEP = 1, M_RESTART_ACCEPT = 2, M_R
 struct PipeCtl {
   int32_t c, base;
   int32_t reorth;  // 0 none, 1 DGKS pass requested, 2 restart copy requested
-  int32_t pad;
+  int32_t bdone;   // core steps (k_step_b) completed since the sequence started
   double xx;       // x.x of the snapshot about to be decided
 };
 
@@ -85,7 +85,8 @@ struct Pipe {
   double* y;       // tvec - N ell
   double* l1;      // L^{-1} e of the first residual
   double* h;       // DGKS coefficients G^{-1} e, later l2
-  double* tmp;     // c_cap scratch
+  double* tmp;     // c_cap scratch (L^{-1} g' of the next snapshot)
+  double* w;       // c_cap scratch (L^{-T} l of an appended column)
   PassOut fo;      // the fused pass
   PassOut ro;      // the second (re-orthogonalisation / restart) pass
   double* vbar;    // (r_cap+2)^2 sorted, sign-fixed V_bar of the core
@@ -176,6 +177,12 @@ struct PassArgs {
   int64_t ccap;
   int32_t dbg;  // diagnostics: 1 = consumers only wait/release (bandwidth probe)
   int32_t x_bulk, xn_bulk;  // x / xn may be staged by bulk copy (16-byte aligned, n even)
+  // decision tail run by the last-arriving CTA: 0 none, 1 decide (FUSED), 2 decide2 (SECOND)
+  int32_t tail;
+  int32_t b_expect;  // decide waits until ctl->bdone >= b_expect (-1: no wait)
+  StateView dsrc;
+  Pipe dpp;
+  IsvdParams dP;
   const PipeCtl* ctl;
   int32_t kind;
   int32_t pstride;
@@ -229,9 +236,287 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // partials through a double-buffered shared array with ONE consumer-only named
 // barrier per stage.  Column dots stay in registers until a deterministic
 // last-CTA reduction.
+// ---------------------------------------------------------------------------
+// Small-space helpers of the decision kernels
+// ---------------------------------------------------------------------------
+// Bordered extension of G's factors by the appended column (physical row c of
+// the block at (base, base)):  L' = [[L, 0], [l^T, lam]],
+// L'^{-1} = [[L^{-1}, 0], [-(L^{-T} l)^T / lam, 1 / lam]].
+__device__ inline void append_factor_row(double* Lb, double* Lib, int ldl, int c, const double* l, double lam,
+                                         double* tmpv) {
+  cta_gemv_t_cm(Lib, ldl, c, c, l, tmpv, true);  // tmpv = L^{-T} l
+  for (int j = threadIdx.x; j < c; j += blockDim.x) {
+    Lb[(int64_t)j * ldl + c] = l[j];
+    Lib[(int64_t)j * ldl + c] = -tmpv[j] / lam;
+  }
+  if (threadIdx.x == 0) {
+    Lb[(int64_t)c * ldl + c] = lam;
+    Lib[(int64_t)c * ldl + c] = 1.0 / lam;
+  }
+  __syncthreads();
+}
+
+// Coefficients of the next snapshot's residual: tvec = L^{-1} g, gt = L^{-T} tvec.
+__device__ inline void prep_next(const IsvdParams& P, const Pipe& pp, double* part) {
+  __syncthreads();  // ctl may have been written by thread 0 of this CTA
+  const int c = *(volatile const int32_t*)&pp.ctl->c, base = *(volatile const int32_t*)&pp.ctl->base;
+  const double* Lib = P.Li + (int64_t)base * (P.ccap + 1);
+  if (c > 0) {
+    cta_gemv_cm<8>(Lib, P.ccap, c, c, pp.fo.gn, 1.0, nullptr, pp.tvec, part, true);
+    cta_gemv_t_cm(Lib, P.ccap, c, c, pp.tvec, pp.gt, true);
+  }
+  if (threadIdx.x == 0) pp.ctl->xx = pp.fo.scal[1];
+}
+
+// A (first snapshot of a sequence, or after a compaction): prepare from a PROJ pass.
+__global__ void __launch_bounds__(kDecideThreads) k_prep(Pipe pp, IsvdParams P) {
+  extern __shared__ double part[];
+  prep_next(P, pp, part);
+}
+
+// ctl <- the columns of a state (start of a sequence / after a compaction)
+__global__ void k_init_ctl(PipeCtl* ctl, const IsvdHdr* h) {
+  ctl->c = h->c;
+  ctl->base = h->base;
+  ctl->reorth = 0;
+  ctl->bdone = 0;
+}
+
+constexpr double kFoldTau = 1e-3;  // append r1 only if its out-of-span part is >= tau |r1|
+
+// ---------------------------------------------------------------------------
+// D: every decision of update t (basis.py:112-139 and the U bookkeeping):
+//   restart / reject (basis.py:112-133), ell = Phi^T x = N^T L^{-1} g, the
+//   Pythagorean p (basis.py:136-138), the dependent test, and for an
+//   independent snapshot how r1 enters U: l = L^{-1} e, lambda^2 = |r1|^2 -
+//   |l|^2 (its out-of-span part in the G metric); append when lambda >= tau |r1|
+//   (extending L, L^{-1} in the store), else request one DGKS pass (k_decide2
+//   finishes).  Without a follow-up pass it also prepares the next snapshot.
+// ---------------------------------------------------------------------------
+__device__ inline void decide_body(const StateView& src, const Pipe& pp, const IsvdParams& P, double* part,
+                                   double* red) {
+  const IsvdHdr h = *src.hdr;
+  IsvdStep* st = pp.step[P.parity];
+  double* ell = pp.ell[P.parity];
+  double* nj = pp.nj[P.parity];
+  const int c = h.c, base = h.base, r = h.r;
+  const int ldl = P.ccap;
+  double* Lb = P.L + (int64_t)base * (ldl + 1);
+  double* Lib = P.Li + (int64_t)base * (ldl + 1);
+  const double xx = pp.ctl->xx;
+  const double rho2 = pp.fo.scal[0];
+  const int slot = base + c;
+  int mode = -1, restart = 0, action = 0, dep = 0, cn = c, base_new = base, reorth = 0;
+  double p = 0.0, p_sq = 0.0, lam = 0.0;
+  if (h.status != 0 || !isfinite(xx)) {
+    mode = M_ERROR;
+  } else {
+    const bool at_cap = P.r_max >= 0 && h.r >= P.r_max;
+    if (r == 0 || (at_cap && P.cap_mode == 0)) {
+      restart = at_cap ? 1 : 0;
+      if (sqrt(xx) > P.tol_svd) {
+        mode = M_RESTART_ACCEPT;
+        if (c == 0) {  // the pass read no U columns: the slot already holds x
+          lam = sqrt(rho2);
+          cn = 1;
+          base_new = slot;
+        } else {
+          reorth = 2;  // copy x into the slot (second pass), k_decide2 finishes
+        }
+      } else {
+        mode = M_REJECT;
+        cn = 0;
+        base_new = base + c;
+      }
+    }
+  }
+  bool prepped = false;  // coefficients of the next snapshot already written
+  if (mode == -1) {
+    const bool nx = P.has_next != 0;
+    double* t1 = pp.tmp;  // L^{-1} g'[:c]: the next snapshot's coordinates in the current Q_U
+    // phase 1 (independent products): ell = N^T tvec;  [l1, t1] = L^{-1} [e, g'[:c]]
+    cta_gemv_t_cm(src.N, src.ldn, c, r, pp.tvec, ell, false);
+    cta_gemv2_cm<8>(Lib, ldl, c, c, pp.fo.e, nx ? pp.fo.gn : nullptr, pp.l1, nx ? t1 : nullptr, part, true);
+    double s_ll = 0.0, s_l1 = 0.0, s_lt = 0.0;
+    for (int i = threadIdx.x; i < r; i += blockDim.x) s_ll = fma(ell[i], ell[i], s_ll);
+    for (int j = threadIdx.x; j < c; j += blockDim.x) {
+      s_l1 = fma(pp.l1[j], pp.l1[j], s_l1);
+      if (nx) s_lt = fma(pp.l1[j], t1[j], s_lt);
+    }
+    block_sum3(s_ll, s_l1, s_lt, red);
+    p_sq = xx - s_ll;  // the Pythagorean residual (basis.py:136-138)
+    p = (p_sq > 0.0) ? sqrt(p_sq) : 0.0;
+    dep = (p < P.tol_svd) || (p == 0.0) || ((int64_t)r >= P.n);
+    mode = dep ? M_NORMAL_DEP : M_NORMAL_INDEP;
+    if (!dep) {
+      const double lam2 = rho2 - s_l1;  // out-of-span part of r1 in the G metric
+      const bool room = (slot < P.ccap) && ((int64_t)c < P.n);
+      const bool app = room && (lam2 > kFoldTau * kFoldTau * rho2) && (rho2 > 0.0);
+      if (app) {
+        lam = sqrt(lam2);
+        // next snapshot in the extended basis: tvec'_c = (g'_c - l1.t1) / lam and
+        // gt'[:c] = L^{-T} (t1 - l1 tvec'_c / lam), gt'_c = tvec'_c / lam
+        const double tc = nx ? (pp.fo.gn[c] - s_lt) / lam : 0.0;
+        if (nx)
+          for (int j = threadIdx.x; j < c; j += blockDim.x) pp.h[j] = t1[j] - pp.l1[j] * (tc / lam);
+        cta_gemv_cm<8>(src.N, src.ldn, c, r, ell, -1.0, pp.tvec, pp.y, part, false);  // y = tvec - N ell
+        // phase 2: [w, u] = L^{-T} [l1, h]  (w for the new row of L^{-1}, u = gt'[:c])
+        cta_gemv2_t_cm(Lib, ldl, c, c, pp.l1, nx ? pp.h : pp.l1, pp.w, pp.gt, true);
+        for (int j = threadIdx.x; j < c; j += blockDim.x) {
+          Lb[(int64_t)j * ldl + c] = pp.l1[j];
+          Lib[(int64_t)j * ldl + c] = -pp.w[j] / lam;
+        }
+        for (int a = threadIdx.x; a <= c; a += blockDim.x) {
+          nj[a] = (a < c) ? (pp.y[a] + pp.l1[a]) / p : lam / p;
+          if (nx) pp.tvec[a] = (a < c) ? t1[a] : tc;
+        }
+        if (threadIdx.x == 0) {
+          Lb[(int64_t)c * ldl + c] = lam;
+          Lib[(int64_t)c * ldl + c] = 1.0 / lam;
+          if (nx) pp.gt[c] = tc / lam;
+        }
+        prepped = nx;
+        cn = c + 1;
+        action = 1;
+      } else if (room) {
+        reorth = 1;
+        cta_gemv_cm<8>(src.N, src.ldn, c, r, ell, -1.0, pp.tvec, pp.y, part, false);
+        cta_gemv_t_cm(Lib, ldl, c, c, pp.l1, pp.h, true);  // h = L^{-T} l1 = G^{-1} e
+      } else if (c >= r + 1) {
+        cta_gemv_cm<8>(src.N, src.ldn, c, r, ell, -1.0, pp.tvec, pp.y, part, false);
+        for (int a = threadIdx.x; a < c; a += blockDim.x) nj[a] = (pp.y[a] + pp.l1[a]) / p;
+        action = 2;
+      } else {
+        dep = 1;
+      }
+    }
+    if ((dep || action == 2) && nx) {  // U unchanged: tvec' = t1, gt' = L^{-T} t1
+      __syncthreads();
+      for (int j = threadIdx.x; j < c; j += blockDim.x) pp.tvec[j] = t1[j];
+      cta_gemv_t_cm(Lib, ldl, c, c, t1, pp.gt, true);
+      prepped = true;
+    }
+    __syncthreads();
+  }
+  if (mode == M_RESTART_ACCEPT && reorth == 0 && threadIdx.x == 0) {
+    P.L[(int64_t)slot * (ldl + 1)] = lam;
+    P.Li[(int64_t)slot * (ldl + 1)] = 1.0 / lam;
+  }
+  if (threadIdx.x == 0) {
+    st->mode = mode;
+    st->restart = restart;
+    st->action = action;
+    st->dep = (mode == M_NORMAL_DEP) ? 1 : dep;
+    st->c = c;
+    st->cn = cn;
+    st->base_new = base_new;
+    st->slot = slot;
+    st->xx = xx;
+    st->rho2 = rho2;
+    st->p = p;
+    st->p_sq = p_sq;
+    st->norm = sqrt(xx);
+    st->lam = lam;
+    pp.ctl->reorth = reorth;
+    if (reorth == 0) {
+      pp.ctl->c = cn;
+      pp.ctl->base = base_new;
+    }
+  }
+  if (reorth == 0 && P.has_next) {
+    if (prepped) {
+      if (threadIdx.x == 0) pp.ctl->xx = pp.fo.scal[1];
+    } else {
+      prep_next(P, pp, part);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kDecideThreads) k_decide(StateView src, Pipe pp, IsvdParams P) {
+  extern __shared__ double part[];  // 2 * nw * c_cap
+  __shared__ double red[96];
+  decide_body(src, pp, P, part, red);
+}
+
+// ---------------------------------------------------------------------------
+// D2: after the second pass.  DGKS: l2 = L^{-1} e2, lambda2^2 = |r2|^2 - |l2|^2;
+// append r2 whenever it carries a genuine out-of-span direction (the reference
+// appends j = (x - Phi ell)/p even when it is rounding noise, basis.py:155-156),
+// else fold it back (U keeps a spare direction) or demote the update to
+// dependent.  Restart copy: the new one-column state.
+// ---------------------------------------------------------------------------
+__device__ inline void decide2_body(const StateView& src, const Pipe& pp, const IsvdParams& P, double* part,
+                                    double* red) {
+  const int ro = pp.ctl->reorth;
+  if (ro == 0) return;
+  IsvdStep* st = pp.step[P.parity];
+  double* nj = pp.nj[P.parity];
+  const int c = st->c, slot = st->slot, r = src.hdr->r, base = src.hdr->base;
+  const int ldl = P.ccap;
+  double* Lb = P.L + (int64_t)base * (ldl + 1);
+  double* Lib = P.Li + (int64_t)base * (ldl + 1);
+  __syncthreads();
+  int cn = c, action = 0, dep = 0, base_new = base;
+  double lam = 0.0;
+  if (ro == 1) {
+    const double p = st->p;
+    double* l2 = pp.h;  // h is spent
+    cta_gemv_cm<8>(Lib, ldl, c, c, pp.ro.e, 1.0, nullptr, l2, part, true);
+    double pq = 0.0;
+    for (int j = threadIdx.x; j < c; j += blockDim.x) pq = fma(l2[j], l2[j], pq);
+    const double ll2 = block_sum(pq, red);
+    const double rho2b = pp.ro.scal[0];
+    const double lam2 = rho2b - ll2;
+    if ((lam2 > 0.25 * rho2b) && (rho2b > 0.0)) {
+      lam = sqrt(lam2);
+      append_factor_row(Lb, Lib, ldl, c, l2, lam, pp.tmp);
+      for (int a = threadIdx.x; a <= c; a += blockDim.x)
+        nj[a] = (a < c) ? (pp.y[a] + pp.l1[a] + l2[a]) / p : lam / p;
+      if (threadIdx.x == 0) pp.fo.gn[c] = pp.ro.scal[2];  // r2 . x_next
+      cn = c + 1;
+      action = 1;
+    } else if (c >= r + 1) {
+      for (int a = threadIdx.x; a < c; a += blockDim.x) nj[a] = (pp.y[a] + pp.l1[a] + l2[a]) / p;
+      action = 2;
+    } else {
+      dep = 1;
+    }
+  } else {
+    lam = sqrt(pp.ro.scal[0]);
+    if (threadIdx.x == 0) {
+      P.L[(int64_t)slot * (ldl + 1)] = lam;
+      P.Li[(int64_t)slot * (ldl + 1)] = 1.0 / lam;
+      pp.fo.gn[0] = pp.ro.scal[2];  // x . x_next
+      st->rho2 = pp.ro.scal[0];
+    }
+    cn = 1;
+    base_new = slot;
+  }
+  if (threadIdx.x == 0) {
+    if (ro == 1) {
+      st->action = action;
+      st->dep = dep;
+    }
+    st->cn = cn;
+    st->base_new = base_new;
+    st->lam = lam;
+    pp.ctl->c = cn;
+    pp.ctl->base = base_new;
+    pp.ctl->reorth = 0;
+  }
+  if (P.has_next) prep_next(P, pp, part);
+}
+
+__global__ void __launch_bounds__(kDecideThreads) k_decide2(StateView src, Pipe pp, IsvdParams P) {
+  extern __shared__ double part[];
+  __shared__ double red[96];
+  decide2_body(src, pp, P, part, red);
+}
+
 template <int MAXJ>
 __global__ void __launch_bounds__(kPassThreads, 1) k_pass(PassArgs a, int nstages) {
   extern __shared__ __align__(128) double stg[];  // nstages x (kStageRows x cs), column segments
+  __shared__ double red_s[96];
   __shared__ __align__(8) uint64_t full[kPassMaxStages];
   __shared__ __align__(8) uint64_t empty[kPassMaxStages];
   __shared__ double gts[kPassConsumers * MAXJ];
@@ -457,234 +742,23 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(PassArgs a, int nstage
       }
     }
   }
-}
-
-// ---------------------------------------------------------------------------
-// Small-space helpers of the decision kernels
-// ---------------------------------------------------------------------------
-// Bordered extension of G's factors by the appended column (physical row c of
-// the block at (base, base)):  L' = [[L, 0], [l^T, lam]],
-// L'^{-1} = [[L^{-1}, 0], [-(L^{-T} l)^T / lam, 1 / lam]].
-__device__ inline void append_factor_row(double* Lb, double* Lib, int ldl, int c, const double* l, double lam,
-                                         double* tmpv) {
-  cta_gemv_t_cm(Lib, ldl, c, c, l, tmpv, true);  // tmpv = L^{-T} l
-  for (int j = threadIdx.x; j < c; j += blockDim.x) {
-    Lb[(int64_t)j * ldl + c] = l[j];
-    Lib[(int64_t)j * ldl + c] = -tmpv[j] / lam;
-  }
-  if (threadIdx.x == 0) {
-    Lb[(int64_t)c * ldl + c] = lam;
-    Lib[(int64_t)c * ldl + c] = 1.0 / lam;
-  }
-  __syncthreads();
-}
-
-// Coefficients of the next snapshot's residual: tvec = L^{-1} g, gt = L^{-T} tvec.
-__device__ inline void prep_next(const IsvdParams& P, const Pipe& pp, double* part) {
-  __syncthreads();  // ctl may have been written by thread 0 of this CTA
-  const int c = *(volatile const int32_t*)&pp.ctl->c, base = *(volatile const int32_t*)&pp.ctl->base;
-  const double* Lib = P.Li + (int64_t)base * (P.ccap + 1);
-  if (c > 0) {
-    cta_gemv_cm<8>(Lib, P.ccap, c, c, pp.fo.gn, 1.0, nullptr, pp.tvec, part, true);
-    cta_gemv_t_cm(Lib, P.ccap, c, c, pp.tvec, pp.gt, true);
-  }
-  if (threadIdx.x == 0) pp.ctl->xx = pp.fo.scal[1];
-}
-
-// A (first snapshot of a sequence, or after a compaction): prepare from a PROJ pass.
-__global__ void __launch_bounds__(kDecideThreads) k_prep(Pipe pp, IsvdParams P) {
-  extern __shared__ double part[];
-  prep_next(P, pp, part);
-}
-
-// ctl <- the columns of a state (start of a sequence / after a compaction)
-__global__ void k_init_ctl(PipeCtl* ctl, const IsvdHdr* h) {
-  ctl->c = h->c;
-  ctl->base = h->base;
-  ctl->reorth = 0;
-}
-
-constexpr double kFoldTau = 1e-3;  // append r1 only if its out-of-span part is >= tau |r1|
-
-// ---------------------------------------------------------------------------
-// D: every decision of update t (basis.py:112-139 and the U bookkeeping):
-//   restart / reject (basis.py:112-133), ell = Phi^T x = N^T L^{-1} g, the
-//   Pythagorean p (basis.py:136-138), the dependent test, and for an
-//   independent snapshot how r1 enters U: l = L^{-1} e, lambda^2 = |r1|^2 -
-//   |l|^2 (its out-of-span part in the G metric); append when lambda >= tau |r1|
-//   (extending L, L^{-1} in the store), else request one DGKS pass (k_decide2
-//   finishes).  Without a follow-up pass it also prepares the next snapshot.
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kDecideThreads) k_decide(StateView src, Pipe pp, IsvdParams P) {
-  extern __shared__ double part[];  // nw * c_cap
-  __shared__ double red[32];
-  const IsvdHdr h = *src.hdr;
-  IsvdStep* st = pp.step[P.parity];
-  double* ell = pp.ell[P.parity];
-  double* nj = pp.nj[P.parity];
-  const int c = h.c, base = h.base, r = h.r;
-  const int ldl = P.ccap;
-  double* Lb = P.L + (int64_t)base * (ldl + 1);
-  double* Lib = P.Li + (int64_t)base * (ldl + 1);
-  const double xx = pp.ctl->xx;
-  const double rho2 = pp.fo.scal[0];
-  const int slot = base + c;
-  int mode = -1, restart = 0, action = 0, dep = 0, cn = c, base_new = base, reorth = 0;
-  double p = 0.0, p_sq = 0.0, lam = 0.0;
-  if (h.status != 0 || !isfinite(xx)) {
-    mode = M_ERROR;
-  } else {
-    const bool at_cap = P.r_max >= 0 && h.r >= P.r_max;
-    if (r == 0 || (at_cap && P.cap_mode == 0)) {
-      restart = at_cap ? 1 : 0;
-      if (sqrt(xx) > P.tol_svd) {
-        mode = M_RESTART_ACCEPT;
-        if (c == 0) {  // the pass read no U columns: the slot already holds x
-          lam = sqrt(rho2);
-          cn = 1;
-          base_new = slot;
-        } else {
-          reorth = 2;  // copy x into the slot (second pass), k_decide2 finishes
-        }
-      } else {
-        mode = M_REJECT;
-        cn = 0;
-        base_new = base + c;
+  if (a.tail) {
+    __syncthreads();  // this CTA's outputs are complete
+    if (a.tail == 1 && a.b_expect >= 0) {
+      // the core step of the previous snapshot (second stream, its own SM) writes
+      // the state this decision reads; it signals completion on ctl->bdone
+      if (threadIdx.x == 0) {
+        const volatile int32_t* bd = &a.dpp.ctl->bdone;
+        while (*bd < a.b_expect) __nanosleep(100);
+        __threadfence();
       }
+      __syncthreads();
     }
+    if (a.tail == 1) decide_body(a.dsrc, a.dpp, a.dP, stg, red_s);
+    else decide2_body(a.dsrc, a.dpp, a.dP, stg, red_s);
   }
-  if (mode == -1) {
-    cta_gemv_t_cm(src.N, src.ldn, c, r, pp.tvec, ell, false);  // ell = N^T tvec
-    double pl = 0.0;
-    for (int i = threadIdx.x; i < r; i += blockDim.x) pl = fma(ell[i], ell[i], pl);
-    const double ll = block_sum(pl, red);
-    p_sq = xx - ll;
-    p = (p_sq > 0.0) ? sqrt(p_sq) : 0.0;
-    dep = (p < P.tol_svd) || (p == 0.0) || ((int64_t)r >= P.n);
-    mode = dep ? M_NORMAL_DEP : M_NORMAL_INDEP;
-    if (!dep) {
-      cta_gemv_cm<8>(src.N, src.ldn, c, r, ell, -1.0, pp.tvec, pp.y, part, false);  // y = tvec - N ell
-      cta_gemv_cm<8>(Lib, ldl, c, c, pp.fo.e, 1.0, nullptr, pp.l1, part, true);      // l1 = L^{-1} e
-      double pq = 0.0;
-      for (int j = threadIdx.x; j < c; j += blockDim.x) pq = fma(pp.l1[j], pp.l1[j], pq);
-      const double ll1 = block_sum(pq, red);
-      const double lam2 = rho2 - ll1;
-      const bool room = (slot < P.ccap) && ((int64_t)c < P.n);
-      const bool app = room && (lam2 > kFoldTau * kFoldTau * rho2) && (rho2 > 0.0);
-      if (app) {
-        lam = sqrt(lam2);
-        append_factor_row(Lb, Lib, ldl, c, pp.l1, lam, pp.tmp);
-        for (int a = threadIdx.x; a <= c; a += blockDim.x) nj[a] = (a < c) ? (pp.y[a] + pp.l1[a]) / p : lam / p;
-        cn = c + 1;
-        action = 1;
-      } else if (room) {
-        reorth = 1;
-        cta_gemv_t_cm(Lib, ldl, c, c, pp.l1, pp.h, true);  // h = L^{-T} l1 = G^{-1} e
-      } else if (c >= r + 1) {
-        for (int a = threadIdx.x; a < c; a += blockDim.x) nj[a] = (pp.y[a] + pp.l1[a]) / p;
-        action = 2;
-      } else {
-        dep = 1;
-      }
-    }
-  }
-  if (mode == M_RESTART_ACCEPT && reorth == 0 && threadIdx.x == 0) {
-    P.L[(int64_t)slot * (ldl + 1)] = lam;
-    P.Li[(int64_t)slot * (ldl + 1)] = 1.0 / lam;
-  }
-  if (threadIdx.x == 0) {
-    st->mode = mode;
-    st->restart = restart;
-    st->action = action;
-    st->dep = (mode == M_NORMAL_DEP) ? 1 : dep;
-    st->c = c;
-    st->cn = cn;
-    st->base_new = base_new;
-    st->slot = slot;
-    st->xx = xx;
-    st->rho2 = rho2;
-    st->p = p;
-    st->p_sq = p_sq;
-    st->norm = sqrt(xx);
-    st->lam = lam;
-    pp.ctl->reorth = reorth;
-    if (reorth == 0) {
-      pp.ctl->c = cn;
-      pp.ctl->base = base_new;
-    }
-  }
-  if (reorth == 0 && P.has_next) prep_next(P, pp, part);
 }
 
-// ---------------------------------------------------------------------------
-// D2: after the second pass.  DGKS: l2 = L^{-1} e2, lambda2^2 = |r2|^2 - |l2|^2;
-// append r2 whenever it carries a genuine out-of-span direction (the reference
-// appends j = (x - Phi ell)/p even when it is rounding noise, basis.py:155-156),
-// else fold it back (U keeps a spare direction) or demote the update to
-// dependent.  Restart copy: the new one-column state.
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kDecideThreads) k_decide2(StateView src, Pipe pp, IsvdParams P) {
-  extern __shared__ double part[];
-  __shared__ double red[32];
-  const int ro = pp.ctl->reorth;
-  if (ro == 0) return;
-  IsvdStep* st = pp.step[P.parity];
-  double* nj = pp.nj[P.parity];
-  const int c = st->c, slot = st->slot, r = src.hdr->r, base = src.hdr->base;
-  const int ldl = P.ccap;
-  double* Lb = P.L + (int64_t)base * (ldl + 1);
-  double* Lib = P.Li + (int64_t)base * (ldl + 1);
-  __syncthreads();
-  int cn = c, action = 0, dep = 0, base_new = base;
-  double lam = 0.0;
-  if (ro == 1) {
-    const double p = st->p;
-    double* l2 = pp.h;  // h is spent
-    cta_gemv_cm<8>(Lib, ldl, c, c, pp.ro.e, 1.0, nullptr, l2, part, true);
-    double pq = 0.0;
-    for (int j = threadIdx.x; j < c; j += blockDim.x) pq = fma(l2[j], l2[j], pq);
-    const double ll2 = block_sum(pq, red);
-    const double rho2b = pp.ro.scal[0];
-    const double lam2 = rho2b - ll2;
-    if ((lam2 > 0.25 * rho2b) && (rho2b > 0.0)) {
-      lam = sqrt(lam2);
-      append_factor_row(Lb, Lib, ldl, c, l2, lam, pp.tmp);
-      for (int a = threadIdx.x; a <= c; a += blockDim.x)
-        nj[a] = (a < c) ? (pp.y[a] + pp.l1[a] + l2[a]) / p : lam / p;
-      if (threadIdx.x == 0) pp.fo.gn[c] = pp.ro.scal[2];  // r2 . x_next
-      cn = c + 1;
-      action = 1;
-    } else if (c >= r + 1) {
-      for (int a = threadIdx.x; a < c; a += blockDim.x) nj[a] = (pp.y[a] + pp.l1[a] + l2[a]) / p;
-      action = 2;
-    } else {
-      dep = 1;
-    }
-  } else {
-    lam = sqrt(pp.ro.scal[0]);
-    if (threadIdx.x == 0) {
-      P.L[(int64_t)slot * (ldl + 1)] = lam;
-      P.Li[(int64_t)slot * (ldl + 1)] = 1.0 / lam;
-      pp.fo.gn[0] = pp.ro.scal[2];  // x . x_next
-      st->rho2 = pp.ro.scal[0];
-    }
-    cn = 1;
-    base_new = slot;
-  }
-  if (threadIdx.x == 0) {
-    if (ro == 1) {
-      st->action = action;
-      st->dep = dep;
-    }
-    st->cn = cn;
-    st->base_new = base_new;
-    st->lam = lam;
-    pp.ctl->c = cn;
-    pp.ctl->base = base_new;
-    pp.ctl->reorth = 0;
-  }
-  if (P.has_next) prep_next(P, pp, part);
-}
 
 // ---------------------------------------------------------------------------
 // B (one CTA; second stream): everything of update t that the next snapshot's
@@ -695,10 +769,8 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide2(StateView src, Pipe 
 //     (basis.py:160-168), drift |phi_0 . phi_last| = |N_0 . N_last| and the QR
 //     of basis.py:170-174 on N' (Q_U is orthonormal: QR(Phi') = Q_U QR(N'))
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kSmallThreads) k_step_b(StateView src, StateView dst, Pipe pp, IsvdParams P,
-                                                          int use_smem) {
-  extern __shared__ double smem[];
-  __shared__ double red[32];
+__device__ inline void step_b_body(const StateView& src, const StateView& dst, const Pipe& pp, const IsvdParams& P,
+                                   int use_smem, double* smem, double* red) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const IsvdHdr h = *src.hdr;
   IsvdStep* st = pp.step[P.parity];
@@ -868,6 +940,18 @@ __global__ void __launch_bounds__(kSmallThreads) k_step_b(StateView src, StateVi
     *dst.hdr = o;
     st->m = m;
     st->mkeep = mk;
+  }
+}
+
+__global__ void __launch_bounds__(kSmallThreads) k_step_b(StateView src, StateView dst, Pipe pp, IsvdParams P,
+                                                          int use_smem) {
+  extern __shared__ double smem[];
+  __shared__ double red[32];
+  step_b_body(src, dst, pp, P, use_smem, smem, red);
+  __syncthreads();
+  if (threadIdx.x == 0) {  // completion signal for the decision of the next snapshot
+    __threadfence();
+    atomicAdd(&pp.ctl->bdone, 1);
   }
 }
 

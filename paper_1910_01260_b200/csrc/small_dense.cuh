@@ -499,6 +499,90 @@ __device__ inline void cta_gemv_t_cm(const double* A, int ld, int rows, int cols
   __syncthreads();
 }
 
+// Two right-hand sides at once: y1 = A x1, y2 = A x2 (same contract as
+// cta_gemv_cm with sgn = 1, no base; `part` holds 2 * nw * rows doubles).
+// x2 may be null (then y2 is not written).
+template <int K>
+__device__ inline void cta_gemv2_cm(const double* A, int ld, int rows, int cols, const double* x1, const double* x2,
+                                    double* y1, double* y2, double* part, bool lower) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double a1[K], a2[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) { a1[k] = 0.0; a2[k] = 0.0; }
+  for (int j = wid; j < cols; j += nw) {
+    const double u1 = x1[j], u2 = x2 ? x2[j] : 0.0;
+    const double* col = A + (int64_t)j * ld;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int i = lane + 32 * k;
+      if (i < rows && (!lower || i >= j)) {
+        const double v = col[i];
+        a1[k] = fma(v, u1, a1[k]);
+        a2[k] = fma(v, u2, a2[k]);
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int i = lane + 32 * k;
+    if (i < rows) {
+      part[wid * rows + i] = a1[k];
+      part[(nw + wid) * rows + i] = a2[k];
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < rows; i += blockDim.x) {
+    double s1 = 0.0, s2 = 0.0;
+    for (int w = 0; w < nw; ++w) {
+      s1 += part[w * rows + i];
+      s2 += part[(nw + w) * rows + i];
+    }
+    y1[i] = s1;
+    if (y2) y2[i] = s2;
+  }
+  __syncthreads();
+}
+
+// y1[j] = sum_i A(i, j) x1[i], y2[j] = sum_i A(i, j) x2[i] (lower: i >= j); warp per column.
+__device__ inline void cta_gemv2_t_cm(const double* A, int ld, int rows, int cols, const double* x1, const double* x2,
+                                      double* y1, double* y2, bool lower) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int j = wid; j < cols; j += nw) {
+    const double* col = A + (int64_t)j * ld;
+    double s1 = 0.0, s2 = 0.0;
+    for (int i = (lower ? j : 0) + lane; i < rows; i += 32) {
+      const double v = col[i];
+      s1 = fma(v, x1[i], s1);
+      s2 = fma(v, x2[i], s2);
+    }
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    if (lane == 0) {
+      y1[j] = s1;
+      y2[j] = s2;
+    }
+  }
+  __syncthreads();
+}
+
+// Three block-wide sums at once (fixed tree, deterministic); `red` >= 3 * 32 doubles.
+__device__ inline void block_sum3(double& a, double& b, double& c, double* red) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  a = warp_sum(a);
+  b = warp_sum(b);
+  c = warp_sum(c);
+  __syncthreads();
+  if (lane == 0) {
+    red[wid] = a;
+    red[32 + wid] = b;
+    red[64 + wid] = c;
+  }
+  __syncthreads();
+  a = warp_sum(lane < nw ? red[lane] : 0.0);
+  b = warp_sum(lane < nw ? red[32 + lane] : 0.0);
+  c = warp_sum(lane < nw ? red[64 + lane] : 0.0);
+}
+
 __device__ inline void cta_lower_mv(const double* Li, int ld, int n, const double* x, double* y) {
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     double s = 0.0;
