@@ -46,7 +46,7 @@ COLS = 500
 WARM_COLS = 100
 RANK = 64
 TOL = 1e-9
-PROF_KINDS = ["proj_pass", "resid_pass", "step_a", "step_b", "v_update", "compact_prep", "tall_gemm",
+PROF_KINDS = ["fused_pass", "reorth_pass", "decide", "core_step", "v_update", "compact_prep", "compact_sweep",
               "spatial", "st_gemm", "st_small", "lu", "temporal", "other"]
 
 
@@ -371,9 +371,12 @@ def run_device(args):
     bw, bw_src = peaks()
     ctx = bench_isvd_device(args, ws, rank)
     kern = ctx["kernels"]
-    # dominant kernel of the step (by event time) and its live roofline
+    # dominant HBM kernel of the step (by event time) and its live roofline.  Only
+    # kernels that count algorithmic bytes qualify: the core step on the second
+    # stream starts early and spins on a device counter, so its event time
+    # includes waiting and says nothing about its own cost.
     pl, pms, pby = ctx["prof"]
-    dom = max(range(len(PROF_KINDS)), key=lambda k: pms[k])
+    dom = max(range(len(PROF_KINDS)), key=lambda k: pms[k] if pby[k] > 0 else -1.0)
     achieved = pby[dom] / (pms[dom] / 1e3) / 1e9 if pms[dom] > 0 else 0.0
     traffic = None
     tpath = os.path.join(HERE, "profiles", "traffic.json")

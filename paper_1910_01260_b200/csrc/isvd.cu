@@ -107,6 +107,32 @@ __global__ void k_copy_g_col(const double* g, int c, double* G, int ld, int j) {
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Launch with programmatic stream serialization (PDL): the kernel may start
+// while its predecessor on the stream is still running; it calls pdl_enter()
+// before touching the predecessor's results.  STROM_NO_PDL=1 disables it.
+bool pdl_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("STROM_NO_PDL");
+    return !(e && atoi(e) != 0);
+  }();
+  return v;
+}
+
+template <class... KArgs, class... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  STROM_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
+
 // diagnostics: STROM_TRACE=1 synchronises and names every launch of the update
 void trace_point(const char* what, cudaStream_t s) {
   static const bool on = [] {
@@ -317,6 +343,8 @@ IsvdParams make_params(const strom_isvd* h, const PipeMem& m, int64_t k_new, boo
   P.work_stride = m.work_stride;
   P.parity = 0;
   P.has_next = 0;
+  P.b_expect = -1;
+  P.d_expect = -1;
   P.L = h->store->L();
   P.Li = h->store->Li();
   P.prof = prof_dev_bytes();
@@ -373,7 +401,7 @@ void launch_pass_t(const PassArgs& a, int cols_ub, int reserve, int kind_prof, c
   const int64_t ntiles = a.ldu / kStageRows;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, std::max(1, sm_count() - reserve)));
   ProfScope ps(kind_prof, s);
-  k_pass<MAXJ><<<grid, kPassThreads, smem, s>>>(a, nst);
+  launch_pdl(k_pass<MAXJ>, dim3(grid), dim3(kPassThreads), smem, s, a, nst);
   {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
@@ -463,10 +491,10 @@ void launch_decide_kernel(bool second, const StateView& src, const PipeMem& m, c
   ProfScope ps(P_STEP_A, s);
   if (!second) {
     set_smem_attr(k_decide, smem, &cfg1);
-    k_decide<<<1, kDecideThreads, smem, s>>>(src, m.pp, P);
+    launch_pdl(k_decide, dim3(1), dim3(kDecideThreads), smem, s, src, m.pp, P);
   } else {
     set_smem_attr(k_decide2, smem, &cfg2);
-    k_decide2<<<1, kDecideThreads, smem, s>>>(src, m.pp, P);
+    launch_pdl(k_decide2, dim3(1), dim3(kDecideThreads), smem, s, src, m.pp, P);
   }
   STROM_LAUNCH_CHECK();
 }
@@ -816,6 +844,8 @@ strom_isvd* ingest_pipelined(strom_isvd* src, ColumnSource& cols, cudaStream_t s
   PipeMem m;
   bool need_prep = true;
   int64_t b_launched = 0;  // core steps queued on s2 since the last k_init_ctl
+  int64_t d_launched = 0;  // decision chains queued on s since then
+  bool fresh_alloc = false;  // this iteration allocated on s: order s2 behind it
   auto join = [&]() {  // s waits for all of s2
     STROM_CUDA(cudaEventRecord(evV, s2));
     STROM_CUDA(cudaStreamWaitEvent(s, evV, 0));
@@ -857,6 +887,7 @@ strom_isvd* ingest_pipelined(strom_isvd* src, ColumnSource& cols, cudaStream_t s
       dslot.reset(new_like(prev, nc));
       alloc_small(dslot.get(), s);
       alloc_v(dslot.get(), s);
+      fresh_alloc = true;
     }
     strom_isvd* dst = dslot.get();
     dst->k = prev->k + 1;
@@ -865,7 +896,9 @@ strom_isvd* ingest_pipelined(strom_isvd* src, ColumnSource& cols, cudaStream_t s
       join();
       m = make_pipe(prev->caps, s);
       need_prep = true;
+      fresh_alloc = true;
     }
+
     IsvdParams P = make_params(dst, m, dst->k, false);
     P.parity = (int)(t & 1);
     P.has_next = (t + 1 < ncols && !(dbg & 2)) ? 1 : 0;
@@ -875,19 +908,46 @@ strom_isvd* ingest_pipelined(strom_isvd* src, ColumnSource& cols, cudaStream_t s
     const double* xn = cols.col(t + 1);
     if (need_prep) {
       if (t > 0) STROM_CUDA(cudaStreamWaitEvent(s, evB, 0));  // prev's header comes from s2
-      k_init_ctl<<<1, 1, 0, s>>>(m.pp.ctl, prev->view.hdr);    // also resets the B counter
+      k_init_ctl<<<1, 1, 0, s>>>(m.pp.ctl, prev->view.hdr);    // also resets the counters
       STROM_LAUNCH_CHECK();
       b_launched = 0;
+      d_launched = 0;
+      fresh_alloc = true;  // s2's next core step must see the reset counters
       launch_pass(PASS_PROJ, cols_ub, dst, m, nullptr, xt, 0, s);
       launch_prep(m, P, s);
       need_prep = false;
     }
+    if (fresh_alloc) {
+      // s2 is ordered behind this point of s: memory the stream-ordered pool
+      // handed out on s, and the counters k_init_ctl reset (a core step spinning
+      // on a stale counter would run ahead of its decisions)
+      STROM_CUDA(cudaEventRecord(evV, s));
+      STROM_CUDA(cudaStreamWaitEvent(s2, evV, 0));
+      fresh_alloc = false;
+    }
     if (decide_as_kernel()) {
+      // s: pass -> decide -> second pass -> decide2, kernel to kernel (PDL);
+      // the cross-stream dependencies are device counters, not events:
+      // k_decide(t) waits for k_step_b(t-1), k_step_b(t) for k_decide2(t)
+      // s: pass -> [wait for k_step_b(t-1)] -> decide -> second pass -> decide2
+      // (kernel to kernel, PDL).  k_step_b(t) on s2 starts on a device counter
+      // that decide2(t) bumps -- no event between decide2 and the next pass.
+      // (Measured at cfg2: the decide waiting on an event beats a device spin,
+      // which keeps an SM busy; the core step spinning costs nothing, it has
+      // the reserved SM anyway.)
+      P.b_expect = -1;
+      P.d_expect = (int32_t)(d_launched + 1);
       launch_pass(PASS_FUSED, cols_ub, dst, m, xt, (dbg & 2) ? nullptr : xn, 1, s);
-      if (t > 0) STROM_CUDA(cudaStreamWaitEvent(s, evB, 0));
+      if (b_launched > 0) STROM_CUDA(cudaStreamWaitEvent(s, evB, 0));
       launch_decide_kernel(false, prev->view, m, P, s);
       launch_pass(PASS_SECOND, cols_ub, dst, m, xt, xn, 1, s);
       launch_decide_kernel(true, prev->view, m, P, s);
+      ++d_launched;
+      cols.release(t);
+      launch_step_b(prev->view, dst->view, m, P, prev->caps, s2);
+      ++b_launched;
+      STROM_CUDA(cudaEventRecord(evB, s2));
+      launch_vupdate(prev->view, dst->view, m, P, prev->caps.rcap, s2);
     } else {
       PassTail tl;
       tl.tail = 1;
@@ -897,14 +957,14 @@ strom_isvd* ingest_pipelined(strom_isvd* src, ColumnSource& cols, cudaStream_t s
       launch_pass(PASS_FUSED, cols_ub, dst, m, xt, (dbg & 2) ? nullptr : xn, 1, s, tl);
       tl.tail = 2;
       launch_pass(PASS_SECOND, cols_ub, dst, m, xt, xn, 1, s, tl);
+      cols.release(t);
+      STROM_CUDA(cudaEventRecord(evD, s));
+      STROM_CUDA(cudaStreamWaitEvent(s2, evD, 0));
+      launch_step_b(prev->view, dst->view, m, P, prev->caps, s2);
+      ++b_launched;
+      STROM_CUDA(cudaEventRecord(evB, s2));
+      launch_vupdate(prev->view, dst->view, m, P, prev->caps.rcap, s2);
     }
-    cols.release(t);
-    STROM_CUDA(cudaEventRecord(evD, s));
-    STROM_CUDA(cudaStreamWaitEvent(s2, evD, 0));
-    launch_step_b(prev->view, dst->view, m, P, prev->caps, s2);
-    ++b_launched;
-    STROM_CUDA(cudaEventRecord(evB, s2));
-    launch_vupdate(prev->view, dst->view, m, P, prev->caps.rcap, s2);
     dst->c_ub = prev->c_ub + 1;
     dst->store->claimed = std::max(dst->store->claimed, dst->c_ub);
     dst->r_ub = std::min(prev->r_ub + 1, prev->caps.rcap);

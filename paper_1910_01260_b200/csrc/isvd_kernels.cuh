@@ -53,10 +53,30 @@ enum : int32_t { M_NORMAL_DEP = 0, M_NORMAL_INDEP = 1, M_RESTART_ACCEPT = 2, M_R
 // them, so the host never needs to know the device-side decisions.
 struct PipeCtl {
   int32_t c, base;
-  int32_t reorth;  // 0 none, 1 DGKS pass requested, 2 restart copy requested
-  int32_t bdone;   // core steps (k_step_b) completed since the sequence started
-  double xx;       // x.x of the snapshot about to be decided
+  int32_t reorth;   // 0 none, 1 DGKS pass requested, 2 restart copy requested
+  int32_t bdone;    // core steps (k_step_b) completed since the sequence started
+  int32_t decided;  // decision chains (k_decide + k_decide2) completed since then
+  int32_t pad;
+  double xx;        // x.x of the snapshot about to be decided
 };
+
+// Cross-stream completion counters: one thread spins (acquire) until *ctr >= target.
+__device__ inline void wait_counter(const int32_t* ctr, int32_t target) {
+  if (target < 0) return;
+  if (threadIdx.x == 0) {
+    const volatile int32_t* v = ctr;
+    while (*v < target) __nanosleep(64);
+    __threadfence();
+  }
+  __syncthreads();
+}
+__device__ inline void signal_counter(int32_t* ctr) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1);
+  }
+}
 
 // One update's decisions (double-buffered by update parity: k_step_b of update
 // t reads record t%2 while the decision kernels of t+1 write the other one).
@@ -118,11 +138,23 @@ struct IsvdParams {
   int32_t work_stride;
   int32_t parity;    // which IsvdStep / ell / nj record this update uses
   int32_t has_next;  // the fused pass also projected the next snapshot
+  int32_t b_expect;  // k_decide waits for ctl->bdone >= b_expect (-1: stream order suffices)
+  int32_t d_expect;  // k_step_b waits for ctl->decided >= d_expect (-1: stream order suffices)
   double* L;         // store pointers (physical indexing), ld = ccap
   double* Li;
   unsigned long long* prof;  // device byte counters (runtime.cuh ProfKind) or null
   long long* tprobe;         // phase timestamps of step B (diagnostics) or null
 };
+
+// Programmatic dependent launch: let the next kernel of the stream launch now
+// (it waits for us itself), and wait for the previous one before reading its
+// results.  Both are no-ops for a kernel launched without the PDL attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_enter() {
+  pdl_trigger();
+  pdl_wait();
+}
 
 #define STROM_TPROBE(P, k)                                  \
   do {                                                      \
@@ -271,6 +303,7 @@ __device__ inline void prep_next(const IsvdParams& P, const Pipe& pp, double* pa
 // A (first snapshot of a sequence, or after a compaction): prepare from a PROJ pass.
 __global__ void __launch_bounds__(kDecideThreads) k_prep(Pipe pp, IsvdParams P) {
   extern __shared__ double part[];
+  pdl_enter();
   prep_next(P, pp, part);
 }
 
@@ -280,6 +313,7 @@ __global__ void k_init_ctl(PipeCtl* ctl, const IsvdHdr* h) {
   ctl->base = h->base;
   ctl->reorth = 0;
   ctl->bdone = 0;
+  ctl->decided = 0;
 }
 
 constexpr double kFoldTau = 1e-3;  // append r1 only if its out-of-span part is >= tau |r1|
@@ -435,6 +469,12 @@ __device__ inline void decide_body(const StateView& src, const Pipe& pp, const I
 __global__ void __launch_bounds__(kDecideThreads) k_decide(StateView src, Pipe pp, IsvdParams P) {
   extern __shared__ double part[];  // 2 * nw * c_cap
   __shared__ double red[96];
+  pdl_wait();
+  // the core step of the previous snapshot (second stream).  Dependents are
+  // released only afterwards: an early-resident next grid must never hold the
+  // SM that k_step_b needs while this CTA spins on it.
+  wait_counter(&pp.ctl->bdone, P.b_expect);
+  pdl_trigger();
   decide_body(src, pp, P, part, red);
 }
 
@@ -510,7 +550,9 @@ __device__ inline void decide2_body(const StateView& src, const Pipe& pp, const 
 __global__ void __launch_bounds__(kDecideThreads) k_decide2(StateView src, Pipe pp, IsvdParams P) {
   extern __shared__ double part[];
   __shared__ double red[96];
+  pdl_enter();
   decide2_body(src, pp, P, part, red);
+  signal_counter(&pp.ctl->decided);  // the decisions of this snapshot are complete
 }
 
 template <int MAXJ>
@@ -523,6 +565,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(PassArgs a, int nstage
   __shared__ __align__(16) double red[2][kPassConsumers][kSubRows];
   __shared__ double wsc[3];
   __shared__ int s_last;
+  pdl_enter();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int c = a.ctl->c;
   const int base = a.ctl->base;
@@ -947,12 +990,9 @@ __global__ void __launch_bounds__(kSmallThreads) k_step_b(StateView src, StateVi
                                                           int use_smem) {
   extern __shared__ double smem[];
   __shared__ double red[32];
+  wait_counter(&pp.ctl->decided, P.d_expect);  // this snapshot's decision chain
   step_b_body(src, dst, pp, P, use_smem, smem, red);
-  __syncthreads();
-  if (threadIdx.x == 0) {  // completion signal for the decision of the next snapshot
-    __threadfence();
-    atomicAdd(&pp.ctl->bdone, 1);
-  }
+  signal_counter(&pp.ctl->bdone);  // the next snapshot's decision may read this state
 }
 
 // ---------------------------------------------------------------------------
