@@ -299,7 +299,9 @@ class BasisSet:
     __slots__ = ("phi_s", "temporal", "n_mu", "_stack")
 
     def __init__(self, phi_s, temporal, n_mu):
-        self.phi_s = to_dev(phi_s)
+        # stored column-major (each spatial mode contiguous): the operator build's
+        # CSR gather then reads 32 consecutive rows of one mode per load
+        self.phi_s = colmajor(to_dev(phi_s, contiguous=False))[0]
         if isinstance(temporal, torch.Tensor) and temporal.dim() == 3:
             stack = to_dev(temporal)
             self.temporal = tuple(stack[i] for i in range(stack.shape[0]))

@@ -380,7 +380,7 @@ size_t pass_stage_budget() {
   static size_t v = [] {
     const char* e = getenv("STROM_STAGE_KB");
     const int kb = e ? atoi(e) : 140;
-    return (size_t)std::max(16, std::min(200, kb)) * 1024;
+    return (size_t)std::max(16, std::min(212, kb)) * 1024;
   }();
   return v;
 }
