@@ -1,6 +1,6 @@
 """Compile the sm_100a C-ABI library in-tree (nvcc cross-compiles without a GPU).
 
-    python -m paper_1910_01260_b200._build
+    python paper_1910_01260_b200/_build.py
 
 Produces ``paper_1910_01260_b200/_lib/libstrom_b200.so`` (static cudart,
 ``-gencode arch=compute_100a,code=sm_100a -lineinfo -O3``).  The .so is

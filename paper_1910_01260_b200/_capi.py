@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(_HERE, "_lib", "libstrom_b200.so")
 if not os.path.exists(LIB_PATH):
     raise ImportError(
         f"{LIB_PATH} is missing: build the sm_100a library first "
-        "(python -m paper_1910_01260_b200._build or __graft_entry__.build())")
+        "(python paper_1910_01260_b200/_build.py or __graft_entry__.build())")
 
 lib = C.CDLL(LIB_PATH)
 
