@@ -170,6 +170,22 @@ int strom_spatial_reduce_csr(int64_t n, const void* indptr_dev, const void* indi
                              int64_t ns, const double* extra_dev, int64_t ext_ld, int64_t ne,
                              const double* xref_dev, double* out_dev, void* stream);
 
+/* Tiled-ELL operator form (built once per operator, like a sparse library's
+ * SpMM preprocessing) and the spatial reduction over it: the fast path for
+ * column-major phi with n_s, q <= 64 (same contractions and output as
+ * strom_spatial_reduce_csr).  Per 64-row tile: K off-diagonal slots (uint32
+ * column, double value) and the diagonal; K in {4, 6, 8, 16} >= max
+ * off-diagonal entries per row.  eidx_dev: ceil(n/64) * K * 64 uint32,
+ * eval_dev: ceil(n/64) * (K+1) * 64 doubles.  *reach_out (host) = max(col -
+ * row) over off-diagonal entries (-1: none), the forward reach used to stream
+ * phi rows into L2 ahead of the gathers. */
+int strom_csr_to_ell(int64_t n, const void* indptr_dev, const void* indices_dev, const double* data_dev,
+                     int32_t index_bits, int32_t K, uint32_t* eidx_dev, double* eval_dev, int64_t* reach_out,
+                     void* stream);
+int strom_spatial_reduce_ell(int64_t n, int32_t K, const uint32_t* eidx_dev, const double* eval_dev, int64_t reach,
+                             const double* phi_dev, int64_t ld, int64_t ns, const double* extra_dev, int64_t ext_ld,
+                             int64_t ne, const double* xref_dev, double* out_dev, void* stream);
+
 /* ------------------------------------------------------------------------
  * Space-time reduced system  (spacetime.py:43-115 build_st_matrix /
  * build_st_input / build_st_init, spacetime.py:128-151 build_st_rom)

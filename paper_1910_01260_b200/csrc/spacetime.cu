@@ -9,9 +9,9 @@
 //   S[i,j',j]  = sum_k   Psi_i[k,j'] Psi_i[k,j]        (same-step)
 //   Cp[i,j',j] = sum_k>0 Psi_i[k,j'] Psi_i[k-1,j]      (step coupling)
 //
-// The (n_s n_t)^2 temporal Gram runs on the fp64 tensor cores (DMMA m8n8k4)
-// with the Hadamard-with-tiled-A_hat and the diagonal terms fused into the
-// epilogue.  f_st (spacetime.py:72-99) and x0_st (spacetime.py:102-115) are
+// The (n_s n_t)^2 temporal Gram (symmetric: upper-triangle tiles only) runs on
+// the fp64 tensor cores (DMMA m8n8k4) with the Hadamard-with-tiled-A_hat and
+// the diagonal terms fused into the epilogue.  f_st (spacetime.py:72-99) and x0_st (spacetime.py:102-115) are
 // O(n_s n_t N_t) and come from one small kernel.
 #include <algorithm>
 
@@ -40,50 +40,108 @@ __global__ void k_st_pack(const double* __restrict__ psi, const double* __restri
   Fd[idx] = vd;
 }
 
-// D[i, j', j] = S - Cp  (n_s x n_t x n_t)
-__global__ void k_st_diag(const double* __restrict__ psi, int nsteps, int ns, int nt, double* __restrict__ D) {
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= ns * nt * nt) return;
-  const int i = idx / (nt * nt), jp = (idx / nt) % nt, j = idx % nt;
+// Per-mode temporal sums over one chunk of kDiagChunk steps (CTA (i, c)):
+//   Dpart[c, i, j', j] = sum_k Psi_i[k,j'] Psi_i[k,j] - sum_{k>0} Psi_i[k,j'] Psi_i[k-1,j]
+//   Wpart[c, i, j]     = sum_k dt_k Psi_i[k,j] g_k,   g_k = b_hat_i . f_k (1 for constant input)
+// Psi_i's chunk (plus the step before it, for the coupling term) is staged in
+// shared memory; thread o < nt^2 owns (j', j).  The chunk partials are summed
+// in chunk order by the consumers (k_st_gemm's epilogue, k_st_vec_final).
+constexpr int kDiagChunk = 64;
+__global__ void __launch_bounds__(256) k_st_temporal(const double* __restrict__ psi, const double* __restrict__ dt,
+                                                     int nsteps, int ns, int nt, const double* __restrict__ bhat,
+                                                     int m, const double* __restrict__ f, int constant_input,
+                                                     double* __restrict__ Dpart, double* __restrict__ Wpart) {
+  extern __shared__ double sp[];  // (kDiagChunk + 1) x nt, then kDiagChunk weights dt_k g_k
+  const int i = blockIdx.x, c = blockIdx.y;
+  const int k0 = c * kDiagChunk, k1 = min(nsteps, k0 + kDiagChunk), nk = k1 - k0;
   const double* p = psi + (int64_t)i * nsteps * nt;
-  double same = 0.0, coup = 0.0;
-  for (int k = 0; k < nsteps; ++k) same = fma(p[(int64_t)k * nt + jp], p[(int64_t)k * nt + j], same);
-  for (int k = 1; k < nsteps; ++k) coup = fma(p[(int64_t)k * nt + jp], p[(int64_t)(k - 1) * nt + j], coup);
-  D[idx] = same - coup;
+  double* wk = sp + (kDiagChunk + 1) * nt;
+  for (int e = threadIdx.x; e < (nk + 1) * nt; e += blockDim.x) {  // row r = step k0 - 1 + r
+    const int k = k0 - 1 + e / nt;
+    sp[e] = k >= 0 ? p[(int64_t)k * nt + e % nt] : 0.0;
+  }
+  for (int r = threadIdx.x; r < nk; r += blockDim.x) {
+    const int k = k0 + r;
+    double g = 1.0;
+    if (!constant_input) {
+      g = 0.0;
+      for (int q = 0; q < m; ++q) g = fma(bhat[(int64_t)i * m + q], f[(int64_t)k * m + q], g);
+    }
+    wk[r] = dt[k] * g;
+  }
+  __syncthreads();
+  const int no = nt * nt;
+  double* Dp = Dpart + ((int64_t)c * ns + i) * no;
+  for (int o = threadIdx.x; o < no; o += blockDim.x) {
+    const int jp = o / nt, j = o % nt;
+    double s0 = 0.0, s1 = 0.0, c0 = 0.0, c1 = 0.0;
+    int r = 1;
+    for (; r + 1 <= nk; r += 2) {  // two independent chains per sum
+      const double a0 = sp[r * nt + jp], a1 = sp[(r + 1) * nt + jp];
+      s0 = fma(a0, sp[r * nt + j], s0);
+      c0 = fma(a0, sp[(r - 1) * nt + j], c0);
+      s1 = fma(a1, sp[(r + 1) * nt + j], s1);
+      c1 = fma(a1, sp[r * nt + j], c1);
+    }
+    if (r <= nk) {
+      const double a0 = sp[r * nt + jp];
+      s0 = fma(a0, sp[r * nt + j], s0);
+      c0 = fma(a0, sp[(r - 1) * nt + j], c0);
+    }
+    Dp[o] = (s0 + s1) - (c0 + c1);  // coupling row 0 is zero for the first chunk (no step before k = 0)
+  }
+  for (int j = threadIdx.x; j < nt; j += blockDim.x) {
+    double w = 0.0;
+    for (int r = 0; r < nk; ++r) w = fma(wk[r], sp[(r + 1) * nt + j], w);
+    Wpart[((int64_t)c * ns + i) * nt + j] = w;
+  }
 }
 
-// f_st and x0_st.  Thread per (j, i).  f: constant -> m values; else N_t x m.
-__global__ void k_st_vecs(const double* __restrict__ psi, const double* __restrict__ dt, int nsteps, int ns,
-                          int nt, const double* __restrict__ bhat, int m, const double* __restrict__ f,
-                          int constant_input, const double* __restrict__ x0hat, double* __restrict__ fst,
-                          double* __restrict__ x0st) {
+// Chunk sums in chunk order: D[i, j', j] = sum_c Dpart[c, i, j', j];
+// f_st[j n_s + i] = (b_hat_i . f) sum_c Wpart (constant input) or sum_c Wpart;
+// x0_st[j n_s + i] = Psi_i[0, j] x0_hat_i  (the reference code's choice, spacetime.py:102-115).
+__global__ void k_st_final(const double* __restrict__ psi, int nsteps, int ns, int nt, int nchunks,
+                           const double* __restrict__ Dpart, double* __restrict__ D, const double* __restrict__ bhat,
+                           int m, const double* __restrict__ f, int constant_input, const double* __restrict__ x0hat,
+                           const double* __restrict__ Wpart, double* __restrict__ fst, double* __restrict__ x0st) {
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= ns * nt) return;
+  const int64_t nd = (int64_t)ns * nt * nt;
+  if (D && idx < nd) {
+    double d = 0.0;
+    for (int c = 0; c < nchunks; ++c) d += Dpart[c * nd + idx];
+    D[idx] = d;
+  }
+  if (!fst || idx >= ns * nt) return;
   const int j = idx / ns, i = idx % ns;
-  const double* p = psi + (int64_t)i * nsteps * nt;
-  double out = 0.0;
+  double w = 0.0;
+  for (int c = 0; c < nchunks; ++c) w += Wpart[((int64_t)c * ns + i) * nt + j];
   if (constant_input) {
-    double w = 0.0;
-    for (int k = 0; k < nsteps; ++k) w += dt[k] * p[(int64_t)k * nt + j];
     double bf = 0.0;
     for (int q = 0; q < m; ++q) bf = fma(bhat[(int64_t)i * m + q], f[q], bf);
-    out = w * bf;
-  } else {
-    for (int k = 0; k < nsteps; ++k) {
-      double g = 0.0;
-      for (int q = 0; q < m; ++q) g = fma(bhat[(int64_t)i * m + q], f[(int64_t)k * m + q], g);
-      out += dt[k] * p[(int64_t)k * nt + j] * g;
-    }
+    w *= bf;
   }
-  fst[idx] = out;
-  x0st[idx] = p[j] * x0hat[i];
+  fst[idx] = w;
+  x0st[idx] = psi[(int64_t)i * nsteps * nt + j] * x0hat[i];
 }
 
 constexpr int kTile = 64;   // output tile (rows and cols)
 constexpr int kKc = 32;     // K chunk staged in shared memory
 constexpr int kLd = kTile + 4;
 
-// A_st (NT x NT, row-major) = -(F^T Fd) o tile(A_hat) + diag terms.
+// A_st (NT x NT, row-major) = -(F^T Fd) o tile(A_hat) + diag terms.  The
+// temporal Gram G = F^T diag(dt) F is symmetric, so only the upper-triangle
+// 64 x 64 tiles are computed (one wave for NT = 1000) and each writes both
+// A_st blocks it determines, each with its own Hadamard factor and diagonal
+// term.  K chunks are prefetched into registers while the previous chunk is
+// contracted.
+__device__ __forceinline__ double st_entry(double gval, int row, int col, int ns, int nt, const double* ahat,
+                                           const double* D) {
+  const int jp = row / ns, i = row % ns, j = col / ns, i2 = col % ns;
+  double v = -gval * ahat[(int64_t)i * ns + i2];
+  if (i == i2) v += D[((int64_t)i * nt + jp) * nt + j];
+  return v;
+}
+
 __global__ void __launch_bounds__(256) k_st_gemm(const double* __restrict__ F, const double* __restrict__ Fd,
                                                  int kpad, int ns, int nt, const double* __restrict__ ahat,
                                                  const double* __restrict__ D, double* __restrict__ out) {
@@ -92,43 +150,55 @@ __global__ void __launch_bounds__(256) k_st_gemm(const double* __restrict__ F, c
   const int NT = ns * nt;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int r0 = blockIdx.x * kTile, c0 = blockIdx.y * kTile;
+  // upper-triangle tile (bx <= by) from the linear block index
+  const int nb = (int)ceil_div(NT, kTile);
+  int bx = 0, rem = blockIdx.x;
+  while (rem >= nb - bx) { rem -= nb - bx; ++bx; }
+  const int by = bx + rem;
+  const int r0 = bx * kTile, c0 = by * kTile;
+  constexpr int kPer = kKc * kTile / 256;  // elements per thread per operand per chunk
+  double pa[kPer], pb[kPer];
+  auto fetch = [&](int k0) {
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const int idx = threadIdx.x + q * 256;
+      const int kk = idx / kTile, cc = idx % kTile, k = k0 + kk;
+      const bool inK = k < kpad;
+      pa[q] = (inK && r0 + cc < NT) ? F[(int64_t)k * NT + r0 + cc] : 0.0;
+      pb[q] = (inK && c0 + cc < NT) ? Fd[(int64_t)k * NT + c0 + cc] : 0.0;
+    }
+  };
   double acc[8][2];
 #pragma unroll
   for (int y = 0; y < 8; ++y) acc[y][0] = acc[y][1] = 0.0;
+  fetch(0);
   for (int k0 = 0; k0 < kpad; k0 += kKc) {
     __syncthreads();
-    for (int idx = threadIdx.x; idx < kKc * kTile; idx += blockDim.x) {
-      const int kk = idx / kTile, cc = idx % kTile;
-      const int k = k0 + kk;
-      const bool inK = k < kpad;
-      As[kk][cc] = (inK && r0 + cc < NT) ? F[(int64_t)k * NT + r0 + cc] : 0.0;
-      Bs[kk][cc] = (inK && c0 + cc < NT) ? Fd[(int64_t)k * NT + c0 + cc] : 0.0;
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const int idx = threadIdx.x + q * 256;
+      As[idx / kTile][idx % kTile] = pa[q];
+      Bs[idx / kTile][idx % kTile] = pb[q];
     }
     __syncthreads();
+    if (k0 + kKc < kpad) fetch(k0 + kKc);
 #pragma unroll
     for (int ks = 0; ks < kKc / 4; ++ks) {
       const double a = As[ks * 4 + t][wid * 8 + g];
 #pragma unroll
-      for (int y = 0; y < 8; ++y) {
-        const double b = Bs[ks * 4 + t][y * 8 + g];
-        dmma884(acc[y][0], acc[y][1], a, b);
-      }
+      for (int y = 0; y < 8; ++y) dmma884(acc[y][0], acc[y][1], a, Bs[ks * 4 + t][y * 8 + g]);
     }
   }
   const int row = r0 + wid * 8 + g;
   if (row >= NT) return;
-  const int jp = row / ns, i = row % ns;
 #pragma unroll
   for (int y = 0; y < 8; ++y) {
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       const int col = c0 + y * 8 + 2 * t + e;
       if (col >= NT) continue;
-      const int j = col / ns, i2 = col % ns;
-      double v = -acc[y][e] * ahat[(int64_t)i * ns + i2];
-      if (i == i2) v += D[((int64_t)i * nt + jp) * nt + j];
-      out[(int64_t)row * NT + col] = v;
+      out[(int64_t)row * NT + col] = st_entry(acc[y][e], row, col, ns, nt, ahat, D);
+      if (bx != by) out[(int64_t)col * NT + row] = st_entry(acc[y][e], col, row, ns, nt, ahat, D);
     }
   }
 }
@@ -152,26 +222,33 @@ int strom_st_assemble(const double* ahat_dev, const double* psi_dev, const doubl
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const int64_t NT = ns * nt;
     const int kpad = (int)round_up(nsteps, kKc);
-    auto ws = dev_alloc(((size_t)2 * kpad * NT + (size_t)ns * nt * nt) * 8, s, false);
+    const int nch = (int)ceil_div(nsteps, kDiagChunk);
+    const bool vecs = fst_dev || x0st_dev;
+    if (vecs) STROM_REQUIRE(fst_dev && x0st_dev && bhat_dev && f_dev && x0hat_dev, "f_st/x0_st need b_hat, f, x0_hat");
+    auto ws = dev_alloc(((size_t)2 * kpad * NT + (size_t)(nch + 1) * ns * nt * nt + (size_t)nch * ns * nt) * 8, s,
+                        false);
     double* F = ws->as<double>();
     double* Fd = F + (size_t)kpad * NT;
     double* D = Fd + (size_t)kpad * NT;
+    double* Dp = D + (size_t)ns * nt * nt;
+    double* Wp = Dp + (size_t)nch * ns * nt * nt;
+    k_st_temporal<<<dim3((unsigned)ns, (unsigned)nch), 256, (size_t)((kDiagChunk + 1) * nt + kDiagChunk) * 8, s>>>(
+        psi_dev, dt_dev, (int)nsteps, (int)ns, (int)nt, vecs ? bhat_dev : nullptr, (int)m, vecs ? f_dev : nullptr,
+        vecs ? constant_input : 1, Dp, Wp);
+    STROM_LAUNCH_CHECK();
+    const int64_t nfin = std::max<int64_t>(ast_dev ? ns * nt * nt : 0, vecs ? NT : 0);
+    k_st_final<<<(unsigned)ceil_div(nfin, 256), 256, 0, s>>>(psi_dev, (int)nsteps, (int)ns, (int)nt, nch,
+                                                           Dp, ast_dev ? D : nullptr, bhat_dev, (int)m, f_dev,
+                                                           constant_input, x0hat_dev, Wp, vecs ? fst_dev : nullptr,
+                                                           x0st_dev);
+    STROM_LAUNCH_CHECK();
     if (ast_dev) {
       k_st_pack<<<(unsigned)ceil_div((int64_t)kpad * NT, 256), 256, 0, s>>>(psi_dev, dt_dev, (int)nsteps, (int)ns,
                                                                              (int)nt, kpad, F, Fd);
       STROM_LAUNCH_CHECK();
-      k_st_diag<<<(unsigned)ceil_div(ns * nt * nt, 128), 128, 0, s>>>(psi_dev, (int)nsteps, (int)ns, (int)nt, D);
-      STROM_LAUNCH_CHECK();
-      dim3 grid((unsigned)ceil_div(NT, kTile), (unsigned)ceil_div(NT, kTile));
+      const int64_t nb = ceil_div(NT, kTile);
       ProfScope ps(P_ST_GEMM, s);
-      k_st_gemm<<<grid, 256, 0, s>>>(F, Fd, kpad, (int)ns, (int)nt, ahat_dev, D, ast_dev);
-      STROM_LAUNCH_CHECK();
-    }
-    if (fst_dev || x0st_dev) {
-      STROM_REQUIRE(fst_dev && x0st_dev && bhat_dev && f_dev && x0hat_dev, "f_st/x0_st need b_hat, f, x0_hat");
-      k_st_vecs<<<(unsigned)ceil_div(NT, 128), 128, 0, s>>>(psi_dev, dt_dev, (int)nsteps, (int)ns, (int)nt,
-                                                           bhat_dev, (int)m, f_dev, constant_input, x0hat_dev,
-                                                           fst_dev, x0st_dev);
+      k_st_gemm<<<(unsigned)(nb * (nb + 1) / 2), 256, 0, s>>>(F, Fd, kpad, (int)ns, (int)nt, ahat_dev, D, ast_dev);
       STROM_LAUNCH_CHECK();
     }
   });

@@ -8,8 +8,11 @@
 // never written to HBM.  Per-CTA partial Grams are reduced in a fixed order
 // (deterministic).
 #include <algorithm>
+#include <climits>
+#include <cstdlib>
 
 #include "../../include/strom_b200.h"
+#include "bulk.cuh"
 #include "dmma.cuh"
 #include "runtime.cuh"
 
@@ -317,14 +320,406 @@ __global__ void __launch_bounds__(256) k_spatial_rm(SpatialArgs<IdxT> A) {
   }
 }
 
-// out (ns x q, row-major) = sum over CTAs of the partials, in CTA order.
-__global__ void k_spatial_reduce(const double* part, int nparts, int MA, int NQ, int ns, int q, double* out) {
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= ns * q) return;
-  const int a = idx / q, b = idx % q;
-  double s = 0.0;
-  for (int p = 0; p < nparts; ++p) s += part[(int64_t)p * MA * NQ + a * NQ + b];
-  out[idx] = s;
+// ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------
+// Column-major Phi (phi_rs == 1, ld = phi_cs), n_s <= 64, q <= 64, operator in
+// the tiled ELL layout of strom_csr_to_ell (diagonal kept apart, K off-
+// diagonal slots per row).  Warp-specialised, one persistent CTA per SM, 64-row
+// tiles dealt round-robin (tile = blockIdx.x + it * gridDim.x) so the grid
+// advances through Phi as one band of gridDim.x * 64 rows (the rows a banded
+// operator reaches stay in L2), through an S-deep shared-memory ring.
+//   * Producer warps (two row halves x NPW/2 column groups, lane = row): the
+//     tile's ELL slices arrive by bulk copy (issued one tile ahead); each lane
+//     gathers kWsCols (4, or 2 when K = 16) columns per round -- all kWsCols x K neighbour loads and
+//     the kWsCols Phi(row, j) loads issued before the first FMA -- and forms
+//     Y(row, j) = d(row) Phi(row, j) + sum_k a_k Phi(c_k, j), reusing the Phi
+//     tile element for the diagonal.  One lane streams the ELL slices two bands
+//     ahead and the Phi rows `reach` + one band ahead into L2.
+//   * NCW = 4 consumer warps (one per SM sub-partition) contract each stage on
+//     the fp64 tensor cores.  For the common fragment grids (TA x TB = 7x7,
+//     8x8) the grid is split into four compile-time fragment ranges (no
+//     predicated MMAs); other shapes use a runtime x-row split.
+// Stage handshakes are named barriers: FULL(s) = 1 + s, EMPTY(s) = 1 + S + s
+// (all threads); barrier 15 orders the producers' reuse of ELL buffers.
+constexpr int kWsRows = 64;
+constexpr int kWsLd = kWsRows + 8;  // 72: conflict-free 16-byte fragment loads
+constexpr int kWsNPW = 12, kWsNCW = 4;
+constexpr int kWsThreads = (kWsNPW + kWsNCW) * 32;
+constexpr int kWsProdBar = 15;
+constexpr int kWsProdRegs = 136, kWsConsRegs = 96;  // setmaxnreg targets (see k_spatial_ell)
+
+struct EllArgs {
+  int64_t N;
+  const uint32_t* eidx;  // per tile: [K][64] off-diagonal column indices
+  const double* eval;    // per tile: [K][64] off-diagonal values, then [64] diagonal values
+  int64_t reach;         // max (col - row) over off-diagonal entries; < 0: no Phi prefetch
+  const double* phi;
+  int64_t ld;
+  int ns;
+  const double* extra;   // column-major N x ne (ld ext_ld)
+  int64_t ext_ld;
+  int ne;
+  const double* xref;    // N or null
+  int q, MA, NQ, S;
+  int dbg;               // diagnostics: 1 = producers skip the gathers, 2 = consumers skip the MMAs
+  double* part;          // gridDim.x x (MA * NQ)
+  unsigned long long* tbuf;  // diagnostics: per-warp phase cycle totals (dbg 5)
+};
+
+// Stage position of tile row i: rows 8u + t (k-step 2u) and 8u + 4 + t (k-step
+// 2u + 1) sit side by side, so one 16-byte load gives a lane both k-steps'
+// fragment values (the Gram sums over rows, so any common row order works).
+__device__ __forceinline__ int ws_pos(int i) { return (i & ~7) | ((i & 3) << 1) | ((i >> 2) & 1); }
+
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+template <int TB, int F0, int F1>
+__host__ __device__ constexpr bool frag_col_used(int y) {
+  for (int f = F0; f < F1; ++f)
+    if (f % TB == y) return true;
+  return false;
+}
+
+// consumer loop over a compile-time fragment range [F0, F1) of the TA x TB grid
+template <int TA, int TB, int F0, int F1>
+__device__ __forceinline__ void ell_consume(const EllArgs& A, const double* smem, int stage_elems, int nmine,
+                                            double* mp) {
+  constexpr int NF = F1 - F0, X0 = F0 / TB, X1 = (F1 - 1) / TB;
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  double acc[NF][2];
+#pragma unroll
+  for (int f = 0; f < NF; ++f) acc[f][0] = acc[f][1] = 0.0;
+  long long pw = 0, pc = 0;
+  for (int it = 0; it < nmine; ++it) {
+    const int s = it % A.S;
+    long long t0 = clock64();
+    named_bar_sync(1 + s, kWsThreads);
+    long long t1 = clock64(); pw += t1 - t0;
+    const double* Ph = smem + (int64_t)s * stage_elems;
+    const double* Ys = Ph + A.MA * kWsLd;
+#pragma unroll 1
+    for (int u = 0; u < (A.dbg == 2 ? 0 : kWsRows / 8); ++u) {  // k-step pairs
+      const int kp = u * 8 + 2 * t;
+      double2 a[X1 - X0 + 1], b[TB];
+#pragma unroll
+      for (int x = X0; x <= X1; ++x) a[x - X0] = *reinterpret_cast<const double2*>(Ph + (x * 8 + g) * kWsLd + kp);
+#pragma unroll
+      for (int y = 0; y < TB; ++y)
+        if (frag_col_used<TB, F0, F1>(y)) b[y] = *reinterpret_cast<const double2*>(Ys + (y * 8 + g) * kWsLd + kp);
+#pragma unroll
+      for (int f = F0; f < F1; ++f) dmma884(acc[f - F0][0], acc[f - F0][1], a[f / TB - X0].x, b[f % TB].x);
+#pragma unroll
+      for (int f = F0; f < F1; ++f) dmma884(acc[f - F0][0], acc[f - F0][1], a[f / TB - X0].y, b[f % TB].y);
+    }
+    pc += clock64() - t1;
+    if (it + A.S < nmine) named_bar_arrive(1 + A.S + s, kWsThreads);
+  }
+  if (A.tbuf && lane == 0) {
+    atomicAdd(A.tbuf + (threadIdx.x >> 5) * 8 + 0, (unsigned long long)pw);
+    atomicAdd(A.tbuf + (threadIdx.x >> 5) * 8 + 1, (unsigned long long)pc);
+  }
+#pragma unroll
+  for (int f = F0; f < F1; ++f) {
+    const int r = (f / TB) * 8 + g, cc = (f % TB) * 8 + 2 * t;
+    mp[r * A.NQ + cc] = acc[f - F0][0];
+    mp[r * A.NQ + cc + 1] = acc[f - F0][1];
+  }
+}
+
+// consumer loop for runtime TA, TB <= 8: warp c owns x-rows c and c + 4
+__device__ __forceinline__ void ell_consume_generic(const EllArgs& A, const double* smem, int stage_elems, int nmine,
+                                                    double* mp, int c) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int TA = A.MA / 8, TB = A.NQ / 8;
+  double acc[2][8][2];
+#pragma unroll
+  for (int x = 0; x < 2; ++x)
+#pragma unroll
+    for (int y = 0; y < 8; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+  for (int it = 0; it < nmine; ++it) {
+    const int s = it % A.S;
+    named_bar_sync(1 + s, kWsThreads);
+    const double* Ph = smem + (int64_t)s * stage_elems;
+    const double* Ys = Ph + A.MA * kWsLd;
+#pragma unroll 1
+    for (int u = 0; u < (A.dbg == 2 ? 0 : kWsRows / 8); ++u) {
+      const int kp = u * 8 + 2 * t;
+      double2 b[8];
+#pragma unroll
+      for (int y = 0; y < 8; ++y)
+        b[y] = (y < TB) ? *reinterpret_cast<const double2*>(Ys + (y * 8 + g) * kWsLd + kp) : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int x = 0; x < 2; ++x) {
+        const int ta = c + kWsNCW * x;
+        if (ta < TA) {
+          const double2 av = *reinterpret_cast<const double2*>(Ph + (ta * 8 + g) * kWsLd + kp);
+#pragma unroll
+          for (int y = 0; y < 8; ++y)
+            if (y < TB) dmma884(acc[x][y][0], acc[x][y][1], av.x, b[y].x);
+#pragma unroll
+          for (int y = 0; y < 8; ++y)
+            if (y < TB) dmma884(acc[x][y][0], acc[x][y][1], av.y, b[y].y);
+        }
+      }
+    }
+    if (it + A.S < nmine) named_bar_arrive(1 + A.S + s, kWsThreads);
+  }
+#pragma unroll
+  for (int x = 0; x < 2; ++x) {
+    const int ta = c + kWsNCW * x;
+    if (ta >= TA) continue;
+#pragma unroll
+    for (int y = 0; y < 8; ++y) {
+      if (y >= TB) continue;
+      const int r = ta * 8 + g, cc = y * 8 + 2 * t;
+      mp[r * A.NQ + cc] = acc[x][y][0];
+      mp[r * A.NQ + cc + 1] = acc[x][y][1];
+    }
+  }
+}
+
+__host__ __device__ inline size_t ell_tile_bytes(int K) { return (size_t)K * kWsRows * 4 + (size_t)(K + 1) * kWsRows * 8; }
+
+template <int K, int TA, int TB>
+__global__ void __launch_bounds__(kWsThreads, 1) k_spatial_ell(EllArgs A) {
+  extern __shared__ __align__(128) double smem[];
+  constexpr int NCG = kWsNPW / 2;
+  // columns gathered per round: kWsCols x (K + 1) loads in flight per lane, sized for the
+  // producers' 136-register budget after the warpgroup register handoff below
+  constexpr int kWsCols = K <= 4 ? 8 : K <= 6 ? 6 : K <= 8 ? 4 : 2;
+  const int stage_elems = (A.MA + A.NQ) * kWsLd;
+  unsigned char* ebase = reinterpret_cast<unsigned char*>(smem + (int64_t)A.S * stage_elems);
+  uint64_t* ebar = reinterpret_cast<uint64_t*>(ebase + 2 * ell_tile_bytes(K));
+  const double** colbase = reinterpret_cast<const double**>(ebar + 2);  // Phi column j at colbase[j]
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t ntiles = ceil_div(A.N, kWsRows);
+  const int nmine = (int)(blockIdx.x < ntiles ? ceil_div(ntiles - blockIdx.x, gridDim.x) : 0);
+  auto tile_of = [&](int it) -> int64_t { return blockIdx.x + (int64_t)it * gridDim.x; };
+  constexpr unsigned kIdxBytes = K * kWsRows * 4, kValBytes = (K + 1) * kWsRows * 8;
+  auto issue_ell = [&](int it) {  // ELL slices of this CTA's tile `it` into buffer it & 1
+    const int64_t tile = tile_of(it);
+    unsigned char* buf = ebase + (it & 1) * ell_tile_bytes(K);
+    mbar_expect_tx(&ebar[it & 1], kIdxBytes + kValBytes);
+    bulk_g2s(buf, A.eidx + tile * K * kWsRows, kIdxBytes, &ebar[it & 1]);
+    bulk_g2s(buf + kIdxBytes, A.eval + tile * (K + 1) * kWsRows, kValBytes, &ebar[it & 1]);
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(&ebar[0], 1);
+    mbar_init(&ebar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (nmine > 0) issue_ell(0);
+  }
+  if (threadIdx.x < 64) colbase[threadIdx.x] = A.phi + (int64_t)(threadIdx.x < A.ns ? threadIdx.x : 0) * A.ld;
+  __syncthreads();
+
+  if (wid < kWsNPW) {
+    // ------------------------------------------------------------ producers
+    // register handoff inside the CTA's launch allocation (512 x 128): the
+    // consumer warpgroup drops to 96 registers, the three producer warpgroups
+    // rise to 136 (3 * 128 * 136 + 128 * 96 = 64512; checked on the host)
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 136;\n" ::: "memory");
+    const int half = wid & 1, cg = wid >> 1;
+    const int i = half * 32 + lane;
+    const int ip = ws_pos(i);  // stage position of row i
+    const int64_t ld = A.ld;
+    long long ph[5] = {0, 0, 0, 0, 0};
+    for (int it = 0; it < nmine; ++it) {
+      const int s = it % A.S;
+      const int64_t tile = tile_of(it);
+      const int64_t row0 = tile * kWsRows, row = row0 + i;
+      const bool live = row < A.N;
+      long long tc0 = clock64();
+      named_bar_sync(kWsProdBar, kWsNPW * 32);  // every producer is past tile it-1: its ELL buffer is free
+      long long tc1 = clock64(); ph[0] += tc1 - tc0;
+      if (lane == 0) {
+        // L2 prefetch, spread over the producer warps: the operator slices and
+        // dense extra columns of the tile three ahead, and Phi rows one band past
+        // the operator's forward reach (the gathers' first touch of a row)
+        const int64_t tp = it + 3 < nmine ? tile_of(it + 3) : ntiles;
+        if (wid == 0) {
+          if (it + 1 < nmine) issue_ell(it + 1);
+          if (tp < ntiles) {
+            prefetch_l2_bulk(A.eidx + tp * K * kWsRows, kIdxBytes);
+            prefetch_l2_bulk(A.eval + tp * (K + 1) * kWsRows, kValBytes);
+          }
+        }
+        if (tp * kWsRows + kWsRows <= A.N)
+          for (int e = wid; e < A.ne; e += kWsNPW) prefetch_l2_bulk(A.extra + e * A.ext_ld + tp * kWsRows, kWsRows * 8);
+        const int64_t pr = row0 + A.reach + (int64_t)gridDim.x * kWsRows;
+        if (A.reach >= 0 && pr + kWsRows <= A.N)
+          for (int j = wid; j < A.ns; j += kWsNPW) prefetch_l2_bulk(A.phi + j * A.ld + pr, kWsRows * 8);
+      }
+      long long tc2 = clock64();
+      mbar_wait(&ebar[it & 1], (it >> 1) & 1);
+      ph[1] += clock64() - tc2;
+      const unsigned char* buf = ebase + (it & 1) * ell_tile_bytes(K);
+      const uint32_t* bi = reinterpret_cast<const uint32_t*>(buf);
+      const double* bv = reinterpret_cast<const double*>(buf + kIdxBytes);
+      uint32_t ci[K];
+      double cv[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        ci[k] = bi[k * kWsRows + i];
+        cv[k] = bv[k * kWsRows + i];
+      }
+      const double dv = bv[K * kWsRows + i];
+      if (A.dbg == 3) {  // diagnostics: every neighbour is the row itself (L1-resident gathers)
+#pragma unroll
+        for (int k = 0; k < K; ++k) ci[k] = (uint32_t)(live ? row : A.N - 1);
+      }
+      long long tc3 = clock64();
+      if (it >= A.S) named_bar_sync(1 + A.S + s, kWsThreads);
+      long long tc4 = clock64(); ph[2] += tc4 - tc3;
+      double* Ph = smem + (int64_t)s * stage_elems;
+      double* Ys = Ph + A.MA * kWsLd;
+      // A Phi and Phi columns, kWsCols per round: j_m = cg + NCG * (r * kWsCols + m);
+      // a fixed round count with warp-uniform predicates keeps every round's
+      // kWsCols x (K + 1) loads in one batch ahead of the FMAs.
+      constexpr int kRounds = ((64 + NCG - 1) / NCG + kWsCols - 1) / kWsCols;
+      const int nsg = A.dbg == 1 ? 0 : A.ns;
+      const uint32_t self = (uint32_t)(live ? row : A.N - 1);
+#pragma unroll 1
+      for (int r = 0; r < kRounds; ++r) {
+        const int jb = cg + NCG * r * kWsCols;
+        if (jb >= nsg) break;
+        const double* cb[kWsCols];
+        bool on[kWsCols];
+#pragma unroll
+        for (int m = 0; m < kWsCols; ++m) {
+          const int jm = jb + m * NCG;
+          on[m] = jm < nsg;
+          cb[m] = colbase[on[m] ? jm : jb];  // loaded, so address = base + 8 * index stays one IMAD.WIDE
+        }
+        double v[kWsCols][K + 1];
+#pragma unroll
+        for (int m = 0; m < kWsCols; ++m) {
+#pragma unroll
+          for (int k = 0; k < K; ++k) v[m][k] = __ldg(cb[m] + ci[k]);
+          v[m][K] = __ldg(cb[m] + self);
+        }
+#pragma unroll
+        for (int m = 0; m < kWsCols; ++m) {
+          const double p = live ? v[m][K] : 0.0;
+          double y = dv * p;
+#pragma unroll
+          for (int k = 0; k < K; ++k) y = fma(cv[k], v[m][k], y);
+          const int jm = jb + m * NCG;
+          if (on[m]) {
+            Ph[jm * kWsLd + ip] = p;
+            Ys[jm * kWsLd + ip] = y;
+          }
+        }
+      }
+      long long tc5 = clock64(); ph[3] += tc5 - tc4;
+      // dense extra columns, A x_ref, zero padding (columns of this group past ns)
+      for (int j = cg + ((A.ns - cg + NCG - 1) / NCG) * NCG; j < A.NQ; j += NCG) {
+        double y = 0.0;
+        if (j < A.ns + A.ne) {
+          if (live) y = __ldg(A.extra + (int64_t)(j - A.ns) * A.ext_ld + row);
+        } else if (j < A.q) {  // A x_ref
+          y = live ? dv * __ldg(A.xref + row) : 0.0;
+#pragma unroll
+          for (int k = 0; k < K; ++k) y = fma(cv[k], __ldg(A.xref + ci[k]), y);
+        }
+        Ys[j * kWsLd + ip] = y;
+        if (j < A.MA) Ph[j * kWsLd + ip] = 0.0;
+      }
+      ph[4] += clock64() - tc5;
+      named_bar_arrive(1 + s, kWsThreads);
+    }
+    if (A.tbuf && lane == 0)
+      for (int q = 0; q < 5; ++q) atomicAdd(A.tbuf + wid * 8 + q, (unsigned long long)ph[q]);
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 96;\n" ::: "memory");
+  const int c = wid - kWsNPW;
+  double* mp = A.part + (int64_t)blockIdx.x * A.MA * A.NQ;
+  if constexpr (TA > 0) {
+    constexpr int NF = TA * TB;
+    if (c == 0) ell_consume<TA, TB, 0, NF / 4>(A, smem, stage_elems, nmine, mp);
+    else if (c == 1) ell_consume<TA, TB, NF / 4, NF / 2>(A, smem, stage_elems, nmine, mp);
+    else if (c == 2) ell_consume<TA, TB, NF / 2, 3 * NF / 4>(A, smem, stage_elems, nmine, mp);
+    else ell_consume<TA, TB, 3 * NF / 4, NF>(A, smem, stage_elems, nmine, mp);
+  } else {
+    ell_consume_generic(A, smem, stage_elems, nmine, mp, c);
+  }
+}
+
+// CSR -> tiled ELL: per 64-row tile, K off-diagonal slots (column index,
+// value; an unused slot points at the row itself with value 0) and the
+// diagonal (sum of the row's diagonal entries).  Also the operator's forward
+// reach max(col - row) over off-diagonal entries and an overflow flag (a row
+// with more than K off-diagonal entries).  One thread per row.
+template <typename IdxT>
+__global__ void k_csr_to_ell(int64_t n, const IdxT* __restrict__ indptr, const IdxT* __restrict__ indices,
+                             const double* __restrict__ data, int K, uint32_t* __restrict__ eidx,
+                             double* __restrict__ eval, unsigned long long* reach_enc, int* overflow) {
+  const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nt = ceil_div(n, kWsRows);
+  if (row >= nt * kWsRows) return;
+  const int64_t tile = row / kWsRows;
+  const int i = (int)(row % kWsRows);
+  const uint32_t self = (uint32_t)(row < n ? row : n - 1);
+  uint32_t* ti = eidx + tile * K * kWsRows;
+  double* tv = eval + tile * (K + 1) * kWsRows;
+  int64_t e0 = 0, e1 = 0;
+  if (row < n) { e0 = (int64_t)indptr[row]; e1 = (int64_t)indptr[row + 1]; }
+  long long reach = LLONG_MIN;
+  double diag = 0.0;
+  int k = 0;
+  for (int64_t e = e0; e < e1; ++e) {
+    const int64_t c = (int64_t)indices[e];
+    if (c == row) { diag += data[e]; continue; }
+    if (k == K) { atomicExch(overflow, 1); break; }
+    ti[k * kWsRows + i] = (uint32_t)c;
+    tv[k * kWsRows + i] = data[e];
+    reach = max(reach, (long long)(c - row));
+    ++k;
+  }
+  for (; k < K; ++k) {
+    ti[k * kWsRows + i] = self;
+    tv[k * kWsRows + i] = 0.0;
+  }
+  tv[K * kWsRows + i] = diag;
+  // order-preserving encoding of a signed max as an unsigned atomicMax
+  if (reach != LLONG_MIN) atomicMax(reach_enc, (unsigned long long)reach ^ 0x8000000000000000ull);
+}
+
+// out (ns x q, row-major) = sum over CTAs of the partials.  A CTA owns 32
+// outputs; warp w sums the partials of its contiguous slice of CTAs, and the
+// eight slice sums are added in slice order (deterministic).
+__global__ void __launch_bounds__(256) k_spatial_reduce(const double* part, int nparts, int MA, int NQ, int ns, int q,
+                                                        double* out) {
+  __shared__ double red[8][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int idx = blockIdx.x * 32 + lane;
+  const bool live = idx < ns * q;
+  const int a = live ? idx / q : 0, b = live ? idx % q : 0;
+  const double* p0 = part + a * NQ + b;
+  const int64_t st = (int64_t)MA * NQ;
+  const int per = (nparts + 7) / 8, pb = w * per, pe = min(nparts, pb + per);
+  double s0 = 0.0, s1 = 0.0;
+  int p = pb;
+  for (; p + 1 < pe; p += 2) {
+    s0 += p0[p * st];
+    s1 += p0[(p + 1) * st];
+  }
+  if (p < pe) s0 += p0[p * st];
+  red[w][lane] = s0 + s1;
+  __syncthreads();
+  if (w == 0 && live) {
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += red[k][lane];
+    out[idx] = t;
+  }
 }
 
 // grid = SMs x resident CTAs of the chosen kernel (one wave), capped by the tiles
@@ -365,6 +760,36 @@ int launch_spatial_t(SpatialArgs<IdxT> a, int max_grid, cudaStream_t s) {
   }
   STROM_LAUNCH_CHECK();
   return grid;
+}
+
+size_t ell_smem(int K, int S, int MA, int NQ) {
+  return (size_t)S * (MA + NQ) * kWsLd * 8 + 2 * ell_tile_bytes(K) + 16 + 64 * 8;
+}
+
+template <int K, int TA, int TB>
+void launch_ell_kernel(const EllArgs& a, int grid, size_t smem, cudaStream_t s) {
+  auto kern = k_spatial_ell<K, TA, TB>;
+  static bool configured = false;
+  if (!configured) {
+    STROM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_smem_optin()));
+    // the warpgroup register handoff must fit the launch allocation, or the
+    // producers' setmaxnreg.inc would wait forever
+    cudaFuncAttributes fa{};
+    STROM_CUDA(cudaFuncGetAttributes(&fa, kern));
+    if ((int64_t)fa.numRegs * kWsThreads < (int64_t)kWsNPW * 32 * kWsProdRegs + (int64_t)kWsNCW * 32 * kWsConsRegs)
+      throw Error(kInternal, "spatial ELL kernel: register handoff exceeds the launch allocation");
+    configured = true;
+  }
+  kern<<<grid, kWsThreads, smem, s>>>(a);
+  STROM_LAUNCH_CHECK();
+}
+
+template <int K>
+void launch_spatial_ell_k(const EllArgs& a, int grid, size_t smem, cudaStream_t s) {
+  const int TA = a.MA / 8, TB = a.NQ / 8;
+  if (TA == 7 && TB == 7) launch_ell_kernel<K, 7, 7>(a, grid, smem, s);
+  else if (TA == 8 && TB == 8) launch_ell_kernel<K, 8, 8>(a, grid, smem, s);
+  else launch_ell_kernel<K, 0, 0>(a, grid, smem, s);
 }
 
 template <typename IdxT>
@@ -431,9 +856,107 @@ int strom_spatial_reduce_csr(int64_t n, const void* indptr_dev, const void* indi
       a.indices = static_cast<const int64_t*>(indices_dev);
       grid = launch_spatial(a, max_grid, s);
     }
-    k_spatial_reduce<<<(unsigned)ceil_div((int64_t)ns * q, 256), 256, 0, s>>>(part->as<double>(), grid, MA, NQ,
+    k_spatial_reduce<<<(unsigned)ceil_div((int64_t)ns * q, 32), 256, 0, s>>>(part->as<double>(), grid, MA, NQ,
                                                                               (int)ns, q, out_dev);
     STROM_LAUNCH_CHECK();
+  });
+}
+
+
+// Tiled ELL form of a CSR operator for strom_spatial_reduce_ell (the device
+// layout the spatial reduction gathers from; built once per operator).
+// K >= max off-diagonal entries per row, K in {4, 6, 8, 16}.  eidx_dev:
+// uint32[ceil(n/64) * K * 64], eval_dev: double[ceil(n/64) * (K+1) * 64].
+// *reach_out (host) = max(col - row) over the off-diagonal entries (-1: none).
+int strom_csr_to_ell(int64_t n, const void* indptr_dev, const void* indices_dev, const double* data_dev,
+                     int32_t index_bits, int32_t K, uint32_t* eidx_dev, double* eval_dev, int64_t* reach_out,
+                     void* stream) {
+  return guarded([&] {
+    STROM_REQUIRE(n >= 1 && n < (int64_t(1) << 31), "ELL operator needs 1 <= n < 2^31 rows");
+    STROM_REQUIRE(K == 4 || K == 6 || K == 8 || K == 16, "ELL width must be 4, 6, 8 or 16");
+    STROM_REQUIRE(index_bits == 32 || index_bits == 64, "index_bits must be 32 or 64");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    auto flags = dev_alloc(16, s, true);
+    unsigned long long* enc = flags->as<unsigned long long>();
+    int* overflow = reinterpret_cast<int*>(enc + 1);
+    const int64_t rows = ceil_div(n, kWsRows) * kWsRows;
+    const unsigned grid = (unsigned)ceil_div(rows, 256);
+    if (index_bits == 32)
+      k_csr_to_ell<int32_t><<<grid, 256, 0, s>>>(n, static_cast<const int32_t*>(indptr_dev),
+                                                static_cast<const int32_t*>(indices_dev), data_dev, K, eidx_dev,
+                                                eval_dev, enc, overflow);
+    else
+      k_csr_to_ell<int64_t><<<grid, 256, 0, s>>>(n, static_cast<const int64_t*>(indptr_dev),
+                                                static_cast<const int64_t*>(indices_dev), data_dev, K, eidx_dev,
+                                                eval_dev, enc, overflow);
+    STROM_LAUNCH_CHECK();
+    unsigned long long h[2] = {0, 0};
+    STROM_CUDA(cudaMemcpyAsync(h, flags->ptr, 16, cudaMemcpyDeviceToHost, s));
+    STROM_CUDA(cudaStreamSynchronize(s));
+    STROM_REQUIRE((h[1] & 0xffffffffull) == 0, "ELL width too small for a row of the operator");
+    *reach_out = h[0] == 0 ? -1 : (int64_t)(h[0] ^ 0x8000000000000000ull);
+  });
+}
+
+// build_spatial_rom's contractions (spatial.py:57-64) from the tiled ELL form:
+// column-major phi (element (i, j) at phi[i + j*ld]), ns <= 64 and
+// q = ns + ne + (xref != NULL) <= 64.  Output as strom_spatial_reduce_csr.
+int strom_spatial_reduce_ell(int64_t n, int32_t K, const uint32_t* eidx_dev, const double* eval_dev, int64_t reach,
+                             const double* phi_dev, int64_t ld, int64_t ns, const double* extra_dev, int64_t ext_ld,
+                             int64_t ne, const double* xref_dev, double* out_dev, void* stream) {
+  return guarded([&] {
+    STROM_REQUIRE(n >= 1 && n < (int64_t(1) << 31) && ld >= n, "bad ELL spatial-reduction shape");
+    STROM_REQUIRE(K == 4 || K == 6 || K == 8 || K == 16, "ELL width must be 4, 6, 8 or 16");
+    const int q = (int)(ns + ne + (xref_dev ? 1 : 0));
+    STROM_REQUIRE(ns >= 1 && ns <= 64 && ne >= 0 && q <= 64, "ELL spatial reduction supports n_s, q <= 64");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    EllArgs a{};
+    a.N = n;
+    a.eidx = eidx_dev;
+    a.eval = eval_dev;
+    a.reach = (reach >= 0 && reach < n / 4) ? reach : -1;
+    a.phi = phi_dev;
+    a.ld = ld;
+    a.ns = (int)ns;
+    a.extra = extra_dev;
+    a.ext_ld = ext_ld;
+    a.ne = (int)ne;
+    a.xref = xref_dev;
+    a.q = q;
+    a.MA = (int)round_up(ns, 8);
+    a.NQ = (int)round_up(q, 8);
+    a.S = ell_smem(K, 3, a.MA, a.NQ) <= max_smem_optin() ? 3 : 2;
+    if (const char* e = getenv("STROM_SPATIAL_DBG")) a.dbg = atoi(e);
+    if (getenv("STROM_SPATIAL_NOPF")) a.reach = -1;
+    if (const char* e = getenv("STROM_SPATIAL_STAGES")) a.S = std::max(1, std::min(a.S, atoi(e)));
+    const size_t smem = ell_smem(K, a.S, a.MA, a.NQ);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sm_count(), ceil_div(n, kWsRows)));
+    auto part = dev_alloc((size_t)grid * a.MA * a.NQ * 8, s, false);
+    a.part = part->as<double>();
+    DevMemPtr tb;
+    if (a.dbg == 5) {
+      tb = dev_alloc(32 * 8 * 8, s, true);
+      a.tbuf = tb->as<unsigned long long>();
+    }
+    {
+      ProfScope ps(P_SPATIAL, s);
+      if (K == 4) launch_spatial_ell_k<4>(a, grid, smem, s);
+      else if (K == 6) launch_spatial_ell_k<6>(a, grid, smem, s);
+      else if (K == 8) launch_spatial_ell_k<8>(a, grid, smem, s);
+      else launch_spatial_ell_k<16>(a, grid, smem, s);
+    }
+    k_spatial_reduce<<<(unsigned)ceil_div((int64_t)ns * q, 32), 256, 0, s>>>(part->as<double>(), grid, a.MA, a.NQ,
+                                                                            (int)ns, q, out_dev);
+    STROM_LAUNCH_CHECK();
+    if (tb) {
+      unsigned long long h[128];
+      STROM_CUDA(cudaMemcpyAsync(h, tb->ptr, sizeof(h), cudaMemcpyDeviceToHost, s));
+      STROM_CUDA(cudaStreamSynchronize(s));
+      for (int w = 0; w < 16; ++w)
+        fprintf(stderr, "warp %2d cycles/CTA: %10.0f %10.0f %10.0f %10.0f %10.0f\n", w, h[w * 8] / (double)grid,
+                h[w * 8 + 1] / (double)grid, h[w * 8 + 2] / (double)grid, h[w * 8 + 3] / (double)grid,
+                h[w * 8 + 4] / (double)grid);
+    }
   });
 }
 

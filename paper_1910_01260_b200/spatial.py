@@ -45,24 +45,33 @@ def _phi_strides(phi: torch.Tensor) -> tuple[torch.Tensor, int, int]:
     return phi, phi.stride(0), phi.stride(1)
 
 
-def spatial_reduce(dev: dict, phi: torch.Tensor, extra: torch.Tensor | None, xref: torch.Tensor | None,
-                   stream=None) -> torch.Tensor:
-    """Phi^T [A Phi | extra | A xref] as one (n_s x q) tensor (C ABI strom_spatial_reduce_csr)."""
+def spatial_reduce(dev: dict, phi: torch.Tensor, extra_cm: torch.Tensor | None, ne: int,
+                   xref: torch.Tensor | None, stream=None) -> torch.Tensor:
+    """Phi^T [A Phi | extra | A xref] as one (n_s x q) tensor (C ABI strom_spatial_reduce_csr).
+
+    ``extra_cm`` holds the extra right-hand columns column-major, as the rows of a
+    C-contiguous (>= ne, N) tensor; the first ``ne`` are used."""
     n, ns = phi.shape
     phi, rs, cs = _phi_strides(phi)
-    ne = 0 if extra is None else extra.shape[1]
     ext_ptr, ext_ld = None, n
-    if extra is not None:
-        ecm = extra.t().contiguous()  # column-major N x ne
-        ext_ptr = ecm.data_ptr()
+    if extra_cm is not None and ne > 0:
+        assert extra_cm.is_contiguous() and extra_cm.shape[1] == n
+        ext_ptr = extra_cm.data_ptr()
+    else:
+        ne = 0
     q = ns + ne + (1 if xref is not None else 0)
     out = torch.empty((ns, q), dtype=F64, device=phi.device)
+    ell = dev.get("ell")
+    if ell is not None and rs == 1 and ns <= 64 and q <= 64:
+        # column-major Phi: warp-specialised gather from the tiled-ELL operator
+        capi.call("strom_spatial_reduce_ell", n, ell["k"], ell["idx"].data_ptr(), ell["val"].data_ptr(),
+                  ell["reach"], phi.data_ptr(), cs, ns, ext_ptr, ext_ld, ne,
+                  None if xref is None else xref.data_ptr(), out.data_ptr(), capi.stream_ptr(stream))
+        return out
     capi.call("strom_spatial_reduce_csr", n, dev["indptr"].data_ptr(), dev["indices"].data_ptr(),
               dev["data"].data_ptr(), dev["index_bits"], phi.data_ptr(), rs, cs, ns, ext_ptr, ext_ld, ne,
               None if xref is None else xref.data_ptr(), out.data_ptr(),
               capi.stream_ptr(stream))
-    if extra is not None:
-        del ecm
     return out
 
 
@@ -77,21 +86,22 @@ def build_spatial_rom(sys: LinearDynamicalSystem, basis: BasisSet,
     dev = sys.device_arrays()
     n, ns = phi.shape
     m, p = dev["b"].shape[1], dev["c"].shape[1]
+    # extras: dev["bcx0"] is [B | C | x0] column-major.  With x_ref = x0 the
+    # x0 - x_ref column is exactly zero (x0_hat = 0) and A x_ref is one more
+    # gathered column; with x_ref = 0 the A x_ref column is exactly zero.
     if ref_mode == "initial_state":
         x_ref = dev["x0"]
-        x0_minus = torch.zeros_like(x_ref)
-        xref_col = x_ref
+        z = spatial_reduce(dev, phi, dev["bcx0"], m + p, x_ref)
+        x0_hat = torch.zeros(ns, dtype=F64, device=phi.device)
+        x_ref_hat = z[:, -1].contiguous()
     else:
         x_ref = torch.zeros(n, dtype=F64, device=phi.device)
-        x0_minus = dev["x0"]
-        xref_col = None  # A 0 = 0 exactly: no column
-    extra = torch.cat([dev["b"], dev["c"], x0_minus[:, None]], dim=1)
-    z = spatial_reduce(dev, phi, extra, xref_col)
+        z = spatial_reduce(dev, phi, dev["bcx0"], m + p + 1, None)
+        x0_hat = z[:, ns + m + p].contiguous()
+        x_ref_hat = torch.zeros(ns, dtype=F64, device=phi.device)
     a_hat = z[:, :ns].contiguous()
     b_hat = z[:, ns:ns + m].contiguous()
     c_hat = z[:, ns + m:ns + m + p].contiguous()
-    x0_hat = z[:, ns + m + p].contiguous()
-    x_ref_hat = z[:, -1].contiguous() if xref_col is not None else torch.zeros(ns, dtype=F64, device=phi.device)
-    y_ref = dev["c"].T @ x_ref
+    y_ref = dev["c"].T @ x_ref if ref_mode == "initial_state" else torch.zeros(p, dtype=F64, device=phi.device)
     return SpatialRom(a_hat=a_hat, b_hat=b_hat, c_hat=c_hat, x_ref=x_ref, x_ref_hat=x_ref_hat,
                       x0_hat=x0_hat, y_ref=y_ref, ref_mode=ref_mode)

@@ -101,7 +101,7 @@ class LinearDynamicalSystem:
         return self.c.shape[1]
 
     def device_arrays(self) -> dict:
-        """HBM-resident copies: CSR (indptr, indices, data, index_bits), B|C dense, x0."""
+        """HBM-resident copies: CSR (indptr, indices, data, index_bits), B|C dense, x0, [B|C|x0]."""
         if self._dev is None:
             dev = device()
             a = self.a
@@ -117,4 +117,26 @@ class LinearDynamicalSystem:
                 c=torch.as_tensor(self.c, dtype=F64, device=dev),
                 x0=torch.as_tensor(self.x0, dtype=F64, device=dev),
             )
+            # tiled-ELL form of A for the spatial reduction's fast path (diagonal
+            # apart, at most 16 off-diagonal entries per row; built once per
+            # operator on the device)
+            rows = np.repeat(np.arange(a.shape[0]), np.diff(a.indptr))
+            offd = np.bincount(rows[a.indices != rows], minlength=a.shape[0]) if a.nnz else np.zeros(1, int)
+            kell = next((k for k in (4, 6, 8, 16) if int(offd.max()) <= k), None)
+            if kell is not None and not big:
+                from . import _capi as capi
+
+                nt = -(-a.shape[0] // 64)
+                eidx = torch.empty(nt * kell * 64, dtype=torch.int32, device=dev)  # uint32 on the device
+                evals = torch.empty(nt * (kell + 1) * 64, dtype=F64, device=dev)
+                reach = capi.i64(0)
+                d = self._dev
+                capi.call("strom_csr_to_ell", a.shape[0], d["indptr"].data_ptr(), d["indices"].data_ptr(),
+                          d["data"].data_ptr(), d["index_bits"], kell, eidx.data_ptr(), evals.data_ptr(),
+                          capi.C.byref(reach), capi.stream_ptr())
+                self._dev["ell"] = dict(k=kell, idx=eidx, val=evals, reach=int(reach.value))
+            # [B | C | x0] column-major (rows of a C-contiguous tensor): the dense
+            # right-hand columns of the spatial reduction, read in place
+            self._dev["bcx0"] = torch.cat([self._dev["b"].T, self._dev["c"].T, self._dev["x0"][None, :]],
+                                          dim=0).contiguous()
         return self._dev
