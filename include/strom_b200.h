@@ -186,6 +186,15 @@ int strom_spatial_reduce_ell(int64_t n, int32_t K, const uint32_t* eidx_dev, con
                              const double* phi_dev, int64_t ld, int64_t ns, const double* extra_dev, int64_t ext_ld,
                              int64_t ne, const double* xref_dev, double* out_dev, void* stream);
 
+/* Workload generator (bench/test support, not a reference interface): nb
+ * columns t0 .. t0+nb-1 of the capacity stream X = Q diag(sigma) W^T + E with
+ * an implicit randomized-Hadamard Q (Q[i,c] = s_i (-1)^popcount(i & p_c) /
+ * sqrt(n), n = 2^m, never stored) and counter-hash Gaussian noise.
+ * coef_dev[c*nb + b] = sigma_c W[t0+b, c]; prow_dev: rank distinct Hadamard
+ * rows; out_dev: n x nb column-major (ldo).  nb in {1, 2, 4, 8, 16}. */
+int strom_gen_lowrank_batch(int64_t n, int32_t rank, int32_t nb, const double* coef_dev, const int64_t* prow_dev,
+                            uint64_t seed, int64_t t0, double noise, double* out_dev, int64_t ldo, void* stream);
+
 /* ------------------------------------------------------------------------
  * Space-time reduced system  (spacetime.py:43-115 build_st_matrix /
  * build_st_input / build_st_init, spacetime.py:128-151 build_st_rom)

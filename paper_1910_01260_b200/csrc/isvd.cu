@@ -207,6 +207,14 @@ Caps make_caps(int64_t n, int32_t r_max, int32_t want_r, int64_t k) {
   if (rc > 254) throw Error(kInvalidArgument, "rank capacity above 254 is not supported by this build");
   c.rcap = (int32_t)rc;
   c.ccap = std::min<int32_t>(256, c.rcap + 1 + slack_for(c.rcap));
+  // capacity: a compaction holds two stores at once; keep both within ~80% of
+  // HBM by trimming the slack (cfg5: 2^26 rows, 0.54 GB per column)
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && total_b > 0) {
+    const int64_t col_bytes = round_up(n, 128) * 8;
+    const int64_t max_cols = (int64_t)(0.40 * (double)total_b) / col_bytes;
+    if (c.ccap > max_cols) c.ccap = (int32_t)std::max<int64_t>(c.rcap + 1 + 8, max_cols);
+  }
   c.kcap = std::max<int64_t>(64, round_up(std::max<int64_t>(k, 1) * 2, 64));
   return c;
 }
@@ -631,7 +639,10 @@ strom_isvd* compact(strom_isvd* src, const Caps& caps, cudaStream_t s) {
   P.ccap = kc.ccap;
   launch_compact_prep(src->view, t->view, m, P, kc, s);
   // p = source c (step->m), q = r (step->mkeep); source columns start at base
-  if (kc.rcap <= 128) {
+  const size_t fused_smem = ((size_t)((src->caps.ccap + 3) & ~3) * (round_up(kc.rcap, 32) + 4) +
+                             (size_t)((src->caps.ccap + 3) & ~3) * (kUTile + 4) +
+                             (size_t)round_up(kc.rcap, 32) * (kUTile + 4)) * 8;
+  if (kc.rcap <= 128 && fused_smem <= max_smem_optin()) {
     // one fused DMMA sweep: U_new = U T and the measured Gram of the stored U_new
     const int RP = (int)round_up(kc.rcap, 32);
     auto part = dev_alloc((size_t)sm_count() * RP * RP * 8, s, false);

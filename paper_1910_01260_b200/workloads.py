@@ -251,3 +251,63 @@ def random_stable_system(rng, n_states, n_inputs=1):
     return dict(a=sp.csr_array(a), b=sp.csr_array(rng.standard_normal((n_states, n_inputs))),
                 c=rng.standard_normal((n_states, 1)), x0=rng.standard_normal(n_states),
                 inputs=signal)
+
+
+# --------------------------------------------------------------------------
+# cfg5: capacity stream on the device (BASELINE.json configs[4])
+# --------------------------------------------------------------------------
+
+class HadamardStream:
+    """Low-rank-plus-noise stream X = Q diag(sigma) W^T + E generated on the device.
+
+    The capacity configuration (2^26 rows, 1000 snapshots, rank 100) does not
+    fit on the host (537 GB) and its Haar Q (54 GB) would not fit next to the
+    iSVD store, so Q is an implicit randomized Hadamard matrix
+    Q[i, c] = s_i (-1)^popcount(i & p_c) / sqrt(n) with orthonormal columns,
+    never stored (C ABI ``strom_gen_lowrank_batch``).  W is Haar (device QR),
+    sigma_c = 10^(-c / decades_per), E = noise * N(0, 1) from a counter hash, so
+    any column can be regenerated bit-identically.
+    """
+
+    def __init__(self, n: int, cols: int, rank: int, decades_per: float = 12.0, seed: int = 0,
+                 noise: float = 1e-12, device: str = "cuda"):
+        import torch
+
+        if n < 2 or n & (n - 1):
+            raise ValueError("HadamardStream needs n = 2^m")
+        self.n, self.cols, self.rank, self.seed, self.noise = n, cols, rank, seed, noise
+        g = torch.Generator(device=device)
+        g.manual_seed(seed)
+        a = torch.randn(cols, rank, generator=g, device=device, dtype=torch.float64)
+        q, r = torch.linalg.qr(a, mode="reduced")
+        d = torch.sign(torch.diagonal(r))
+        d[d == 0] = 1.0
+        self.w = (q * d).contiguous()                                   # cols x rank
+        self.sigma = torch.tensor(cfg2_sigma(rank, decades_per), device=device, dtype=torch.float64)
+        self.prow = torch.tensor([((c + 1) * 0x9E3779B1) % n for c in range(rank)], device=device,
+                                 dtype=torch.int64)
+        self.device = device
+
+    def _gen(self, coef, t0: int, nb: int, noise: float, out=None):
+        import torch
+
+        from . import _capi as capi
+
+        if out is None:
+            out = torch.empty((nb, self.n), dtype=torch.float64, device=self.device)
+        capi.call("strom_gen_lowrank_batch", self.n, self.rank, nb, coef.data_ptr(), self.prow.data_ptr(),
+                  self.seed, t0, noise, out.data_ptr(), self.n, capi.stream_ptr())
+        return out.T  # n x nb, column-major
+
+    def batch(self, t0: int, nb: int, out=None):
+        """Columns t0 .. t0+nb-1 of X as an (n, nb) column-major CUDA tensor."""
+        coef = (self.w[t0:t0 + nb] * self.sigma).T.contiguous()        # rank x nb, row-major
+        return self._gen(coef, t0, nb, self.noise, out)
+
+    def q_columns(self, c0: int, nc: int, out=None):
+        """Columns c0 .. c0+nc-1 of the implicit Q (noise-free), (n, nc) column-major."""
+        import torch
+
+        coef = torch.zeros((self.rank, nc), dtype=torch.float64, device=self.device)
+        coef[torch.arange(c0, c0 + nc), torch.arange(nc)] = 1.0
+        return self._gen(coef, 0, nc, 0.0, out)

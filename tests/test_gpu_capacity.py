@@ -1,0 +1,59 @@
+"""Capacity configuration (BASELINE configs[4]) at reduced size.
+
+The full run (2^26 rows, 1000 snapshots; tools/cfg5_capacity.py, profiles/)
+has no CPU oracle; its checks are invariants, exercised here on 2^18 rows:
+  * the device generator's implicit Q has orthonormal columns (to rounding);
+  * sigma_i against the construction's 10^(-i/12) for the modes far above the
+    noise (first-order noise bound |dsigma| ~ noise, so rel <= 1e-10 for i < 16);
+  * sampled-column reconstruction at the noise level (||E_t|| / ||x_t||);
+  * principal angles of the leading modes at the noise limit ||E v_i|| / sigma_i.
+"""
+
+import math
+
+import pytest
+import torch
+
+from paper_1910_01260_b200 import basis, workloads as wl
+
+pytestmark = pytest.mark.gpu
+
+
+def test_generator_q_orthonormal_and_deterministic(cuda):
+    n = 1 << 16
+    s = wl.HadamardStream(n, 40, 24, seed=3)
+    q = torch.cat([s.q_columns(0, 16).clone(), s.q_columns(16, 8).clone()], dim=1)
+    g = q.T @ q
+    assert float((g - torch.eye(24, dtype=g.dtype, device=g.device)).abs().max()) <= 1e-13
+    a = s.batch(5, 4).clone()
+    b = s.batch(5, 4).clone()
+    assert torch.equal(a, b)
+    # columns are Q diag(sigma) W^T plus 1e-12 N(0, 1) noise
+    lr = q @ (s.sigma[:, None] * s.w[5:9].T)
+    assert float((a - lr).abs().max()) <= 1e-11
+
+
+def test_capacity_stream_invariants(cuda):
+    n, cols, rank = 1 << 18, 160, 100
+    s = wl.HadamardStream(n, cols, rank, decades_per=12.0, seed=0)
+    st = basis.isvd_init(s.batch(0, 1)[:, 0], 1e-9, tol_sv=1e-9, r_max=rank, cap_mode="truncate")
+    t0 = 1
+    while t0 < cols:
+        nb = 1 << int(math.floor(math.log2(min(8, cols - t0))))
+        st = basis.ingest_simulation(st, s.batch(t0, nb))
+        t0 += nb
+    assert st.rank == rank
+    sig = st.sigma
+    rel = (sig - s.sigma).abs() / s.sigma
+    assert float(rel[:16].max()) <= 1e-10
+    phi = st.phi
+    noise_rel = s.noise * math.sqrt(n)
+    for t in (3, cols // 2, cols - 1):
+        x = s.batch(t, 1)[:, 0]
+        xr = phi @ (sig * st.v[t])
+        assert float(torch.linalg.norm(x - xr) / torch.linalg.norm(x)) <= 20 * noise_rel / float(torch.linalg.norm(x))
+    m = 16
+    q = s.q_columns(0, m)
+    sv = torch.linalg.svdvals(phi[:, :m].T @ q).clamp(max=1.0)
+    sin_max = float(torch.sqrt(1 - sv.min() ** 2))
+    assert sin_max <= 10 * noise_rel / float(s.sigma[m - 1])
