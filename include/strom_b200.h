@@ -186,6 +186,18 @@ int strom_spatial_reduce_ell(int64_t n, int32_t K, const uint32_t* eidx_dev, con
                              const double* phi_dev, int64_t ld, int64_t ns, const double* extra_dev, int64_t ext_ld,
                              int64_t ne, const double* xref_dev, double* out_dev, void* stream);
 
+/* fom_march (system.py:150-163) on the device: (I - dt_k A) x_k = x_{k-1} +
+ * dt_k B f_k for k = 1..N_t by Jacobi-preconditioned BiCGSTAB (relative
+ * residual tol, at most maxit iterations per step) in one cooperative kernel,
+ * over A's tiled-ELL form (strom_csr_to_ell).  b_dev: n x m column-major;
+ * f_dev: N_t x m row-major (row k = input of step k+1); dt_dev: N_t;
+ * states_dev: n x N_t column-major (column k-1 = x_k).  iters_out (host,
+ * may be NULL): iterations per step.  A step that misses tol is a numerical
+ * error. */
+int strom_fom_march(int64_t n, int32_t K, const uint32_t* eidx_dev, const double* eval_dev, const double* b_dev,
+                    int64_t m, const double* x0_dev, const double* dt_dev, const double* f_dev, int64_t nt, double tol,
+                    int32_t maxit, double* states_dev, int32_t* iters_out, void* stream);
+
 /* Workload generator (bench/test support, not a reference interface): nb
  * columns t0 .. t0+nb-1 of the capacity stream X = Q diag(sigma) W^T + E with
  * an implicit randomized-Hadamard Q (Q[i,c] = s_i (-1)^popcount(i & p_c) /

@@ -9,7 +9,7 @@ numerical step runs in ``_lib/libstrom_b200.so`` (C ABI: include/strom_b200.h).
 from .errors import BasisError, CapExceededError, ConvergenceError, SingularMatrixError
 from .basis import (BasisSet, SvdState, build_basis_set, ingest_simulation, isvd_init, isvd_update,
                     temporal_snapshots)
-from .system import LinearDynamicalSystem, TimeGrid
+from .system import FomResult, LinearDynamicalSystem, TimeGrid, fom_march
 from .spatial import SpatialRom, build_spatial_rom
 from .spacetime import (SpaceTimeRom, build_st_init, build_st_input, build_st_matrix, build_st_rom,
                         reconstruct_states, solve_st_rom)
@@ -17,9 +17,9 @@ from .spacetime import (SpaceTimeRom, build_st_init, build_st_input, build_st_ma
 __version__ = "0.1.0"
 
 __all__ = [
-    "BasisError", "BasisSet", "CapExceededError", "ConvergenceError", "LinearDynamicalSystem",
+    "BasisError", "BasisSet", "CapExceededError", "ConvergenceError", "FomResult", "LinearDynamicalSystem",
     "SingularMatrixError", "SpaceTimeRom", "SpatialRom", "SvdState", "TimeGrid", "build_basis_set",
-    "build_spatial_rom", "build_st_init", "build_st_input", "build_st_matrix", "build_st_rom",
+    "build_spatial_rom", "build_st_init", "build_st_input", "build_st_matrix", "build_st_rom", "fom_march",
     "ingest_simulation", "isvd_init", "isvd_update", "reconstruct_states", "solve_st_rom",
     "temporal_snapshots",
 ]

@@ -20,7 +20,7 @@ LIBDIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIBDIR, "libstrom_b200.so")
 INCLUDE = os.path.join(os.path.dirname(PKG), "include")
 
-SOURCES = ["runtime.cu", "isvd.cu", "temporal.cu", "spatial.cu", "spacetime.cu", "dense.cu", "workloads.cu"]
+SOURCES = ["runtime.cu", "isvd.cu", "temporal.cu", "spatial.cu", "spacetime.cu", "dense.cu", "workloads.cu", "fom.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr"]
 

@@ -1,0 +1,270 @@
+// Full-order backward-Euler march on the device (reference system.py:150-163
+// fom_march, system.py:106-147 StepSolver / backward_euler_step): the snapshot
+// producer that feeds the incremental SVD without a host round trip.
+//
+//   (I - dt_k A) x_k = x_{k-1} + dt_k B f_k ,   k = 1 .. N_t
+//
+// The reference factors I - dt A with SuperLU; at the transport-proxy size
+// (2^20 dofs in 3D) that is infeasible, so each step is
+// solved by Jacobi-preconditioned BiCGSTAB started from x_{k-1}, to a relative
+// residual tol (default 1e-13), over the tiled-ELL operator of the spatial
+// reduction (diagonal kept apart: M = I - dt A has diagonal 1 - dt a_ii and
+// off-diagonals -dt a_ij).
+//
+// One cooperative persistent kernel marches every step: grid-wide syncs
+// separate the phases; dot products are per-CTA partials summed by every CTA
+// in CTA order (deterministic, identical on every CTA).
+#include <cooperative_groups.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/strom_b200.h"
+#include "common.cuh"
+#include "runtime.cuh"
+
+using namespace strom;
+namespace cg = cooperative_groups;
+
+namespace {
+
+constexpr int kFomThreads = 256;
+constexpr int kEllRows = 64;  // tile height of the ELL layout (spatial.cu)
+
+struct FomArgs {
+  int64_t n;
+  int K;
+  const uint32_t* eidx;  // per 64-row tile: [K][64] off-diagonal columns
+  const double* eval;    // per tile: [K][64] off-diagonal values, then [64] diagonal
+  const double* b;       // n x m column-major (ldb = n)
+  int m;
+  const double* x0;
+  const double* dt;      // N_t
+  const double* f;       // N_t x m row-major (row k = input of step k+1)
+  int nt;
+  double tol;
+  int maxit;
+  double* states;        // n x N_t column-major (ld = n)
+  double* w;             // 8 work vectors of n: b, r, rh, p, v, s, t, ph (sh shares ph's slot)
+  double* part;          // 2 x 3 x gridDim partial sums
+  int* iters;            // N_t iteration counts (-1: not converged)
+};
+
+// y = (I - dt A) z for the rows owned by this thread (grid-stride)
+template <int K>
+__device__ __forceinline__ double mrow(const FomArgs& a, int64_t i, double dt, const double* __restrict__ z) {
+  const int64_t tile = i / kEllRows;
+  const int li = (int)(i % kEllRows);
+  const uint32_t* ti = a.eidx + tile * K * kEllRows + li;
+  const double* tv = a.eval + tile * (K + 1) * kEllRows + li;
+  double acc = (1.0 - dt * tv[K * kEllRows]) * z[i];
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc = fma(-dt * tv[k * kEllRows], z[ti[k * kEllRows]], acc);
+  return acc;
+}
+
+template <int K>
+__device__ __forceinline__ double mdiag(const FomArgs& a, int64_t i, double dt) {
+  return 1.0 - dt * a.eval[(i / kEllRows) * (K + 1) * kEllRows + K * kEllRows + i % kEllRows];
+}
+
+// deterministic grid reduction of up to 3 values: every CTA returns the same
+// sums.  Consecutive reductions alternate between two partial buffers, so a
+// CTA writing reduction R+1 never races a CTA still reading reduction R.
+__device__ __forceinline__ void grid_reduce3(cg::grid_group& grid, double* part_base, int& nred, double v0,
+                                             double v1, double v2, double* out, double* sred) {
+  double* part = part_base + (int64_t)(nred++ & 1) * 3 * gridDim.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double vv[3] = {v0, v1, v2};
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    double s = warp_sum(vv[q]);
+    if (lane == 0) sred[q * 8 + w] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double s = 0.0;
+    for (int k = 0; k < kFomThreads / 32; ++k) s += sred[threadIdx.x * 8 + k];
+    part[(int64_t)threadIdx.x * gridDim.x + blockIdx.x] = s;
+  }
+  grid.sync();
+  if (w < 3) {
+    double s = 0.0;
+    for (int c = lane; c < (int)gridDim.x; c += 32) s += part[(int64_t)w * gridDim.x + c];
+    s = warp_sum(s);  // fixed shuffle tree: the same on every CTA
+    if (lane == 0) sred[24 + w] = s;
+  }
+  __syncthreads();
+  out[0] = sred[24];
+  out[1] = sred[25];
+  out[2] = sred[26];
+  __syncthreads();
+}
+
+template <int K>
+__global__ void __launch_bounds__(kFomThreads) k_fom_march(FomArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sred[32];
+  const int64_t n = a.n;
+  const int64_t g0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gs = (int64_t)gridDim.x * blockDim.x;
+  double* bb = a.w;
+  double* r = a.w + n;
+  double* rh = a.w + 2 * n;
+  double* p = a.w + 3 * n;
+  double* v = a.w + 4 * n;
+  double* s = a.w + 5 * n;
+  double* t = a.w + 6 * n;
+  double* ph = a.w + 7 * n;  // preconditioned direction (p-hat, then s-hat)
+  double red[3];
+  int nred = 0;
+  for (int k = 0; k < a.nt; ++k) {
+    const double dt = a.dt[k];
+    const double* xp = k == 0 ? a.x0 : a.states + (int64_t)(k - 1) * n;
+    double* x = a.states + (int64_t)k * n;
+    // rhs and initial guess x = x_{k-1}
+    for (int64_t i = g0; i < n; i += gs) {
+      double bi = xp[i];
+      for (int q = 0; q < a.m; ++q) bi = fma(dt * a.b[(int64_t)q * n + i], a.f[(int64_t)k * a.m + q], bi);
+      bb[i] = bi;
+      x[i] = xp[i];
+    }
+    grid.sync();
+    double pr = 0.0, pb = 0.0;
+    for (int64_t i = g0; i < n; i += gs) {
+      const double ri = bb[i] - mrow<K>(a, i, dt, x);
+      r[i] = ri;
+      rh[i] = ri;
+      p[i] = ri;
+      pr = fma(ri, ri, pr);
+      pb = fma(bb[i], bb[i], pb);
+    }
+    grid_reduce3(grid, a.part, nred, pr, pb, 0.0, red, sred);
+    double rho = red[0], rr = red[0];
+    const double bnorm2 = red[1];
+    const double stop2 = a.tol * a.tol * bnorm2;
+    int it = 0;
+    bool ok = rr <= stop2;
+    while (!ok && it < a.maxit) {
+      ++it;
+      // p-hat = D^-1 p ; v = M p-hat ; (rh, v)
+      for (int64_t i = g0; i < n; i += gs) ph[i] = p[i] / mdiag<K>(a, i, dt);
+      grid.sync();
+      double prv = 0.0;
+      for (int64_t i = g0; i < n; i += gs) {
+        const double vi = mrow<K>(a, i, dt, ph);
+        v[i] = vi;
+        prv = fma(rh[i], vi, prv);
+      }
+      grid_reduce3(grid, a.part, nred, prv, 0.0, 0.0, red, sred);
+      if (red[0] == 0.0) break;  // breakdown: keep the last iterate
+      const double alpha = rho / red[0];
+      // x += alpha p-hat ; s = r - alpha v ; s-hat = D^-1 s (into ph after x is updated)
+      for (int64_t i = g0; i < n; i += gs) {
+        x[i] = fma(alpha, ph[i], x[i]);
+        s[i] = fma(-alpha, v[i], r[i]);
+      }
+      grid.sync();
+      for (int64_t i = g0; i < n; i += gs) ph[i] = s[i] / mdiag<K>(a, i, dt);
+      grid.sync();
+      double pts = 0.0, ptt = 0.0, pss = 0.0;
+      for (int64_t i = g0; i < n; i += gs) {
+        const double ti = mrow<K>(a, i, dt, ph);
+        t[i] = ti;
+        pts = fma(ti, s[i], pts);
+        ptt = fma(ti, ti, ptt);
+        pss = fma(s[i], s[i], pss);
+      }
+      grid_reduce3(grid, a.part, nred, pts, ptt, pss, red, sred);
+      if (red[2] <= stop2) {  // converged on s: x already holds x + alpha p-hat
+        ok = true;
+        break;
+      }
+      if (red[1] == 0.0) break;
+      const double omega = red[0] / red[1];
+      double prr = 0.0, prh = 0.0;
+      for (int64_t i = g0; i < n; i += gs) {
+        x[i] = fma(omega, ph[i], x[i]);
+        const double ri = fma(-omega, t[i], s[i]);
+        r[i] = ri;
+        prr = fma(ri, ri, prr);
+        prh = fma(rh[i], ri, prh);
+      }
+      grid_reduce3(grid, a.part, nred, prr, prh, 0.0, red, sred);
+      rr = red[0];
+      if (rr <= stop2) {
+        ok = true;
+        break;
+      }
+      if (omega == 0.0 || rho == 0.0) break;
+      const double beta = (red[1] / rho) * (alpha / omega);
+      rho = red[1];
+      for (int64_t i = g0; i < n; i += gs) p[i] = r[i] + beta * fma(-omega, v[i], p[i]);
+      grid.sync();
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.iters[k] = ok ? it : -1;
+    grid.sync();
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+// fom_march (system.py:150-163) on the device: states (n x N_t, column-major)
+// column k-1 = x_k.  The operator is the tiled ELL form of A
+// (strom_csr_to_ell, K in {4, 6, 8, 16}); b_dev n x m column-major; f_dev
+// N_t x m row-major (row k = input of step k+1); dt_dev N_t.  iters_out
+// (host, N_t ints, may be NULL): BiCGSTAB iterations per step, -1 where the
+// relative residual did not reach tol within maxit (the call then returns a
+// numerical error).
+int strom_fom_march(int64_t n, int32_t K, const uint32_t* eidx_dev, const double* eval_dev, const double* b_dev,
+                    int64_t m, const double* x0_dev, const double* dt_dev, const double* f_dev, int64_t nt, double tol,
+                    int32_t maxit, double* states_dev, int32_t* iters_out, void* stream) {
+  return guarded([&] {
+    STROM_REQUIRE(n >= 1 && nt >= 1 && m >= 0, "bad fom_march shape");
+    STROM_REQUIRE(K == 4 || K == 6 || K == 8 || K == 16, "ELL width must be 4, 6, 8 or 16");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    auto kern = K == 4 ? k_fom_march<4> : K == 6 ? k_fom_march<6> : K == 8 ? k_fom_march<8> : k_fom_march<16>;
+    int occ = 0;
+    STROM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kFomThreads, 0));
+    STROM_REQUIRE(occ >= 1, "fom_march kernel cannot be resident");
+    const int64_t want = ceil_div(n, kFomThreads);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count() * std::min(occ, 4)));
+    auto work = dev_alloc((size_t)8 * n * 8, s, false);
+    auto part = dev_alloc((size_t)6 * grid * 8, s, true);
+    auto its = dev_alloc((size_t)nt * 4, s, true);
+    FomArgs a{};
+    a.n = n;
+    a.K = K;
+    a.eidx = eidx_dev;
+    a.eval = eval_dev;
+    a.b = b_dev;
+    a.m = (int)m;
+    a.x0 = x0_dev;
+    a.dt = dt_dev;
+    a.f = f_dev;
+    a.nt = (int)nt;
+    a.tol = tol;
+    a.maxit = maxit;
+    a.states = states_dev;
+    a.w = work->as<double>();
+    a.part = part->as<double>();
+    a.iters = its->as<int>();
+    void* args[] = {&a};
+    STROM_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kFomThreads), args, 0, s));
+    STROM_LAUNCH_CHECK();
+    std::vector<int> h((size_t)nt);
+    STROM_CUDA(cudaMemcpyAsync(h.data(), its->ptr, (size_t)nt * 4, cudaMemcpyDeviceToHost, s));
+    STROM_CUDA(cudaStreamSynchronize(s));
+    if (iters_out)
+      for (int64_t k = 0; k < nt; ++k) iters_out[k] = h[k];
+    for (int64_t k = 0; k < nt; ++k)
+      if (h[k] < 0)
+        throw Error(kNumericalError, "fom_march: step " + std::to_string(k + 1) +
+                                         " did not reach the residual tolerance (BiCGSTAB)");
+  });
+}
+
+}  // extern "C"

@@ -9,7 +9,8 @@ operator builds read HBM-resident operands.
 from __future__ import annotations
 
 from dataclasses import dataclass, field
-from typing import Callable
+import time
+from typing import Callable, NamedTuple
 
 import numpy as np
 import scipy.sparse as sp
@@ -140,3 +141,46 @@ class LinearDynamicalSystem:
             self._dev["bcx0"] = torch.cat([self._dev["b"].T, self._dev["c"].T, self._dev["x0"][None, :]],
                                           dim=0).contiguous()
         return self._dev
+
+
+class FomResult(NamedTuple):
+    """Full-order march result (system.py:143-147): states n x N_t (column k-1 = x_k)."""
+
+    states: torch.Tensor
+    outputs: torch.Tensor
+    wall_time: float
+    iterations: list
+
+
+def fom_march(sys: LinearDynamicalSystem, grid: TimeGrid, tol: float = 1e-13, maxit: int = 500) -> FomResult:
+    """March the full-order model over the grid on the device (system.py:150-163).
+
+    The reference solves each backward-Euler step (I - dt A) x_k = x_{k-1} +
+    dt B f_k with a cached SuperLU factor; here one cooperative kernel
+    (C ABI ``strom_fom_march``) marches all steps with Jacobi-preconditioned
+    BiCGSTAB to a relative residual ``tol``, over the operator's tiled-ELL form,
+    so snapshots stay in HBM for ``ingest_simulation``.  The clock covers the
+    march only, like the reference's.
+    """
+    from . import _capi as capi
+
+    dev = sys.device_arrays()
+    ell = dev.get("ell")
+    if ell is None:
+        raise ValueError("fom_march on the device needs at most 16 off-diagonal entries per row of A")
+    n, nt, m = sys.n_states, grid.n_steps, sys.n_inputs
+    f = np.stack([np.atleast_1d(np.asarray(sys.input_signal(k), dtype=float)).reshape(m)
+                  for k in range(1, nt + 1)])
+    f_dev = torch.as_tensor(f, dtype=F64, device=device()).contiguous()
+    b_cm = dev["b"].T.contiguous()  # m x n: B column-major
+    states = torch.empty((nt, n), dtype=F64, device=device())
+    iters = (capi.C.c_int32 * nt)()
+    torch.cuda.synchronize()
+    start = time.perf_counter()
+    capi.call("strom_fom_march", n, ell["k"], ell["idx"].data_ptr(), ell["val"].data_ptr(), b_cm.data_ptr(), m,
+              dev["x0"].data_ptr(), grid.dt_device().data_ptr(), f_dev.data_ptr(), nt, float(tol), int(maxit),
+              states.data_ptr(), iters, capi.stream_ptr())
+    wall = time.perf_counter() - start
+    st = states.T  # n x N_t, column-major
+    outputs = dev["c"].T @ st
+    return FomResult(st, outputs, wall, list(iters))

@@ -311,3 +311,93 @@ class HadamardStream:
         coef = torch.zeros((self.rank, nc), dtype=torch.float64, device=self.device)
         coef[torch.arange(c0, c0 + nc), torch.arange(nc)] = 1.0
         return self._gen(coef, 0, nc, 0.0, out)
+
+
+# --------------------------------------------------------------------------
+# cfg3: 3D discrete-ordinates transport proxy (BASELINE.json configs[2])
+# --------------------------------------------------------------------------
+
+CFG3_NC = 64
+CFG3_DT = 0.01
+CFG3_NT = 100
+CFG3_AMPLITUDES = (0.5, 1.0, 1.5, 2.0)
+CFG3_TOL = 1e-8
+CFG3_DIRECTIONS = np.array([[1.0, 1.0, 1.0], [-1.0, -1.0, -1.0], [1.0, -1.0, 1.0], [-1.0, 1.0, -1.0]]) / np.sqrt(3.0)
+
+
+def cfg3_source(nc: int = CFG3_NC, seed: int = 6, n_gauss: int = 8, width: float = 0.1) -> np.ndarray:
+    """Sum of 8 Gaussians (width 0.1, centres U[0,1]^3, seed 6) at the cell centres, x fastest."""
+    rng = np.random.default_rng(seed)
+    centres = rng.uniform(0.0, 1.0, (n_gauss, 3))
+    xc = (np.arange(nc) + 0.5) / nc
+    z, y, x = np.meshgrid(xc, xc, xc, indexing="ij")  # cell (iz, iy, ix) at index (iz*nc + iy)*nc + ix
+    g = np.zeros((nc, nc, nc))
+    for c in centres:
+        g += np.exp(-((x - c[0]) ** 2 + (y - c[1]) ** 2 + (z - c[2]) ** 2) / (2.0 * width**2))
+    return g.ravel()
+
+
+def cfg3_operator(nc: int = CFG3_NC, sigma_t: float = 1.0, sigma_s: float = 0.5, speed: float = 1.0):
+    """dx/dt = nu (scatter - H) x on nc^3 cells x 4 directions, direction-major.
+
+    The 3D analogue of the reference's transport1d (problems.py:196-247): per
+    direction H_d = first-order upwind streaming Omega_d . grad with vacuum
+    inflow plus sigma_t; isotropic scattering with equal weights 1/4 couples
+    the directions of a cell.  Unknown (d, iz, iy, ix) at d * nc^3 +
+    (iz * nc + iy) * nc + ix."""
+    nd = CFG3_DIRECTIONS.shape[0]
+    ncell = nc**3
+    h = 1.0 / nc
+    iz, iy, ix = np.meshgrid(np.arange(nc), np.arange(nc), np.arange(nc), indexing="ij")
+    iz, iy, ix = iz.ravel(), iy.ravel(), ix.ravel()
+    cell = np.arange(ncell)
+    rows, cols, vals = [], [], []
+    w = 1.0 / nd
+    for d, om in enumerate(CFG3_DIRECTIONS):
+        base = d * ncell
+        diag = np.full(ncell, -speed * (np.sum(np.abs(om)) / h + sigma_t) + speed * sigma_s * w)
+        rows.append(base + cell)
+        cols.append(base + cell)
+        vals.append(diag)
+        for axis, (coord, stride) in enumerate(((ix, 1), (iy, nc), (iz, nc * nc))):
+            o = om[axis]
+            up = coord - 1 if o > 0 else coord + 1  # upstream neighbour along this axis
+            ok = (up >= 0) & (up < nc)               # vacuum inflow: no entry at the boundary
+            shift = -stride if o > 0 else stride
+            rows.append(base + cell[ok])
+            cols.append(base + cell[ok] + shift)
+            vals.append(np.full(int(ok.sum()), speed * abs(o) / h))
+        for d2 in range(nd):
+            if d2 != d:
+                rows.append(base + cell)
+                cols.append(d2 * ncell + cell)
+                vals.append(np.full(ncell, speed * sigma_s * w))
+    n = nd * ncell
+    a = sp.csr_array((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))), shape=(n, n))
+    a.sort_indices()
+    return a
+
+
+@dataclass
+class Cfg3Inputs:
+    a: sp.csr_array
+    b: np.ndarray
+    c: np.ndarray
+    x0: np.ndarray
+    amplitude: float
+
+    def inputs(self, k):
+        return np.array([self.amplitude])
+
+
+def cfg3_system(amplitude: float, nc: int = CFG3_NC, seed: int = 6, a=None) -> Cfg3Inputs:
+    """Transport proxy at one training amplitude: x0 = the smooth source in every
+    direction, B = the same field, constant input f = amplitude; output = the
+    scalar flux integral (weights 1/4 x cell volume, as transport1d's c_out)."""
+    g = cfg3_source(nc, seed)
+    nd = CFG3_DIRECTIONS.shape[0]
+    if a is None:
+        a = cfg3_operator(nc)
+    field = np.tile(g, nd)
+    c = np.full((nd * nc**3, 1), (1.0 / nd) / nc**3)
+    return Cfg3Inputs(a=a, b=field[:, None].copy(), c=c, x0=field.copy(), amplitude=float(amplitude))

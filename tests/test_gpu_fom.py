@@ -1,0 +1,107 @@
+"""Device full-order march (reference system.py:150-163 fom_march) against the
+reference's own states and the oracle's SuperLU march.
+
+The reference factors I - dt A once per dt; the device runs Jacobi-
+preconditioned BiCGSTAB per step to a relative residual of 1e-13, so states
+agree to the solver tolerance carried through the march: the bar is 1e-10
+relative (max-abs, per column) against the reference.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import strom_oracle as so
+from paper_1910_01260_b200 import LinearDynamicalSystem, TimeGrid, fom_march, workloads as wl
+
+from conftest import load_golden
+from helpers import npy
+
+pytestmark = pytest.mark.gpu
+
+
+def _lds(d, constant=True):
+    return LinearDynamicalSystem(a=d.a, b=d.b, c=d.c, x0=d.x0, input_signal=d.inputs, constant_input=constant)
+
+
+def _col_rel(a, b):
+    return float(np.max(np.abs(a - b).max(axis=0) / np.maximum(np.abs(b).max(axis=0), 1e-300)))
+
+
+def test_cfg1_states_match_reference_golden(cuda):
+    """The four cfg1 training marches vs the reference's fom_march checksums."""
+    g = load_golden("golden_cfg1.npz")
+    grid = TimeGrid(wl.cfg1_dt())
+    mats = []
+    for nu in wl.CFG1_TRAIN_NU:
+        res = fom_march(_lds(wl.cfg1_system(nu)), grid)
+        assert all(0 < it <= 500 for it in res.iterations)
+        mats.append(npy(res.states))
+    u = np.hstack(mats)
+    assert np.max(np.abs(u.sum(axis=0) - g["u_colsum"]) / np.abs(g["u_colsum"])) <= 1e-10
+    assert np.max(np.abs(np.abs(u).sum(axis=0) - g["u_abssum"]) / g["u_abssum"]) <= 1e-10
+    assert _col_rel(u[::97, ::7], g["u_sample"]) <= 1e-9
+
+
+def test_transport_proxy_matches_oracle(cuda):
+    """cfg3's operator at 8^3 cells x 4 directions vs the SuperLU march."""
+    a = wl.cfg3_operator(8)
+    for amp in (0.5, 2.0):
+        d = wl.cfg3_system(amp, nc=8, a=a)
+        grid = TimeGrid(np.full(20, wl.CFG3_DT))
+        res = fom_march(_lds(d), grid)
+        ref = so.fom_march(d.a, d.b, d.x0, grid.dt, d.inputs)
+        assert _col_rel(npy(res.states), ref) <= 1e-11
+        # output C^T x like the reference's FomResult.outputs
+        np.testing.assert_allclose(npy(res.outputs), d.c.T @ ref, rtol=1e-11)
+
+
+def test_nonuniform_grid_and_inputs(cuda):
+    """Per-step dt and a time-varying input (the general rhs of backward_euler_step)."""
+    a = wl.cfg3_operator(4)
+    d = wl.cfg3_system(1.0, nc=4, a=a)
+    rng = np.random.default_rng(4)
+    f = rng.uniform(0.5, 2.0, 12)
+    sys_ = LinearDynamicalSystem(a=d.a, b=d.b, c=d.c, x0=d.x0, input_signal=lambda k: np.array([f[k - 1]]))
+    dt = rng.uniform(0.002, 0.02, 12)
+    res = fom_march(sys_, TimeGrid(dt))
+    ref = so.fom_march(d.a, d.b, d.x0, dt, lambda k: np.array([f[k - 1]]))
+    assert _col_rel(npy(res.states), ref) <= 1e-11
+
+
+def test_unconverged_step_raises(cuda):
+    d = wl.cfg3_system(1.0, nc=4)
+    with pytest.raises(ValueError, match="did not reach"):
+        fom_march(_lds(d), TimeGrid(np.full(3, 0.5)), tol=1e-15, maxit=1)
+
+
+def test_dense_operator_rejected(cuda):
+    rng = np.random.default_rng(0)
+    d = wl.random_stable_system(rng, 40)
+    sys_ = LinearDynamicalSystem(a=d["a"], b=d["b"], c=d["c"], x0=d["x0"], input_signal=d["inputs"])
+    with pytest.raises(ValueError, match="off-diagonal"):
+        fom_march(sys_, TimeGrid(np.full(3, 0.01)))
+
+
+def test_cfg3_pipeline_scaled_vs_oracle(cuda):
+    """cfg3 at 12^3 x 4: device FOM -> device iSVD (tol 1e-8) vs SuperLU FOM -> oracle iSVD."""
+    from paper_1910_01260_b200 import basis
+
+    a = wl.cfg3_operator(12)
+    grid = TimeGrid(np.full(40, wl.CFG3_DT))
+    st, ref = None, None
+    for amp in wl.CFG3_AMPLITUDES:
+        d = wl.cfg3_system(amp, nc=12, a=a)
+        x = fom_march(_lds(d), grid).states
+        xr = so.fom_march(d.a, d.b, d.x0, grid.dt, d.inputs)
+        if st is None:
+            st = basis.isvd_init(x[:, 0], wl.CFG3_TOL, tol_sv=wl.CFG3_TOL)
+            st = basis.ingest_simulation(st, x[:, 1:])
+            ref = so.stream(xr, wl.CFG3_TOL, tol_sv=wl.CFG3_TOL)
+        else:
+            st = basis.ingest_simulation(st, x)
+            ref = so.ingest(ref, xr)
+    s, rs = npy(st.sigma), ref.sigma
+    # modes far above the truncation floor agree to the north-star bar
+    big = rs >= 1e-2 * rs[0]
+    assert np.max(np.abs(s[:big.sum()] - rs[big]) / rs[big]) <= 1e-10
