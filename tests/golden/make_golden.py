@@ -244,9 +244,19 @@ def gen_cfg4_small():
     _save("golden_cfg4_small.npz", **out)
 
 
+def gen_persist():
+    """A STROMMAT file written by the reference's persist.write_matrix (persist.py:35-48)."""
+    from strom import persist
+
+    m = np.random.default_rng(7).standard_normal((5, 3))
+    persist.write_matrix(os.path.join(HERE, "golden_ref_5x3.strommat"), m)
+    np.save(os.path.join(HERE, "golden_ref_5x3_values.npy"), m)
+
+
 if __name__ == "__main__":
     gen_linalg()
     gen_isvd_small()
     gen_cfg1()
     gen_blocks()
     gen_cfg4_small()
+    gen_persist()
