@@ -23,6 +23,7 @@ using namespace strom;
 namespace {
 
 constexpr int kNb = 32;
+constexpr int kNbReg = 16;  // panel width of the register-resident panel factorisation
 
 __global__ void k_fro_norm(const double* A, int64_t ld, int64_t n, double* out) {
   __shared__ double red[32];
@@ -204,6 +205,238 @@ __global__ void __launch_bounds__(1024) k_lu_solve(const double* A, int64_t ld, 
   }
 }
 
+// Panel factorisation with the panel held in registers: thread t owns rows
+// k0 + t + 512 q (q < RPT) of the nb <= kNbReg panel columns.  Per column: an
+// argmax reduction (largest |a|, lowest row on ties, like idamax), the pivot
+// row exchanged through shared memory, then scale and rank-1 update in
+// registers.  Row interchanges are applied to the panel only; k_lu_laswp
+// applies them to the other columns afterwards (LAPACK's getrf order).
+template <int RPT>
+__global__ void __launch_bounds__(512, 1) k_lu_panel_reg(double* A, int64_t ld, int n, int k0, int nb, int* piv) {
+  __shared__ double srow[2][kNbReg];  // [0]: pivot row, [1]: the displaced row k0 + j
+  __shared__ double sv[16];
+  __shared__ int si[16];
+  __shared__ int s_p;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double a[RPT][kNbReg];
+#pragma unroll
+  for (int q = 0; q < RPT; ++q) {
+    const int i = k0 + threadIdx.x + 512 * q;
+#pragma unroll
+    for (int c = 0; c < kNbReg; ++c) a[q][c] = (i < n && c < nb) ? A[(int64_t)(k0 + c) * ld + i] : 0.0;
+  }
+#pragma unroll 1
+  for (int j = 0; j < nb; ++j) {
+    const int jr = k0 + j;
+    double best = -1.0;
+    int bi = 0x7fffffff;
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      const int i = k0 + threadIdx.x + 512 * q;
+      double v = 0.0;
+#pragma unroll
+      for (int c = 0; c < kNbReg; ++c)
+        if (c == j) v = a[q][c];
+      if (i >= jr && i < n) {
+        const double av = fabs(v);
+        if (av > best || (av == best && i < bi)) { best = av; bi = i; }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    if (lane == 0) { sv[wid] = best; si[wid] = bi; }
+    __syncthreads();
+    if (wid == 0) {
+      best = lane < 16 ? sv[lane] : -1.0;
+      bi = lane < 16 ? si[lane] : 0x7fffffff;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (lane == 0) {
+        s_p = (bi == 0x7fffffff) ? jr : bi;
+        piv[jr] = s_p;
+      }
+    }
+    __syncthreads();
+    const int p = s_p;
+    // owners publish the pivot row and the row it displaces
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      const int i = k0 + threadIdx.x + 512 * q;
+      if (i == p)
+#pragma unroll
+        for (int c = 0; c < kNbReg; ++c) srow[0][c] = a[q][c];
+      if (i == jr && p != jr)
+#pragma unroll
+        for (int c = 0; c < kNbReg; ++c) srow[1][c] = a[q][c];
+    }
+    __syncthreads();
+    const double d = srow[0][j];
+    const double inv = d != 0.0 ? 1.0 / d : 0.0;
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      const int i = k0 + threadIdx.x + 512 * q;
+      if (i == jr && p != jr) {
+#pragma unroll
+        for (int c = 0; c < kNbReg; ++c) a[q][c] = srow[0][c];
+      } else if (i == p && p != jr) {
+#pragma unroll
+        for (int c = 0; c < kNbReg; ++c) a[q][c] = srow[1][c];
+      }
+      if (i > jr && i < n && d != 0.0) {
+        double l = 0.0;
+#pragma unroll
+        for (int c = 0; c < kNbReg; ++c)
+          if (c == j) { l = a[q][c] * inv; a[q][c] = l; }
+#pragma unroll
+        for (int c = 0; c < kNbReg; ++c)
+          if (c > j) a[q][c] = fma(-l, srow[0][c], a[q][c]);
+      }
+    }
+    __syncthreads();  // srow is rewritten by the next column
+  }
+#pragma unroll
+  for (int q = 0; q < RPT; ++q) {
+    const int i = k0 + threadIdx.x + 512 * q;
+    if (i < n)
+#pragma unroll
+      for (int c = 0; c < kNbReg; ++c)
+        if (c < nb) A[(int64_t)(k0 + c) * ld + i] = a[q][c];
+  }
+}
+
+// Row interchanges of panel [k0, k0+nb) applied to the columns outside it,
+// in order; one thread per column.
+__global__ void k_lu_laswp(double* A, int64_t ld, int n, int k0, int nb, const int* piv) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n - nb) return;
+  if (c >= k0) c += nb;
+  double* col = A + (int64_t)c * ld;
+  for (int j = 0; j < nb; ++j) {
+    const int p = piv[k0 + j];
+    if (p != k0 + j) {
+      const double t = col[k0 + j];
+      col[k0 + j] = col[p];
+      col[p] = t;
+    }
+  }
+}
+
+// Pivot check + blocked triangular solves with the whole CTA, x in shared
+// memory.  Per 32-row block: warp 0 solves the diagonal block (each lane holds
+// its row of the block in registers; the columns are broadcast by shuffle),
+// then every thread subtracts the block's contribution from its remaining
+// rows (coalesced column reads) -- two barriers per block instead of one per row.
+__global__ void __launch_bounds__(512) k_lu_solve_cta(const double* A, int64_t ld, int n, const int* piv,
+                                                       double* X, int64_t ldx, int nrhs, const double* fro,
+                                                       double* info) {
+  extern __shared__ double xs[];
+  __shared__ int s_bad;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_bad = 0x7fffffff;
+  __syncthreads();
+  const double floor = 1e-14 * fro[0];
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    if (fabs(A[(int64_t)i * ld + i]) <= floor) atomicMin(&s_bad, i);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    info[0] = (s_bad == 0x7fffffff) ? -1.0 : (double)s_bad;
+    info[1] = (s_bad == 0x7fffffff) ? 0.0 : fabs(A[(int64_t)s_bad * ld + s_bad]);
+    info[2] = floor;
+  }
+  if (s_bad != 0x7fffffff) return;
+  for (int rc = 0; rc < nrhs; ++rc) {
+    double* x = X + (int64_t)rc * ldx;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) xs[i] = x[i];
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int j = 0; j < n; ++j) {
+        const int p = piv[j];
+        if (p != j) { const double t = xs[j]; xs[j] = xs[p]; xs[p] = t; }
+      }
+    __syncthreads();
+    // forward: unit lower L
+    for (int b0 = 0; b0 < n; b0 += 32) {
+      const int bw = min(32, n - b0);
+      if (wid == 0) {
+        double lrow[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) lrow[j] = (lane < bw && j < lane) ? A[(int64_t)(b0 + j) * ld + b0 + lane] : 0.0;
+        double xi = lane < bw ? xs[b0 + lane] : 0.0;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const double xj = __shfl_sync(0xffffffffu, xi, j);
+          if (lane > j) xi = fma(-lrow[j], xj, xi);
+        }
+        if (lane < bw) xs[b0 + lane] = xi;
+      }
+      __syncthreads();
+      for (int i = b0 + bw + threadIdx.x; i < n; i += blockDim.x) {
+        double acc = 0.0;
+        for (int j = 0; j < bw; ++j) acc = fma(A[(int64_t)(b0 + j) * ld + i], xs[b0 + j], acc);
+        xs[i] -= acc;
+      }
+      __syncthreads();
+    }
+    // backward: upper U (blocks from the bottom)
+    for (int b1 = n; b1 > 0; b1 -= 32) {
+      const int b0 = max(0, b1 - 32), bw = b1 - b0;
+      if (wid == 0) {
+        double urow[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) urow[j] = (lane < bw && j >= lane && j < bw) ? A[(int64_t)(b0 + j) * ld + b0 + lane] : 0.0;
+        double xi = lane < bw ? xs[b0 + lane] : 0.0;
+#pragma unroll
+        for (int j = 31; j >= 0; --j) {
+          if (j < bw) {
+            double xj = __shfl_sync(0xffffffffu, xi, j);
+            if (lane == j) { xi = xi / urow[j]; }
+            xj = __shfl_sync(0xffffffffu, xi, j);
+            if (lane < j) xi = fma(-urow[j], xj, xi);
+          }
+        }
+        if (lane < bw) xs[b0 + lane] = xi;
+      }
+      __syncthreads();
+      for (int i = threadIdx.x; i < b0; i += blockDim.x) {
+        double acc = 0.0;
+        for (int j = 0; j < bw; ++j) acc = fma(A[(int64_t)(b0 + j) * ld + i], xs[b0 + j], acc);
+        xs[i] -= acc;
+      }
+      __syncthreads();
+    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] = xs[i];
+    __syncthreads();
+  }
+}
+
+// ||A||_F: per-CTA partial sums of squares, then one CTA adds them in order.
+__global__ void __launch_bounds__(256) k_fro_part(const double* A, int64_t ld, int64_t n, double* part) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n * n;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const double v = A[(idx / n) * ld + idx % n];
+    s = fma(v, v, s);
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+__global__ void __launch_bounds__(256) k_fro_final(const double* part, int np, double* out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) s += part[i];
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) out[0] = sqrt(s);
+}
+
 __global__ void __launch_bounds__(1024) k_qr(double* M, int64_t ld, int rows, int cols, double* R, double* work) {
   __shared__ double red[32];
   cta_householder_qr(M, (int)ld, rows, cols, R, cols, work, work + cols, red);
@@ -226,12 +459,30 @@ int strom_dense_solve(int64_t n, double* a_dev, double* x_dev, int64_t nrhs, int
     double* fro = scratch->as<double>();
     double* info = info_dev ? info_dev : fro + 2;
     int* piv = piv_dev ? piv_dev : reinterpret_cast<int*>(fro + 8);
-    k_fro_norm<<<1, 1024, 0, s>>>(a_dev, n, n, fro);
-    STROM_LAUNCH_CHECK();
-    for (int64_t k0 = 0; k0 < n; k0 += kNb) {
-      const int nb = (int)std::min<int64_t>(kNb, n - k0);
-      k_lu_panel<<<1, 1024, 0, s>>>(a_dev, n, (int)n, (int)k0, nb, piv);
+    {
+      const int np = 256;
+      auto fp = dev_alloc((size_t)np * 8, s, false);
+      k_fro_part<<<np, 256, 0, s>>>(a_dev, n, n, fp->as<double>());
+      k_fro_final<<<1, 256, 0, s>>>(fp->as<double>(), np, fro);
       STROM_LAUNCH_CHECK();
+    }
+    const bool reg_panel = n <= 1024;  // panel rows fit two per thread (512 threads) in registers
+    const bool cta_solve = (size_t)n * 8 <= 96 * 1024;
+    const int step = reg_panel ? kNbReg : kNb;
+    for (int64_t k0 = 0; k0 < n; k0 += step) {
+      const int nb = (int)std::min<int64_t>(step, n - k0);
+      if (reg_panel) {
+        if (n - k0 <= 512) k_lu_panel_reg<1><<<1, 512, 0, s>>>(a_dev, n, (int)n, (int)k0, nb, piv);
+        else k_lu_panel_reg<2><<<1, 512, 0, s>>>(a_dev, n, (int)n, (int)k0, nb, piv);
+        STROM_LAUNCH_CHECK();
+        if (n > nb) {
+          k_lu_laswp<<<(unsigned)ceil_div(n - nb, 128), 128, 0, s>>>(a_dev, n, (int)n, (int)k0, nb, piv);
+          STROM_LAUNCH_CHECK();
+        }
+      } else {
+        k_lu_panel<<<1, 1024, 0, s>>>(a_dev, n, (int)n, (int)k0, nb, piv);
+        STROM_LAUNCH_CHECK();
+      }
       const int64_t rest = n - k0 - nb;
       if (rest > 0) {
         k_lu_trsm<<<(unsigned)ceil_div(rest, 128), 128, 0, s>>>(a_dev, n, (int)n, (int)k0, nb);
@@ -241,7 +492,16 @@ int strom_dense_solve(int64_t n, double* a_dev, double* x_dev, int64_t nrhs, int
         STROM_LAUNCH_CHECK();
       }
     }
-    k_lu_solve<<<1, 1024, 0, s>>>(a_dev, n, (int)n, piv, x_dev, n, (int)nrhs, fro, info);
+    if (cta_solve) {
+      static bool cfg = false;
+      if (!cfg) {
+        STROM_CUDA(cudaFuncSetAttribute(k_lu_solve_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+        cfg = true;
+      }
+      k_lu_solve_cta<<<1, 512, (size_t)n * 8, s>>>(a_dev, n, (int)n, piv, x_dev, n, (int)nrhs, fro, info);
+    } else {
+      k_lu_solve<<<1, 1024, 0, s>>>(a_dev, n, (int)n, piv, x_dev, n, (int)nrhs, fro, info);
+    }
     STROM_LAUNCH_CHECK();
     double h[3];
     STROM_CUDA(cudaMemcpyAsync(h, info, 3 * 8, cudaMemcpyDeviceToHost, s));

@@ -20,8 +20,11 @@ __all__ = ["SingularMatrixError", "ConvergenceError", "thin_svd", "qr", "solve_d
 
 
 def _cm(m: torch.Tensor) -> torch.Tensor:
-    """Column-major contiguous copy of a 2-D tensor as a flat storage owner."""
-    return m.t().contiguous()  # (cols, rows) row-major == (rows, cols) column-major
+    """Column-major copy of a 2-D tensor as a flat storage owner (always a copy:
+    ``t().contiguous()`` would alias an (n, 1) input, and the kernels work in place)."""
+    out = torch.empty((m.shape[1], m.shape[0]), dtype=m.dtype, device=m.device)
+    out.copy_(m.t())
+    return out  # (cols, rows) row-major == (rows, cols) column-major
 
 
 def thin_svd(m):

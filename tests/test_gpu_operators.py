@@ -302,3 +302,16 @@ class TestCfg1EndToEnd:
         print(f"cfg1 ST-ROM states rel vs reference {rel:.2e}; reference reduction-order envelope {env:.2e}")
         assert np.allclose(ref.sum(axis=0), g["states_colsum"], rtol=1e-12)
         assert rel <= max(1e-8, 10 * env)
+
+
+def test_solve_dense_leaves_inputs_untouched(cuda):
+    """solve_dense is pure like the reference's (linalg.py:75-99): a 1-D right-hand side
+    must not be overwritten by the in-place device solve."""
+    rng = np.random.default_rng(40)
+    a = torch.as_tensor(rng.standard_normal((40, 40)) + 2.0 * np.eye(40), device="cuda")
+    b = torch.as_tensor(rng.standard_normal(40), device="cuda")
+    a0, b0 = a.clone(), b.clone()
+    x1 = linalg.solve_dense(a, b)
+    x2 = linalg.solve_dense(a, b)
+    assert torch.equal(a, a0) and torch.equal(b, b0) and torch.equal(x1, x2)
+    assert float(torch.linalg.norm(a @ x1 - b)) <= 1e-12 * float(torch.linalg.norm(b))
