@@ -186,6 +186,15 @@ int strom_spatial_reduce_ell(int64_t n, int32_t K, const uint32_t* eidx_dev, con
                              const double* phi_dev, int64_t ld, int64_t ns, const double* extra_dev, int64_t ext_ld,
                              int64_t ne, const double* xref_dev, double* out_dev, void* stream);
 
+/* Dense LU with partial pivoting kept for repeated solves -- the reference's
+ * StepSolver pattern (system.py:106-125: one factor per dt, one solve per
+ * step).  a_dev / lu_dev: n x n column-major, factored in place; piv_dev: n
+ * ints; x_dev: n x nrhs column-major, overwritten.  Asynchronous; no pivot-floor
+ * test (strom_dense_solve has it). */
+int strom_dense_lu(int64_t n, double* a_dev, int32_t* piv_dev, void* stream);
+int strom_dense_lu_solve(int64_t n, const double* lu_dev, const int32_t* piv_dev, double* x_dev, int64_t nrhs,
+                         void* stream);
+
 /* fom_march (system.py:150-163) on the device: (I - dt_k A) x_k = x_{k-1} +
  * dt_k B f_k for k = 1..N_t by Jacobi-preconditioned BiCGSTAB (relative
  * residual tol, at most maxit iterations per step) in one cooperative kernel,

@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(1024) k_lu_solve(const double* A, int64_t ld, 
   __shared__ int s_bad;
   if (threadIdx.x == 0) s_bad = 0x7fffffff;
   __syncthreads();
-  const double floor = 1e-14 * fro[0];
+  const double floor = fro ? 1e-14 * fro[0] : -1.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x)
     if (fabs(A[(int64_t)i * ld + i]) <= floor) atomicMin(&s_bad, i);
   __syncthreads();
@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(512) k_lu_solve_cta(const double* A, int64_t l
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (threadIdx.x == 0) s_bad = 0x7fffffff;
   __syncthreads();
-  const double floor = 1e-14 * fro[0];
+  const double floor = fro ? 1e-14 * fro[0] : -1.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x)
     if (fabs(A[(int64_t)i * ld + i]) <= floor) atomicMin(&s_bad, i);
   __syncthreads();
@@ -442,9 +442,77 @@ __global__ void __launch_bounds__(1024) k_qr(double* M, int64_t ld, int rows, in
   cta_householder_qr(M, (int)ld, rows, cols, R, cols, work, work + cols, red);
 }
 
+// Blocked right-looking LU with partial pivoting of the n x n column-major a (in place).
+void lu_factor(int64_t n, double* a_dev, int* piv, cudaStream_t s) {
+  const bool reg_panel = n <= 1024;  // panel rows fit two per thread (512 threads) in registers
+  const int step = reg_panel ? kNbReg : kNb;
+  for (int64_t k0 = 0; k0 < n; k0 += step) {
+    const int nb = (int)std::min<int64_t>(step, n - k0);
+    if (reg_panel) {
+      if (n - k0 <= 512) k_lu_panel_reg<1><<<1, 512, 0, s>>>(a_dev, n, (int)n, (int)k0, nb, piv);
+      else k_lu_panel_reg<2><<<1, 512, 0, s>>>(a_dev, n, (int)n, (int)k0, nb, piv);
+      STROM_LAUNCH_CHECK();
+      if (n > nb) {
+        k_lu_laswp<<<(unsigned)ceil_div(n - nb, 128), 128, 0, s>>>(a_dev, n, (int)n, (int)k0, nb, piv);
+        STROM_LAUNCH_CHECK();
+      }
+    } else {
+      k_lu_panel<<<1, 1024, 0, s>>>(a_dev, n, (int)n, (int)k0, nb, piv);
+      STROM_LAUNCH_CHECK();
+    }
+    const int64_t rest = n - k0 - nb;
+    if (rest > 0) {
+      k_lu_trsm<<<(unsigned)ceil_div(rest, 128), 128, 0, s>>>(a_dev, n, (int)n, (int)k0, nb);
+      STROM_LAUNCH_CHECK();
+      dim3 g((unsigned)ceil_div(rest, 64), (unsigned)ceil_div(rest, 64));
+      k_lu_gemm<<<g, 256, 0, s>>>(a_dev, n, (int)n, (int)k0, nb);
+      STROM_LAUNCH_CHECK();
+    }
+  }
+}
+
+// Pivot-floor check (floor = 1e-14 fro[0]; fro NULL: no check) and the two
+// triangular solves of nrhs columns of x (ldx).
+void lu_solve(int64_t n, const double* a_dev, const int* piv, double* x_dev, int64_t ldx, int64_t nrhs,
+              const double* fro, double* info, cudaStream_t s) {
+  if ((size_t)n * 8 <= 96 * 1024) {
+    static bool cfg = false;
+    if (!cfg) {
+      STROM_CUDA(cudaFuncSetAttribute(k_lu_solve_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+      cfg = true;
+    }
+    k_lu_solve_cta<<<1, 512, (size_t)n * 8, s>>>(a_dev, n, (int)n, piv, x_dev, ldx, (int)nrhs, fro, info);
+  } else {
+    k_lu_solve<<<1, 1024, 0, s>>>(a_dev, n, (int)n, piv, x_dev, ldx, (int)nrhs, fro, info);
+  }
+  STROM_LAUNCH_CHECK();
+}
+
 }  // namespace
 
 extern "C" {
+
+// LU of the n x n column-major a_dev in place (pivots in piv_dev, n ints) and
+// the solves with a stored factor -- the reference's StepSolver pattern
+// (system.py:106-125: factor once per dt, solve per step).  Asynchronous; no
+// pivot-floor test (a singular factor yields non-finite solutions).
+int strom_dense_lu(int64_t n, double* a_dev, int32_t* piv_dev, void* stream) {
+  return guarded([&] {
+    STROM_REQUIRE(n >= 1 && a_dev && piv_dev, "bad LU arguments");
+    lu_factor(n, a_dev, piv_dev, reinterpret_cast<cudaStream_t>(stream));
+  });
+}
+
+int strom_dense_lu_solve(int64_t n, const double* lu_dev, const int32_t* piv_dev, double* x_dev, int64_t nrhs,
+                         void* stream) {
+  return guarded([&] {
+    STROM_REQUIRE(n >= 1 && lu_dev && piv_dev && x_dev && nrhs >= 0, "bad LU-solve arguments");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    auto info = dev_alloc(3 * 8, s, false);
+    lu_solve(n, lu_dev, piv_dev, x_dev, n, nrhs, nullptr, info->as<double>(), s);
+  });
+}
+
 
 // LU factorization with partial pivoting of A (n x n, column-major, in place)
 // and solve for nrhs right-hand sides X (in place).  On a pivot with
@@ -466,43 +534,8 @@ int strom_dense_solve(int64_t n, double* a_dev, double* x_dev, int64_t nrhs, int
       k_fro_final<<<1, 256, 0, s>>>(fp->as<double>(), np, fro);
       STROM_LAUNCH_CHECK();
     }
-    const bool reg_panel = n <= 1024;  // panel rows fit two per thread (512 threads) in registers
-    const bool cta_solve = (size_t)n * 8 <= 96 * 1024;
-    const int step = reg_panel ? kNbReg : kNb;
-    for (int64_t k0 = 0; k0 < n; k0 += step) {
-      const int nb = (int)std::min<int64_t>(step, n - k0);
-      if (reg_panel) {
-        if (n - k0 <= 512) k_lu_panel_reg<1><<<1, 512, 0, s>>>(a_dev, n, (int)n, (int)k0, nb, piv);
-        else k_lu_panel_reg<2><<<1, 512, 0, s>>>(a_dev, n, (int)n, (int)k0, nb, piv);
-        STROM_LAUNCH_CHECK();
-        if (n > nb) {
-          k_lu_laswp<<<(unsigned)ceil_div(n - nb, 128), 128, 0, s>>>(a_dev, n, (int)n, (int)k0, nb, piv);
-          STROM_LAUNCH_CHECK();
-        }
-      } else {
-        k_lu_panel<<<1, 1024, 0, s>>>(a_dev, n, (int)n, (int)k0, nb, piv);
-        STROM_LAUNCH_CHECK();
-      }
-      const int64_t rest = n - k0 - nb;
-      if (rest > 0) {
-        k_lu_trsm<<<(unsigned)ceil_div(rest, 128), 128, 0, s>>>(a_dev, n, (int)n, (int)k0, nb);
-        STROM_LAUNCH_CHECK();
-        dim3 g((unsigned)ceil_div(rest, 64), (unsigned)ceil_div(rest, 64));
-        k_lu_gemm<<<g, 256, 0, s>>>(a_dev, n, (int)n, (int)k0, nb);
-        STROM_LAUNCH_CHECK();
-      }
-    }
-    if (cta_solve) {
-      static bool cfg = false;
-      if (!cfg) {
-        STROM_CUDA(cudaFuncSetAttribute(k_lu_solve_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-        cfg = true;
-      }
-      k_lu_solve_cta<<<1, 512, (size_t)n * 8, s>>>(a_dev, n, (int)n, piv, x_dev, n, (int)nrhs, fro, info);
-    } else {
-      k_lu_solve<<<1, 1024, 0, s>>>(a_dev, n, (int)n, piv, x_dev, n, (int)nrhs, fro, info);
-    }
-    STROM_LAUNCH_CHECK();
+    lu_factor(n, a_dev, piv, s);
+    lu_solve(n, a_dev, piv, x_dev, n, nrhs, fro, info, s);
     double h[3];
     STROM_CUDA(cudaMemcpyAsync(h, info, 3 * 8, cudaMemcpyDeviceToHost, s));
     STROM_CUDA(cudaStreamSynchronize(s));

@@ -152,35 +152,78 @@ class FomResult(NamedTuple):
     iterations: list
 
 
-def fom_march(sys: LinearDynamicalSystem, grid: TimeGrid, tol: float = 1e-13, maxit: int = 500) -> FomResult:
+DIRECT_MAX_N = 4096  # the dense StepSolver path is offered up to this size
+
+
+def fom_march(sys: LinearDynamicalSystem, grid: TimeGrid, tol: float = 1e-13, maxit: int = 500,
+              method: str = "auto") -> FomResult:
     """March the full-order model over the grid on the device (system.py:150-163).
 
-    The reference solves each backward-Euler step (I - dt A) x_k = x_{k-1} +
-    dt B f_k with a cached SuperLU factor; here one cooperative kernel
-    (C ABI ``strom_fom_march``) marches all steps with Jacobi-preconditioned
-    BiCGSTAB to a relative residual ``tol``, over the operator's tiled-ELL form,
-    so snapshots stay in HBM for ``ingest_simulation``.  The clock covers the
-    march only, like the reference's.
+    ``method="krylov"`` (the default for sparse operators) runs one cooperative
+    kernel that marches all steps with Jacobi-preconditioned BiCGSTAB to a
+    relative residual ``tol`` over the operator's tiled-ELL form
+    (``strom_fom_march``) -- the path for operators SuperLU cannot factor
+    (cfg3: 2^20 dofs in 3D).  ``method="direct"`` (the default for operators
+    with more than 16 off-diagonals per row, n <= 4096) mirrors the
+    reference's StepSolver: one dense LU of I - dt A per distinct dt
+    (system.py:106-125), then two triangular solves per step (C ABI
+    ``strom_dense_lu`` / ``strom_dense_lu_solve``).  States stay in HBM for ``ingest_simulation``;
+    the clock covers the march only, like the reference's.
     """
     from . import _capi as capi
 
-    dev = sys.device_arrays()
-    ell = dev.get("ell")
-    if ell is None:
-        raise ValueError("fom_march on the device needs at most 16 off-diagonal entries per row of A")
     n, nt, m = sys.n_states, grid.n_steps, sys.n_inputs
+    if method not in ("auto", "direct", "krylov"):
+        raise ValueError(f"unknown fom_march method {method!r}")
+    dev = sys.device_arrays()
+    if method == "auto":
+        method = "krylov" if (dev.get("ell") is not None or n > DIRECT_MAX_N) else "direct"
+    if method == "direct" and n > DIRECT_MAX_N:
+        raise ValueError(f"the dense StepSolver path supports n <= {DIRECT_MAX_N}")
     f = np.stack([np.atleast_1d(np.asarray(sys.input_signal(k), dtype=float)).reshape(m)
                   for k in range(1, nt + 1)])
     f_dev = torch.as_tensor(f, dtype=F64, device=device()).contiguous()
-    b_cm = dev["b"].T.contiguous()  # m x n: B column-major
     states = torch.empty((nt, n), dtype=F64, device=device())
-    iters = (capi.C.c_int32 * nt)()
-    torch.cuda.synchronize()
-    start = time.perf_counter()
-    capi.call("strom_fom_march", n, ell["k"], ell["idx"].data_ptr(), ell["val"].data_ptr(), b_cm.data_ptr(), m,
-              dev["x0"].data_ptr(), grid.dt_device().data_ptr(), f_dev.data_ptr(), nt, float(tol), int(maxit),
-              states.data_ptr(), iters, capi.stream_ptr())
-    wall = time.perf_counter() - start
+    if method == "direct":
+        a_dense = torch.as_tensor(sys.a.toarray(), dtype=F64, device=device())
+        eye = torch.eye(n, dtype=F64, device=device())
+        torch.cuda.synchronize()
+        start = time.perf_counter()
+        facs = {}
+        x = dev["x0"]
+        b = dev["b"]
+        iters = []
+        for k in range(nt):
+            h = float(grid.dt[k])
+            fac = facs.get(h)
+            if fac is None:
+                lu = (eye - h * a_dense).T.contiguous()  # column-major copy of I - h A
+                piv = torch.empty(n, dtype=torch.int32, device=device())
+                capi.call("strom_dense_lu", n, lu.data_ptr(), piv.data_ptr(), capi.stream_ptr())
+                fac = facs[h] = (lu, piv)
+            xk = states[k]
+            torch.add(x, b @ f_dev[k], alpha=h, out=xk)  # rhs = x_{k-1} + dt B f_k
+            capi.call("strom_dense_lu_solve", n, fac[0].data_ptr(), fac[1].data_ptr(), xk.data_ptr(), 1,
+                      capi.stream_ptr())
+            x = xk
+            iters.append(0)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - start
+        if not bool(torch.isfinite(states).all()):
+            raise ValueError("fom_march: I - dt A is singular for a step of the grid")
+    else:
+        ell = dev.get("ell")
+        if ell is None:
+            raise ValueError("fom_march on the device needs at most 16 off-diagonal entries per row of A")
+        b_cm = dev["b"].T.contiguous()  # m x n: B column-major
+        it = (capi.C.c_int32 * nt)()
+        torch.cuda.synchronize()
+        start = time.perf_counter()
+        capi.call("strom_fom_march", n, ell["k"], ell["idx"].data_ptr(), ell["val"].data_ptr(), b_cm.data_ptr(),
+                  m, dev["x0"].data_ptr(), grid.dt_device().data_ptr(), f_dev.data_ptr(), nt, float(tol),
+                  int(maxit), states.data_ptr(), it, capi.stream_ptr())
+        wall = time.perf_counter() - start
+        iters = list(it)
     st = states.T  # n x N_t, column-major
     outputs = dev["c"].T @ st
-    return FomResult(st, outputs, wall, list(iters))
+    return FomResult(st, outputs, wall, iters)

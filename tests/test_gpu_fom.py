@@ -1,10 +1,10 @@
 """Device full-order march (reference system.py:150-163 fom_march) against the
 reference's own states and the oracle's SuperLU march.
 
-The reference factors I - dt A once per dt; the device runs Jacobi-
-preconditioned BiCGSTAB per step to a relative residual of 1e-13, so states
-agree to the solver tolerance carried through the march: the bar is 1e-10
-relative (max-abs, per column) against the reference.
+The reference factors I - dt A once per dt (SuperLU).  The device's "direct"
+path does the same with a dense LU (n <= 2048); the "krylov" path runs
+Jacobi-preconditioned BiCGSTAB per step to a relative residual of 1e-13.  Both
+are held to 1e-10 relative (max-abs, per column) against the reference.
 """
 
 import numpy as np
@@ -28,14 +28,16 @@ def _col_rel(a, b):
     return float(np.max(np.abs(a - b).max(axis=0) / np.maximum(np.abs(b).max(axis=0), 1e-300)))
 
 
-def test_cfg1_states_match_reference_golden(cuda):
+@pytest.mark.parametrize("method", ["direct", "krylov"])
+def test_cfg1_states_match_reference_golden(cuda, method):
     """The four cfg1 training marches vs the reference's fom_march checksums."""
     g = load_golden("golden_cfg1.npz")
     grid = TimeGrid(wl.cfg1_dt())
     mats = []
     for nu in wl.CFG1_TRAIN_NU:
-        res = fom_march(_lds(wl.cfg1_system(nu)), grid)
-        assert all(0 < it <= 500 for it in res.iterations)
+        res = fom_march(_lds(wl.cfg1_system(nu)), grid, method=method)
+        if method == "krylov":
+            assert all(0 < it <= 500 for it in res.iterations)
         mats.append(npy(res.states))
     u = np.hstack(mats)
     assert np.max(np.abs(u.sum(axis=0) - g["u_colsum"]) / np.abs(g["u_colsum"])) <= 1e-10
@@ -43,20 +45,22 @@ def test_cfg1_states_match_reference_golden(cuda):
     assert _col_rel(u[::97, ::7], g["u_sample"]) <= 1e-9
 
 
-def test_transport_proxy_matches_oracle(cuda):
+@pytest.mark.parametrize("method", ["direct", "krylov"])
+def test_transport_proxy_matches_oracle(cuda, method):
     """cfg3's operator at 8^3 cells x 4 directions vs the SuperLU march."""
     a = wl.cfg3_operator(8)
     for amp in (0.5, 2.0):
         d = wl.cfg3_system(amp, nc=8, a=a)
         grid = TimeGrid(np.full(20, wl.CFG3_DT))
-        res = fom_march(_lds(d), grid)
+        res = fom_march(_lds(d), grid, method=method)
         ref = so.fom_march(d.a, d.b, d.x0, grid.dt, d.inputs)
         assert _col_rel(npy(res.states), ref) <= 1e-11
         # output C^T x like the reference's FomResult.outputs
         np.testing.assert_allclose(npy(res.outputs), d.c.T @ ref, rtol=1e-11)
 
 
-def test_nonuniform_grid_and_inputs(cuda):
+@pytest.mark.parametrize("method", ["direct", "krylov"])
+def test_nonuniform_grid_and_inputs(cuda, method):
     """Per-step dt and a time-varying input (the general rhs of backward_euler_step)."""
     a = wl.cfg3_operator(4)
     d = wl.cfg3_system(1.0, nc=4, a=a)
@@ -64,7 +68,7 @@ def test_nonuniform_grid_and_inputs(cuda):
     f = rng.uniform(0.5, 2.0, 12)
     sys_ = LinearDynamicalSystem(a=d.a, b=d.b, c=d.c, x0=d.x0, input_signal=lambda k: np.array([f[k - 1]]))
     dt = rng.uniform(0.002, 0.02, 12)
-    res = fom_march(sys_, TimeGrid(dt))
+    res = fom_march(sys_, TimeGrid(dt), method=method)
     ref = so.fom_march(d.a, d.b, d.x0, dt, lambda k: np.array([f[k - 1]]))
     assert _col_rel(npy(res.states), ref) <= 1e-11
 
@@ -72,15 +76,21 @@ def test_nonuniform_grid_and_inputs(cuda):
 def test_unconverged_step_raises(cuda):
     d = wl.cfg3_system(1.0, nc=4)
     with pytest.raises(ValueError, match="did not reach"):
-        fom_march(_lds(d), TimeGrid(np.full(3, 0.5)), tol=1e-15, maxit=1)
+        fom_march(_lds(d), TimeGrid(np.full(3, 0.5)), tol=1e-15, maxit=1, method="krylov")
 
 
-def test_dense_operator_rejected(cuda):
+def test_dense_operator_direct_and_krylov_rejected(cuda):
+    """A dense operator: the direct path marches it like the reference; the ELL
+    (Krylov) path refuses rows with more than 16 off-diagonal entries."""
     rng = np.random.default_rng(0)
     d = wl.random_stable_system(rng, 40)
     sys_ = LinearDynamicalSystem(a=d["a"], b=d["b"], c=d["c"], x0=d["x0"], input_signal=d["inputs"])
+    dt = np.full(5, 0.01)
+    res = fom_march(sys_, TimeGrid(dt))
+    ref = so.fom_march(d["a"], d["b"], d["x0"], dt, d["inputs"])
+    assert _col_rel(npy(res.states), ref) <= 1e-12
     with pytest.raises(ValueError, match="off-diagonal"):
-        fom_march(sys_, TimeGrid(np.full(3, 0.01)))
+        fom_march(sys_, TimeGrid(dt), method="krylov")
 
 
 def test_cfg3_pipeline_scaled_vs_oracle(cuda):
