@@ -141,3 +141,26 @@ def reconstruct_states(basis: BasisSet, x_hat_st) -> torch.Tensor:
     blocks = x_hat_st.reshape(basis.n_t, basis.n_s)            # (n_t, n_s)
     coeffs = torch.einsum("ikj,ji->ik", basis.temporal_stack(), blocks)  # (n_s, N_t)
     return basis.phi_s @ coeffs
+
+
+ST_VERIFICATION_CAP = 20_000  # system.py:23
+
+
+def explicit_st_basis(basis: BasisSet, cap: int = ST_VERIFICATION_CAP) -> torch.Tensor:
+    """The space-time basis, column i + n_s j = psi_i^j (x) phi_i (spacetime.py:189-210).
+
+    A verification oracle only, refused above ``cap`` rows like the
+    reference's: at production size it is exactly what the block-structured
+    assembly avoids.  Built on the device as one broadcast product.
+    """
+    from .errors import CapExceededError
+
+    n_rows = basis.phi_s.shape[0] * basis.n_steps
+    if n_rows > cap:
+        raise CapExceededError(f"explicit space-time basis would have {n_rows} rows, above the "
+                               f"verification cap {cap}; it exists only as a testing oracle")
+    psi = basis.temporal_stack()                          # (n_s, N_t, n_t)
+    phi = basis.phi_s                                     # (N, n_s)
+    # [k, r, j, i] = psi[i, k, j] * phi[r, i]  ->  rows k N + r, columns j n_s + i
+    out = psi.permute(1, 2, 0)[:, None, :, :] * phi[None, :, None, :]
+    return out.reshape(basis.n_steps * phi.shape[0], basis.n_t * basis.n_s)
