@@ -10,6 +10,7 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import numpy as np
 import torch
 
 from . import _capi as capi
@@ -105,3 +106,48 @@ def build_spatial_rom(sys: LinearDynamicalSystem, basis: BasisSet,
     y_ref = dev["c"].T @ x_ref if ref_mode == "initial_state" else torch.zeros(p, dtype=F64, device=phi.device)
     return SpatialRom(a_hat=a_hat, b_hat=b_hat, c_hat=c_hat, x_ref=x_ref, x_ref_hat=x_ref_hat,
                       x0_hat=x0_hat, y_ref=y_ref, ref_mode=ref_mode)
+
+
+def srom_march(rom: SpatialRom, grid, inputs) -> torch.Tensor:
+    """March the reduced coordinates over the grid; column k-1 holds xhat_k (spatial.py:68-85).
+
+    One device LU of I - dt A_hat per distinct dt (``strom_dense_lu``), two
+    triangular solves per step (``strom_dense_lu_solve``), like the
+    reference's ``lu_factor`` / ``lu_solve`` cache.
+    """
+    n_s, nt = rom.n_s, grid.n_steps
+    dev = rom.a_hat.device
+    traj = torch.empty((nt, n_s), dtype=F64, device=dev)
+    eye = torch.eye(n_s, dtype=F64, device=dev)
+    factors = {}
+    x = rom.x0_hat
+    for k in range(nt):
+        dt = float(grid.dt[k])
+        fac = factors.get(dt)
+        if fac is None:
+            lu = (eye - dt * rom.a_hat).T.contiguous()  # column-major
+            piv = torch.empty(n_s, dtype=torch.int32, device=dev)
+            capi.call("strom_dense_lu", n_s, lu.data_ptr(), piv.data_ptr(), capi.stream_ptr())
+            fac = factors[dt] = (lu, piv)
+        f = torch.as_tensor(np.atleast_1d(np.asarray(inputs(k + 1), dtype=float)), dtype=F64, device=dev)
+        xk = traj[k]
+        torch.add(x + dt * rom.x_ref_hat, rom.b_hat @ f, alpha=dt, out=xk)
+        capi.call("strom_dense_lu_solve", n_s, fac[0].data_ptr(), fac[1].data_ptr(), xk.data_ptr(), 1,
+                  capi.stream_ptr())
+        x = xk
+    return traj.T
+
+
+def srom_output(rom: SpatialRom, x_hat) -> torch.Tensor:
+    """y = C_hat^T xhat + C^T x_ref, for a vector or a trajectory (spatial.py:88-92)."""
+    x_hat = to_dev(x_hat)
+    y = rom.c_hat.T @ x_hat
+    return y + (rom.y_ref if x_hat.dim() == 1 else rom.y_ref[:, None])
+
+
+def reconstruct_states(rom: SpatialRom, basis: BasisSet, x_hat) -> torch.Tensor:
+    """Lift reduced coordinates: x_ref + Phi_s xhat (spatial.py:95-100; not the
+    space-time ``reconstruct_states`` that the package exports)."""
+    x_hat = to_dev(x_hat)
+    lifted = basis.phi_s @ x_hat
+    return lifted + (rom.x_ref if x_hat.dim() == 1 else rom.x_ref[:, None])
