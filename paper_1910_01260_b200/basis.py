@@ -23,9 +23,11 @@ from . import _capi as capi
 from ._tensors import F64, colmajor, device, to_dev
 from .errors import BasisError
 
+EPS = float(np.finfo(float).eps)
+
 __all__ = [
     "BasisError", "SvdState", "isvd_init", "isvd_update", "ingest_simulation",
-    "temporal_snapshots", "BasisSet", "build_basis_set",
+    "temporal_snapshots", "BasisSet", "build_basis_set", "batch_pod", "basis_set_from_pod",
 ]
 
 _CAP_MODES = ("restart", "truncate")
@@ -365,3 +367,32 @@ def build_basis_set(state: SvdState, n_s: int, n_t: int, n_steps: int, n_mu: int
         raise BasisError(
             f"temporal snapshots of mode {i} have rank {int(ranks[i])}, cannot supply n_t={n_t}")
     return BasisSet(phi_s=state.phi[:, :n_s].clone(), temporal=psi, n_mu=n_mu)
+
+
+def batch_pod(u, n_s: int):
+    """One-shot POD of a snapshot matrix (basis.py:197-212): ``(phi_s, sigma, v)``
+    with phi_s the leading n_s left singular vectors, by the device thin SVD.
+    The oracle the streaming path is checked against."""
+    from . import linalg
+
+    u = to_dev(u)
+    if n_s < 1:
+        raise BasisError(f"need n_s >= 1, got {n_s}")
+    w, sigma, v = linalg.thin_svd(u)
+    smax = float(sigma[0]) if sigma.numel() else 0.0
+    rank = int((sigma > max(u.shape) * EPS * smax).sum())
+    if n_s > rank:
+        raise BasisError(f"requested {n_s} modes but the snapshots have rank {rank}")
+    return w[:, :n_s], sigma, v
+
+
+def basis_set_from_pod(u, n_s: int, n_t: int, n_steps: int, n_mu: int) -> BasisSet:
+    """Batch-POD twin of :func:`build_basis_set` (basis.py:305-315)."""
+    from . import linalg
+
+    phi_s, _, v = batch_pod(u, n_s)
+    temporal = []
+    for i in range(n_s):
+        w_i, _, _ = linalg.thin_svd(temporal_snapshots(v, i, n_steps, n_mu))
+        temporal.append(w_i[:, :n_t])
+    return BasisSet(phi_s=phi_s, temporal=tuple(temporal), n_mu=n_mu)
