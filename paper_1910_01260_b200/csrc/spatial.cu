@@ -362,6 +362,7 @@ struct EllArgs {
   const double* xref;    // N or null
   int q, MA, NQ, S;
   int dbg;               // diagnostics: 1 = producers skip the gathers, 2 = consumers skip the MMAs
+  int pf_bands;          // Phi L2 prefetch distance past the forward reach, in bands of gridDim.x * 64 rows
   double* part;          // gridDim.x x (MA * NQ)
   unsigned long long* tbuf;  // diagnostics: per-warp phase cycle totals (dbg 5)
 };
@@ -550,7 +551,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_spatial_ell(EllArgs A) {
         }
         if (tp * kWsRows + kWsRows <= A.N)
           for (int e = wid; e < A.ne; e += kWsNPW) prefetch_l2_bulk(A.extra + e * A.ext_ld + tp * kWsRows, kWsRows * 8);
-        const int64_t pr = row0 + A.reach + (int64_t)gridDim.x * kWsRows;
+        const int64_t pr = row0 + A.reach + (int64_t)A.pf_bands * gridDim.x * kWsRows;
         if (A.reach >= 0 && pr + kWsRows <= A.N)
           for (int j = wid; j < A.ns; j += kWsNPW) prefetch_l2_bulk(A.phi + j * A.ld + pr, kWsRows * 8);
       }
@@ -925,9 +926,14 @@ int strom_spatial_reduce_ell(int64_t n, int32_t K, const uint32_t* eidx_dev, con
     a.q = q;
     a.MA = (int)round_up(ns, 8);
     a.NQ = (int)round_up(q, 8);
-    a.S = ell_smem(K, 3, a.MA, a.NQ) <= max_smem_optin() ? 3 : 2;
+    // two stages: a third buys no producer slack (the wait on a free stage is
+    // short) and costs ~64 KB of L1, which the neighbour gathers hit (measured
+    // cfg4 build: 0.59 ms with two stages, 0.65 ms with three)
+    a.S = 2;
     if (const char* e = getenv("STROM_SPATIAL_DBG")) a.dbg = atoi(e);
     if (getenv("STROM_SPATIAL_NOPF")) a.reach = -1;
+    a.pf_bands = 1;
+    if (const char* e = getenv("STROM_SPATIAL_PF")) a.pf_bands = std::max(0, atoi(e));
     if (const char* e = getenv("STROM_SPATIAL_STAGES")) a.S = std::max(1, std::min(a.S, atoi(e)));
     const size_t smem = ell_smem(K, a.S, a.MA, a.NQ);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sm_count(), ceil_div(n, kWsRows)));
