@@ -6,10 +6,11 @@
 //
 // The reference factors I - dt A with SuperLU; at the transport-proxy size
 // (2^20 dofs in 3D) that is infeasible, so each step is
-// solved by Jacobi-preconditioned BiCGSTAB started from x_{k-1}, to a relative
-// residual tol (default 1e-13), over the tiled-ELL operator of the spatial
-// reduction (diagonal kept apart: M = I - dt A has diagonal 1 - dt a_ii and
-// off-diagonals -dt a_ij).
+// solved by BiCGSTAB on the left-Jacobi-preconditioned system D^-1 M x =
+// D^-1 b (M = I - dt A, D = diag M; the scaling is applied row by row inside
+// the SpMV, so no preconditioned copies of the iterates exist), started from
+// x_{k-1}, to a relative preconditioned residual tol (default 1e-13), over the
+// tiled-ELL operator of the spatial reduction (diagonal kept apart).
 //
 // One cooperative persistent kernel marches every step: grid-wide syncs
 // separate the phases; dot products are per-CTA partials summed by every CTA
@@ -46,22 +47,24 @@ struct FomArgs {
   double tol;
   int maxit;
   double* states;        // n x N_t column-major (ld = n)
-  double* w;             // 8 work vectors of n: b, r, rh, p, v, s, t, ph (sh shares ph's slot)
+  double* w;             // 7 work vectors of n: r, rh, p, v, s, t, b
   double* part;          // 2 x 3 x gridDim partial sums
   int* iters;            // N_t iteration counts (-1: not converged)
 };
 
-// y = (I - dt A) z for the rows owned by this thread (grid-stride)
+// Row i of the left-Jacobi-preconditioned step operator D^-1 (I - dt A), D =
+// diag(I - dt A):  y_i = z_i - (dt / d_i) sum_k a_ik z_{c_ik}  (off-diagonal
+// slots only; the scaled diagonal is 1).
 template <int K>
 __device__ __forceinline__ double mrow(const FomArgs& a, int64_t i, double dt, const double* __restrict__ z) {
   const int64_t tile = i / kEllRows;
   const int li = (int)(i % kEllRows);
   const uint32_t* ti = a.eidx + tile * K * kEllRows + li;
   const double* tv = a.eval + tile * (K + 1) * kEllRows + li;
-  double acc = (1.0 - dt * tv[K * kEllRows]) * z[i];
+  double acc = 0.0;
 #pragma unroll
-  for (int k = 0; k < K; ++k) acc = fma(-dt * tv[k * kEllRows], z[ti[k * kEllRows]], acc);
-  return acc;
+  for (int k = 0; k < K; ++k) acc = fma(tv[k * kEllRows], z[ti[k * kEllRows]], acc);
+  return fma(-dt / (1.0 - dt * tv[K * kEllRows]), acc, z[i]);
 }
 
 template <int K>
@@ -109,25 +112,25 @@ __global__ void __launch_bounds__(kFomThreads) k_fom_march(FomArgs a) {
   const int64_t n = a.n;
   const int64_t g0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t gs = (int64_t)gridDim.x * blockDim.x;
-  double* bb = a.w;
-  double* r = a.w + n;
-  double* rh = a.w + 2 * n;
-  double* p = a.w + 3 * n;
-  double* v = a.w + 4 * n;
-  double* s = a.w + 5 * n;
-  double* t = a.w + 6 * n;
-  double* ph = a.w + 7 * n;  // preconditioned direction (p-hat, then s-hat)
+  // BiCGSTAB on the left-preconditioned system D^-1 M x = D^-1 b (M = I - dt A)
+  double* r = a.w;
+  double* rh = a.w + n;
+  double* p = a.w + 2 * n;
+  double* v = a.w + 3 * n;
+  double* s = a.w + 4 * n;
+  double* t = a.w + 5 * n;
+  double* bb = a.w + 6 * n;
   double red[3];
   int nred = 0;
   for (int k = 0; k < a.nt; ++k) {
     const double dt = a.dt[k];
     const double* xp = k == 0 ? a.x0 : a.states + (int64_t)(k - 1) * n;
     double* x = a.states + (int64_t)k * n;
-    // rhs and initial guess x = x_{k-1}
+    // preconditioned rhs D^-1 (x_{k-1} + dt B f_k); initial guess x = x_{k-1}
     for (int64_t i = g0; i < n; i += gs) {
       double bi = xp[i];
       for (int q = 0; q < a.m; ++q) bi = fma(dt * a.b[(int64_t)q * n + i], a.f[(int64_t)k * a.m + q], bi);
-      bb[i] = bi;
+      bb[i] = bi / mdiag<K>(a, i, dt);
       x[i] = xp[i];
     }
     grid.sync();
@@ -141,43 +144,37 @@ __global__ void __launch_bounds__(kFomThreads) k_fom_march(FomArgs a) {
       pb = fma(bb[i], bb[i], pb);
     }
     grid_reduce3(grid, a.part, nred, pr, pb, 0.0, red, sred);
-    double rho = red[0], rr = red[0];
-    const double bnorm2 = red[1];
-    const double stop2 = a.tol * a.tol * bnorm2;
+    double rho = red[0];
+    const double stop2 = a.tol * a.tol * red[1];
     int it = 0;
-    bool ok = rr <= stop2;
+    bool ok = red[0] <= stop2;
     while (!ok && it < a.maxit) {
       ++it;
-      // p-hat = D^-1 p ; v = M p-hat ; (rh, v)
-      for (int64_t i = g0; i < n; i += gs) ph[i] = p[i] / mdiag<K>(a, i, dt);
-      grid.sync();
+      // v = M' p ; (rh, v)
       double prv = 0.0;
       for (int64_t i = g0; i < n; i += gs) {
-        const double vi = mrow<K>(a, i, dt, ph);
+        const double vi = mrow<K>(a, i, dt, p);
         v[i] = vi;
         prv = fma(rh[i], vi, prv);
       }
       grid_reduce3(grid, a.part, nred, prv, 0.0, 0.0, red, sred);
       if (red[0] == 0.0) break;  // breakdown: keep the last iterate
       const double alpha = rho / red[0];
-      // x += alpha p-hat ; s = r - alpha v ; s-hat = D^-1 s (into ph after x is updated)
-      for (int64_t i = g0; i < n; i += gs) {
-        x[i] = fma(alpha, ph[i], x[i]);
-        s[i] = fma(-alpha, v[i], r[i]);
-      }
+      for (int64_t i = g0; i < n; i += gs) s[i] = fma(-alpha, v[i], r[i]);
       grid.sync();
-      for (int64_t i = g0; i < n; i += gs) ph[i] = s[i] / mdiag<K>(a, i, dt);
-      grid.sync();
+      // t = M' s ; (t, s), (t, t), (s, s)
       double pts = 0.0, ptt = 0.0, pss = 0.0;
       for (int64_t i = g0; i < n; i += gs) {
-        const double ti = mrow<K>(a, i, dt, ph);
+        const double ti = mrow<K>(a, i, dt, s);
+        const double si = s[i];
         t[i] = ti;
-        pts = fma(ti, s[i], pts);
+        pts = fma(ti, si, pts);
         ptt = fma(ti, ti, ptt);
-        pss = fma(s[i], s[i], pss);
+        pss = fma(si, si, pss);
       }
       grid_reduce3(grid, a.part, nred, pts, ptt, pss, red, sred);
-      if (red[2] <= stop2) {  // converged on s: x already holds x + alpha p-hat
+      if (red[2] <= stop2) {  // converged on s: x + alpha p
+        for (int64_t i = g0; i < n; i += gs) x[i] = fma(alpha, p[i], x[i]);
         ok = true;
         break;
       }
@@ -185,15 +182,14 @@ __global__ void __launch_bounds__(kFomThreads) k_fom_march(FomArgs a) {
       const double omega = red[0] / red[1];
       double prr = 0.0, prh = 0.0;
       for (int64_t i = g0; i < n; i += gs) {
-        x[i] = fma(omega, ph[i], x[i]);
+        x[i] = fma(omega, s[i], fma(alpha, p[i], x[i]));
         const double ri = fma(-omega, t[i], s[i]);
         r[i] = ri;
         prr = fma(ri, ri, prr);
         prh = fma(rh[i], ri, prh);
       }
       grid_reduce3(grid, a.part, nred, prr, prh, 0.0, red, sred);
-      rr = red[0];
-      if (rr <= stop2) {
+      if (red[0] <= stop2) {
         ok = true;
         break;
       }

@@ -70,7 +70,7 @@ out = {
     "operator_build_s_host": t_op,
     "fom": {"s_per_sample": fom_s, "ms_per_step": float(np.mean(fom_s)) / args.steps * 1e3,
             "bicgstab_iterations_mean": float(np.mean(iters)), "bicgstab_iterations_max": int(np.max(iters)),
-            "solver": "Jacobi-preconditioned BiCGSTAB, relative residual 1e-13, one cooperative kernel per march"},
+            "solver": "BiCGSTAB on the left-Jacobi-preconditioned step system, relative residual 1e-13, one cooperative kernel per march"},
     "isvd": {"snapshots": nsnap, "ingest_ms": ingest_ms, "snapshots_per_s": nsnap / (sum(ingest_ms) / 1e3),
              "rank": st.rank, "counters": {"n_dependent": st.n_dependent, "n_truncated": st.n_truncated},
              "sigma_head": sig[:8].tolist(), "sigma_tail": sig[-3:].tolist()},
