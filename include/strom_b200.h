@@ -207,6 +207,15 @@ int strom_fom_march(int64_t n, int32_t K, const uint32_t* eidx_dev, const double
                     int64_t m, const double* x0_dev, const double* dt_dev, const double* f_dev, int64_t nt, double tol,
                     int32_t maxit, double* states_dev, int32_t* iters_out, void* stream);
 
+/* (A_st)^{-1} v by forward block substitution (system.py:195-213): x_k solves
+ * (I - dt_k A) x_k = x_{k-1} + v_k with x_0 = 0, by the same cooperative
+ * BiCGSTAB march as strom_fom_march; v_dev, out_dev: n x N_t column-major.
+ * The adjoint (system.py:216-233) is this call on the transposed operator's
+ * ELL form with the blocks and steps reversed. */
+int strom_st_apply_inverse(int64_t n, int32_t K, const uint32_t* eidx_dev, const double* eval_dev, const double* dt_dev,
+                           const double* v_dev, int64_t nt, double tol, int32_t maxit, double* out_dev,
+                           int32_t* iters_out, void* stream);
+
 /* Workload generator (bench/test support, not a reference interface): nb
  * columns t0 .. t0+nb-1 of the capacity stream X = Q diag(sigma) W^T + E with
  * an implicit randomized-Hadamard Q (Q[i,c] = s_i (-1)^popcount(i & p_c) /

@@ -61,6 +61,7 @@ _PROTOS = {
     # spatial ROM (spatial.py:45-67)
     "strom_dense_lu": (C.c_int, [i64, vp, vp, vp]),
     "strom_dense_lu_solve": (C.c_int, [i64, vp, vp, vp, i64, vp]),
+    "strom_st_apply_inverse": (C.c_int, [i64, i32, vp, vp, vp, vp, i64, dbl, i32, vp, P_I32, vp]),
     "strom_fom_march": (C.c_int, [i64, i32, vp, vp, vp, i64, vp, vp, vp, i64, dbl, i32, vp, P_I32, vp]),
     "strom_gen_lowrank_batch": (C.c_int, [i64, i32, i32, vp, vp, C.c_uint64, i64, dbl, vp, i64, vp]),
     "strom_csr_to_ell": (C.c_int, [i64, vp, vp, vp, i32, i32, vp, vp, C.POINTER(i64), vp]),

@@ -43,6 +43,7 @@ struct FomArgs {
   const double* x0;
   const double* dt;      // N_t
   const double* f;       // N_t x m row-major (row k = input of step k+1)
+  const double* v;       // or: n x N_t column-major right-hand-side blocks (rhs_k = x_{k-1} + v_k), x0 = 0
   int nt;
   double tol;
   int maxit;
@@ -124,14 +125,17 @@ __global__ void __launch_bounds__(kFomThreads) k_fom_march(FomArgs a) {
   int nred = 0;
   for (int k = 0; k < a.nt; ++k) {
     const double dt = a.dt[k];
-    const double* xp = k == 0 ? a.x0 : a.states + (int64_t)(k - 1) * n;
+    const double* xp = k == 0 ? a.x0 : a.states + (int64_t)(k - 1) * n;  // x0 may be null (zero)
     double* x = a.states + (int64_t)k * n;
     // preconditioned rhs D^-1 (x_{k-1} + dt B f_k); initial guess x = x_{k-1}
     for (int64_t i = g0; i < n; i += gs) {
-      double bi = xp[i];
-      for (int q = 0; q < a.m; ++q) bi = fma(dt * a.b[(int64_t)q * n + i], a.f[(int64_t)k * a.m + q], bi);
+      const double xpi = xp ? xp[i] : 0.0;
+      double bi = xpi;
+      if (a.v) bi += a.v[(int64_t)k * n + i];
+      else
+        for (int q = 0; q < a.m; ++q) bi = fma(dt * a.b[(int64_t)q * n + i], a.f[(int64_t)k * a.m + q], bi);
       bb[i] = bi / mdiag<K>(a, i, dt);
-      x[i] = xp[i];
+      x[i] = xpi;
     }
     grid.sync();
     double pr = 0.0, pb = 0.0;
@@ -215,9 +219,33 @@ extern "C" {
 // (host, N_t ints, may be NULL): BiCGSTAB iterations per step, -1 where the
 // relative residual did not reach tol within maxit (the call then returns a
 // numerical error).
+static int fom_march_impl(int64_t n, int32_t K, const uint32_t* eidx_dev, const double* eval_dev,
+                          const double* b_dev, int64_t m, const double* x0_dev, const double* dt_dev,
+                          const double* f_dev, const double* v_dev, int64_t nt, double tol, int32_t maxit,
+                          double* states_dev, int32_t* iters_out, void* stream);
+
 int strom_fom_march(int64_t n, int32_t K, const uint32_t* eidx_dev, const double* eval_dev, const double* b_dev,
                     int64_t m, const double* x0_dev, const double* dt_dev, const double* f_dev, int64_t nt, double tol,
                     int32_t maxit, double* states_dev, int32_t* iters_out, void* stream) {
+  return fom_march_impl(n, K, eidx_dev, eval_dev, b_dev, m, x0_dev, dt_dev, f_dev, nullptr, nt, tol, maxit, states_dev,
+                        iters_out, stream);
+}
+
+// (A_st)^{-1} v by forward block substitution (system.py:195-213 st_apply_inverse):
+// x_k solves (I - dt_k A) x_k = x_{k-1} + v_k, x_0 = 0; v_dev and out_dev n x N_t
+// column-major.  The adjoint (system.py:216-233) is the same march over the
+// transposed operator's ELL form with the blocks and steps in reverse order.
+int strom_st_apply_inverse(int64_t n, int32_t K, const uint32_t* eidx_dev, const double* eval_dev, const double* dt_dev,
+                           const double* v_dev, int64_t nt, double tol, int32_t maxit, double* out_dev,
+                           int32_t* iters_out, void* stream) {
+  return fom_march_impl(n, K, eidx_dev, eval_dev, nullptr, 0, nullptr, dt_dev, nullptr, v_dev, nt, tol, maxit,
+                        out_dev, iters_out, stream);
+}
+
+static int fom_march_impl(int64_t n, int32_t K, const uint32_t* eidx_dev, const double* eval_dev,
+                          const double* b_dev, int64_t m, const double* x0_dev, const double* dt_dev,
+                          const double* f_dev, const double* v_dev, int64_t nt, double tol, int32_t maxit,
+                          double* states_dev, int32_t* iters_out, void* stream) {
   return guarded([&] {
     STROM_REQUIRE(n >= 1 && nt >= 1 && m >= 0, "bad fom_march shape");
     STROM_REQUIRE(K == 4 || K == 6 || K == 8 || K == 16, "ELL width must be 4, 6, 8 or 16");
@@ -241,6 +269,7 @@ int strom_fom_march(int64_t n, int32_t K, const uint32_t* eidx_dev, const double
     a.x0 = x0_dev;
     a.dt = dt_dev;
     a.f = f_dev;
+    a.v = v_dev;
     a.nt = (int)nt;
     a.tol = tol;
     a.maxit = maxit;

@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import ctypes as C
 
+import numpy as np
 import torch
 
 from . import _capi as capi
@@ -97,3 +98,59 @@ def kron(a, b):
     if not (bool(torch.isfinite(a).all()) and bool(torch.isfinite(b).all())):
         raise ValueError("kron factors must be finite")
     return torch.kron(a, b)
+
+
+class AdjointConsistencyError(Exception):
+    """``apply_adjoint`` is not the transpose of ``apply`` (linalg.py:27-28)."""
+
+
+def largest_singular_value(apply, apply_adjoint, dim_in: int, dim_out: int, tol: float = 1e-8,
+                           max_iter: int = 10_000, seed: int = 0) -> float:
+    """Largest singular value of a linear map by power iteration on A^T A (linalg.py:111-171).
+
+    Same protocol as the reference: three random adjoint-consistency probes,
+    then sweeps until the estimate is stable to ``tol`` twice in a row; the
+    start vectors come from ``numpy.random.default_rng(seed)`` in the
+    reference's draw order, and the applies run on device vectors.
+    """
+    from .errors import ConvergenceError
+
+    rng = np.random.default_rng(seed)
+
+    def dev(x):
+        return torch.as_tensor(x, dtype=F64, device=device())
+
+    for _ in range(3):
+        v = rng.standard_normal(dim_in)
+        w = rng.standard_normal(dim_out)
+        v /= np.linalg.norm(v)
+        w /= np.linalg.norm(w)
+        lhs = float(torch.dot(apply(dev(v)), dev(w)))
+        rhs = float(torch.dot(dev(v), apply_adjoint(dev(w))))
+        if abs(lhs - rhs) > 1e-10 * max(1.0, abs(lhs), abs(rhs)):
+            raise AdjointConsistencyError(f"<Av, w> = {lhs:.16e} but <v, A^T w> = {rhs:.16e}")
+    v = rng.standard_normal(dim_in)
+    v = dev(v / np.linalg.norm(v))
+    sigma, stable, gap = 0.0, 0, np.inf
+    for _ in range(max_iter):
+        t = apply_adjoint(apply(v))
+        lam = float(torch.linalg.norm(t))
+        if lam == 0.0:
+            v = rng.standard_normal(dim_in)
+            v = dev(v / np.linalg.norm(v))
+            t = apply_adjoint(apply(v))
+            lam = float(torch.linalg.norm(t))
+            if lam == 0.0:
+                return 0.0
+        new_sigma = float(np.sqrt(lam))
+        v = t / lam
+        gap = abs(new_sigma - sigma)
+        if gap <= tol * max(new_sigma, np.finfo(float).tiny):
+            stable += 1
+            if stable >= 2:
+                return new_sigma
+        else:
+            stable = 0
+        sigma = new_sigma
+    raise ConvergenceError(f"power iteration failed to converge in {max_iter} iterations "
+                           f"(last estimate {sigma:.6e}, last gap {gap:.3e})")

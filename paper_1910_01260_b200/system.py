@@ -105,42 +105,52 @@ class LinearDynamicalSystem:
         """HBM-resident copies: CSR (indptr, indices, data, index_bits), B|C dense, x0, [B|C|x0]."""
         if self._dev is None:
             dev = device()
-            a = self.a
-            a.sort_indices()
-            big = a.nnz >= 2**31 or a.shape[0] >= 2**31
-            it = np.int64 if big else np.int32
-            self._dev = dict(
-                indptr=torch.as_tensor(a.indptr.astype(it), device=dev),
-                indices=torch.as_tensor(a.indices.astype(it), device=dev),
-                data=torch.as_tensor(a.data.astype(np.float64), device=dev),
-                index_bits=64 if big else 32,
+            self._dev = _csr_device(self.a, dev)
+            self._dev.update(
                 b=torch.as_tensor(self.b.toarray(), dtype=F64, device=dev),
                 c=torch.as_tensor(self.c, dtype=F64, device=dev),
                 x0=torch.as_tensor(self.x0, dtype=F64, device=dev),
             )
-            # tiled-ELL form of A for the spatial reduction's fast path (diagonal
-            # apart, at most 16 off-diagonal entries per row; built once per
-            # operator on the device)
-            rows = np.repeat(np.arange(a.shape[0]), np.diff(a.indptr))
-            offd = np.bincount(rows[a.indices != rows], minlength=a.shape[0]) if a.nnz else np.zeros(1, int)
-            kell = next((k for k in (4, 6, 8, 16) if int(offd.max()) <= k), None)
-            if kell is not None and not big:
-                from . import _capi as capi
-
-                nt = -(-a.shape[0] // 64)
-                eidx = torch.empty(nt * kell * 64, dtype=torch.int32, device=dev)  # uint32 on the device
-                evals = torch.empty(nt * (kell + 1) * 64, dtype=F64, device=dev)
-                reach = capi.i64(0)
-                d = self._dev
-                capi.call("strom_csr_to_ell", a.shape[0], d["indptr"].data_ptr(), d["indices"].data_ptr(),
-                          d["data"].data_ptr(), d["index_bits"], kell, eidx.data_ptr(), evals.data_ptr(),
-                          capi.C.byref(reach), capi.stream_ptr())
-                self._dev["ell"] = dict(k=kell, idx=eidx, val=evals, reach=int(reach.value))
             # [B | C | x0] column-major (rows of a C-contiguous tensor): the dense
             # right-hand columns of the spatial reduction, read in place
             self._dev["bcx0"] = torch.cat([self._dev["b"].T, self._dev["c"].T, self._dev["x0"][None, :]],
                                           dim=0).contiguous()
         return self._dev
+
+    def device_arrays_transposed(self) -> dict:
+        """CSR and tiled-ELL form of A^T (the adjoint marches of the bounds), cached."""
+        if getattr(self, "_dev_t", None) is None:
+            self._dev_t = _csr_device(sp.csr_array(self.a.T), device())
+        return self._dev_t
+
+
+def _csr_device(a, dev) -> dict:
+    """CSR with int32/int64 indices on the device plus, when every row has at most
+    16 off-diagonal entries, the tiled-ELL form (built on the device, diagonal
+    apart) that the spatial reduction and the Krylov marches gather from."""
+    a = sp.csr_array(a)
+    a.sort_indices()
+    big = a.nnz >= 2**31 or a.shape[0] >= 2**31
+    it = np.int64 if big else np.int32
+    d = dict(indptr=torch.as_tensor(a.indptr.astype(it), device=dev),
+             indices=torch.as_tensor(a.indices.astype(it), device=dev),
+             data=torch.as_tensor(a.data.astype(np.float64), device=dev),
+             index_bits=64 if big else 32)
+    rows = np.repeat(np.arange(a.shape[0]), np.diff(a.indptr))
+    offd = np.bincount(rows[a.indices != rows], minlength=a.shape[0]) if a.nnz else np.zeros(1, int)
+    kell = next((k for k in (4, 6, 8, 16) if int(offd.max()) <= k), None)
+    if kell is not None and not big:
+        from . import _capi as capi
+
+        nt = -(-a.shape[0] // 64)
+        eidx = torch.empty(nt * kell * 64, dtype=torch.int32, device=dev)  # uint32 on the device
+        evals = torch.empty(nt * (kell + 1) * 64, dtype=F64, device=dev)
+        reach = capi.i64(0)
+        capi.call("strom_csr_to_ell", a.shape[0], d["indptr"].data_ptr(), d["indices"].data_ptr(),
+                  d["data"].data_ptr(), d["index_bits"], kell, eidx.data_ptr(), evals.data_ptr(),
+                  capi.C.byref(reach), capi.stream_ptr())
+        d["ell"] = dict(k=kell, idx=eidx, val=evals, reach=int(reach.value))
+    return d
 
 
 class FomResult(NamedTuple):
@@ -227,3 +237,144 @@ def fom_march(sys: LinearDynamicalSystem, grid: TimeGrid, tol: float = 1e-13, ma
     st = states.T  # n x N_t, column-major
     outputs = dev["c"].T @ st
     return FomResult(st, outputs, wall, iters)
+
+
+# --------------------------------------------------------------------------
+# matrix-free space-time inverse, residuals (system.py:195-288)
+# --------------------------------------------------------------------------
+
+def _lu_factors(sys: LinearDynamicalSystem, dt: float, transpose: bool, cache: dict):
+    """Device LU of I - dt A (or its transpose), cached per (dt, transpose)."""
+    from . import _capi as capi
+
+    key = (float(dt), transpose)
+    fac = cache.get(key)
+    if fac is None:
+        n = sys.n_states
+        a = cache.get("a")
+        if a is None:
+            a = cache["a"] = torch.as_tensor(sys.a.toarray(), dtype=F64, device=device())
+        m = torch.eye(n, dtype=F64, device=device()) - float(dt) * a
+        lu = (m if transpose else m.T).contiguous()  # column-major copy of M (or of M^T)
+        piv = torch.empty(n, dtype=torch.int32, device=device())
+        capi.call("strom_dense_lu", n, lu.data_ptr(), piv.data_ptr(), capi.stream_ptr())
+        fac = cache[key] = (lu, piv)
+    return fac
+
+
+def _march_blocks(sys: LinearDynamicalSystem, dts, v: torch.Tensor, transpose: bool, cache: dict,
+                  tol: float = 1e-13, maxit: int = 500) -> torch.Tensor:
+    """x_k = M_k^{-1} (x_{k-1} + v_k), x_0 = 0, for blocks v (N_t, n); M_k = I - dt_k A (or ^T)."""
+    from . import _capi as capi
+
+    n, nt = sys.n_states, v.shape[0]
+    dev = sys.device_arrays_transposed() if transpose else sys.device_arrays()
+    ell = dev.get("ell")
+    out = torch.empty((nt, n), dtype=F64, device=device())
+    if ell is None or (n <= DIRECT_MAX_N and cache.get("direct", False)):
+        if n > DIRECT_MAX_N:
+            raise ValueError("the space-time inverse needs at most 16 off-diagonal entries per row of A "
+                             f"or n <= {DIRECT_MAX_N}")
+        x = torch.zeros(n, dtype=F64, device=device())
+        for k in range(nt):
+            lu, piv = _lu_factors(sys, float(dts[k]), transpose, cache)
+            xk = out[k]
+            torch.add(x, v[k], out=xk)
+            capi.call("strom_dense_lu_solve", n, lu.data_ptr(), piv.data_ptr(), xk.data_ptr(), 1,
+                      capi.stream_ptr())
+            x = xk
+        return out
+    dt_dev = torch.as_tensor(np.asarray(dts, dtype=float), dtype=F64, device=device())
+    iters = (capi.C.c_int32 * nt)()
+    capi.call("strom_st_apply_inverse", n, ell["k"], ell["idx"].data_ptr(), ell["val"].data_ptr(),
+              dt_dev.data_ptr(), v.contiguous().data_ptr(), nt, float(tol), int(maxit), out.data_ptr(), iters,
+              capi.stream_ptr())
+    return out
+
+
+def _blocks(sys: LinearDynamicalSystem, grid: TimeGrid, v) -> torch.Tensor:
+    from ._tensors import to_dev
+
+    n, nt = sys.n_states, grid.n_steps
+    v = to_dev(v)
+    if tuple(v.shape) != (n * nt,):
+        raise ValueError(f"expected vector of length {n * nt}, got {tuple(v.shape)}")
+    return v.reshape(nt, n)
+
+
+def st_apply_inverse(sys: LinearDynamicalSystem, grid: TimeGrid, v, cache: dict | None = None) -> torch.Tensor:
+    """(A_st)^{-1} v by forward block substitution (system.py:195-213), on the device."""
+    vb = _blocks(sys, grid, v)
+    return _march_blocks(sys, grid.dt, vb, False, {} if cache is None else cache).reshape(-1)
+
+
+def st_apply_inverse_adjoint(sys: LinearDynamicalSystem, grid: TimeGrid, v,
+                             cache: dict | None = None) -> torch.Tensor:
+    """(A_st)^{-T} v by reverse-time substitution with the transposed steps (system.py:216-233)."""
+    vb = _blocks(sys, grid, v)
+    out = _march_blocks(sys, grid.dt[::-1].copy(), torch.flip(vb, dims=[0]), True,
+                        {} if cache is None else cache)
+    return torch.flip(out, dims=[0]).reshape(-1)
+
+
+def st_inverse_operator(sys: LinearDynamicalSystem, grid: TimeGrid, direct: bool = False):
+    """Matrix-free (A_st)^{-1} and its adjoint sharing cached factors (system.py:236-246).
+
+    ``direct=True`` uses one dense device LU per distinct dt for both (the
+    reference's StepSolver; n <= 4096), otherwise the Krylov march over the
+    tiled-ELL forms of A and A^T (exact to the solver tolerance 1e-13)."""
+    cache = {"direct": bool(direct)}
+
+    def apply(v):
+        return st_apply_inverse(sys, grid, v, cache)
+
+    def apply_adjoint(v):
+        return st_apply_inverse_adjoint(sys, grid, v, cache)
+
+    return apply, apply_adjoint
+
+
+def _spmv(sys: LinearDynamicalSystem, x: torch.Tensor) -> torch.Tensor:
+    d = sys.device_arrays()
+    a = d.get("_sparse")
+    if a is None:
+        n = sys.n_states
+        a = d["_sparse"] = torch.sparse_csr_tensor(d["indptr"].to(torch.int64), d["indices"].to(torch.int64),
+                                                   d["data"], size=(n, n))
+    return (a @ x[:, None])[:, 0] if x.dim() == 1 else a @ x
+
+
+def step_residual(sys: LinearDynamicalSystem, dt: float, x_k, x_prev, f_k) -> torch.Tensor:
+    """x_k - x_prev - dt A x_k - dt B f_k (system.py:249-257)."""
+    from ._tensors import to_dev
+
+    x_k, x_prev = to_dev(x_k), to_dev(x_prev)
+    f = torch.as_tensor(np.atleast_1d(np.asarray(f_k, dtype=float)), dtype=F64, device=device())
+    return x_k - x_prev - dt * _spmv(sys, x_k) - dt * (sys.device_arrays()["b"] @ f)
+
+
+def st_residual(sys: LinearDynamicalSystem, grid: TimeGrid, xst) -> torch.Tensor:
+    """A_st x - f_st - x0_st block-wise without assembly (system.py:260-275)."""
+    xb = _blocks(sys, grid, xst)
+    n, nt = sys.n_states, grid.n_steps
+    prev = torch.cat([sys.device_arrays()["x0"][None, :], xb[:-1]], dim=0)  # x_{k-1} per block
+    ax = _spmv(sys, xb.T.contiguous()).T                                     # A x_k for every k
+    f = torch.as_tensor(np.stack([np.atleast_1d(np.asarray(sys.input_signal(k + 1), dtype=float))
+                                  for k in range(nt)]), dtype=F64, device=device())
+    bf = f @ sys.device_arrays()["b"].T                                        # (N_t, n)
+    dt = grid.dt_device()[:, None]
+    return (xb - prev - dt * ax - dt * bf).reshape(-1)
+
+
+def snapshot_matrix(state_mats) -> torch.Tensor:
+    """Concatenate per-sample state matrices columnwise (system.py:278-288)."""
+    from ._tensors import to_dev
+
+    if not state_mats:
+        raise ValueError("need at least one state matrix")
+    mats = [to_dev(m) for m in state_mats]
+    rows = mats[0].shape[0]
+    for m in mats:
+        if m.dim() != 2 or m.shape[0] != rows:
+            raise ValueError("state matrices must share their row dimension")
+    return torch.cat(mats, dim=1)

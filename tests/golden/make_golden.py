@@ -253,6 +253,46 @@ def gen_persist():
     np.save(os.path.join(HERE, "golden_ref_5x3_values.npy"), m)
 
 
+def gen_bounds():
+    """Space-time inverse applies, residuals and the three a-posteriori bounds
+    (bounds.py, system.py:195-275) on small heat1d / random systems."""
+    from strom import bounds
+
+    out = {}
+    rng = np.random.default_rng(31)
+    sys_ = random_stable_system(rng, 10)
+    grid = system.TimeGrid(rng.uniform(0.02, 0.08, 6))
+    v = rng.standard_normal(60)
+    out["inv_a"] = sys_.a.toarray()
+    out["inv_b"] = sys_.b.toarray()
+    out["inv_dt"] = grid.dt
+    out["inv_v"] = v
+    out["inv_fwd"] = system.st_apply_inverse(sys_, grid, v)
+    out["inv_adj"] = system.st_apply_inverse_adjoint(sys_, grid, v)
+    for tag, nx, dt, nt in (("small", 12, 1e-3, 10), ("large", 300, 2e-6, 6)):
+        heat = make_heat1d(ProblemSpec(kind="heat1d", nx=nx), {"kappa": 1.0})
+        grid = system.TimeGrid.uniform(dt, nt)
+        fom = system.fom_march(heat, grid).states
+        st = basis.isvd_init(fom[:, 0], tol_svd=0.0)
+        st = basis.ingest_simulation(st, fom[:, 1:])
+        bs = basis.build_basis_set(st, 3, 1, nt, 1)
+        srom = spatial.build_spatial_rom(heat, bs, ref_mode="zero")
+        approx = spatial.reconstruct_states(srom, bs, spatial.srom_march(srom, grid, heat.input_signal))
+        rom = spacetime.build_st_rom(srom, bs, grid, heat.input_signal, True)
+        approx_st = spacetime.reconstruct_states(bs, spacetime.solve_st_rom(rom)).T.ravel()
+        out[f"{tag}_approx"] = approx
+        out[f"{tag}_approx_st"] = approx_st
+        out[f"{tag}_st_res"] = system.st_residual(heat, grid, approx_st)
+        for name, rep in (("residual", bounds.residual_error_bound(heat, grid, approx)),
+                          ("rom", bounds.rom_error_bound(heat, grid, approx)),
+                          ("st", bounds.space_time_error_bound(heat, grid, approx_st))):
+            out[f"{tag}_{name}_errors"] = rep.step_errors
+            out[f"{tag}_{name}_bounds"] = rep.step_bounds
+            out[f"{tag}_{name}_constants"] = rep.constants
+            out[f"{tag}_{name}_valid"] = np.array([rep.valid])
+    _save("golden_bounds.npz", **out)
+
+
 if __name__ == "__main__":
     gen_linalg()
     gen_isvd_small()
@@ -260,3 +300,4 @@ if __name__ == "__main__":
     gen_blocks()
     gen_cfg4_small()
     gen_persist()
+    gen_bounds()
