@@ -760,21 +760,30 @@ strom_isvd* update_once(strom_isvd* src, const double* x, cudaStream_t s, bool i
 
 // ------------------------------------------------------------------ ingestion
 // Columns of an ingest call: device pointers, or host columns staged through a
-// ring of device chunks on a copy stream.
+// ring of device chunks on a copy stream.  Chunks grow 1, 2, 4, 8, 16, 16, ...
+// columns, so the first update waits for one column's copy, not a full chunk.
 struct ColumnSource {
   const double* X = nullptr;
   int64_t ldx = 0, n = 0, ncols = 0;
   bool host = false;
   cudaStream_t s = nullptr, cs = nullptr;
-  static constexpr int64_t kChunk = 16;
+  static constexpr int64_t kChunk = 16;  // largest chunk (ring slot capacity, columns)
   static constexpr int kRing = 3;
   std::vector<DevMemPtr> ring;
   std::vector<cudaEvent_t> ready, freed;
+  std::vector<int64_t> start;  // chunk q holds columns [start[q], start[q+1])
   int64_t issued = 0, waited = -1;
 
+  int64_t nchunks() const { return (int64_t)start.size() - 1; }
+  int64_t chunk_of(int64_t t) const {
+    return (int64_t)(std::upper_bound(start.begin(), start.end(), t) - start.begin()) - 1;
+  }
   void open(const double* X_, int64_t ldx_, int64_t n_, int64_t ncols_, bool host_, cudaStream_t s_) {
     X = X_; ldx = ldx_; n = n_; ncols = ncols_; host = host_; s = s_;
     if (!host) return;
+    start.clear();
+    for (int64_t c = 0, w = 1; c < ncols; c += w, w = std::min<int64_t>(2 * w, kChunk)) start.push_back(c);
+    start.push_back(ncols);
     STROM_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
     ring.resize(kRing);
     ready.resize(kRing);
@@ -785,12 +794,11 @@ struct ColumnSource {
       STROM_CUDA(cudaEventCreateWithFlags(&freed[i], cudaEventDisableTiming));
       STROM_CUDA(cudaEventRecord(freed[i], s));
     }
-    const int64_t nchunks = ceil_div(ncols, kChunk);
-    while (issued < std::min<int64_t>(kRing, nchunks)) issue(issued++);
+    while (issued < std::min<int64_t>(kRing, nchunks())) issue(issued++);
   }
   void issue(int64_t q) {
     const int slot = (int)(q % kRing);
-    const int64_t c0 = q * kChunk, cn = std::min(kChunk, ncols - c0);
+    const int64_t c0 = start[q], cn = start[q + 1] - start[q];
     STROM_CUDA(cudaStreamWaitEvent(cs, freed[slot], 0));
     STROM_CUDA(cudaMemcpy2DAsync(ring[slot]->ptr, n * 8, X + c0 * ldx, ldx * 8, n * 8, cn, cudaMemcpyHostToDevice,
                                  cs));
@@ -800,21 +808,20 @@ struct ColumnSource {
   const double* col(int64_t t) {
     if (t < 0 || t >= ncols) return nullptr;
     if (!host) return X + t * ldx;
-    const int64_t q = t / kChunk;
+    const int64_t q = chunk_of(t);
     if (q > waited) {
       for (int64_t w = waited + 1; w <= q; ++w) STROM_CUDA(cudaStreamWaitEvent(s, ready[w % kRing], 0));
       waited = q;
     }
-    return ring[q % kRing]->as<double>() + (t - q * kChunk) * n;
+    return ring[q % kRing]->as<double>() + (t - start[q]) * n;
   }
   // every kernel reading columns <= t has been queued on s
   void release(int64_t t) {
     if (!host) return;
-    if ((t + 1) % kChunk != 0 && t + 1 != ncols) return;
-    const int64_t q = t / kChunk;
+    const int64_t q = chunk_of(t);
+    if (t + 1 != start[q + 1]) return;
     STROM_CUDA(cudaEventRecord(freed[q % kRing], s));
-    const int64_t nchunks = ceil_div(ncols, kChunk);
-    if (issued < nchunks && issued <= q + kRing) issue(issued++);
+    if (issued < nchunks() && issued <= q + kRing) issue(issued++);
   }
   void close() {
     if (!host) return;
