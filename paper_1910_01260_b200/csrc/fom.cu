@@ -14,7 +14,10 @@
 //
 // One cooperative persistent kernel marches every step: grid-wide syncs
 // separate the phases; dot products are per-CTA partials summed by every CTA
-// in CTA order (deterministic, identical on every CTA).
+// in CTA order (deterministic, identical on every CTA).  Systems of up to 8192
+// rows march in one 512-thread CTA instead: a grid barrier costs microseconds,
+// a CTA barrier tens of nanoseconds; up to 2560 rows the vectors (the iterate
+// included) live in shared memory, above that in L1.
 #include <cooperative_groups.h>
 
 #include <cstdint>
@@ -31,6 +34,14 @@ namespace cg = cooperative_groups;
 namespace {
 
 constexpr int kFomThreads = 256;
+constexpr int kFomOneThreads = 512;
+constexpr int64_t kFomOneMax = 8192;   // single-CTA march up to this many rows
+constexpr int64_t kFomSmemMax = 2560;  // ... with its vectors in shared memory (180 KB)
+// BiCGSTAB restarts from the true residual every kFomRestart iterations: near
+// a 1e-13 relative residual the shadow residual loses its grip ((r^, r) at
+// rounding level) and the recursion can wander for hundreds of iterations
+// (the cfg1 test system shows it at step 92); a fresh start converges in a few.
+constexpr int kFomRestart = 100;
 constexpr int kEllRows = 64;  // tile height of the ELL layout (spatial.cu)
 
 struct FomArgs {
@@ -56,8 +67,11 @@ struct FomArgs {
 // Row i of the left-Jacobi-preconditioned step operator D^-1 (I - dt A), D =
 // diag(I - dt A):  y_i = z_i - (dt / d_i) sum_k a_ik z_{c_ik}  (off-diagonal
 // slots only; the scaled diagonal is 1).
-template <int K>
-__device__ __forceinline__ double mrow(const FomArgs& a, int64_t i, double dt, const double* __restrict__ z) {
+// ONE passes the precomputed row scale sc = -dt / d_i (one fp64 division per
+// row and step instead of per SpMV); the HBM-bound grid mode recomputes it.
+template <int K, bool ONE>
+__device__ __forceinline__ double mrow(const FomArgs& a, int64_t i, double dt, const double* __restrict__ z,
+                                       const double* __restrict__ sc) {
   const int64_t tile = i / kEllRows;
   const int li = (int)(i % kEllRows);
   const uint32_t* ti = a.eidx + tile * K * kEllRows + li;
@@ -65,7 +79,8 @@ __device__ __forceinline__ double mrow(const FomArgs& a, int64_t i, double dt, c
   double acc = 0.0;
 #pragma unroll
   for (int k = 0; k < K; ++k) acc = fma(tv[k * kEllRows], z[ti[k * kEllRows]], acc);
-  return fma(-dt / (1.0 - dt * tv[K * kEllRows]), acc, z[i]);
+  if constexpr (ONE) return fma(sc[i], acc, z[i]);
+  else return fma(-dt / (1.0 - dt * tv[K * kEllRows]), acc, z[i]);
 }
 
 template <int K>
@@ -73,60 +88,89 @@ __device__ __forceinline__ double mdiag(const FomArgs& a, int64_t i, double dt) 
   return 1.0 - dt * a.eval[(i / kEllRows) * (K + 1) * kEllRows + K * kEllRows + i % kEllRows];
 }
 
-// deterministic grid reduction of up to 3 values: every CTA returns the same
-// sums.  Consecutive reductions alternate between two partial buffers, so a
-// CTA writing reduction R+1 never races a CTA still reading reduction R.
-__device__ __forceinline__ void grid_reduce3(cg::grid_group& grid, double* part_base, int& nred, double v0,
-                                             double v1, double v2, double* out, double* sred) {
-  double* part = part_base + (int64_t)(nred++ & 1) * 3 * gridDim.x;
+// deterministic reduction of NV <= 3 values: every CTA returns the same sums.
+// Grid mode: per-CTA partials summed by every CTA in CTA order; consecutive
+// reductions alternate between two partial buffers, so a CTA writing
+// reduction R+1 never races a CTA still reading reduction R.  Single-CTA mode
+// (small n): warp partials summed in warp order, no grid barrier.
+template <bool ONE, int NT, int NV>
+__device__ __forceinline__ void reduce3(cg::grid_group& grid, double* part_base, int& nred, double v0, double v1,
+                                        double v2, double* out, double* sred) {
+  constexpr int NW = NT / 32;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   double vv[3] = {v0, v1, v2};
 #pragma unroll
-  for (int q = 0; q < 3; ++q) {
+  for (int q = 0; q < NV; ++q) {
     double s = warp_sum(vv[q]);
-    if (lane == 0) sred[q * 8 + w] = s;
+    if (lane == 0) sred[q * NW + w] = s;
   }
   __syncthreads();
-  if (threadIdx.x < 3) {
-    double s = 0.0;
-    for (int k = 0; k < kFomThreads / 32; ++k) s += sred[threadIdx.x * 8 + k];
-    part[(int64_t)threadIdx.x * gridDim.x + blockIdx.x] = s;
-  }
-  grid.sync();
-  if (w < 3) {
-    double s = 0.0;
-    for (int c = lane; c < (int)gridDim.x; c += 32) s += part[(int64_t)w * gridDim.x + c];
-    s = warp_sum(s);  // fixed shuffle tree: the same on every CTA
-    if (lane == 0) sred[24 + w] = s;
+  if constexpr (ONE) {
+    static_assert(NW <= 32, "single-CTA mode reduces one partial per lane");
+    if (w < NV) {
+      const double s = warp_sum(lane < NW ? sred[w * NW + lane] : 0.0);  // fixed shuffle tree
+      if (lane == 0) sred[3 * NW + w] = s;
+    }
+  } else {
+    double* part = part_base + (int64_t)(nred++ & 1) * 3 * gridDim.x;
+    if (threadIdx.x < NV) {
+      double s = 0.0;
+      for (int k = 0; k < NW; ++k) s += sred[threadIdx.x * NW + k];
+      part[(int64_t)threadIdx.x * gridDim.x + blockIdx.x] = s;
+    }
+    grid.sync();
+    if (w < NV) {
+      double s = 0.0;
+      for (int c = lane; c < (int)gridDim.x; c += 32) s += part[(int64_t)w * gridDim.x + c];
+      s = warp_sum(s);  // fixed shuffle tree: the same on every CTA
+      if (lane == 0) sred[3 * NW + w] = s;
+    }
   }
   __syncthreads();
-  out[0] = sred[24];
-  out[1] = sred[25];
-  out[2] = sred[26];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) out[q] = sred[3 * NW + q];
   __syncthreads();
 }
 
-template <int K>
-__global__ void __launch_bounds__(kFomThreads) k_fom_march(FomArgs a) {
+template <bool ONE>
+__device__ __forceinline__ void sync_all(cg::grid_group& grid) {
+  if constexpr (ONE) __syncthreads();
+  else grid.sync();
+}
+
+// ONE: a single 512-thread CTA marches a small system (n <= kFomOneMax); the
+// vectors stay in L1 and every barrier is a CTA barrier.  Otherwise one
+// cooperative grid of kFomThreads-thread CTAs.
+// SMEM (single-CTA only, n <= kFomSmemMax): the eight vectors, x included,
+// live in shared memory; x is copied out to the states column after each step.
+template <int K, bool ONE, bool SMEM>
+__global__ void __launch_bounds__(ONE ? kFomOneThreads : kFomThreads) k_fom_march(FomArgs a) {
+  constexpr int NT = ONE ? kFomOneThreads : kFomThreads;
+  static_assert(ONE || !SMEM, "shared-memory vectors need the single-CTA mode");
   cg::grid_group grid = cg::this_grid();
-  __shared__ double sred[32];
+  __shared__ double sred[3 * (NT / 32) + 3];
+  extern __shared__ double svec[];
   const int64_t n = a.n;
   const int64_t g0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t gs = (int64_t)gridDim.x * blockDim.x;
   // BiCGSTAB on the left-preconditioned system D^-1 M x = D^-1 b (M = I - dt A)
-  double* r = a.w;
-  double* rh = a.w + n;
-  double* p = a.w + 2 * n;
-  double* v = a.w + 3 * n;
-  double* s = a.w + 4 * n;
-  double* t = a.w + 5 * n;
-  double* bb = a.w + 6 * n;
+  double* wv = SMEM ? svec : a.w;
+  double* r = wv;
+  double* rh = wv + n;
+  double* p = wv + 2 * n;
+  double* v = wv + 3 * n;
+  double* s = wv + 4 * n;
+  double* t = wv + 5 * n;
+  double* bb = wv + 6 * n;
+  double* xs = wv + 7 * n;  // SMEM: the iterate
+  double* sc = wv + 8 * n;  // ONE: row scales -dt / d_i of the current step
   double red[3];
   int nred = 0;
   for (int k = 0; k < a.nt; ++k) {
     const double dt = a.dt[k];
-    const double* xp = k == 0 ? a.x0 : a.states + (int64_t)(k - 1) * n;  // x0 may be null (zero)
-    double* x = a.states + (int64_t)k * n;
+    // x0 may be null (zero); SMEM marches x in place from x_{k-1}
+    const double* xp = k == 0 ? a.x0 : SMEM ? xs : a.states + (int64_t)(k - 1) * n;
+    double* x = SMEM ? xs : a.states + (int64_t)k * n;
     // preconditioned rhs D^-1 (x_{k-1} + dt B f_k); initial guess x = x_{k-1}
     for (int64_t i = g0; i < n; i += gs) {
       const double xpi = xp ? xp[i] : 0.0;
@@ -134,55 +178,72 @@ __global__ void __launch_bounds__(kFomThreads) k_fom_march(FomArgs a) {
       if (a.v) bi += a.v[(int64_t)k * n + i];
       else
         for (int q = 0; q < a.m; ++q) bi = fma(dt * a.b[(int64_t)q * n + i], a.f[(int64_t)k * a.m + q], bi);
-      bb[i] = bi / mdiag<K>(a, i, dt);
+      const double di = mdiag<K>(a, i, dt);
+      bb[i] = bi / di;
+      if constexpr (ONE) sc[i] = -dt / di;
       x[i] = xpi;
     }
-    grid.sync();
-    double pr = 0.0, pb = 0.0;
-    for (int64_t i = g0; i < n; i += gs) {
-      const double ri = bb[i] - mrow<K>(a, i, dt, x);
-      r[i] = ri;
-      rh[i] = ri;
-      p[i] = ri;
-      pr = fma(ri, ri, pr);
-      pb = fma(bb[i], bb[i], pb);
-    }
-    grid_reduce3(grid, a.part, nred, pr, pb, 0.0, red, sred);
-    double rho = red[0];
-    const double stop2 = a.tol * a.tol * red[1];
+    sync_all<ONE>(grid);
+    double rho = 0.0, stop2 = 0.0;
     int it = 0;
-    bool ok = red[0] <= stop2;
-    while (!ok && it < a.maxit) {
+    bool ok = false, fresh = true;
+    for (;;) {
+      if (fresh) {
+        // (re)start from the true residual of the current iterate; restarts
+        // recover from breakdowns and from the stagnation BiCGSTAB shows once
+        // the recursive residual nears rounding level (see kFomRestart)
+        fresh = false;
+        double pr = 0.0, pb = 0.0;
+        for (int64_t i = g0; i < n; i += gs) {
+          const double ri = bb[i] - mrow<K, ONE>(a, i, dt, x, sc);
+          r[i] = ri;
+          rh[i] = ri;
+          p[i] = ri;
+          pr = fma(ri, ri, pr);
+          pb = fma(bb[i], bb[i], pb);
+        }
+        reduce3<ONE, NT, 2>(grid, a.part, nred, pr, pb, 0.0, red, sred);
+        rho = red[0];
+        stop2 = a.tol * a.tol * red[1];
+        if (red[0] <= stop2) {
+          ok = true;
+          break;
+        }
+      }
+      if (it >= a.maxit) break;
       ++it;
       // v = M' p ; (rh, v)
       double prv = 0.0;
       for (int64_t i = g0; i < n; i += gs) {
-        const double vi = mrow<K>(a, i, dt, p);
+        const double vi = mrow<K, ONE>(a, i, dt, p, sc);
         v[i] = vi;
         prv = fma(rh[i], vi, prv);
       }
-      grid_reduce3(grid, a.part, nred, prv, 0.0, 0.0, red, sred);
-      if (red[0] == 0.0) break;  // breakdown: keep the last iterate
+      reduce3<ONE, NT, 1>(grid, a.part, nred, prv, 0.0, 0.0, red, sred);
+      if (red[0] == 0.0) {  // breakdown
+        fresh = true;
+        continue;
+      }
       const double alpha = rho / red[0];
       for (int64_t i = g0; i < n; i += gs) s[i] = fma(-alpha, v[i], r[i]);
-      grid.sync();
+      sync_all<ONE>(grid);
       // t = M' s ; (t, s), (t, t), (s, s)
       double pts = 0.0, ptt = 0.0, pss = 0.0;
       for (int64_t i = g0; i < n; i += gs) {
-        const double ti = mrow<K>(a, i, dt, s);
+        const double ti = mrow<K, ONE>(a, i, dt, s, sc);
         const double si = s[i];
         t[i] = ti;
         pts = fma(ti, si, pts);
         ptt = fma(ti, ti, ptt);
         pss = fma(si, si, pss);
       }
-      grid_reduce3(grid, a.part, nred, pts, ptt, pss, red, sred);
+      reduce3<ONE, NT, 3>(grid, a.part, nred, pts, ptt, pss, red, sred);
       if (red[2] <= stop2) {  // converged on s: x + alpha p
         for (int64_t i = g0; i < n; i += gs) x[i] = fma(alpha, p[i], x[i]);
         ok = true;
         break;
       }
-      if (red[1] == 0.0) break;
+      if (red[1] == 0.0) break;  // t = M s = 0 with s != 0: M is singular
       const double omega = red[0] / red[1];
       double prr = 0.0, prh = 0.0;
       for (int64_t i = g0; i < n; i += gs) {
@@ -192,19 +253,24 @@ __global__ void __launch_bounds__(kFomThreads) k_fom_march(FomArgs a) {
         prr = fma(ri, ri, prr);
         prh = fma(rh[i], ri, prh);
       }
-      grid_reduce3(grid, a.part, nred, prr, prh, 0.0, red, sred);
+      reduce3<ONE, NT, 2>(grid, a.part, nred, prr, prh, 0.0, red, sred);
       if (red[0] <= stop2) {
         ok = true;
         break;
       }
-      if (omega == 0.0 || rho == 0.0) break;
+      if (omega == 0.0 || red[1] == 0.0 || it % kFomRestart == 0) {
+        fresh = true;
+        continue;
+      }
       const double beta = (red[1] / rho) * (alpha / omega);
       rho = red[1];
       for (int64_t i = g0; i < n; i += gs) p[i] = r[i] + beta * fma(-omega, v[i], p[i]);
-      grid.sync();
+      sync_all<ONE>(grid);
     }
+    if constexpr (SMEM)
+      for (int64_t i = g0; i < n; i += gs) a.states[(int64_t)k * n + i] = x[i];
     if (blockIdx.x == 0 && threadIdx.x == 0) a.iters[k] = ok ? it : -1;
-    grid.sync();
+    sync_all<ONE>(grid);
   }
 }
 
@@ -250,13 +316,20 @@ static int fom_march_impl(int64_t n, int32_t K, const uint32_t* eidx_dev, const 
     STROM_REQUIRE(n >= 1 && nt >= 1 && m >= 0, "bad fom_march shape");
     STROM_REQUIRE(K == 4 || K == 6 || K == 8 || K == 16, "ELL width must be 4, 6, 8 or 16");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    auto kern = K == 4 ? k_fom_march<4> : K == 6 ? k_fom_march<6> : K == 8 ? k_fom_march<8> : k_fom_march<16>;
+    const bool one = n <= kFomOneMax, smem = n <= kFomSmemMax;
+#define STROM_FOM_K(O, S) (K == 4 ? k_fom_march<4, O, S> : K == 6 ? k_fom_march<6, O, S> \
+                           : K == 8 ? k_fom_march<8, O, S> : k_fom_march<16, O, S>)
+    auto kern = smem ? STROM_FOM_K(true, true) : one ? STROM_FOM_K(true, false) : STROM_FOM_K(false, false);
+#undef STROM_FOM_K
+    const int threads = one ? kFomOneThreads : kFomThreads;
+    const size_t dsmem = smem ? (size_t)9 * n * sizeof(double) : 0;
+    if (smem) STROM_CUDA(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem));
     int occ = 0;
-    STROM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kFomThreads, 0));
+    STROM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, dsmem));
     STROM_REQUIRE(occ >= 1, "fom_march kernel cannot be resident");
     const int64_t want = ceil_div(n, kFomThreads);
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count() * std::min(occ, 4)));
-    auto work = dev_alloc((size_t)8 * n * 8, s, false);
+    const int grid = one ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sm_count() * std::min(occ, 4)));
+    auto work = dev_alloc((size_t)9 * n * 8, s, false);
     auto part = dev_alloc((size_t)6 * grid * 8, s, true);
     auto its = dev_alloc((size_t)nt * 4, s, true);
     FomArgs a{};
@@ -278,7 +351,7 @@ static int fom_march_impl(int64_t n, int32_t K, const uint32_t* eidx_dev, const 
     a.part = part->as<double>();
     a.iters = its->as<int>();
     void* args[] = {&a};
-    STROM_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kFomThreads), args, 0, s));
+    STROM_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(threads), args, dsmem, s));
     STROM_LAUNCH_CHECK();
     std::vector<int> h((size_t)nt);
     STROM_CUDA(cudaMemcpyAsync(h.data(), its->ptr, (size_t)nt * 4, cudaMemcpyDeviceToHost, s));
