@@ -209,8 +209,8 @@ Caps make_caps(int64_t n, int32_t r_max, int32_t want_r, int64_t k) {
   c.ccap = std::min<int32_t>(256, c.rcap + 1 + slack_for(c.rcap));
   // capacity: a compaction holds two stores at once; keep both within ~80% of
   // HBM by trimming the slack (cfg5: 2^26 rows, 0.54 GB per column)
-  size_t free_b = 0, total_b = 0;
-  if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && total_b > 0) {
+  const size_t total_b = device_total_mem();
+  if (total_b > 0) {
     const int64_t col_bytes = round_up(n, 128) * 8;
     const int64_t max_cols = (int64_t)(0.40 * (double)total_b) / col_bytes;
     if (c.ccap > max_cols) c.ccap = (int32_t)std::max<int64_t>(c.rcap + 1 + 8, max_cols);
@@ -767,8 +767,14 @@ struct ColumnSource {
   int64_t ldx = 0, n = 0, ncols = 0;
   bool host = false;
   cudaStream_t s = nullptr, cs = nullptr;
-  static constexpr int64_t kChunk = 16;  // largest chunk (ring slot capacity, columns)
-  static constexpr int kRing = 3;
+  // largest chunk (ring slot capacity, columns) and ring depth; STROM_H2D_CHUNK /
+  // STROM_H2D_RING override them for measurements
+  const int64_t kChunk = env_int("STROM_H2D_CHUNK", 16);
+  const int kRing = (int)env_int("STROM_H2D_RING", 3);
+  static int64_t env_int(const char* name, int64_t dflt) {
+    const char* e = getenv(name);
+    return e && atoll(e) > 0 ? atoll(e) : dflt;
+  }
   std::vector<DevMemPtr> ring;
   std::vector<cudaEvent_t> ready, freed;
   std::vector<int64_t> start;  // chunk q holds columns [start[q], start[q+1])
@@ -784,14 +790,14 @@ struct ColumnSource {
     start.clear();
     for (int64_t c = 0, w = 1; c < ncols; c += w, w = std::min<int64_t>(2 * w, kChunk)) start.push_back(c);
     start.push_back(ncols);
-    STROM_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    cs = acquire_stream();
     ring.resize(kRing);
     ready.resize(kRing);
     freed.resize(kRing);
     for (int i = 0; i < kRing; ++i) {
       ring[i] = dev_alloc((size_t)n * kChunk * 8, s, false);
-      STROM_CUDA(cudaEventCreateWithFlags(&ready[i], cudaEventDisableTiming));
-      STROM_CUDA(cudaEventCreateWithFlags(&freed[i], cudaEventDisableTiming));
+      ready[i] = acquire_event();
+      freed[i] = acquire_event();
       STROM_CUDA(cudaEventRecord(freed[i], s));
     }
     while (issued < std::min<int64_t>(kRing, nchunks())) issue(issued++);
@@ -827,10 +833,10 @@ struct ColumnSource {
     if (!host) return;
     STROM_CUDA(cudaStreamSynchronize(cs));
     for (int i = 0; i < kRing; ++i) {
-      cudaEventDestroy(ready[i]);
-      cudaEventDestroy(freed[i]);
+      release_event(ready[i]);
+      release_event(freed[i]);
     }
-    cudaStreamDestroy(cs);
+    release_stream(cs);
     cs = nullptr;
   }
 };
@@ -845,13 +851,13 @@ strom_isvd* ingest_pipelined(strom_isvd* src, ColumnSource& cols, cudaStream_t s
     return e ? atoi(e) : 0;
   }();
   cudaStream_t s2;
-  STROM_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+  s2 = acquire_stream();
   cudaStream_t s2_created = s2;
   if (dbg & 1) s2 = s;  // diagnostics: one stream
   cudaEvent_t evD, evB, evV;
-  STROM_CUDA(cudaEventCreateWithFlags(&evD, cudaEventDisableTiming));
-  STROM_CUDA(cudaEventCreateWithFlags(&evB, cudaEventDisableTiming));
-  STROM_CUDA(cudaEventCreateWithFlags(&evV, cudaEventDisableTiming));
+  evD = acquire_event();
+  evB = acquire_event();
+  evV = acquire_event();
   // s2 starts after everything queued on s so far
   STROM_CUDA(cudaEventRecord(evV, s));
   STROM_CUDA(cudaStreamWaitEvent(s2, evV, 0));
@@ -992,10 +998,10 @@ strom_isvd* ingest_pipelined(strom_isvd* src, ColumnSource& cols, cudaStream_t s
   // the result owns its block; the other ping-pong block dies here (stream-ordered free)
   strom_isvd* out = slot[(ncols - 1) & 1].release();
   STROM_CUDA(cudaStreamSynchronize(s2));
-  cudaEventDestroy(evD);
-  cudaEventDestroy(evB);
-  cudaEventDestroy(evV);
-  cudaStreamDestroy(s2_created);
+  release_event(evD);
+  release_event(evB);
+  release_event(evV);
+  release_stream(s2_created);
   return out;
 }
 

@@ -53,6 +53,69 @@ int sm_count() {
   return n;
 }
 
+size_t device_total_mem() {
+  static size_t n = [] {
+    size_t f = 0, t = 0;
+    return cudaMemGetInfo(&f, &t) == cudaSuccess ? t : (size_t)0;
+  }();
+  return n;
+}
+
+namespace {
+std::mutex g_res_mu;
+std::vector<std::pair<int, cudaStream_t>> g_streams;
+std::vector<std::pair<int, cudaEvent_t>> g_events;
+int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+}  // namespace
+
+cudaStream_t acquire_stream() {
+  const int d = current_device();
+  {
+    std::lock_guard<std::mutex> g(g_res_mu);
+    for (size_t i = 0; i < g_streams.size(); ++i)
+      if (g_streams[i].first == d) {
+        cudaStream_t s = g_streams[i].second;
+        g_streams.erase(g_streams.begin() + (std::ptrdiff_t)i);
+        return s;
+      }
+  }
+  cudaStream_t s;
+  STROM_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  return s;
+}
+
+void release_stream(cudaStream_t s) {
+  if (!s) return;
+  std::lock_guard<std::mutex> g(g_res_mu);
+  g_streams.emplace_back(current_device(), s);
+}
+
+cudaEvent_t acquire_event() {
+  const int d = current_device();
+  {
+    std::lock_guard<std::mutex> g(g_res_mu);
+    for (size_t i = 0; i < g_events.size(); ++i)
+      if (g_events[i].first == d) {
+        cudaEvent_t e = g_events[i].second;
+        g_events.erase(g_events.begin() + (std::ptrdiff_t)i);
+        return e;
+      }
+  }
+  cudaEvent_t e;
+  STROM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return e;
+}
+
+void release_event(cudaEvent_t e) {
+  if (!e) return;
+  std::lock_guard<std::mutex> g(g_res_mu);
+  g_events.emplace_back(current_device(), e);
+}
+
 size_t max_smem_optin() {
   static size_t n = [] {
     int dev = 0, v = 48 * 1024;

@@ -70,6 +70,16 @@ DevMemPtr dev_alloc(size_t bytes, cudaStream_t s, bool zero = false);
 
 int sm_count();
 size_t max_smem_optin();
+size_t device_total_mem();  // HBM bytes of the current device (queried once)
+
+// Non-blocking streams and timing-free events recycled across calls: creating
+// and destroying them per ingest call is a driver round trip each, and those
+// occasionally stall for hundreds of milliseconds.  A recycled stream may
+// still hold work of an earlier call; new work queues behind it.
+cudaStream_t acquire_stream();
+void release_stream(cudaStream_t s);
+cudaEvent_t acquire_event();
+void release_event(cudaEvent_t e);
 
 // Wrap a C-ABI body: map exceptions to status codes + thread-local message.
 template <class F>
