@@ -760,8 +760,8 @@ strom_isvd* update_once(strom_isvd* src, const double* x, cudaStream_t s, bool i
 
 // ------------------------------------------------------------------ ingestion
 // Columns of an ingest call: device pointers, or host columns staged through a
-// ring of device chunks on a copy stream.  Chunks grow 1, 2, 4, 8, 16, 16, ...
-// columns, so the first update waits for one column's copy, not a full chunk.
+// ring of device chunks on a copy stream.  Chunks grow 1, 2, 4, 4, ... columns,
+// so the first update waits for one column's copy, not a full chunk.
 struct ColumnSource {
   const double* X = nullptr;
   int64_t ldx = 0, n = 0, ncols = 0;
@@ -769,8 +769,10 @@ struct ColumnSource {
   cudaStream_t s = nullptr, cs = nullptr;
   // largest chunk (ring slot capacity, columns) and ring depth; STROM_H2D_CHUNK /
   // STROM_H2D_RING override them for measurements
-  const int64_t kChunk = env_int("STROM_H2D_CHUNK", 16);
-  const int kRing = (int)env_int("STROM_H2D_RING", 3);
+  // (cfg2 e2e, steady state: 4 x 4 columns 79.1 ms per 400 snapshots, 3 x 16
+  // 80.3 ms; the device-resident path 76.5 ms)
+  const int64_t kChunk = env_int("STROM_H2D_CHUNK", 4);
+  const int kRing = (int)env_int("STROM_H2D_RING", 4);
   static int64_t env_int(const char* name, int64_t dflt) {
     const char* e = getenv(name);
     return e && atoll(e) > 0 ? atoll(e) : dflt;
