@@ -25,6 +25,30 @@ namespace {
 constexpr int kNb = 32;
 constexpr int kNbReg = 16;  // panel width of the register-resident panel factorisation
 
+// Programmatic dependent launch along the factorisation chain (panel ->
+// swap/TRSM -> update -> next panel): each kernel lets its successor launch
+// at once and waits for its predecessor before touching A, so the launch
+// latency hides behind the running kernel.
+__device__ __forceinline__ void lu_pdl_enter() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+template <class... KArgs, class... Args>
+void lu_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  STROM_CUDA(cudaLaunchKernelEx(&cfg, kernel, args...));
+}
+
 __global__ void k_fro_norm(const double* A, int64_t ld, int64_t n, double* out) {
   __shared__ double red[32];
   double s = 0.0;
@@ -124,6 +148,7 @@ __global__ void k_lu_trsm(double* A, int64_t ld, int n, int k0, int nb) {
 
 // A22 -= L21 U12 ; tiles of 64 x 64, 256 threads, 4 x 4 per thread.
 __global__ void __launch_bounds__(256) k_lu_gemm(double* A, int64_t ld, int n, int k0, int nb) {
+  lu_pdl_enter();
   __shared__ double Ls[64][kNb + 1];
   __shared__ double Us[kNb][64 + 1];
   const int s0 = k0 + nb;
@@ -209,14 +234,18 @@ __global__ void __launch_bounds__(1024) k_lu_solve(const double* A, int64_t ld, 
 // k0 + t + 512 q (q < RPT) of the nb <= kNbReg panel columns.  Per column: an
 // argmax reduction (largest |a|, lowest row on ties, like idamax), the pivot
 // row exchanged through shared memory, then scale and rank-1 update in
-// registers.  Row interchanges are applied to the panel only; k_lu_laswp
+// registers.  Row interchanges are applied to the panel only; k_lu_swap_trsm
 // applies them to the other columns afterwards (LAPACK's getrf order).
 template <int RPT>
 __global__ void __launch_bounds__(512, 1) k_lu_panel_reg(double* A, int64_t ld, int n, int k0, int nb, int* piv) {
-  __shared__ double srow[2][kNbReg];  // [0]: pivot row, [1]: the displaced row k0 + j
-  __shared__ double sv[16];
-  __shared__ int si[16];
-  __shared__ int s_p;
+  lu_pdl_enter();
+  // per column, double-buffered by column parity: each warp's pivot candidate
+  // (value, row, the row's panel entries) and the row the pivot displaces.  One
+  // barrier per column: every warp reduces the 16 candidates itself.
+  __shared__ double cand[2][16][kNbReg];
+  __shared__ double cval[2][16];
+  __shared__ int cidx[2][16];
+  __shared__ double drow[2][kNbReg];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double a[RPT][kNbReg];
 #pragma unroll
@@ -227,7 +256,7 @@ __global__ void __launch_bounds__(512, 1) k_lu_panel_reg(double* A, int64_t ld, 
   }
 #pragma unroll 1
   for (int j = 0; j < nb; ++j) {
-    const int jr = k0 + j;
+    const int jr = k0 + j, buf = j & 1;
     double best = -1.0;
     int bi = 0x7fffffff;
 #pragma unroll
@@ -248,47 +277,47 @@ __global__ void __launch_bounds__(512, 1) k_lu_panel_reg(double* A, int64_t ld, 
       const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
       if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
     }
-    if (lane == 0) { sv[wid] = best; si[wid] = bi; }
-    __syncthreads();
-    if (wid == 0) {
-      best = lane < 16 ? sv[lane] : -1.0;
-      bi = lane < 16 ? si[lane] : 0x7fffffff;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-      }
-      if (lane == 0) {
-        s_p = (bi == 0x7fffffff) ? jr : bi;
-        piv[jr] = s_p;
-      }
-    }
-    __syncthreads();
-    const int p = s_p;
-    // owners publish the pivot row and the row it displaces
+    // the owner of the warp's candidate row and of row jr publish them
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
       const int i = k0 + threadIdx.x + 512 * q;
-      if (i == p)
+      if (i == bi)
 #pragma unroll
-        for (int c = 0; c < kNbReg; ++c) srow[0][c] = a[q][c];
-      if (i == jr && p != jr)
+        for (int c = 0; c < kNbReg; ++c) cand[buf][wid][c] = a[q][c];
+      if (i == jr)
 #pragma unroll
-        for (int c = 0; c < kNbReg; ++c) srow[1][c] = a[q][c];
+        for (int c = 0; c < kNbReg; ++c) drow[buf][c] = a[q][c];
+    }
+    if (lane == 0) {
+      cval[buf][wid] = best;
+      cidx[buf][wid] = bi;
     }
     __syncthreads();
-    const double d = srow[0][j];
+    // every warp: argmax over the 16 warp candidates (same rule), carrying the warp
+    double gb = lane < 16 ? cval[buf][lane] : -1.0;
+    int gi = lane < 16 ? cidx[buf][lane] : 0x7fffffff;
+    int gw = lane;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, gb, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, gi, o);
+      const int ow = __shfl_xor_sync(0xffffffffu, gw, o);
+      if (ob > gb || (ob == gb && oi < gi)) { gb = ob; gi = oi; gw = ow; }
+    }
+    const int p = gi;  // a candidate always exists: row jr itself
+    if (threadIdx.x == 0) piv[jr] = p;
+    const double* prow = cand[buf][gw];
+    const double d = prow[j];
     const double inv = d != 0.0 ? 1.0 / d : 0.0;
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
       const int i = k0 + threadIdx.x + 512 * q;
       if (i == jr && p != jr) {
 #pragma unroll
-        for (int c = 0; c < kNbReg; ++c) a[q][c] = srow[0][c];
+        for (int c = 0; c < kNbReg; ++c) a[q][c] = prow[c];
       } else if (i == p && p != jr) {
 #pragma unroll
-        for (int c = 0; c < kNbReg; ++c) a[q][c] = srow[1][c];
+        for (int c = 0; c < kNbReg; ++c) a[q][c] = drow[buf][c];
       }
       if (i > jr && i < n && d != 0.0) {
         double l = 0.0;
@@ -297,10 +326,12 @@ __global__ void __launch_bounds__(512, 1) k_lu_panel_reg(double* A, int64_t ld, 
           if (c == j) { l = a[q][c] * inv; a[q][c] = l; }
 #pragma unroll
         for (int c = 0; c < kNbReg; ++c)
-          if (c > j) a[q][c] = fma(-l, srow[0][c], a[q][c]);
+          if (c > j) a[q][c] = fma(-l, prow[c], a[q][c]);
       }
     }
-    __syncthreads();  // srow is rewritten by the next column
+    // no trailing barrier: column j+1 writes the other buffers, and column j+2
+    // reaches these only after column j+1's barrier, which every thread passes
+    // after finishing column j
   }
 #pragma unroll
   for (int q = 0; q < RPT; ++q) {
@@ -310,6 +341,61 @@ __global__ void __launch_bounds__(512, 1) k_lu_panel_reg(double* A, int64_t ld, 
       for (int c = 0; c < kNbReg; ++c)
         if (c < nb) A[(int64_t)(k0 + c) * ld + i] = a[q][c];
   }
+}
+
+// getrf's laswp + trsm for a register panel in one launch: every column
+// outside the panel gets the panel's row interchanges in order; the columns
+// right of it then U12 = L11^-1 A12 (unit lower L11 staged in shared memory).
+// One thread per column; rows k0..k0+nb-1 of it live in registers.
+__global__ void __launch_bounds__(64) k_lu_swap_trsm(double* A, int64_t ld, int n, int k0, int nb, const int* piv) {
+  lu_pdl_enter();
+  __shared__ double sL[kNbReg][kNbReg + 1];
+  __shared__ int spv[kNbReg];
+  for (int e = threadIdx.x; e < kNbReg * kNbReg; e += blockDim.x) {
+    const int i = e % kNbReg, j = e / kNbReg;
+    sL[i][j] = (j < i && i < nb) ? A[(int64_t)(k0 + j) * ld + k0 + i] : 0.0;
+  }
+  if (threadIdx.x < kNbReg) spv[threadIdx.x] = threadIdx.x < nb ? piv[k0 + threadIdx.x] : k0 + threadIdx.x;
+  __syncthreads();
+  const int cc = blockIdx.x * blockDim.x + threadIdx.x;
+  if (cc >= n - nb) return;
+  const int c = cc < k0 ? cc : cc + nb;
+  double* col = A + (int64_t)c * ld;
+  double x[kNbReg];
+#pragma unroll
+  for (int r = 0; r < kNbReg; ++r) x[r] = r < nb ? col[k0 + r] : 0.0;
+#pragma unroll
+  for (int j = 0; j < kNbReg; ++j) {
+    if (j >= nb) break;
+    const int p = spv[j];
+    if (p == k0 + j) continue;
+    if (p < k0 + nb) {  // both rows in the register block
+      double t = 0.0;
+#pragma unroll
+      for (int r = 0; r < kNbReg; ++r)
+        if (r == p - k0) t = x[r];
+#pragma unroll
+      for (int r = 0; r < kNbReg; ++r)
+        if (r == p - k0) x[r] = x[j];
+      x[j] = t;
+    } else {
+      const double t = col[p];
+      col[p] = x[j];
+      x[j] = t;
+    }
+  }
+  if (c >= k0 + nb) {
+#pragma unroll
+    for (int j = 0; j < kNbReg; ++j) {
+      if (j >= nb) break;
+#pragma unroll
+      for (int i = j + 1; i < kNbReg; ++i)
+        if (i < nb) x[i] = fma(-sL[i][j], x[j], x[i]);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < kNbReg; ++r)
+    if (r < nb) col[k0 + r] = x[r];
 }
 
 // Row interchanges of panel [k0, k0+nb) applied to the columns outside it,
@@ -449,24 +535,23 @@ void lu_factor(int64_t n, double* a_dev, int* piv, cudaStream_t s) {
   for (int64_t k0 = 0; k0 < n; k0 += step) {
     const int nb = (int)std::min<int64_t>(step, n - k0);
     if (reg_panel) {
-      if (n - k0 <= 512) k_lu_panel_reg<1><<<1, 512, 0, s>>>(a_dev, n, (int)n, (int)k0, nb, piv);
-      else k_lu_panel_reg<2><<<1, 512, 0, s>>>(a_dev, n, (int)n, (int)k0, nb, piv);
-      STROM_LAUNCH_CHECK();
-      if (n > nb) {
-        k_lu_laswp<<<(unsigned)ceil_div(n - nb, 128), 128, 0, s>>>(a_dev, n, (int)n, (int)k0, nb, piv);
-        STROM_LAUNCH_CHECK();
-      }
+      if (n - k0 <= 512) lu_launch(k_lu_panel_reg<1>, dim3(1), dim3(512), s, a_dev, (int64_t)n, (int)n, (int)k0, nb, piv);
+      else lu_launch(k_lu_panel_reg<2>, dim3(1), dim3(512), s, a_dev, (int64_t)n, (int)n, (int)k0, nb, piv);
+      if (n > nb)  // interchanges outside the panel + TRSM, one launch
+        lu_launch(k_lu_swap_trsm, dim3((unsigned)ceil_div(n - nb, 64)), dim3(64), s, a_dev, (int64_t)n, (int)n,
+                  (int)k0, nb, (const int*)piv);
     } else {
       k_lu_panel<<<1, 1024, 0, s>>>(a_dev, n, (int)n, (int)k0, nb, piv);
       STROM_LAUNCH_CHECK();
     }
     const int64_t rest = n - k0 - nb;
     if (rest > 0) {
-      k_lu_trsm<<<(unsigned)ceil_div(rest, 128), 128, 0, s>>>(a_dev, n, (int)n, (int)k0, nb);
-      STROM_LAUNCH_CHECK();
+      if (!reg_panel) {
+        k_lu_trsm<<<(unsigned)ceil_div(rest, 128), 128, 0, s>>>(a_dev, n, (int)n, (int)k0, nb);
+        STROM_LAUNCH_CHECK();
+      }
       dim3 g((unsigned)ceil_div(rest, 64), (unsigned)ceil_div(rest, 64));
-      k_lu_gemm<<<g, 256, 0, s>>>(a_dev, n, (int)n, (int)k0, nb);
-      STROM_LAUNCH_CHECK();
+      lu_launch(k_lu_gemm, g, dim3(256), s, a_dev, (int64_t)n, (int)n, (int)k0, nb);
     }
   }
 }
