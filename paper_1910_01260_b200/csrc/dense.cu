@@ -254,8 +254,12 @@ __global__ void __launch_bounds__(512, 1) k_lu_panel_reg(double* A, int64_t ld, 
 #pragma unroll
     for (int c = 0; c < kNbReg; ++c) a[q][c] = (i < n && c < nb) ? A[(int64_t)(k0 + c) * ld + i] : 0.0;
   }
-#pragma unroll 1
-  for (int j = 0; j < nb; ++j) {
+  // fully unrolled over the panel width: j is a compile-time constant in each
+  // copy, so a[q][j] is a plain register and the update covers c > j statically
+  // (no per-column register-select chains)
+#pragma unroll
+  for (int j = 0; j < kNbReg; ++j) {
+    if (j >= nb) break;
     const int jr = k0 + j, buf = j & 1;
     double best = -1.0;
     int bi = 0x7fffffff;
@@ -464,9 +468,12 @@ __global__ void __launch_bounds__(512) k_lu_solve_cta(const double* A, int64_t l
         if (lane < bw) xs[b0 + lane] = xi;
       }
       __syncthreads();
+      // unrolled over the block width so the 32 column loads are in flight at once
       for (int i = b0 + bw + threadIdx.x; i < n; i += blockDim.x) {
         double acc = 0.0;
-        for (int j = 0; j < bw; ++j) acc = fma(A[(int64_t)(b0 + j) * ld + i], xs[b0 + j], acc);
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j < bw) acc = fma(A[(int64_t)(b0 + j) * ld + i], xs[b0 + j], acc);
         xs[i] -= acc;
       }
       __syncthreads();
@@ -493,7 +500,9 @@ __global__ void __launch_bounds__(512) k_lu_solve_cta(const double* A, int64_t l
       __syncthreads();
       for (int i = threadIdx.x; i < b0; i += blockDim.x) {
         double acc = 0.0;
-        for (int j = 0; j < bw; ++j) acc = fma(A[(int64_t)(b0 + j) * ld + i], xs[b0 + j], acc);
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j < bw) acc = fma(A[(int64_t)(b0 + j) * ld + i], xs[b0 + j], acc);
         xs[i] -= acc;
       }
       __syncthreads();
