@@ -452,58 +452,82 @@ __global__ void __launch_bounds__(512) k_lu_solve_cta(const double* A, int64_t l
         if (p != j) { const double t = xs[j]; xs[j] = xs[p]; xs[p] = t; }
       }
     __syncthreads();
+    // Both sweeps keep one block of look-ahead: warp 0 applies block b's
+    // contribution to the next block's rows and solves that block's diagonal
+    // while warps 1.. apply it to the rows beyond -- one barrier per block.
+    // Every row sees the same fma sequence as in a plain blocked sweep.
+    auto diag_fwd = [&](int b0, int bw) {  // warp 0: unit lower diagonal block
+      double lrow[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) lrow[j] = (lane < bw && j < lane) ? A[(int64_t)(b0 + j) * ld + b0 + lane] : 0.0;
+      double xi = lane < bw ? xs[b0 + lane] : 0.0;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const double xj = __shfl_sync(0xffffffffu, xi, j);
+        if (lane > j) xi = fma(-lrow[j], xj, xi);
+      }
+      if (lane < bw) xs[b0 + lane] = xi;
+    };
+    auto diag_bwd = [&](int b0, int bw) {  // warp 0: upper diagonal block
+      double urow[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) urow[j] = (lane < bw && j >= lane && j < bw) ? A[(int64_t)(b0 + j) * ld + b0 + lane] : 0.0;
+      double xi = lane < bw ? xs[b0 + lane] : 0.0;
+#pragma unroll
+      for (int j = 31; j >= 0; --j) {
+        if (j < bw) {
+          double xj = __shfl_sync(0xffffffffu, xi, j);
+          if (lane == j) { xi = xi / urow[j]; }
+          xj = __shfl_sync(0xffffffffu, xi, j);
+          if (lane < j) xi = fma(-urow[j], xj, xi);
+        }
+      }
+      if (lane < bw) xs[b0 + lane] = xi;
+    };
+    // row i minus the contribution of block [b0, b0 + bw) (unrolled: the 32
+    // column loads are in flight at once)
+    auto apply_block = [&](int i, int b0, int bw) {
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < bw) acc = fma(A[(int64_t)(b0 + j) * ld + i], xs[b0 + j], acc);
+      xs[i] -= acc;
+    };
+    const int nt_rest = blockDim.x - 32;
     // forward: unit lower L
+    if (wid == 0) diag_fwd(0, min(32, n));
+    __syncthreads();
     for (int b0 = 0; b0 < n; b0 += 32) {
       const int bw = min(32, n - b0);
+      const int nb0 = b0 + bw, nbw = min(32, n - nb0);
       if (wid == 0) {
-        double lrow[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) lrow[j] = (lane < bw && j < lane) ? A[(int64_t)(b0 + j) * ld + b0 + lane] : 0.0;
-        double xi = lane < bw ? xs[b0 + lane] : 0.0;
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const double xj = __shfl_sync(0xffffffffu, xi, j);
-          if (lane > j) xi = fma(-lrow[j], xj, xi);
+        if (nbw > 0) {
+          if (lane < nbw) apply_block(nb0 + lane, b0, bw);
+          __syncwarp();
+          diag_fwd(nb0, nbw);
         }
-        if (lane < bw) xs[b0 + lane] = xi;
-      }
-      __syncthreads();
-      // unrolled over the block width so the 32 column loads are in flight at once
-      for (int i = b0 + bw + threadIdx.x; i < n; i += blockDim.x) {
-        double acc = 0.0;
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (j < bw) acc = fma(A[(int64_t)(b0 + j) * ld + i], xs[b0 + j], acc);
-        xs[i] -= acc;
+      } else if (nbw > 0) {
+        for (int i = nb0 + nbw + (int)threadIdx.x - 32; i < n; i += nt_rest) apply_block(i, b0, bw);
       }
       __syncthreads();
     }
     // backward: upper U (blocks from the bottom)
+    {
+      const int lb0 = max(0, n - 32);
+      if (wid == 0) diag_bwd(lb0, n - lb0);
+      __syncthreads();
+    }
     for (int b1 = n; b1 > 0; b1 -= 32) {
       const int b0 = max(0, b1 - 32), bw = b1 - b0;
+      const int pb0 = max(0, b0 - 32), pbw = b0 - pb0;  // the block above
       if (wid == 0) {
-        double urow[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) urow[j] = (lane < bw && j >= lane && j < bw) ? A[(int64_t)(b0 + j) * ld + b0 + lane] : 0.0;
-        double xi = lane < bw ? xs[b0 + lane] : 0.0;
-#pragma unroll
-        for (int j = 31; j >= 0; --j) {
-          if (j < bw) {
-            double xj = __shfl_sync(0xffffffffu, xi, j);
-            if (lane == j) { xi = xi / urow[j]; }
-            xj = __shfl_sync(0xffffffffu, xi, j);
-            if (lane < j) xi = fma(-urow[j], xj, xi);
-          }
+        if (pbw > 0) {
+          if (lane < pbw) apply_block(pb0 + lane, b0, bw);
+          __syncwarp();
+          diag_bwd(pb0, pbw);
         }
-        if (lane < bw) xs[b0 + lane] = xi;
-      }
-      __syncthreads();
-      for (int i = threadIdx.x; i < b0; i += blockDim.x) {
-        double acc = 0.0;
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (j < bw) acc = fma(A[(int64_t)(b0 + j) * ld + i], xs[b0 + j], acc);
-        xs[i] -= acc;
+      } else {
+        for (int i = (int)threadIdx.x - 32; i < pb0; i += nt_rest) apply_block(i, b0, bw);
       }
       __syncthreads();
     }
