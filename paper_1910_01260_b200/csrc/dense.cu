@@ -10,6 +10,7 @@
 // register-blocked GEMM across all SMs.  The matrix (<= a few thousand) stays
 // L2-resident between kernels.
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <string>
 #include <vector>
@@ -308,9 +309,12 @@ __global__ void __launch_bounds__(512, 1) k_lu_panel_reg(double* A, int64_t ld, 
       const int ow = __shfl_xor_sync(0xffffffffu, gw, o);
       if (ob > gb || (ob == gb && oi < gi)) { gb = ob; gi = oi; gw = ow; }
     }
-    const int p = gi;  // a candidate always exists: row jr itself
+    // a candidate exists unless the whole sub-column is NaN (every |a| > best
+    // test fails): then row jr pivots on itself, like k_lu_panel
+    const bool none = (gi == 0x7fffffff);
+    const int p = none ? jr : gi;
     if (threadIdx.x == 0) piv[jr] = p;
-    const double* prow = cand[buf][gw];
+    const double* prow = none ? drow[buf] : cand[buf][gw & 15];
     const double d = prow[j];
     const double inv = d != 0.0 ? 1.0 / d : 0.0;
 #pragma unroll
@@ -537,16 +541,26 @@ __global__ void __launch_bounds__(512) k_lu_solve_cta(const double* A, int64_t l
 }
 
 // ||A||_F: per-CTA partial sums of squares, then one CTA adds them in order.
-__global__ void __launch_bounds__(256) k_fro_part(const double* A, int64_t ld, int64_t n, double* part) {
+// Frobenius norm partials of the rows x cols column-major A (ld); a block that
+// saw a non-finite entry writes NaN, so the norm doubles as the finiteness
+// test of scipy's lu_factor / lu_solve (check_finite=True).
+__global__ void __launch_bounds__(256) k_fro_part(const double* A, int64_t ld, int64_t rows, int64_t cols,
+                                                  double* part) {
   __shared__ double red[32];
+  __shared__ int s_bad;
+  if (threadIdx.x == 0) s_bad = 0;
+  __syncthreads();
   double s = 0.0;
-  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n * n;
+  bool bad = false;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < rows * cols;
        idx += (int64_t)gridDim.x * blockDim.x) {
-    const double v = A[(idx / n) * ld + idx % n];
+    const double v = A[(idx / rows) * ld + idx % rows];
+    bad |= !isfinite(v);
     s = fma(v, v, s);
   }
+  if (bad) s_bad = 1;
   s = block_sum(s, red);
-  if (threadIdx.x == 0) part[blockIdx.x] = s;
+  if (threadIdx.x == 0) part[blockIdx.x] = s_bad ? __longlong_as_double(0x7ff8000000000000LL) : s;
 }
 __global__ void __launch_bounds__(256) k_fro_final(const double* part, int np, double* out) {
   __shared__ double red[32];
@@ -594,7 +608,8 @@ void lu_factor(int64_t n, double* a_dev, int* piv, cudaStream_t s) {
 void lu_solve(int64_t n, const double* a_dev, const int* piv, double* x_dev, int64_t ldx, int64_t nrhs,
               const double* fro, double* info, cudaStream_t s) {
   if ((size_t)n * 8 <= 96 * 1024) {
-    static bool cfg = false;
+    static PerDevice<bool> cfgs;
+    bool& cfg = cfgs.get();
     if (!cfg) {
       STROM_CUDA(cudaFuncSetAttribute(k_lu_solve_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
       cfg = true;
@@ -642,21 +657,27 @@ int strom_dense_solve(int64_t n, double* a_dev, double* x_dev, int64_t nrhs, int
     STROM_REQUIRE(n >= 1 && a_dev && x_dev && nrhs >= 0, "bad solve arguments");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     auto scratch = dev_alloc(8 * 8 + (size_t)n * 4, s, true);
-    double* fro = scratch->as<double>();
+    double* fro = scratch->as<double>();  // [0] ||A||_F, [1] ||B||_F (NaN: non-finite entry)
     double* info = info_dev ? info_dev : fro + 2;
     int* piv = piv_dev ? piv_dev : reinterpret_cast<int*>(fro + 8);
     {
       const int np = 256;
-      auto fp = dev_alloc((size_t)np * 8, s, false);
-      k_fro_part<<<np, 256, 0, s>>>(a_dev, n, n, fp->as<double>());
+      auto fp = dev_alloc((size_t)2 * np * 8, s, false);
+      k_fro_part<<<np, 256, 0, s>>>(a_dev, n, n, n, fp->as<double>());
       k_fro_final<<<1, 256, 0, s>>>(fp->as<double>(), np, fro);
+      k_fro_part<<<np, 256, 0, s>>>(x_dev, n, n, nrhs, fp->as<double>() + np);
+      k_fro_final<<<1, 256, 0, s>>>(fp->as<double>() + np, np, fro + 1);
       STROM_LAUNCH_CHECK();
     }
     lu_factor(n, a_dev, piv, s);
     lu_solve(n, a_dev, piv, x_dev, n, nrhs, fro, info, s);
-    double h[3];
+    double h[3], nf[2];
     STROM_CUDA(cudaMemcpyAsync(h, info, 3 * 8, cudaMemcpyDeviceToHost, s));
+    STROM_CUDA(cudaMemcpyAsync(nf, fro, 2 * 8, cudaMemcpyDeviceToHost, s));
     STROM_CUDA(cudaStreamSynchronize(s));
+    // scipy.linalg.lu_factor / lu_solve (check_finite=True), linalg.py:90,99
+    if (!std::isfinite(nf[0]) || !std::isfinite(nf[1]))
+      throw Error(kInvalidArgument, "array must not contain infs or NaNs");
     if (h[0] >= 0.0) {
       char buf[160];
       snprintf(buf, sizeof(buf), "matrix numerically singular: pivot %lld is %.3e (floor %.3e)",

@@ -404,8 +404,8 @@ void launch_pass_t(const PassArgs& a, int cols_ub, int reserve, int kind_prof, c
   // stages (+ x and x_next segments); the decision tail reuses them as its workspace
   const size_t smem = std::max((size_t)nst * kStageRows * (cols + 2) * 8,
                                (size_t)2 * (kPassThreads / 32) * round_up(a.ccap, 32) * 8);
-  static size_t cfg = 0;
-  set_smem_attr(k_pass<MAXJ>, smem, &cfg);
+  static PerDevice<size_t> cfg;
+  set_smem_attr(k_pass<MAXJ>, smem, &cfg.get());
   const int64_t ntiles = a.ldu / kStageRows;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, std::max(1, sm_count() - reserve)));
   ProfScope ps(kind_prof, s);
@@ -484,9 +484,9 @@ size_t decide_smem(const PipeMem& m) { return (size_t)2 * (kDecideThreads / 32) 
 
 
 void launch_prep(const PipeMem& m, const IsvdParams& P, cudaStream_t s) {
-  static size_t cfg = 0;
+  static PerDevice<size_t> cfg;
   const size_t smem = decide_smem(m);
-  set_smem_attr(k_prep, smem, &cfg);
+  set_smem_attr(k_prep, smem, &cfg.get());
   ProfScope ps(P_STEP_A, s);
   k_prep<<<1, kDecideThreads, smem, s>>>(m.pp, P);
   STROM_LAUNCH_CHECK();
@@ -494,14 +494,14 @@ void launch_prep(const PipeMem& m, const IsvdParams& P, cudaStream_t s) {
 
 void launch_decide_kernel(bool second, const StateView& src, const PipeMem& m, const IsvdParams& P,
                           cudaStream_t s) {
-  static size_t cfg1 = 0, cfg2 = 0;
+  static PerDevice<size_t> cfg1, cfg2;
   const size_t smem = decide_smem(m);
   ProfScope ps(P_STEP_A, s);
   if (!second) {
-    set_smem_attr(k_decide, smem, &cfg1);
+    set_smem_attr(k_decide, smem, &cfg1.get());
     launch_pdl(k_decide, dim3(1), dim3(kDecideThreads), smem, s, src, m.pp, P);
   } else {
-    set_smem_attr(k_decide2, smem, &cfg2);
+    set_smem_attr(k_decide2, smem, &cfg2.get());
     launch_pdl(k_decide2, dim3(1), dim3(kDecideThreads), smem, s, src, m.pp, P);
   }
   STROM_LAUNCH_CHECK();
@@ -531,8 +531,8 @@ void launch_step_b(const StateView& src, const StateView& dst, const PipeMem& m,
                    const Caps& caps, cudaStream_t s) {
   int use_smem = 0;
   const size_t smem = small_kernel_smem(caps, &use_smem);
-  static size_t cfg = 0;
-  set_smem_attr(k_step_b, smem, &cfg);
+  static PerDevice<size_t> cfg;
+  set_smem_attr(k_step_b, smem, &cfg.get());
   ProfScope ps(P_STEP_B, s);
   k_step_b<<<1, kSmallThreads, smem, s>>>(src, dst, m.pp, P, use_smem);
   STROM_LAUNCH_CHECK();
@@ -550,8 +550,8 @@ void launch_compact_prep(const StateView& src, const StateView& dst, const PipeM
                          const Caps& caps, cudaStream_t s) {
   int use_smem = 0;
   const size_t smem = small_kernel_smem(caps, &use_smem);
-  static size_t cfg = 0;
-  set_smem_attr(k_compact_prep, smem, &cfg);
+  static PerDevice<size_t> cfg;
+  set_smem_attr(k_compact_prep, smem, &cfg.get());
   ProfScope ps(P_COMPACT, s);
   k_compact_prep<<<1, kSmallThreads, smem, s>>>(src, dst, m.pp, P, use_smem);
   STROM_LAUNCH_CHECK();
@@ -585,8 +585,8 @@ void launch_compact_pass(const Store& src, const int32_t* base_dev, const int32_
                          cudaStream_t s) {
   const int c4 = (cmax + 3) & ~3, RP = (rmax + 31) & ~31;
   const size_t smem = ((size_t)c4 * (RP + 4) + (size_t)c4 * (kUTile + 4) + (size_t)RP * (kUTile + 4)) * 8;
-  static size_t cfg = 0;
-  set_smem_attr(k_compact_pass<GB>, smem, &cfg);
+  static PerDevice<size_t> cfg;
+  set_smem_attr(k_compact_pass<GB>, smem, &cfg.get());
   ProfScope ps(P_TALL_GEMM, s);
   k_compact_pass<GB><<<sm_count(), kCompactThreads, smem, s>>>(src.U(), src.ccap, base_dev, c_dev, r_dev, T, ldt,
                                                                dst.U(), dst.ccap, src.ldu / kUTile, part, QP);
@@ -607,7 +607,8 @@ void gram_cholesky(const Tall& A, const int32_t* col0_dev, const int32_t* q_dev,
   if (QP <= 64) {
     k_tall_gram<1, 8><<<grid, 256, smem, s>>>(A, col0_dev, q_dev, q_fixed, n, part->as<double>(), QP);
   } else if (QP <= 128) {
-    static bool cfg = false;
+    static PerDevice<bool> cfgs;
+    bool& cfg = cfgs.get();
     if (!cfg) {
       STROM_CUDA(cudaFuncSetAttribute(k_tall_gram<2, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
       cfg = true;
@@ -772,7 +773,9 @@ struct ColumnSource {
   // (cfg2 e2e, steady state: 4 x 4 columns 79.1 ms per 400 snapshots, 3 x 16
   // 80.3 ms; the device-resident path 76.5 ms)
   const int64_t kChunk = env_int("STROM_H2D_CHUNK", 4);
-  const int kRing = (int)env_int("STROM_H2D_RING", 4);
+  // at least 2 slots: col(t + 1) is requested before release(t) issues the
+  // next chunk, so one slot would hand out a column still being copied
+  const int kRing = (int)std::max<int64_t>(2, env_int("STROM_H2D_RING", 4));
   static int64_t env_int(const char* name, int64_t dflt) {
     const char* e = getenv(name);
     return e && atoll(e) > 0 ? atoll(e) : dflt;

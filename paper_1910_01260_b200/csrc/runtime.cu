@@ -44,20 +44,30 @@ DevMemPtr dev_alloc(size_t bytes, cudaStream_t s, bool zero) {
   return m;
 }
 
+int current_device_id() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kMaxDevices) d = 0;
+  return d;
+}
+
 int sm_count() {
-  static int n = [] {
-    int dev = 0, v = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    return v;
-  }();
+  static PerDevice<int> cache;
+  int& n = cache.get();
+  if (n == 0) {
+    int v = 148;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, current_device_id());
+    n = v;
+  }
   return n;
 }
 
 size_t device_total_mem() {
-  static size_t n = [] {
+  static PerDevice<size_t> cache;
+  size_t& n = cache.get();
+  if (n == 0) {
     size_t f = 0, t = 0;
-    return cudaMemGetInfo(&f, &t) == cudaSuccess ? t : (size_t)0;
-  }();
+    n = cudaMemGetInfo(&f, &t) == cudaSuccess ? t : (size_t)0;
+  }
   return n;
 }
 
@@ -117,11 +127,13 @@ void release_event(cudaEvent_t e) {
 }
 
 size_t max_smem_optin() {
-  static size_t n = [] {
-    int dev = 0, v = 48 * 1024;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    return (size_t)v;
-  }();
+  static PerDevice<size_t> cache;
+  size_t& n = cache.get();
+  if (n == 0) {
+    int v = 48 * 1024;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, current_device_id());
+    n = (size_t)v;
+  }
   return n;
 }
 

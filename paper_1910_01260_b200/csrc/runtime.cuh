@@ -68,9 +68,19 @@ struct DevMem {
 using DevMemPtr = std::shared_ptr<DevMem>;
 DevMemPtr dev_alloc(size_t bytes, cudaStream_t s, bool zero = false);
 
+// Process-wide caches are keyed by device: a function attribute set or an
+// attribute queried on one GPU says nothing about another GPU of the process.
+constexpr int kMaxDevices = 64;
+int current_device_id();  // cudaGetDevice, clamped to [0, kMaxDevices)
+template <class T>
+struct PerDevice {
+  T v[kMaxDevices] = {};
+  T& get() { return v[current_device_id()]; }
+};
+
 int sm_count();
 size_t max_smem_optin();
-size_t device_total_mem();  // HBM bytes of the current device (queried once)
+size_t device_total_mem();  // HBM bytes of the current device (queried once per device)
 
 // Non-blocking streams and timing-free events recycled across calls: creating
 // and destroying them per ingest call is a driver round trip each, and those

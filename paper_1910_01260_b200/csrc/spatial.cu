@@ -734,7 +734,8 @@ int one_wave(K kernel, size_t smem, int64_t ntiles) {
 template <typename IdxT, int TAW, int TBM>
 int launch_spatial_t(SpatialArgs<IdxT> a, int max_grid, cudaStream_t s) {
   const size_t smem = (size_t)kLdK * (a.MA + a.NQ) * 8;
-  static bool configured = false;
+  static PerDevice<bool> configured_dev;
+  bool& configured = configured_dev.get();
   if (!configured) {
     STROM_CUDA(cudaFuncSetAttribute(k_spatial<IdxT, TAW, TBM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     64 * 1024));
@@ -770,7 +771,8 @@ size_t ell_smem(int K, int S, int MA, int NQ) {
 template <int K, int TA, int TB>
 void launch_ell_kernel(const EllArgs& a, int grid, size_t smem, cudaStream_t s) {
   auto kern = k_spatial_ell<K, TA, TB>;
-  static bool configured = false;
+  static PerDevice<bool> configured_dev;
+  bool& configured = configured_dev.get();
   if (!configured) {
     STROM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_smem_optin()));
     // the warpgroup register handoff must fit the launch allocation, or the

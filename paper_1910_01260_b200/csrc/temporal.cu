@@ -168,7 +168,8 @@ void launch_small_svd(SvdBatchArgs args, int batch, cudaStream_t s, DevMemPtr* k
     args.work_per = elems;
   }
   const size_t smem = args.use_smem ? bytes : 0;
-  static size_t configured = 0;
+  static PerDevice<size_t> configured_dev;
+  size_t& configured = configured_dev.get();
   if (smem > 48 * 1024 && smem > configured) {
     STROM_CUDA(cudaFuncSetAttribute(k_small_svd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = smem;

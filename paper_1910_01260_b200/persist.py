@@ -150,5 +150,6 @@ def load_basis(bases_dir, n_s: int | None = None, n_t: int | None = None):
                          f"n_t={stored_nt}")
     n_steps = temporal[0].shape[0]
     v_path = bases_dir / "v.strommat"
-    n_mu = _read_checked(v_path)[0] // n_steps if v_path.exists() else n_t
+    # read_matrix, as the reference does (pipeline.py:171): it validates the payload too
+    n_mu = read_matrix(v_path).shape[0] // n_steps if v_path.exists() else n_t
     return BasisSet(phi_s=phi_s[:, :n_s], temporal=tuple(t[:, :n_t] for t in temporal[:n_s]), n_mu=n_mu)

@@ -121,6 +121,8 @@ def srom_march(rom: SpatialRom, grid, inputs) -> torch.Tensor:
     eye = torch.eye(n_s, dtype=F64, device=dev)
     factors = {}
     x = rom.x0_hat
+    if not bool(torch.isfinite(rom.a_hat).all()):  # scipy lu_factor(check_finite=True), spatial.py:80
+        raise ValueError("array must not contain infs or NaNs")
     for k in range(nt):
         dt = float(grid.dt[k])
         fac = factors.get(dt)
