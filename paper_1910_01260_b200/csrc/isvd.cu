@@ -5,6 +5,10 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <thread>
+#include <string>
+#include <mutex>
+#include <condition_variable>
 #include <vector>
 
 #include "../../include/strom_b200.h"
@@ -763,10 +767,16 @@ strom_isvd* update_once(strom_isvd* src, const double* x, cudaStream_t s, bool i
 // Columns of an ingest call: device pointers, or host columns staged through a
 // ring of device chunks on a copy stream.  Chunks grow 1, 2, 4, 4, ... columns,
 // so the first update waits for one column's copy, not a full chunk.
+//
+// Pageable host columns (a plain numpy array, what the reference's callers
+// pass: pipeline.py:95-111) cannot be DMA'd asynchronously.  A stager thread
+// copies each chunk into a recycled pinned buffer (parallel_memcpy) and issues
+// its H2D copy itself, so the host copy of chunk q+1 overlaps the DMA of chunk
+// q and the updates; the compute thread only waits for a chunk it needs.
 struct ColumnSource {
   const double* X = nullptr;
   int64_t ldx = 0, n = 0, ncols = 0;
-  bool host = false;
+  bool host = false, pageable = false;
   cudaStream_t s = nullptr, cs = nullptr;
   // largest chunk (ring slot capacity, columns) and ring depth; STROM_H2D_CHUNK /
   // STROM_H2D_RING override them for measurements
@@ -781,17 +791,28 @@ struct ColumnSource {
     return e && atoll(e) > 0 ? atoll(e) : dflt;
   }
   std::vector<DevMemPtr> ring;
-  std::vector<cudaEvent_t> ready, freed;
+  std::vector<cudaEvent_t> ready, freed, hdone;
+  std::vector<void*> pinned;  // pageable mode: one staging buffer per slot
   std::vector<int64_t> start;  // chunk q holds columns [start[q], start[q+1])
   int64_t issued = 0, waited = -1;
+  // pageable mode: the stager thread and its handshakes with the compute thread
+  std::thread stager;
+  std::mutex mu;
+  std::condition_variable cv;
+  int64_t staged = 0;    // chunks whose H2D copy (and ready event) the stager has enqueued
+  int64_t released = 0;  // chunks whose freed event the compute thread has recorded
+  bool abort = false;
+  std::string stage_error;
 
   int64_t nchunks() const { return (int64_t)start.size() - 1; }
   int64_t chunk_of(int64_t t) const {
     return (int64_t)(std::upper_bound(start.begin(), start.end(), t) - start.begin()) - 1;
   }
+  size_t slot_bytes() const { return (size_t)n * kChunk * 8; }
   void open(const double* X_, int64_t ldx_, int64_t n_, int64_t ncols_, bool host_, cudaStream_t s_) {
     X = X_; ldx = ldx_; n = n_; ncols = ncols_; host = host_; s = s_;
     if (!host) return;
+    pageable = is_pageable_host(X);
     start.clear();
     for (int64_t c = 0, w = 1; c < ncols; c += w, w = std::min<int64_t>(2 * w, kChunk)) start.push_back(c);
     start.push_back(ncols);
@@ -800,10 +821,22 @@ struct ColumnSource {
     ready.resize(kRing);
     freed.resize(kRing);
     for (int i = 0; i < kRing; ++i) {
-      ring[i] = dev_alloc((size_t)n * kChunk * 8, s, false);
+      ring[i] = dev_alloc(slot_bytes(), s, false);
       ready[i] = acquire_event();
       freed[i] = acquire_event();
       STROM_CUDA(cudaEventRecord(freed[i], s));
+    }
+    if (pageable) {
+      hdone.resize(kRing);
+      pinned.resize(kRing);
+      for (int i = 0; i < kRing; ++i) {
+        hdone[i] = acquire_event();
+        pinned[i] = acquire_pinned(slot_bytes());
+      }
+      int dev = 0;
+      STROM_CUDA(cudaGetDevice(&dev));
+      stager = std::thread([this, dev] { stage_all(dev); });
+      return;
     }
     while (issued < std::min<int64_t>(kRing, nchunks())) issue(issued++);
   }
@@ -815,12 +848,58 @@ struct ColumnSource {
                                  cs));
     STROM_CUDA(cudaEventRecord(ready[slot], cs));
   }
+  // pageable mode, stager thread: chunk q -> pinned[slot] -> ring[slot]
+  void stage_all(int dev) {
+    try {
+      STROM_CUDA(cudaSetDevice(dev));
+      for (int64_t q = 0; q < nchunks(); ++q) {
+        const int slot = (int)(q % kRing);
+        const int64_t c0 = start[q], cn = start[q + 1] - start[q];
+        if (q >= kRing) STROM_CUDA(cudaEventSynchronize(hdone[slot]));  // DMA of chunk q - kRing is done
+        {
+          std::unique_lock<std::mutex> g(mu);
+          if (abort) return;
+        }
+        double* dst = static_cast<double*>(pinned[slot]);
+        if (ldx == n) {
+          parallel_memcpy(dst, X + c0 * ldx, (size_t)cn * n * 8);
+        } else {
+          for (int64_t c = 0; c < cn; ++c) parallel_memcpy(dst + c * n, X + (c0 + c) * ldx, (size_t)n * 8);
+        }
+        {
+          // the compute thread must have recorded freed[slot] for chunk q - kRing
+          std::unique_lock<std::mutex> g(mu);
+          cv.wait(g, [&] { return abort || released > q - kRing; });
+          if (abort) return;
+        }
+        STROM_CUDA(cudaStreamWaitEvent(cs, freed[slot], 0));
+        STROM_CUDA(cudaMemcpyAsync(ring[slot]->ptr, dst, (size_t)cn * n * 8, cudaMemcpyHostToDevice, cs));
+        STROM_CUDA(cudaEventRecord(ready[slot], cs));
+        STROM_CUDA(cudaEventRecord(hdone[slot], cs));
+        {
+          std::lock_guard<std::mutex> g(mu);
+          staged = q + 1;
+        }
+        cv.notify_all();
+      }
+    } catch (const std::exception& e) {
+      std::lock_guard<std::mutex> g(mu);
+      stage_error = e.what();
+      abort = true;
+      cv.notify_all();
+    }
+  }
   // device pointer of column t; the compute stream waits for its chunk once
   const double* col(int64_t t) {
     if (t < 0 || t >= ncols) return nullptr;
     if (!host) return X + t * ldx;
     const int64_t q = chunk_of(t);
     if (q > waited) {
+      if (pageable) {
+        std::unique_lock<std::mutex> g(mu);
+        cv.wait(g, [&] { return abort || staged > q; });
+        if (!stage_error.empty()) throw Error(kCudaError, "host staging: " + stage_error);
+      }
       for (int64_t w = waited + 1; w <= q; ++w) STROM_CUDA(cudaStreamWaitEvent(s, ready[w % kRing], 0));
       waited = q;
     }
@@ -832,14 +911,36 @@ struct ColumnSource {
     const int64_t q = chunk_of(t);
     if (t + 1 != start[q + 1]) return;
     STROM_CUDA(cudaEventRecord(freed[q % kRing], s));
+    if (pageable) {
+      {
+        std::lock_guard<std::mutex> g(mu);
+        released = q + 1;
+      }
+      cv.notify_all();
+      return;
+    }
     if (issued < nchunks() && issued <= q + kRing) issue(issued++);
   }
   void close() {
     if (!host) return;
+    if (pageable) {
+      {
+        std::lock_guard<std::mutex> g(mu);
+        abort = true;
+      }
+      cv.notify_all();
+      if (stager.joinable()) stager.join();
+    }
     STROM_CUDA(cudaStreamSynchronize(cs));
     for (int i = 0; i < kRing; ++i) {
       release_event(ready[i]);
       release_event(freed[i]);
+    }
+    if (pageable) {
+      for (int i = 0; i < kRing; ++i) {
+        release_event(hdone[i]);
+        release_pinned(pinned[i], slot_bytes());
+      }
     }
     release_stream(cs);
     cs = nullptr;

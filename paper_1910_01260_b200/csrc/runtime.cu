@@ -1,5 +1,9 @@
 #include <cstring>
 #include <mutex>
+#include <algorithm>
+#include <cstdlib>
+#include <thread>
+#include <condition_variable>
 #include <vector>
 
 #include "runtime.cuh"
@@ -124,6 +128,127 @@ void release_event(cudaEvent_t e) {
   if (!e) return;
   std::lock_guard<std::mutex> g(g_res_mu);
   g_events.emplace_back(current_device(), e);
+}
+
+namespace {
+std::vector<std::pair<size_t, void*>> g_pinned;
+}  // namespace
+
+void* acquire_pinned(size_t bytes) {
+  {
+    std::lock_guard<std::mutex> g(g_res_mu);
+    for (size_t i = 0; i < g_pinned.size(); ++i)
+      if (g_pinned[i].first == bytes) {
+        void* p = g_pinned[i].second;
+        g_pinned.erase(g_pinned.begin() + (std::ptrdiff_t)i);
+        return p;
+      }
+  }
+  void* p = nullptr;
+  STROM_CUDA(cudaHostAlloc(&p, bytes, cudaHostAllocPortable));
+  return p;
+}
+
+void release_pinned(void* p, size_t bytes) {
+  if (!p) return;
+  std::lock_guard<std::mutex> g(g_res_mu);
+  g_pinned.emplace_back(bytes, p);
+}
+
+bool is_pageable_host(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeUnregistered;
+}
+
+namespace {
+// Persistent copy workers: job = [dst, src, bytes) split in equal pieces; the
+// caller copies piece 0 and waits for the rest.
+struct CopyPool {
+  std::mutex mu;
+  std::condition_variable cv_job, cv_done;
+  std::vector<std::thread> workers;
+  char* dst = nullptr;
+  const char* src = nullptr;
+  size_t bytes = 0;
+  int pieces = 1;
+  uint64_t gen = 0;
+  int pending = 0;
+  bool stop = false;
+
+  explicit CopyPool(int nworkers) {
+    for (int w = 0; w < nworkers; ++w) workers.emplace_back([this, w] { run(w + 1); });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> g(mu);
+      stop = true;
+    }
+    cv_job.notify_all();
+    for (auto& t : workers) t.join();
+  }
+  void piece(int i, char* d, const char* s0, size_t b, int np) {
+    const size_t per = (b / np + 63) & ~(size_t)63;
+    const size_t lo = std::min(b, per * (size_t)i), hi = std::min(b, lo + per);
+    if (hi > lo) std::memcpy(d + lo, s0 + lo, hi - lo);
+  }
+  void run(int idx) {
+    uint64_t seen = 0;
+    for (;;) {
+      char* d;
+      const char* s0;
+      size_t b;
+      int np;
+      {
+        std::unique_lock<std::mutex> g(mu);
+        cv_job.wait(g, [&] { return stop || gen != seen; });
+        if (stop) return;
+        seen = gen;
+        d = dst; s0 = src; b = bytes; np = pieces;
+      }
+      if (idx < np) piece(idx, d, s0, b, np);
+      {
+        std::lock_guard<std::mutex> g(mu);
+        if (--pending == 0) cv_done.notify_one();
+      }
+    }
+  }
+  void copy(void* d, const void* s0, size_t b) {
+    const int np = (int)workers.size() + 1;
+    if (b < ((size_t)1 << 20) || np == 1) {
+      std::memcpy(d, s0, b);
+      return;
+    }
+    {
+      std::lock_guard<std::mutex> g(mu);
+      dst = static_cast<char*>(d);
+      src = static_cast<const char*>(s0);
+      bytes = b;
+      pieces = np;
+      pending = (int)workers.size();
+      ++gen;
+    }
+    cv_job.notify_all();
+    piece(0, static_cast<char*>(d), static_cast<const char*>(s0), b, np);
+    std::unique_lock<std::mutex> g(mu);
+    cv_done.wait(g, [&] { return pending == 0; });
+  }
+};
+std::mutex g_copy_mu;  // one job at a time
+}  // namespace
+
+void parallel_memcpy(void* dst, const void* src, size_t bytes) {
+  static CopyPool* pool = [] {
+    const char* e = getenv("STROM_COPY_THREADS");
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    int nt = e ? atoi(e) : (int)std::min(8u, std::max(1u, hw / 2));
+    return new CopyPool(std::max(0, nt - 1));  // leaked: lives for the process
+  }();
+  std::lock_guard<std::mutex> g(g_copy_mu);
+  pool->copy(dst, src, bytes);
 }
 
 size_t max_smem_optin() {

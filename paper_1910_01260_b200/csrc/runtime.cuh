@@ -91,6 +91,16 @@ void release_stream(cudaStream_t s);
 cudaEvent_t acquire_event();
 void release_event(cudaEvent_t e);
 
+// Pinned host staging buffers recycled across calls (cudaHostAlloc of tens of
+// MB is a millisecond-scale driver call).  Contents are undefined.
+void* acquire_pinned(size_t bytes);
+void release_pinned(void* p, size_t bytes);
+// Host memcpy split over a small persistent worker pool (pageable -> pinned
+// staging runs at several threads' memory bandwidth, not one's).
+void parallel_memcpy(void* dst, const void* src, size_t bytes);
+// true when p is ordinary pageable host memory (not cudaHostAlloc'ed or registered)
+bool is_pageable_host(const void* p);
+
 // Wrap a C-ABI body: map exceptions to status codes + thread-local message.
 template <class F>
 int guarded(F&& f) {

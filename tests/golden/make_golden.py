@@ -244,6 +244,44 @@ def gen_cfg4_small():
     _save("golden_cfg4_small.npz", **out)
 
 
+def gen_cfg4_kron():
+    """BASELINE configs[3]'s stated check instance: the cfg4 recipe on a 20^3 grid,
+    N_t = 50, n_s = 50, n_t = 20, block-assembled (spacetime.py:43-115) and by the
+    explicit Kronecker basis (spacetime.py:189-210, system.py:166-194; the
+    verify.py:124-158 protocol).  Phi_st is 400,000 x 1,000 (3.2 GB), so the
+    1000 x 1000 operators are stored as checksums plus a seeded sample of entries."""
+    d = wl.cfg4_inputs(nx=20, n_s=50, n_t=20, n_steps=50, dt=1e-3)
+    grid = system.TimeGrid(d.dt)
+    sys_ = system.LinearDynamicalSystem(a=d.a, b=d.b, c=d.c, x0=d.x0, input_signal=d.inputs,
+                                        constant_input=True)
+    bs = basis.BasisSet(phi_s=d.phi_s, temporal=d.temporal, n_mu=20)
+    srom = spatial.build_spatial_rom(sys_, bs, ref_mode="zero")
+    rom = spacetime.build_st_rom(srom, bs, grid, sys_.input_signal, True)
+    cap = d.a.shape[0] * len(d.dt)  # above the reference's verification cap (20,000 rows); SURVEY 8(d)
+    phi_st = spacetime.explicit_st_basis(bs, cap=cap)
+    a_st, f_st, x0_st = system.assemble_st(sys_, grid, cap=cap)
+    a_exp = phi_st.T @ (a_st @ phi_st)
+    f_exp = phi_st.T @ f_st
+    i_exp = phi_st.T @ x0_st
+    del phi_st
+    worst = max(np.max(np.abs(a_exp - rom.a_st_hat)), np.max(np.abs(f_exp - rom.f_st_hat)),
+                np.max(np.abs(i_exp - rom.x0_st_hat)))
+    print(f"cfg4 Kronecker instance: block vs explicit max-abs {worst:.3e}")
+    assert worst <= 1e-11
+    rng = np.random.default_rng(11)
+    m = a_exp.shape[0]
+    idx = rng.choice(m * m, size=20000, replace=False)
+    out = dict(a_nnz=np.array(d.a.nnz), a_datasum=np.array(d.a.data.sum()), phi_sum=np.array(d.phi_s.sum()),
+               a_hat=srom.a_hat, b_hat=srom.b_hat, x0_hat=srom.x0_hat,
+               sample_idx=idx.astype(np.int64),
+               a_exp_sample=a_exp.ravel()[idx], a_blk_sample=rom.a_st_hat.ravel()[idx],
+               a_exp_diag=np.diag(a_exp).copy(), a_exp_rowsum=a_exp.sum(axis=1), a_exp_colsum=a_exp.sum(axis=0),
+               a_exp_fro=np.array(np.linalg.norm(a_exp)), a_blk_fro=np.array(np.linalg.norm(rom.a_st_hat)),
+               f_exp=f_exp, i_exp=i_exp, f_blk=rom.f_st_hat, i_blk=rom.x0_st_hat,
+               x_st=spacetime.solve_st_rom(rom), worst_blk_vs_exp=np.array(worst))
+    _save("golden_cfg4_kron.npz", **out)
+
+
 def gen_persist():
     """A STROMMAT file written by the reference's persist.write_matrix (persist.py:35-48)."""
     from strom import persist
@@ -294,10 +332,14 @@ def gen_bounds():
 
 
 if __name__ == "__main__":
+    if "--only-kron" in sys.argv:
+        gen_cfg4_kron()
+        sys.exit(0)
     gen_linalg()
     gen_isvd_small()
     gen_cfg1()
     gen_blocks()
     gen_cfg4_small()
+    gen_cfg4_kron()
     gen_persist()
     gen_bounds()

@@ -1,0 +1,185 @@
+"""The headline configuration (BASELINE configs[1]) at full size.
+
+n_s = 2^20 rows x 500 snapshots of X = Q diag(10^(-i/8)) W^T + 1e-12 E from numpy
+default_rng(0) -- the same bytes bench.py times on both arms -- tol_svd = tol_sv =
+1e-9, r_max = 64 truncate.  At this size the fused pass gives each CTA ~111
+64-row tiles, so its shared-memory stage ring wraps (empty-mbarrier waits and
+phase flips) in every pass, which the smaller parity cases never reach.
+
+  (a) free run over all 500 columns (init on column 0, ingest_simulation of the
+      rest -- the pipelined two-stream path with its compactions) against the
+      batch SVD of X: sigma_0..15 relative <= 1e-10 (the modes
+      with sigma_i >= 1e-2 sigma_0), the leading-16 subspace against the true Q
+      to 1e-7 (the reference reaches 3.3e-8);
+  (b) P1 lock-step over snapshots 101-120 from the common start state (the
+      rank-64 truncated SVD of snapshots 1-100): each device update starts from
+      the oracle's previous state; decisions on non-noise steps, sigma <= 1e-10
+      and Phi columns <= 1e-8 on modes sigma_i >= 1e6 delta with gap >= 1e-3;
+  (c) the pipelined ingest of the same 20 snapshots from the same start against
+      the oracle's 20-update chain;
+  (d) 2^18 rows x 150 columns free-running against the oracle's own stream, with
+      r_max = 64 and with r_max = 24 (an append on every update: a compaction
+      every ~16 updates, so long compaction chains are compared too).
+Reference: basis.py:65-194 (isvd_init / isvd_update / ingest_simulation),
+verify.py:108-121 (the streamed-vs-batch check).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import strom_oracle as so
+from paper_1910_01260_b200 import _capi, basis, workloads as wl
+
+from helpers import align_columns, npy, principal_sine, sigma_rel
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+TOL = 1e-9
+RMAX = 64
+LOCK_STEPS = 20
+
+
+@pytest.fixture(scope="module")
+def cfg2():
+    x, q, _, s = wl.cfg2_stream_numpy()  # n x 500, Fortran order (columns contiguous)
+    return x, q, s
+
+
+@pytest.fixture(scope="module")
+def start_state(cfg2):
+    """The common start state of bench.py's two arms: rank-64 truncated SVD of columns 0-99."""
+    x = cfg2[0]
+    q, r = np.linalg.qr(x[:, :100])
+    w, s, vt = np.linalg.svd(r)
+    return dict(phi=np.ascontiguousarray(q @ w[:, :RMAX]), sigma=s[:RMAX].copy(),
+                v=np.ascontiguousarray(vt.T[:, :RMAX]), k=100)
+
+
+@pytest.fixture(scope="module")
+def oracle_chain(cfg2, start_state):
+    """The oracle's states after each of snapshots 101..120, with its decision records."""
+    x = cfg2[0]
+    st = so.OState(phi=start_state["phi"], sigma=start_state["sigma"], v=start_state["v"], k=start_state["k"],
+                   tol_svd=TOL, tol_sv=TOL, r_max=RMAX, cap_mode="truncate")
+    chain = [(st, None)]
+    for t in range(100, 100 + LOCK_STEPS):
+        d = so.Decision()
+        st = so.update(st, np.ascontiguousarray(x[:, t]), d)
+        chain.append((st, d))
+    return chain
+
+
+def _load(st):
+    return basis.SvdState(st.phi, st.sigma, st.v, st.k, TOL, tol_sv=TOL, r_max=RMAX, cap_mode="truncate",
+                          n_rejected=st.n_rejected, n_dependent=st.n_dependent, n_truncated=st.n_truncated,
+                          n_restarts=st.n_restarts)
+
+
+def test_free_run_all_500_vs_batch_svd(cuda, cfg2):
+    x, q, s_true = cfg2
+    xd = torch.as_tensor(x, device="cuda")
+    assert xd.stride() == (1, x.shape[0])  # column-major on the device, like the host array
+    st = basis.isvd_init(xd[:, 0], TOL, tol_sv=TOL, r_max=RMAX, cap_mode="truncate")
+    st = basis.ingest_simulation(st, xd[:, 1:])
+    assert st.k == 500 and st.rank == RMAX
+    s_dev = npy(st.sigma)
+    del xd
+    r = np.linalg.qr(x, mode="r")
+    s_batch = np.linalg.svd(r, compute_uv=False)
+    rel = sigma_rel(s_dev[:16], s_batch[:16])
+    rel_c = sigma_rel(s_dev[:16], s_true[:16])
+    print("cfg2 full free-run: sigma_0..15 rel vs batch max", rel.max(), "vs construction max", rel_c.max(),
+          "| counters dep", st.n_dependent, "trunc", st.n_truncated)
+    assert rel.max() <= 1e-10
+    # the construction's sigma differ from X's by the first-order noise term
+    # u_i^T E w_i ~ 1e-12 absolute (rel <= ~1e-10 at sigma_15 = 0.013)
+    assert rel_c.max() <= 2e-10
+    sine = principal_sine(npy(st.phi)[:, :16], q[:, :16])
+    print("leading-16 principal-angle sine vs the true Q", sine)
+    assert sine <= 1e-7
+
+
+def test_lockstep_101_to_120(cuda, cfg2, oracle_chain):
+    x = cfg2[0]
+    stats = dict(checked=0, noise=0, flips=0, modes=0, worst_sigma=0.0, worst_phi=0.0)
+    for i in range(1, len(oracle_chain)):
+        prev, _ = oracle_chain[i - 1]
+        nxt, dec = oracle_chain[i]
+        xt = np.ascontiguousarray(x[:, 99 + i])
+        got = basis.isvd_update(_load(prev), xt)
+        delta = np.sqrt(2 * np.finfo(float).eps) * np.linalg.norm(xt)
+        if dec.p > 10 * delta:
+            stats["checked"] += 1
+            same = (bool(got.last_flags & 1) == dec.dependent) and got.rank == nxt.rank
+            stats["flips"] += 0 if same else 1
+        else:
+            stats["noise"] += 1
+        assert got.rank == nxt.rank
+        s_ref, s_dev = nxt.sigma, npy(got.sigma)
+        gap = np.full(s_ref.size, np.inf)
+        dd = np.abs(np.diff(s_ref)) / s_ref[:-1]
+        gap[:-1] = np.minimum(gap[:-1], dd)
+        gap[1:] = np.minimum(gap[1:], dd)
+        sel = (s_ref >= 1e6 * delta) & (gap >= 1e-3)
+        stats["modes"] += int(sel.sum())
+        stats["worst_sigma"] = max(stats["worst_sigma"], float(np.max(sigma_rel(s_dev[sel], s_ref[sel]))))
+        phi = npy(got.phi)[:, sel]
+        pa, _ = align_columns(phi, nxt.phi[:, sel])
+        stats["worst_phi"] = max(stats["worst_phi"], float(np.max(np.abs(pa - nxt.phi[:, sel]))))
+    print("cfg2 full lock-step", stats)
+    assert stats["flips"] == 0
+    assert stats["modes"] >= 16 * LOCK_STEPS
+    assert stats["worst_sigma"] <= 1e-10
+    assert stats["worst_phi"] <= 1e-8
+
+
+def test_pipelined_ingest_vs_oracle_chain(cuda, cfg2, start_state, oracle_chain):
+    x = cfg2[0]
+    st0 = basis.SvdState(start_state["phi"], start_state["sigma"], start_state["v"], start_state["k"], TOL,
+                         tol_sv=TOL, r_max=RMAX, cap_mode="truncate")
+    cols = torch.as_tensor(x[:, 100:100 + LOCK_STEPS], device="cuda")
+    got = basis.ingest_simulation(st0, cols)
+    ref = oracle_chain[-1][0]
+    assert got.k == ref.k and got.rank == ref.rank
+    delta = np.sqrt(2 * np.finfo(float).eps) * np.linalg.norm(x[:, 100:100 + LOCK_STEPS], axis=0).max()
+    lead = ref.sigma >= 1e6 * delta
+    rel = sigma_rel(npy(got.sigma)[lead], ref.sigma[lead])
+    sine = principal_sine(npy(got.phi)[:, :16], ref.phi[:, :16])
+    print(f"cfg2 full pipelined 101-120 vs oracle: {int(lead.sum())} modes >= 1e6 delta, sigma rel max "
+          f"{rel.max():.3e}, leading-16 sine {sine:.3e}")
+    assert lead.sum() >= 16
+    assert rel.max() <= 1e-10
+    assert sine <= 1e-8
+
+
+def _compactions_during(fn):
+    lib = _capi.lib
+    lib.strom_profile_reset()
+    out = fn()
+    torch.cuda.synchronize()
+    pl = (_capi.i64 * 16)()
+    lib.strom_profile_read(16, pl, None, None)
+    return out, int(pl[6])  # P_TALL_GEMM: the compaction sweep (runtime.cuh ProfKind)
+
+
+@pytest.mark.parametrize("r_max", [64, 24])
+def test_quarter_size_free_run_vs_oracle(cuda, r_max):
+    x, _, _, _ = wl.cfg2_stream_numpy(n=1 << 18, cols=150)
+    xd = torch.as_tensor(x, device="cuda")
+
+    def run():
+        st = basis.isvd_init(xd[:, 0], TOL, tol_sv=TOL, r_max=r_max, cap_mode="truncate")
+        return basis.ingest_simulation(st, xd[:, 1:])
+
+    got, ncomp = _compactions_during(run)
+    ref = so.stream(x, TOL, tol_sv=TOL, r_max=r_max, cap_mode="truncate")
+    assert got.rank == ref.rank == r_max
+    rel = sigma_rel(npy(got.sigma)[:16], ref.sigma[:16])
+    sine = principal_sine(npy(got.phi)[:, :16], ref.phi[:, :16])
+    print(f"2^18 x 150, r_max {r_max}: {ncomp} compactions, sigma_0..15 rel max {rel.max():.3e}, "
+          f"leading-16 sine {sine:.3e}, dependent dev/ref {got.n_dependent}/{ref.n_dependent}")
+    assert rel.max() <= 1e-10
+    assert sine <= 1e-8
+    if r_max == 24:
+        assert ncomp >= 3

@@ -239,6 +239,32 @@ class TestCfg4:
         assert np.max(np.abs(npy(rom.a_st_hat) - g["a_exp"])) <= 1e-11
         assert max_rel(spacetime.solve_st_rom(rom), g["x_st"]) <= 1e-10
 
+    def test_kronecker_check_instance(self, cuda):
+        """BASELINE configs[3]'s stated check instance: 20^3 cells, N_t = 50, n_s = 50,
+        n_t = 20, against the reference's explicit Kronecker assembly
+        (spacetime.py:189-210, system.py:166-194, the verify.py:124-158 bar 1e-11)
+        stored as seeded samples + checksums (tests/golden/golden_cfg4_kron.npz)."""
+        g = load_golden("golden_cfg4_kron.npz")
+        d = wl.cfg4_inputs(nx=20, n_s=50, n_t=20, n_steps=50, dt=1e-3)
+        sys_ = LinearDynamicalSystem(a=d.a, b=d.b, c=d.c, x0=d.x0, input_signal=d.inputs, constant_input=True)
+        bs = BasisSet(d.phi_s, d.temporal, n_mu=20)
+        grid = TimeGrid(d.dt)
+        srom = spatial.build_spatial_rom(sys_, bs, ref_mode="zero")
+        for key in ("a_hat", "b_hat", "x0_hat"):
+            assert max_rel(getattr(srom, key), g[key]) <= 1e-12, key
+        rom = spacetime.build_st_rom(srom, bs, grid, sys_.input_signal, True)
+        a = npy(rom.a_st_hat)
+        idx = g["sample_idx"]
+        assert max_rel(a.ravel()[idx], g["a_blk_sample"]) <= 1e-12
+        assert np.max(np.abs(a.ravel()[idx] - g["a_exp_sample"])) <= 1e-11
+        assert np.max(np.abs(np.diag(a) - g["a_exp_diag"])) <= 1e-11
+        assert np.max(np.abs(a.sum(axis=1) - g["a_exp_rowsum"])) <= 1e-10
+        assert np.max(np.abs(a.sum(axis=0) - g["a_exp_colsum"])) <= 1e-10
+        assert abs(np.linalg.norm(a) - float(g["a_exp_fro"])) <= 1e-11 * float(g["a_exp_fro"])
+        assert np.max(np.abs(npy(rom.f_st_hat) - g["f_exp"])) <= 1e-11
+        assert np.max(np.abs(npy(rom.x0_st_hat) - g["i_exp"])) <= 1e-11
+        assert max_rel(spacetime.solve_st_rom(rom), g["x_st"]) <= 1e-10
+
     def test_full_size_vs_oracle(self, cuda):
         """BASELINE config 4 at full size (N = 10^6, n_s = 50, n_t = 20, N_t = 500)."""
         d = wl.cfg4_inputs()

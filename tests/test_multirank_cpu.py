@@ -59,7 +59,7 @@ def test_replica_timing_world2_gloo():
         assert (got_ws, got_rank) == (ws, rank)
         assert ms_max == 15.0  # max over ranks, identical everywhere
         assert rate == pytest.approx(400 * 5 * 2 / 0.015)  # whole-job units / slowest rank
-    assert len({r[5] for r in res}) == ws  # independent replica streams
+    assert {r[5] for r in res} == {0}  # every replica ingests the reference arm's stream (numpy seed 0)
 
 
 def test_reference_arm_rank_gating(monkeypatch, capsys):
@@ -75,3 +75,18 @@ def test_reference_arm_rank_gating(monkeypatch, capsys):
 
     assert bench.run_reference(A()) is None
     assert capsys.readouterr().out == ""
+
+
+def test_reference_arm_never_maps_the_library():
+    """The reference arm loads the numpy generators by path: neither the product
+    package nor libstrom_b200.so may enter the process (BENCH native_so_loaded)."""
+    import subprocess
+
+    code = ("import sys; sys.path.insert(0, %r); import bench; wl = bench._workloads(); "
+            "x, _, _, _ = wl.cfg2_stream_numpy(n=256, cols=8, rank=4); "
+            "from oracle import strom_oracle; "
+            "assert not any(m.startswith('paper_1910_01260_b200') for m in sys.modules), sorted(sys.modules); "
+            "maps = open('/proc/self/maps').read(); assert 'libstrom_b200' not in maps; print('clean')" % ROOT)
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    assert "clean" in out.stdout

@@ -193,3 +193,28 @@ class TestCfg4Small:
         assert np.max(np.abs(phi_st.T @ (a_x @ phi_st) - a_st)) <= 1e-11
         assert np.max(np.abs(phi_st.T @ f_x - f_st)) <= 1e-11
         assert np.max(np.abs(phi_st.T @ i_x - x0_st)) <= 1e-11
+
+
+class TestCfg4KroneckerInstance:
+    def test_baseline_check_instance(self):
+        """BASELINE configs[3]'s check instance (20^3 cells, N_t = 50, n_s = 50,
+        n_t = 20): the oracle's block assembly against the reference's explicit
+        Kronecker assembly (golden samples + checksums, make_golden.gen_cfg4_kron)."""
+        g = load_golden("golden_cfg4_kron.npz")
+        d = wl.cfg4_inputs(nx=20, n_s=50, n_t=20, n_steps=50, dt=1e-3)
+        assert d.a.nnz == int(g["a_nnz"]) == 7 * 20**3 - 6 * 20**2
+        assert float(d.a.data.sum()) == float(g["a_datasum"])
+        sr = so.spatial_rom(d.a, d.b, d.c, d.x0, d.phi_s, "zero")
+        _close(sr.a_hat, g["a_hat"]); _close(sr.b_hat, g["b_hat"]); _close(sr.x0_hat, g["x0_hat"])
+        a_st = so.st_matrix(sr.a_hat, d.temporal, d.dt)
+        f_st = so.st_input(sr.b_hat, d.temporal, d.dt, d.inputs, True)
+        x0_st = so.st_init(sr.x0_hat, d.temporal)
+        idx = g["sample_idx"]
+        _close(a_st.ravel()[idx], g["a_blk_sample"])
+        assert np.max(np.abs(a_st.ravel()[idx] - g["a_exp_sample"])) <= 1e-11
+        assert np.max(np.abs(np.diag(a_st) - g["a_exp_diag"])) <= 1e-11
+        assert np.max(np.abs(a_st.sum(axis=1) - g["a_exp_rowsum"])) <= 1e-10
+        assert np.max(np.abs(a_st.sum(axis=0) - g["a_exp_colsum"])) <= 1e-10
+        assert np.max(np.abs(f_st - g["f_exp"])) <= 1e-11
+        assert np.max(np.abs(x0_st - g["i_exp"])) <= 1e-11
+        _close(so.st_solve(a_st, f_st, x0_st), g["x_st"], 1e-11)
