@@ -719,6 +719,18 @@ def bench_cfg5(args, ncols=400, timed_from=100):
     return out
 
 
+def _guarded(name, fn, *a, **kw):
+    """Secondary measurements must not cost the primary line: a failure is
+    reported in its key (and on stderr) instead of aborting the run."""
+    try:
+        return fn(*a, **kw)
+    except Exception as e:  # noqa: BLE001
+        import traceback
+
+        traceback.print_exc()
+        return {"error": f"{name}: {type(e).__name__}: {e}"}
+
+
 def run_device(args):
     import torch
 
@@ -790,7 +802,7 @@ def run_device(args):
     seed0 = ctx["seed0"]
     ctx.pop("xd", None)
     if rank == 0 and ws == 1 and not args.no_seeds:
-        line["seeds"] = bench_isvd_seeds(args, ctx)
+        line["seeds"] = _guarded("seeds", bench_isvd_seeds, args, ctx)
     else:
         line["seeds"] = {"per_seed": [seed0]}
     del ctx
@@ -806,12 +818,12 @@ def run_device(args):
         line["st_build"] = st
         torch.cuda.empty_cache()
     if rank == 0 and not args.skip_extra:
-        line["cfg1"] = bench_cfg1(args, with_cpu=(ws == 1 and not args.no_cpu_baseline))
+        line["cfg1"] = _guarded("cfg1", bench_cfg1, args, with_cpu=(ws == 1 and not args.no_cpu_baseline))
         torch.cuda.empty_cache()
-        line["cfg3"] = bench_cfg3(args)
+        line["cfg3"] = _guarded("cfg3", bench_cfg3, args)
         torch.cuda.empty_cache()
         if not args.skip_cfg5:
-            line["cfg5"] = bench_cfg5(args)
+            line["cfg5"] = _guarded("cfg5", bench_cfg5, args)
             torch.cuda.empty_cache()
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -291,7 +291,7 @@ class HadamardStream:
     def _gen(self, coef, t0: int, nb: int, noise: float, out=None):
         import torch
 
-        from . import _capi as capi
+        from paper_1910_01260_b200 import _capi as capi  # absolute: bench.py loads this file by path
 
         if out is None:
             out = torch.empty((nb, self.n), dtype=torch.float64, device=self.device)
