@@ -17,6 +17,7 @@
 
 #include "../../include/strom_b200.h"
 #include "runtime.cuh"
+#include "dmma.cuh"
 #include "small_dense.cuh"
 
 using namespace strom;
@@ -575,8 +576,327 @@ __global__ void __launch_bounds__(1024) k_qr(double* M, int64_t ld, int rows, in
   cta_householder_qr(M, (int)ld, rows, cols, R, cols, work, work + cols, red);
 }
 
+// ---------------------------------------------------------------------------
+// Persistent dataflow LU (getrf semantics) with the right-hand sides riding
+// along as extra columns.  One CTA per 16-column block column of [A | B], held
+// in shared memory for the whole factorisation; CTAs hand work to each other
+// through release/acquire flags instead of kernel boundaries:
+//   block column j (A part): for k < j, when panel k is published, apply its
+//     row interchanges, U_kj = L_kk^{-1} A_kj and the trailing update
+//     A_ij -= L_ik U_kj on DMMA (m8n8k4); then factor its own panel (partial
+//     pivoting, first index on ties like idamax), publish it, and afterwards
+//     apply the later panels' interchanges to its L rows (dlaswp on the left
+//     columns) before the final write-back;
+//   B block columns: the same updates give L^{-1} P b (the forward solve of
+//     getrs), then the backward solve U x = y in the same CTA.
+// The critical path is the chain panel k -> update of block column k+1 ->
+// panel k+1: one flag hand-off per 16 columns instead of three launches.
+// Reference: linalg.py:75-99 (scipy lu_factor / lu_solve).
+// ---------------------------------------------------------------------------
+constexpr int kPlNb = 16;
+constexpr int kPlThreads = 512;
+constexpr int kPlWarps = kPlThreads / 32;
+
+struct PlArgs {
+  double* A;
+  int64_t lda;
+  double* B;
+  int64_t ldb;
+  int n, nrhs, nbA, ncb, ldS;
+  int* piv;
+  int* flag;  // [ncb] panel published (A blocks) / forward updates done (B blocks)
+  int* fin;   // [nbA] final write-back of an A block column done
+};
+
+__device__ __forceinline__ int pl_ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void pl_wait(const int* f) {
+  if (threadIdx.x == 0)
+    while (pl_ld_acquire(f) == 0) __nanosleep(20);
+  __syncthreads();
+}
+__device__ __forceinline__ void pl_signal(int* f) {
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(f), "r"(1) : "memory");
+}
+
+// S[lo:hi, 0:16] -= M[lo:hi, k0:k0+kw] * S[k0:k0+kw, 0:16]   (M global, read via L2)
+// DMMA m8n8k4: warp w takes 8-row tiles w, w + 16, ...; two 8-column n-tiles.
+__device__ inline void pl_gemm(double* S, int ld, const double* M, int64_t ldm, int lo, int hi, int k0, int kw) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+  double b[4][2];
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    const int kc = 4 * ks + t;
+    b[ks][0] = kc < kw ? S[g * ld + k0 + kc] : 0.0;
+    b[ks][1] = kc < kw ? S[(8 + g) * ld + k0 + kc] : 0.0;
+  }
+  for (int r0 = lo + 8 * wid; r0 < hi; r0 += 8 * kPlWarps) {
+    const int row = r0 + g;
+    const bool ok = row < hi;
+    double a[4];
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      const int kc = 4 * ks + t;
+      a[ks] = (ok && kc < kw) ? -__ldcg(M + (int64_t)(k0 + kc) * ldm + row) : 0.0;
+    }
+    double c00 = 0, c01 = 0, c10 = 0, c11 = 0;
+    if (ok) {
+      c00 = S[(2 * t) * ld + row];
+      c01 = S[(2 * t + 1) * ld + row];
+      c10 = S[(8 + 2 * t) * ld + row];
+      c11 = S[(9 + 2 * t) * ld + row];
+    }
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      dmma884(c00, c01, a[ks], b[ks][0]);
+      dmma884(c10, c11, a[ks], b[ks][1]);
+    }
+    if (ok) {
+      S[(2 * t) * ld + row] = c00;
+      S[(2 * t + 1) * ld + row] = c01;
+      S[(8 + 2 * t) * ld + row] = c10;
+      S[(9 + 2 * t) * ld + row] = c11;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kPlThreads, 1) k_lu_persistent(PlArgs a) {
+  extern __shared__ double S[];  // kPlNb columns x ldS rows (column-major)
+  __shared__ double sT[kPlNb][kPlNb + 1];
+  __shared__ double cval[kPlWarps];
+  __shared__ int cidx[kPlWarps];
+  const int j = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int n = a.n, ld = a.ldS;
+  const bool rhs = j >= a.nbA;
+  const int c0 = rhs ? (j - a.nbA) * kPlNb : j * kPlNb;
+  const int w = rhs ? min(kPlNb, a.nrhs - c0) : min(kPlNb, n - c0);
+  double* G = rhs ? a.B + (int64_t)c0 * a.ldb : a.A + (int64_t)c0 * a.lda;
+  const int64_t gld = rhs ? a.ldb : a.lda;
+  for (int idx = tid; idx < kPlNb * n; idx += kPlThreads) {
+    const int c = idx / n, r = idx - c * n;
+    S[c * ld + r] = c < w ? G[(int64_t)c * gld + r] : 0.0;
+  }
+  __syncthreads();
+  // ---- updates from the panels to the left
+  const int kend = rhs ? a.nbA : j;
+  for (int k = 0; k < kend; ++k) {
+    pl_wait(a.flag + k);
+    const int k0 = k * kPlNb, kw = min(kPlNb, n - k0);
+    if (tid < kPlNb) {  // this panel's row interchanges, in order (laswp)
+      for (int i = 0; i < kw; ++i) {
+        const int p = __ldcg(a.piv + k0 + i);
+        if (p != k0 + i) {
+          const double tmp = S[tid * ld + k0 + i];
+          S[tid * ld + k0 + i] = S[tid * ld + p];
+          S[tid * ld + p] = tmp;
+        }
+      }
+    }
+    for (int e = tid; e < kPlNb * kPlNb; e += kPlThreads) {  // L_kk (unit lower)
+      const int r = e % kPlNb, c = e / kPlNb;
+      sT[r][c] = (c < r && r < kw) ? __ldcg(a.A + (int64_t)(k0 + c) * a.lda + k0 + r) : 0.0;
+    }
+    __syncthreads();
+    if (tid < kPlNb) {  // U_kj = L_kk^{-1} A_kj, one column per thread
+      double x[kPlNb];
+#pragma unroll
+      for (int i = 0; i < kPlNb; ++i) x[i] = i < kw ? S[tid * ld + k0 + i] : 0.0;
+#pragma unroll
+      for (int i = 1; i < kPlNb; ++i)
+#pragma unroll
+        for (int q = 0; q < i; ++q) x[i] = fma(-sT[i][q], x[q], x[i]);
+#pragma unroll
+      for (int i = 0; i < kPlNb; ++i)
+        if (i < kw) S[tid * ld + k0 + i] = x[i];
+    }
+    __syncthreads();
+    pl_gemm(S, ld, a.A, a.lda, k0 + kw, n, k0, kw);
+    __syncthreads();
+  }
+  if (!rhs) {
+    // ---- factor this panel: rows j0.., columns 0..w-1; thread tid owns rows tid + 512 m
+    const int j0 = c0;
+    for (int c = 0; c < w; ++c) {
+      const int gr = j0 + c;
+      double best = -1.0;
+      int bi = 0x7fffffff;
+      for (int r = tid; r < n; r += kPlThreads)
+        if (r >= gr) {
+          const double v = fabs(S[c * ld + r]);
+          if (v > best) { best = v; bi = r; }
+        }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (lane == 0) { cval[wid] = best; cidx[wid] = bi; }
+      __syncthreads();
+      best = cval[0];
+      bi = cidx[0];
+#pragma unroll
+      for (int q = 1; q < kPlWarps; ++q) {
+        const double ob = cval[q];
+        const int oi = cidx[q];
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      const int p = (bi == 0x7fffffff) ? gr : bi;  // an all-NaN column pivots on itself
+      if (tid < kPlNb && p != gr) {
+        const double tmp = S[tid * ld + gr];
+        S[tid * ld + gr] = S[tid * ld + p];
+        S[tid * ld + p] = tmp;
+      }
+      if (tid == 0) a.piv[gr] = p;
+      __syncthreads();
+      const double d = S[c * ld + gr];
+      if (d != 0.0) {
+        const double inv = 1.0 / d;
+        for (int r = tid; r < n; r += kPlThreads)
+          if (r > gr) {
+            const double l = S[c * ld + r] * inv;
+            S[c * ld + r] = l;
+            for (int c2 = c + 1; c2 < w; ++c2) S[c2 * ld + r] = fma(-l, S[c2 * ld + gr], S[c2 * ld + r]);
+          }
+      }
+      // no trailing barrier: the next column's search reads only this thread's
+      // own rows; the pivot row it broadcasts is swapped before the next barrier
+    }
+    __syncthreads();
+    for (int idx = tid; idx < kPlNb * n; idx += kPlThreads) {
+      const int c = idx / n, r = idx - c * n;
+      if (c < w) G[(int64_t)c * gld + r] = S[c * ld + r];  // U blocks above, this panel's LU below
+    }
+    pl_signal(a.flag + j);
+    // ---- the later panels' interchanges reach this block column's L rows
+    for (int k = j + 1; k < a.nbA; ++k) {
+      pl_wait(a.flag + k);
+      const int k0 = k * kPlNb, kw = min(kPlNb, n - k0);
+      if (tid < w)
+        for (int i = 0; i < kw; ++i) {
+          const int p = __ldcg(a.piv + k0 + i);
+          if (p != k0 + i) {
+            const double tmp = S[tid * ld + k0 + i];
+            S[tid * ld + k0 + i] = S[tid * ld + p];
+            S[tid * ld + p] = tmp;
+          }
+        }
+    }
+    // every reader of this panel's L is done once all later block columns have
+    // published (A) or finished their forward updates (B)
+    for (int m = a.nbA; m < a.ncb; ++m) pl_wait(a.flag + m);
+    __syncthreads();
+    for (int idx = tid; idx < kPlNb * n; idx += kPlThreads) {
+      const int c = idx / n, r = idx - c * n;
+      if (c < w && r >= j0 + kPlNb) G[(int64_t)c * gld + r] = S[c * ld + r];
+    }
+    pl_signal(a.fin + j);
+    return;
+  }
+  // ---- right-hand sides: S = L^{-1} P B; now U X = S, block rows from the bottom
+  pl_signal(a.flag + j);
+  for (int m = 0; m < a.nbA; ++m) pl_wait(a.fin + m);
+  for (int J = a.nbA - 1; J >= 0; --J) {
+    const int b0 = J * kPlNb, bw = min(kPlNb, n - b0);
+    for (int e = tid; e < kPlNb * kPlNb; e += kPlThreads) {  // U_JJ (upper, with the diagonal)
+      const int r = e % kPlNb, c = e / kPlNb;
+      sT[r][c] = (r <= c && c < bw) ? __ldcg(a.A + (int64_t)(b0 + c) * a.lda + b0 + r) : 0.0;
+    }
+    __syncthreads();
+    if (tid < w) {
+      double x[kPlNb];
+#pragma unroll
+      for (int i = 0; i < kPlNb; ++i) x[i] = i < bw ? S[tid * ld + b0 + i] : 0.0;
+#pragma unroll
+      for (int i = kPlNb - 1; i >= 0; --i) {
+        if (i < bw) {
+#pragma unroll
+          for (int q = i + 1; q < kPlNb; ++q) x[i] = fma(-sT[i][q], x[q], x[i]);
+          x[i] = x[i] / sT[i][i];
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < kPlNb; ++i)
+        if (i < bw) S[tid * ld + b0 + i] = x[i];
+    }
+    __syncthreads();
+    pl_gemm(S, ld, a.A, a.lda, 0, b0, b0, bw);
+    __syncthreads();
+  }
+  for (int idx = tid; idx < kPlNb * n; idx += kPlThreads) {
+    const int c = idx / n, r = idx - c * n;
+    if (c < w) G[(int64_t)c * gld + r] = S[c * ld + r];
+  }
+}
+
+// Pivot-floor test of a stored factor: info[0] = first i with |U_ii| <= 1e-14
+// ||A||_F (or -1), info[1] = |U_ii|, info[2] = the floor (linalg.py:91-98).
+__global__ void __launch_bounds__(1024) k_lu_check(const double* A, int64_t ld, int n, const double* fro,
+                                                   double* info) {
+  __shared__ int s_bad;
+  if (threadIdx.x == 0) s_bad = 0x7fffffff;
+  __syncthreads();
+  const double floor = 1e-14 * fro[0];
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    if (fabs(A[(int64_t)i * ld + i]) <= floor) atomicMin(&s_bad, i);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    info[0] = (s_bad == 0x7fffffff) ? -1.0 : (double)s_bad;
+    info[1] = (s_bad == 0x7fffffff) ? 0.0 : fabs(A[(int64_t)s_bad * ld + s_bad]);
+    info[2] = floor;
+  }
+}
+
+size_t pl_smem(int n) { return (size_t)kPlNb * (((n + 7) & ~7) + 4) * 8; }
+
+// The persistent LU applies when every block column fits one co-resident CTA.
+bool pl_fits(int64_t n, int64_t nrhs) {
+  if (n < 1 || n > 4096 || nrhs < 0) return false;
+  const int64_t ncb = ceil_div(n, kPlNb) + ceil_div(nrhs, kPlNb);
+  const size_t smem = pl_smem((int)n);
+  if (smem > max_smem_optin()) return false;
+  static PerDevice<int> occ_cache;
+  int& occ = occ_cache.get();
+  static PerDevice<size_t> cfg;
+  if (cfg.get() < smem) {
+    STROM_CUDA(cudaFuncSetAttribute(k_lu_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cfg.get() = smem;
+  }
+  int o = 0;
+  STROM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_lu_persistent, kPlThreads, smem));
+  occ = o;
+  if (getenv("STROM_LU_LEGACY")) return false;
+  return (int64_t)o * sm_count() >= ncb;
+}
+
+// LU of A (and, with nrhs > 0, the solve A X = B in place) by the persistent kernel.
+void pl_run(int64_t n, double* A, int64_t lda, double* B, int64_t ldb, int64_t nrhs, int* piv, cudaStream_t s) {
+  const int nbA = (int)ceil_div(n, kPlNb);
+  const int ncb = nbA + (int)ceil_div(nrhs, kPlNb);
+  auto flags = dev_alloc((size_t)(ncb + nbA) * 4, s, true);
+  PlArgs a;
+  a.A = A; a.lda = lda; a.B = B; a.ldb = ldb;
+  a.n = (int)n; a.nrhs = (int)nrhs; a.nbA = nbA; a.ncb = ncb; a.ldS = (((int)n + 7) & ~7) + 4;
+  a.piv = piv;
+  a.flag = flags->as<int>();
+  a.fin = flags->as<int>() + ncb;
+  void* args[] = {&a};
+  ProfScope ps(P_LU, s);
+  STROM_CUDA(cudaLaunchCooperativeKernel((const void*)k_lu_persistent, dim3(ncb), dim3(kPlThreads), args,
+                                         pl_smem((int)n), s));
+}
+
 // Blocked right-looking LU with partial pivoting of the n x n column-major a (in place).
 void lu_factor(int64_t n, double* a_dev, int* piv, cudaStream_t s) {
+  if (pl_fits(n, 0)) {
+    pl_run(n, a_dev, n, nullptr, 0, 0, piv, s);
+    return;
+  }
   const bool reg_panel = n <= 1024;  // panel rows fit two per thread (512 threads) in registers
   const int step = reg_panel ? kNbReg : kNb;
   for (int64_t k0 = 0; k0 < n; k0 += step) {
@@ -669,8 +989,14 @@ int strom_dense_solve(int64_t n, double* a_dev, double* x_dev, int64_t nrhs, int
       k_fro_final<<<1, 256, 0, s>>>(fp->as<double>() + np, np, fro + 1);
       STROM_LAUNCH_CHECK();
     }
-    lu_factor(n, a_dev, piv, s);
-    lu_solve(n, a_dev, piv, x_dev, n, nrhs, fro, info, s);
+    if (pl_fits(n, nrhs)) {  // factor + forward + backward solve in one persistent launch
+      pl_run(n, a_dev, n, x_dev, n, nrhs, piv, s);
+      k_lu_check<<<1, 1024, 0, s>>>(a_dev, n, (int)n, fro, info);
+      STROM_LAUNCH_CHECK();
+    } else {
+      lu_factor(n, a_dev, piv, s);
+      lu_solve(n, a_dev, piv, x_dev, n, nrhs, fro, info, s);
+    }
     double h[3], nf[2];
     STROM_CUDA(cudaMemcpyAsync(h, info, 3 * 8, cudaMemcpyDeviceToHost, s));
     STROM_CUDA(cudaMemcpyAsync(nf, fro, 2 * 8, cudaMemcpyDeviceToHost, s));

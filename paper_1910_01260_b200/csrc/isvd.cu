@@ -593,7 +593,8 @@ void launch_compact_pass(const Store& src, const int32_t* base_dev, const int32_
   set_smem_attr(k_compact_pass<GB>, smem, &cfg.get());
   ProfScope ps(P_TALL_GEMM, s);
   k_compact_pass<GB><<<sm_count(), kCompactThreads, smem, s>>>(src.U(), src.ccap, base_dev, c_dev, r_dev, T, ldt,
-                                                               dst.U(), dst.ccap, src.ldu / kUTile, part, QP);
+                                                               dst.U(), dst.ccap, src.ldu / kUTile, part, QP,
+                                                               prof_dev_bytes());
   STROM_LAUNCH_CHECK();
 }
 

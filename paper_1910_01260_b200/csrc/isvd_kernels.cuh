@@ -1149,11 +1149,15 @@ __global__ void __launch_bounds__(kCompactThreads, 1) k_compact_pass(const doubl
                                                                      const int32_t* r_dev, const double* __restrict__ T,
                                                                      int64_t ldt, double* __restrict__ Unew,
                                                                      int64_t dst_ccap, int64_t ntiles,
-                                                                     double* __restrict__ part, int QP) {
+                                                                     double* __restrict__ part, int QP,
+                                                                     unsigned long long* prof) {
   extern __shared__ __align__(16) double csm[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int base = *base_dev, c = *c_dev, r = *r_dev;
+  // algorithmic bytes: read c live columns, write r new ones (ntiles * kUTile rows)
+  if (prof && blockIdx.x == 0 && threadIdx.x == 0)
+    atomicAdd(prof + 6, 8ull * (unsigned long long)(ntiles * kUTile) * (unsigned long long)(c + r));
   const int c4 = (c + 3) & ~3;   // K padded to the DMMA k-step
   const int RP = (r + 31) & ~31;  // C / G columns padded to 32-wide blocks
   // leading dimensions = 4 (mod 16) doubles: the 16 lanes of a half-warp that
