@@ -239,6 +239,13 @@ int strom_st_assemble(const double* ahat_dev, const double* psi_dev, const doubl
                       int32_t constant_input, const double* x0hat_dev, double* ast_dev, double* fst_dev,
                       double* x0st_dev, void* stream);
 
+/* reconstruct_states (spacetime.py:180-186; replaces its einsum + phi_s @ coeffs):
+ * out (N x nsteps, row-major, ldo) = phi (N x ns, column-major, ldphi) C with
+ * C[i, k] = sum_j psi[i, k, j] xhat[j*ns + i]; psi is the (ns, nsteps, nt)
+ * temporal stack, xhat the ns*nt space-time solution (index j*ns + i). */
+int strom_st_reconstruct(int64_t N, int64_t ns, int64_t nt, int64_t nsteps, const double* phi_dev, int64_t ldphi,
+                         const double* psi_dev, const double* xhat_dev, double* out_dev, int64_t ldo, void* stream);
+
 /* ------------------------------------------------------------------------
  * Dense kernels  (linalg.py:41-99)
  * ------------------------------------------------------------------------ */

@@ -70,6 +70,7 @@ _PROTOS = {
                                            vp]),
     # space-time assembly (spacetime.py:43-115)
     "strom_st_assemble": (C.c_int, [vp, vp, vp, i64, i64, i64, vp, i64, vp, i32, vp, vp, vp, vp, vp]),
+    "strom_st_reconstruct": (C.c_int, [i64, i64, i64, i64, vp, i64, vp, vp, vp, i64, vp]),
     # dense LU solve (linalg.py:75-99)
     "strom_dense_solve": (C.c_int, [i64, vp, vp, i64, vp, vp, vp]),
     # small SVD / QR on device (linalg.py:41-72)

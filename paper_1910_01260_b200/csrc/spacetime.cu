@@ -205,6 +205,91 @@ __global__ void __launch_bounds__(256) k_st_gemm(const double* __restrict__ F, c
 
 }  // namespace
 
+// ---------------------------------------------------------------------------
+// reconstruct_states (spacetime.py:180-186): X = Phi_s C with
+// C[i, k] = sum_j Psi_i[k, j] xhat[j n_s + i]  (n_s x N_t), the space-time
+// basis never formed.  At cfg4 (N = 10^6, n_s = 50, N_t = 500) the tall GEMM
+// is 50 GFlop against a 4 GB output: fp64 tensor-core bound, so it runs on
+// DMMA m8n8k4 -- 128-row x 64-column CTA tiles, 32 x 32 warp tiles, K = n_s
+// (padded to 4) in one shared-memory stage, the Phi tile kept while the CTA
+// walks its row block's column tiles; output written straight from the
+// accumulators (row-major, 16-byte pairs).
+// ---------------------------------------------------------------------------
+__global__ void k_rc_coeffs(const double* __restrict__ psi, const double* __restrict__ xhat, int ns, int nsteps,
+                            int nt, double* __restrict__ C) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)ns * nsteps) return;
+  const int i = (int)(idx / nsteps), k = (int)(idx % nsteps);
+  const double* ps = psi + ((int64_t)i * nsteps + k) * nt;
+  double acc = 0.0;
+  for (int j = 0; j < nt; ++j) acc = fma(ps[j], xhat[(int64_t)j * ns + i], acc);
+  C[(int64_t)i * nsteps + k] = acc;
+}
+
+constexpr int kRcRows = 128, kRcCols = 64, kRcThreads = 256;
+
+__global__ void __launch_bounds__(kRcThreads, 2) k_reconstruct(int64_t N, int ns, int nsteps,
+                                                               const double* __restrict__ phi, int64_t ldphi,
+                                                               const double* __restrict__ C,
+                                                               double* __restrict__ out, int64_t ldo) {
+  extern __shared__ __align__(16) double rsm[];
+  const int K4 = (ns + 3) & ~3;
+  constexpr int LA = kRcRows + 4, LB = kRcCols + 4;  // = 4 (mod 16): conflict-free fragment loads
+  double* As = rsm;                 // As[k * LA + r] = Phi[r0 + r, k]
+  double* Bs = As + (size_t)K4 * LA;  // Bs[k * LB + c] = C[k, c0 + c]
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, g = lane >> 2, t = lane & 3;
+  const int wm = wid & 3, wn = wid >> 2;  // warp tile: rows 32 wm.., columns 32 wn..
+  const bool pairs = (ldo % 2) == 0;
+  for (int64_t rb = blockIdx.x; rb * kRcRows < N; rb += gridDim.x) {
+    const int64_t r0 = rb * kRcRows;
+    __syncthreads();
+    for (int idx = tid; idx < K4 * kRcRows; idx += kRcThreads) {
+      const int k = idx / kRcRows, r = idx % kRcRows;
+      As[k * LA + r] = (k < ns && r0 + r < N) ? __ldg(phi + (int64_t)k * ldphi + r0 + r) : 0.0;
+    }
+    for (int c0 = 0; c0 < nsteps; c0 += kRcCols) {
+      __syncthreads();
+      for (int idx = tid; idx < K4 * kRcCols; idx += kRcThreads) {
+        const int k = idx / kRcCols, c = idx % kRcCols;
+        Bs[k * LB + c] = (k < ns && c0 + c < nsteps) ? __ldg(C + (int64_t)k * nsteps + c0 + c) : 0.0;
+      }
+      __syncthreads();
+      double acc[4][4][2];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+      for (int ks = 0; ks < K4; ks += 4) {
+        double fa[4], fb[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) fa[a] = As[(ks + t) * LA + 32 * wm + 8 * a + g];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) fb[b] = Bs[(ks + t) * LB + 32 * wn + 8 * b + g];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) dmma884(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const int64_t row = r0 + 32 * wm + 8 * a + g;
+        if (row >= N) continue;
+        double* orow = out + row * ldo;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int col = c0 + 32 * wn + 8 * b + 2 * t;
+          if (pairs && col + 1 < nsteps) {
+            __stcs(reinterpret_cast<double2*>(orow + col), make_double2(acc[a][b][0], acc[a][b][1]));
+          } else {
+            if (col < nsteps) orow[col] = acc[a][b][0];
+            if (col + 1 < nsteps) orow[col + 1] = acc[a][b][1];
+          }
+        }
+      }
+    }
+  }
+}
+
 extern "C" {
 
 // build_st_matrix / build_st_input / build_st_init (spacetime.py:43-115).
@@ -251,6 +336,38 @@ int strom_st_assemble(const double* ahat_dev, const double* psi_dev, const doubl
       k_st_gemm<<<(unsigned)(nb * (nb + 1) / 2), 256, 0, s>>>(F, Fd, kpad, (int)ns, (int)nt, ahat_dev, D, ast_dev);
       STROM_LAUNCH_CHECK();
     }
+  });
+}
+
+// reconstruct_states: out (N x N_t, row-major, ldo) = Phi_s C,
+// C[i, k] = sum_j psi[i, k, j] xhat[j n_s + i]; phi column-major (ldphi).
+int strom_st_reconstruct(int64_t N, int64_t ns, int64_t nt, int64_t nsteps, const double* phi_dev, int64_t ldphi,
+                         const double* psi_dev, const double* xhat_dev, double* out_dev, int64_t ldo, void* stream) {
+  return guarded([&] {
+    STROM_REQUIRE(N >= 1 && ns >= 1 && nt >= 1 && nsteps >= 1 && phi_dev && psi_dev && xhat_dev && out_dev,
+                  "bad reconstruct arguments");
+    STROM_REQUIRE(ldphi >= N && ldo >= nsteps, "bad leading dimensions");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    auto cbuf = dev_alloc((size_t)ns * nsteps * 8, s, false);
+    double* C = cbuf->as<double>();
+    ProfScope ps(P_ST_SMALL, s);
+    k_rc_coeffs<<<(unsigned)ceil_div(ns * nsteps, 256), 256, 0, s>>>(psi_dev, xhat_dev, (int)ns, (int)nsteps, (int)nt,
+                                                                     C);
+    STROM_LAUNCH_CHECK();
+    const int K4 = (int)((ns + 3) & ~3);
+    const size_t smem = (size_t)K4 * ((kRcRows + 4) + (kRcCols + 4)) * 8;
+    STROM_REQUIRE(smem <= max_smem_optin(), "reconstruct: n_s too large for one shared-memory K stage");
+    static PerDevice<size_t> cfg;
+    if (cfg.get() < smem) {
+      STROM_CUDA(cudaFuncSetAttribute(k_reconstruct, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      cfg.get() = smem;
+    }
+    int occ = 0;
+    STROM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_reconstruct, kRcThreads, smem));
+    const int64_t nrb = ceil_div(N, (int64_t)kRcRows);
+    const int grid = (int)std::min<int64_t>(nrb, (int64_t)sm_count() * std::max(occ, 1));
+    k_reconstruct<<<grid, kRcThreads, smem, s>>>(N, (int)ns, (int)nsteps, phi_dev, ldphi, C, out_dev, ldo);
+    STROM_LAUNCH_CHECK();
   });
 }
 

@@ -18,7 +18,7 @@ import torch
 
 from . import _capi as capi
 from . import linalg
-from ._tensors import F64, device, to_dev
+from ._tensors import F64, colmajor, device, to_dev
 from .basis import BasisSet
 from .errors import SingularMatrixError
 from .spatial import SpatialRom
@@ -136,11 +136,23 @@ def reconstruct_step(basis: BasisSet, x_hat_st, k: int) -> torch.Tensor:
 
 
 def reconstruct_states(basis: BasisSet, x_hat_st) -> torch.Tensor:
-    """Lift the reduced space-time solution at every step: N_s x N_t (spacetime.py:180-186)."""
-    x_hat_st = to_dev(x_hat_st)
-    blocks = x_hat_st.reshape(basis.n_t, basis.n_s)            # (n_t, n_s)
-    coeffs = torch.einsum("ikj,ji->ik", basis.temporal_stack(), blocks)  # (n_s, N_t)
-    return basis.phi_s @ coeffs
+    """Lift the reduced space-time solution at every step: N_s x N_t (spacetime.py:180-186).
+
+    One coefficient kernel (C = sum_j E^(j) xhat^(j), n_s x N_t) and one DMMA
+    tall GEMM Phi_s C (``strom_st_reconstruct``); the result is row-major like
+    the reference's array.
+    """
+    x_hat_st = to_dev(x_hat_st).contiguous()
+    ns, nt, nsteps = basis.n_s, basis.n_t, basis.n_steps
+    if x_hat_st.numel() != ns * nt:
+        raise ValueError(f"space-time solution has {x_hat_st.numel()} entries, expected n_s*n_t = {ns * nt}")
+    phi, ldphi = colmajor(basis.phi_s)
+    psi = basis.temporal_stack().contiguous()
+    n = phi.shape[0]
+    out = torch.empty((n, nsteps), dtype=F64, device=phi.device)
+    capi.call("strom_st_reconstruct", n, ns, nt, nsteps, phi.data_ptr(), ldphi, psi.data_ptr(),
+              x_hat_st.data_ptr(), out.data_ptr(), nsteps, capi.stream_ptr())
+    return out
 
 
 ST_VERIFICATION_CAP = 20_000  # system.py:23

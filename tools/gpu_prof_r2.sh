@@ -1,0 +1,31 @@
+#!/bin/bash
+# Round-2 ncu captures of every hot-path kernel (one capture each, after the
+# plain command has exited 0).  Usage: gpurun -- 'bash tools/gpu_prof_r2.sh TAG'
+tag=${1:-prof}
+out=gpurun_out/$tag
+mkdir -p $out
+run() {  # name, kernel regex, skip, count, command...
+  local name=$1 rx=$2 skip=$3 cnt=$4; shift 4
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"$rx" -s $skip -c $cnt \
+      -o $out/$name "$@" > $out/ncu_$name.log 2>&1
+  echo "$name rc=$?" >> $out/status.txt
+}
+timeout 600 python tools/profile_isvd.py --cols 150 > $out/plain_isvd.log 2>&1 && {
+  timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
+      --log-file $out/launches_isvd.csv python tools/profile_isvd.py --cols 40 > $out/ncu_launch.log 2>&1
+  run step_b 'k_step_b' 150 2 python tools/profile_isvd.py --cols 40
+  run decide 'k_decide' 300 3 python tools/profile_isvd.py --cols 40
+  run vupdate 'k_vupdate' 150 2 python tools/profile_isvd.py --cols 40
+  run pass 'k_pass' 230 2 python tools/profile_isvd.py --cols 40
+  run compact 'k_compact' 0 4 python tools/profile_isvd.py --cols 150
+}
+timeout 600 python tools/prof_targets.py st 2 > $out/plain_st.log 2>&1 && {
+  timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+      --log-file $out/launches_st.csv python tools/prof_targets.py st 1 > $out/ncu_launch_st.log 2>&1
+  run st_kernels 'k_st_|k_spatial_ell' 6 6 python tools/prof_targets.py st 2
+  run lu 'k_lu_persistent' 0 1 python tools/prof_targets.py st 1
+  run reconstruct 'k_reconstruct' 0 1 python tools/prof_targets.py st 1
+}
+timeout 600 python tools/prof_targets.py cfg1 2 > $out/plain_cfg1.log 2>&1 && \
+  run small_svd 'k_small_svd' 0 1 python tools/prof_targets.py cfg1 1
+echo done > $out/done
