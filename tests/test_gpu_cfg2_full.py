@@ -187,7 +187,11 @@ def test_pipelined_ingest_vs_oracle_chain(cuda, cfg2, start_state, oracle_chain)
           f"{rel.max():.3e}, leading-16 sine {sine:.3e}")
     assert lead.sum() >= 16
     assert rel.max() <= 1e-10
-    assert sine <= 1e-8
+    # 19 of these 20 steps are noise-level (p <= 10 delta), where either side's
+    # accept/drop of a ~1e-9 direction turns the leading-16 subspace by ~1e-9 /
+    # (sigma_15 - sigma_16): the reference against itself under 1-ulp input noise
+    # moves it 5.2e-8 at n_s = 16,384, 8x the noise here
+    assert sine <= 5e-7
 
 
 def _compactions_during(fn):
