@@ -626,6 +626,9 @@ __device__ __forceinline__ void pl_signal(int* f) {
 
 // S[lo:hi, 0:16] -= M[lo:hi, k0:k0+kw] * S[k0:k0+kw, 0:16]   (M global, read via L2)
 // DMMA m8n8k4: warp w takes 8-row tiles w, w + 16, ...; two 8-column n-tiles.
+// The M fragments of kPlBatch tiles are loaded before any of them is used, so
+// the L2 latency is paid once per batch, not once per tile.
+constexpr int kPlBatch = 4;
 __device__ inline void pl_gemm(double* S, int ld, const double* M, int64_t ldm, int lo, int hi, int k0, int kw) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
   double b[4][2];
@@ -635,32 +638,42 @@ __device__ inline void pl_gemm(double* S, int ld, const double* M, int64_t ldm, 
     b[ks][0] = kc < kw ? S[g * ld + k0 + kc] : 0.0;
     b[ks][1] = kc < kw ? S[(8 + g) * ld + k0 + kc] : 0.0;
   }
-  for (int r0 = lo + 8 * wid; r0 < hi; r0 += 8 * kPlWarps) {
-    const int row = r0 + g;
-    const bool ok = row < hi;
-    double a[4];
+  constexpr int kStride = 8 * kPlWarps;
+  for (int base = lo + 8 * wid; base < hi; base += kStride * kPlBatch) {
+    double a[kPlBatch][4];
 #pragma unroll
-    for (int ks = 0; ks < 4; ++ks) {
-      const int kc = 4 * ks + t;
-      a[ks] = (ok && kc < kw) ? -__ldcg(M + (int64_t)(k0 + kc) * ldm + row) : 0.0;
-    }
-    double c00 = 0, c01 = 0, c10 = 0, c11 = 0;
-    if (ok) {
-      c00 = S[(2 * t) * ld + row];
-      c01 = S[(2 * t + 1) * ld + row];
-      c10 = S[(8 + 2 * t) * ld + row];
-      c11 = S[(9 + 2 * t) * ld + row];
+    for (int q = 0; q < kPlBatch; ++q) {
+      const int row = base + q * kStride + g;
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        const int kc = 4 * ks + t;
+        a[q][ks] = (row < hi && kc < kw) ? -__ldcg(M + (int64_t)(k0 + kc) * ldm + row) : 0.0;
+      }
     }
 #pragma unroll
-    for (int ks = 0; ks < 4; ++ks) {
-      dmma884(c00, c01, a[ks], b[ks][0]);
-      dmma884(c10, c11, a[ks], b[ks][1]);
-    }
-    if (ok) {
-      S[(2 * t) * ld + row] = c00;
-      S[(2 * t + 1) * ld + row] = c01;
-      S[(8 + 2 * t) * ld + row] = c10;
-      S[(9 + 2 * t) * ld + row] = c11;
+    for (int q = 0; q < kPlBatch; ++q) {
+      const int r0 = base + q * kStride;
+      if (r0 >= hi) break;
+      const int row = r0 + g;
+      const bool ok = row < hi;
+      double c00 = 0, c01 = 0, c10 = 0, c11 = 0;
+      if (ok) {
+        c00 = S[(2 * t) * ld + row];
+        c01 = S[(2 * t + 1) * ld + row];
+        c10 = S[(8 + 2 * t) * ld + row];
+        c11 = S[(9 + 2 * t) * ld + row];
+      }
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        dmma884(c00, c01, a[q][ks], b[ks][0]);
+        dmma884(c10, c11, a[q][ks], b[ks][1]);
+      }
+      if (ok) {
+        S[(2 * t) * ld + row] = c00;
+        S[(2 * t + 1) * ld + row] = c01;
+        S[(8 + 2 * t) * ld + row] = c10;
+        S[(9 + 2 * t) * ld + row] = c11;
+      }
     }
   }
 }
@@ -670,6 +683,7 @@ __global__ void __launch_bounds__(kPlThreads, 1) k_lu_persistent(PlArgs a) {
   __shared__ double sT[kPlNb][kPlNb + 1];
   __shared__ double cval[kPlWarps];
   __shared__ int cidx[kPlWarps];
+  __shared__ int spiv[kPlNb];
   const int j = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int n = a.n, ld = a.ldS;
   const bool rhs = j >= a.nbA;
@@ -687,22 +701,24 @@ __global__ void __launch_bounds__(kPlThreads, 1) k_lu_persistent(PlArgs a) {
   for (int k = 0; k < kend; ++k) {
     pl_wait(a.flag + k);
     const int k0 = k * kPlNb, kw = min(kPlNb, n - k0);
+    if (tid < kPlNb) spiv[tid] = tid < kw ? __ldcg(a.piv + k0 + tid) : k0 + tid;
+    for (int e = tid; e < kPlNb * kPlNb; e += kPlThreads) {  // L_kk (unit lower)
+      const int r = e % kPlNb, c = e / kPlNb;
+      sT[r][c] = (c < r && r < kw) ? __ldcg(a.A + (int64_t)(k0 + c) * a.lda + k0 + r) : 0.0;
+    }
+    __syncthreads();
     if (tid < kPlNb) {  // this panel's row interchanges, in order (laswp)
       for (int i = 0; i < kw; ++i) {
-        const int p = __ldcg(a.piv + k0 + i);
+        const int p = spiv[i];
         if (p != k0 + i) {
           const double tmp = S[tid * ld + k0 + i];
           S[tid * ld + k0 + i] = S[tid * ld + p];
           S[tid * ld + p] = tmp;
         }
       }
+      // U_kj = L_kk^{-1} A_kj: the same thread's column, no barrier needed
     }
-    for (int e = tid; e < kPlNb * kPlNb; e += kPlThreads) {  // L_kk (unit lower)
-      const int r = e % kPlNb, c = e / kPlNb;
-      sT[r][c] = (c < r && r < kw) ? __ldcg(a.A + (int64_t)(k0 + c) * a.lda + k0 + r) : 0.0;
-    }
-    __syncthreads();
-    if (tid < kPlNb) {  // U_kj = L_kk^{-1} A_kj, one column per thread
+    if (tid < kPlNb) {
       double x[kPlNb];
 #pragma unroll
       for (int i = 0; i < kPlNb; ++i) x[i] = i < kw ? S[tid * ld + k0 + i] : 0.0;
@@ -738,12 +754,12 @@ __global__ void __launch_bounds__(kPlThreads, 1) k_lu_persistent(PlArgs a) {
       }
       if (lane == 0) { cval[wid] = best; cidx[wid] = bi; }
       __syncthreads();
-      best = cval[0];
-      bi = cidx[0];
+      best = cval[lane & (kPlWarps - 1)];
+      bi = cidx[lane & (kPlWarps - 1)];
 #pragma unroll
-      for (int q = 1; q < kPlWarps; ++q) {
-        const double ob = cval[q];
-        const int oi = cidx[q];
+      for (int o = kPlWarps / 2; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
         if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
       }
       const int p = (bi == 0x7fffffff) ? gr : bi;  // an all-NaN column pivots on itself
@@ -777,9 +793,11 @@ __global__ void __launch_bounds__(kPlThreads, 1) k_lu_persistent(PlArgs a) {
     for (int k = j + 1; k < a.nbA; ++k) {
       pl_wait(a.flag + k);
       const int k0 = k * kPlNb, kw = min(kPlNb, n - k0);
+      if (tid < kPlNb) spiv[tid] = tid < kw ? __ldcg(a.piv + k0 + tid) : k0 + tid;
+      __syncthreads();
       if (tid < w)
         for (int i = 0; i < kw; ++i) {
-          const int p = __ldcg(a.piv + k0 + i);
+          const int p = spiv[i];
           if (p != k0 + i) {
             const double tmp = S[tid * ld + k0 + i];
             S[tid * ld + k0 + i] = S[tid * ld + p];

@@ -16,6 +16,7 @@
 #include <algorithm>
 
 #include "../../include/strom_b200.h"
+#include "bulk.cuh"
 #include "dmma.cuh"
 #include "runtime.cuh"
 
@@ -228,6 +229,9 @@ __global__ void k_rc_coeffs(const double* __restrict__ psi, const double* __rest
 
 constexpr int kRcRows = 128, kRcCols = 64, kRcThreads = 256;
 
+// One CTA: a 128-row block of Phi (K4 x 128, one cp.async stage) against every
+// 64-column tile of C in turn (double-buffered cp.async stages, the next tile's
+// copy in flight while the current one is multiplied).
 __global__ void __launch_bounds__(kRcThreads, 2) k_reconstruct(int64_t N, int ns, int nsteps,
                                                                const double* __restrict__ phi, int64_t ldphi,
                                                                const double* __restrict__ C,
@@ -235,24 +239,35 @@ __global__ void __launch_bounds__(kRcThreads, 2) k_reconstruct(int64_t N, int ns
   extern __shared__ __align__(16) double rsm[];
   const int K4 = (ns + 3) & ~3;
   constexpr int LA = kRcRows + 4, LB = kRcCols + 4;  // = 4 (mod 16): conflict-free fragment loads
-  double* As = rsm;                 // As[k * LA + r] = Phi[r0 + r, k]
-  double* Bs = As + (size_t)K4 * LA;  // Bs[k * LB + c] = C[k, c0 + c]
+  double* As = rsm;                              // As[k * LA + r] = Phi[r0 + r, k]
+  double* Bs0 = As + (size_t)K4 * LA;             // Bs[k * LB + c] = C[k, c0 + c], two buffers
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, g = lane >> 2, t = lane & 3;
   const int wm = wid & 3, wn = wid >> 2;  // warp tile: rows 32 wm.., columns 32 wn..
   const bool pairs = (ldo % 2) == 0;
+  const int ntiles = (nsteps + kRcCols - 1) / kRcCols;
+  auto load_b = [&](double* Bs, int c0) {
+    for (int idx = tid; idx < K4 * kRcCols; idx += kRcThreads) {
+      const int k = idx / kRcCols, c = idx % kRcCols;
+      const bool ok = k < ns && c0 + c < nsteps;
+      cp_async8(Bs + k * LB + c, ok ? C + (int64_t)k * nsteps + c0 + c : C, ok);
+    }
+  };
   for (int64_t rb = blockIdx.x; rb * kRcRows < N; rb += gridDim.x) {
     const int64_t r0 = rb * kRcRows;
-    __syncthreads();
+    __syncthreads();  // the previous row block's last tile is consumed
     for (int idx = tid; idx < K4 * kRcRows; idx += kRcThreads) {
       const int k = idx / kRcRows, r = idx % kRcRows;
-      As[k * LA + r] = (k < ns && r0 + r < N) ? __ldg(phi + (int64_t)k * ldphi + r0 + r) : 0.0;
+      const bool ok = k < ns && r0 + r < N;
+      cp_async8(As + k * LA + r, ok ? phi + (int64_t)k * ldphi + r0 + r : phi, ok);
     }
-    for (int c0 = 0; c0 < nsteps; c0 += kRcCols) {
-      __syncthreads();
-      for (int idx = tid; idx < K4 * kRcCols; idx += kRcThreads) {
-        const int k = idx / kRcCols, c = idx % kRcCols;
-        Bs[k * LB + c] = (k < ns && c0 + c < nsteps) ? __ldg(C + (int64_t)k * nsteps + c0 + c) : 0.0;
-      }
+    load_b(Bs0, 0);
+    cp_async_commit();
+    for (int ct = 0; ct < ntiles; ++ct) {
+      const int c0 = ct * kRcCols;
+      double* Bs = Bs0 + (size_t)(ct & 1) * K4 * LB;
+      if (ct + 1 < ntiles) load_b(Bs0 + (size_t)((ct + 1) & 1) * K4 * LB, c0 + kRcCols);
+      cp_async_commit();
+      cp_async_wait<1>();  // everything but the copy just issued
       __syncthreads();
       double acc[4][4][2];
 #pragma unroll
@@ -270,6 +285,7 @@ __global__ void __launch_bounds__(kRcThreads, 2) k_reconstruct(int64_t N, int ns
 #pragma unroll
           for (int b = 0; b < 4; ++b) dmma884(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
       }
+      __syncthreads();  // this buffer may be refilled by the next iteration's copy
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
         const int64_t row = r0 + 32 * wm + 8 * a + g;
@@ -355,7 +371,7 @@ int strom_st_reconstruct(int64_t N, int64_t ns, int64_t nt, int64_t nsteps, cons
                                                                      C);
     STROM_LAUNCH_CHECK();
     const int K4 = (int)((ns + 3) & ~3);
-    const size_t smem = (size_t)K4 * ((kRcRows + 4) + (kRcCols + 4)) * 8;
+    const size_t smem = (size_t)K4 * ((kRcRows + 4) + 2 * (kRcCols + 4)) * 8;
     STROM_REQUIRE(smem <= max_smem_optin(), "reconstruct: n_s too large for one shared-memory K stage");
     static PerDevice<size_t> cfg;
     if (cfg.get() < smem) {

@@ -1,0 +1,45 @@
+"""Phase timestamps (clock64) inside k_step_b / the core SVD for steady-state cfg2
+updates (strom_debug_tprobe).  Prints the median cycles per phase.
+
+    python tools/tprobe_step_b.py [--cols 40]
+"""
+import argparse
+import sys
+
+sys.path.insert(0, '.')
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_1910_01260_b200 import _capi, basis, workloads as wl  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument('--cols', type=int, default=40)
+args = ap.parse_args()
+xt, _, _, _ = wl.cfg2_stream_torch(n=1 << 20, cols=100 + args.cols, rank=64, seed=0)
+st = basis.isvd_init(xt[0], 1e-9, tol_sv=1e-9, r_max=64, cap_mode='truncate')
+st = basis.ingest_simulation(st, xt[1:100].T)
+buf = torch.zeros(512, dtype=torch.int64, device='cuda')
+_capi.lib.strom_debug_tprobe(_capi.C.c_void_p(buf.data_ptr()))
+rows = []
+for t in range(100, 100 + args.cols):
+    buf.zero_()
+    st = basis.ingest_simulation(st, xt[t:t + 1].T)
+    torch.cuda.synchronize()
+    b = buf.cpu().numpy()
+    rows.append(b.copy())
+_capi.lib.strom_debug_tprobe(_capi.C.c_void_p(0))
+R = np.array(rows)
+names = {0: 'B0 start', 1: 'B1 setup', 2: 'B2 core svd', 3: 'B3', 4: 'B4 N update', 5: 'B5 drift', 6: 'B6 qr'}
+base = R[:, 0]
+print('step_b phases (cycles from B0, median over updates; QR count %d)' % int((R[:, 7] > 0).sum()))
+for k in range(1, 7):
+    ok = R[:, k] > 0
+    if ok.any():
+        print(f'  {names.get(k, k):14s} {np.median(R[ok, k] - base[ok]):10.0f}')
+print('core svd phases (cycles from CORE_TP(0))')
+c0 = R[:, 300]
+for k in range(301, 308):
+    ok = R[:, k] > 0
+    if ok.any():
+        print(f'  core {k - 300}: {np.median(R[ok, k] - c0[ok]):10.0f}')
+print('iterations slot 8..', np.median(R[:, 8:16], axis=0))
