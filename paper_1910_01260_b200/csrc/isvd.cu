@@ -14,6 +14,7 @@
 #include "../../include/strom_b200.h"
 #include "gram.cuh"
 #include "isvd_kernels.cuh"
+#include "isvd_window.cuh"
 #include "runtime.cuh"
 
 using namespace strom;
@@ -294,6 +295,14 @@ struct PipeMem {
   Pipe pp{};
   int32_t ccap = 0, rcap = 0;
   int pstride = 0, work_stride = 0, max_grid = 0;
+  // window mode: projections G (ldg x kWB), their Gram XX (kWB x kWB), the
+  // window pass's per-CTA partials, and a second V_bar (parity-buffered: the
+  // V update trails on its own stream)
+  double* wG = nullptr;
+  double* wXX = nullptr;
+  double* wpart = nullptr;
+  double* vbar2 = nullptr;
+  int ldg = 0, wpstride = 0;
 };
 
 PipeMem make_pipe(const Caps& c, cudaStream_t s) {
@@ -308,7 +317,11 @@ PipeMem make_pipe(const Caps& c, cudaStream_t s) {
                             (size_t)c.ccap * rc2;  // step B's layout (global fallback)
   const size_t nv = round_up(c.ccap + 2, 4), nell = round_up(rc2, 4);
   const size_t n_part = (size_t)m.max_grid * m.pstride;
-  size_t total = 2 * nell + 2 * nv + 7 * nv + 2 * (2 * nv + 8) + rc2 * rc2 + work_elems + (size_t)c.ccap * rc2 + n_part;
+  m.ldg = (int)round_up(c.ccap + 1, 8);
+  m.wpstride = (int)(round_up(c.ccap, 8) * kWB + kWB * kWB);
+  const size_t n_win = (size_t)m.ldg * kWB + kWB * kWB + (size_t)m.max_grid * m.wpstride + rc2 * rc2;
+  size_t total = 2 * nell + 2 * nv + 7 * nv + 2 * (2 * nv + 8) + rc2 * rc2 + work_elems + (size_t)c.ccap * rc2 + n_part +
+                 n_win;
   total = round_up(total, 32);
   const size_t bytes = total * 8 + 512;
   m.mem = dev_alloc(bytes, s, true);
@@ -332,11 +345,17 @@ PipeMem make_pipe(const Caps& c, cudaStream_t s) {
   m.pp.work = p; p += work_elems;
   m.pp.T = p; p += (size_t)c.ccap * rc2;
   m.pp.part = p; p += n_part;
+  m.wG = p; p += (size_t)m.ldg * kWB;
+  m.wXX = p; p += kWB * kWB;
+  m.wpart = p; p += (size_t)m.max_grid * m.wpstride;
+  m.vbar2 = p; p += rc2 * rc2;
   char* q = m.mem->as<char>() + total * 8;
   m.pp.ctl = reinterpret_cast<PipeCtl*>(q);
   m.pp.step[0] = reinterpret_cast<IsvdStep*>(q + 64);
   m.pp.step[1] = reinterpret_cast<IsvdStep*>(q + 192);
   m.pp.counter = reinterpret_cast<unsigned*>(q + 384);
+  m.pp.vrec[0] = reinterpret_cast<VRec*>(q + 416);
+  m.pp.vrec[1] = reinterpret_cast<VRec*>(q + 448);
   return m;
 }
 
@@ -361,6 +380,12 @@ IsvdParams make_params(const strom_isvd* h, const PipeMem& m, int64_t k_new, boo
   P.Li = h->store->Li();
   P.prof = prof_dev_bytes();
   P.tprobe = g_tprobe;
+  P.wG = nullptr;
+  P.wXX = nullptr;
+  P.ldg = 0;
+  P.wcol = 0;
+  P.wn = 0;
+  P.wpad = 0;
   return P;
 }
 
@@ -459,7 +484,7 @@ void launch_pass(int kind, int cols_ub, const strom_isvd* h, const PipeMem& m, c
   a.kind = kind;
   a.pstride = m.pstride;
   a.x = x;
-  a.coef = (kind == PASS_FUSED) ? m.pp.gt : (kind == PASS_SECOND ? m.pp.h : nullptr);
+  a.coef = (kind == PASS_FUSED || kind == PASS_RESID) ? m.pp.gt : (kind == PASS_SECOND ? m.pp.h : nullptr);
   a.xn = xn;
   a.out = (kind == PASS_SECOND) ? m.pp.ro : m.pp.fo;
   a.part = m.pp.part;
@@ -762,6 +787,125 @@ strom_isvd* update_once(strom_isvd* src, const double* x, cudaStream_t s, bool i
   dst->store->claimed = std::max(dst->store->claimed, dst->c_ub);
   dst->r_ub = std::min(cur->r_ub + 1, cur->caps.rcap);
   return dguard.release();
+}
+
+// ------------------------------------------------------------------ window-mode launchers
+// Window width in snapshots (STROM_WINDOW; 0 or 1 = the per-snapshot fused pass).
+int window_width() {
+  static const int v = [] {
+    const char* e = getenv("STROM_WINDOW");
+    const int w = e ? atoi(e) : kWB;
+    return std::max(0, std::min(kWB, w));
+  }();
+  return v;
+}
+
+size_t wproj_stage_bytes(int c) { return (size_t)(round_up(std::max(c, 1), 8) + kWB) * kWLd * 8; }
+
+template <int MT>
+void launch_wproj_t(const WprojArgs& a, int cols_ub, cudaStream_t s) {
+  const size_t per = wproj_stage_bytes(cols_ub);
+  const size_t budget = max_smem_optin() - 2048;
+  const int nst = (int)std::max<size_t>(1, std::min<size_t>(kWMaxStages, std::min<size_t>(3, budget / per)));
+  const size_t smem = (size_t)nst * per;
+  static PerDevice<size_t> cfg;
+  if (smem > cfg.get()) {
+    STROM_CUDA(cudaFuncSetAttribute(k_wproj<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cfg.get() = smem;
+  }
+  const int64_t ntiles = a.ldu / kStageRows;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, std::max(1, sm_count() - 1)));
+  ProfScope ps(P_WPROJ, s);
+  launch_pdl(k_wproj<MT>, dim3(grid), dim3(kWThreads), smem, s, a, nst);
+  STROM_LAUNCH_CHECK();
+}
+
+// G = U^T [x_w0 .. x_w0+nw-1], XX = their Gram; then the coefficients of the
+// window's first snapshot (k_prep_w).  cols_ub bounds the live U columns.
+void launch_window(const strom_isvd* h, const PipeMem& m, const double* const* xs, int nw, int cols_ub,
+                   const IsvdParams& P0, cudaStream_t s) {
+  WprojArgs a;
+  a.U = h->store->U();
+  a.ldu = h->ldu;
+  a.n = h->n;
+  a.ccap = h->store->ccap;
+  a.ctl = m.pp.ctl;
+  bool bulk = (h->n % 2 == 0);
+  for (int j = 0; j < kWB; ++j) {
+    a.xs[j] = j < nw ? xs[j] : nullptr;
+    if (j < nw && reinterpret_cast<uintptr_t>(xs[j]) % 16 != 0) bulk = false;
+  }
+  a.nw = nw;
+  a.xbulk = bulk ? 1 : 0;
+  a.part = m.wpart;
+  a.pstride = m.wpstride;
+  a.prof = prof_dev_bytes();
+  const int cu = std::max(cols_ub, 1);
+  const int mt = (int)ceil_div(ceil_div(cu, 8), kWConsumers);
+  switch (mt) {
+    case 1: launch_wproj_t<1>(a, cu, s); break;
+    case 2: launch_wproj_t<2>(a, cu, s); break;
+    case 3: launch_wproj_t<3>(a, cu, s); break;
+    default: launch_wproj_t<4>(a, cu, s); break;
+  }
+  const int64_t ntiles = h->ldu / kStageRows;
+  const int nparts = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, std::max(1, sm_count() - 1)));
+  const int nout = (int)(round_up(cu, 8) * kWB + kWB * kWB);
+  launch_pdl(k_wreduce, dim3((unsigned)ceil_div(nout, 32)), dim3(256), 0, s, (const double*)m.wpart, nparts,
+             m.wpstride, (const PipeCtl*)m.pp.ctl, nw, m.wG, m.ldg, m.wXX);
+  STROM_LAUNCH_CHECK();
+  IsvdParams P = P0;
+  P.wG = m.wG;
+  P.wXX = m.wXX;
+  P.ldg = m.ldg;
+  P.wn = nw;
+  P.wcol = -1;  // "next" = column 0
+  P.has_next = 1;
+  Pipe pp = m.pp;
+  pp.fo.gn = m.wG;
+  static PerDevice<size_t> cfg;
+  const size_t smem = decide_smem(m);
+  set_smem_attr(k_prep_w, smem, &cfg.get());
+  ProfScope ps(P_STEP_A, s);
+  launch_pdl(k_prep_w, dim3(1), dim3(kDecideThreads), smem, s, pp, P);
+  STROM_LAUNCH_CHECK();
+}
+
+void launch_decide_w(int which, const StateView& src, const Pipe& pp, const PipeMem& m, const IsvdParams& P,
+                     cudaStream_t s) {
+  static PerDevice<size_t> cfga, cfgb, cfg2;
+  const size_t smem = decide_smem(m);
+  ProfScope ps(P_STEP_A, s);
+  if (which == 0) {
+    set_smem_attr(k_decide_a, smem, &cfga.get());
+    launch_pdl(k_decide_a, dim3(1), dim3(kDecideThreads), smem, s, src, pp, P);
+  } else if (which == 1) {
+    set_smem_attr(k_decide_b, smem, &cfgb.get());
+    launch_pdl(k_decide_b, dim3(1), dim3(kDecideThreads), smem, s, src, pp, P);
+  } else {
+    set_smem_attr(k_decide2, smem, &cfg2.get());
+    launch_pdl(k_decide2, dim3(1), dim3(kDecideThreads), smem, s, src, pp, P);
+  }
+  STROM_LAUNCH_CHECK();
+}
+
+void launch_step_b_pp(const StateView& src, const StateView& dst, const Pipe& pp, const IsvdParams& P,
+                      const Caps& caps, cudaStream_t s) {
+  int use_smem = 0;
+  const size_t smem = small_kernel_smem(caps, &use_smem);
+  static PerDevice<size_t> cfg;
+  set_smem_attr(k_step_b, smem, &cfg.get());
+  ProfScope ps(P_STEP_B, s);
+  k_step_b<<<1, kSmallThreads, smem, s>>>(src, dst, pp, P, use_smem);
+  STROM_LAUNCH_CHECK();
+}
+
+void launch_vupdate_pp(const StateView& src, const StateView& dst, const Pipe& pp, const IsvdParams& P, int rcap,
+                       cudaStream_t s) {
+  dim3 grid((unsigned)ceil_div(P.k_new, kVRows), (unsigned)ceil_div(rcap + 1, kVCols));
+  ProfScope ps(P_VUPDATE, s);
+  k_vupdate<<<grid, kVRows, (size_t)(rcap + 2) * kVCols * 8, s>>>(src, dst, pp, P);
+  STROM_LAUNCH_CHECK();
 }
 
 // ------------------------------------------------------------------ ingestion
@@ -1112,6 +1256,156 @@ strom_isvd* ingest_pipelined(strom_isvd* src, ColumnSource& cols, cudaStream_t s
   return out;
 }
 
+// Window-mode ingestion: per window of up to kWB
+// snapshots one projection pass G = U^T X_w (k_wproj); per snapshot t
+//   s : k_decide_a(t) -> PASS_RESID(t) [no-op when dependent] -> k_decide_b(t)
+//       -> PASS_SECOND(t) [rare] -> k_decide2(t)
+//   s2: k_step_b(t): the core SVD as soon as k_decide_a(t) is done (overlapping
+//       the residual pass), the N update after k_decide2(t)
+//   s3: k_vupdate(t) (off the critical path; V_bar and its record are
+//       parity-buffered, k_step_b(t+2) waits for k_vupdate(t))
+// Every decision stays on the device; the host only orders the launches.
+strom_isvd* ingest_windowed(strom_isvd* src, ColumnSource& cols, cudaStream_t s, int wb) {
+  const int64_t ncols = cols.ncols;
+  cudaStream_t s2 = acquire_stream(), s3 = acquire_stream();
+  cudaEvent_t evB = acquire_event(), evJ = acquire_event(), evJ3 = acquire_event();
+  cudaEvent_t evU[2] = {acquire_event(), acquire_event()};
+  bool u_pending[2] = {false, false};
+  STROM_CUDA(cudaEventRecord(evJ, s));
+  STROM_CUDA(cudaStreamWaitEvent(s2, evJ, 0));
+  STROM_CUDA(cudaStreamWaitEvent(s3, evJ, 0));
+  std::unique_ptr<strom_isvd> slot[2];
+  std::unique_ptr<strom_isvd> hold;
+  strom_isvd* prev = src;
+  const int64_t kfinal = src->k + ncols;
+  PipeMem m;
+  bool need_init = true;
+  int64_t w0 = 0, wn = 0;
+  int64_t b_launched = 0, d_launched = 0;
+  bool fresh_alloc = false;
+  auto join = [&]() {  // s waits for all of s2 and s3
+    STROM_CUDA(cudaEventRecord(evJ, s2));
+    STROM_CUDA(cudaStreamWaitEvent(s, evJ, 0));
+    STROM_CUDA(cudaEventRecord(evJ3, s3));
+    STROM_CUDA(cudaStreamWaitEvent(s, evJ3, 0));
+  };
+  for (int64_t t = 0; t < ncols; ++t) {
+    {
+      const bool rank_hit = prev->r_max < 0 && prev->r_ub + 1 > prev->caps.rcap && prev->caps.rcap < prev->n;
+      const bool col_hit = prev->c_ub + 1 > prev->caps.ccap;
+      if (rank_hit || col_hit) {
+        join();
+        std::unique_ptr<strom_isvd> h2;
+        strom_isvd* nx = ensure_capacity(prev, &h2, s);
+        if (nx != prev) {
+          hold = std::move(h2);
+          prev = nx;
+          need_init = true;
+        }
+        fresh_alloc = true;  // s2 / s3 may not run ahead of the compaction
+      }
+    }
+    if (t == 0 && prev->store->claimed != prev->c_ub) {
+      std::shared_ptr<Store> st = successor_store(prev, s);
+      auto* cp = new strom_isvd(*prev);
+      set_store(cp, st);
+      hold.reset(cp);
+      prev = cp;
+    }
+    std::unique_ptr<strom_isvd>& dslot = slot[t & 1];
+    if (!dslot || dslot->caps.rcap != prev->caps.rcap || dslot->caps.ccap != prev->caps.ccap) {
+      Caps nc = prev->caps;
+      nc.kcap = std::max<int64_t>(prev->caps.kcap, round_up(kfinal, 64));
+      if (dslot) join();
+      dslot.reset(new_like(prev, nc));
+      alloc_small(dslot.get(), s);
+      alloc_v(dslot.get(), s);
+      fresh_alloc = true;
+    }
+    strom_isvd* dst = dslot.get();
+    dst->k = prev->k + 1;
+    set_store(dst, prev->store);
+    if (!m.mem || m.ccap != prev->caps.ccap || m.rcap != prev->caps.rcap) {
+      join();
+      m = make_pipe(prev->caps, s);
+      need_init = true;
+      fresh_alloc = true;
+    }
+    const int cols_ub = prev->c_ub;
+    IsvdParams P = make_params(dst, m, dst->k, false);
+    P.parity = (int)(t & 1);
+    if (need_init) {
+      join();  // prev's header comes from s2; the counters restart
+      k_init_ctl<<<1, 1, 0, s>>>(m.pp.ctl, prev->view.hdr);
+      STROM_LAUNCH_CHECK();
+      b_launched = 0;
+      d_launched = 0;
+      fresh_alloc = true;
+      wn = 0;  // a new window (U may have changed under the old one)
+      need_init = false;
+    }
+    if (t >= w0 + wn) {
+      w0 = t;
+      wn = std::min<int64_t>(wb, ncols - t);
+      const double* xs[kWB];
+      for (int j = 0; j < wn; ++j) xs[j] = cols.col(t + j);
+      launch_window(dst, m, xs, (int)wn, cols_ub, P, s);
+    }
+    if (fresh_alloc) {
+      STROM_CUDA(cudaEventRecord(evJ, s));
+      STROM_CUDA(cudaStreamWaitEvent(s2, evJ, 0));
+      STROM_CUDA(cudaStreamWaitEvent(s3, evJ, 0));
+      fresh_alloc = false;
+    }
+    P.wG = m.wG;
+    P.wXX = m.wXX;
+    P.ldg = m.ldg;
+    P.wn = (int)wn;
+    P.wcol = (int)(t - w0);
+    P.has_next = (P.wcol + 1 < P.wn) ? 1 : 0;
+    P.b_expect = -1;
+    P.d_expect = (int32_t)(d_launched + 1);
+    Pipe pp = m.pp;
+    pp.fo.gn = m.wG + (int64_t)(P.has_next ? P.wcol + 1 : 0) * m.ldg;
+    pp.vbar = (t & 1) ? m.vbar2 : m.pp.vbar;
+    const double* xt = cols.col(t);
+    if (b_launched > 0) STROM_CUDA(cudaStreamWaitEvent(s, evB, 0));  // k_step_b(t-1) wrote N, sigma
+    launch_decide_w(0, prev->view, pp, m, P, s);
+    launch_pass(PASS_RESID, cols_ub, dst, m, xt, nullptr, 1, s);
+    launch_decide_w(1, prev->view, pp, m, P, s);
+    launch_pass(PASS_SECOND, cols_ub, dst, m, xt, nullptr, 1, s);
+    launch_decide_w(2, prev->view, pp, m, P, s);
+    ++d_launched;
+    cols.release(t);
+    // s2: the core step (V_bar[t & 1] is free once k_vupdate(t - 2) is done)
+    if (u_pending[t & 1]) STROM_CUDA(cudaStreamWaitEvent(s2, evU[t & 1], 0));
+    launch_step_b_pp(prev->view, dst->view, pp, P, prev->caps, s2);
+    ++b_launched;
+    STROM_CUDA(cudaEventRecord(evB, s2));
+    // s3: the V update
+    STROM_CUDA(cudaStreamWaitEvent(s3, evB, 0));
+    launch_vupdate_pp(prev->view, dst->view, pp, P, prev->caps.rcap, s3);
+    STROM_CUDA(cudaEventRecord(evU[t & 1], s3));
+    u_pending[t & 1] = true;
+    dst->c_ub = prev->c_ub + 1;
+    dst->store->claimed = std::max(dst->store->claimed, dst->c_ub);
+    dst->r_ub = std::min(prev->r_ub + 1, prev->caps.rcap);
+    prev = dst;
+  }
+  join();
+  strom_isvd* out = slot[(ncols - 1) & 1].release();
+  STROM_CUDA(cudaStreamSynchronize(s2));
+  STROM_CUDA(cudaStreamSynchronize(s3));
+  release_event(evB);
+  release_event(evJ);
+  release_event(evJ3);
+  release_event(evU[0]);
+  release_event(evU[1]);
+  release_stream(s2);
+  release_stream(s3);
+  return out;
+}
+
 strom_isvd* init_state(int64_t n, const double* x, int64_t k, double tol_svd, double tol_sv, int64_t r_max,
                        int32_t cap_mode, cudaStream_t s) {
   STROM_REQUIRE(n >= 1, "need n >= 1");
@@ -1170,7 +1464,8 @@ int strom_isvd_ingest(strom_isvd* src, const double* X, int64_t ldx, int64_t nco
     cols.open(X, ldx, src->n, ncols, x_on_host != 0, s);
     strom_isvd* res = nullptr;
     try {
-      res = ingest_pipelined(src, cols, s);
+      const int wb = window_width();
+      res = wb > 1 ? ingest_windowed(src, cols, s, wb) : ingest_pipelined(src, cols, s);
     } catch (...) {
       cols.close();
       throw;

@@ -57,6 +57,8 @@ struct PipeCtl {
   int32_t reorth;   // 0 none, 1 DGKS pass requested, 2 restart copy requested
   int32_t bdone;    // core steps (k_step_b) completed since the sequence started
   int32_t decided;  // decision chains (k_decide + k_decide2) completed since then
+  int32_t resid;    // window mode: the residual pass of this snapshot is needed
+  int32_t adone;    // window mode: first-half decisions (k_decide_a) completed
   int32_t pad;
   double xx;        // x.x of the snapshot about to be decided
 };
@@ -96,9 +98,16 @@ struct PassOut {
   double* scal;
 };
 
+// What k_vupdate needs from k_step_b, in a record of its own: in window mode
+// the V update runs on a third stream and may trail the decisions.
+struct VRec {
+  int32_t mode, m, mkeep, pad;
+};
+
 struct Pipe {
   PipeCtl* ctl;
   IsvdStep* step[2];
+  VRec* vrec[2];
   double* ell[2];  // r_cap + 2: Phi^T x
   double* nj[2];   // c_cap + 1: the new N column (x - Phi ell)/p in Q_U coordinates
   double* tvec;    // L^{-1} g: x's coordinates in Q_U
@@ -145,7 +154,20 @@ struct IsvdParams {
   double* Li;
   unsigned long long* prof;  // device byte counters (runtime.cuh ProfKind) or null
   long long* tprobe;         // phase timestamps of step B (diagnostics) or null
+  // window mode (wn > 0): projections of the window's snapshots onto U,
+  // G[i + j ldg] = U_i . x_j (logical columns i), and their Gram XX[i kWB + j];
+  // wcol is this snapshot's column.  pp.fo.gn then points at column wcol + 1.
+  double* wG;
+  const double* wXX;
+  int32_t ldg, wcol, wn, wpad;
 };
+
+constexpr int kWB = 8;  // window width: snapshots projected by one pass over U
+
+// x.x of the next snapshot: the pass's scal[1], or the window Gram's diagonal
+__device__ __forceinline__ double next_xx(const IsvdParams& P, const Pipe& pp) {
+  return P.wn > 0 ? P.wXX[(P.wcol + 1) * (kWB + 1)] : pp.fo.scal[1];
+}
 
 // Programmatic dependent launch: let the next kernel of the stream launch now
 // (it waits for us itself), and wait for the previous one before reading its
@@ -202,7 +224,9 @@ __device__ inline bool last_cta_arrives(unsigned* counter, int* s_is_last) {
 // column dots stay in registers until a deterministic last-CTA reduction.
 // Reference: basis.py:135-139 (projection, Pythagorean p) and 150-156 (j).
 // ---------------------------------------------------------------------------
-enum : int32_t { PASS_PROJ = 0, PASS_FUSED = 1, PASS_SECOND = 2 };
+enum : int32_t { PASS_PROJ = 0, PASS_FUSED = 1, PASS_SECOND = 2, PASS_RESID = 3 };
+// PASS_RESID (window mode): FUSED without the next projection, and only when
+// k_decide_a found the snapshot independent (ctl->resid); a no-op otherwise.
 
 struct PassArgs {
   double* U;  // row-tiled store (kUTile-row tiles of ccap column segments)
@@ -267,7 +291,7 @@ __device__ inline void prep_next(const IsvdParams& P, const Pipe& pp, double* pa
     cta_gemv_cm<8>(Lib, P.ccap, c, c, pp.fo.gn, 1.0, nullptr, pp.tvec, part, true);
     cta_gemv_t_cm(Lib, P.ccap, c, c, pp.tvec, pp.gt, true);
   }
-  if (threadIdx.x == 0) pp.ctl->xx = pp.fo.scal[1];
+  if (threadIdx.x == 0) pp.ctl->xx = next_xx(P, pp);
 }
 
 // A (first snapshot of a sequence, or after a compaction): prepare from a PROJ pass.
@@ -284,9 +308,30 @@ __global__ void k_init_ctl(PipeCtl* ctl, const IsvdHdr* h) {
   ctl->reorth = 0;
   ctl->bdone = 0;
   ctl->decided = 0;
+  ctl->resid = 0;
+  ctl->adone = 0;
 }
 
 constexpr double kFoldTau = 1e-3;  // append r1 only if its out-of-span part is >= tau |r1|
+
+// Window mode: row `row` of the window projections for the snapshots after
+// this one, for a U column r = x_t - U (coef + coef2) (coef null: r = x_t):
+//   G[row, j] = x_t . x_j - (coef + coef2)^T G[:c, j]      (j = wcol+1 .. wn-1)
+// -- the same quantity the per-snapshot pass measured as r . x_next, from the
+// window's Gram instead of another read of U.  One warp per window column.
+__device__ inline void window_row(const IsvdParams& P, int row, int c, const double* coef, const double* coef2) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  for (int j = P.wcol + 1 + wid; j < P.wn; j += nw) {
+    double* gcol = P.wG + (int64_t)j * P.ldg;
+    double s = 0.0;
+    if (coef)
+      for (int i = lane; i < c; i += 32) s = fma(coef[i] + (coef2 ? coef2[i] : 0.0), gcol[i], s);
+    s = warp_sum(s);
+    if (lane == 0) gcol[row] = P.wXX[P.wcol * kWB + j] - s;
+  }
+  __syncthreads();
+}
 
 // ---------------------------------------------------------------------------
 // D: every decision of update t (basis.py:112-139 and the U bookkeeping):
@@ -429,7 +474,7 @@ __device__ inline void decide_body(const StateView& src, const Pipe& pp, const I
   }
   if (reorth == 0 && P.has_next) {
     if (prepped) {
-      if (threadIdx.x == 0) pp.ctl->xx = pp.fo.scal[1];
+      if (threadIdx.x == 0) pp.ctl->xx = next_xx(P, pp);
     } else {
       prep_next(P, pp, part);
     }
@@ -470,6 +515,9 @@ __device__ inline void decide2_body(const StateView& src, const Pipe& pp, const 
   double lam = 0.0;
   if (ro == 1) {
     const double p = st->p;
+    // window mode: the row of r2 = x - U (gt + h) for the rest of the window,
+    // before h is reused (harmless if r2 is not appended: c does not grow)
+    if (P.wn > 0) window_row(P, c, c, pp.gt, pp.h);
     double* l2 = pp.h;  // h is spent
     cta_gemv_cm<8>(Lib, ldl, c, c, pp.ro.e, 1.0, nullptr, l2, part, true);
     double pq = 0.0;
@@ -482,7 +530,7 @@ __device__ inline void decide2_body(const StateView& src, const Pipe& pp, const 
       append_factor_row(Lb, Lib, ldl, c, l2, lam, pp.tmp);
       for (int a = threadIdx.x; a <= c; a += blockDim.x)
         nj[a] = (a < c) ? (pp.y[a] + pp.l1[a] + l2[a]) / p : lam / p;
-      if (threadIdx.x == 0) pp.fo.gn[c] = pp.ro.scal[2];  // r2 . x_next
+      if (P.wn == 0 && threadIdx.x == 0) pp.fo.gn[c] = pp.ro.scal[2];  // r2 . x_next
       cn = c + 1;
       action = 1;
     } else if (c >= r + 1) {
@@ -493,10 +541,11 @@ __device__ inline void decide2_body(const StateView& src, const Pipe& pp, const 
     }
   } else {
     lam = sqrt(pp.ro.scal[0]);
+    if (P.wn > 0) window_row(P, 0, 0, nullptr, nullptr);  // U = [x]: row 0 = x . x_j
     if (threadIdx.x == 0) {
       P.L[(int64_t)slot * (ldl + 1)] = lam;
       P.Li[(int64_t)slot * (ldl + 1)] = 1.0 / lam;
-      pp.fo.gn[0] = pp.ro.scal[2];  // x . x_next
+      if (P.wn == 0) pp.fo.gn[0] = pp.ro.scal[2];  // x . x_next
       st->rho2 = pp.ro.scal[0];
     }
     cn = 1;
@@ -523,6 +572,204 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide2(StateView src, Pipe 
   pdl_enter();
   decide2_body(src, pp, P, part, red);
   signal_counter(&pp.ctl->decided);  // the decisions of this snapshot are complete
+}
+
+// ---------------------------------------------------------------------------
+// Window mode: the decisions of update t in two halves around an optional
+// residual pass (the projection g_t = U^T x_t came from the window pass).
+//   A (k_decide_a): restart / reject, ell = N^T L^{-1} g, the Pythagorean p and
+//     the dependent test (basis.py:112-139).  A dependent snapshot needs no pass
+//     over U at all: A prepares the next snapshot and the decision is final.
+//   B (k_decide_b): after the residual pass (independent snapshots and a first
+//     accept): how r enters U, exactly as decide_body's independent branch,
+//     plus the new U column's row of the window projections (window_row).
+// ---------------------------------------------------------------------------
+__device__ inline void decide_a_body(const StateView& src, const Pipe& pp, const IsvdParams& P, double* part,
+                                     double* red) {
+  const IsvdHdr h = *src.hdr;
+  IsvdStep* st = pp.step[P.parity];
+  double* ell = pp.ell[P.parity];
+  const int c = h.c, base = h.base, r = h.r;
+  const double xx = pp.ctl->xx;
+  const int slot = base + c;
+  int mode = -1, restart = 0, dep = 0, cn = c, base_new = base, reorth = 0, resid = 0;
+  double p = 0.0, p_sq = 0.0;
+  if (h.status != 0 || !isfinite(xx)) {
+    mode = M_ERROR;
+  } else {
+    const bool at_cap = P.r_max >= 0 && h.r >= P.r_max;
+    if (r == 0 || (at_cap && P.cap_mode == 0)) {
+      restart = at_cap ? 1 : 0;
+      if (sqrt(xx) > P.tol_svd) {
+        mode = M_RESTART_ACCEPT;
+        if (c == 0) resid = 1;  // the residual pass writes x itself into the slot (B finishes)
+        else reorth = 2;        // the second pass copies x into the slot (k_decide2 finishes)
+      } else {
+        mode = M_REJECT;
+        cn = 0;
+        base_new = base + c;
+      }
+    }
+  }
+  if (mode == -1) {
+    cta_gemv_t_cm(src.N, src.ldn, c, r, pp.tvec, ell, false);  // ell = N^T L^{-1} g
+    double s_ll = 0.0;
+    for (int i = threadIdx.x; i < r; i += blockDim.x) s_ll = fma(ell[i], ell[i], s_ll);
+    s_ll = block_sum(s_ll, red);
+    p_sq = xx - s_ll;  // the Pythagorean residual (basis.py:136-138)
+    p = (p_sq > 0.0) ? sqrt(p_sq) : 0.0;
+    dep = (p < P.tol_svd) || (p == 0.0) || ((int64_t)r >= P.n);
+    mode = dep ? M_NORMAL_DEP : M_NORMAL_INDEP;
+    resid = dep ? 0 : 1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    st->mode = mode;
+    st->restart = restart;
+    st->action = 0;
+    st->dep = (mode == M_NORMAL_DEP) ? 1 : 0;
+    st->c = c;
+    st->cn = cn;
+    st->base_new = base_new;
+    st->slot = slot;
+    st->xx = xx;
+    st->rho2 = 0.0;
+    st->p = p;
+    st->p_sq = p_sq;
+    st->norm = sqrt(xx);
+    st->lam = 0.0;
+    pp.ctl->resid = resid;
+    pp.ctl->reorth = reorth;
+    if (!resid && reorth == 0) {
+      pp.ctl->c = cn;
+      pp.ctl->base = base_new;
+    }
+  }
+  // a final decision (dependent, reject, error): U is unchanged or emptied,
+  // so the next snapshot's coefficients come straight from the window
+  if (!resid && reorth == 0 && P.has_next) prep_next(P, pp, part);
+}
+
+__device__ inline void decide_b_body(const StateView& src, const Pipe& pp, const IsvdParams& P, double* part,
+                                     double* red) {
+  if (!*(volatile const int32_t*)&pp.ctl->resid) return;
+  const IsvdHdr h = *src.hdr;
+  IsvdStep* st = pp.step[P.parity];
+  double* ell = pp.ell[P.parity];
+  double* nj = pp.nj[P.parity];
+  const int mode = st->mode;
+  const int c = st->c, base = h.base, r = h.r, slot = st->slot;
+  const int ldl = P.ccap;
+  double* Lb = P.L + (int64_t)base * (ldl + 1);
+  double* Lib = P.Li + (int64_t)base * (ldl + 1);
+  const double rho2 = pp.fo.scal[0];
+  const double p = st->p;
+  int action = 0, dep = 0, cn = c, base_new = base, reorth = 0;
+  double lam = 0.0;
+  bool prepped = false;
+  const bool nx = P.has_next != 0;
+  if (mode == M_RESTART_ACCEPT) {  // first accept into an empty U: the slot holds x
+    lam = sqrt(rho2);
+    cn = 1;
+    base_new = slot;
+    window_row(P, 0, 0, nullptr, nullptr);
+    if (threadIdx.x == 0) {
+      P.L[(int64_t)slot * (ldl + 1)] = lam;
+      P.Li[(int64_t)slot * (ldl + 1)] = 1.0 / lam;
+    }
+  } else {
+    double* t1 = pp.tmp;  // L^{-1} g'[:c]: the next snapshot's coordinates in the current Q_U
+    cta_gemv2_cm<8>(Lib, ldl, c, c, pp.fo.e, nx ? pp.fo.gn : nullptr, pp.l1, nx ? t1 : nullptr, part, true);
+    double s_l1 = 0.0, s_lt = 0.0, s_zero = 0.0;
+    for (int j = threadIdx.x; j < c; j += blockDim.x) {
+      s_l1 = fma(pp.l1[j], pp.l1[j], s_l1);
+      if (nx) s_lt = fma(pp.l1[j], t1[j], s_lt);
+    }
+    block_sum3(s_l1, s_lt, s_zero, red);
+    const double lam2 = rho2 - s_l1;  // out-of-span part of r1 in the G metric
+    const bool room = (slot < P.ccap) && ((int64_t)c < P.n);
+    const bool app = room && (lam2 > kFoldTau * kFoldTau * rho2) && (rho2 > 0.0);
+    if (app) {
+      // r1 = x - U gt becomes U column c: its row of the window (and g'_c = r1 . x_next)
+      window_row(P, c, c, pp.gt, nullptr);
+      lam = sqrt(lam2);
+      const double tc = nx ? (pp.fo.gn[c] - s_lt) / lam : 0.0;
+      if (nx)
+        for (int j = threadIdx.x; j < c; j += blockDim.x) pp.h[j] = t1[j] - pp.l1[j] * (tc / lam);
+      cta_gemv_cm<8>(src.N, src.ldn, c, r, ell, -1.0, pp.tvec, pp.y, part, false);  // y = tvec - N ell
+      cta_gemv2_t_cm(Lib, ldl, c, c, pp.l1, nx ? pp.h : pp.l1, pp.w, pp.gt, true);
+      for (int j = threadIdx.x; j < c; j += blockDim.x) {
+        Lb[(int64_t)j * ldl + c] = pp.l1[j];
+        Lib[(int64_t)j * ldl + c] = -pp.w[j] / lam;
+      }
+      for (int a = threadIdx.x; a <= c; a += blockDim.x) {
+        nj[a] = (a < c) ? (pp.y[a] + pp.l1[a]) / p : lam / p;
+        if (nx) pp.tvec[a] = (a < c) ? t1[a] : tc;
+      }
+      if (threadIdx.x == 0) {
+        Lb[(int64_t)c * ldl + c] = lam;
+        Lib[(int64_t)c * ldl + c] = 1.0 / lam;
+        if (nx) pp.gt[c] = tc / lam;
+      }
+      prepped = nx;
+      cn = c + 1;
+      action = 1;
+    } else if (room) {
+      reorth = 1;
+      cta_gemv_cm<8>(src.N, src.ldn, c, r, ell, -1.0, pp.tvec, pp.y, part, false);
+      cta_gemv_t_cm(Lib, ldl, c, c, pp.l1, pp.h, true);  // h = L^{-T} l1 = G^{-1} e
+    } else if (c >= r + 1) {
+      cta_gemv_cm<8>(src.N, src.ldn, c, r, ell, -1.0, pp.tvec, pp.y, part, false);
+      for (int a = threadIdx.x; a < c; a += blockDim.x) nj[a] = (pp.y[a] + pp.l1[a]) / p;
+      action = 2;
+    } else {
+      dep = 1;
+    }
+    if ((dep || action == 2) && nx) {  // U unchanged: tvec' = t1, gt' = L^{-T} t1
+      __syncthreads();
+      for (int j = threadIdx.x; j < c; j += blockDim.x) pp.tvec[j] = t1[j];
+      cta_gemv_t_cm(Lib, ldl, c, c, t1, pp.gt, true);
+      prepped = true;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    st->action = action;
+    if (dep) st->dep = 1;
+    st->cn = cn;
+    st->base_new = base_new;
+    st->rho2 = rho2;
+    st->lam = lam;
+    pp.ctl->reorth = reorth;
+    if (reorth == 0) {
+      pp.ctl->c = cn;
+      pp.ctl->base = base_new;
+    }
+  }
+  if (reorth == 0 && nx) {
+    if (prepped) {
+      if (threadIdx.x == 0) pp.ctl->xx = next_xx(P, pp);
+    } else {
+      prep_next(P, pp, part);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kDecideThreads) k_decide_a(StateView src, Pipe pp, IsvdParams P) {
+  extern __shared__ double part[];
+  __shared__ double red[96];
+  pdl_wait();
+  wait_counter(&pp.ctl->bdone, P.b_expect);  // the previous snapshot's core step wrote N, sigma
+  pdl_trigger();
+  decide_a_body(src, pp, P, part, red);
+  signal_counter(&pp.ctl->adone);  // the core step of this snapshot may start its SVD
+}
+
+__global__ void __launch_bounds__(kDecideThreads) k_decide_b(StateView src, Pipe pp, IsvdParams P) {
+  extern __shared__ double part[];
+  __shared__ double red[96];
+  pdl_enter();
+  decide_b_body(src, pp, P, part, red);
 }
 
 template <int MAXJ>
@@ -554,7 +801,8 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(PassArgs a, int nstage
       coef = nullptr;  // slot <- x
       c = 0;
     }
-  } else if (a.kind == PASS_FUSED) {
+  } else if (a.kind == PASS_FUSED || a.kind == PASS_RESID) {
+    if (a.kind == PASS_RESID && *(volatile const int32_t*)&a.ctl->resid == 0) return;
     do_e = true;
     do_gn = a.xn != nullptr;
   } else {
@@ -782,13 +1030,22 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(PassArgs a, int nstage
 //     (basis.py:160-168), drift |phi_0 . phi_last| = |N_0 . N_last| and the QR
 //     of basis.py:170-174 on N' (Q_U is orthonormal: QR(Phi') = Q_U QR(N'))
 // ---------------------------------------------------------------------------
+// mid_ctr (window mode): the core SVD only needs k_decide_a's results; the
+// rest (how r entered U: cn, n_j, a demotion to dependent) waits here for
+// *mid_ctr >= mid_target (the decision chain's end).
 __device__ inline void step_b_body(const StateView& src, const StateView& dst, const Pipe& pp, const IsvdParams& P,
-                                   int use_smem, double* smem, double* red) {
+                                   int use_smem, double* smem, double* red, const int32_t* mid_ctr = nullptr,
+                                   int32_t mid_target = -1) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const IsvdHdr h = *src.hdr;
   IsvdStep* st = pp.step[P.parity];
   const double* ell = pp.ell[P.parity];
   const double* wj = pp.nj[P.parity];
+  const int mode0 = *(volatile const int32_t*)&st->mode;
+  if (mid_ctr && mode0 != M_NORMAL_DEP && mode0 != M_NORMAL_INDEP) {
+    wait_counter(mid_ctr, mid_target);  // restart / reject / error: cheap, needs the whole chain
+    mid_ctr = nullptr;
+  }
   const int mode = st->mode;
   IsvdHdr o = h;
   o.flags = 0;
@@ -802,6 +1059,7 @@ __device__ inline void step_b_body(const StateView& src, const StateView& dst, c
       *dst.hdr = o;
       st->m = 0;
       st->mkeep = -1;
+      *pp.vrec[P.parity] = VRec{mode, 0, -1, 0};
     }
     return;
   }
@@ -823,18 +1081,16 @@ __device__ inline void step_b_body(const StateView& src, const StateView& dst, c
       }
       st->m = 0;
       *dst.hdr = o;
+      *pp.vrec[P.parity] = VRec{mode, 0, st->mkeep, 0};
     }
     return;
   }
   STROM_TPROBE(P, 0);
-  const bool dep = st->dep != 0;
+  bool dep = *(volatile const int32_t*)&st->dep != 0;
   const int r = h.r, c = st->c, m = r + 1;
-  const int cn = st->cn;
-  const int action = st->action;
   const double p = st->p;
   o.p = p;
   o.p_sq = st->p_sq;
-  const bool appended = (action == 1);
   STROM_TPROBE(P, 1);
   // ---- shared-memory plan (global fallback when it does not fit) ----------
   //   WS m^2 | Wt m^2 | Vt m^2 | core work 16 ms | WB ccap x m (staged N_b, later QR's M)
@@ -854,6 +1110,21 @@ __device__ inline void step_b_body(const StateView& src, const StateView& dst, c
     cw.org = ib; cw.kset = ib + ms; cw.defl = ib + 2 * ms; cw.ra = ib + 3 * ms; cw.rb = ib + 4 * ms;
     cw.perm = ib + 5 * ms; cw.cnt = ib + 6 * ms;
   }
+  // ---- 2. the bordered core and its SVD (rank-one secular solver) ----------
+  core_svd_secular(src.sigma, ell, dep ? 0.0 : p, r, cw, Wt, Vt, svs, WS, pp.vbar, red,
+                   P.tprobe ? P.tprobe + 8 : nullptr, P.tprobe ? P.tprobe + 300 : nullptr);
+  if (mid_ctr) {
+    wait_counter(mid_ctr, mid_target);
+    const bool dep2 = *(volatile const int32_t*)&st->dep != 0;
+    if (dep2 != dep) {  // the residual could not enter U: the update is dependent after all
+      dep = dep2;
+      __syncthreads();
+      core_svd_secular(src.sigma, ell, dep ? 0.0 : p, r, cw, Wt, Vt, svs, WS, pp.vbar, red, nullptr, nullptr);
+    }
+  }
+  const int cn = st->cn;
+  const int action = st->action;
+  const bool appended = (action == 1);
   // stage N_b: columns 0..r-1 = N (c rows; the appended row is 0), column r = n_j
   for (int b = wid; b < m; b += nw) {
     const double* ns = src.N + (int64_t)b * src.ldn;
@@ -865,9 +1136,7 @@ __device__ inline void step_b_body(const StateView& src, const StateView& dst, c
       wb[a] = v;
     }
   }
-  // ---- 2. the bordered core and its SVD (rank-one secular solver) ----------
-  core_svd_secular(src.sigma, ell, dep ? 0.0 : p, r, cw, Wt, Vt, svs, WS, pp.vbar, red,
-                   P.tprobe ? P.tprobe + 8 : nullptr, P.tprobe ? P.tprobe + 300 : nullptr);
+  __syncthreads();
   STROM_TPROBE(P, 2);
   // (no orthogonality polish needed: the Gu-Eisenstat vectors are orthogonal to
   // working precision, unlike accumulated Jacobi rotations)
@@ -953,6 +1222,7 @@ __device__ inline void step_b_body(const StateView& src, const StateView& dst, c
     *dst.hdr = o;
     st->m = m;
     st->mkeep = mk;
+    *pp.vrec[P.parity] = VRec{mode, m, mk, 0};
   }
 }
 
@@ -960,8 +1230,13 @@ __global__ void __launch_bounds__(kSmallThreads) k_step_b(StateView src, StateVi
                                                           int use_smem) {
   extern __shared__ double smem[];
   __shared__ double red[32];
-  wait_counter(&pp.ctl->decided, P.d_expect);  // this snapshot's decision chain
-  step_b_body(src, dst, pp, P, use_smem, smem, red);
+  if (P.wn > 0) {  // window mode: the SVD needs only k_decide_a; the rest waits mid-way
+    wait_counter(&pp.ctl->adone, P.d_expect);
+    step_b_body(src, dst, pp, P, use_smem, smem, red, &pp.ctl->decided, P.d_expect);
+  } else {
+    wait_counter(&pp.ctl->decided, P.d_expect);  // this snapshot's decision chain
+    step_b_body(src, dst, pp, P, use_smem, smem, red);
+  }
   signal_counter(&pp.ctl->bdone);  // the next snapshot's decision may read this state
 }
 
@@ -973,7 +1248,7 @@ constexpr int kVCols = 16;
 constexpr int kVRows = 64;
 __global__ void __launch_bounds__(kVRows) k_vupdate(StateView src, StateView dst, Pipe pp, IsvdParams P) {
   extern __shared__ double vbs[];  // (r+1) x kVCols slice of V_bar
-  const IsvdStep* st = pp.step[P.parity];
+  const VRec* st = pp.vrec[P.parity];
   const int mode = st->mode;
   const int64_t k = P.k_new;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

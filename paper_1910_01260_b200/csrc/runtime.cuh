@@ -127,7 +127,7 @@ namespace strom {
 // passes) add theirs into prof_dev_bytes() with one atomic per launch.
 enum ProfKind : int {
   P_PROJ = 0, P_RESID, P_STEP_A, P_STEP_B, P_VUPDATE, P_COMPACT, P_TALL_GEMM, P_SPATIAL,
-  P_ST_GEMM, P_ST_SMALL, P_LU, P_TEMPORAL, P_OTHER, P_NKINDS
+  P_ST_GEMM, P_ST_SMALL, P_LU, P_TEMPORAL, P_OTHER, P_WPROJ, P_NKINDS
 };
 void prof_begin(int kind, cudaStream_t s);
 void prof_end(int kind, cudaStream_t s);
