@@ -141,6 +141,8 @@ int strom_debug_pass_bw(int64_t n, int32_t c, int32_t iters, int32_t reserve, do
 
 /* Diagnostics: step-B phase timestamps (clock64, 8 slots) into dev_buf; NULL disables. */
 void strom_debug_tprobe(long long* dev_buf);
+void strom_debug_lu_probe(long long* dev_buf); /* persistent LU: 8 globaltimer stamps per CTA (diagnostics) */
+void strom_debug_trace(long long* dev_buf, int64_t rows); /* window-mode iSVD: 16 stamps per update (diagnostics) */
 
 void strom_isvd_free(strom_isvd* h);
 

@@ -54,6 +54,8 @@ _PROTOS = {
                                            dbl, dbl, i64, i32, P_I32, vp, C.POINTER(vp)]),
     "strom_isvd_factors": (C.c_int, [vp, vp, vp, vp, vp]),
     "strom_debug_tprobe": (None, [vp]),
+    "strom_debug_lu_probe": (None, [vp]),
+    "strom_debug_trace": (None, [vp, i64]),
     "strom_debug_pass_bw": (C.c_int, [i64, i32, i32, i32, C.POINTER(dbl)]),
     "strom_isvd_free": (None, [vp]),
     # temporal bases (basis.py:275-302)

@@ -606,7 +606,16 @@ struct PlArgs {
   int* piv;
   int* flag;  // [ncb] panel published (A blocks) / forward updates done (B blocks)
   int* fin;   // [nbA] final write-back of an A block column done
+  long long* probe;  // diagnostics (STROM_LU_PROBE): 8 globaltimer stamps per CTA, or null
 };
+#define PL_PROBE(k)                                                                         \
+  do {                                                                                      \
+    if (a.probe && threadIdx.x == 0) {                                                      \
+      unsigned long long _t;                                                                \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                                \
+      a.probe[blockIdx.x * 8 + (k)] = (long long)_t;                                        \
+    }                                                                                       \
+  } while (0)
 
 __device__ __forceinline__ int pl_ld_acquire(const int* p) {
   int v;
@@ -698,8 +707,11 @@ __global__ void __launch_bounds__(kPlThreads, 1) k_lu_persistent(PlArgs a) {
   __syncthreads();
   // ---- updates from the panels to the left
   const int kend = rhs ? a.nbA : j;
+  PL_PROBE(0);
   for (int k = 0; k < kend; ++k) {
+    if (k == kend - 1) PL_PROBE(1);
     pl_wait(a.flag + k);
+    if (k == kend - 1) PL_PROBE(2);
     const int k0 = k * kPlNb, kw = min(kPlNb, n - k0);
     if (tid < kPlNb) spiv[tid] = tid < kw ? __ldcg(a.piv + k0 + tid) : k0 + tid;
     for (int e = tid; e < kPlNb * kPlNb; e += kPlThreads) {  // L_kk (unit lower)
@@ -736,6 +748,7 @@ __global__ void __launch_bounds__(kPlThreads, 1) k_lu_persistent(PlArgs a) {
   }
   if (!rhs) {
     // ---- factor this panel: rows j0.., columns 0..w-1; thread tid owns rows tid + 512 m
+    PL_PROBE(3);
     const int j0 = c0;
     for (int c = 0; c < w; ++c) {
       const int gr = j0 + c;
@@ -788,6 +801,7 @@ __global__ void __launch_bounds__(kPlThreads, 1) k_lu_persistent(PlArgs a) {
       const int c = idx / n, r = idx - c * n;
       if (c < w) G[(int64_t)c * gld + r] = S[c * ld + r];  // U blocks above, this panel's LU below
     }
+    PL_PROBE(4);
     pl_signal(a.flag + j);
     // ---- the later panels' interchanges reach this block column's L rows
     for (int k = j + 1; k < a.nbA; ++k) {
@@ -813,12 +827,15 @@ __global__ void __launch_bounds__(kPlThreads, 1) k_lu_persistent(PlArgs a) {
       const int c = idx / n, r = idx - c * n;
       if (c < w && r >= j0 + kPlNb) G[(int64_t)c * gld + r] = S[c * ld + r];
     }
+    PL_PROBE(5);
     pl_signal(a.fin + j);
     return;
   }
   // ---- right-hand sides: S = L^{-1} P B; now U X = S, block rows from the bottom
+  PL_PROBE(3);
   pl_signal(a.flag + j);
   for (int m = 0; m < a.nbA; ++m) pl_wait(a.fin + m);
+  PL_PROBE(4);
   for (int J = a.nbA - 1; J >= 0; --J) {
     const int b0 = J * kPlNb, bw = min(kPlNb, n - b0);
     for (int e = tid; e < kPlNb * kPlNb; e += kPlThreads) {  // U_JJ (upper, with the diagonal)
@@ -850,6 +867,7 @@ __global__ void __launch_bounds__(kPlThreads, 1) k_lu_persistent(PlArgs a) {
     const int c = idx / n, r = idx - c * n;
     if (c < w) G[(int64_t)c * gld + r] = S[c * ld + r];
   }
+  PL_PROBE(5);
 }
 
 // Pivot-floor test of a stored factor: info[0] = first i with |U_ii| <= 1e-14
@@ -892,6 +910,8 @@ bool pl_fits(int64_t n, int64_t nrhs) {
   return (int64_t)o * sm_count() >= ncb;
 }
 
+long long* g_lu_probe = nullptr;  // strom_debug_lu_probe
+
 // LU of A (and, with nrhs > 0, the solve A X = B in place) by the persistent kernel.
 void pl_run(int64_t n, double* A, int64_t lda, double* B, int64_t ldb, int64_t nrhs, int* piv, cudaStream_t s) {
   const int nbA = (int)ceil_div(n, kPlNb);
@@ -903,6 +923,7 @@ void pl_run(int64_t n, double* A, int64_t lda, double* B, int64_t ldb, int64_t n
   a.piv = piv;
   a.flag = flags->as<int>();
   a.fin = flags->as<int>() + ncb;
+  a.probe = g_lu_probe;
   void* args[] = {&a};
   ProfScope ps(P_LU, s);
   STROM_CUDA(cudaLaunchCooperativeKernel((const void*)k_lu_persistent, dim3(ncb), dim3(kPlThreads), args,
@@ -1030,6 +1051,10 @@ int strom_dense_solve(int64_t n, double* a_dev, double* x_dev, int64_t nrhs, int
     }
   });
 }
+
+// Diagnostics: 8 globaltimer stamps per CTA of the persistent LU into dev_buf
+// (ncb x 8 int64), or NULL to disable.
+void strom_debug_lu_probe(long long* dev_buf) { g_lu_probe = dev_buf; }
 
 // Positive-diagonal thin QR of M (rows x cols, column-major, ld) in place
 // (M <- Q); R (cols x cols, column-major) receives the matching R.

@@ -151,7 +151,10 @@ void trace_point(const char* what, cudaStream_t s) {
   fprintf(stderr, " %s\n", cudaGetErrorString(e));
 }
 
-long long* g_tprobe = nullptr;  // step-B phase timestamps (strom_debug_tprobe)
+long long* g_tprobe = nullptr;     // step-B phase timestamps (strom_debug_tprobe)
+long long* g_trace = nullptr;      // strom_debug_trace: 16 stamps per update of the next ingest calls
+int64_t g_trace_rows = 0;
+long long* g_cur_trace = nullptr;  // the row of the update being launched (window mode)
 
 // ------------------------------------------------------------------ state
 // The append-only store shared by a state and its successors: U (ldu x ccap,
@@ -380,6 +383,7 @@ IsvdParams make_params(const strom_isvd* h, const PipeMem& m, int64_t k_new, boo
   P.Li = h->store->Li();
   P.prof = prof_dev_bytes();
   P.tprobe = g_tprobe;
+  P.trace = nullptr;
   P.wG = nullptr;
   P.wXX = nullptr;
   P.ldg = 0;
@@ -490,6 +494,7 @@ void launch_pass(int kind, int cols_ub, const strom_isvd* h, const PipeMem& m, c
   a.part = m.pp.part;
   a.counter = m.pp.counter;
   a.prof = prof_dev_bytes();
+  a.trace = g_cur_trace;
   a.tail = tl.tail;
   a.b_expect = tl.b_expect;
   a.dpp = m.pp;
@@ -840,6 +845,7 @@ void launch_window(const strom_isvd* h, const PipeMem& m, const double* const* x
   a.part = m.wpart;
   a.pstride = m.wpstride;
   a.prof = prof_dev_bytes();
+  a.trace = g_cur_trace;
   const int cu = std::max(cols_ub, 1);
   const int mt = (int)ceil_div(ceil_div(cu, 8), kWConsumers);
   switch (mt) {
@@ -1344,6 +1350,8 @@ strom_isvd* ingest_windowed(strom_isvd* src, ColumnSource& cols, cudaStream_t s,
       wn = 0;  // a new window (U may have changed under the old one)
       need_init = false;
     }
+    g_cur_trace = (g_trace && t < g_trace_rows) ? g_trace + 16 * t : nullptr;
+    P.trace = g_cur_trace;
     if (t >= w0 + wn) {
       w0 = t;
       wn = std::min<int64_t>(wb, ncols - t);
@@ -1365,6 +1373,8 @@ strom_isvd* ingest_windowed(strom_isvd* src, ColumnSource& cols, cudaStream_t s,
     P.has_next = (P.wcol + 1 < P.wn) ? 1 : 0;
     P.b_expect = -1;
     P.d_expect = (int32_t)(d_launched + 1);
+    P.trace = (g_trace && t < g_trace_rows) ? g_trace + 16 * t : nullptr;
+    g_cur_trace = P.trace;
     Pipe pp = m.pp;
     pp.fo.gn = m.wG + (int64_t)(P.has_next ? P.wcol + 1 : 0) * m.ldg;
     pp.vbar = (t & 1) ? m.vbar2 : m.pp.vbar;
@@ -1386,6 +1396,7 @@ strom_isvd* ingest_windowed(strom_isvd* src, ColumnSource& cols, cudaStream_t s,
     STROM_CUDA(cudaStreamWaitEvent(s3, evB, 0));
     launch_vupdate_pp(prev->view, dst->view, pp, P, prev->caps.rcap, s3);
     STROM_CUDA(cudaEventRecord(evU[t & 1], s3));
+    g_cur_trace = nullptr;
     u_pending[t & 1] = true;
     dst->c_ub = prev->c_ub + 1;
     dst->store->claimed = std::max(dst->store->claimed, dst->c_ub);
@@ -1692,6 +1703,14 @@ int strom_debug_pass_bw(int64_t n, int32_t c, int32_t iters, int32_t reserve, do
 // Diagnostics: point step B's phase timestamps (clock64, 8 slots) at a device
 // buffer, or NULL to disable.
 void strom_debug_tprobe(long long* dev_buf) { g_tprobe = dev_buf; }
+
+// Diagnostics: globaltimer stamps (16 per update: decide A/B, passes, core step,
+// V update, window pass) of the first `rows` updates of the next window-mode
+// ingest calls into dev_buf (rows x 16 int64); NULL disables.
+void strom_debug_trace(long long* dev_buf, int64_t rows) {
+  g_trace = dev_buf;
+  g_trace_rows = dev_buf ? rows : 0;
+}
 
 void strom_isvd_free(strom_isvd* h) { delete h; }
 

@@ -154,6 +154,7 @@ struct IsvdParams {
   double* Li;
   unsigned long long* prof;  // device byte counters (runtime.cuh ProfKind) or null
   long long* tprobe;         // phase timestamps of step B (diagnostics) or null
+  long long* trace;          // per-update globaltimer trace (diagnostics, strom_debug_trace) or null
   // window mode (wn > 0): projections of the window's snapshots onto U,
   // G[i + j ldg] = U_i . x_j (logical columns i), and their Gram XX[i kWB + j];
   // wcol is this snapshot's column.  pp.fo.gn then points at column wcol + 1.
@@ -177,6 +178,15 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void pdl_enter() {
   pdl_trigger();
   pdl_wait();
+}
+
+// Diagnostics trace: globaltimer stamp into row[k] by thread 0 of CTA 0.
+__device__ __forceinline__ void trace_stamp(long long* row, int k) {
+  if (row && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    row[k] = (long long)t;
+  }
 }
 
 #define STROM_TPROBE(P, k)                                  \
@@ -250,6 +260,7 @@ struct PassArgs {
   double* part;
   unsigned* counter;
   unsigned long long* prof;
+  long long* trace;  // diagnostics: this update's trace row, or null
 };
 
 constexpr int kPassMaxStages = 8;
@@ -572,6 +583,7 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide2(StateView src, Pipe 
   pdl_enter();
   decide2_body(src, pp, P, part, red);
   signal_counter(&pp.ctl->decided);  // the decisions of this snapshot are complete
+  trace_stamp(P.trace, 7);
 }
 
 // ---------------------------------------------------------------------------
@@ -761,15 +773,19 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide_a(StateView src, Pipe
   pdl_wait();
   wait_counter(&pp.ctl->bdone, P.b_expect);  // the previous snapshot's core step wrote N, sigma
   pdl_trigger();
+  trace_stamp(P.trace, 0);
   decide_a_body(src, pp, P, part, red);
   signal_counter(&pp.ctl->adone);  // the core step of this snapshot may start its SVD
+  trace_stamp(P.trace, 1);
 }
 
 __global__ void __launch_bounds__(kDecideThreads) k_decide_b(StateView src, Pipe pp, IsvdParams P) {
   extern __shared__ double part[];
   __shared__ double red[96];
   pdl_enter();
+  trace_stamp(P.trace, 4);
   decide_b_body(src, pp, P, part, red);
+  trace_stamp(P.trace, 5);
 }
 
 template <int MAXJ>
@@ -783,6 +799,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(PassArgs a, int nstage
   __shared__ double wsc[3];
   __shared__ int s_last;
   pdl_enter();
+  trace_stamp(a.trace, a.kind == PASS_SECOND ? 6 : 2);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int c = a.ctl->c;
   const int base = a.ctl->base;
@@ -973,6 +990,11 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(PassArgs a, int nstage
     }
   }
   if (!last_cta_arrives(a.counter, &s_last)) return;
+  if (a.trace && threadIdx.x == 0 && a.kind != PASS_SECOND) {
+    unsigned long long tt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+    a.trace[3] = (long long)tt;
+  }
   // one warp per output, lanes stride over the CTA partials, fixed tree: deterministic
   const int PG = (a.pstride - 8) / 2;
   const int nwarps = blockDim.x >> 5;
@@ -1113,8 +1135,10 @@ __device__ inline void step_b_body(const StateView& src, const StateView& dst, c
   // ---- 2. the bordered core and its SVD (rank-one secular solver) ----------
   core_svd_secular(src.sigma, ell, dep ? 0.0 : p, r, cw, Wt, Vt, svs, WS, pp.vbar, red,
                    P.tprobe ? P.tprobe + 8 : nullptr, P.tprobe ? P.tprobe + 300 : nullptr);
+  trace_stamp(P.trace, 9);
   if (mid_ctr) {
     wait_counter(mid_ctr, mid_target);
+    trace_stamp(P.trace, 10);
     const bool dep2 = *(volatile const int32_t*)&st->dep != 0;
     if (dep2 != dep) {  // the residual could not enter U: the update is dependent after all
       dep = dep2;
@@ -1232,12 +1256,15 @@ __global__ void __launch_bounds__(kSmallThreads) k_step_b(StateView src, StateVi
   __shared__ double red[32];
   if (P.wn > 0) {  // window mode: the SVD needs only k_decide_a; the rest waits mid-way
     wait_counter(&pp.ctl->adone, P.d_expect);
+    trace_stamp(P.trace, 8);
     step_b_body(src, dst, pp, P, use_smem, smem, red, &pp.ctl->decided, P.d_expect);
   } else {
     wait_counter(&pp.ctl->decided, P.d_expect);  // this snapshot's decision chain
+    trace_stamp(P.trace, 8);
     step_b_body(src, dst, pp, P, use_smem, smem, red);
   }
   signal_counter(&pp.ctl->bdone);  // the next snapshot's decision may read this state
+  trace_stamp(P.trace, 11);
 }
 
 // ---------------------------------------------------------------------------
@@ -1248,6 +1275,7 @@ constexpr int kVCols = 16;
 constexpr int kVRows = 64;
 __global__ void __launch_bounds__(kVRows) k_vupdate(StateView src, StateView dst, Pipe pp, IsvdParams P) {
   extern __shared__ double vbs[];  // (r+1) x kVCols slice of V_bar
+  trace_stamp(P.trace, 12);
   const VRec* st = pp.vrec[P.parity];
   const int mode = st->mode;
   const int64_t k = P.k_new;

@@ -36,6 +36,7 @@ struct WprojArgs {
   double* part;   // per-CTA partials, pstride doubles each: [i * kWB + j] G, then kWB^2 XX
   int32_t pstride;
   unsigned long long* prof;
+  long long* trace;
 };
 
 template <int MT>  // m-tiles (8 U columns) per consumer warp: c <= 64 MT
@@ -44,6 +45,7 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wproj(WprojArgs a, int nstages
   __shared__ __align__(8) uint64_t full[kWMaxStages];
   __shared__ __align__(8) uint64_t empty[kWMaxStages];
   pdl_enter();
+  trace_stamp(a.trace, 14);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
   const int c = a.ctl->c, base = a.ctl->base;
   const int c8 = (c + 7) & ~7;
@@ -172,6 +174,7 @@ __global__ void __launch_bounds__(kDecideThreads) k_prep_w(Pipe pp, IsvdParams P
   extern __shared__ double part[];
   pdl_enter();
   prep_next(P, pp, part);
+  trace_stamp(P.trace, 15);
 }
 
 }  // namespace strom
