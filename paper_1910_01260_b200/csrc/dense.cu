@@ -687,12 +687,103 @@ __device__ inline void pl_gemm(double* S, int ld, const double* M, int64_t ldm, 
   }
 }
 
+// Panel factorisation with the panel's rows in registers (thread tid owns rows
+// tid + 512 q, q < kPlRpt): per column one argmax (idamax's rule: largest |a|,
+// first row on ties), the pivot row and the row it displaces exchanged through
+// shared memory, then scale and rank-1 update in registers; two barriers per
+// column.  Fully unrolled over the 16 panel columns so every register index is
+// static.
+constexpr int kPlRpt = 2;
+__device__ inline void pl_panel_reg(double* S, int ld, int n, int j0, int w, int* piv, double* cval, int* cidx,
+                                    double* prow, double* grow) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  double v[kPlRpt][kPlNb];
+#pragma unroll
+  for (int q = 0; q < kPlRpt; ++q) {
+    const int r = tid + kPlThreads * q;
+#pragma unroll
+    for (int c = 0; c < kPlNb; ++c) v[q][c] = (r < n && r >= j0) ? S[c * ld + r] : 0.0;
+  }
+#pragma unroll
+  for (int c = 0; c < kPlNb; ++c) {
+    if (c >= w) break;
+    const int gr = j0 + c;
+    double best = -1.0;
+    int bi = 0x7fffffff;
+#pragma unroll
+    for (int q = 0; q < kPlRpt; ++q) {
+      const int r = tid + kPlThreads * q;
+      if (r >= gr && r < n) {
+        const double av = fabs(v[q][c]);
+        if (av > best) { best = av; bi = r; }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    if (lane == 0) { cval[wid] = best; cidx[wid] = bi; }
+    __syncthreads();
+    best = cval[lane & (kPlWarps - 1)];
+    bi = cidx[lane & (kPlWarps - 1)];
+#pragma unroll
+    for (int o = kPlWarps / 2; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    const int p = (bi == 0x7fffffff) ? gr : bi;  // an all-NaN column pivots on itself
+#pragma unroll
+    for (int q = 0; q < kPlRpt; ++q) {
+      const int r = tid + kPlThreads * q;
+      if (r == p)
+#pragma unroll
+        for (int c2 = 0; c2 < kPlNb; ++c2) prow[c2] = v[q][c2];
+      if (r == gr)
+#pragma unroll
+        for (int c2 = 0; c2 < kPlNb; ++c2) grow[c2] = v[q][c2];
+    }
+    if (tid == 0) piv[gr] = p;
+    __syncthreads();
+    const double d = prow[c];
+    const double inv = d != 0.0 ? 1.0 / d : 0.0;
+#pragma unroll
+    for (int q = 0; q < kPlRpt; ++q) {
+      const int r = tid + kPlThreads * q;
+      if (r == gr) {
+#pragma unroll
+        for (int c2 = 0; c2 < kPlNb; ++c2) v[q][c2] = prow[c2];
+      } else if (r == p) {
+#pragma unroll
+        for (int c2 = 0; c2 < kPlNb; ++c2) v[q][c2] = grow[c2];
+      }
+      if (r > gr && r < n && d != 0.0) {
+        const double l = v[q][c] * inv;
+        v[q][c] = l;
+#pragma unroll
+        for (int c2 = c + 1; c2 < kPlNb; ++c2) v[q][c2] = fma(-l, prow[c2], v[q][c2]);
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < kPlRpt; ++q) {
+    const int r = tid + kPlThreads * q;
+    if (r < n && r >= j0)
+#pragma unroll
+      for (int c = 0; c < kPlNb; ++c)
+        if (c < w) S[c * ld + r] = v[q][c];
+  }
+}
+
 __global__ void __launch_bounds__(kPlThreads, 1) k_lu_persistent(PlArgs a) {
   extern __shared__ double S[];  // kPlNb columns x ldS rows (column-major)
   __shared__ double sT[kPlNb][kPlNb + 1];
   __shared__ double cval[kPlWarps];
   __shared__ int cidx[kPlWarps];
   __shared__ int spiv[kPlNb];
+  __shared__ double prow[kPlNb], grow[kPlNb];
   const int j = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int n = a.n, ld = a.ldS;
   const bool rhs = j >= a.nbA;
@@ -750,51 +841,57 @@ __global__ void __launch_bounds__(kPlThreads, 1) k_lu_persistent(PlArgs a) {
     // ---- factor this panel: rows j0.., columns 0..w-1; thread tid owns rows tid + 512 m
     PL_PROBE(3);
     const int j0 = c0;
-    for (int c = 0; c < w; ++c) {
-      const int gr = j0 + c;
-      double best = -1.0;
-      int bi = 0x7fffffff;
-      for (int r = tid; r < n; r += kPlThreads)
-        if (r >= gr) {
-          const double v = fabs(S[c * ld + r]);
-          if (v > best) { best = v; bi = r; }
-        }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-      }
-      if (lane == 0) { cval[wid] = best; cidx[wid] = bi; }
-      __syncthreads();
-      best = cval[lane & (kPlWarps - 1)];
-      bi = cidx[lane & (kPlWarps - 1)];
-#pragma unroll
-      for (int o = kPlWarps / 2; o > 0; o >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-      }
-      const int p = (bi == 0x7fffffff) ? gr : bi;  // an all-NaN column pivots on itself
-      if (tid < kPlNb && p != gr) {
-        const double tmp = S[tid * ld + gr];
-        S[tid * ld + gr] = S[tid * ld + p];
-        S[tid * ld + p] = tmp;
-      }
-      if (tid == 0) a.piv[gr] = p;
-      __syncthreads();
-      const double d = S[c * ld + gr];
-      if (d != 0.0) {
-        const double inv = 1.0 / d;
+    if (n <= kPlThreads * kPlRpt) {
+      pl_panel_reg(S, ld, n, j0, w, a.piv, cval, cidx, prow, grow);
+    } else {
+      for (int c = 0; c < w; ++c) {
+        const int gr = j0 + c;
+        double best = -1.0;
+        int bi = 0x7fffffff;
         for (int r = tid; r < n; r += kPlThreads)
-          if (r > gr) {
-            const double l = S[c * ld + r] * inv;
-            S[c * ld + r] = l;
-            for (int c2 = c + 1; c2 < w; ++c2) S[c2 * ld + r] = fma(-l, S[c2 * ld + gr], S[c2 * ld + r]);
+          if (r >= gr) {
+            const double v = fabs(S[c * ld + r]);
+            if (v > best) { best = v; bi = r; }
           }
+  #pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+        }
+        if (lane == 0) { cval[wid] = best; cidx[wid] = bi; }
+        __syncthreads();
+        best = cval[lane & (kPlWarps - 1)];
+        bi = cidx[lane & (kPlWarps - 1)];
+  #pragma unroll
+        for (int o = kPlWarps / 2; o > 0; o >>= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+        }
+        const int p = (bi == 0x7fffffff) ? gr : bi;  // an all-NaN column pivots on itself
+        if (tid < kPlNb && p != gr) {
+          const double tmp = S[tid * ld + gr];
+          S[tid * ld + gr] = S[tid * ld + p];
+          S[tid * ld + p] = tmp;
+        }
+        if (tid == 0) a.piv[gr] = p;
+        __syncthreads();
+        const double d = S[c * ld + gr];
+        if (d != 0.0) {
+          const double inv = 1.0 / d;
+          for (int r = tid; r < n; r += kPlThreads)
+            if (r > gr) {
+              const double l = S[c * ld + r] * inv;
+              S[c * ld + r] = l;
+#pragma unroll
+              for (int c2 = 0; c2 < kPlNb; ++c2)
+                if (c2 > c && c2 < w) S[c2 * ld + r] = fma(-l, S[c2 * ld + gr], S[c2 * ld + r]);
+            }
+        }
+        // no trailing barrier: the next column's search reads only this thread's
+        // own rows; the pivot row it broadcasts is swapped before the next barrier
       }
-      // no trailing barrier: the next column's search reads only this thread's
-      // own rows; the pivot row it broadcasts is swapped before the next barrier
     }
     __syncthreads();
     for (int idx = tid; idx < kPlNb * n; idx += kPlThreads) {

@@ -805,7 +805,7 @@ int window_width() {
   return v;
 }
 
-size_t wproj_stage_bytes(int c) { return (size_t)(round_up(std::max(c, 1), 8) + kWB) * kWLd * 8; }
+size_t wproj_stage_bytes(int c) { return wproj_stage_elems(std::max(c, 1)) * 8; }
 
 template <int MT>
 void launch_wproj_t(const WprojArgs& a, int cols_ub, cudaStream_t s) {

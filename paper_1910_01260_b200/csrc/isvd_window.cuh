@@ -8,12 +8,10 @@
 // their rows of G from XX (window_row, isvd_kernels.cuh).  Bytes per snapshot
 // drop from 8 n (c + 3) to 8 n ((c + kWB) / kWB + [independent] (c + 2)).
 //
-// k_wproj: one CTA per SM (minus the core step's), a warp of bulk-copy
-// producers and 8 consumer warps.  Each 64-row stage holds the c live U column
-// segments and the kWB x segments, each copied into a 68-double slot so the
-// DMMA fragment loads (8 columns x 4 rows per load) hit distinct banks.  The
-// contraction G_cta += U_tile^T X_tile is DMMA m8n8k4 (M = U columns, N = the
-// window, K = rows); per-CTA partials are summed by k_wreduce in a fixed order.
+// k_wproj: one CTA per SM (minus the core step's), a bulk-copy producer warp
+// and 8 consumer warps.  The contraction G_cta += U_tile^T X_tile is DMMA
+// m8n8k4 (M = U columns, N = the window, K = rows); per-CTA partials are
+// summed by k_wreduce in a fixed order.
 #pragma once
 
 #include "isvd_kernels.cuh"
@@ -21,7 +19,7 @@
 
 namespace strom {
 
-constexpr int kWLd = kStageRows + 4;  // 68: padded column slot in a window stage
+constexpr int kWXLd = kStageRows + 8;  // 72: x slot stride (conflict-free 16-byte fragment loads)
 constexpr int kWConsumers = 8;
 constexpr int kWThreads = 32 * (kWConsumers + 1);
 constexpr int kWMaxStages = 4;
@@ -39,6 +37,15 @@ struct WprojArgs {
   long long* trace;
 };
 
+// Stage layout: the tile's c live U column segments as ONE contiguous bulk copy
+// (a TMA op costs tens of cycles whatever its size: one per stage, not one per
+// column), then kWB x slots of kWXLd doubles.  Fragment loads are 16 bytes:
+// k-steps are taken in pairs whose rows interleave (lane t of pair kp holds
+// rows 8 kp + 2t and 8 kp + 2t + 1), so one LDS.128 feeds two DMMAs.
+__host__ __device__ inline size_t wproj_stage_elems(int c) {
+  return (size_t)c * kStageRows + (size_t)kWB * kWXLd;
+}
+
 template <int MT>  // m-tiles (8 U columns) per consumer warp: c <= 64 MT
 __global__ void __launch_bounds__(kWThreads, 1) k_wproj(WprojArgs a, int nstages) {
   extern __shared__ __align__(128) double wst[];
@@ -49,8 +56,8 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wproj(WprojArgs a, int nstages
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
   const int c = a.ctl->c, base = a.ctl->base;
   const int c8 = (c + 7) & ~7;
-  const int cs = c8 + kWB;
-  const size_t stage_elems = (size_t)cs * kWLd;
+  const size_t stage_elems = wproj_stage_elems(c);
+  const size_t xoff = (size_t)c * kStageRows;
   const int64_t tstride = (int64_t)kUTile * a.ccap;
   if (a.prof && blockIdx.x == 0 && threadIdx.x == 0)
     atomicAdd(a.prof + P_WPROJ, 8ull * (unsigned long long)a.n * (unsigned long long)(c + a.nw));
@@ -58,10 +65,6 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wproj(WprojArgs a, int nstages
   const int64_t per = ceil_div(ntiles, gridDim.x);
   const int64_t t0 = blockIdx.x * per;
   const int64_t nt = max((int64_t)0, min(ntiles, t0 + per) - t0);
-  // U padding columns c..c8-1 are never copied: zero them once in every stage
-  for (int st = 0; st < nstages; ++st)
-    for (int idx = threadIdx.x; idx < (c8 - c) * kWLd; idx += blockDim.x)
-      wst[st * stage_elems + (size_t)c * kWLd + idx] = 0.0;
   if (threadIdx.x == 0) {
     for (int st = 0; st < nstages; ++st) {
       mbar_init(&full[st], 1);
@@ -71,22 +74,22 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wproj(WprojArgs a, int nstages
   }
   __syncthreads();
   if (wid == 0) {
-    // ---------------- producers: lane 0 arms the stage, all lanes issue copies
-    for (int64_t i = 0; i < nt; ++i) {
-      const int st = (int)(i % nstages);
-      const int64_t use = i / nstages;
-      if (use > 0) mbar_wait(&empty[st], (unsigned)((use - 1) & 1));
-      const int64_t row0 = (t0 + i) * kStageRows;
-      const int valid = (int)max((int64_t)0, min((int64_t)kStageRows, a.n - row0));
-      const unsigned xb = a.xbulk ? (unsigned)valid * 8u : 0u;
-      if (lane == 0) mbar_expect_tx(&full[st], (unsigned)c * kStageRows * 8u + xb * (unsigned)a.nw);
-      __syncwarp();
-      double* dst = wst + (size_t)st * stage_elems;
-      const double* src = a.U + (t0 + i) * tstride + (int64_t)base * kUTile;
-      for (int col = lane; col < c; col += 32)
-        bulk_g2s(dst + (size_t)col * kWLd, src + (int64_t)col * kUTile, kStageRows * 8u, &full[st]);
-      if (xb)
-        for (int j = lane; j < a.nw; j += 32) bulk_g2s(dst + (size_t)(c8 + j) * kWLd, a.xs[j] + row0, xb, &full[st]);
+    // ---------------- producer: lane 0 issues one U copy and the x copies per stage
+    if (lane == 0) {
+      for (int64_t i = 0; i < nt; ++i) {
+        const int st = (int)(i % nstages);
+        const int64_t use = i / nstages;
+        if (use > 0) mbar_wait(&empty[st], (unsigned)((use - 1) & 1));
+        const int64_t row0 = (t0 + i) * kStageRows;
+        const int valid = (int)max((int64_t)0, min((int64_t)kStageRows, a.n - row0));
+        const unsigned ub = (unsigned)c * kStageRows * 8u;
+        const unsigned xb = a.xbulk ? (unsigned)valid * 8u : 0u;
+        mbar_expect_tx(&full[st], ub + xb * (unsigned)a.nw);
+        double* dst = wst + (size_t)st * stage_elems;
+        if (ub) bulk_g2s(dst, a.U + (t0 + i) * tstride + (int64_t)base * kUTile, ub, &full[st]);
+        if (xb)
+          for (int j = 0; j < a.nw; ++j) bulk_g2s(dst + xoff + (size_t)j * kWXLd, a.xs[j] + row0, xb, &full[st]);
+      }
     }
   } else {
     // ---------------- consumers: warp cw owns m-tiles cw, cw + 8, ...
@@ -103,21 +106,30 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wproj(WprojArgs a, int nstages
       const double* tile = wst + (size_t)st * stage_elems;
       const int64_t row0 = (t0 + i) * kStageRows;
       const int valid = (int)max((int64_t)0, min((int64_t)kStageRows, a.n - row0));
-#pragma unroll 4
-      for (int ks = 0; ks < kStageRows / 4; ++ks) {
-        const int kr = 4 * ks + t;
-        double b;
-        if (a.xbulk) b = (xg && kr < valid) ? tile[(size_t)(c8 + g) * kWLd + kr] : 0.0;
-        else b = (xg && kr < valid) ? __ldg(xg + row0 + kr) : 0.0;
+#pragma unroll 2
+      for (int kp = 0; kp < kStageRows / 8; ++kp) {
+        const int kr = 8 * kp + 2 * t;  // this lane's two rows of the k-step pair
+        double2 b = make_double2(0.0, 0.0);
+        if (xg) {
+          if (a.xbulk) b = *reinterpret_cast<const double2*>(tile + xoff + (size_t)g * kWXLd + kr);
+          else if (kr < valid) b = make_double2(__ldg(xg + row0 + kr), kr + 1 < valid ? __ldg(xg + row0 + kr + 1) : 0.0);
+          if (kr >= valid) b.x = 0.0;
+          if (kr + 1 >= valid) b.y = 0.0;
+        }
 #pragma unroll
         for (int q = 0; q < MT; ++q) {
-          const int mt = cw + kWConsumers * q;
-          if (8 * mt < c) {
-            const double av = tile[(size_t)(8 * mt + g) * kWLd + kr];
-            dmma884(acc[q][0], acc[q][1], av, b);
+          const int col = 8 * (cw + kWConsumers * q) + g;
+          if (8 * (cw + kWConsumers * q) < c) {
+            const double2 u = col < c ? *reinterpret_cast<const double2*>(tile + (size_t)col * kStageRows + kr)
+                                      : make_double2(0.0, 0.0);
+            dmma884(acc[q][0], acc[q][1], u.x, b.x);
+            dmma884(acc[q][0], acc[q][1], u.y, b.y);
           }
         }
-        if (cw == 0) dmma884(xa0, xa1, b, b);  // XX = X^T X (A = X^T: a = X(kr, g) = b)
+        if (cw == 0) {  // XX = X^T X (A = X^T: a = X(kr, g) = b)
+          dmma884(xa0, xa1, b.x, b.x);
+          dmma884(xa0, xa1, b.y, b.y);
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
