@@ -313,7 +313,7 @@ PipeMem make_pipe(const Caps& c, cudaStream_t s) {
   m.ccap = c.ccap;
   m.rcap = c.rcap;
   m.max_grid = sm_count() * 8;
-  m.pstride = (int)(2 * round_up(c.ccap + 1, 4) + 8);
+  m.pstride = (int)(2 * round_up(c.ccap + 1, 4) + 16);
   const int64_t rc2 = c.rcap + 2;
   m.work_stride = (int)round_up(std::max<int64_t>(c.ccap, rc2), 32);
   const size_t work_elems = 4 * (size_t)m.work_stride + 3 * rc2 * rc2 + 16 * (size_t)m.work_stride +
@@ -323,7 +323,7 @@ PipeMem make_pipe(const Caps& c, cudaStream_t s) {
   m.ldg = (int)round_up(c.ccap + 1, 8);
   m.wpstride = (int)(round_up(c.ccap, 8) * kWB + kWB * kWB);
   const size_t n_win = (size_t)m.ldg * kWB + kWB * kWB + (size_t)m.max_grid * m.wpstride + rc2 * rc2;
-  size_t total = 2 * nell + 2 * nv + 7 * nv + 2 * (2 * nv + 8) + rc2 * rc2 + work_elems + (size_t)c.ccap * rc2 + n_part +
+  size_t total = 2 * nell + 2 * nv + 7 * nv + 2 * (2 * nv + 8 + kWB) + rc2 * rc2 + work_elems + (size_t)c.ccap * rc2 + n_part +
                  n_win;
   total = round_up(total, 32);
   const size_t bytes = total * 8 + 512;
@@ -341,9 +341,11 @@ PipeMem make_pipe(const Caps& c, cudaStream_t s) {
   m.pp.fo.e = p; p += nv;
   m.pp.fo.gn = p; p += nv;
   m.pp.fo.scal = p; p += 8;
+  m.pp.fo.gw = p; p += kWB;
   m.pp.ro.e = p; p += nv;
   m.pp.ro.gn = p; p += nv;
   m.pp.ro.scal = p; p += 8;
+  m.pp.ro.gw = p; p += kWB;
   m.pp.vbar = p; p += rc2 * rc2;
   m.pp.work = p; p += work_elems;
   m.pp.T = p; p += (size_t)c.ccap * rc2;
@@ -466,8 +468,11 @@ struct PassTail {
 };
 
 void launch_pass(int kind, int cols_ub, const strom_isvd* h, const PipeMem& m, const double* x, const double* xn,
-                 int reserve, cudaStream_t s, const PassTail& tl = PassTail()) {
+                 int reserve, cudaStream_t s, const PassTail& tl = PassTail(), const double* const* xw = nullptr,
+                 int nxw = 0) {
   PassArgs a;
+  a.nxw = nxw;
+  for (int j = 0; j < kWB - 1; ++j) a.xw[j] = j < nxw ? xw[j] : nullptr;
   a.U = h->store->U();
   a.ldu = h->ldu;
   a.n = h->n;
@@ -1379,11 +1384,14 @@ strom_isvd* ingest_windowed(strom_isvd* src, ColumnSource& cols, cudaStream_t s,
     pp.fo.gn = m.wG + (int64_t)(P.has_next ? P.wcol + 1 : 0) * m.ldg;
     pp.vbar = (t & 1) ? m.vbar2 : m.pp.vbar;
     const double* xt = cols.col(t);
+    const double* xw[kWB];
+    const int nxw = (int)(wn - 1 - P.wcol);
+    for (int j = 0; j < nxw; ++j) xw[j] = cols.col(t + 1 + j);
     if (b_launched > 0) STROM_CUDA(cudaStreamWaitEvent(s, evB, 0));  // k_step_b(t-1) wrote N, sigma
     launch_decide_w(0, prev->view, pp, m, P, s);
-    launch_pass(PASS_RESID, cols_ub, dst, m, xt, nullptr, 1, s);
+    launch_pass(PASS_RESID, cols_ub, dst, m, xt, nullptr, 1, s, PassTail(), xw, nxw);
     launch_decide_w(1, prev->view, pp, m, P, s);
-    launch_pass(PASS_SECOND, cols_ub, dst, m, xt, nullptr, 1, s);
+    launch_pass(PASS_SECOND, cols_ub, dst, m, xt, nullptr, 1, s, PassTail(), xw, nxw);
     launch_decide_w(2, prev->view, pp, m, P, s);
     ++d_launched;
     cols.release(t);

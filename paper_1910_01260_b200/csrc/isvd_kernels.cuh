@@ -96,6 +96,7 @@ struct PassOut {
   double* e;
   double* gn;
   double* scal;
+  double* gw;  // window mode: r . x_j for the window's later snapshots (measured on the stored r)
 };
 
 // What k_vupdate needs from k_step_b, in a record of its own: in window mode
@@ -261,6 +262,10 @@ struct PassArgs {
   unsigned* counter;
   unsigned long long* prof;
   long long* trace;  // diagnostics: this update's trace row, or null
+  // window mode: dots of the new column r with these later snapshots of the
+  // window (consumer warp w takes column w); one more read of nxw columns
+  const double* xw[kWB - 1];
+  int32_t nxw;
 };
 
 constexpr int kPassMaxStages = 8;
@@ -328,8 +333,17 @@ constexpr double kFoldTau = 1e-3;  // append r1 only if its out-of-span part is 
 // Window mode: row `row` of the window projections for the snapshots after
 // this one, for a U column r = x_t - U (coef + coef2) (coef null: r = x_t):
 //   G[row, j] = x_t . x_j - (coef + coef2)^T G[:c, j]      (j = wcol+1 .. wn-1)
-// -- the same quantity the per-snapshot pass measured as r . x_next, from the
-// window's Gram instead of another read of U.  One warp per window column.
+// Only used with coef null (the slot holds x_t itself: its dots ARE the
+// window Gram); a residual's row is measured by its pass (window_row_measured):
+// the algebraic form loses all relative accuracy when r is rounding-level.
+// Row `row` of the window projections from a pass's measured dots gw[j - wcol - 1].
+__device__ inline void window_row_measured(const IsvdParams& P, int row, const double* gw) {
+  __syncthreads();
+  for (int j = P.wcol + 1 + (int)threadIdx.x; j < P.wn; j += blockDim.x)
+    P.wG[(int64_t)j * P.ldg + row] = gw[j - P.wcol - 1];
+  __syncthreads();
+}
+
 __device__ inline void window_row(const IsvdParams& P, int row, int c, const double* coef, const double* coef2) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   __syncthreads();
@@ -526,9 +540,9 @@ __device__ inline void decide2_body(const StateView& src, const Pipe& pp, const 
   double lam = 0.0;
   if (ro == 1) {
     const double p = st->p;
-    // window mode: the row of r2 = x - U (gt + h) for the rest of the window,
-    // before h is reused (harmless if r2 is not appended: c does not grow)
-    if (P.wn > 0) window_row(P, c, c, pp.gt, pp.h);
+    // window mode: the row of r2 for the rest of the window, as the second pass
+    // measured it (harmless if r2 is not appended: c does not grow)
+    if (P.wn > 0) window_row_measured(P, c, pp.ro.gw);
     double* l2 = pp.h;  // h is spent
     cta_gemv_cm<8>(Lib, ldl, c, c, pp.ro.e, 1.0, nullptr, l2, part, true);
     double pq = 0.0;
@@ -702,8 +716,9 @@ __device__ inline void decide_b_body(const StateView& src, const Pipe& pp, const
     const bool room = (slot < P.ccap) && ((int64_t)c < P.n);
     const bool app = room && (lam2 > kFoldTau * kFoldTau * rho2) && (rho2 > 0.0);
     if (app) {
-      // r1 = x - U gt becomes U column c: its row of the window (and g'_c = r1 . x_next)
-      window_row(P, c, c, pp.gt, nullptr);
+      // r1 becomes U column c: its row of the window (and g'_c = r1 . x_next), as
+      // the residual pass measured it on the stored r1
+      window_row_measured(P, c, pp.fo.gw);
       lam = sqrt(lam2);
       const double tc = nx ? (pp.fo.gn[c] - s_lt) / lam : 0.0;
       if (nx)
@@ -879,7 +894,8 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(PassArgs a, int nstage
     double ae[MAXJ], ag[MAXJ];
 #pragma unroll
     for (int q = 0; q < MAXJ; ++q) { ae[q] = 0.0; ag[q] = 0.0; }
-    double rr = 0.0, gs = 0.0, xq = 0.0;
+    double rr = 0.0, gs = 0.0, xq = 0.0, gwa = 0.0;
+    const double* xwc = (cw < a.nxw) ? a.xw[cw] : nullptr;
     for (int64_t i = 0; i < nt; ++i) {
       const int st = (int)(i % nstages);
       const int64_t use = i / nstages;
@@ -945,6 +961,10 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(PassArgs a, int nstage
         }
         if (!live0) r.x = 0.0;
         if (!live1) r.y = 0.0;
+        if (do_r && xwc) {  // r . x_j against the stored (rounded) r, not an algebraic proxy
+          const double w0 = live0 ? __ldg(xwc + row) : 0.0, w1 = live1 ? __ldg(xwc + row + 1) : 0.0;
+          gwa = fma(r.y, w1, fma(r.x, w0, gwa));
+        }
         if (do_r) {
           if (cw == kPassConsumers - 1) {
             reinterpret_cast<double2*>(scol)[lane] = r;
@@ -988,6 +1008,10 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(PassArgs a, int nstage
         mypart[2 * PG + 2] = gs;
       }
     }
+    if (xwc) {
+      gwa = warp_sum(gwa);
+      if (lane == 0) mypart[2 * PG + 3 + cw] = gwa;
+    }
   }
   if (!last_cta_arrives(a.counter, &s_last)) return;
   if (a.trace && threadIdx.x == 0 && a.kind != PASS_SECOND) {
@@ -999,7 +1023,8 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(PassArgs a, int nstage
   const int PG = (a.pstride - 8) / 2;
   const int nwarps = blockDim.x >> 5;
   const int ne = do_e ? c : 0, ng = do_gn ? c : 0;
-  const int nout = ne + ng + 3;
+  const int nxw = x ? a.nxw : 0;
+  const int nout = ne + ng + 3 + nxw;
   for (int o = wid; o < nout; o += nwarps) {
     int col;
     if (o < ne) col = o;
@@ -1020,7 +1045,8 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(PassArgs a, int nstage
       else if (o < ne + ng) a.out.gn[o - ne] = sum;
       else {
         const int k = o - ne - ng;
-        a.out.scal[k] = sum;
+        if (k < 3) a.out.scal[k] = sum;
+        else a.out.gw[k - 3] = sum;
         if (k == 2 && a.kind == PASS_FUSED && do_gn) a.out.gn[c] = sum;  // r . x_next
       }
     }
