@@ -984,7 +984,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(PassArgs a, int nstage
       }
     }
     // per-CTA partials: [0, PG) e | [PG, 2 PG) gn | 2 PG + {0: r.r, 1: xn.xn, 2: r.xn}
-    const int PG = (a.pstride - 8) / 2;
+    const int PG = (a.pstride - 16) / 2;  // [e | gn | r.r, xn.xn, r.xn, r.x_w (kWB - 1)]
     double* mypart = a.part + (int64_t)blockIdx.x * a.pstride;
 #pragma unroll
     for (int q = 0; q < MAXJ; ++q) {
@@ -1020,7 +1020,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(PassArgs a, int nstage
     a.trace[3] = (long long)tt;
   }
   // one warp per output, lanes stride over the CTA partials, fixed tree: deterministic
-  const int PG = (a.pstride - 8) / 2;
+  const int PG = (a.pstride - 16) / 2;  // [e | gn | r.r, xn.xn, r.xn, r.x_w (kWB - 1)]
   const int nwarps = blockDim.x >> 5;
   const int ne = do_e ? c : 0, ng = do_gn ? c : 0;
   const int nxw = x ? a.nxw : 0;
