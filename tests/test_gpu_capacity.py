@@ -56,4 +56,6 @@ def test_capacity_stream_invariants(cuda):
     q = s.q_columns(0, m)
     sv = torch.linalg.svdvals(phi[:, :m].T @ q).clamp(max=1.0)
     sin_max = float(torch.sqrt(1 - sv.min() ** 2))
+    print(f"capacity invariants: sigma rel {float(rel[:16].max()):.2e}, leading-{m} sine {sin_max:.3e} "
+          f"(noise limit {noise_rel / float(s.sigma[m - 1]):.3e})")
     assert sin_max <= 10 * noise_rel / float(s.sigma[m - 1])
