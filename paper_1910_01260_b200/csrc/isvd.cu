@@ -489,7 +489,11 @@ void launch_pass(int kind, int cols_ub, const strom_isvd* h, const PipeMem& m, c
   };
   a.x_bulk = bulk_ok(x) ? 1 : 0;
   a.xn_bulk = bulk_ok(xn) ? 1 : 0;
-  a.xw_bulk = 1;
+  static const bool xw_stage = [] {
+    const char* e = getenv("STROM_XW_STAGE");
+    return !(e && atoi(e) == 0);
+  }();
+  a.xw_bulk = xw_stage ? 1 : 0;
   for (int j = 0; j < nxw; ++j)
     if (!bulk_ok(xw[j])) a.xw_bulk = 0;
   a.ctl = m.pp.ctl;
@@ -944,7 +948,8 @@ struct ColumnSource {
   const int64_t kChunk = env_int("STROM_H2D_CHUNK", 4);
   // at least 2 slots: col(t + 1) is requested before release(t) issues the
   // next chunk, so one slot would hand out a column still being copied
-  const int kRing = (int)std::max<int64_t>(2, env_int("STROM_H2D_RING", 4));
+  // (window mode reads kWB columns ahead: 6 slots keep the copies ahead of it)
+  const int kRing = (int)std::max<int64_t>(2, env_int("STROM_H2D_RING", 6));
   static int64_t env_int(const char* name, int64_t dflt) {
     const char* e = getenv(name);
     return e && atoll(e) > 0 ? atoll(e) : dflt;

@@ -933,6 +933,14 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(PassArgs a, int nstage
         }
         if (!live0) { xv.x = 0.0; xnv.x = 0.0; }
         if (!live1) { xv.y = 0.0; xnv.y = 0.0; }
+        // this warp's later window snapshot (r . x_j below): read before the stage is released
+        double2 wv = make_double2(0.0, 0.0);
+        if (do_r && xwc) {
+          if (nxw_st) wv = reinterpret_cast<const double2*>(tile + (xw_col + cw) * kStageRows + hh * kSubRows)[lane];
+          else wv = make_double2(live0 ? __ldg(xwc + row) : 0.0, live1 ? __ldg(xwc + row + 1) : 0.0);
+          if (!live0) wv.x = 0.0;
+          if (!live1) wv.y = 0.0;
+        }
         double2 u[MAXJ];
 #pragma unroll
         for (int q = 0; q < MAXJ; ++q) {
@@ -967,19 +975,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(PassArgs a, int nstage
         }
         if (!live0) r.x = 0.0;
         if (!live1) r.y = 0.0;
-        if (do_r && xwc) {  // r . x_j against the stored (rounded) r, not an algebraic proxy
-          double w0, w1;
-          if (nxw_st) {
-            const double2 wv =
-                reinterpret_cast<const double2*>(tile + (xw_col + cw) * kStageRows + hh * kSubRows)[lane];
-            w0 = live0 ? wv.x : 0.0;
-            w1 = live1 ? wv.y : 0.0;
-          } else {
-            w0 = live0 ? __ldg(xwc + row) : 0.0;
-            w1 = live1 ? __ldg(xwc + row + 1) : 0.0;
-          }
-          gwa = fma(r.y, w1, fma(r.x, w0, gwa));
-        }
+        if (do_r && xwc) gwa = fma(r.y, wv.y, fma(r.x, wv.x, gwa));  // r . x_j on the stored (rounded) r
         if (do_r) {
           if (cw == kPassConsumers - 1) {
             reinterpret_cast<double2*>(scol)[lane] = r;
