@@ -817,6 +817,14 @@ int window_width() {
   return v;
 }
 
+bool decide_spins() {
+  static const bool v = [] {
+    const char* e = getenv("STROM_DECIDE_EVENT");
+    return !(e && atoi(e) != 0);
+  }();
+  return v;
+}
+
 size_t wproj_stage_bytes(int c) { return wproj_stage_elems(std::max(c, 1)) * 8; }
 
 template <int MT>
@@ -1384,7 +1392,9 @@ strom_isvd* ingest_windowed(strom_isvd* src, ColumnSource& cols, cudaStream_t s,
     P.wn = (int)wn;
     P.wcol = (int)(t - w0);
     P.has_next = (P.wcol + 1 < P.wn) ? 1 : 0;
-    P.b_expect = -1;
+    // k_decide_a(t) spins on the device counter k_step_b(t-1) bumps (STROM_DECIDE_EVENT=1:
+    // a cross-stream event instead); no pass competes for SMs while it waits
+    P.b_expect = decide_spins() ? (int32_t)b_launched : -1;
     P.d_expect = (int32_t)(d_launched + 1);
     P.trace = (g_trace && t < g_trace_rows) ? g_trace + 16 * t : nullptr;
     g_cur_trace = P.trace;
@@ -1395,7 +1405,7 @@ strom_isvd* ingest_windowed(strom_isvd* src, ColumnSource& cols, cudaStream_t s,
     const double* xw[kWB];
     const int nxw = (int)(wn - 1 - P.wcol);
     for (int j = 0; j < nxw; ++j) xw[j] = cols.col(t + 1 + j);
-    if (b_launched > 0) STROM_CUDA(cudaStreamWaitEvent(s, evB, 0));  // k_step_b(t-1) wrote N, sigma
+    if (b_launched > 0 && !decide_spins()) STROM_CUDA(cudaStreamWaitEvent(s, evB, 0));  // k_step_b(t-1) wrote N
     launch_decide_w(0, prev->view, pp, m, P, s);
     launch_pass(PASS_RESID, cols_ub, dst, m, xt, nullptr, 1, s, PassTail(), xw, nxw);
     launch_decide_w(1, prev->view, pp, m, P, s);

@@ -1036,29 +1036,39 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(PassArgs a, int nstage
   const int ne = do_e ? c : 0, ng = do_gn ? c : 0;
   const int nxw = x ? a.nxw : 0;
   const int nout = ne + ng + 3 + nxw;
-  for (int o = wid; o < nout; o += nwarps) {
-    int col;
-    if (o < ne) col = o;
-    else if (o < ne + ng) col = PG + (o - ne);
-    else col = 2 * PG + (o - ne - ng);
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    int b = lane;
-    for (; b + 96 < (int)gridDim.x; b += 128) {
-      s0 += a.part[(int64_t)b * a.pstride + col];
-      s1 += a.part[(int64_t)(b + 32) * a.pstride + col];
-      s2 += a.part[(int64_t)(b + 64) * a.pstride + col];
-      s3 += a.part[(int64_t)(b + 96) * a.pstride + col];
+  // four outputs per warp at a time (their loads in flight together); each
+  // output keeps the same lane / stripe summation order: deterministic
+  auto out_col = [&](int o) { return o < ne ? o : (o < ne + ng ? PG + (o - ne) : 2 * PG + (o - ne - ng)); };
+  for (int o0 = wid; o0 < nout; o0 += 4 * nwarps) {
+    double s[4][4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int o = o0 + q * nwarps;
+      s[q][0] = s[q][1] = s[q][2] = s[q][3] = 0.0;
+      if (o >= nout) continue;
+      const int col = out_col(o);
+      int b = lane;
+      for (; b + 96 < (int)gridDim.x; b += 128) {
+        s[q][0] += a.part[(int64_t)b * a.pstride + col];
+        s[q][1] += a.part[(int64_t)(b + 32) * a.pstride + col];
+        s[q][2] += a.part[(int64_t)(b + 64) * a.pstride + col];
+        s[q][3] += a.part[(int64_t)(b + 96) * a.pstride + col];
+      }
+      for (; b < (int)gridDim.x; b += 32) s[q][0] += a.part[(int64_t)b * a.pstride + col];
     }
-    for (; b < (int)gridDim.x; b += 32) s0 += a.part[(int64_t)b * a.pstride + col];
-    const double sum = warp_sum((s0 + s1) + (s2 + s3));
-    if (lane == 0) {
-      if (o < ne) a.out.e[o] = sum;
-      else if (o < ne + ng) a.out.gn[o - ne] = sum;
-      else {
-        const int k = o - ne - ng;
-        if (k < 3) a.out.scal[k] = sum;
-        else a.out.gw[k - 3] = sum;
-        if (k == 2 && a.kind == PASS_FUSED && do_gn) a.out.gn[c] = sum;  // r . x_next
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int o = o0 + q * nwarps;
+      const double sum = warp_sum((s[q][0] + s[q][1]) + (s[q][2] + s[q][3]));
+      if (lane == 0 && o < nout) {
+        if (o < ne) a.out.e[o] = sum;
+        else if (o < ne + ng) a.out.gn[o - ne] = sum;
+        else {
+          const int k = o - ne - ng;
+          if (k < 3) a.out.scal[k] = sum;
+          else a.out.gw[k - 3] = sum;
+          if (k == 2 && a.kind == PASS_FUSED && do_gn) a.out.gn[c] = sum;  // r . x_next
+        }
       }
     }
   }
