@@ -272,9 +272,10 @@ struct PassArgs {
 constexpr int kPassMaxStages = 8;
 
 
-// The pass: warp 0 streams U (kStageRows rows x c columns per stage, 2D TMA
-// boxes of kStageRows x 8) into a ring of shared-memory stages (full/empty
-// mbarriers); the kPassConsumers consumer warps process every stage together
+// The pass: lane 0 of warp 0 streams U (kStageRows rows x c columns per stage:
+// the tile's live column segments are contiguous, so ONE 1-D bulk copy,
+// cp.async.bulk, plus one per x / x_next / window segment) into a ring of
+// shared-memory stages (full/empty mbarriers); the kPassConsumers consumer warps process every stage together
 // -- warp w owns columns w + 8q, lane l rows 2l, 2l+1 -- and exchange row-dot
 // partials through a double-buffered shared array with ONE consumer-only named
 // barrier per stage.  Column dots stay in registers until a deterministic
