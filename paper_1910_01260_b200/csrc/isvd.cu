@@ -817,10 +817,13 @@ int window_width() {
   return v;
 }
 
+// Measured: spinning k_decide_a on the core step's counter (STROM_DECIDE_SPIN=1)
+// is slower than the cross-stream event -- the spinner and the core step it
+// waits for hold SMs the V update and the passes then queue behind.
 bool decide_spins() {
   static const bool v = [] {
-    const char* e = getenv("STROM_DECIDE_EVENT");
-    return !(e && atoi(e) != 0);
+    const char* e = getenv("STROM_DECIDE_SPIN");
+    return e && atoi(e) != 0;
   }();
   return v;
 }
@@ -1392,8 +1395,8 @@ strom_isvd* ingest_windowed(strom_isvd* src, ColumnSource& cols, cudaStream_t s,
     P.wn = (int)wn;
     P.wcol = (int)(t - w0);
     P.has_next = (P.wcol + 1 < P.wn) ? 1 : 0;
-    // k_decide_a(t) spins on the device counter k_step_b(t-1) bumps (STROM_DECIDE_EVENT=1:
-    // a cross-stream event instead); no pass competes for SMs while it waits
+    // k_decide_a(t) waits for k_step_b(t-1) on a cross-stream event (or spins on
+    // its device counter with STROM_DECIDE_SPIN=1)
     P.b_expect = decide_spins() ? (int32_t)b_launched : -1;
     P.d_expect = (int32_t)(d_launched + 1);
     P.trace = (g_trace && t < g_trace_rows) ? g_trace + 16 * t : nullptr;
