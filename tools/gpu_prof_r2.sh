@@ -13,10 +13,11 @@ run() {  # name, kernel regex, skip, count, command...
 timeout 600 python tools/profile_isvd.py --cols 150 > $out/plain_isvd.log 2>&1 && {
   timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
       --log-file $out/launches_isvd.csv python tools/profile_isvd.py --cols 40 > $out/ncu_launch.log 2>&1
-  run step_b 'k_step_b' 150 2 python tools/profile_isvd.py --cols 40
-  run decide 'k_decide' 300 3 python tools/profile_isvd.py --cols 40
-  run vupdate 'k_vupdate' 150 2 python tools/profile_isvd.py --cols 40
-  run pass 'k_pass' 230 2 python tools/profile_isvd.py --cols 40
+  run step_b 'k_step_b' 110 2 python tools/profile_isvd.py --cols 40
+  run decide 'k_decide' 330 4 python tools/profile_isvd.py --cols 40
+  run vupdate 'k_vupdate' 110 2 python tools/profile_isvd.py --cols 40
+  run pass 'k_pass' 120 4 python tools/profile_isvd.py --cols 40
+  run wproj 'k_wproj' 14 2 python tools/profile_isvd.py --cols 40
   run compact 'k_compact' 0 4 python tools/profile_isvd.py --cols 150
 }
 timeout 600 python tools/prof_targets.py st 2 > $out/plain_st.log 2>&1 && {
