@@ -9,6 +9,11 @@ run() {  # name, kernel regex, skip, count, command...
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"$rx" -s $skip -c $cnt \
       -o $out/$name "$@" > $out/ncu_$name.log 2>&1
   echo "$name rc=$?" >> $out/status.txt
+  # summaries on the box (the reports themselves exceed gpurun's copy-back cap)
+  python tools/ncu_summary.py $out/$name.ncu-rep > $out/sum_$name.txt 2>&1
+  python tools/ncu_stalls.py $out/$name.ncu-rep "$rx" > $out/stalls_$name.txt 2>&1
+  ncu -i $out/$name.ncu-rep --page details --csv > $out/details_$name.csv 2>/dev/null
+  rm -f $out/$name.ncu-rep
 }
 timeout 600 python tools/profile_isvd.py --cols 150 > $out/plain_isvd.log 2>&1 && {
   timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
