@@ -833,7 +833,7 @@ size_t wproj_stage_bytes(int c) { return wproj_stage_elems(std::max(c, 1)) * 8; 
 template <int MT>
 void launch_wproj_t(const WprojArgs& a, int cols_ub, cudaStream_t s) {
   const size_t per = wproj_stage_bytes(cols_ub);
-  const size_t budget = max_smem_optin() - 2048;
+  const size_t budget = max_smem_optin() - 24 * 1024;  // the static half-sum buffer
   const int nst = (int)std::max<size_t>(1, std::min<size_t>(kWMaxStages, std::min<size_t>(3, budget / per)));
   const size_t smem = (size_t)nst * per;
   static PerDevice<size_t> cfg;
@@ -870,7 +870,7 @@ void launch_window(const strom_isvd* h, const PipeMem& m, const double* const* x
   a.prof = prof_dev_bytes();
   a.trace = g_cur_trace;
   const int cu = std::max(cols_ub, 1);
-  const int mt = (int)ceil_div(ceil_div(cu, 8), kWConsumers);
+  const int mt = (int)ceil_div(ceil_div(cu, 8), kWGroups);
   switch (mt) {
     case 1: launch_wproj_t<1>(a, cu, s); break;
     case 2: launch_wproj_t<2>(a, cu, s); break;

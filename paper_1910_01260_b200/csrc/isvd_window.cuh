@@ -20,7 +20,8 @@
 namespace strom {
 
 constexpr int kWXLd = kStageRows + 8;  // 72: x slot stride (conflict-free 16-byte fragment loads)
-constexpr int kWConsumers = 8;
+constexpr int kWConsumers = 16;  // two warps per m-tile group, one per half of the stage's rows
+constexpr int kWGroups = 8;      // m-tile groups (warp cw: group cw % 8, row half cw / 8)
 constexpr int kWThreads = 32 * (kWConsumers + 1);
 constexpr int kWMaxStages = 4;
 
@@ -65,6 +66,7 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wproj(WprojArgs a, int nstages
   const int64_t per = ceil_div(ntiles, gridDim.x);
   const int64_t t0 = blockIdx.x * per;
   const int64_t nt = max((int64_t)0, min(ntiles, t0 + per) - t0);
+  __shared__ double hsum[kWGroups][(kWB / 2 + 1) * 64];  // the upper row half's accumulators
   if (threadIdx.x == 0) {
     for (int st = 0; st < nstages; ++st) {
       mbar_init(&full[st], 1);
@@ -92,8 +94,10 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wproj(WprojArgs a, int nstages
       }
     }
   } else {
-    // ---------------- consumers: warp cw owns m-tiles cw, cw + 8, ...
+    // ---------------- consumers: warp cw owns m-tiles (cw % 8) + 8 q over the row
+    // half cw / 8 of every stage (two accumulation chains per tile, halved latency)
     const int cw = wid - 1;
+    const int grp = cw % kWGroups, half = cw / kWGroups;
     double acc[MT][2];
 #pragma unroll
     for (int q = 0; q < MT; ++q) acc[q][0] = acc[q][1] = 0.0;
@@ -107,7 +111,7 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wproj(WprojArgs a, int nstages
       const int64_t row0 = (t0 + i) * kStageRows;
       const int valid = (int)max((int64_t)0, min((int64_t)kStageRows, a.n - row0));
 #pragma unroll 2
-      for (int kp = 0; kp < kStageRows / 8; ++kp) {
+      for (int kp = half * (kStageRows / 16); kp < (half + 1) * (kStageRows / 16); ++kp) {
         const int kr = 8 * kp + 2 * t;  // this lane's two rows of the k-step pair
         double2 b = make_double2(0.0, 0.0);
         if (xg) {
@@ -118,15 +122,15 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wproj(WprojArgs a, int nstages
         }
 #pragma unroll
         for (int q = 0; q < MT; ++q) {
-          const int col = 8 * (cw + kWConsumers * q) + g;
-          if (8 * (cw + kWConsumers * q) < c) {
+          const int col = 8 * (grp + kWGroups * q) + g;
+          if (8 * (grp + kWGroups * q) < c) {
             const double2 u = col < c ? *reinterpret_cast<const double2*>(tile + (size_t)col * kStageRows + kr)
                                       : make_double2(0.0, 0.0);
             dmma884(acc[q][0], acc[q][1], u.x, b.x);
             dmma884(acc[q][0], acc[q][1], u.y, b.y);
           }
         }
-        if (cw == 0) {  // XX = X^T X (A = X^T: a = X(kr, g) = b)
+        if (grp == 0) {  // XX = X^T X (A = X^T: a = X(kr, g) = b)
           dmma884(xa0, xa1, b.x, b.x);
           dmma884(xa0, xa1, b.y, b.y);
         }
@@ -134,19 +138,35 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wproj(WprojArgs a, int nstages
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
     }
-    double* mypart = a.part + (int64_t)blockIdx.x * a.pstride;
+    // upper half -> shared, then the lower half adds it (fixed order: deterministic)
+    double* hs = hsum[grp];
+    if (half == 1) {
 #pragma unroll
-    for (int q = 0; q < MT; ++q) {
-      const int i = 8 * (cw + kWConsumers * q) + g;
-      if (i < c) {
-        mypart[i * kWB + 2 * t] = acc[q][0];
-        mypart[i * kWB + 2 * t + 1] = acc[q][1];
+      for (int q = 0; q < MT; ++q) {
+        hs[(2 * q) * 32 + lane] = acc[q][0];
+        hs[(2 * q + 1) * 32 + lane] = acc[q][1];
+      }
+      if (grp == 0) {
+        hs[(2 * MT) * 32 + lane] = xa0;
+        hs[(2 * MT + 1) * 32 + lane] = xa1;
       }
     }
-    if (cw == 0) {
-      double* xp = mypart + (int64_t)c8 * kWB;
-      xp[g * kWB + 2 * t] = xa0;
-      xp[g * kWB + 2 * t + 1] = xa1;
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * kWConsumers) : "memory");
+    if (half == 0) {
+      double* mypart = a.part + (int64_t)blockIdx.x * a.pstride;
+#pragma unroll
+      for (int q = 0; q < MT; ++q) {
+        const int i = 8 * (grp + kWGroups * q) + g;
+        if (i < c) {
+          mypart[i * kWB + 2 * t] = acc[q][0] + hs[(2 * q) * 32 + lane];
+          mypart[i * kWB + 2 * t + 1] = acc[q][1] + hs[(2 * q + 1) * 32 + lane];
+        }
+      }
+      if (grp == 0) {
+        double* xp = mypart + (int64_t)c8 * kWB;
+        xp[g * kWB + 2 * t] = xa0 + hs[(2 * MT) * 32 + lane];
+        xp[g * kWB + 2 * t + 1] = xa1 + hs[(2 * MT + 1) * 32 + lane];
+      }
     }
   }
 }
