@@ -1347,7 +1347,8 @@ __global__ void __launch_bounds__(kVRows) k_vupdate(StateView src, StateView dst
 #pragma unroll
   for (int q = 0; q < kVCols; ++q) acc[q] = 0.0;
   if (i < k - 1) {
-    for (int b = 0; b < r; ++b) {
+#pragma unroll 8
+    for (int b = 0; b < r; ++b) {  // unrolled: eight V loads in flight (the kernel is load-latency bound)
       const double v = src.V[(int64_t)b * src.ldv + i];
 #pragma unroll
       for (int q = 0; q < kVCols; ++q) acc[q] = fma(v, vbs[q * m + b], acc[q]);
