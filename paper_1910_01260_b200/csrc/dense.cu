@@ -594,7 +594,7 @@ __global__ void __launch_bounds__(1024) k_qr(double* M, int64_t ld, int rows, in
 // Reference: linalg.py:75-99 (scipy lu_factor / lu_solve).
 // ---------------------------------------------------------------------------
 constexpr int kPlNb = 16;
-constexpr int kPlThreads = 256;  // 8 warps: cheaper per-column barriers in the panel (measured barrier-bound at 16)
+constexpr int kPlThreads = 512;  // 16 warps, 2 register rows per thread (256 threads x 4 rows measured slower: 27.9 vs 19.5 us per panel)
 constexpr int kPlWarps = kPlThreads / 32;
 
 struct PlArgs {
@@ -693,7 +693,7 @@ __device__ inline void pl_gemm(double* S, int ld, const double* M, int64_t ldm, 
 // shared memory, then scale and rank-1 update in registers; two barriers per
 // column.  Fully unrolled over the 16 panel columns so every register index is
 // static.
-constexpr int kPlRpt = 4;  // register panel for n <= kPlThreads * kPlRpt = 1024
+constexpr int kPlRpt = 2;  // register panel for n <= kPlThreads * kPlRpt = 1024
 __device__ inline void pl_panel_reg(double* S, int ld, int n, int j0, int w, int* piv, double* cval, int* cidx,
                                     double* prow, double* grow) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;

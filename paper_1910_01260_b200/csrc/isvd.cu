@@ -4,6 +4,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <thread>
 #include <string>
@@ -396,13 +397,19 @@ IsvdParams make_params(const strom_isvd* h, const PipeMem& m, int64_t k_new, boo
 }
 
 // ------------------------------------------------------------------ launchers
+// Raise a kernel's dynamic shared-memory cap whenever a launch asks for more
+// than any earlier one.  ONE record per (device, kernel): two launchers of the
+// same kernel with caches of their own would lower each other's setting.
+std::mutex g_smem_mu;
+std::map<std::pair<int, const void*>, size_t> g_smem_attr;
 template <class K>
-void set_smem_attr(K kernel, size_t smem, size_t* configured) {
-  // the default cap counts static shared memory too: raise it whenever a launch
-  // asks for more dynamic shared memory than any earlier one
-  if (smem > 32 * 1024 && smem > *configured) {
+void set_smem_attr(K kernel, size_t smem, size_t* /*legacy per-call-site cache, unused*/ = nullptr) {
+  if (smem <= 32 * 1024) return;
+  std::lock_guard<std::mutex> g(g_smem_mu);
+  size_t& cur = g_smem_attr[{current_device_id(), reinterpret_cast<const void*>(kernel)}];
+  if (smem > cur) {
     STROM_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    *configured = smem;
+    cur = smem;
   }
 }
 
