@@ -392,7 +392,7 @@ IsvdParams make_params(const strom_isvd* h, const PipeMem& m, int64_t k_new, boo
   P.ldg = 0;
   P.wcol = 0;
   P.wn = 0;
-  P.wpad = 0;
+  P.inline_next = 0;
   return P;
 }
 
@@ -827,6 +827,15 @@ int window_width() {
 // Measured: spinning k_decide_a on the core step's counter (STROM_DECIDE_SPIN=1)
 // is slower than the cross-stream event -- the spinner and the core step it
 // waits for hold SMs the V update and the passes then queue behind.
+// STROM_INLINE_DECIDE=0: k_decide_a always runs the first half itself
+bool inline_decide() {
+  static const bool v = [] {
+    const char* e = getenv("STROM_INLINE_DECIDE");
+    return !(e && atoi(e) == 0);
+  }();
+  return v;
+}
+
 bool decide_spins() {
   static const bool v = [] {
     const char* e = getenv("STROM_DECIDE_SPIN");
@@ -1423,8 +1432,17 @@ strom_isvd* ingest_windowed(strom_isvd* src, ColumnSource& cols, cudaStream_t s,
     launch_decide_w(2, prev->view, pp, m, P, s);
     ++d_launched;
     cols.release(t);
-    // s2: the core step (V_bar[t & 1] is free once k_vupdate(t - 2) is done)
+    // s2: the core step (V_bar[t & 1] is free once k_vupdate(t - 2) is done).  It
+    // may also run snapshot t+1's first-half decision when nothing can come
+    // between them: same window, and no capacity event at t+1 (host bounds)
     if (u_pending[t & 1]) STROM_CUDA(cudaStreamWaitEvent(s2, evU[t & 1], 0));
+    {
+      const int32_t c_ub = prev->c_ub + 1;
+      const int32_t r_ub = std::min(prev->r_ub + 1, prev->caps.rcap);
+      const bool rank_hit = prev->r_max < 0 && r_ub + 1 > prev->caps.rcap && prev->caps.rcap < prev->n;
+      const bool col_hit = c_ub + 1 > prev->caps.ccap;
+      P.inline_next = (P.has_next && !rank_hit && !col_hit && inline_decide()) ? 1 : 0;
+    }
     launch_step_b_pp(prev->view, dst->view, pp, P, prev->caps, s2);
     ++b_launched;
     STROM_CUDA(cudaEventRecord(evB, s2));

@@ -59,7 +59,7 @@ struct PipeCtl {
   int32_t decided;  // decision chains (k_decide + k_decide2) completed since then
   int32_t resid;    // window mode: the residual pass of this snapshot is needed
   int32_t adone;    // window mode: first-half decisions (k_decide_a) completed
-  int32_t pad;
+  int32_t a_inline; // window mode: d_expect of the snapshot whose first half k_step_b already ran
   double xx;        // x.x of the snapshot about to be decided
 };
 
@@ -161,7 +161,8 @@ struct IsvdParams {
   // wcol is this snapshot's column.  pp.fo.gn then points at column wcol + 1.
   double* wG;
   const double* wXX;
-  int32_t ldg, wcol, wn, wpad;
+  int32_t ldg, wcol, wn;
+  int32_t inline_next;  // window mode: k_step_b also runs the next snapshot's first-half decision
 };
 
 constexpr int kWB = 8;  // window width: snapshots projected by one pass over U
@@ -328,6 +329,7 @@ __global__ void k_init_ctl(PipeCtl* ctl, const IsvdHdr* h) {
   ctl->decided = 0;
   ctl->resid = 0;
   ctl->adone = 0;
+  ctl->a_inline = -1;
 }
 
 constexpr double kFoldTau = 1e-3;  // append r1 only if its out-of-span part is >= tau |r1|
@@ -791,8 +793,14 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide_a(StateView src, Pipe
   wait_counter(&pp.ctl->bdone, P.b_expect);  // the previous snapshot's core step wrote N, sigma
   pdl_trigger();
   trace_stamp(P.trace, 0);
-  decide_a_body(src, pp, P, part, red);
-  signal_counter(&pp.ctl->adone);  // the core step of this snapshot may start its SVD
+  if (*(volatile const int32_t*)&pp.ctl->a_inline == P.d_expect) {
+    // the previous core step already decided this snapshot's first half
+    // (decide_next_inline): only the next snapshot's coefficients remain
+    if (!pp.ctl->resid && pp.ctl->reorth == 0 && P.has_next) prep_next(P, pp, part);
+  } else {
+    decide_a_body(src, pp, P, part, red);
+    signal_counter(&pp.ctl->adone);  // the core step of this snapshot may start its SVD
+  }
   trace_stamp(P.trace, 1);
 }
 
@@ -1298,6 +1306,50 @@ __device__ inline void step_b_body(const StateView& src, const StateView& dst, c
   }
 }
 
+// Window mode: the next snapshot's first-half decision (decide_a_body's normal
+// branch, the same arithmetic in the same order, so identical bits) run by the
+// core step right after it produced N' -- the next core step can then start
+// without waiting for k_decide_a.  Not for restarts, rejects or errors (those
+// stay with k_decide_a).  Returns false when it did not run.
+__device__ inline bool decide_next_inline(const StateView& dst, const Pipe& pp, const IsvdParams& P, double* red) {
+  __syncthreads();
+  const IsvdHdr h = *dst.hdr;
+  const double xx = *(volatile const double*)&pp.ctl->xx;
+  const bool at_cap = P.r_max >= 0 && h.r >= P.r_max;
+  if (h.status != 0 || !isfinite(xx) || h.r == 0 || (at_cap && P.cap_mode == 0)) return false;
+  const int np = P.parity ^ 1, c = h.c, r = h.r;
+  double* ell = pp.ell[np];
+  cta_gemv_t_cm(dst.N, dst.ldn, c, r, pp.tvec, ell, false);
+  double s_ll = 0.0;
+  for (int i = threadIdx.x; i < r; i += blockDim.x) s_ll = fma(ell[i], ell[i], s_ll);
+  s_ll = block_sum(s_ll, red);
+  const double p_sq = xx - s_ll;
+  const double p = (p_sq > 0.0) ? sqrt(p_sq) : 0.0;
+  const int dep = (p < P.tol_svd) || (p == 0.0) || ((int64_t)r >= P.n);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    IsvdStep* st = pp.step[np];
+    st->mode = dep ? M_NORMAL_DEP : M_NORMAL_INDEP;
+    st->restart = 0;
+    st->action = 0;
+    st->dep = dep;
+    st->c = c;
+    st->cn = c;
+    st->base_new = h.base;
+    st->slot = h.base + c;
+    st->xx = xx;
+    st->rho2 = 0.0;
+    st->p = p;
+    st->p_sq = p_sq;
+    st->norm = sqrt(xx);
+    st->lam = 0.0;
+    pp.ctl->resid = dep ? 0 : 1;
+    pp.ctl->reorth = 0;
+    pp.ctl->a_inline = P.d_expect + 1;
+  }
+  return true;
+}
+
 __global__ void __launch_bounds__(kSmallThreads) k_step_b(StateView src, StateView dst, Pipe pp, IsvdParams P,
                                                           int use_smem) {
   extern __shared__ double smem[];
@@ -1306,6 +1358,9 @@ __global__ void __launch_bounds__(kSmallThreads) k_step_b(StateView src, StateVi
     wait_counter(&pp.ctl->adone, P.d_expect);
     trace_stamp(P.trace, 8);
     step_b_body(src, dst, pp, P, use_smem, smem, red, &pp.ctl->decided, P.d_expect);
+    if (P.inline_next && decide_next_inline(dst, pp, P, red)) {
+      signal_counter(&pp.ctl->adone);  // the next core step may start its SVD now
+    }
   } else {
     wait_counter(&pp.ctl->decided, P.d_expect);  // this snapshot's decision chain
     trace_stamp(P.trace, 8);
