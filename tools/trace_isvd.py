@@ -15,9 +15,14 @@ from paper_1910_01260_b200 import _capi, basis, workloads as wl  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument('--cols', type=int, default=120)
+ap.add_argument('--uncapped', action='store_true', help='r_max = None (the cfg1 / cfg3 setting)')
+ap.add_argument('--tol', type=float, default=1e-9)
 args = ap.parse_args()
 xt, _, _, _ = wl.cfg2_stream_torch(n=1 << 20, cols=100 + args.cols, rank=64, seed=0)
-st = basis.isvd_init(xt[0], 1e-9, tol_sv=1e-9, r_max=64, cap_mode='truncate')
+if args.uncapped:
+    st = basis.isvd_init(xt[0], args.tol, tol_sv=args.tol)
+else:
+    st = basis.isvd_init(xt[0], args.tol, tol_sv=args.tol, r_max=64, cap_mode='truncate')
 st = basis.ingest_simulation(st, xt[1:100].T)
 basis.ingest_simulation(st, xt[100:].T).rank  # warm
 buf = torch.zeros(args.cols * 16, dtype=torch.int64, device='cuda')
