@@ -461,7 +461,8 @@ __device__ inline void cta_gemv_cm(const double* A, int ld, int rows, int cols, 
   double acc[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) acc[k] = 0.0;
-  for (int j = wid; j < cols; j += nw) {
+#pragma unroll 2
+  for (int j = wid; j < cols; j += nw) {  // unrolled: two columns' loads in flight (L2-latency bound)
     const double xj = x[j];
     const double* col = A + (int64_t)j * ld;
 #pragma unroll
@@ -489,9 +490,11 @@ __device__ inline void cta_gemv_cm(const double* A, int ld, int rows, int cols, 
 __device__ inline void cta_gemv_t_cm(const double* A, int ld, int rows, int cols, const double* x, double* y,
                                      bool lower) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll 2
   for (int j = wid; j < cols; j += nw) {
     const double* col = A + (int64_t)j * ld;
     double s = 0.0;
+#pragma unroll 4
     for (int i = (lower ? j : 0) + lane; i < rows; i += 32) s = fma(col[i], x[i], s);
     s = warp_sum(s);
     if (lane == 0) y[j] = s;
@@ -509,6 +512,7 @@ __device__ inline void cta_gemv2_cm(const double* A, int ld, int rows, int cols,
   double a1[K], a2[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) { a1[k] = 0.0; a2[k] = 0.0; }
+#pragma unroll 2
   for (int j = wid; j < cols; j += nw) {
     const double u1 = x1[j], u2 = x2 ? x2[j] : 0.0;
     const double* col = A + (int64_t)j * ld;
@@ -547,9 +551,11 @@ __device__ inline void cta_gemv2_cm(const double* A, int ld, int rows, int cols,
 __device__ inline void cta_gemv2_t_cm(const double* A, int ld, int rows, int cols, const double* x1, const double* x2,
                                       double* y1, double* y2, bool lower) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll 2
   for (int j = wid; j < cols; j += nw) {
     const double* col = A + (int64_t)j * ld;
     double s1 = 0.0, s2 = 0.0;
+#pragma unroll 4
     for (int i = (lower ? j : 0) + lane; i < rows; i += 32) {
       const double v = col[i];
       s1 = fma(v, x1[i], s1);

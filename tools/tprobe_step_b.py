@@ -42,4 +42,6 @@ for k in range(301, 308):
     ok = R[:, k] > 0
     if ok.any():
         print(f'  core {k - 300}: {np.median(R[ok, k] - c0[ok]):10.0f}')
-print('iterations slot 8..', np.median(R[:, 8:16], axis=0))
+it = R[:, 8:8 + 66]
+print('root iterations: median over roots', np.median(it), ' max per update (median over updates)',
+      np.median(it.max(axis=1)), ' max overall', it.max())
