@@ -59,7 +59,7 @@ COLS = 500
 WARM_COLS = 100
 RANK = 64
 TOL = 1e-9
-PROF_KINDS = ["fused_pass", "reorth_pass", "decide", "core_step", "v_update", "compact_prep", "compact_sweep",
+PROF_KINDS = ["u_pass", "reorth_pass", "decide", "core_step", "v_update", "compact_prep", "compact_sweep",
               "spatial", "st_gemm", "st_small", "lu", "temporal", "other", "window_pass"]
 WORKLOAD = ("cfg2: n_s=2^20 fp64, 500-snapshot stream X=Q diag(10^(-i/8)) W^T + 1e-12 N(0,1) from numpy "
             "default_rng(0) (draw order Q, W, E); tol_svd=tol_sv=1e-9, r_max=64 truncate; start = rank-64 "

@@ -814,19 +814,31 @@ strom_isvd* update_once(strom_isvd* src, const double* x, cudaStream_t s, bool i
 }
 
 // ------------------------------------------------------------------ window-mode launchers
-// Window width in snapshots (STROM_WINDOW; 0 or 1 = the per-snapshot fused pass).
-int window_width() {
-  static const int v = [] {
-    const char* e = getenv("STROM_WINDOW");
-    const int w = e ? atoi(e) : kWB;
-    return std::max(0, std::min(kWB, w));
-  }();
-  return v;
-}
 
 // Measured: spinning k_decide_a on the core step's counter (STROM_DECIDE_SPIN=1)
 // is slower than the cross-stream event -- the spinner and the core step it
 // waits for hold SMs the V update and the passes then queue behind.
+// Window or per-snapshot pipeline for one ingest call.  A window pass costs
+// ~(c + kWB) / kWB column reads per snapshot and saves a full pass for every
+// dependent snapshot, so it pays when at least ~15 % of updates are dependent;
+// with (nearly) every update independent -- cfg5's rank-100 stream, whose
+// residuals sit above tol -- the fused per-snapshot pass is cheaper.  The
+// choice uses the source state's own history (one header read per call);
+// STROM_WINDOW forces a width.
+int choose_window(const strom_isvd* src, cudaStream_t s) {
+  static const int forced = [] {
+    const char* e = getenv("STROM_WINDOW");
+    return e ? std::max(0, std::min(kWB, atoi(e))) : -1;
+  }();
+  if (forced >= 0) return forced;
+  if (src->k < 16) return kWB;
+  IsvdHdr hh;
+  read_hdr(src, s, &hh);
+  if (hh.n_dependent == 0 && hh.n_truncated == 0) return kWB;  // no history (e.g. a loaded state)
+  const double updates = (double)std::max<int64_t>(1, src->k - 1 - hh.n_rejected - hh.n_restarts);
+  return (hh.n_dependent / updates >= 0.15) ? kWB : 1;
+}
+
 // STROM_INLINE_DECIDE=0: k_decide_a always runs the first half itself
 bool inline_decide() {
   static const bool v = [] {
@@ -1529,7 +1541,7 @@ int strom_isvd_ingest(strom_isvd* src, const double* X, int64_t ldx, int64_t nco
     cols.open(X, ldx, src->n, ncols, x_on_host != 0, s);
     strom_isvd* res = nullptr;
     try {
-      const int wb = window_width();
+      const int wb = choose_window(src, s);
       res = wb > 1 ? ingest_windowed(src, cols, s, wb) : ingest_pipelined(src, cols, s);
     } catch (...) {
       cols.close();
