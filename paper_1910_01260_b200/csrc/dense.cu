@@ -701,6 +701,12 @@ __device__ inline void pl_stamp(long long* cp, int k) {
     cp[k] = (long long)t;
   }
 }
+// The column loop is NOT unrolled (a fully unrolled 16-column panel is ~100 KB
+// of SASS: every column missed the instruction cache, ~1 us per column).
+// Static register indices come from a shift register instead: at column c a
+// thread's row values for columns c .. c+15 sit in v[q][0..15]; after the
+// update each active row shifts left by one, the L entry and, for the pivot
+// row, its U entries go to shared memory right away.
 __device__ inline void pl_panel_reg(double* S, int ld, int n, int j0, int w, int* piv, double (*candv)[kPlWarps][kPlNb + 1],
                                     double (*cval)[kPlWarps], int (*cidx)[kPlWarps], double (*drow)[kPlNb],
                                     long long* cp = nullptr) {
@@ -710,15 +716,14 @@ __device__ inline void pl_panel_reg(double* S, int ld, int n, int j0, int w, int
   for (int q = 0; q < kPlRpt; ++q) {
     const int r = tid + kPlThreads * q;
 #pragma unroll
-    for (int c = 0; c < kPlNb; ++c) v[q][c] = (r < n && r >= j0) ? S[c * ld + r] : 0.0;
+    for (int c = 0; c < kPlNb; ++c) v[q][c] = (r < n && r >= j0 && c < w) ? S[c * ld + r] : 0.0;
   }
   // ONE barrier per column: every warp publishes its candidate row (with the
   // reciprocal of its pivot entry, computed before the barrier) and the owner
   // of row gr publishes it, into buffers double-buffered by column parity; after
   // the barrier every warp reduces the candidates itself.
-#pragma unroll
-  for (int c = 0; c < kPlNb; ++c) {
-    if (c >= w) break;
+#pragma unroll 1
+  for (int c = 0; c < w; ++c) {
     const int gr = j0 + c, buf = c & 1;
     double best = -1.0;
     int bi = 0x7fffffff;
@@ -726,7 +731,7 @@ __device__ inline void pl_panel_reg(double* S, int ld, int n, int j0, int w, int
     for (int q = 0; q < kPlRpt; ++q) {
       const int r = tid + kPlThreads * q;
       if (r >= gr && r < n) {
-        const double av = fabs(v[q][c]);
+        const double av = fabs(v[q][0]);
         if (av > best) { best = av; bi = r; }
       }
     }
@@ -741,12 +746,12 @@ __device__ inline void pl_panel_reg(double* S, int ld, int n, int j0, int w, int
       const int r = tid + kPlThreads * q;
       if (r == bi) {
 #pragma unroll
-        for (int c2 = 0; c2 < kPlNb; ++c2) candv[buf][wid][c2] = v[q][c2];
-        candv[buf][wid][kPlNb] = v[q][c] != 0.0 ? 1.0 / v[q][c] : 0.0;
+        for (int k = 0; k < kPlNb; ++k) candv[buf][wid][k] = v[q][k];
+        candv[buf][wid][kPlNb] = v[q][0] != 0.0 ? 1.0 / v[q][0] : 0.0;
       }
       if (r == gr)
 #pragma unroll
-        for (int c2 = 0; c2 < kPlNb; ++c2) drow[buf][c2] = v[q][c2];
+        for (int k = 0; k < kPlNb; ++k) drow[buf][k] = v[q][k];
     }
     if (lane == 0) { cval[buf][wid] = best; cidx[buf][wid] = bi; }
     pl_stamp(cp, 3 * c);
@@ -767,35 +772,28 @@ __device__ inline void pl_panel_reg(double* S, int ld, int n, int j0, int w, int
     const double* prow = none ? drow[buf] : candv[buf][gw];
     if (tid == 0) piv[gr] = p;
     pl_stamp(cp, 3 * c + 2);
-    const double d = prow[c];
+    const double d = prow[0];
     const double inv = none ? (d != 0.0 ? 1.0 / d : 0.0) : candv[buf][gw][kPlNb];
 #pragma unroll
     for (int q = 0; q < kPlRpt; ++q) {
       const int r = tid + kPlThreads * q;
-      if (r == gr) {
+      if (r == gr) {  // the pivot row: its U entries of columns c .. w-1 are final
 #pragma unroll
-        for (int c2 = 0; c2 < kPlNb; ++c2) v[q][c2] = prow[c2];
-      } else if (r == p) {
+        for (int k = 0; k < kPlNb; ++k)
+          if (c + k < w) S[(c + k) * ld + gr] = prow[k];
+      } else if (r > gr && r < n) {
+        if (r == p)
 #pragma unroll
-        for (int c2 = 0; c2 < kPlNb; ++c2) v[q][c2] = drow[buf][c2];
-      }
-      if (r > gr && r < n && d != 0.0) {
-        const double l = v[q][c] * inv;
-        v[q][c] = l;
+          for (int k = 0; k < kPlNb; ++k) v[q][k] = drow[buf][k];
+        const double l = (d != 0.0) ? v[q][0] * inv : v[q][0];
+        S[c * ld + r] = l;  // the L entry of column c is final
 #pragma unroll
-        for (int c2 = c + 1; c2 < kPlNb; ++c2) v[q][c2] = fma(-l, prow[c2], v[q][c2]);
+        for (int k = 1; k < kPlNb; ++k) v[q][k - 1] = (d != 0.0) ? fma(-l, prow[k], v[q][k]) : v[q][k];
+        v[q][kPlNb - 1] = 0.0;
       }
     }
   }
   __syncthreads();
-#pragma unroll
-  for (int q = 0; q < kPlRpt; ++q) {
-    const int r = tid + kPlThreads * q;
-    if (r < n && r >= j0)
-#pragma unroll
-      for (int c = 0; c < kPlNb; ++c)
-        if (c < w) S[c * ld + r] = v[q][c];
-  }
 }
 
 __global__ void __launch_bounds__(kPlThreads, 1) k_lu_persistent(PlArgs a) {
