@@ -694,44 +694,27 @@ __device__ inline void pl_gemm(double* S, int ld, const double* M, int64_t ldm, 
 // column.  Fully unrolled over the 16 panel columns so every register index is
 // static.
 constexpr int kPlRpt = 2;  // register panel for n <= kPlThreads * kPlRpt = 1024
-__device__ inline void pl_stamp(long long* cp, int k) {
-  if (cp && threadIdx.x == 0) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    cp[k] = (long long)t;
-  }
-}
-// The column loop is NOT unrolled (a fully unrolled 16-column panel is ~100 KB
-// of SASS: every column missed the instruction cache, ~1 us per column).
-// Static register indices come from a shift register instead: at column c a
-// thread's row values for columns c .. c+15 sit in v[q][0..15]; after the
-// update each active row shifts left by one, the L entry and, for the pivot
-// row, its U entries go to shared memory right away.
-__device__ inline void pl_panel_reg(double* S, int ld, int n, int j0, int w, int* piv, double (*candv)[kPlWarps][kPlNb + 1],
-                                    double (*cval)[kPlWarps], int (*cidx)[kPlWarps], double (*drow)[kPlNb],
-                                    long long* cp = nullptr) {
+__device__ inline void pl_panel_reg(double* S, int ld, int n, int j0, int w, int* piv, double* cval, int* cidx,
+                                    double* prow, double* grow) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   double v[kPlRpt][kPlNb];
 #pragma unroll
   for (int q = 0; q < kPlRpt; ++q) {
     const int r = tid + kPlThreads * q;
 #pragma unroll
-    for (int c = 0; c < kPlNb; ++c) v[q][c] = (r < n && r >= j0 && c < w) ? S[c * ld + r] : 0.0;
+    for (int c = 0; c < kPlNb; ++c) v[q][c] = (r < n && r >= j0) ? S[c * ld + r] : 0.0;
   }
-  // ONE barrier per column: every warp publishes its candidate row (with the
-  // reciprocal of its pivot entry, computed before the barrier) and the owner
-  // of row gr publishes it, into buffers double-buffered by column parity; after
-  // the barrier every warp reduces the candidates itself.
-#pragma unroll 1
-  for (int c = 0; c < w; ++c) {
-    const int gr = j0 + c, buf = c & 1;
+#pragma unroll
+  for (int c = 0; c < kPlNb; ++c) {
+    if (c >= w) break;
+    const int gr = j0 + c;
     double best = -1.0;
     int bi = 0x7fffffff;
 #pragma unroll
     for (int q = 0; q < kPlRpt; ++q) {
       const int r = tid + kPlThreads * q;
       if (r >= gr && r < n) {
-        const double av = fabs(v[q][0]);
+        const double av = fabs(v[q][c]);
         if (av > best) { best = av; bi = r; }
       }
     }
@@ -741,59 +724,57 @@ __device__ inline void pl_panel_reg(double* S, int ld, int n, int j0, int w, int
       const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
       if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
     }
-#pragma unroll
-    for (int q = 0; q < kPlRpt; ++q) {
-      const int r = tid + kPlThreads * q;
-      if (r == bi) {
-#pragma unroll
-        for (int k = 0; k < kPlNb; ++k) candv[buf][wid][k] = v[q][k];
-        candv[buf][wid][kPlNb] = v[q][0] != 0.0 ? 1.0 / v[q][0] : 0.0;
-      }
-      if (r == gr)
-#pragma unroll
-        for (int k = 0; k < kPlNb; ++k) drow[buf][k] = v[q][k];
-    }
-    if (lane == 0) { cval[buf][wid] = best; cidx[buf][wid] = bi; }
-    pl_stamp(cp, 3 * c);
+    if (lane == 0) { cval[wid] = best; cidx[wid] = bi; }
     __syncthreads();
-    pl_stamp(cp, 3 * c + 1);
-    best = cval[buf][lane & (kPlWarps - 1)];
-    bi = cidx[buf][lane & (kPlWarps - 1)];
-    int gw = lane & (kPlWarps - 1);
+    best = cval[lane & (kPlWarps - 1)];
+    bi = cidx[lane & (kPlWarps - 1)];
 #pragma unroll
     for (int o = kPlWarps / 2; o > 0; o >>= 1) {
       const double ob = __shfl_xor_sync(0xffffffffu, best, o);
       const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      const int ow = __shfl_xor_sync(0xffffffffu, gw, o);
-      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; gw = ow; }
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
     }
-    const bool none = (bi == 0x7fffffff);  // an all-NaN column pivots on itself
-    const int p = none ? gr : bi;
-    const double* prow = none ? drow[buf] : candv[buf][gw];
-    if (tid == 0) piv[gr] = p;
-    pl_stamp(cp, 3 * c + 2);
-    const double d = prow[0];
-    const double inv = none ? (d != 0.0 ? 1.0 / d : 0.0) : candv[buf][gw][kPlNb];
+    const int p = (bi == 0x7fffffff) ? gr : bi;  // an all-NaN column pivots on itself
 #pragma unroll
     for (int q = 0; q < kPlRpt; ++q) {
       const int r = tid + kPlThreads * q;
-      if (r == gr) {  // the pivot row: its U entries of columns c .. w-1 are final
+      if (r == p)
 #pragma unroll
-        for (int k = 0; k < kPlNb; ++k)
-          if (c + k < w) S[(c + k) * ld + gr] = prow[k];
-      } else if (r > gr && r < n) {
-        if (r == p)
+        for (int c2 = 0; c2 < kPlNb; ++c2) prow[c2] = v[q][c2];
+      if (r == gr)
 #pragma unroll
-          for (int k = 0; k < kPlNb; ++k) v[q][k] = drow[buf][k];
-        const double l = (d != 0.0) ? v[q][0] * inv : v[q][0];
-        S[c * ld + r] = l;  // the L entry of column c is final
+        for (int c2 = 0; c2 < kPlNb; ++c2) grow[c2] = v[q][c2];
+    }
+    if (tid == 0) piv[gr] = p;
+    __syncthreads();
+    const double d = prow[c];
+    const double inv = d != 0.0 ? __drcp_rn(d) : 0.0;  // = 1.0 / d (correctly rounded), without the division routine
 #pragma unroll
-        for (int k = 1; k < kPlNb; ++k) v[q][k - 1] = (d != 0.0) ? fma(-l, prow[k], v[q][k]) : v[q][k];
-        v[q][kPlNb - 1] = 0.0;
+    for (int q = 0; q < kPlRpt; ++q) {
+      const int r = tid + kPlThreads * q;
+      if (r == gr) {
+#pragma unroll
+        for (int c2 = 0; c2 < kPlNb; ++c2) v[q][c2] = prow[c2];
+      } else if (r == p) {
+#pragma unroll
+        for (int c2 = 0; c2 < kPlNb; ++c2) v[q][c2] = grow[c2];
+      }
+      if (r > gr && r < n && d != 0.0) {
+        const double l = v[q][c] * inv;
+        v[q][c] = l;
+#pragma unroll
+        for (int c2 = c + 1; c2 < kPlNb; ++c2) v[q][c2] = fma(-l, prow[c2], v[q][c2]);
       }
     }
   }
-  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < kPlRpt; ++q) {
+    const int r = tid + kPlThreads * q;
+    if (r < n && r >= j0)
+#pragma unroll
+      for (int c = 0; c < kPlNb; ++c)
+        if (c < w) S[c * ld + r] = v[q][c];
+  }
 }
 
 __global__ void __launch_bounds__(kPlThreads, 1) k_lu_persistent(PlArgs a) {
@@ -802,10 +783,7 @@ __global__ void __launch_bounds__(kPlThreads, 1) k_lu_persistent(PlArgs a) {
   __shared__ double cval[kPlWarps];
   __shared__ int cidx[kPlWarps];
   __shared__ int spiv[kPlNb];
-  __shared__ double s_candv[2][kPlWarps][kPlNb + 1];
-  __shared__ double s_cval[2][kPlWarps];
-  __shared__ int s_cidx[2][kPlWarps];
-  __shared__ double s_drow[2][kPlNb];
+  __shared__ double prow[kPlNb], grow[kPlNb];
   const int j = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int n = a.n, ld = a.ldS;
   const bool rhs = j >= a.nbA;
@@ -864,8 +842,7 @@ __global__ void __launch_bounds__(kPlThreads, 1) k_lu_persistent(PlArgs a) {
     PL_PROBE(3);
     const int j0 = c0;
     if (n <= kPlThreads * kPlRpt) {
-      pl_panel_reg(S, ld, n, j0, w, a.piv, s_candv, s_cval, s_cidx, s_drow,
-                   (a.probe && blockIdx.x == 1) ? a.probe + a.ncb * 8 : nullptr);
+      pl_panel_reg(S, ld, n, j0, w, a.piv, cval, cidx, prow, grow);
     } else {
       for (int c = 0; c < w; ++c) {
         const int gr = j0 + c;
