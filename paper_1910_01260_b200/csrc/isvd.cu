@@ -820,11 +820,10 @@ strom_isvd* update_once(strom_isvd* src, const double* x, cudaStream_t s, bool i
 // waits for hold SMs the V update and the passes then queue behind.
 // Window or per-snapshot pipeline for one ingest call.  A window pass costs
 // ~(c + kWB) / kWB column reads per snapshot and saves a full pass for every
-// dependent snapshot, so it pays when at least ~15 % of updates are dependent;
-// with (nearly) every update independent -- cfg5's rank-100 stream, whose
-// residuals sit above tol -- the fused per-snapshot pass is cheaper.  The
-// choice uses the source state's own history (one header read per call);
-// STROM_WINDOW forces a width.
+// dependent snapshot; with every update independent -- cfg5's rank-100
+// stream, whose residuals sit above tol -- the fused per-snapshot pass is
+// cheaper.  The choice uses the source state's own counters (one header read
+// per call); STROM_WINDOW forces a width.
 int choose_window(const strom_isvd* src, cudaStream_t s) {
   static const int forced = [] {
     const char* e = getenv("STROM_WINDOW");
@@ -834,9 +833,11 @@ int choose_window(const strom_isvd* src, cudaStream_t s) {
   if (src->k < 16) return kWB;
   IsvdHdr hh;
   read_hdr(src, s, &hh);
-  if (hh.n_dependent == 0 && hh.n_truncated == 0) return kWB;  // no history (e.g. a loaded state)
-  const double updates = (double)std::max<int64_t>(1, src->k - 1 - hh.n_rejected - hh.n_restarts);
-  return (hh.n_dependent / updates >= 0.15) ? kWB : 1;
+  // the per-snapshot pipeline only for a stream that has sat at its rank cap
+  // (>= 8 truncations) without a single dependent update: every snapshot
+  // would need its residual pass anyway.  (A cumulative dependent fraction
+  // misleads: the rank build-up phase is all independent.)
+  return (hh.n_dependent == 0 && hh.n_truncated >= 8) ? 1 : kWB;
 }
 
 // STROM_INLINE_DECIDE=0: k_decide_a always runs the first half itself
