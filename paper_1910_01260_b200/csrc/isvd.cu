@@ -834,10 +834,10 @@ int choose_window(const strom_isvd* src, cudaStream_t s) {
   IsvdHdr hh;
   read_hdr(src, s, &hh);
   // the per-snapshot pipeline only for a stream that has sat at its rank cap
-  // (>= 8 truncations) without a single dependent update: every snapshot
+  // (>= 64 truncations) without a single dependent update: every snapshot
   // would need its residual pass anyway.  (A cumulative dependent fraction
   // misleads: the rank build-up phase is all independent.)
-  return (hh.n_dependent == 0 && hh.n_truncated >= 8) ? 1 : kWB;
+  return (hh.n_dependent == 0 && hh.n_truncated >= 64) ? 1 : kWB;
 }
 
 // STROM_INLINE_DECIDE=0: k_decide_a always runs the first half itself
