@@ -136,6 +136,48 @@ int strom_isvd_load_factored(int64_t n, int64_t k, int64_t c, int64_t r, const d
  * Synchronizes.  Any output may be NULL. */
 int strom_isvd_factors(strom_isvd* h, double* u_dev, double* w_dev, double* l_dev, void* stream);
 
+/* ------------------------------------------------------------------------
+ * Row-sharded incremental SVD over several GPUs (the reference
+ * is single-process -- this is the multi-GPU form of basis.py:105-194).
+ *
+ * Rank r of a group owns a block of rows of every snapshot and of the left
+ * basis; sigma, V and every decision are replicated bit-identically.  The
+ * per-rank partial sums of the tall kernels (U^T x, x.x, U^T r, r.r, window
+ * projections, compaction Grams) cross the GPUs in ONE small kernel over
+ * NVLink peer memory (mailboxes mapped by CUDA IPC; csrc/shard.cuh), summed in
+ * rank order on every rank.
+ *
+ * Set-up (one process per GPU):
+ *   1. strom_shard_mailbox_create(world, &g, handle)   on every rank
+ *   2. all-gather the 64-byte handles in rank order (torch.distributed / MPI)
+ *   3. strom_shard_connect(g, rank, n_global, handles)
+ *   4. strom_shard_make_current(g); strom_isvd_init(n_local, x_local, ...) --
+ *      a state created while a group is current is that rank's shard; its
+ *      successors (update / ingest) inherit the group.  make_current(NULL)
+ *      afterwards.  Every rank must issue the same sequence of calls.
+ * strom_isvd_export then yields the rank's rows of phi and the replicated
+ * sigma and V.  A peer that stops responding makes the exchange time out
+ * (STROM_SHARD_TIMEOUT_MS, default 5000) and the next strom_isvd_query fail
+ * with STROM_ECUDA instead of hanging the GPU.
+ * ------------------------------------------------------------------------ */
+typedef struct strom_shard strom_shard;
+#define STROM_SHARD_HANDLE_BYTES 64
+#define STROM_SHARD_MAX_RANKS 8
+
+int strom_shard_mailbox_create(int32_t world, strom_shard** out, void* handle64_out_host);
+int strom_shard_connect(strom_shard* g, int32_t rank, int64_t n_global, const void* handles_host);
+/* Single-process group of `world` virtual ranks on the current device (test
+ * harness): out[world]; each rank is driven by its own host thread and the
+ * exchanges are ordered by stream events, never by kernels waiting on kernels. */
+int strom_shard_create_local(int32_t world, int64_t n_global, strom_shard** out);
+/* Thread-local: states created by strom_isvd_init / strom_isvd_load* on this
+ * thread join group g (NULL: none). */
+void strom_shard_make_current(strom_shard* g);
+/* Synchronizes the device; exchanges completed and the sticky error word
+ * (0 ok, 1 peer timeout, 2 vector too large). */
+int strom_shard_status(strom_shard* g, int64_t* exchanges_out, int32_t* error_out);
+void strom_shard_free(strom_shard* g);
+
 /* Diagnostics: mean ms of `iters` fused passes over a synthetic n x c store. */
 int strom_debug_pass_bw(int64_t n, int32_t c, int32_t iters, int32_t reserve, double* ms_out);
 

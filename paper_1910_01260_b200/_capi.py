@@ -58,6 +58,13 @@ _PROTOS = {
     "strom_debug_trace": (None, [vp, i64]),
     "strom_debug_pass_bw": (C.c_int, [i64, i32, i32, i32, C.POINTER(dbl)]),
     "strom_isvd_free": (None, [vp]),
+    # row-shard groups (csrc/shard.cuh)
+    "strom_shard_mailbox_create": (C.c_int, [i32, C.POINTER(vp), vp]),
+    "strom_shard_connect": (C.c_int, [vp, i32, i64, vp]),
+    "strom_shard_create_local": (C.c_int, [i32, i64, C.POINTER(vp)]),
+    "strom_shard_make_current": (None, [vp]),
+    "strom_shard_status": (C.c_int, [vp, C.POINTER(i64), C.POINTER(i32)]),
+    "strom_shard_free": (None, [vp]),
     # temporal bases (basis.py:275-302)
     "strom_temporal_bases": (C.c_int, [vp, i64, i64, i64, i64, i64, i64, vp, vp, vp, vp]),
     # spatial ROM (spatial.py:45-67)

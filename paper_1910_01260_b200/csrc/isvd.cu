@@ -1,6 +1,7 @@
 // Host orchestration + C ABI of the streaming incremental SVD
 // (reference basis.py:30-194).  See isvd_kernels.cuh for the representation.
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -17,6 +18,7 @@
 #include "isvd_kernels.cuh"
 #include "isvd_window.cuh"
 #include "runtime.cuh"
+#include "shard.cuh"
 
 using namespace strom;
 
@@ -179,10 +181,117 @@ struct Caps {
   int64_t kcap = 0;
 };
 
+
+// ------------------------------------------------------------------ row sharding (shard.cuh)
+// Single-process groups (the one-GPU test harness): the ranks are host threads
+// of one process; their exchanges are ordered by stream events, so no kernel
+// ever waits for another rank's kernel.
+struct LocalSync {
+  std::mutex mu;
+  std::condition_variable cv;
+  int world = 1, arrived = 0;
+  uint64_t gen = 0;
+  bool broken = false;
+  static constexpr int kRing = 4;
+  cudaEvent_t ev[kShardMax][kRing] = {};
+  ~LocalSync() {
+    for (int r = 0; r < kShardMax; ++r)
+      for (int i = 0; i < kRing; ++i)
+        if (ev[r][i]) cudaEventDestroy(ev[r][i]);
+  }
+  void barrier() {
+    std::unique_lock<std::mutex> g(mu);
+    if (broken) throw Error(kInternal, "shard group: a rank left the exchange");
+    const uint64_t my = gen;
+    if (++arrived == world) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+      return;
+    }
+    if (!cv.wait_for(g, std::chrono::seconds(60), [&] { return gen != my || broken; })) {
+      broken = true;
+      cv.notify_all();
+      throw Error(kInternal, "shard group: the ranks' exchange sequences diverged (host barrier timed out)");
+    }
+    if (broken && gen == my) throw Error(kInternal, "shard group: a rank left the exchange");
+  }
+};
+
+struct MailboxMem {  // one rank's [flags | boxes] block (cudaMalloc: exportable by CUDA IPC)
+  void* ptr = nullptr;
+  explicit MailboxMem(size_t bytes) {
+    STROM_CUDA(cudaMalloc(&ptr, bytes));
+    STROM_CUDA(cudaMemset(ptr, 0, bytes));
+  }
+  ~MailboxMem() {
+    if (ptr) cudaFree(ptr);
+  }
+};
+
+struct ShardImpl {
+  int rank = 0, world = 1, device = 0;
+  int64_t n_global = 0;
+  std::shared_ptr<MailboxMem> box_mem;
+  std::vector<std::shared_ptr<MailboxMem>> peers_mem;  // single-process groups: the peers' blocks stay alive
+  void* mailbox = nullptr;
+  size_t mailbox_bytes = 0;
+  void* peer[kShardMax] = {};
+  bool ipc_opened[kShardMax] = {};
+  void* local = nullptr;  // seq counter + error word
+  bool connected = false;
+  ShardDev dev{};
+  std::shared_ptr<LocalSync> lsync;  // event-ordered mode
+  uint64_t nsync = 0;
+  static constexpr size_t kFlagBytes = 1024;
+  static size_t bytes_for(int world) {
+    return kFlagBytes + (size_t)kShardSlots * world * kShardMaxCount * 8;
+  }
+  void alloc(int world_) {
+    world = world_;
+    STROM_CUDA(cudaGetDevice(&device));
+    mailbox_bytes = bytes_for(world);
+    box_mem = std::make_shared<MailboxMem>(mailbox_bytes);
+    mailbox = box_mem->ptr;
+    STROM_CUDA(cudaMalloc(&local, 64));
+    STROM_CUDA(cudaMemset(local, 0, 64));
+    STROM_CUDA(cudaDeviceSynchronize());
+  }
+  void finish(int rank_, int64_t n_global_) {
+    rank = rank_;
+    n_global = n_global_;
+    dev.rank = rank;
+    dev.world = world;
+    dev.maxcount = kShardMaxCount;
+    for (int p = 0; p < world; ++p) {
+      dev.flag[p] = static_cast<unsigned long long*>(peer[p]);
+      dev.box[p] = reinterpret_cast<double*>(static_cast<char*>(peer[p]) + kFlagBytes);
+    }
+    dev.seq = static_cast<unsigned long long*>(local);
+    dev.err = reinterpret_cast<int32_t*>(static_cast<char*>(local) + 16);
+    const char* e = getenv("STROM_SHARD_TIMEOUT_MS");
+    dev.timeout_ns = (long long)(e && atoll(e) > 0 ? atoll(e) : 5000) * 1000000ll;
+    connected = true;
+  }
+  ~ShardImpl() {
+    for (int p = 0; p < kShardMax; ++p)
+      if (ipc_opened[p] && peer[p]) cudaIpcCloseMemHandle(peer[p]);
+    if (local) cudaFree(local);
+  }
+};
+
+thread_local std::shared_ptr<ShardImpl> t_current_shard;  // strom_shard_make_current
+
 }  // namespace
+
+struct strom_shard {
+  std::shared_ptr<ShardImpl> impl;
+};
 
 struct strom_isvd {
   int64_t n = 0, ldu = 0, k = 0;
+  int64_t n_global = 0;  // rows of the whole (sharded) matrix; == n for an unsharded state
+  std::shared_ptr<ShardImpl> shard;  // row-sharded: the exchange after every partial reduction
   double tol_svd = 0.0, tol_sv = 0.0;
   int32_t r_max = -1, cap_mode = 0;
   Caps caps;
@@ -207,7 +316,12 @@ int32_t slack_for(int32_t rcap) {
   return std::max<int32_t>(16, rcap / 2);
 }
 
-Caps make_caps(int64_t n, int32_t r_max, int32_t want_r, int64_t k) {
+// n bounds the rank (the matrix's rows: the GLOBAL count of a sharded state);
+// mem_rows sizes the store (this GPU's rows; for a sharded state the largest
+// row block of the group, so that every rank derives the same capacities and
+// with them the same compaction schedule).
+Caps make_caps(int64_t n, int32_t r_max, int32_t want_r, int64_t k, int64_t mem_rows = -1) {
+  if (mem_rows < 0) mem_rows = n;
   Caps c;
   int64_t rc;
   if (r_max >= 0) rc = std::min<int64_t>(std::max<int32_t>(r_max, 1), n);
@@ -220,12 +334,18 @@ Caps make_caps(int64_t n, int32_t r_max, int32_t want_r, int64_t k) {
   // HBM by trimming the slack (cfg5: 2^26 rows, 0.54 GB per column)
   const size_t total_b = device_total_mem();
   if (total_b > 0) {
-    const int64_t col_bytes = round_up(n, 128) * 8;
+    const int64_t col_bytes = round_up(mem_rows, 128) * 8;
     const int64_t max_cols = (int64_t)(0.40 * (double)total_b) / col_bytes;
     if (c.ccap > max_cols) c.ccap = (int32_t)std::max<int64_t>(c.rcap + 1 + 8, max_cols);
   }
   c.kcap = std::max<int64_t>(64, round_up(std::max<int64_t>(k, 1) * 2, 64));
   return c;
+}
+
+int64_t rank_rows(const strom_isvd* h) { return h->n_global > 0 ? h->n_global : h->n; }
+int64_t mem_rows(const strom_isvd* h) {
+  if (!h->shard) return h->n;
+  return round_up(ceil_div(rank_rows(h), h->shard->world), 128);
 }
 
 std::shared_ptr<Store> alloc_store(int64_t n, int64_t ldu, int32_t ccap, cudaStream_t s) {
@@ -283,6 +403,8 @@ void alloc_v(strom_isvd* h, cudaStream_t s) {
 strom_isvd* new_like(const strom_isvd* src, const Caps& caps) {
   auto* h = new strom_isvd();
   h->n = src->n;
+  h->n_global = src->n_global;
+  h->shard = src->shard;
   h->ldu = src->ldu;
   h->k = src->k;
   h->tol_svd = src->tol_svd;
@@ -367,7 +489,7 @@ PipeMem make_pipe(const Caps& c, cudaStream_t s) {
 
 IsvdParams make_params(const strom_isvd* h, const PipeMem& m, int64_t k_new, bool init_call) {
   IsvdParams P;
-  P.n = h->n;
+  P.n = h->n_global > 0 ? h->n_global : h->n;  // decisions compare ranks with the GLOBAL row count
   P.ldu = h->ldu;
   P.ccap = h->caps.ccap;
   P.rcap = h->caps.rcap;
@@ -411,6 +533,100 @@ void set_smem_attr(K kernel, size_t smem, size_t* /*legacy per-call-site cache, 
     STROM_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     cur = smem;
   }
+}
+
+// ------------------------------------------------------------------ shard exchange kernels
+// Each mirrors the reduction it follows: the same skip conditions and output
+// ranges, read from the same device control block, so every rank exchanges (or
+// skips) alike without a host decision.
+__global__ void __launch_bounds__(kShardThreads) k_shard_pass(ShardDev sd, PassOut out, const PipeCtl* ctl, int kind,
+                                                              int has_x, int has_xn, int nxw_arg, int phase) {
+  pdl_enter();
+  int c = ctl->c;
+  bool do_e = false, do_gn = false, have_x = has_x != 0;
+  if (kind == PASS_SECOND) {
+    const int ro = ctl->reorth;
+    if (ro == 0) return;
+    have_x = true;
+    if (ro == 1) do_e = true;
+    else c = 0;
+  } else if (kind == PASS_FUSED || kind == PASS_RESID) {
+    if (kind == PASS_RESID && *(volatile const int32_t*)&ctl->resid == 0) return;
+    do_e = true;
+    do_gn = has_xn != 0;
+  } else {
+    have_x = false;
+    do_gn = true;
+  }
+  ShardSegs sg;
+  sg.n = 4;
+  sg.s[0] = ShardSeg{out.e, do_e ? c : 0, 1, 0};
+  sg.s[1] = ShardSeg{out.gn, do_gn ? c : 0, 1, 0};
+  sg.s[2] = ShardSeg{out.scal, 3, 1, 0};
+  sg.s[3] = ShardSeg{out.gw, have_x ? nxw_arg : 0, 1, 0};
+  shard_exchange(sd, sg, phase);
+  __syncthreads();
+  if (phase != SHARD_PUBLISH && kind == PASS_FUSED && do_gn && threadIdx.x == 0)
+    out.gn[c] = out.scal[2];  // r . x_next, as the pass's own reduction stores it
+}
+
+__global__ void __launch_bounds__(kShardThreads) k_shard_window(ShardDev sd, const PipeCtl* ctl, int nw, double* G,
+                                                                int ldg, double* XX, int phase) {
+  pdl_enter();
+  ShardSegs sg;
+  sg.n = 2;
+  sg.s[0] = ShardSeg{G, ctl->c, nw, ldg};
+  sg.s[1] = ShardSeg{XX, kWB * kWB, 1, 0};
+  shard_exchange(sd, sg, phase);
+}
+
+__global__ void __launch_bounds__(kShardThreads) k_shard_gram(ShardDev sd, const int32_t* q_dev, int q_fixed,
+                                                              double* G, int ld, int phase) {
+  const int q = q_dev ? *q_dev : q_fixed;
+  ShardSegs sg;
+  sg.n = 1;
+  sg.s[0] = ShardSeg{G, q, q, ld};
+  shard_exchange(sd, sg, phase);
+}
+
+// Launch one exchange: a single kernel over peer memory, or -- in a
+// single-process group -- publish, a host rendezvous that orders the ranks'
+// streams by events, then combine.
+template <class LaunchFn>
+void shard_run(ShardImpl* g, cudaStream_t s, LaunchFn&& launch) {
+  if (!g->lsync) {
+    launch(SHARD_BOTH);
+    return;
+  }
+  launch(SHARD_PUBLISH);
+  LocalSync& ls = *g->lsync;
+  const int slot = (int)(g->nsync++ % LocalSync::kRing);
+  STROM_CUDA(cudaEventRecord(ls.ev[g->rank][slot], s));
+  ls.barrier();  // every rank has recorded its publish
+  for (int p = 0; p < g->world; ++p)
+    if (p != g->rank) STROM_CUDA(cudaStreamWaitEvent(s, ls.ev[p][slot], 0));
+  ls.barrier();  // every rank has queued its waits: the events may be re-recorded
+  launch(SHARD_COMBINE);
+}
+
+void shard_after_pass(const strom_isvd* h, const PassArgs& a, cudaStream_t s) {
+  if (!h->shard) return;
+  ShardImpl* g = h->shard.get();
+  shard_run(g, s, [&](int phase) {
+    launch_pdl(k_shard_pass, dim3(1), dim3(kShardThreads), 0, s, g->dev, a.out, (const PipeCtl*)a.ctl, (int)a.kind,
+               a.x ? 1 : 0, a.xn ? 1 : 0, (int)a.nxw, phase);
+    STROM_LAUNCH_CHECK();
+  });
+}
+
+void shard_after_gram(const std::shared_ptr<ShardImpl>& sh, const int32_t* q_dev, int q_fixed, double* G, int ld,
+                      cudaStream_t s) {
+  if (!sh) return;
+  ShardImpl* g = sh.get();
+  shard_run(g, s, [&](int phase) {
+    k_shard_gram<<<1, kShardThreads, 0, s>>>(g->dev, q_dev, q_fixed, G, ld, phase);
+    STROM_LAUNCH_CHECK();
+  });
 }
 
 inline int pass_maxj(int cols) {
@@ -531,6 +747,10 @@ void launch_pass(int kind, int cols_ub, const strom_isvd* h, const PipeMem& m, c
     case 24: launch_pass_t<24>(a, cu, reserve, pk, s); break;
     default: launch_pass_t<32>(a, cu, reserve, pk, s); break;
   }
+  if (h->shard) {
+    if (tl.tail) throw Error(kInternal, "sharded passes take their decisions in their own kernels");
+    shard_after_pass(h, a, s);
+  }
 }
 
 size_t decide_smem(const PipeMem& m) { return (size_t)2 * (kDecideThreads / 32) * round_up(m.ccap, 32) * 8; }
@@ -623,9 +843,11 @@ void launch_tall_gemm(const Tall& A, const int32_t* col0_dev, const double* T, i
 
 // Gram from per-CTA partials (QP x QP each, summed in CTA order) -> L = chol, Li = L^{-1}
 void gram_finish(const double* part, int nparts, int QP, const int32_t* q_dev, int q_fixed, double* L, double* Li,
-                 int ldl, const IsvdHdr* hdr_c, int* status_dev, cudaStream_t s) {
+                 int ldl, const IsvdHdr* hdr_c, int* status_dev, cudaStream_t s,
+                 const std::shared_ptr<ShardImpl>& shard) {
   k_gram_reduce<<<(unsigned)ceil_div((int64_t)QP * QP, 256), 256, 0, s>>>(part, nparts, QP, q_dev, q_fixed, L, ldl);
   STROM_LAUNCH_CHECK();
+  shard_after_gram(shard, q_dev, q_fixed, L, ldl, s);  // row-sharded: the Gram of all ranks' rows
   k_cholesky<<<1, 256, 0, s>>>(L, ldl, hdr_c, q_fixed, status_dev);
   STROM_LAUNCH_CHECK();
   k_lower_inverse<<<1, 1024, 0, s>>>(L, ldl, hdr_c, q_fixed, Li);
@@ -651,7 +873,7 @@ void launch_compact_pass(const Store& src, const int32_t* base_dev, const int32_
 // q is read on the device (q_dev) or fixed; the Cholesky reads c from hdr_c.
 void gram_cholesky(const Tall& A, const int32_t* col0_dev, const int32_t* q_dev, int q_fixed,
                    int qmax, int64_t n, double* L, double* Li, int ldl, const IsvdHdr* hdr_c, int* status_dev,
-                   cudaStream_t s) {
+                   cudaStream_t s, const std::shared_ptr<ShardImpl>& shard) {
   const int QP = (int)round_up(std::max(qmax, 1), 8);
   const int64_t ntiles = ceil_div(n, kGramRows);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)sm_count() * 2));
@@ -672,7 +894,7 @@ void gram_cholesky(const Tall& A, const int32_t* col0_dev, const int32_t* q_dev,
     throw Error(kInvalidArgument, "Gram of more than 128 columns is not supported");
   }
   STROM_LAUNCH_CHECK();
-  gram_finish(part->as<double>(), grid, QP, q_dev, q_fixed, L, Li, ldl, hdr_c, status_dev, s);
+  gram_finish(part->as<double>(), grid, QP, q_dev, q_fixed, L, Li, ldl, hdr_c, status_dev, s, shard);
 }
 
 // Compaction into a fresh store (also used to grow capacities):
@@ -714,14 +936,14 @@ strom_isvd* compact(strom_isvd* src, const Caps& caps, cudaStream_t s) {
       default: launch_compact_pass<4>(*src->store, bptr, cptr, rptr, m.pp.T, P.ccap, cmax, kc.rcap, *t->store, part->as<double>(), RP, s); break;
     }
     gram_finish(part->as<double>(), sm_count(), RP, rptr, 0, t->view.L, t->view.Li, t->view.ldl, t->view.hdr,
-                &m.pp.step[0]->pad0, s);
+                &m.pp.step[0]->pad0, s, src->shard);
   } else {
     launch_tall_gemm(tall_tiled(src->store->U(), src->store->ccap), &src->view.hdr->base, m.pp.T, P.ccap,
                      &m.pp.step[0]->m, &m.pp.step[0]->mkeep, tall_tiled(t->store->U(), t->store->ccap), false, t->n,
                      t->ldu, s);
     // measure the Gram of the stored U_new: L describes the memory, not an assumed identity
     gram_cholesky(tall_tiled(t->store->U(), t->store->ccap), nullptr, &m.pp.step[0]->mkeep, 0, caps.rcap, t->n,
-                  t->view.L, t->view.Li, t->view.ldl, t->view.hdr, &m.pp.step[0]->pad0, s);
+                  t->view.L, t->view.Li, t->view.ldl, t->view.hdr, &m.pp.step[0]->pad0, s, src->shard);
   }
   k_compact_finish<<<1, 256, 0, s>>>(t->view, m.pp.T, P.ccap);
   STROM_LAUNCH_CHECK();
@@ -729,6 +951,15 @@ strom_isvd* compact(strom_isvd* src, const Caps& caps, cudaStream_t s) {
   t->c_ub = t->r_ub;
   t->store->claimed = t->c_ub;
   return guard.release();
+}
+
+// Sticky exchange errors of a shard group (the caller has synchronised).
+void shard_check(ShardImpl* g) {
+  int32_t err = 0;
+  STROM_CUDA(cudaMemcpy(&err, g->dev.err, sizeof(err), cudaMemcpyDeviceToHost));
+  if (err == SHARD_ERR_TIMEOUT)
+    throw Error(kCudaError, "shard exchange timed out waiting for a peer rank (results are invalid)");
+  if (err) throw Error(kInternal, "shard exchange: vector larger than the mailbox");
 }
 
 void read_hdr(const strom_isvd* h, cudaStream_t s, IsvdHdr* out) {
@@ -740,13 +971,14 @@ void read_hdr(const strom_isvd* h, cudaStream_t s, IsvdHdr* out) {
 // when a bound says it might be needed).  Returns the state to update from
 // (cur itself, or a compacted copy owned by *hold).
 strom_isvd* ensure_capacity(strom_isvd* cur, std::unique_ptr<strom_isvd>* hold, cudaStream_t s) {
-  if (cur->r_max < 0 && cur->r_ub + 1 > cur->caps.rcap && cur->caps.rcap < cur->n) {
+  if (cur->r_max < 0 && cur->r_ub + 1 > cur->caps.rcap && cur->caps.rcap < rank_rows(cur)) {
     IsvdHdr hh;
     read_hdr(cur, s, &hh);
     cur->r_ub = hh.r;
     cur->c_ub = std::min(cur->c_ub, hh.base + hh.c);
     if (hh.r + 1 > cur->caps.rcap) {
-      Caps nc = make_caps(cur->n, -1, std::min<int64_t>(cur->n, 2 * (int64_t)cur->caps.rcap), cur->k);
+      Caps nc = make_caps(rank_rows(cur), -1, std::min<int64_t>(rank_rows(cur), 2 * (int64_t)cur->caps.rcap),
+                          cur->k, mem_rows(cur));
       nc.kcap = cur->caps.kcap;
       hold->reset(compact(cur, nc, s));
       cur = hold->get();
@@ -792,7 +1024,13 @@ strom_isvd* update_once(strom_isvd* src, const double* x, cudaStream_t s, bool i
   trace_point("proj", s);
   launch_prep(m, P, s);
   trace_point("prep", s);
-  {
+  if (cur->shard) {
+    // row-sharded: the partial sums cross the ranks between a pass and its decision
+    launch_pass(PASS_FUSED, cols, dst, m, x, nullptr, 0, s);
+    launch_decide_kernel(false, cur->view, m, P, s);
+    launch_pass(PASS_SECOND, cols, dst, m, x, nullptr, 0, s);
+    launch_decide_kernel(true, cur->view, m, P, s);
+  } else {
     PassTail tl;
     tl.tail = 1;  // decide (basis.py:112-139) in the pass's last CTA
     tl.src = &cur->view;
@@ -912,6 +1150,14 @@ void launch_window(const strom_isvd* h, const PipeMem& m, const double* const* x
   launch_pdl(k_wreduce, dim3((unsigned)ceil_div(nout, 32)), dim3(256), 0, s, (const double*)m.wpart, nparts,
              m.wpstride, (const PipeCtl*)m.pp.ctl, nw, m.wG, m.ldg, m.wXX);
   STROM_LAUNCH_CHECK();
+  if (h->shard) {
+    ShardImpl* g = h->shard.get();
+    shard_run(g, s, [&](int phase) {
+      launch_pdl(k_shard_window, dim3(1), dim3(kShardThreads), 0, s, g->dev, (const PipeCtl*)m.pp.ctl, nw, m.wG,
+                 m.ldg, m.wXX, phase);
+      STROM_LAUNCH_CHECK();
+    });
+  }
   IsvdParams P = P0;
   P.wG = m.wG;
   P.wXX = m.wXX;
@@ -1187,7 +1433,7 @@ strom_isvd* ingest_pipelined(strom_isvd* src, ColumnSource& cols, cudaStream_t s
   for (int64_t t = 0; t < ncols; ++t) {
     // ---- capacity (host bounds; synchronises only when a bound is hit)
     {
-      const bool rank_hit = prev->r_max < 0 && prev->r_ub + 1 > prev->caps.rcap && prev->caps.rcap < prev->n;
+      const bool rank_hit = prev->r_max < 0 && prev->r_ub + 1 > prev->caps.rcap && prev->caps.rcap < rank_rows(prev);
       const bool col_hit = prev->c_ub + 1 > prev->caps.ccap;
       if (rank_hit || col_hit) {
         join();
@@ -1259,7 +1505,7 @@ strom_isvd* ingest_pipelined(strom_isvd* src, ColumnSource& cols, cudaStream_t s
       STROM_CUDA(cudaStreamWaitEvent(s2, evV, 0));
       fresh_alloc = false;
     }
-    if (decide_as_kernel()) {
+    if (decide_as_kernel() || prev->shard) {
       // s: pass -> decide -> second pass -> decide2, kernel to kernel (PDL);
       // the cross-stream dependencies are device counters, not events:
       // k_decide(t) waits for k_step_b(t-1), k_step_b(t) for k_decide2(t)
@@ -1350,7 +1596,7 @@ strom_isvd* ingest_windowed(strom_isvd* src, ColumnSource& cols, cudaStream_t s,
   };
   for (int64_t t = 0; t < ncols; ++t) {
     {
-      const bool rank_hit = prev->r_max < 0 && prev->r_ub + 1 > prev->caps.rcap && prev->caps.rcap < prev->n;
+      const bool rank_hit = prev->r_max < 0 && prev->r_ub + 1 > prev->caps.rcap && prev->caps.rcap < rank_rows(prev);
       const bool col_hit = prev->c_ub + 1 > prev->caps.ccap;
       if (rank_hit || col_hit) {
         join();
@@ -1452,7 +1698,7 @@ strom_isvd* ingest_windowed(strom_isvd* src, ColumnSource& cols, cudaStream_t s,
     {
       const int32_t c_ub = prev->c_ub + 1;
       const int32_t r_ub = std::min(prev->r_ub + 1, prev->caps.rcap);
-      const bool rank_hit = prev->r_max < 0 && r_ub + 1 > prev->caps.rcap && prev->caps.rcap < prev->n;
+      const bool rank_hit = prev->r_max < 0 && r_ub + 1 > prev->caps.rcap && prev->caps.rcap < rank_rows(prev);
       const bool col_hit = c_ub + 1 > prev->caps.ccap;
       P.inline_next = (P.has_next && !rank_hit && !col_hit && inline_decide()) ? 1 : 0;
     }
@@ -1484,6 +1730,17 @@ strom_isvd* ingest_windowed(strom_isvd* src, ColumnSource& cols, cudaStream_t s,
   return out;
 }
 
+// A brand-new state created while a shard group is current (strom_shard_make_current)
+// is that rank's row block of the group's matrix.
+void adopt_current_shard(strom_isvd* h) {
+  h->n_global = h->n;
+  if (!t_current_shard) return;
+  STROM_REQUIRE(t_current_shard->connected, "the current shard group is not connected");
+  STROM_REQUIRE(t_current_shard->n_global >= h->n, "shard group: global row count below the local one");
+  h->shard = t_current_shard;
+  h->n_global = t_current_shard->n_global;
+}
+
 strom_isvd* init_state(int64_t n, const double* x, int64_t k, double tol_svd, double tol_sv, int64_t r_max,
                        int32_t cap_mode, cudaStream_t s) {
   STROM_REQUIRE(n >= 1, "need n >= 1");
@@ -1493,13 +1750,14 @@ strom_isvd* init_state(int64_t n, const double* x, int64_t k, double tol_svd, do
   // restart branch then implements isvd_init (basis.py:65-102)
   strom_isvd e;
   e.n = n;
+  adopt_current_shard(&e);
   e.ldu = round_up(n, kGemmRows);
   e.k = k - 1;
   e.tol_svd = tol_svd;
   e.tol_sv = tol_sv;
   e.r_max = (int32_t)r_max;
   e.cap_mode = cap_mode;
-  e.caps = make_caps(n, e.r_max, 1, k);
+  e.caps = make_caps(rank_rows(&e), e.r_max, 1, k, mem_rows(&e));
   alloc_small(&e, s);
   alloc_v(&e, s);
   set_store(&e, alloc_store(n, e.ldu, e.caps.ccap, s));
@@ -1558,6 +1816,7 @@ int strom_isvd_query(strom_isvd* h, void* stream, strom_isvd_info* out) {
     STROM_REQUIRE(h && out, "null argument");
     IsvdHdr hh;
     read_hdr(h, as_stream(stream), &hh);
+    if (h->shard) shard_check(h->shard.get());
     h->r_ub = hh.r;  // refine the host bounds while we are synchronised
     memset(out, 0, sizeof(*out));
     out->n = h->n;
@@ -1619,13 +1878,14 @@ int strom_isvd_load_factored(int64_t n, int64_t k, int64_t c, int64_t r, const d
     auto* h = new strom_isvd();
     std::unique_ptr<strom_isvd> guard(h);
     h->n = n;
+    adopt_current_shard(h);
     h->ldu = round_up(n, kGemmRows);
     h->k = k;
     h->tol_svd = tol_svd;
     h->tol_sv = tol_sv;
     h->r_max = (int32_t)r_max;
     h->cap_mode = cap_mode;
-    h->caps = make_caps(n, h->r_max, (int32_t)std::max<int64_t>(c, r + 1), k);
+    h->caps = make_caps(rank_rows(h), h->r_max, (int32_t)std::max<int64_t>(c, r + 1), k, mem_rows(h));
     STROM_REQUIRE(c + 1 <= h->caps.ccap, "too many factored columns for this capacity");
     alloc_small(h, s);
     alloc_v(h, s);
@@ -1660,7 +1920,7 @@ int strom_isvd_load_factored(int64_t n, int64_t k, int64_t c, int64_t r, const d
         auto st = dev_alloc(sizeof(int), s, true);
         gram_cholesky(tall_tiled(h->store->U(), h->store->ccap), nullptr, nullptr, (int)c, (int)c, n, h->view.L,
                       h->view.Li,
-                      h->view.ldl, nullptr, st->as<int>(), s);
+                      h->view.ldl, nullptr, st->as<int>(), s, h->shard);
         int bad = 0;
         STROM_CUDA(cudaMemcpyAsync(&bad, st->ptr, sizeof(int), cudaMemcpyDeviceToHost, s));
         STROM_CUDA(cudaStreamSynchronize(s));
@@ -1778,6 +2038,91 @@ void strom_debug_trace(long long* dev_buf, int64_t rows) {
   g_trace = dev_buf;
   g_trace_rows = dev_buf ? rows : 0;
 }
+
+// ------------------------------------------------------------------ row-shard groups (shard.cuh)
+int strom_shard_mailbox_create(int32_t world, strom_shard** out, void* handle64_out) {
+  return guarded([&] {
+    STROM_REQUIRE(out && handle64_out, "null argument");
+    STROM_REQUIRE(world >= 1 && world <= kShardMax, "shard groups hold 1..8 ranks");
+    static_assert(sizeof(cudaIpcMemHandle_t) == STROM_SHARD_HANDLE_BYTES, "IPC handle size");
+    auto g = std::make_unique<strom_shard>();
+    g->impl = std::make_shared<ShardImpl>();
+    g->impl->alloc(world);
+    cudaIpcMemHandle_t hnd;
+    memset(&hnd, 0, sizeof(hnd));
+    if (world > 1) STROM_CUDA(cudaIpcGetMemHandle(&hnd, g->impl->mailbox));
+    memcpy(handle64_out, &hnd, sizeof(hnd));
+    *out = g.release();
+  });
+}
+
+int strom_shard_connect(strom_shard* g, int32_t rank, int64_t n_global, const void* handles_host) {
+  return guarded([&] {
+    STROM_REQUIRE(g && g->impl, "null argument");
+    ShardImpl* im = g->impl.get();
+    STROM_REQUIRE(!im->connected, "shard group already connected");
+    STROM_REQUIRE(rank >= 0 && rank < im->world, "rank outside the group");
+    STROM_REQUIRE(n_global >= 1, "need n_global >= 1");
+    STROM_REQUIRE(im->world == 1 || handles_host, "need the peers' mailbox handles");
+    for (int p = 0; p < im->world; ++p) {
+      if (p == rank) {
+        im->peer[p] = im->mailbox;
+        continue;
+      }
+      cudaIpcMemHandle_t hnd;
+      memcpy(&hnd, static_cast<const char*>(handles_host) + (size_t)p * sizeof(hnd), sizeof(hnd));
+      // maps the peer GPU's mailbox here and enables peer access (NVLink / NVSwitch)
+      STROM_CUDA(cudaIpcOpenMemHandle(&im->peer[p], hnd, cudaIpcMemLazyEnablePeerAccess));
+      im->ipc_opened[p] = true;
+    }
+    im->finish(rank, n_global);
+  });
+}
+
+int strom_shard_create_local(int32_t world, int64_t n_global, strom_shard** out) {
+  return guarded([&] {
+    STROM_REQUIRE(out, "null argument");
+    STROM_REQUIRE(world >= 1 && world <= kShardMax, "shard groups hold 1..8 ranks");
+    STROM_REQUIRE(n_global >= 1, "need n_global >= 1");
+    std::vector<std::unique_ptr<strom_shard>> gs;
+    auto ls = std::make_shared<LocalSync>();
+    ls->world = world;
+    for (int r = 0; r < world; ++r)
+      for (int i = 0; i < LocalSync::kRing; ++i)
+        STROM_CUDA(cudaEventCreateWithFlags(&ls->ev[r][i], cudaEventDisableTiming));
+    for (int r = 0; r < world; ++r) {
+      gs.emplace_back(new strom_shard());
+      gs.back()->impl = std::make_shared<ShardImpl>();
+      gs.back()->impl->alloc(world);
+      gs.back()->impl->lsync = ls;
+    }
+    for (int r = 0; r < world; ++r) {
+      for (int p = 0; p < world; ++p) {
+        gs[r]->impl->peer[p] = gs[p]->impl->mailbox;
+        gs[r]->impl->peers_mem.push_back(gs[p]->impl->box_mem);  // outlives every rank that stores into it
+      }
+      gs[r]->impl->finish(r, n_global);
+    }
+    for (int r = 0; r < world; ++r) out[r] = gs[r].release();
+  });
+}
+
+void strom_shard_make_current(strom_shard* g) { t_current_shard = g ? g->impl : nullptr; }
+
+int strom_shard_status(strom_shard* g, int64_t* exchanges_out, int32_t* error_out) {
+  return guarded([&] {
+    STROM_REQUIRE(g && g->impl && g->impl->connected, "shard group not connected");
+    STROM_CUDA(cudaDeviceSynchronize());
+    unsigned long long seq = 0;
+    int32_t err = 0;
+    STROM_CUDA(cudaMemcpy(&seq, g->impl->dev.seq, sizeof(seq), cudaMemcpyDeviceToHost));
+    STROM_CUDA(cudaMemcpy(&err, g->impl->dev.err, sizeof(err), cudaMemcpyDeviceToHost));
+    if (exchanges_out) *exchanges_out = (int64_t)seq;
+    if (error_out) *error_out = err;
+  });
+}
+
+void strom_shard_free(strom_shard* g) { delete g; }
 
 void strom_isvd_free(strom_isvd* h) { delete h; }
 

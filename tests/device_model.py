@@ -17,9 +17,35 @@ EPS = np.finfo(float).eps
 FOLD_TAU = 1e-3
 
 
+class LocalSums:
+    """Sums over rows, all rows in this process (the unsharded device)."""
+
+    def total(self, partial):
+        return partial
+
+
+class BlockSums:
+    """Sums over rows as the row-sharded device forms them (csrc/shard.cuh): a
+    partial per row block, exchanged, added in BLOCK (rank) order on every rank.
+    `exchange(partial) -> list of every rank's partial in rank order`."""
+
+    def __init__(self, exchange):
+        self.exchange = exchange
+
+    def total(self, partial):
+        parts = self.exchange(np.asarray(partial, dtype=float))
+        out = np.zeros_like(parts[0])
+        for q in parts:  # rank order: identical bits on every rank
+            out = out + q
+        return out
+
+
 class DevState:
-    def __init__(self, n, tol_svd, tol_sv=0.0, r_max=None, ccap=None):
+    """n is the matrix's (global) row count; U holds this process's rows."""
+
+    def __init__(self, n, tol_svd, tol_sv=0.0, r_max=None, ccap=None, sums=None):
         self.n = n
+        self.sums = sums or LocalSums()
         self.U = np.zeros((n, 0))
         self.W = np.zeros((0, 0))
         self.L = np.zeros((0, 0))
@@ -39,14 +65,15 @@ class DevState:
         return self.U @ self.W
 
 
-def init(x, tol_svd, k=1, **kw):
-    s = DevState(x.size, tol_svd, **kw)
+def init(x, tol_svd, k=1, n=None, **kw):
+    s = DevState(x.size if n is None else n, tol_svd, **kw)
     s.k = k
-    nrm = np.sqrt(x @ x)
+    xx = float(s.sums.total(x @ x))
+    nrm = np.sqrt(xx)
     if nrm > tol_svd:
         s.U = x[:, None].copy()
         s.W = np.array([[1.0 / nrm]])
-        s.L = np.array([[np.sqrt(x @ x)]])
+        s.L = np.array([[np.sqrt(xx)]])
         s.sigma = np.array([nrm])
         s.V = np.zeros((k, 1))
         s.V[k - 1, 0] = 1.0
@@ -58,14 +85,15 @@ def init(x, tol_svd, k=1, **kw):
 def compact(s):
     c, r = s.W.shape
     if r == 0:
-        s.U = np.zeros((s.n, 0)); s.W = np.zeros((0, 0)); s.L = np.zeros((0, 0))
+        s.U = np.zeros((s.U.shape[0], 0)); s.W = np.zeros((0, 0)); s.L = np.zeros((0, 0))
         return
     m = s.L.T @ s.W
     q, rr = np.linalg.qr(m)
     t = np.linalg.solve(s.L.T, q)
     s.U = s.U @ t
     s.W = rr
-    s.L = np.eye(r)
+    # the device measures the Gram of the stored U_new (one more exchange when sharded)
+    s.L = np.linalg.cholesky(s.sums.total(s.U.T @ s.U))
 
 
 def update(s, x):
@@ -75,10 +103,11 @@ def update(s, x):
         compact(s)
         c = s.U.shape[1]
     if r == 0:
-        t = init(x, s.tol_svd, k, tol_sv=s.tol_sv, r_max=s.r_max, ccap=s.ccap)
+        t = init(x, s.tol_svd, k, n=s.n, tol_sv=s.tol_sv, r_max=s.r_max, ccap=s.ccap, sums=s.sums)
         return t
-    g = s.U.T @ x
-    xx = x @ x
+    # one exchange per pass: [U^T x | x.x], then [U^T r | r.r] (the k_pass partial layout)
+    gx = s.sums.total(np.concatenate([s.U.T @ x, [x @ x]]))
+    g, xx = gx[:-1], gx[-1]
     ell = s.W.T @ g
     p_sq = xx - ell @ ell
     p = np.sqrt(p_sq) if p_sq > 0 else 0.0
@@ -90,8 +119,8 @@ def update(s, x):
     if not dep:
         gt = np.linalg.solve(s.L.T, np.linalg.solve(s.L, g))
         r1 = x - s.U @ gt
-        e = s.U.T @ r1
-        rho2 = r1 @ r1
+        er = s.sums.total(np.concatenate([s.U.T @ r1, [r1 @ r1]]))
+        e, rho2 = er[:-1], er[-1]
         lv = np.linalg.solve(s.L, e) if c else np.zeros(0)
         lam2 = rho2 - lv @ lv
         app = lam2 > FOLD_TAU ** 2 * rho2 and rho2 > 0
@@ -99,8 +128,8 @@ def update(s, x):
             # DGKS: second classical Gram-Schmidt pass on r1 (in place)
             h = np.linalg.solve(s.L.T, lv)
             r1 = r1 - s.U @ h
-            e = s.U.T @ r1
-            rho2 = r1 @ r1
+            er = s.sums.total(np.concatenate([s.U.T @ r1, [r1 @ r1]]))
+            e, rho2 = er[:-1], er[-1]
             lv = np.linalg.solve(s.L, e) if c else np.zeros(0)
             lam2 = rho2 - lv @ lv
             app = lam2 > 0.25 * rho2 and rho2 > 0
@@ -159,7 +188,7 @@ def update(s, x):
             qs = qs * d
             W = np.linalg.solve(Ln.T, qs)
             did_qr = True
-    t = DevState(s.n, s.tol_svd, s.tol_sv, s.r_max, s.ccap)
+    t = DevState(s.n, s.tol_svd, s.tol_sv, s.r_max, s.ccap, s.sums)
     t.U, t.W, t.L, t.sigma, t.V, t.k = Un, W, Ln, sig, V, k
     t.flags = dict(dep=dep, trunc=trunc, qr=did_qr, drift=drift, p=p, appended=cn > c)
     return t
