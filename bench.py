@@ -239,6 +239,18 @@ def _prof_read(lib, capi):
     return list(pl), list(pms), list(pby)
 
 
+SKIP_LAUNCH_MS = 0.03  # a pass that streams U at n_s = 2^20 takes > 0.1 ms; an early return < 0.02 ms
+
+
+def _prof_durations(lib, capi, kind, cap=1 << 16):
+    import ctypes as C
+
+    buf = (C.c_float * cap)()
+    n = C.c_int32()
+    lib.strom_profile_durations(kind, cap, buf, C.byref(n))
+    return [float(buf[i]) for i in range(min(cap, n.value))]
+
+
 def time_ingest(start_state, cols, steps, warmup, ws=1, clocks=False):
     """Warm-up + `steps` timed ingests of `cols` from `start_state`; CUDA events
     on the launching (current) stream; returns (ms total, last state, launches,
@@ -306,6 +318,25 @@ def bench_isvd_device(args, ws, rank):
                                "gbs": (pby[k] / (pms[k] / 1e3) / 1e9) if pms[k] > 0 and pby[k] > 0 else None,
                                "bytes": pby[k] or None}
                for k in range(len(PROF_KINDS)) if pl[k]}
+    # A pass launched for a snapshot that the device-side decision found dependent returns
+    # at once and moves no bytes (window mode, DESIGN 3a): split the per-launch event times
+    # of the byte-counting passes into the launches that streamed U and the ones that did not.
+    pms = list(pms)
+    for name in ("u_pass",):
+        k = PROF_KINDS.index(name)
+        if not pl[k] or not pby[k]:
+            continue
+        durs = _prof_durations(lib, _capi, k)
+        live = [t for t in durs if t >= SKIP_LAUNCH_MS]
+        if durs and live and len(live) < len(durs):
+            kernels[name].update({"ms_all_launches": kernels[name]["ms"], "ms": round(sum(live), 4),
+                                  "launches_with_work": len(live),
+                                  "launches_skipped_on_device": len(durs) - len(live),
+                                  "skipped_ms": round(sum(durs) - sum(live), 4),
+                                  "gbs": pby[k] / (sum(live) / 1e3) / 1e9,
+                                  "note": f"ms / gbs over the launches that streamed U (event time >= "
+                                          f"{SKIP_LAUNCH_MS} ms); a skipped launch moves no bytes"})
+            pms[k] = sum(live)
     seed0 = dict(seed="numpy 0", snapshots_per_s=value / ws, **counts_of(prof_last, pl))
     del prof_last
     info = last.info()
@@ -782,7 +813,8 @@ def run_device(args):
                      "step_bytes_per_snapshot": dev_bytes_step / nsnap,
                      "floor_frac": per_rank_rate * floor_bytes / (bw * 1e9),
                      "floor_bytes_per_snapshot": floor_bytes,
-                     "note": "frac: the dominant kernel's algorithmic bytes / its event time; step_frac: all of "
+                     "note": "frac: the dominant kernel's algorithmic bytes / its event time over the launches "
+                             "that did work (kernels.*.launches_skipped_on_device returned at once); step_frac: all of "
                              "the step's device HBM bytes / step time; floor_frac: snapshots/s x 8 n (k+1) (read Phi "
                              "and x once: the any-algorithm floor of SURVEY 8(d)) / peak"},
         "north_star": {"target": ">= 0.70 of the HBM roofline at n_s=2^20, k=64",

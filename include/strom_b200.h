@@ -49,6 +49,11 @@ int strom_device_synchronize(void);
 void strom_profile_enable(int32_t on);
 int strom_profile_reset(void);
 int strom_profile_read(int32_t nkinds, int64_t* launches_host, double* ms_host, double* bytes_host);
+/* Per-launch event durations (ms, launch order) of one kind recorded since the
+ * last reset: at most `max` values into ms_host, the total count into n_out.
+ * Lets a caller separate launches that returned at once (a pass skipped by a
+ * device-side decision moves no bytes) from the ones that did the work. */
+int strom_profile_durations(int32_t kind, int32_t max, float* ms_host, int32_t* n_out);
 
 /* fp64 tensor-pipe (DMMA) throughput probe: launches ctas_per_sm x SMs CTAs of
  * `iters` DMMA rounds on `stream`; *flops_out = flops issued (time it with events). */

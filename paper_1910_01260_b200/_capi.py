@@ -43,6 +43,7 @@ _PROTOS = {
     "strom_profile_enable": (None, [i32]),
     "strom_profile_reset": (C.c_int, []),
     "strom_profile_read": (C.c_int, [i32, C.POINTER(i64), C.POINTER(dbl), C.POINTER(dbl)]),
+    "strom_profile_durations": (C.c_int, [i32, i32, C.POINTER(C.c_float), C.POINTER(i32)]),
     "strom_fp64_probe": (C.c_int, [i32, i32, vp, C.POINTER(dbl)]),
     "strom_isvd_init": (C.c_int, [i64, vp, i64, dbl, dbl, i64, i32, vp, C.POINTER(vp)]),
     "strom_isvd_update": (C.c_int, [vp, vp, vp, C.POINTER(vp)]),

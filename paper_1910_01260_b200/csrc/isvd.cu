@@ -804,10 +804,13 @@ void launch_step_b(const StateView& src, const StateView& dst, const PipeMem& m,
                    const Caps& caps, cudaStream_t s) {
   int use_smem = 0;
   const size_t smem = small_kernel_smem(caps, &use_smem);
-  static PerDevice<size_t> cfg;
-  set_smem_attr(k_step_b, smem, &cfg.get());
   ProfScope ps(P_STEP_B, s);
-  k_step_b<<<1, kSmallThreads, smem, s>>>(src, dst, m.pp, P, use_smem);
+  if (use_smem) {
+    set_smem_attr(k_step_b<true>, smem);
+    k_step_b<true><<<1, kSmallThreads, smem, s>>>(src, dst, m.pp, P);
+  } else {
+    k_step_b<false><<<1, kSmallThreads, 0, s>>>(src, dst, m.pp, P);
+  }
   STROM_LAUNCH_CHECK();
 }
 
@@ -1197,10 +1200,13 @@ void launch_step_b_pp(const StateView& src, const StateView& dst, const Pipe& pp
                       const Caps& caps, cudaStream_t s) {
   int use_smem = 0;
   const size_t smem = small_kernel_smem(caps, &use_smem);
-  static PerDevice<size_t> cfg;
-  set_smem_attr(k_step_b, smem, &cfg.get());
   ProfScope ps(P_STEP_B, s);
-  k_step_b<<<1, kSmallThreads, smem, s>>>(src, dst, pp, P, use_smem);
+  if (use_smem) {
+    set_smem_attr(k_step_b<true>, smem);
+    k_step_b<true><<<1, kSmallThreads, smem, s>>>(src, dst, pp, P);
+  } else {
+    k_step_b<false><<<1, kSmallThreads, 0, s>>>(src, dst, pp, P);
+  }
   STROM_LAUNCH_CHECK();
 }
 

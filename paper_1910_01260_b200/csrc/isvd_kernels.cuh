@@ -1111,9 +1111,10 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(PassArgs a, int nstage
 // mid_ctr (window mode): the core SVD only needs k_decide_a's results; the
 // rest (how r entered U: cn, n_j, a demotion to dependent) waits here for
 // *mid_ctr >= mid_target (the decision chain's end).
+template <bool kSmem>  // the work area in shared memory (LDS/STS instead of generic accesses) or in pp.work
 __device__ inline void step_b_body(const StateView& src, const StateView& dst, const Pipe& pp, const IsvdParams& P,
-                                   int use_smem, double* smem, double* red, const int32_t* mid_ctr = nullptr,
-                                   int32_t mid_target = -1) {
+                                   double* smem, double* red, const int32_t* mid_ctr = nullptr,
+                                   int32_t mid_target = -1, const double** n_sm = nullptr, int* n_sm_ld = nullptr) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const IsvdHdr h = *src.hdr;
   IsvdStep* st = pp.step[P.parity];
@@ -1173,49 +1174,67 @@ __device__ inline void step_b_body(const StateView& src, const StateView& dst, c
   // ---- shared-memory plan (global fallback when it does not fit) ----------
   //   WS m^2 | Wt m^2 | Vt m^2 | core work 16 ms | WB ccap x m (staged N_b, later QR's M)
   const int64_t ms = P.work_stride;
-  double* base = use_smem ? smem : pp.work + 4 * ms;
+  double* base = kSmem ? smem : pp.work + 4 * ms;
   double* WS = base;                      // sorted, signed W_bar (m x m)
   double* Wt = WS + (int64_t)m * m;       // vectors by slot, later W^T W
   double* Vt = Wt + (int64_t)m * m;       // vectors by slot, later the polished W_bar
   double* cb = Vt + (int64_t)m * m;
   double* WB = cb + 16 * ms;              // N_b = [[N, n_j]] (cn x m, ld ccap)
+  double* NS = Wt;                        // after the SVD: N' (cn x mk, ld cn) over the dead Wt | Vt
   double* svs = cb + 14 * ms;             // m sorted singular values
   CoreSvdWork cw;
   cw.d = cb; cw.z = cb + ms; cw.zh = cb + 2 * ms; cw.mu = cb + 3 * ms; cw.sv = cb + 4 * ms;
   cw.rc = cb + 5 * ms; cw.rs = cb + 6 * ms;
+  cw.dk = cb + 11 * ms; cw.zk = cb + 12 * ms; cw.dorg = cb + 13 * ms;
   {
     int* ib = reinterpret_cast<int*>(cb + 7 * ms);
     cw.org = ib; cw.kset = ib + ms; cw.defl = ib + 2 * ms; cw.ra = ib + 3 * ms; cw.rb = ib + 4 * ms;
     cw.perm = ib + 5 * ms; cw.cnt = ib + 6 * ms;
   }
+  // stage N (c x r) into N_b now: the L2 loads overlap the solver's set-up; the appended
+  // row and the n_j column follow once the decision chain is known (below)
+  // (a warp per column, 4 x 4 loads per thread in flight: one L2 latency per 64 x 128 block)
+  for (int b0 = 0; b0 < r; b0 += 4 * nw)
+    for (int a0 = 0; a0 < c; a0 += 128) {
+      double v[4][4];
+#pragma unroll
+      for (int q1 = 0; q1 < 4; ++q1)
+#pragma unroll
+        for (int q2 = 0; q2 < 4; ++q2) {
+          const int b = b0 + wid + nw * q1, a = a0 + lane + 32 * q2;
+          v[q1][q2] = (b < r && a < c) ? __ldcg(src.N + (int64_t)b * src.ldn + a) : 0.0;
+        }
+#pragma unroll
+      for (int q1 = 0; q1 < 4; ++q1)
+#pragma unroll
+        for (int q2 = 0; q2 < 4; ++q2) {
+          const int b = b0 + wid + nw * q1, a = a0 + lane + 32 * q2;
+          if (b < r && a < c) WB[b * P.ccap + a] = v[q1][q2];
+        }
+    }
   // ---- 2. the bordered core and its SVD (rank-one secular solver) ----------
-  core_svd_secular(src.sigma, ell, dep ? 0.0 : p, r, cw, Wt, Vt, svs, WS, pp.vbar, red,
-                   P.tprobe ? P.tprobe + 8 : nullptr, P.tprobe ? P.tprobe + 300 : nullptr);
-  trace_stamp(P.trace, 9);
-  if (mid_ctr) {
+  for (int attempt = 0; attempt < 2; ++attempt) {  // (one inlined copy of the solver)
+    core_svd_secular(src.sigma, ell, dep ? 0.0 : p, r, cw, Wt, Vt, svs, WS, pp.vbar, red,
+                     (P.tprobe && attempt == 0) ? P.tprobe + 8 : nullptr,
+                     (P.tprobe && attempt == 0) ? P.tprobe + 300 : nullptr);
+    if (attempt == 0) trace_stamp(P.trace, 9);
+    if (attempt == 1 || !mid_ctr) break;
     wait_counter(mid_ctr, mid_target);
     trace_stamp(P.trace, 10);
     const bool dep2 = *(volatile const int32_t*)&st->dep != 0;
-    if (dep2 != dep) {  // the residual could not enter U: the update is dependent after all
-      dep = dep2;
-      __syncthreads();
-      core_svd_secular(src.sigma, ell, dep ? 0.0 : p, r, cw, Wt, Vt, svs, WS, pp.vbar, red, nullptr, nullptr);
-    }
+    if (dep2 == dep) break;
+    dep = dep2;  // the residual could not enter U: the update is dependent after all
+    __syncthreads();
   }
   const int cn = st->cn;
   const int action = st->action;
   const bool appended = (action == 1);
-  // stage N_b: columns 0..r-1 = N (c rows; the appended row is 0), column r = n_j
-  for (int b = wid; b < m; b += nw) {
-    const double* ns = src.N + (int64_t)b * src.ldn;
-    double* wb = WB + b * P.ccap;
-    for (int a = lane; a < cn; a += 32) {
-      double v;
-      if (b < r) v = (a < c) ? ns[a] : 0.0;
-      else v = dep ? 0.0 : wj[a];
-      wb[a] = v;
-    }
+  // rest of N_b: the appended row of columns 0..r-1 is 0, column r = n_j
+  for (int idx = threadIdx.x; idx < r * (cn - c); idx += blockDim.x) {
+    const int b = idx / (cn - c), a = c + idx - b * (cn - c);
+    WB[b * P.ccap + a] = 0.0;
   }
+  for (int a = threadIdx.x; a < cn; a += blockDim.x) WB[r * P.ccap + a] = dep ? 0.0 : wj[a];
   __syncthreads();
   STROM_TPROBE(P, 2);
   // (no orthogonality polish needed: the Gu-Eisenstat vectors are orthogonal to
@@ -1227,10 +1246,21 @@ __device__ inline void step_b_body(const StateView& src, const StateView& dst, c
   if (mk > 0 && svs[mk - 1] < P.tol_sv) { mk -= 1; trunc = true; }
   if (P.r_max >= 0 && mk > P.r_max) { mk = P.r_max; trunc = true; }
   // ---- 4. N' = N_b W_bar[:, :mk]  (basis.py:150-158 in Q_U coordinates) ---
+  // a second copy of N' stays in the work area (over the dead Wt | Vt) for the drift test,
+  // the QR and the next snapshot's inline decision, when it fits there
+  const bool ns_ok = (int64_t)cn * mk <= 2 * (int64_t)m * m;
+  const double* Nn = ns_ok ? NS : dst.N;
+  const int64_t ldnn = ns_ok ? cn : dst.ldn;
   {
     const int kdim = dep ? r : m;
-    cta_gemm_dmma(cn, mk, kdim, WB, 1, P.ccap, WS, 1, m,
-                  [&](int a, int k, double v) { dst.N[(int64_t)k * dst.ldn + a] = v; });
+    if (ns_ok)
+      cta_gemm_dmma_n2(cn, mk, kdim, WB, 1, P.ccap, WS, 1, m, [&](int a, int k, double v) {
+        dst.N[(int64_t)k * dst.ldn + a] = v;
+        NS[k * cn + a] = v;
+      });
+    else
+      cta_gemm_dmma_n2(cn, mk, kdim, WB, 1, P.ccap, WS, 1, m,
+                       [&](int a, int k, double v) { dst.N[(int64_t)k * dst.ldn + a] = v; });
   }
   for (int k = threadIdx.x; k < mk; k += blockDim.x) dst.sigma[k] = svs[k];
   __syncthreads();
@@ -1241,8 +1271,7 @@ __device__ inline void step_b_body(const StateView& src, const StateView& dst, c
   if (mk > 1) {
     // phi_0 . phi_last = N_0 . N_last (Q_U is orthonormal)
     double part = 0.0;
-    for (int a = threadIdx.x; a < cn; a += blockDim.x)
-      part = fma(dst.N[a], dst.N[(int64_t)(mk - 1) * dst.ldn + a], part);
+    for (int a = threadIdx.x; a < cn; a += blockDim.x) part = fma(Nn[a], Nn[(mk - 1) * ldnn + a], part);
     drift = fabs(block_sum(part, red));
     const double thr = fmin(P.tol_svd, 2.220446049250313e-16 * (double)P.n);
     STROM_TPROBE(P, 5);
@@ -1254,10 +1283,10 @@ __device__ inline void step_b_body(const StateView& src, const StateView& dst, c
       // an ill-conditioned N' (the reference's non-unit j columns can make it so)
       // takes the Householder path.
       double* M = WB;   // cn x mk, ld cn  (N_b is dead)
-      double* Bm = Wt;  // mk x mk Gram, then its Cholesky factor
+      double* Bm = Wt;  // mk x mk Gram, then its Cholesky factor (N' has moved to M by then)
       bool chol_ok = true;
       for (int k = wid; k < mk; k += nw)
-        for (int a = lane; a < cn; a += 32) M[k * cn + a] = dst.N[(int64_t)k * dst.ldn + a];
+        for (int a = lane; a < cn; a += 32) M[k * cn + a] = Nn[k * ldnn + a];
       __syncthreads();
       for (int pass = 0; pass < 2 && chol_ok; ++pass) {
         STROM_TPROBE(P, 280 + 6 * pass);
@@ -1290,6 +1319,10 @@ __device__ inline void step_b_body(const StateView& src, const StateView& dst, c
       __syncthreads();
     }
   }
+  if (n_sm) {  // where the caller finds N' in shared memory (the QR result lives in M)
+    *n_sm = did_qr ? WB : (ns_ok ? NS : nullptr);
+    *n_sm_ld = cn;
+  }
   STROM_TPROBE(P, 6);
   if (threadIdx.x == 0) {
     o.r = mk;
@@ -1311,7 +1344,8 @@ __device__ inline void step_b_body(const StateView& src, const StateView& dst, c
 // core step right after it produced N' -- the next core step can then start
 // without waiting for k_decide_a.  Not for restarts, rejects or errors (those
 // stay with k_decide_a).  Returns false when it did not run.
-__device__ inline bool decide_next_inline(const StateView& dst, const Pipe& pp, const IsvdParams& P, double* red) {
+__device__ inline bool decide_next_inline(const StateView& dst, const Pipe& pp, const IsvdParams& P, double* red,
+                                          const double* n_sm, int n_sm_ld) {
   __syncthreads();
   const IsvdHdr h = *dst.hdr;
   const double xx = *(volatile const double*)&pp.ctl->xx;
@@ -1319,7 +1353,8 @@ __device__ inline bool decide_next_inline(const StateView& dst, const Pipe& pp, 
   if (h.status != 0 || !isfinite(xx) || h.r == 0 || (at_cap && P.cap_mode == 0)) return false;
   const int np = P.parity ^ 1, c = h.c, r = h.r;
   double* ell = pp.ell[np];
-  cta_gemv_t_cm(dst.N, dst.ldn, c, r, pp.tvec, ell, false);
+  if (n_sm) cta_gemv_t_cm(n_sm, n_sm_ld, c, r, pp.tvec, ell, false);  // N' still in shared memory: same values
+  else cta_gemv_t_cm(dst.N, dst.ldn, c, r, pp.tvec, ell, false);
   double s_ll = 0.0;
   for (int i = threadIdx.x; i < r; i += blockDim.x) s_ll = fma(ell[i], ell[i], s_ll);
   s_ll = block_sum(s_ll, red);
@@ -1350,21 +1385,23 @@ __device__ inline bool decide_next_inline(const StateView& dst, const Pipe& pp, 
   return true;
 }
 
-__global__ void __launch_bounds__(kSmallThreads) k_step_b(StateView src, StateView dst, Pipe pp, IsvdParams P,
-                                                          int use_smem) {
+template <bool kSmem>
+__global__ void __launch_bounds__(kSmallThreads) k_step_b(StateView src, StateView dst, Pipe pp, IsvdParams P) {
   extern __shared__ double smem[];
   __shared__ double red[32];
   if (P.wn > 0) {  // window mode: the SVD needs only k_decide_a; the rest waits mid-way
     wait_counter(&pp.ctl->adone, P.d_expect);
     trace_stamp(P.trace, 8);
-    step_b_body(src, dst, pp, P, use_smem, smem, red, &pp.ctl->decided, P.d_expect);
-    if (P.inline_next && decide_next_inline(dst, pp, P, red)) {
+    const double* n_sm = nullptr;
+    int n_sm_ld = 0;
+    step_b_body<kSmem>(src, dst, pp, P, smem, red, &pp.ctl->decided, P.d_expect, &n_sm, &n_sm_ld);
+    if (P.inline_next && decide_next_inline(dst, pp, P, red, n_sm, n_sm_ld)) {
       signal_counter(&pp.ctl->adone);  // the next core step may start its SVD now
     }
   } else {
     wait_counter(&pp.ctl->decided, P.d_expect);  // this snapshot's decision chain
     trace_stamp(P.trace, 8);
-    step_b_body(src, dst, pp, P, use_smem, smem, red);
+    step_b_body<kSmem>(src, dst, pp, P, smem, red);
   }
   signal_counter(&pp.ctl->bdone);  // the next snapshot's decision may read this state
   trace_stamp(P.trace, 11);

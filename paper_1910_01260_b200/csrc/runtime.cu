@@ -401,6 +401,24 @@ int strom_profile_read(int32_t nkinds, int64_t* launches, double* ms, double* by
   });
 }
 
+int strom_profile_durations(int32_t kind, int32_t max, float* ms, int32_t* n_out) {
+  return strom::guarded([&] {
+    STROM_REQUIRE(kind >= 0 && kind < strom::P_NKINDS && n_out, "bad profile kind");
+    STROM_CUDA(cudaDeviceSynchronize());
+    auto& p = strom::prof();
+    std::lock_guard<std::mutex> g(p.mu);
+    int n = 0;
+    for (auto& pr : p.pairs) {
+      if (pr.first != kind) continue;
+      float t = 0.f;
+      if (cudaEventElapsedTime(&t, pr.second.first, pr.second.second) != cudaSuccess) t = -1.f;
+      if (ms && n < max) ms[n] = t;
+      ++n;
+    }
+    *n_out = n;
+  });
+}
+
 int strom_fp64_probe(int32_t iters, int32_t ctas_per_sm, void* stream, double* flops_out) {
   return strom::guarded([&] {
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);

@@ -31,9 +31,11 @@ void set_last_error(const std::string& msg);
 #define STROM_CUDA(expr)                                                                  \
   do {                                                                                    \
     cudaError_t _e = (expr);                                                              \
-    if (_e != cudaSuccess)                                                                \
+    if (_e != cudaSuccess) {                                                              \
+      (void)cudaGetLastError(); /* reported here: a later launch check must not see it */ \
       throw ::strom::Error(::strom::kCudaError, std::string(#expr) + ": " +               \
                                                     cudaGetErrorString(_e));              \
+    }                                                                                     \
   } while (0)
 
 #define STROM_STR2(x) #x

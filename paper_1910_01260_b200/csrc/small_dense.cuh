@@ -334,6 +334,46 @@ __device__ inline void cta_gemm_dmma(int M, int N, int K, const double* A, int64
   }
 }
 
+// The same product with two accumulator tiles per warp (an 8 x 16 output block:
+// one A fragment feeds two independent DMMA chains, the k-steps unrolled so the
+// fragment loads run ahead).  B200's fp64 tensor rate equals its vector rate
+// (~64 FMA/clk/SM), so a one-CTA product is latency work: what matters is
+// independent chains in flight.  Every output sums its k-steps in the same
+// order as cta_gemm_dmma: identical results.
+template <class Store>
+__device__ inline void cta_gemm_dmma_n2(int M, int N, int K, const double* A, int64_t asi, int64_t ask,
+                                        const double* B, int64_t bsk, int64_t bsj, Store store) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int tm = (M + 7) >> 3, tn = (N + 15) >> 4, ks = (K + 3) >> 2;
+  for (int tile = wid; tile < tm * tn; tile += nw) {
+    const int i0 = (tile % tm) << 3, j0 = (tile / tm) << 4;
+    const int ia = i0 + g, jb0 = j0 + g, jb1 = j0 + 8 + g;
+    const bool va = ia < M, vb0 = jb0 < N, vb1 = jb1 < N;
+    const double* ap = A + (int64_t)(va ? ia : 0) * asi;
+    const double* bp0 = B + (int64_t)(vb0 ? jb0 : 0) * bsj;
+    const double* bp1 = B + (int64_t)(vb1 ? jb1 : 0) * bsj;
+    double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
+#pragma unroll 4
+    for (int kk = 0; kk < ks; ++kk) {
+      const int k = (kk << 2) + t;
+      const bool vk = k < K;
+      const double av = (va && vk) ? ap[(int64_t)k * ask] : 0.0;
+      const double b0 = (vb0 && vk) ? bp0[(int64_t)k * bsk] : 0.0;
+      const double b1 = (vb1 && vk) ? bp1[(int64_t)k * bsk] : 0.0;
+      dmma884(c00, c01, av, b0);
+      dmma884(c10, c11, av, b1);
+    }
+    const int r = i0 + g, c = j0 + 2 * t;
+    if (r < M) {
+      if (c < N) store(r, c, c00);
+      if (c + 1 < N) store(r, c + 1, c01);
+      if (c + 8 < N) store(r, c + 8, c10);
+      if (c + 9 < N) store(r, c + 9, c11);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // In-place lower Cholesky B = L L^T (n x n, column-major, ld), right-looking,
 // block-parallel, two barriers per column.  Returns min/max pivot ratio, or -1

@@ -219,3 +219,11 @@ def test_diverging_ranks_fail_instead_of_hanging(cuda, monkeypatch):
         for o in (out0, out1):
             if o.value:
                 capi.lib.strom_shard_free(o)
+        # a refused connect or a timed-out exchange must not leave a CUDA error behind
+        # for the next launch check of an unrelated call
+        y = torch.randn(256, 3, dtype=torch.float64, device="cuda")
+        st2 = basis.ingest_simulation(basis.isvd_init(y[:, 0].contiguous(), 1e-8), y[:, 1:])
+        assert st2.rank == 3
+        from paper_1910_01260_b200 import linalg
+        q, r = linalg.qr(y)
+        assert torch.allclose(q @ r, y, atol=1e-12)

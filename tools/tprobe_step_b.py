@@ -14,19 +14,29 @@ from paper_1910_01260_b200 import _capi, basis, workloads as wl  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument('--cols', type=int, default=40)
+ap.add_argument('--pipelined', action='store_true')
 args = ap.parse_args()
-xt, _, _, _ = wl.cfg2_stream_torch(n=1 << 20, cols=100 + args.cols, rank=64, seed=0)
+xt, _, _, _ = wl.cfg2_stream_torch(n=1 << 20, cols=100 + args.cols + 24, rank=64, seed=0)
 st = basis.isvd_init(xt[0], 1e-9, tol_sv=1e-9, r_max=64, cap_mode='truncate')
 st = basis.ingest_simulation(st, xt[1:100].T)
 buf = torch.zeros(512, dtype=torch.int64, device='cuda')
 _capi.lib.strom_debug_tprobe(_capi.C.c_void_p(buf.data_ptr()))
 rows = []
-for t in range(100, 100 + args.cols):
-    buf.zero_()
-    st = basis.ingest_simulation(st, xt[t:t + 1].T)
-    torch.cuda.synchronize()
-    b = buf.cpu().numpy()
-    rows.append(b.copy())
+if args.pipelined:
+    # the probes of the LAST update of a pipelined multi-column ingest (warm instruction cache,
+    # neighbours running): one sample per call
+    for q in range(args.cols):
+        buf.zero_()
+        basis.ingest_simulation(st, xt[100:100 + 24 + q].T).rank
+        torch.cuda.synchronize()
+        rows.append(buf.cpu().numpy().copy())
+else:
+    for t in range(100, 100 + args.cols):
+        buf.zero_()
+        st = basis.ingest_simulation(st, xt[t:t + 1].T)
+        torch.cuda.synchronize()
+        b = buf.cpu().numpy()
+        rows.append(b.copy())
 _capi.lib.strom_debug_tprobe(_capi.C.c_void_p(0))
 R = np.array(rows)
 names = {0: 'B0 start', 1: 'B1 setup', 2: 'B2 core svd', 3: 'B3', 4: 'B4 N update', 5: 'B5 drift', 6: 'B6 qr'}

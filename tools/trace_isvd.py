@@ -47,6 +47,18 @@ for k in range(16):
     v = v[np.isfinite(v)]
     if v.size:
         print(f'  {names[k]:15s} {np.median(v):8.1f} [{np.percentile(v, 10):7.1f}, {np.percentile(v, 90):7.1f}]  ({v.size})')
+ind = np.isfinite(T[:, 3])
+for label, sel in (('independent', ind), ('dependent', ~ind)):
+    print(f'-- {label} updates only ({int(sel.sum())}): median [p10, p90]')
+    for k in range(14):
+        v = rel[sel, k]
+        v = v[np.isfinite(v)]
+        if v.size:
+            print(f'  {names[k]:15s} {np.median(v):8.1f} [{np.percentile(v, 10):7.1f}, {np.percentile(v, 90):7.1f}]')
+    nxt = (T[1:, 0] - T[:-1, 0]) / 1e3
+    v = nxt[sel[:-1]]
+    v = v[np.isfinite(v)]
+    print(f'  next A start    {np.median(v):8.1f} [{np.percentile(v, 10):7.1f}, {np.percentile(v, 90):7.1f}]')
 per = np.diff(T[:, 0]) / 1e3
 print(f'A-to-A period: median {np.nanmedian(per):.1f} us, mean {np.nanmean(per):.1f}')
 dep = np.isnan(T[:, 3])
