@@ -675,19 +675,32 @@ def bench_cfg3(args):
         d = wl.cfg3_system(amp, a=a)
         sys_ = LinearDynamicalSystem(a=d.a, b=d.b, c=d.c, x0=d.x0, input_signal=d.inputs, constant_input=True)
         sys_.device_arrays()
-        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        # The GPU idles while the host assembles each sample's system and drops its clocks
+        # (clocks_throttle_reasons gpu_idle, 120-900 MHz seen); one-CTA latency phases then run
+        # several times slower for a while.  So: one untimed repetition to bring the clocks
+        # back, then the march once and the (functional: the source state is immutable)
+        # ingest three times, median.
+        fom_march(sys_, grid)
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         e[0].record()
         res = fom_march(sys_, grid)
         e[1].record()
-        if st is None:
-            st = basis.isvd_init(res.states[:, 0], wl.CFG3_TOL, tol_sv=wl.CFG3_TOL)
-            st = basis.ingest_simulation(st, res.states[:, 1:])
-        else:
-            st = basis.ingest_simulation(st, res.states)
-        e[2].record()
-        torch.cuda.synchronize()
+        reps = []
+        for rep in range(4):
+            ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ea.record()
+            if st is None:
+                nxt = basis.ingest_simulation(basis.isvd_init(res.states[:, 0], wl.CFG3_TOL, tol_sv=wl.CFG3_TOL),
+                                              res.states[:, 1:])
+            else:
+                nxt = basis.ingest_simulation(st, res.states)
+            eb.record()
+            torch.cuda.synchronize()
+            if rep:
+                reps.append(ea.elapsed_time(eb))
+        st = nxt
         fom_ms.append(e[0].elapsed_time(e[1]))
-        ingest_ms.append(e[1].elapsed_time(e[2]))
+        ingest_ms.append(float(np.median(reps)))
         iters += res.iterations
         del res
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -702,6 +715,9 @@ def bench_cfg3(args):
             "isvd_snapshots_per_s": nsnap / (sum(ingest_ms) / 1e3), "rank": st.rank,
             "temporal_bases_ms": e0.elapsed_time(e1), "device_total_ms": sum(fom_ms) + sum(ingest_ms) +
             e0.elapsed_time(e1), "operator_assembly_s_host": t_op,
+            "ingest_ms_per_sample": [round(v, 3) for v in ingest_ms],
+            "timing": "per sample: one untimed march (GPU clocks back up after the host-side assembly), the march "
+                      "timed once, the ingest median of 3 after one untimed repetition",
             "note": "the reference cannot produce these snapshots (SuperLU fill-in; SURVEY 8(d))"}
 
 

@@ -515,6 +515,9 @@ IsvdParams make_params(const strom_isvd* h, const PipeMem& m, int64_t k_new, boo
   P.wcol = 0;
   P.wn = 0;
   P.inline_next = 0;
+  P.stage_doubles = 0;
+  P.step_try = 0;
+  P.step_smem_doubles = 0;
   return P;
 }
 
@@ -722,6 +725,7 @@ void launch_pass(int kind, int cols_ub, const strom_isvd* h, const PipeMem& m, c
   a.ctl = m.pp.ctl;
   a.kind = kind;
   a.pstride = m.pstride;
+  a.pld = m.max_grid;
   a.x = x;
   a.coef = (kind == PASS_FUSED || kind == PASS_RESID) ? m.pp.gt : (kind == PASS_SECOND ? m.pp.h : nullptr);
   a.xn = xn;
@@ -790,9 +794,12 @@ bool decide_as_kernel() {
   return v;
 }
 
-size_t small_kernel_smem(const Caps& c, int* use_smem) {
+// r_ub >= 0: a bound on the state's current rank (the kernel lays its work area out by the
+// current m = r + 1, not by the capacity: an uncapped state whose rank capacity has grown past
+// what shared memory holds keeps the fast path while its rank still fits).
+size_t small_kernel_smem(const Caps& c, int* use_smem, int r_ub = -1) {
   // step B layout: 3 m^2 + 16 ms (secular work) + ccap m (staged N_b / QR's M)
-  const size_t m = c.rcap + 1;
+  const size_t m = (r_ub >= 0 ? std::min<int>(c.rcap, r_ub) : c.rcap) + 1;
   const size_t ms = round_up(std::max<int64_t>(c.ccap, c.rcap + 2), 32);
   const size_t need = (3 * m * m + 16 * ms + (size_t)c.ccap * m) * 8;
   const size_t limit = max_smem_optin() - 8 * 1024;
@@ -800,18 +807,41 @@ size_t small_kernel_smem(const Caps& c, int* use_smem) {
   return *use_smem ? need : 0;
 }
 
-void launch_step_b(const StateView& src, const StateView& dst, const PipeMem& m, const IsvdParams& P,
-                   const Caps& caps, cudaStream_t s) {
-  int use_smem = 0;
-  const size_t smem = small_kernel_smem(caps, &use_smem);
+// The core step.  Its work area (3 m^2 + 16 ms + ccap m doubles, m = r + 1) lives in shared
+// memory when the layout of the rank CAPACITY fits, or of the host's rank bound; otherwise
+// (an uncapped state whose capacity has grown) the shared-memory kernel is still tried with
+// all the shared memory there is -- it decides on the device by the CURRENT rank -- with the
+// global-memory kernel queued behind it as its fallback (IsvdParams::step_try).
+void launch_step_b_pp(const StateView& src, const StateView& dst, const Pipe& pp, const IsvdParams& P,
+                      const Caps& caps, cudaStream_t s, int r_ub = -1, int r_max = -1) {
+  int fits_cap = 0, fits_ub = 0;
+  size_t smem = small_kernel_smem(caps, &fits_cap);
+  if (!fits_cap && r_ub >= 0) smem = small_kernel_smem(caps, &fits_ub, r_ub);
   ProfScope ps(P_STEP_B, s);
-  if (use_smem) {
+  if (fits_cap || fits_ub) {
     set_smem_attr(k_step_b<true>, smem);
-    k_step_b<true><<<1, kSmallThreads, smem, s>>>(src, dst, m.pp, P);
+    k_step_b<true><<<1, kSmallThreads, smem, s>>>(src, dst, pp, P);
   } else {
-    k_step_b<false><<<1, kSmallThreads, 0, s>>>(src, dst, m.pp, P);
+    int fits_rmax = 1;
+    if (r_max >= 0) small_kernel_smem(caps, &fits_rmax, r_max);  // a capped stream sits at its cap
+    if (fits_rmax) {
+      const size_t room = max_smem_optin() - 8 * 1024;
+      IsvdParams Pt = P;
+      Pt.step_try = 1;
+      Pt.step_smem_doubles = (int32_t)(room / 8);
+      set_smem_attr(k_step_b<true>, room);
+      k_step_b<true><<<1, kSmallThreads, room, s>>>(src, dst, pp, Pt);
+      Pt.step_try = 2;
+      k_step_b<false><<<1, kSmallThreads, 0, s>>>(src, dst, pp, Pt);
+    } else {
+      k_step_b<false><<<1, kSmallThreads, 0, s>>>(src, dst, pp, P);
+    }
   }
   STROM_LAUNCH_CHECK();
+}
+void launch_step_b(const StateView& src, const StateView& dst, const PipeMem& m, const IsvdParams& P,
+                   const Caps& caps, cudaStream_t s, int r_ub = -1, int r_max = -1) {
+  launch_step_b_pp(src, dst, m.pp, P, caps, s, r_ub, r_max);
 }
 
 void launch_vupdate(const StateView& src, const StateView& dst, const PipeMem& m, const IsvdParams& P, int rcap,
@@ -1044,7 +1074,7 @@ strom_isvd* update_once(strom_isvd* src, const double* x, cudaStream_t s, bool i
     launch_pass(PASS_SECOND, cols, dst, m, x, nullptr, 0, s, tl);
     trace_point("second+decide2", s);
   }
-  launch_step_b(cur->view, dst->view, m, P, cur->caps, s);
+  launch_step_b(cur->view, dst->view, m, P, cur->caps, s, cur->r_ub, cur->r_max);
   trace_point("step_b", s);
   launch_vupdate(cur->view, dst->view, m, P, cur->caps.rcap, s);
   trace_point("vupdate", s);
@@ -1187,25 +1217,17 @@ void launch_decide_w(int which, const StateView& src, const Pipe& pp, const Pipe
     set_smem_attr(k_decide_a, smem, &cfga.get());
     launch_pdl(k_decide_a, dim3(1), dim3(kDecideThreads), smem, s, src, pp, P);
   } else if (which == 1) {
-    set_smem_attr(k_decide_b, smem, &cfgb.get());
-    launch_pdl(k_decide_b, dim3(1), dim3(kDecideThreads), smem, s, src, pp, P);
+    // room for the live block of L^{-1} and for N (decide_b_body stages them when they fit)
+    const size_t want = (size_t)m.ccap * (m.ccap + m.rcap + 1) * 8;
+    const size_t lim = max_smem_optin() - 4 * 1024;
+    IsvdParams Pb = P;
+    Pb.stage_doubles = (smem + want <= lim) ? (int32_t)(want / 8) : 0;
+    const size_t smem_b = smem + (size_t)Pb.stage_doubles * 8;
+    set_smem_attr(k_decide_b, smem_b, &cfgb.get());
+    launch_pdl(k_decide_b, dim3(1), dim3(kDecideThreads), smem_b, s, src, pp, Pb);
   } else {
     set_smem_attr(k_decide2, smem, &cfg2.get());
     launch_pdl(k_decide2, dim3(1), dim3(kDecideThreads), smem, s, src, pp, P);
-  }
-  STROM_LAUNCH_CHECK();
-}
-
-void launch_step_b_pp(const StateView& src, const StateView& dst, const Pipe& pp, const IsvdParams& P,
-                      const Caps& caps, cudaStream_t s) {
-  int use_smem = 0;
-  const size_t smem = small_kernel_smem(caps, &use_smem);
-  ProfScope ps(P_STEP_B, s);
-  if (use_smem) {
-    set_smem_attr(k_step_b<true>, smem);
-    k_step_b<true><<<1, kSmallThreads, smem, s>>>(src, dst, pp, P);
-  } else {
-    k_step_b<false><<<1, kSmallThreads, 0, s>>>(src, dst, pp, P);
   }
   STROM_LAUNCH_CHECK();
 }
@@ -1530,7 +1552,7 @@ strom_isvd* ingest_pipelined(strom_isvd* src, ColumnSource& cols, cudaStream_t s
       launch_decide_kernel(true, prev->view, m, P, s);
       ++d_launched;
       cols.release(t);
-      launch_step_b(prev->view, dst->view, m, P, prev->caps, s2);
+      launch_step_b(prev->view, dst->view, m, P, prev->caps, s2, prev->r_ub, prev->r_max);
       ++b_launched;
       STROM_CUDA(cudaEventRecord(evB, s2));
       launch_vupdate(prev->view, dst->view, m, P, prev->caps.rcap, s2);
@@ -1546,7 +1568,7 @@ strom_isvd* ingest_pipelined(strom_isvd* src, ColumnSource& cols, cudaStream_t s
       cols.release(t);
       STROM_CUDA(cudaEventRecord(evD, s));
       STROM_CUDA(cudaStreamWaitEvent(s2, evD, 0));
-      launch_step_b(prev->view, dst->view, m, P, prev->caps, s2);
+      launch_step_b(prev->view, dst->view, m, P, prev->caps, s2, prev->r_ub, prev->r_max);
       ++b_launched;
       STROM_CUDA(cudaEventRecord(evB, s2));
       launch_vupdate(prev->view, dst->view, m, P, prev->caps.rcap, s2);
@@ -1600,6 +1622,8 @@ strom_isvd* ingest_windowed(strom_isvd* src, ColumnSource& cols, cudaStream_t s,
     STROM_CUDA(cudaEventRecord(evJ3, s3));
     STROM_CUDA(cudaStreamWaitEvent(s, evJ3, 0));
   };
+  static const bool host_timing = getenv("STROM_HOST_TIMING") != nullptr;  // diagnostics: enqueue time of the loop
+  const auto host_t0 = std::chrono::steady_clock::now();
   for (int64_t t = 0; t < ncols; ++t) {
     {
       const bool rank_hit = prev->r_max < 0 && prev->r_ub + 1 > prev->caps.rcap && prev->caps.rcap < rank_rows(prev);
@@ -1708,7 +1732,7 @@ strom_isvd* ingest_windowed(strom_isvd* src, ColumnSource& cols, cudaStream_t s,
       const bool col_hit = c_ub + 1 > prev->caps.ccap;
       P.inline_next = (P.has_next && !rank_hit && !col_hit && inline_decide()) ? 1 : 0;
     }
-    launch_step_b_pp(prev->view, dst->view, pp, P, prev->caps, s2);
+    launch_step_b_pp(prev->view, dst->view, pp, P, prev->caps, s2, prev->r_ub, prev->r_max);
     ++b_launched;
     STROM_CUDA(cudaEventRecord(evB, s2));
     // s3: the V update
@@ -1721,6 +1745,11 @@ strom_isvd* ingest_windowed(strom_isvd* src, ColumnSource& cols, cudaStream_t s,
     dst->store->claimed = std::max(dst->store->claimed, dst->c_ub);
     dst->r_ub = std::min(prev->r_ub + 1, prev->caps.rcap);
     prev = dst;
+  }
+  if (host_timing) {
+    const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - host_t0).count();
+    fprintf(stderr, "[strom] window ingest: %lld snapshots enqueued in %.0f us (%.1f us each)\n", (long long)ncols, us,
+            us / (double)std::max<int64_t>(1, ncols));
   }
   join();
   strom_isvd* out = slot[(ncols - 1) & 1].release();

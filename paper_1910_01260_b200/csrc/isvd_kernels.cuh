@@ -60,6 +60,8 @@ struct PipeCtl {
   int32_t resid;    // window mode: the residual pass of this snapshot is needed
   int32_t adone;    // window mode: first-half decisions (k_decide_a) completed
   int32_t a_inline; // window mode: d_expect of the snapshot whose first half k_step_b already ran
+  int32_t slow_step;  // k_new of the update whose shared-memory core step handed over to the global-memory one
+  int32_t pad_;
   double xx;        // x.x of the snapshot about to be decided
 };
 
@@ -163,6 +165,13 @@ struct IsvdParams {
   const double* wXX;
   int32_t ldg, wcol, wn;
   int32_t inline_next;  // window mode: k_step_b also runs the next snapshot's first-half decision
+  int32_t stage_doubles;  // k_decide_b: doubles of shared memory behind its partials for L^{-1} and N (0: none)
+  // Core step when the CAPACITY's work area exceeds shared memory (an uncapped state whose rank
+  // capacity has grown): 1 = the shared-memory kernel, launched with step_smem_doubles of room,
+  // runs if the CURRENT rank's work area fits and otherwise hands over (ctl->slow_step = k_new)
+  // to the global-memory kernel queued behind it (2), which runs only then.  0: no hand-over.
+  int32_t step_try;
+  int32_t step_smem_doubles;
 };
 
 constexpr int kWB = 8;  // window width: snapshots projected by one pass over U
@@ -255,6 +264,7 @@ struct PassArgs {
   const PipeCtl* ctl;
   int32_t kind;
   int32_t pstride;
+  int32_t pld;  // partials are stored output-major: (CTA b, output o) at part[o * pld + b]
   const double* x;
   const double* coef;
   const double* xn;
@@ -330,6 +340,7 @@ __global__ void k_init_ctl(PipeCtl* ctl, const IsvdHdr* h) {
   ctl->resid = 0;
   ctl->adone = 0;
   ctl->a_inline = -1;
+  ctl->slow_step = 0;
 }
 
 constexpr double kFoldTau = 1e-3;  // append r1 only if its out-of-span part is >= tau |r1|
@@ -680,8 +691,11 @@ __device__ inline void decide_a_body(const StateView& src, const Pipe& pp, const
   if (!resid && reorth == 0 && P.has_next) prep_next(P, pp, part);
 }
 
+// `stage` (or null): room for L^{-1}'s live block and N in shared memory.  After a pass over U
+// the small state is no longer in L2; the four matrix-vector sweeps below would each pay
+// several memory latencies on it, so both are fetched once with every load in flight.
 __device__ inline void decide_b_body(const StateView& src, const Pipe& pp, const IsvdParams& P, double* part,
-                                     double* red) {
+                                     double* red, double* stage = nullptr, size_t stage_doubles = 0) {
   if (!*(volatile const int32_t*)&pp.ctl->resid) return;
   const IsvdHdr h = *src.hdr;
   IsvdStep* st = pp.step[P.parity];
@@ -692,6 +706,19 @@ __device__ inline void decide_b_body(const StateView& src, const Pipe& pp, const
   const int ldl = P.ccap;
   double* Lb = P.L + (int64_t)base * (ldl + 1);
   double* Lib = P.Li + (int64_t)base * (ldl + 1);
+  const double* Lir = Lib;  // what the sweeps read
+  int ldlr = ldl;
+  const double* Nr = src.N;
+  int ldnr = src.ldn;
+  if (stage && mode != M_RESTART_ACCEPT && (size_t)c * (c + r) <= stage_doubles) {
+    cta_stage_block(stage, c, Lib, ldl, c, c, true);
+    cta_stage_block(stage + (size_t)c * c, c, src.N, src.ldn, c, r, false);
+    Lir = stage;
+    ldlr = c;
+    Nr = stage + (size_t)c * c;
+    ldnr = c;
+    __syncthreads();
+  }
   const double rho2 = pp.fo.scal[0];
   const double p = st->p;
   int action = 0, dep = 0, cn = c, base_new = base, reorth = 0;
@@ -709,7 +736,7 @@ __device__ inline void decide_b_body(const StateView& src, const Pipe& pp, const
     }
   } else {
     double* t1 = pp.tmp;  // L^{-1} g'[:c]: the next snapshot's coordinates in the current Q_U
-    cta_gemv2_cm<8>(Lib, ldl, c, c, pp.fo.e, nx ? pp.fo.gn : nullptr, pp.l1, nx ? t1 : nullptr, part, true);
+    cta_gemv2_cm<8>(Lir, ldlr, c, c, pp.fo.e, nx ? pp.fo.gn : nullptr, pp.l1, nx ? t1 : nullptr, part, true);
     double s_l1 = 0.0, s_lt = 0.0, s_zero = 0.0;
     for (int j = threadIdx.x; j < c; j += blockDim.x) {
       s_l1 = fma(pp.l1[j], pp.l1[j], s_l1);
@@ -727,8 +754,8 @@ __device__ inline void decide_b_body(const StateView& src, const Pipe& pp, const
       const double tc = nx ? (pp.fo.gn[c] - s_lt) / lam : 0.0;
       if (nx)
         for (int j = threadIdx.x; j < c; j += blockDim.x) pp.h[j] = t1[j] - pp.l1[j] * (tc / lam);
-      cta_gemv_cm<8>(src.N, src.ldn, c, r, ell, -1.0, pp.tvec, pp.y, part, false);  // y = tvec - N ell
-      cta_gemv2_t_cm(Lib, ldl, c, c, pp.l1, nx ? pp.h : pp.l1, pp.w, pp.gt, true);
+      cta_gemv_cm<8>(Nr, ldnr, c, r, ell, -1.0, pp.tvec, pp.y, part, false);  // y = tvec - N ell
+      cta_gemv2_t_cm(Lir, ldlr, c, c, pp.l1, nx ? pp.h : pp.l1, pp.w, pp.gt, true);
       for (int j = threadIdx.x; j < c; j += blockDim.x) {
         Lb[(int64_t)j * ldl + c] = pp.l1[j];
         Lib[(int64_t)j * ldl + c] = -pp.w[j] / lam;
@@ -747,10 +774,10 @@ __device__ inline void decide_b_body(const StateView& src, const Pipe& pp, const
       action = 1;
     } else if (room) {
       reorth = 1;
-      cta_gemv_cm<8>(src.N, src.ldn, c, r, ell, -1.0, pp.tvec, pp.y, part, false);
-      cta_gemv_t_cm(Lib, ldl, c, c, pp.l1, pp.h, true);  // h = L^{-T} l1 = G^{-1} e
+      cta_gemv_cm<8>(Nr, ldnr, c, r, ell, -1.0, pp.tvec, pp.y, part, false);
+      cta_gemv_t_cm(Lir, ldlr, c, c, pp.l1, pp.h, true);  // h = L^{-T} l1 = G^{-1} e
     } else if (c >= r + 1) {
-      cta_gemv_cm<8>(src.N, src.ldn, c, r, ell, -1.0, pp.tvec, pp.y, part, false);
+      cta_gemv_cm<8>(Nr, ldnr, c, r, ell, -1.0, pp.tvec, pp.y, part, false);
       for (int a = threadIdx.x; a < c; a += blockDim.x) nj[a] = (pp.y[a] + pp.l1[a]) / p;
       action = 2;
     } else {
@@ -759,7 +786,7 @@ __device__ inline void decide_b_body(const StateView& src, const Pipe& pp, const
     if ((dep || action == 2) && nx) {  // U unchanged: tvec' = t1, gt' = L^{-T} t1
       __syncthreads();
       for (int j = threadIdx.x; j < c; j += blockDim.x) pp.tvec[j] = t1[j];
-      cta_gemv_t_cm(Lib, ldl, c, c, t1, pp.gt, true);
+      cta_gemv_t_cm(Lir, ldlr, c, c, t1, pp.gt, true);
       prepped = true;
     }
     __syncthreads();
@@ -809,7 +836,8 @@ __global__ void __launch_bounds__(kDecideThreads) k_decide_b(StateView src, Pipe
   __shared__ double red[96];
   pdl_enter();
   trace_stamp(P.trace, 4);
-  decide_b_body(src, pp, P, part, red);
+  const size_t npart = (size_t)2 * (kDecideThreads / 32) * ((P.ccap + 31) / 32 * 32);
+  decide_b_body(src, pp, P, part, red, P.stage_doubles > 0 ? part + npart : nullptr, (size_t)P.stage_doubles);
   trace_stamp(P.trace, 5);
 }
 
@@ -886,6 +914,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(PassArgs a, int nstage
   if (wid == 0) {
     // ---------------- producer ----------------
     if (lane == 0 && cs > 0) {
+      const uint64_t pol_stream = l2_policy_evict_first();  // U is read once per pass (bulk.cuh)
       for (int64_t i = 0; i < nt; ++i) {
         const int st = (int)(i % nstages);
         const int64_t use = i / nstages;
@@ -896,7 +925,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(PassArgs a, int nstage
         mbar_expect_tx(&full[st], bu + (x_own ? bv : 0u) + (xn_stage ? bv : 0u) + bv * (unsigned)nxw_st);
         double* dst = stg + (size_t)st * stage_elems;
         // the live column segments of U tile t0 + i are one contiguous run
-        if (bu) bulk_g2s(dst, a.U + (t0 + i) * tstride + (int64_t)base * kUTile, bu, &full[st]);
+        if (bu) bulk_g2s_stream(dst, a.U + (t0 + i) * tstride + (int64_t)base * kUTile, bu, &full[st], pol_stream);
         if (x_own && bv) bulk_g2s(dst + x_col * kStageRows, x + row0, bv, &full[st]);
         if (xn_stage && bv) bulk_g2s(dst + xn_col * kStageRows, a.xn + row0, bv, &full[st]);
         if (bv)
@@ -1005,17 +1034,20 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(PassArgs a, int nstage
     }
     // per-CTA partials: [0, PG) e | [PG, 2 PG) gn | 2 PG + {0: r.r, 1: xn.xn, 2: r.xn}
     const int PG = (a.pstride - 16) / 2;  // [e | gn | r.r, xn.xn, r.xn, r.x_w (kWB - 1)]
-    double* mypart = a.part + (int64_t)blockIdx.x * a.pstride;
+    // output-major: the last CTA's sum over the CTAs then reads contiguous runs (8 sectors
+    // per 32 CTAs instead of 32: that reduction is one SM's L2 bandwidth)
+    double* mypart = a.part + blockIdx.x;
+    const int64_t pl = a.pld;
 #pragma unroll
     for (int q = 0; q < MAXJ; ++q) {
       const int j = cw + kPassConsumers * q;
       if (do_e) {
         const double v = warp_sum(ae[q]);
-        if (lane == 0 && j < c) mypart[j] = v;
+        if (lane == 0 && j < c) mypart[j * pl] = v;
       }
       if (do_gn) {
         const double v = warp_sum(ag[q]);
-        if (lane == 0 && j < c) mypart[PG + j] = v;
+        if (lane == 0 && j < c) mypart[(PG + j) * pl] = v;
       }
     }
     if (cw == kPassConsumers - 1) {
@@ -1023,14 +1055,14 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(PassArgs a, int nstage
       gs = warp_sum(gs);
       xq = warp_sum(xq);
       if (lane == 0) {
-        mypart[2 * PG] = rr;
-        mypart[2 * PG + 1] = xq;
-        mypart[2 * PG + 2] = gs;
+        mypart[(2 * PG) * pl] = rr;
+        mypart[(2 * PG + 1) * pl] = xq;
+        mypart[(2 * PG + 2) * pl] = gs;
       }
     }
     if (xwc) {
       gwa = warp_sum(gwa);
-      if (lane == 0) mypart[2 * PG + 3 + cw] = gwa;
+      if (lane == 0) mypart[(2 * PG + 3 + cw) * pl] = gwa;
     }
   }
   if (!last_cta_arrives(a.counter, &s_last)) return;
@@ -1055,15 +1087,32 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(PassArgs a, int nstage
       const int o = o0 + q * nwarps;
       s[q][0] = s[q][1] = s[q][2] = s[q][3] = 0.0;
       if (o >= nout) continue;
-      const int col = out_col(o);
-      int b = lane;
-      for (; b + 96 < (int)gridDim.x; b += 128) {
-        s[q][0] += a.part[(int64_t)b * a.pstride + col];
-        s[q][1] += a.part[(int64_t)(b + 32) * a.pstride + col];
-        s[q][2] += a.part[(int64_t)(b + 64) * a.pstride + col];
-        s[q][3] += a.part[(int64_t)(b + 96) * a.pstride + col];
+      const double* pc = a.part + (int64_t)out_col(o) * a.pld;
+      const int G = (int)gridDim.x;
+      if (G <= 160) {
+        // every load of the four outputs in flight at once (the loops below stall on
+        // memory once per trip: ~25k cycles for ~100 outputs); the same summation order
+        double v[5];
+#pragma unroll
+        for (int k = 0; k < 5; ++k) v[k] = (lane + 32 * k < G) ? __ldcg(pc + lane + 32 * k) : 0.0;
+        if (lane + 96 < G) {
+          s[q][0] = v[0]; s[q][1] = v[1]; s[q][2] = v[2]; s[q][3] = v[3];
+          if (lane + 128 < G) s[q][0] += v[4];
+        } else {
+#pragma unroll
+          for (int k = 0; k < 5; ++k)
+            if (lane + 32 * k < G) s[q][0] += v[k];
+        }
+        continue;
       }
-      for (; b < (int)gridDim.x; b += 32) s[q][0] += a.part[(int64_t)b * a.pstride + col];
+      int b = lane;
+      for (; b + 96 < G; b += 128) {
+        s[q][0] += __ldcg(pc + b);
+        s[q][1] += __ldcg(pc + b + 32);
+        s[q][2] += __ldcg(pc + b + 64);
+        s[q][3] += __ldcg(pc + b + 96);
+      }
+      for (; b < G; b += 32) s[q][0] += __ldcg(pc + b);
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -1080,6 +1129,11 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(PassArgs a, int nstage
         }
       }
     }
+  }
+  if (a.trace && threadIdx.x == 0 && a.kind != PASS_SECOND) {  // the reduction's end
+    unsigned long long tt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+    a.trace[13] = (long long)tt;
   }
   if (a.tail) {
     __syncthreads();  // this CTA's outputs are complete
@@ -1193,25 +1247,7 @@ __device__ inline void step_b_body(const StateView& src, const StateView& dst, c
   }
   // stage N (c x r) into N_b now: the L2 loads overlap the solver's set-up; the appended
   // row and the n_j column follow once the decision chain is known (below)
-  // (a warp per column, 4 x 4 loads per thread in flight: one L2 latency per 64 x 128 block)
-  for (int b0 = 0; b0 < r; b0 += 4 * nw)
-    for (int a0 = 0; a0 < c; a0 += 128) {
-      double v[4][4];
-#pragma unroll
-      for (int q1 = 0; q1 < 4; ++q1)
-#pragma unroll
-        for (int q2 = 0; q2 < 4; ++q2) {
-          const int b = b0 + wid + nw * q1, a = a0 + lane + 32 * q2;
-          v[q1][q2] = (b < r && a < c) ? __ldcg(src.N + (int64_t)b * src.ldn + a) : 0.0;
-        }
-#pragma unroll
-      for (int q1 = 0; q1 < 4; ++q1)
-#pragma unroll
-        for (int q2 = 0; q2 < 4; ++q2) {
-          const int b = b0 + wid + nw * q1, a = a0 + lane + 32 * q2;
-          if (b < r && a < c) WB[b * P.ccap + a] = v[q1][q2];
-        }
-    }
+  cta_stage_block(WB, P.ccap, src.N, src.ldn, c, r, false);
   // ---- 2. the bordered core and its SVD (rank-one secular solver) ----------
   for (int attempt = 0; attempt < 2; ++attempt) {  // (one inlined copy of the solver)
     core_svd_secular(src.sigma, ell, dep ? 0.0 : p, r, cw, Wt, Vt, svs, WS, pp.vbar, red,
@@ -1389,6 +1425,19 @@ template <bool kSmem>
 __global__ void __launch_bounds__(kSmallThreads) k_step_b(StateView src, StateView dst, Pipe pp, IsvdParams P) {
   extern __shared__ double smem[];
   __shared__ double red[32];
+  if (P.step_try) {
+    if (P.wn > 0) wait_counter(&pp.ctl->adone, P.d_expect);
+    else wait_counter(&pp.ctl->decided, P.d_expect);
+    if (kSmem) {
+      const int64_t mm = src.hdr->r + 1;
+      if (3 * mm * mm + 16 * (int64_t)P.work_stride + (int64_t)P.ccap * mm > (int64_t)P.step_smem_doubles) {
+        if (threadIdx.x == 0) pp.ctl->slow_step = (int32_t)P.k_new;
+        return;  // the global-memory kernel behind this one takes the update
+      }
+    } else if (*(volatile const int32_t*)&pp.ctl->slow_step != (int32_t)P.k_new) {
+      return;  // the shared-memory kernel did it
+    }
+  }
   if (P.wn > 0) {  // window mode: the SVD needs only k_decide_a; the rest waits mid-way
     wait_counter(&pp.ctl->adone, P.d_expect);
     trace_stamp(P.trace, 8);

@@ -78,6 +78,7 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wproj(WprojArgs a, int nstages
   if (wid == 0) {
     // ---------------- producer: lane 0 issues one U copy and the x copies per stage
     if (lane == 0) {
+      const uint64_t pol_stream = l2_policy_evict_first();  // U is read once per pass (bulk.cuh)
       for (int64_t i = 0; i < nt; ++i) {
         const int st = (int)(i % nstages);
         const int64_t use = i / nstages;
@@ -88,7 +89,7 @@ __global__ void __launch_bounds__(kWThreads, 1) k_wproj(WprojArgs a, int nstages
         const unsigned xb = a.xbulk ? (unsigned)valid * 8u : 0u;
         mbar_expect_tx(&full[st], ub + xb * (unsigned)a.nw);
         double* dst = wst + (size_t)st * stage_elems;
-        if (ub) bulk_g2s(dst, a.U + (t0 + i) * tstride + (int64_t)base * kUTile, ub, &full[st]);
+        if (ub) bulk_g2s_stream(dst, a.U + (t0 + i) * tstride + (int64_t)base * kUTile, ub, &full[st], pol_stream);
         if (xb)
           for (int j = 0; j < a.nw; ++j) bulk_g2s(dst + xoff + (size_t)j * kWXLd, a.xs[j] + row0, xb, &full[st]);
       }

@@ -611,6 +611,33 @@ __device__ inline void cta_gemv2_t_cm(const double* A, int ld, int rows, int col
   __syncthreads();
 }
 
+// Copy a rows x cols column-major block (lower: only i >= j) from global memory into the
+// work area: a warp per column, 4 x 4 loads per thread in flight, so a block of up to
+// 64 columns x 128 rows costs one memory latency instead of one per element row.  The
+// small state is usually cold (every pass over U sweeps L2).  No synchronisation.
+__device__ inline void cta_stage_block(double* dst, int ldd, const double* src, int64_t lds, int rows, int cols,
+                                       bool lower) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int b0 = 0; b0 < cols; b0 += 4 * nw)
+    for (int a0 = 0; a0 < rows; a0 += 128) {
+      double v[4][4];
+#pragma unroll
+      for (int q1 = 0; q1 < 4; ++q1)
+#pragma unroll
+        for (int q2 = 0; q2 < 4; ++q2) {
+          const int b = b0 + wid + nw * q1, a = a0 + lane + 32 * q2;
+          v[q1][q2] = (b < cols && a < rows && (!lower || a >= b)) ? __ldcg(src + (int64_t)b * lds + a) : 0.0;
+        }
+#pragma unroll
+      for (int q1 = 0; q1 < 4; ++q1)
+#pragma unroll
+        for (int q2 = 0; q2 < 4; ++q2) {
+          const int b = b0 + wid + nw * q1, a = a0 + lane + 32 * q2;
+          if (b < cols && a < rows) dst[b * ldd + a] = v[q1][q2];
+        }
+    }
+}
+
 // Three block-wide sums at once (fixed tree, deterministic); `red` >= 3 * 32 doubles.
 __device__ inline void block_sum3(double& a, double& b, double& c, double* red) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;

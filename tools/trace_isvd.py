@@ -38,7 +38,7 @@ print(f'{args.cols} updates in {e0.elapsed_time(e1):.2f} ms = {e0.elapsed_time(e
 T = buf.cpu().numpy().reshape(args.cols, 16).astype(np.float64)
 T[T == 0] = np.nan
 names = ['A start', 'A end', 'resid start', 'resid end', 'B start', 'B end', 'second start', 'decide2 end',
-         'stepb start', 'stepb svd done', 'stepb mid ok', 'stepb end', 'vupd start', '-', 'wproj start',
+         'stepb start', 'stepb svd done', 'stepb mid ok', 'stepb end', 'vupd start', 'resid reduced', 'wproj start',
          'prep_w end']
 rel = (T - T[:, [0]]) / 1e3
 print('phase (us from A start): median [p10, p90]   (n)')
