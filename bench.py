@@ -365,13 +365,17 @@ def bench_isvd_seeds(args, ctx):
                             TOL, tol_sv=TOL, r_max=RANK, cap_mode="truncate")
         del q, r, w, vt
         cols = xt[WARM_COLS:].T
-        ms, last, _, _ = time_ingest(st, cols, max(2, args.steps // 2), 2)
+        # three steps timed one by one, median: a step is ~60 ms of mostly one-CTA latency work
+        # and the box's host or clock hiccups show up as single slow steps (DESIGN 3a)
+        step_ms = []
+        for rep in range(3):
+            ms, last, _, _ = time_ingest(st, cols, 1, 2 if rep == 0 else 0)
+            step_ms.append(ms)
         pl, _, _ = _prof_read(_capi.lib, _capi)
-        rate = (COLS - WARM_COLS) * max(2, args.steps // 2) / (ms / 1e3)
-        # compactions of ONE step: the profile counters cover all timed steps
-        c = counts_of(last, pl)
-        c["compactions"] = c["compactions"] // max(2, args.steps // 2)
-        out.append(dict(seed=f"torch {seed}", snapshots_per_s=rate, **c))
+        rate = (COLS - WARM_COLS) / (statistics.median(step_ms) / 1e3)
+        c = counts_of(last, pl)  # the profile counters cover the last timed step
+        out.append(dict(seed=f"torch {seed}", snapshots_per_s=rate,
+                        step_ms=[round(v, 2) for v in step_ms], **c))
         del xt, cols, st, last
         torch.cuda.empty_cache()
     rates = [o["snapshots_per_s"] for o in out]

@@ -915,6 +915,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(PassArgs a, int nstage
     // ---------------- producer ----------------
     if (lane == 0 && cs > 0) {
       const uint64_t pol_stream = l2_policy_evict_first();  // U is read once per pass (bulk.cuh)
+      const bool x_stream = a.n >= ((int64_t)8 << 20);
       for (int64_t i = 0; i < nt; ++i) {
         const int st = (int)(i % nstages);
         const int64_t use = i / nstages;
@@ -926,10 +927,20 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(PassArgs a, int nstage
         double* dst = stg + (size_t)st * stage_elems;
         // the live column segments of U tile t0 + i are one contiguous run
         if (bu) bulk_g2s_stream(dst, a.U + (t0 + i) * tstride + (int64_t)base * kUTile, bu, &full[st], pol_stream);
-        if (x_own && bv) bulk_g2s(dst + x_col * kStageRows, x + row0, bv, &full[st]);
-        if (xn_stage && bv) bulk_g2s(dst + xn_col * kStageRows, a.xn + row0, bv, &full[st]);
-        if (bv)
-          for (int j = 0; j < nxw_st; ++j) bulk_g2s(dst + (xw_col + j) * kStageRows, a.xw[j] + row0, bv, &full[st]);
+        // snapshot columns: a window's columns are re-read from L2 by its passes while they fit
+        // there (8 x 8 MB at n = 2^20); columns of 64 MB and more stream like U
+        if (x_stream) {
+          if (x_own && bv) bulk_g2s_stream(dst + x_col * kStageRows, x + row0, bv, &full[st], pol_stream);
+          if (xn_stage && bv) bulk_g2s_stream(dst + xn_col * kStageRows, a.xn + row0, bv, &full[st], pol_stream);
+          if (bv)
+            for (int j = 0; j < nxw_st; ++j)
+              bulk_g2s_stream(dst + (xw_col + j) * kStageRows, a.xw[j] + row0, bv, &full[st], pol_stream);
+        } else {
+          if (x_own && bv) bulk_g2s(dst + x_col * kStageRows, x + row0, bv, &full[st]);
+          if (xn_stage && bv) bulk_g2s(dst + xn_col * kStageRows, a.xn + row0, bv, &full[st]);
+          if (bv)
+            for (int j = 0; j < nxw_st; ++j) bulk_g2s(dst + (xw_col + j) * kStageRows, a.xw[j] + row0, bv, &full[st]);
+        }
       }
     }
   } else {
@@ -1016,7 +1027,7 @@ __global__ void __launch_bounds__(kPassThreads, 1) k_pass(PassArgs a, int nstage
         if (do_r && xwc) gwa = fma(r.y, wv.y, fma(r.x, wv.x, gwa));  // r . x_j on the stored (rounded) r
         if (do_r) {
           if (cw == kPassConsumers - 1) {
-            reinterpret_cast<double2*>(scol)[lane] = r;
+            __stcs(reinterpret_cast<double2*>(scol) + lane, r);  // streaming: written once, read by the next pass
             rr = fma(r.y, r.y, fma(r.x, r.x, rr));
             gs = fma(r.y, xnv.y, fma(r.x, xnv.x, gs));
           }
