@@ -16,6 +16,7 @@ ap.add_argument('--log2n', type=int, default=26)
 ap.add_argument('--cols', type=int, default=160)
 ap.add_argument('--timed-from', type=int, default=100)
 ap.add_argument('--rank', type=int, default=100)
+ap.add_argument('--call-cols', type=int, default=8, help='columns per timed ingest call')
 args = ap.parse_args()
 n, B = 1 << args.log2n, 8
 dev = torch.device('cuda')
@@ -30,7 +31,14 @@ while t < args.cols:
     nb = min(B, args.cols - t)
     if st is not None:
         nb = 1 << int(math.floor(math.log2(nb)))
-    x = stream.batch(t, nb, out=buf[:nb])
+    if t >= args.timed_from and args.call_cols > B:
+        nb = min(args.call_cols, args.cols - t)
+        big = torch.empty((nb, n), dtype=torch.float64, device=dev)
+        for j0 in range(0, nb, B):
+            stream.batch(t + j0, min(B, nb - j0), out=big[j0:j0 + min(B, nb - j0)])
+        x = big.T
+    else:
+        x = stream.batch(t, nb, out=buf[:nb])
     if t >= args.timed_from and not getattr(lib, '_on', False):
         torch.cuda.synchronize()
         lib.strom_profile_reset()
