@@ -322,3 +322,54 @@ class TestCfg1FreeRunning:
         assert np.all(err_dev[lead] <= err_ref[lead] + np.maximum(10 * env[lead], 1e-10) + 1e-12)
         # leading-5 subspace: reference envelope 3.7e-8
         assert principal_sine(npy(st.phi)[:, :5], g["phi10"][:, :5]) <= 3.7e-7
+
+
+class TestUncappedRankGrowth:
+    """An uncapped stream whose rank grows past 64: the rank capacity is re-allocated
+    (64 -> 128), the core step's work area for the CAPACITY no longer fits shared memory,
+    and the step runs in the shared-memory kernel while the CURRENT rank's layout fits
+    and hands over on the device to the global-memory kernel beyond (IsvdParams::step_try);
+    past 68 non-deflated poles the secular solver also leaves its register-cached form.
+    Reference: basis.py:105-194 with r_max=None."""
+
+    @pytest.mark.parametrize("mode", ["ingest", "updates"])
+    def test_rank_80_stream_vs_oracle_and_batch(self, cuda, mode):
+        n, cols, rank = 4096, 150, 80
+        x, _, _, _ = wl.cfg2_stream_numpy(n=n, cols=cols, rank=rank, seed=5, decades_per=12.0)
+        x = np.ascontiguousarray(x)
+        tol = 1e-9  # sigma_79 = 2.6e-7 above it; modes beyond the 80 signal ones are accumulated noise
+        xd = torch.as_tensor(x, device="cuda")
+        st = basis.isvd_init(xd[:, 0].contiguous(), tol, tol_sv=tol)
+        if mode == "ingest":
+            st = basis.ingest_simulation(st, xd[:, 1:])
+        else:
+            st = basis.ingest_simulation(st, xd[:, 1:60])
+            for j in range(60, cols):  # one functional update per call across the growth
+                st = basis.isvd_update(st, xd[:, j].contiguous())
+        ref = so.stream(x, tol, tol_sv=tol)
+        assert rank <= st.rank <= rank + 16 and ref.rank >= rank, (st.rank, ref.rank)
+        s = npy(st.sigma)
+        sb = np.linalg.svd(x, compute_uv=False)
+        m = 60  # sigma_60 = 1e-5 sigma_0
+        # leading modes to relative rounding; the rest on sigma_0's scale (the accuracy an SVD
+        # update can carry through 150 steps), against the oracle and against the batch SVD
+        assert np.max(np.abs(s[:16] - ref.sigma[:16]) / ref.sigma[:16]) <= 1e-10
+        assert np.max(np.abs(s[:16] - sb[:16]) / sb[:16]) <= 1e-10
+        assert np.max(np.abs(s[:m] - ref.sigma[:m])) <= 1e-11 * sb[0]
+        assert np.max(np.abs(s[:m] - sb[:m])) <= 1e-11 * sb[0]
+        print(f"rank {st.rank} (oracle {ref.rank}); sigma abs err / sigma_0 vs oracle "
+              f"{np.max(np.abs(s[:m] - ref.sigma[:m])) / sb[0]:.2e}, vs batch {np.max(np.abs(s[:m] - sb[:m])) / sb[0]:.2e}; "
+              f"oracle vs batch {np.max(np.abs(ref.sigma[:m] - sb[:m])) / sb[0]:.2e}")
+        phi = npy(st.phi)
+        ub = np.linalg.svd(x, full_matrices=False)[0]
+        # subspaces against the batch SVD: every dependent update drops a residual of norm up
+        # to tol (basis.py:139), which turns the leading-q subspace by up to tol / gap_q; both
+        # streams must sit inside that envelope of the batch basis and of each other
+        for q in (16, 40):
+            bound = tol / (sb[q - 1] - sb[q])
+            sd, sr = principal_sine(phi[:, :q], ub[:, :q]), principal_sine(ref.phi[:, :q], ub[:, :q])
+            sx = principal_sine(phi[:, :q], ref.phi[:, :q])
+            print(f"leading {q}: device vs batch {sd:.2e}, oracle vs batch {sr:.2e}, device vs oracle {sx:.2e}, "
+                  f"tol / gap {bound:.2e}")
+            assert sd <= bound and sr <= bound and sx <= bound
+        assert np.max(np.abs(phi[:, :m].T @ phi[:, :m] - np.eye(m))) <= 1e-8
