@@ -166,11 +166,46 @@ long long* g_cur_trace = nullptr;  // the row of the update being launched (wind
 // by physical column.  `claimed` bounds the physical columns any live state
 // may have written: a successor that would append past a state whose c_ub is
 // below `claimed` copies the store first (copy-on-write).
+// A large store's U block outlives its Store in a one-slot spare cache (per device): a
+// compaction ping-pongs between two blocks of the same size, and a fresh 75 GB allocation
+// costs the driver ~0.4 s (cfg5) even from the stream-ordered pool's point of view when the
+// pool cannot hand the freed block back.  Reuse is on the stream that allocated the block
+// (stream order covers the last owner's kernels); anything else takes the allocator.
+constexpr size_t kSpareStoreMin = (size_t)1 << 30;
+struct SpareStore {
+  std::mutex mu;
+  DevMemPtr mem[kMaxDevices];
+  int live[kMaxDevices] = {};  // stores alive per device: the spare goes when the last one does
+};
+SpareStore& spare_store() {
+  static SpareStore s;
+  return s;
+}
+
 struct Store {
   DevMemPtr umem, lmem;
   int64_t ldu = 0;
   int32_t ccap = 0;
   int32_t claimed = 0;
+  int dev = 0;
+  Store() {
+    dev = current_device_id();
+    SpareStore& sp = spare_store();
+    std::lock_guard<std::mutex> g(sp.mu);
+    ++sp.live[dev];
+  }
+  Store(const Store&) = delete;
+  Store& operator=(const Store&) = delete;
+  ~Store() {
+    SpareStore& sp = spare_store();
+    std::lock_guard<std::mutex> g(sp.mu);
+    DevMemPtr& slot = sp.mem[dev];
+    if (--sp.live[dev] <= 0) {
+      slot.reset();  // nothing left to compact: hold no memory
+    } else if (umem && umem->bytes >= kSpareStoreMin && umem.use_count() == 1) {
+      if (!slot || slot->bytes < umem->bytes) slot = std::move(umem);  // the smaller one goes back to the pool
+    }
+  }
   double* U() const { return umem->as<double>(); }
   double* L() const { return lmem->as<double>(); }
   double* Li() const { return L() + (size_t)ccap * ccap; }
@@ -350,7 +385,15 @@ int64_t mem_rows(const strom_isvd* h) {
 
 std::shared_ptr<Store> alloc_store(int64_t n, int64_t ldu, int32_t ccap, cudaStream_t s) {
   auto st = std::make_shared<Store>();
-  st->umem = dev_alloc((size_t)ldu * ccap * 8, s, false);
+  const size_t ubytes = (size_t)ldu * ccap * 8;
+  if (ubytes >= kSpareStoreMin) {
+    SpareStore& sp = spare_store();
+    std::lock_guard<std::mutex> g(sp.mu);
+    DevMemPtr& slot = sp.mem[current_device_id()];
+    if (slot && slot->bytes == ubytes && slot->stream == s) st->umem = std::move(slot);
+    else slot.reset();  // another shape or stream: do not sit on the memory
+  }
+  if (!st->umem) st->umem = dev_alloc(ubytes, s, false);
   // tiles holding padding rows (>= n) are read by the passes: keep them zero (never NaN)
   const int64_t first_pad_tile = n / kUTile;
   const int64_t ntile = ldu / kUTile;
@@ -887,18 +930,31 @@ void gram_finish(const double* part, int nparts, int QP, const int32_t* q_dev, i
   STROM_LAUNCH_CHECK();
 }
 
+// Shared memory of the fused compaction sweep handling `tr` rows of a tile per step.
+size_t compact_pass_smem(int cmax, int rmax, int tr) {
+  const int c4 = (cmax + 3) & ~3, RP = (rmax + 31) & ~31;
+  return ((size_t)c4 * (RP + 4) + (size_t)c4 * (tr + 4) + (size_t)RP * (tr + 4)) * 8;
+}
+// 64 (whole tiles), 32 (half tiles) or 0 (does not fit: the unfused GEMM + Gram)
+int compact_pass_rows(int cmax, int rmax) {
+  if (rmax > 128) return 0;
+  for (int tr : {64, 32})
+    if (compact_pass_smem(cmax, rmax, tr) <= max_smem_optin()) return tr;
+  return 0;
+}
+
 template <int GB>
 void launch_compact_pass(const Store& src, const int32_t* base_dev, const int32_t* c_dev, const int32_t* r_dev,
                          const double* T, int64_t ldt, int cmax, int rmax, const Store& dst, double* part, int QP,
                          cudaStream_t s) {
-  const int c4 = (cmax + 3) & ~3, RP = (rmax + 31) & ~31;
-  const size_t smem = ((size_t)c4 * (RP + 4) + (size_t)c4 * (kUTile + 4) + (size_t)RP * (kUTile + 4)) * 8;
+  const int tr = compact_pass_rows(cmax, rmax);
+  const size_t smem = compact_pass_smem(cmax, rmax, tr);
   static PerDevice<size_t> cfg;
   set_smem_attr(k_compact_pass<GB>, smem, &cfg.get());
   ProfScope ps(P_TALL_GEMM, s);
   k_compact_pass<GB><<<sm_count(), kCompactThreads, smem, s>>>(src.U(), src.ccap, base_dev, c_dev, r_dev, T, ldt,
                                                                dst.U(), dst.ccap, src.ldu / kUTile, part, QP,
-                                                               prof_dev_bytes());
+                                                               prof_dev_bytes(), tr);
   STROM_LAUNCH_CHECK();
 }
 
@@ -949,10 +1005,7 @@ strom_isvd* compact(strom_isvd* src, const Caps& caps, cudaStream_t s) {
   P.ccap = kc.ccap;
   launch_compact_prep(src->view, t->view, m, P, kc, s);
   // p = source c (step->m), q = r (step->mkeep); source columns start at base
-  const size_t fused_smem = ((size_t)((src->caps.ccap + 3) & ~3) * (round_up(kc.rcap, 32) + 4) +
-                             (size_t)((src->caps.ccap + 3) & ~3) * (kUTile + 4) +
-                             (size_t)round_up(kc.rcap, 32) * (kUTile + 4)) * 8;
-  if (kc.rcap <= 128 && fused_smem <= max_smem_optin()) {
+  if (compact_pass_rows(src->caps.ccap, kc.rcap) > 0) {
     // one fused DMMA sweep: U_new = U T and the measured Gram of the stored U_new
     const int RP = (int)round_up(kc.rcap, 32);
     auto part = dev_alloc((size_t)sm_count() * RP * RP * 8, s, false);

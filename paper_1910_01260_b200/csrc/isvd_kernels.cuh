@@ -1647,6 +1647,9 @@ __global__ void __launch_bounds__(256) k_w_to_n(StateView v, double* tmp) {
 // persistent blocks of G.  Per-CTA Gram partials (QP x QP) go to `part`.
 // ---------------------------------------------------------------------------
 constexpr int kCompactThreads = 256;
+// tr: rows of a store tile handled per step, 64 (the whole tile) or 32 (two half-tiles: the
+// U and U_new staging buffers halve, so T (c x r), the U half-tile and the U_new half-tile
+// fit shared memory up to r = 128, c ~ 140: 225 KB at cfg5's r = 100 instead of 294 KB).
 template <int GB>
 __global__ void __launch_bounds__(kCompactThreads, 1) k_compact_pass(const double* __restrict__ U, int64_t src_ccap,
                                                                      const int32_t* base_dev, const int32_t* c_dev,
@@ -1654,7 +1657,7 @@ __global__ void __launch_bounds__(kCompactThreads, 1) k_compact_pass(const doubl
                                                                      int64_t ldt, double* __restrict__ Unew,
                                                                      int64_t dst_ccap, int64_t ntiles,
                                                                      double* __restrict__ part, int QP,
-                                                                     unsigned long long* prof) {
+                                                                     unsigned long long* prof, int tr) {
   extern __shared__ __align__(16) double csm[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
@@ -1666,7 +1669,7 @@ __global__ void __launch_bounds__(kCompactThreads, 1) k_compact_pass(const doubl
   const int RP = (r + 31) & ~31;  // C / G columns padded to 32-wide blocks
   // leading dimensions = 4 (mod 16) doubles: the 16 lanes of a half-warp that
   // load one DMMA fragment (lane = 4 g + t, address t ld + g) hit 16 distinct banks
-  const int LT = RP + 4, LA = kUTile + 4, LC = kUTile + 4;
+  const int LT = RP + 4, LA = tr + 4, LC = tr + 4;
   double* Ts = csm;                       // c4 x LT, T(k, j) at Ts[k * LT + j]
   double* At = Ts + (size_t)c4 * LT;      // c4 x LA, U(i, k) at At[k * LA + i]
   double* Cs = At + (size_t)c4 * LA;      // RP x LC, C(i, j) at Cs[j * LC + i]
@@ -1674,10 +1677,11 @@ __global__ void __launch_bounds__(kCompactThreads, 1) k_compact_pass(const doubl
     const int k = idx / RP, j = idx % RP;
     Ts[k * LT + j] = (k < c && j < r) ? T[(int64_t)j * ldt + k] : 0.0;
   }
-  for (int idx = threadIdx.x; idx < (c4 - c) * kUTile; idx += blockDim.x)
-    At[(size_t)(c + idx / kUTile) * LA + idx % kUTile] = 0.0;
-  const int nbc = (kUTile / 16) * (RP / 32);     // C blocks per tile
+  for (int idx = threadIdx.x; idx < (c4 - c) * tr; idx += blockDim.x)
+    At[(size_t)(c + idx / tr) * LA + idx % tr] = 0.0;
+  const int nbc = (tr / 16) * (RP / 32);          // C blocks per step
   const int nbg = (RP / 16) * (RP / 32);          // G blocks
+  const int nsub = kUTile / tr, h2 = tr / 2;
   double gacc[GB][2][4][2];
 #pragma unroll
   for (int b = 0; b < GB; ++b)
@@ -1687,19 +1691,22 @@ __global__ void __launch_bounds__(kCompactThreads, 1) k_compact_pass(const doubl
       for (int y = 0; y < 4; ++y) gacc[b][x][y][0] = gacc[b][x][y][1] = 0.0;
   const int64_t per = ceil_div(ntiles, gridDim.x);
   const int64_t tt0 = blockIdx.x * per, tt1 = min(ntiles, tt0 + per);
-  for (int64_t tile = tt0; tile < tt1; ++tile) {
-    __syncthreads();  // previous tile's At / Cs fully consumed
+  for (int64_t step = tt0 * nsub; step < tt1 * nsub; ++step) {
+    const int64_t tile = step / nsub;
+    const int sub = (int)(step - tile * nsub);
+    __syncthreads();  // previous step's At / Cs fully consumed
     {
-      const double2* src = reinterpret_cast<const double2*>(U + tile * kUTile * src_ccap + (int64_t)base * kUTile);
-      for (int idx = threadIdx.x; idx < c * kUTile / 2; idx += blockDim.x) {
-        const int k = idx / (kUTile / 2), i2 = idx % (kUTile / 2);
-        reinterpret_cast<double2*>(At + (size_t)k * LA)[i2] = __ldg(src + idx);
+      const double* src = U + tile * kUTile * src_ccap + (int64_t)base * kUTile + sub * tr;
+      for (int idx = threadIdx.x; idx < c * h2; idx += blockDim.x) {
+        const int k = idx / h2, i2 = idx - k * h2;
+        reinterpret_cast<double2*>(At + (size_t)k * LA)[i2] =
+            __ldg(reinterpret_cast<const double2*>(src + (int64_t)k * kUTile) + i2);
       }
     }
     __syncthreads();
     // C(i, j) = sum_k U(i, k) T(k, j)
     for (int blk = wid; blk < nbc; blk += kCompactThreads / 32) {
-      const int i0 = (blk % (kUTile / 16)) * 16, j0 = (blk / (kUTile / 16)) * 32;
+      const int i0 = (blk % (tr / 16)) * 16, j0 = (blk / (tr / 16)) * 32;
       double acc[2][4][2];
 #pragma unroll
       for (int x = 0; x < 2; ++x)
@@ -1728,10 +1735,11 @@ __global__ void __launch_bounds__(kCompactThreads, 1) k_compact_pass(const doubl
     }
     __syncthreads();
     {  // the r live column segments of the new tile are one contiguous run
-      double2* dst = reinterpret_cast<double2*>(Unew + tile * kUTile * dst_ccap);
-      for (int idx = threadIdx.x; idx < r * kUTile / 2; idx += blockDim.x) {
-        const int j = idx / (kUTile / 2), i2 = idx % (kUTile / 2);
-        dst[idx] = reinterpret_cast<const double2*>(Cs + (size_t)j * LC)[i2];
+      double* dst = Unew + tile * kUTile * dst_ccap + sub * tr;
+      for (int idx = threadIdx.x; idx < r * h2; idx += blockDim.x) {
+        const int j = idx / h2, i2 = idx - j * h2;
+        reinterpret_cast<double2*>(dst + (int64_t)j * kUTile)[i2] =
+            reinterpret_cast<const double2*>(Cs + (size_t)j * LC)[i2];
       }
     }
     // G += C^T C: G(a, b) = sum_i C(i, a) C(i, b)
@@ -1740,7 +1748,7 @@ __global__ void __launch_bounds__(kCompactThreads, 1) k_compact_pass(const doubl
       const int blk = wid + bb * (kCompactThreads / 32);
       if (blk >= nbg) break;
       const int a0 = (blk % (RP / 16)) * 16, b0 = (blk / (RP / 16)) * 32;
-      for (int k0 = 0; k0 < kUTile; k0 += 4) {
+      for (int k0 = 0; k0 < tr; k0 += 4) {
         const int k = k0 + t;
         double av[2], bv[4];
 #pragma unroll

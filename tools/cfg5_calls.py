@@ -1,7 +1,10 @@
 import math, sys, time
 sys.path.insert(0, '.')
 import torch
-from paper_1910_01260_b200 import basis, workloads as wl
+from paper_1910_01260_b200 import _capi, basis, workloads as wl
+KINDS = ['u_pass', 'reorth', 'decide', 'core_step', 'v_update', 'compact_prep', 'compact_sweep', 'spatial', 'st', 'lu', 'window_pass', 'other']
+lib = _capi.lib
+lib.strom_profile_enable(1)
 n, B = 1 << 26, 8
 dev = torch.device('cuda')
 stream = wl.HadamardStream(n, 1000, 100, decades_per=12.0, seed=0)
@@ -13,13 +16,17 @@ while t0 < 280:
     nb = 1 << int(math.floor(math.log2(min(B, 280 - t0))))
     xb = stream.batch(t0, nb, out=buf[:nb])
     torch.cuda.synchronize()
+    lib.strom_profile_reset()
     w0 = time.perf_counter()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     st = basis.ingest_simulation(st, xb)
     e1.record()
     torch.cuda.synchronize()
-    rows.append((t0, nb, e0.elapsed_time(e1), (time.perf_counter() - w0) * 1e3))
+    pl = (_capi.i64 * 16)(); pms = (_capi.dbl * 16)(); pby = (_capi.dbl * 16)()
+    lib.strom_profile_read(16, pl, pms, pby)
+    kinds = ', '.join(f'{KINDS[k]} {pms[k]:.0f}' for k in range(len(KINDS)) if pms[k] >= 5.0 and KINDS[k] != 'core_step')
+    rows.append((t0, nb, e0.elapsed_time(e1), (time.perf_counter() - w0) * 1e3, kinds))
     t0 += nb
 for r in rows[10:]:
-    print(f't0 {r[0]:4d} nb {r[1]} gpu {r[2]:8.1f} ms  wall {r[3]:8.1f} ms  per update {r[2] / r[1]:6.1f}')
+    print(f't0 {r[0]:4d} nb {r[1]} gpu {r[2]:8.1f} ms  wall {r[3]:8.1f} ms  per update {r[2] / r[1]:6.1f}   [{r[4]}]')
