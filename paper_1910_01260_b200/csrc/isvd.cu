@@ -683,6 +683,7 @@ inline int pass_maxj(int cols) {
   if (need <= 8) return 8;
   if (need <= 12) return 12;
   if (need <= 16) return 16;
+  if (need <= 18) return 18;  // c <= 144: cfg5's store (c_cap 139) without the 24-column variant's spills
   if (need <= 24) return 24;
   return 32;
 }
@@ -791,6 +792,7 @@ void launch_pass(int kind, int cols_ub, const strom_isvd* h, const PipeMem& m, c
     case 8: launch_pass_t<8>(a, cu, reserve, pk, s); break;
     case 12: launch_pass_t<12>(a, cu, reserve, pk, s); break;
     case 16: launch_pass_t<16>(a, cu, reserve, pk, s); break;
+    case 18: launch_pass_t<18>(a, cu, reserve, pk, s); break;
     case 24: launch_pass_t<24>(a, cu, reserve, pk, s); break;
     default: launch_pass_t<32>(a, cu, reserve, pk, s); break;
   }
