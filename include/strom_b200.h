@@ -40,6 +40,11 @@ extern "C" {
 const char* strom_last_error(void);
 int strom_abi_version(void);
 int strom_device_synchronize(void);
+/* Give back device memory the library keeps for reuse: the spare store block a compaction
+ * ping-pongs with (kept only for stores of 1 GiB and more, and only while a state is alive).
+ * Call it before a large allocation of your own, e.g. the n x r export of phi at capacity
+ * sizes.  No reference counterpart (device memory management). */
+void strom_trim_cache(void);
 
 /* Built-in profiling (used by bench.py for the live roofline): per kernel kind
  * (0 proj pass, 1 residual pass, 2 step A, 3 step B, 4 V update, 5 compaction,

@@ -41,6 +41,7 @@ _PROTOS = {
     "strom_abi_version": (C.c_int, []),
     "strom_device_synchronize": (C.c_int, []),
     "strom_profile_enable": (None, [i32]),
+    "strom_trim_cache": (None, []),
     "strom_profile_reset": (C.c_int, []),
     "strom_profile_read": (C.c_int, [i32, C.POINTER(i64), C.POINTER(dbl), C.POINTER(dbl)]),
     "strom_profile_durations": (C.c_int, [i32, i32, C.POINTER(C.c_float), C.POINTER(i32)]),

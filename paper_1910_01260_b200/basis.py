@@ -158,18 +158,21 @@ class SvdState:
         """Decision bits (STROM_F_*) of the update that produced this state."""
         return int(self.info().flags)
 
-    def _export(self):
-        if "phi" not in self._cache:
+    def _export(self, want: str):
+        """Materialise one of the reference's arrays on first use.  phi = U W is a tall GEMM
+        and n x r doubles (50 GiB at n = 2^26, r = 100): reading sigma or v must not cost it."""
+        if want not in self._cache:
             r = self.rank
             dev = device()
-            phi = torch.empty((self.n, r), dtype=F64, device=dev)
-            sig = torch.empty((r,), dtype=F64, device=dev)
-            v = torch.empty((self.k, r), dtype=F64, device=dev)
+            shape = {"phi": (self.n, r), "sigma": (r,), "v": (self.k, r)}[want]
+            if want == "phi":
+                capi.lib.strom_trim_cache()  # the spare compaction block must not starve this allocation
+            out = torch.empty(shape, dtype=F64, device=dev)
             if r:
-                capi.call("strom_isvd_export", self._h, phi.data_ptr(), sig.data_ptr(), v.data_ptr(),
-                          capi.stream_ptr())
-            self._cache.update(phi=phi, sigma=sig, v=v)
-        return self._cache
+                ptr = {k: (out.data_ptr() if k == want else None) for k in ("phi", "sigma", "v")}
+                capi.call("strom_isvd_export", self._h, ptr["phi"], ptr["sigma"], ptr["v"], capi.stream_ptr())
+            self._cache[want] = out
+        return self._cache[want]
 
     def factors(self):
         """(U, W, L) of the device representation phi = U W, L = chol(U^T U) (diagnostics)."""
@@ -185,15 +188,15 @@ class SvdState:
 
     @property
     def phi(self) -> torch.Tensor:
-        return self._export()["phi"]
+        return self._export("phi")
 
     @property
     def sigma(self) -> torch.Tensor:
-        return self._export()["sigma"]
+        return self._export("sigma")
 
     @property
     def v(self) -> torch.Tensor:
-        return self._export()["v"]
+        return self._export("v")
 
     def __repr__(self):
         return f"SvdState(n={self.n}, k={self.k}, rank={self.rank})"

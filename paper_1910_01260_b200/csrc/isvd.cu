@@ -1930,6 +1930,12 @@ int strom_isvd_query(strom_isvd* h, void* stream, strom_isvd_info* out) {
   });
 }
 
+void strom_trim_cache(void) {
+  SpareStore& sp = spare_store();
+  std::lock_guard<std::mutex> g(sp.mu);
+  for (auto& m : sp.mem) m.reset();
+}
+
 int strom_isvd_export(strom_isvd* h, double* phi_dev, double* sigma_dev, double* v_dev, void* stream) {
   return guarded([&] {
     STROM_REQUIRE(h, "null argument");
