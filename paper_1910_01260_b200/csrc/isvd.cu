@@ -946,18 +946,30 @@ int compact_pass_rows(int cmax, int rmax) {
 }
 
 template <int GB>
-void launch_compact_pass(const Store& src, const int32_t* base_dev, const int32_t* c_dev, const int32_t* r_dev,
+int launch_compact_pass(const Store& src, const int32_t* base_dev, const int32_t* c_dev, const int32_t* r_dev,
                          const double* T, int64_t ldt, int cmax, int rmax, const Store& dst, double* part, int QP,
                          cudaStream_t s) {
-  const int tr = compact_pass_rows(cmax, rmax);
+  int tr = compact_pass_rows(cmax, rmax);
+  int ctas_per_sm = 1;
+  // STROM_COMPACT_TWO_CTA=1 (small Gram blocks, r <= 64): half tiles let two CTAs share an SM, so
+  // one loads its next tile while the other multiplies.  Off by default: at cfg2 it saves well
+  // under a millisecond per step, and the other split of the Gram partials re-rolls the
+  // noise-level decisions (262 / 220 / 324 dependent updates on the three bench streams
+  // instead of 331 / 226 / 280: no net gain).
+  static const bool two = getenv("STROM_COMPACT_TWO_CTA") != nullptr;
+  if (GB == 1 && two && 2 * (compact_pass_smem(cmax, rmax, 32) + 1024) <= max_smem_optin()) {
+    tr = 32;
+    ctas_per_sm = 2;
+  }
   const size_t smem = compact_pass_smem(cmax, rmax, tr);
   static PerDevice<size_t> cfg;
   set_smem_attr(k_compact_pass<GB>, smem, &cfg.get());
   ProfScope ps(P_TALL_GEMM, s);
-  k_compact_pass<GB><<<sm_count(), kCompactThreads, smem, s>>>(src.U(), src.ccap, base_dev, c_dev, r_dev, T, ldt,
+  k_compact_pass<GB><<<sm_count() * ctas_per_sm, kCompactThreads, smem, s>>>(src.U(), src.ccap, base_dev, c_dev, r_dev, T, ldt,
                                                                dst.U(), dst.ccap, src.ldu / kUTile, part, QP,
                                                                prof_dev_bytes(), tr);
   STROM_LAUNCH_CHECK();
+  return sm_count() * ctas_per_sm;  // per-CTA Gram partials written
 }
 
 // L = chol(A[:, col0:col0+q]^T A[:, col0:col0+q]) with the DMMA tall Gram.
@@ -1010,7 +1022,8 @@ strom_isvd* compact(strom_isvd* src, const Caps& caps, cudaStream_t s) {
   if (compact_pass_rows(src->caps.ccap, kc.rcap) > 0) {
     // one fused DMMA sweep: U_new = U T and the measured Gram of the stored U_new
     const int RP = (int)round_up(kc.rcap, 32);
-    auto part = dev_alloc((size_t)sm_count() * RP * RP * 8, s, false);
+    auto part = dev_alloc((size_t)2 * sm_count() * RP * RP * 8, s, false);  // up to two CTAs per SM
+    int nparts = sm_count();
     const int nbg = (RP / 16) * (RP / 32);
     const int gb = (nbg + 7) / 8;
     const int32_t* bptr = &src->view.hdr->base;
@@ -1018,12 +1031,12 @@ strom_isvd* compact(strom_isvd* src, const Caps& caps, cudaStream_t s) {
     const int32_t* rptr = &m.pp.step[0]->mkeep;
     const int cmax = src->caps.ccap;
     switch (gb) {
-      case 1: launch_compact_pass<1>(*src->store, bptr, cptr, rptr, m.pp.T, P.ccap, cmax, kc.rcap, *t->store, part->as<double>(), RP, s); break;
-      case 2: launch_compact_pass<2>(*src->store, bptr, cptr, rptr, m.pp.T, P.ccap, cmax, kc.rcap, *t->store, part->as<double>(), RP, s); break;
-      case 3: launch_compact_pass<3>(*src->store, bptr, cptr, rptr, m.pp.T, P.ccap, cmax, kc.rcap, *t->store, part->as<double>(), RP, s); break;
-      default: launch_compact_pass<4>(*src->store, bptr, cptr, rptr, m.pp.T, P.ccap, cmax, kc.rcap, *t->store, part->as<double>(), RP, s); break;
+      case 1: nparts = launch_compact_pass<1>(*src->store, bptr, cptr, rptr, m.pp.T, P.ccap, cmax, kc.rcap, *t->store, part->as<double>(), RP, s); break;
+      case 2: nparts = launch_compact_pass<2>(*src->store, bptr, cptr, rptr, m.pp.T, P.ccap, cmax, kc.rcap, *t->store, part->as<double>(), RP, s); break;
+      case 3: nparts = launch_compact_pass<3>(*src->store, bptr, cptr, rptr, m.pp.T, P.ccap, cmax, kc.rcap, *t->store, part->as<double>(), RP, s); break;
+      default: nparts = launch_compact_pass<4>(*src->store, bptr, cptr, rptr, m.pp.T, P.ccap, cmax, kc.rcap, *t->store, part->as<double>(), RP, s); break;
     }
-    gram_finish(part->as<double>(), sm_count(), RP, rptr, 0, t->view.L, t->view.Li, t->view.ldl, t->view.hdr,
+    gram_finish(part->as<double>(), nparts, RP, rptr, 0, t->view.L, t->view.Li, t->view.ldl, t->view.hdr,
                 &m.pp.step[0]->pad0, s, src->shard);
   } else {
     launch_tall_gemm(tall_tiled(src->store->U(), src->store->ccap), &src->view.hdr->base, m.pp.T, P.ccap,
