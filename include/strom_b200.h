@@ -240,6 +240,14 @@ int strom_spatial_reduce_ell(int64_t n, int32_t K, const uint32_t* eidx_dev, con
                              const double* phi_dev, int64_t ld, int64_t ns, const double* extra_dev, int64_t ext_ld,
                              int64_t ne, const double* xref_dev, double* out_dev, void* stream);
 
+/* Y = A X for the CSR operator and a row-major X (n_cols(A) x m, leading dimension ldx);
+ * Y is n x m row-major (ldy).  The sparse applies of the a-posteriori bounds: A x_k for
+ * every step of a trajectory (system.py:249-275) and operator_norm's power iteration on a
+ * sparse operator (bounds.py:60-70).  Rows are summed in CSR order. */
+int strom_csr_spmm(int64_t n, const void* indptr_dev, const void* indices_dev, const double* data_dev,
+                   int32_t index_bits, const double* x_dev, int64_t ldx, int64_t m, double* y_dev, int64_t ldy,
+                   void* stream);
+
 /* Dense LU with partial pivoting kept for repeated solves -- the reference's
  * StepSolver pattern (system.py:106-125: one factor per dt, one solve per
  * step).  a_dev / lu_dev: n x n column-major, factored in place; piv_dev: n

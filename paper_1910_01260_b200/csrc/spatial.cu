@@ -806,6 +806,27 @@ int launch_spatial(SpatialArgs<IdxT> a, int max_grid, cudaStream_t s) {
 
 }  // namespace
 
+// Y = A X for a CSR operator and a row-major right-hand side (X(j, k) at X[j * ldx + k],
+// m columns): one thread per (row, column), a row's entries added in CSR order, so neighbouring
+// threads read neighbouring X entries.  The residual evaluations of the a-posteriori bounds
+// (system.py:249-275: A x_k for every step) and the sparse applies of operator_norm
+// (bounds.py:60-70).
+namespace {
+template <class I>
+__global__ void __launch_bounds__(256) k_csr_spmm(int64_t n, const I* __restrict__ indptr,
+                                                  const I* __restrict__ indices, const double* __restrict__ data,
+                                                  const double* __restrict__ X, int64_t ldx, int64_t m,
+                                                  double* __restrict__ Y, int64_t ldy) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n * m) return;
+  const int64_t row = idx / m, k = idx - row * m;
+  const I p0 = indptr[row], p1 = indptr[row + 1];
+  double acc = 0.0;
+  for (I p = p0; p < p1; ++p) acc = fma(data[p], X[(int64_t)indices[p] * ldx + k], acc);
+  Y[row * ldy + k] = acc;
+}
+}  // namespace
+
 extern "C" {
 
 // build_spatial_rom's contractions (spatial.py:57-64).  A: CSR (indptr N+1,
@@ -965,6 +986,27 @@ int strom_spatial_reduce_ell(int64_t n, int32_t K, const uint32_t* eidx_dev, con
                 h[w * 8 + 1] / (double)grid, h[w * 8 + 2] / (double)grid, h[w * 8 + 3] / (double)grid,
                 h[w * 8 + 4] / (double)grid);
     }
+  });
+}
+
+int strom_csr_spmm(int64_t n, const void* indptr_dev, const void* indices_dev, const double* data_dev,
+                   int32_t index_bits, const double* x_dev, int64_t ldx, int64_t m, double* y_dev, int64_t ldy,
+                   void* stream) {
+  return guarded([&] {
+    STROM_REQUIRE(n >= 1 && m >= 1 && ldx >= m && ldy >= m, "bad spmm shape");
+    STROM_REQUIRE(index_bits == 32 || index_bits == 64, "index_bits must be 32 or 64");
+    STROM_REQUIRE(indptr_dev && x_dev && y_dev, "null argument");  // indices / data may be empty (no entries)
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const unsigned grid = (unsigned)ceil_div(n * m, 256);
+    if (index_bits == 32)
+      k_csr_spmm<int32_t><<<grid, 256, 0, s>>>(n, static_cast<const int32_t*>(indptr_dev),
+                                               static_cast<const int32_t*>(indices_dev), data_dev, x_dev, ldx, m,
+                                               y_dev, ldy);
+    else
+      k_csr_spmm<int64_t><<<grid, 256, 0, s>>>(n, static_cast<const int64_t*>(indptr_dev),
+                                               static_cast<const int64_t*>(indices_dev), data_dev, x_dev, ldx, m,
+                                               y_dev, ldy);
+    STROM_LAUNCH_CHECK();
   });
 }
 

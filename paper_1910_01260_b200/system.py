@@ -334,14 +334,29 @@ def st_inverse_operator(sys: LinearDynamicalSystem, grid: TimeGrid, direct: bool
     return apply, apply_adjoint
 
 
+def csr_apply(csr: dict, x: torch.Tensor) -> torch.Tensor:
+    """A x (x a vector) or A X (X: n_cols x m) for a device CSR dict (indptr, indices, data,
+    index_bits, shape) with the library's SpMM kernel (C ABI ``strom_csr_spmm``)."""
+    from . import _capi as capi
+
+    n, ncol = csr["shape"]
+    vec = x.dim() == 1
+    xm = (x[:, None] if vec else x).to(F64).contiguous()
+    if xm.shape[0] != ncol:
+        raise ValueError(f"operator has {ncol} columns, got {xm.shape[0]} rows")
+    m = xm.shape[1]
+    y = torch.empty((n, m), dtype=F64, device=xm.device)
+    if m:
+        capi.call("strom_csr_spmm", n, csr["indptr"].data_ptr(), csr["indices"].data_ptr(), csr["data"].data_ptr(),
+                  csr["index_bits"], xm.data_ptr(), m, m, y.data_ptr(), m, capi.stream_ptr())
+    return y[:, 0] if vec else y
+
+
 def _spmv(sys: LinearDynamicalSystem, x: torch.Tensor) -> torch.Tensor:
     d = sys.device_arrays()
-    a = d.get("_sparse")
-    if a is None:
-        n = sys.n_states
-        a = d["_sparse"] = torch.sparse_csr_tensor(d["indptr"].to(torch.int64), d["indices"].to(torch.int64),
-                                                   d["data"], size=(n, n))
-    return (a @ x[:, None])[:, 0] if x.dim() == 1 else a @ x
+    n = sys.n_states
+    return csr_apply(dict(indptr=d["indptr"], indices=d["indices"], data=d["data"], index_bits=d["index_bits"],
+                          shape=(n, n)), x)
 
 
 def step_residual(sys: LinearDynamicalSystem, dt: float, x_k, x_prev, f_k) -> torch.Tensor:

@@ -87,3 +87,32 @@ def test_preconditions_and_power_iteration_guards(cuda):
         linalg.largest_singular_value(lambda v: a @ v, lambda v: 2.0 * (a @ v), 4, 4)
     assert linalg.largest_singular_value(lambda v: 0.0 * v, lambda v: 0.0 * v, 4, 4) == 0.0
     assert abs(linalg.largest_singular_value(lambda v: 3.0 * v, lambda v: 3.0 * v, 5, 5) - 3.0) <= 1e-12
+
+
+def test_csr_apply_matches_scipy(cuda):
+    """The library SpMM (C ABI strom_csr_spmm) behind the residual evaluations and
+    operator_norm's sparse applies (reference system.py:249-275, bounds.py:60-70):
+    vector and multi-column right-hand sides, a rectangular operator, empty rows."""
+    import scipy.sparse as sp
+
+    from paper_1910_01260_b200.system import csr_apply
+
+    rng = np.random.default_rng(4)
+    for (n, ncol, m) in ((1, 1, 1), (300, 300, 1), (257, 190, 7), (1000, 1000, 33)):
+        a = sp.random(n, ncol, density=0.05, random_state=int(rng.integers(1 << 30)), format="csr")
+        a.sort_indices()
+        csr = dict(indptr=torch.as_tensor(a.indptr.astype(np.int32), device="cuda"),
+                   indices=torch.as_tensor(a.indices.astype(np.int32), device="cuda"),
+                   data=torch.as_tensor(a.data, device="cuda"), index_bits=32, shape=a.shape)
+        x = rng.standard_normal((ncol, m))
+        ref = a @ x
+        got = csr_apply(csr, torch.as_tensor(x, device="cuda")).cpu().numpy()
+        scale = max(1.0, np.max(np.abs(ref)))
+        assert np.max(np.abs(got - ref)) <= 1e-13 * scale
+        v = csr_apply(csr, torch.as_tensor(x[:, 0].copy(), device="cuda")).cpu().numpy()
+        assert v.shape == (n,) and np.max(np.abs(v - ref[:, 0])) <= 1e-13 * scale
+        csr64 = dict(csr, indptr=csr["indptr"].to(torch.int64), indices=csr["indices"].to(torch.int64), index_bits=64)
+        got64 = csr_apply(csr64, torch.as_tensor(x, device="cuda")).cpu().numpy()
+        np.testing.assert_array_equal(got64, got)
+    with pytest.raises(ValueError):
+        csr_apply(csr, torch.zeros(3, dtype=torch.float64, device="cuda"))
