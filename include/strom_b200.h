@@ -269,6 +269,18 @@ int strom_fom_march(int64_t n, int32_t K, const uint32_t* eidx_dev, const double
                     int64_t m, const double* x0_dev, const double* dt_dev, const double* f_dev, int64_t nt, double tol,
                     int32_t maxit, double* states_dev, int32_t* iters_out, void* stream);
 
+/* The same march for a tridiagonal or periodic tridiagonal A (1-D problems; n <= 4096,
+ * n = 2^k when periodic): a direct solve per step by parallel cyclic reduction in one CTA --
+ * the reference's StepSolver pattern (system.py:106-125: factor once per dt, solve per step),
+ * with the elimination multipliers tabulated per distinct dt.  lo[i] = A(i, i-1), di[i] =
+ * A(i, i), up[i] = A(i, i+1); periodic: lo[0] = A(0, n-1), up[n-1] = A(n-1, 0).  No pivoting:
+ * the caller checks that I - dt A is strictly diagonally dominant.  v_dev non-null (then
+ * b, f, x0 may be null): the block substitution of strom_st_apply_inverse instead. */
+int strom_fom_march_tridiag(int64_t n, const double* lo_dev, const double* di_dev, const double* up_dev,
+                            int32_t periodic, const double* b_dev, int64_t m, const double* x0_dev,
+                            const double* dt_dev, const double* f_dev, const double* v_dev, int64_t nt,
+                            double* states_dev, void* stream);
+
 /* (A_st)^{-1} v by forward block substitution (system.py:195-213): x_k solves
  * (I - dt_k A) x_k = x_{k-1} + v_k with x_0 = 0, by the same cooperative
  * BiCGSTAB march as strom_fom_march; v_dev, out_dev: n x N_t column-major.

@@ -74,6 +74,7 @@ _PROTOS = {
     "strom_dense_lu_solve": (C.c_int, [i64, vp, vp, vp, i64, vp]),
     "strom_st_apply_inverse": (C.c_int, [i64, i32, vp, vp, vp, vp, i64, dbl, i32, vp, P_I32, vp]),
     "strom_fom_march": (C.c_int, [i64, i32, vp, vp, vp, i64, vp, vp, vp, i64, dbl, i32, vp, P_I32, vp]),
+    "strom_fom_march_tridiag": (C.c_int, [i64, vp, vp, vp, i32, vp, i64, vp, vp, vp, vp, i64, vp, vp]),
     "strom_gen_lowrank_batch": (C.c_int, [i64, i32, i32, vp, vp, C.c_uint64, i64, dbl, vp, i64, vp]),
     "strom_csr_to_ell": (C.c_int, [i64, vp, vp, vp, i32, i32, vp, vp, C.POINTER(i64), vp]),
     "strom_csr_spmm": (C.c_int, [i64, vp, vp, vp, i32, vp, i64, i64, vp, i64, vp]),

@@ -276,6 +276,131 @@ __global__ void __launch_bounds__(ONE ? kFomOneThreads : kFomThreads) k_fom_marc
 
 }  // namespace
 
+// ---------------------------------------------------------------------------
+// Direct march for (periodic) tridiagonal operators: 1-D problems (cfg1: periodic
+// advection-diffusion, n = 1024) are latency work for a Krylov solver (33
+// BiCGSTAB iterations of 3.6 us per step) and a trivial direct solve, which is
+// what the reference does (SuperLU factor once per dt, system.py:106-125).
+// Parallel cyclic reduction in ONE CTA: level s combines equation i with
+// equations i -+ 2^s,
+//   alpha = -l_i / d_{i-s},  gamma = -u_i / d_{i+s},
+//   l_i' = alpha l_{i-s},  u_i' = gamma u_{i+s},  d_i' = d_i + alpha u_{i-s} + gamma l_{i+s},
+//   r_i' = r_i + alpha r_{i-s} + gamma r_{i+s},
+// and after ceil(log2 n) levels x_i = r_i / d_i (non-periodic) or
+// r_i / (l_i + d_i + u_i) (periodic, n a power of two: the neighbours are i itself).
+// The multipliers depend on dt only: they are tabulated per distinct dt
+// (levels x n alpha / gamma and the final reciprocal, in global memory and then
+// L1), so a step is the right-hand side's levels: two fused multiply-adds per
+// row and level.  No pivoting: the host checks strict diagonal dominance of
+// I - dt A before taking this path (otherwise the Krylov march runs).
+// ---------------------------------------------------------------------------
+namespace {
+constexpr int kTriThreads = 1024;
+constexpr int kTriMaxN = 4096;
+constexpr int kTriRows = kTriMaxN / kTriThreads;
+
+struct TriArgs {
+  int n, nt, m, periodic, levels;
+  const double* lo;   // A(i, i-1)  (periodic: lo[0] = A(0, n-1))
+  const double* di;   // A(i, i)
+  const double* up;   // A(i, i+1)  (periodic: up[n-1] = A(n-1, 0))
+  const double* b;    // m x n (B column-major)
+  const double* x0;
+  const double* dt;
+  const double* f;    // nt x m row-major, or null
+  const double* v;    // n x nt column-major right-hand-side blocks (st_apply_inverse), or null
+  double* states;     // n x nt column-major
+  double* tab;        // (2 levels + 1) x n: alpha, gamma per level, then the final reciprocal
+};
+
+__global__ void __launch_bounds__(kTriThreads, 1) k_fom_tridiag(TriArgs a) {
+  extern __shared__ double sm[];  // 6 n: l, d, u ping-pong during the set-up; 2 n: r ping-pong afterwards
+  const int n = a.n, L = a.levels;
+  const int tid = threadIdx.x;
+  double* alpha = a.tab;
+  double* gamma = a.tab + (size_t)L * n;
+  double* rinv = a.tab + (size_t)2 * L * n;
+  double dt_tab = -1.0;  // the dt the tables hold
+  auto nb = [&](int i, int s, bool& ok) {  // neighbour index of i at distance s (s may be negative)
+    int j = i + s;
+    if (a.periodic) {
+      ok = true;
+      j %= n;
+      if (j < 0) j += n;
+    } else {
+      ok = j >= 0 && j < n;
+      if (!ok) j = i;
+    }
+    return j;
+  };
+  for (int k = 0; k < a.nt; ++k) {
+    const double h = a.dt[k];
+    if (h != dt_tab) {
+      // ---- tables of M = I - h A
+      double* l0 = sm; double* d0 = sm + n; double* u0 = sm + 2 * n;
+      double* l1 = sm + 3 * n; double* d1 = sm + 4 * n; double* u1 = sm + 5 * n;
+      __syncthreads();
+      for (int i = tid; i < n; i += kTriThreads) {
+        l0[i] = (a.periodic || i > 0) ? -h * a.lo[i] : 0.0;
+        d0[i] = 1.0 - h * a.di[i];
+        u0[i] = (a.periodic || i < n - 1) ? -h * a.up[i] : 0.0;
+      }
+      __syncthreads();
+      for (int lev = 0, s = 1; lev < L; ++lev, s <<= 1) {
+        for (int i = tid; i < n; i += kTriThreads) {
+          bool okm, okp;
+          const int im = nb(i, -s, okm), ip = nb(i, s, okp);
+          const double al = okm ? -l0[i] / d0[im] : 0.0;
+          const double ga = okp ? -u0[i] / d0[ip] : 0.0;
+          alpha[(size_t)lev * n + i] = al;
+          gamma[(size_t)lev * n + i] = ga;
+          l1[i] = okm ? al * l0[im] : 0.0;
+          u1[i] = okp ? ga * u0[ip] : 0.0;
+          d1[i] = d0[i] + (okm ? al * u0[im] : 0.0) + (okp ? ga * l0[ip] : 0.0);
+        }
+        __syncthreads();
+        double* t;
+        t = l0; l0 = l1; l1 = t;
+        t = d0; d0 = d1; d1 = t;
+        t = u0; u0 = u1; u1 = t;
+      }
+      for (int i = tid; i < n; i += kTriThreads)
+        rinv[i] = 1.0 / (a.periodic ? (l0[i] + d0[i] + u0[i]) : d0[i]);
+      __threadfence_block();
+      __syncthreads();
+      dt_tab = h;
+    }
+    // ---- right-hand side: x_{k-1} + h B f_k  (or x_{k-1} + v_k)
+    double* r0 = sm; double* r1 = sm + n;
+    const double* xp = k ? a.states + (size_t)(k - 1) * n : a.x0;
+    for (int i = tid; i < n; i += kTriThreads) {
+      double r = (k || a.x0) ? xp[i] : 0.0;
+      if (a.v) r += a.v[(size_t)k * n + i];
+      if (a.f) {
+        double bf = 0.0;
+        for (int q = 0; q < a.m; ++q) bf = fma(a.b[(size_t)q * n + i], a.f[(size_t)k * a.m + q], bf);
+        r = fma(h, bf, r);
+      }
+      r0[i] = r;
+    }
+    __syncthreads();
+    for (int lev = 0, s = 1; lev < L; ++lev, s <<= 1) {
+      for (int i = tid; i < n; i += kTriThreads) {
+        bool okm, okp;
+        const int im = nb(i, -s, okm), ip = nb(i, s, okp);
+        r1[i] = fma(alpha[(size_t)lev * n + i], r0[im], fma(gamma[(size_t)lev * n + i], r0[ip], r0[i]));
+      }
+      __syncthreads();
+      double* t = r0; r0 = r1; r1 = t;
+    }
+    double* xk = a.states + (size_t)k * n;
+    for (int i = tid; i < n; i += kTriThreads) xk[i] = r0[i] * rinv[i];
+    __threadfence_block();
+    __syncthreads();
+  }
+}
+}  // namespace
+
 extern "C" {
 
 // fom_march (system.py:150-163) on the device: states (n x N_t, column-major)
@@ -295,6 +420,31 @@ int strom_fom_march(int64_t n, int32_t K, const uint32_t* eidx_dev, const double
                     int32_t maxit, double* states_dev, int32_t* iters_out, void* stream) {
   return fom_march_impl(n, K, eidx_dev, eval_dev, b_dev, m, x0_dev, dt_dev, f_dev, nullptr, nt, tol, maxit, states_dev,
                         iters_out, stream);
+}
+
+// fom_march for a tridiagonal or periodic tridiagonal A (diagonals lo, di, up; see k_fom_tridiag).
+// v_dev non-null: the forward block substitution of st_apply_inverse instead (b, f, x0 null).
+int strom_fom_march_tridiag(int64_t n, const double* lo_dev, const double* di_dev, const double* up_dev,
+                            int32_t periodic, const double* b_dev, int64_t m, const double* x0_dev,
+                            const double* dt_dev, const double* f_dev, const double* v_dev, int64_t nt,
+                            double* states_dev, void* stream) {
+  return guarded([&] {
+    STROM_REQUIRE(n >= 2 && n <= kTriMaxN && nt >= 1 && m >= 0, "bad tridiagonal march shape");
+    STROM_REQUIRE(lo_dev && di_dev && up_dev && dt_dev && states_dev, "null argument");
+    STROM_REQUIRE(!periodic || (n & (n - 1)) == 0, "the periodic tridiagonal march needs n = 2^k");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    int levels = 0;
+    while (((int64_t)1 << levels) < n) ++levels;
+    auto tab = dev_alloc((size_t)(2 * levels + 1) * n * 8, s, false);
+    TriArgs a{};
+    a.n = (int)n; a.nt = (int)nt; a.m = (int)m; a.periodic = periodic ? 1 : 0; a.levels = levels;
+    a.lo = lo_dev; a.di = di_dev; a.up = up_dev; a.b = b_dev; a.x0 = x0_dev; a.dt = dt_dev; a.f = f_dev; a.v = v_dev;
+    a.states = states_dev; a.tab = tab->as<double>();
+    const size_t smem = (size_t)6 * n * 8;
+    STROM_CUDA(cudaFuncSetAttribute(k_fom_tridiag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_fom_tridiag<<<1, kTriThreads, smem, s>>>(a);
+    STROM_LAUNCH_CHECK();
+  });
 }
 
 // (A_st)^{-1} v by forward block substitution (system.py:195-213 st_apply_inverse):

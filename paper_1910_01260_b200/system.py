@@ -150,7 +150,49 @@ def _csr_device(a, dev) -> dict:
                   d["data"].data_ptr(), d["index_bits"], kell, eidx.data_ptr(), evals.data_ptr(),
                   capi.C.byref(reach), capi.stream_ptr())
         d["ell"] = dict(k=kell, idx=eidx, val=evals, reach=int(reach.value))
+    tri = _tridiagonal(a)
+    if tri is not None:
+        d["tri"] = dict(lo=torch.as_tensor(tri[0], device=dev), di=torch.as_tensor(tri[1], device=dev),
+                        up=torch.as_tensor(tri[2], device=dev), periodic=tri[3], host=tri[:3])
     return d
+
+
+TRIDIAG_MAX_N = 4096
+
+
+def _tridiagonal(a):
+    """(lo, di, up, periodic) when the square CSR operator is tridiagonal, or tridiagonal with
+    the two periodic corner entries (1-D problems, reference problems.py), else None.
+    lo[i] = A(i, i-1), up[i] = A(i, i+1), wrapping at the ends when periodic."""
+    n = a.shape[0]
+    if a.shape[0] != a.shape[1] or n < 3 or n > TRIDIAG_MAX_N:
+        return None
+    rows = np.repeat(np.arange(n), np.diff(a.indptr))
+    off = (a.indices - rows) % n  # 0 diagonal, 1 super (wrapping), n - 1 sub (wrapping)
+    if not np.all((off == 0) | (off == 1) | (off == n - 1)):
+        return None
+    wraps = ((rows == 0) & (a.indices == n - 1)) | ((rows == n - 1) & (a.indices == 0))
+    periodic = bool(np.any(wraps & (a.data != 0.0)))
+    if periodic and (n & (n - 1)):
+        return None  # the cyclic reduction closes on itself only for n = 2^k
+    lo, di, up = np.zeros(n), np.zeros(n), np.zeros(n)
+    np.add.at(di, rows[off == 0], a.data[off == 0])
+    np.add.at(up, rows[off == 1], a.data[off == 1])
+    np.add.at(lo, rows[off == n - 1], a.data[off == n - 1])
+    return lo, di, up, periodic
+
+
+def _tridiag_ok(dev: dict, grid) -> bool:
+    """The direct tridiagonal march applies: structure found and I - dt A strictly diagonally
+    dominant for every step size (the cyclic reduction does not pivot)."""
+    tri = dev.get("tri")
+    if tri is None:
+        return False
+    lo, di, up = tri["host"]
+    for h in np.unique(np.asarray(grid.dt, dtype=float)):
+        if not np.all(np.abs(1.0 - h * di) > h * (np.abs(lo) + np.abs(up))):
+            return False
+    return True
 
 
 class FomResult(NamedTuple):
@@ -177,24 +219,44 @@ def fom_march(sys: LinearDynamicalSystem, grid: TimeGrid, tol: float = 1e-13, ma
     with more than 16 off-diagonals per row, n <= 4096) mirrors the
     reference's StepSolver: one dense LU of I - dt A per distinct dt
     (system.py:106-125), then two triangular solves per step (C ABI
-    ``strom_dense_lu`` / ``strom_dense_lu_solve``).  States stay in HBM for ``ingest_simulation``;
+    ``strom_dense_lu`` / ``strom_dense_lu_solve``).  ``method="tridiag"`` (the default whenever it
+    applies: a tridiagonal or periodic tridiagonal A with I - dt A strictly diagonally
+    dominant, n <= 4096) solves every step directly by parallel cyclic reduction
+    (``strom_fom_march_tridiag``).  States stay in HBM for ``ingest_simulation``;
     the clock covers the march only, like the reference's.
     """
     from . import _capi as capi
 
     n, nt, m = sys.n_states, grid.n_steps, sys.n_inputs
-    if method not in ("auto", "direct", "krylov"):
+    if method not in ("auto", "direct", "krylov", "tridiag"):
         raise ValueError(f"unknown fom_march method {method!r}")
     dev = sys.device_arrays()
+    if method == "tridiag" and not _tridiag_ok(dev, grid):
+        raise ValueError("the tridiagonal march needs a (periodic) tridiagonal A with I - dt A strictly "
+                         "diagonally dominant (n <= 4096; n = 2^k when periodic)")
     if method == "auto":
-        method = "krylov" if (dev.get("ell") is not None or n > DIRECT_MAX_N) else "direct"
+        if _tridiag_ok(dev, grid):
+            method = "tridiag"
+        else:
+            method = "krylov" if (dev.get("ell") is not None or n > DIRECT_MAX_N) else "direct"
     if method == "direct" and n > DIRECT_MAX_N:
         raise ValueError(f"the dense StepSolver path supports n <= {DIRECT_MAX_N}")
     f = np.stack([np.atleast_1d(np.asarray(sys.input_signal(k), dtype=float)).reshape(m)
                   for k in range(1, nt + 1)])
     f_dev = torch.as_tensor(f, dtype=F64, device=device()).contiguous()
     states = torch.empty((nt, n), dtype=F64, device=device())
-    if method == "direct":
+    if method == "tridiag":
+        tri = dev["tri"]
+        b_cm = dev["b"].T.contiguous()  # m x n: B column-major
+        torch.cuda.synchronize()
+        start = time.perf_counter()
+        capi.call("strom_fom_march_tridiag", n, tri["lo"].data_ptr(), tri["di"].data_ptr(), tri["up"].data_ptr(),
+                  1 if tri["periodic"] else 0, b_cm.data_ptr(), m, dev["x0"].data_ptr(),
+                  grid.dt_device().data_ptr(), f_dev.data_ptr(), None, nt, states.data_ptr(), capi.stream_ptr())
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - start
+        iters = [0] * nt
+    elif method == "direct":
         a_dense = torch.as_tensor(sys.a.toarray(), dtype=F64, device=device())
         eye = torch.eye(n, dtype=F64, device=device())
         torch.cuda.synchronize()

@@ -28,7 +28,7 @@ def _col_rel(a, b):
     return float(np.max(np.abs(a - b).max(axis=0) / np.maximum(np.abs(b).max(axis=0), 1e-300)))
 
 
-@pytest.mark.parametrize("method", ["direct", "krylov"])
+@pytest.mark.parametrize("method", ["direct", "krylov", "tridiag", "auto"])
 def test_cfg1_states_match_reference_golden(cuda, method):
     """The four cfg1 training marches vs the reference's fom_march checksums."""
     g = load_golden("golden_cfg1.npz")
@@ -141,3 +141,58 @@ def test_cfg3_pipeline_scaled_vs_oracle(cuda):
         big = rs >= 1e-2 * rs[0]
         assert np.max(np.abs(s[:big.sum()] - rs[big])) <= 1e-10 * rs[0]
         assert abs(s[0] - rs[0]) <= 1e-12 * rs[0]
+
+
+def test_tridiagonal_march_vs_superlu(cuda):
+    """The direct march by parallel cyclic reduction (C ABI strom_fom_march_tridiag; reference
+    StepSolver system.py:106-125): non-periodic and periodic tridiagonal operators, sizes that
+    are not powers of two (non-periodic), two inputs, a time-varying input and a non-uniform
+    grid (the tables are rebuilt per distinct dt), against the SuperLU march of the oracle."""
+    import scipy.sparse as sp
+
+    rng = np.random.default_rng(12)
+    for n, periodic in ((3, False), (37, False), (1000, False), (64, True), (2048, True), (4096, False)):
+        lo, up = rng.uniform(0.2, 1.0, n), rng.uniform(0.2, 1.0, n)
+        di = -(lo + up) - rng.uniform(0.1, 1.0, n)  # a stable, diagonally dominant generator
+        a = sp.diags([lo[1:], di, up[:-1]], [-1, 0, 1], format="lil")
+        if periodic:
+            a[0, n - 1] = lo[0]
+            a[n - 1, 0] = up[n - 1]
+        a = sp.csr_array(a)
+        m = 2
+        b = sp.csr_array(rng.standard_normal((n, m)))
+        c = rng.standard_normal((n, 1))
+        x0 = rng.standard_normal(n)
+        nt = 15
+        f = rng.uniform(0.5, 2.0, (nt, m))
+        dt = np.where(np.arange(nt) % 4 == 3, 0.03, 0.01) * (1.0 + (np.arange(nt) > 9))
+        sys_ = LinearDynamicalSystem(a=a, b=b, c=c, x0=x0, input_signal=lambda k: f[k - 1])
+        assert ("tri" in sys_.device_arrays()) and sys_.device_arrays()["tri"]["periodic"] == periodic
+        res = fom_march(sys_, TimeGrid(dt), method="tridiag")
+        ref = so.fom_march(a, b, x0, dt, lambda k: f[k - 1])
+        assert _col_rel(npy(res.states), ref) <= 1e-12, (n, periodic)
+        auto = fom_march(sys_, TimeGrid(dt))  # auto picks the same path
+        np.testing.assert_array_equal(npy(auto.states), npy(res.states))
+        np.testing.assert_allclose(npy(res.outputs), c.T @ ref, rtol=1e-10, atol=1e-12)
+
+
+def test_tridiagonal_march_refuses_what_it_cannot_do(cuda):
+    import scipy.sparse as sp
+
+    n = 48  # periodic, not a power of two: no structure entry, the Krylov march takes it
+    a = sp.diags([np.full(n - 1, 1.0), np.full(n, -2.5), np.full(n - 1, 1.0)], [-1, 0, 1], format="lil")
+    a[0, n - 1] = 1.0
+    a[n - 1, 0] = 1.0
+    d = dict(a=sp.csr_array(a), b=sp.csr_array(np.ones((n, 1))), c=np.ones((n, 1)), x0=np.ones(n))
+    sys_ = LinearDynamicalSystem(input_signal=lambda k: np.array([1.0]), **d)
+    assert "tri" not in sys_.device_arrays()
+    with pytest.raises(ValueError, match="tridiagonal"):
+        fom_march(sys_, TimeGrid(np.full(3, 0.01)), method="tridiag")
+    ref = so.fom_march(d["a"], d["b"], d["x0"], np.full(3, 0.01), lambda k: np.array([1.0]))
+    assert _col_rel(npy(fom_march(sys_, TimeGrid(np.full(3, 0.01))).states), ref) <= 1e-11
+    # not diagonally dominant for this step: the tridiagonal path is not taken
+    a2 = sp.diags([np.full(7, 5.0), np.full(8, 1.0), np.full(7, 5.0)], [-1, 0, 1], format="csr")
+    sys2 = LinearDynamicalSystem(a=sp.csr_array(a2), b=sp.csr_array(np.ones((8, 1))), c=np.ones((8, 1)),
+                                 x0=np.ones(8), input_signal=lambda k: np.array([1.0]))
+    with pytest.raises(ValueError, match="diagonally dominant"):
+        fom_march(sys2, TimeGrid(np.full(2, 0.5)), method="tridiag")
