@@ -172,7 +172,7 @@ class ClockSampler:
         reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 4 + i and "Active" in r[4 + i]
                           and "Not" not in r[4 + i]})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "sm_mhz_min": min(sm) if sm else None, "reasons": reasons, "samples": len(self.rows)}
 
 
 # --------------------------------------------------------------------------- dist
@@ -407,13 +407,19 @@ def bench_isvd_e2e(args, ctx, pinned=True):
         step()
     torch.cuda.synchronize()
     steps = args.steps if pinned else max(2, args.steps // 2)
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        sig = step()
-    torch.cuda.synchronize()
-    dt = time.perf_counter() - t0
+    step_s = []
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            ts = time.perf_counter()
+            sig = step()
+            step_s.append(time.perf_counter() - ts)  # (sigma.cpu() has synchronised)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
     nsnap = COLS - WARM_COLS
     return {"value": nsnap * steps / dt, "unit": "snapshots/s",
+            "step_ms": [round(v * 1e3, 1) for v in step_s], "clocks": clk.summary(),
+            "value_at_median_step": nsnap / statistics.median(step_s),
             "h2d_bytes_per_step": int(nsnap * N_S * 8), "d2h_bytes_per_step": int(sig.numel() * 8),
             "path": ("ingest_simulation(pinned host X) -> chunked H2D on a copy stream overlapped with the "
                      "updates; sigma read back") if pinned else
@@ -742,18 +748,26 @@ def bench_cfg5(args, ncols=400, timed_from=100):
     buf = torch.empty((B, n), dtype=torch.float64, device=dev)
     st = basis.isvd_init(stream.batch(0, 1, out=buf[:1])[:, 0], TOL, tol_sv=TOL, r_max=100, cap_mode="truncate")
     t0, timed_ms, timed_n = 1, 0.0, 0
-    while t0 < ncols:
-        nb = 1 << int(math.floor(math.log2(min(B, ncols - t0))))
-        xb = stream.batch(t0, nb, out=buf[:nb])
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        st = basis.ingest_simulation(st, xb)
-        e1.record()
-        torch.cuda.synchronize()
-        if t0 >= timed_from:
-            timed_ms += e0.elapsed_time(e1)
-            timed_n += nb
-        t0 += nb
+    call_ms = []
+    clk = ClockSampler(torch.cuda.current_device())
+    clk.__enter__()
+    try:
+        while t0 < ncols:
+            nb = 1 << int(math.floor(math.log2(min(B, ncols - t0))))
+            xb = stream.batch(t0, nb, out=buf[:nb])
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            st = basis.ingest_simulation(st, xb)
+            e1.record()
+            torch.cuda.synchronize()
+            if t0 >= timed_from:
+                timed_ms += e0.elapsed_time(e1)
+                timed_n += nb
+                if nb == B:
+                    call_ms.append(e0.elapsed_time(e1))
+            t0 += nb
+    finally:
+        clk.__exit__(None, None, None)
     # singular values of this prefix of the stream: X[:, :ncols] = Q diag(sigma) W[:ncols]^T + E
     # (the W rows of a prefix are not orthonormal, so they differ from sigma)
     known = torch.linalg.svdvals(stream.w[:ncols] * stream.sigma)
@@ -766,7 +780,11 @@ def bench_cfg5(args, ncols=400, timed_from=100):
            "snapshots_per_s": timed_n / (timed_ms / 1e3), "ms_per_update": timed_ms / timed_n,
            "rank": st.rank, "sigma_rel_err_max_i_lt_16_vs_prefix_svd": float(rel.max()),
            "peak_mem_gb": torch.cuda.max_memory_allocated() / 1e9,
-           "floor_frac_of_hbm": None}
+           "floor_frac_of_hbm": None,
+           "ms_per_8_column_call": {"median": statistics.median(call_ms) if call_ms else None,
+                                    "max": max(call_ms) if call_ms else None,
+                                    "note": "calls with a compaction are the slow ones"},
+           "clocks": clk.summary()}
     bw, _ = peaks()
     out["floor_frac_of_hbm"] = out["snapshots_per_s"] * 8.0 * n * 101 / (bw * 1e9)
     del st, buf, sig, c_avg

@@ -394,6 +394,21 @@ std::shared_ptr<Store> alloc_store(int64_t n, int64_t ldu, int32_t ccap, cudaStr
     else slot.reset();  // another shape or stream: do not sit on the memory
   }
   if (!st->umem) st->umem = dev_alloc(ubytes, s, false);
+  if (ubytes >= kSpareStoreMin) {
+    // The first store of this size: reserve its compaction partner now (make_caps sized the
+    // store so that two fit) -- a fresh allocation of tens of GB costs the driver 0.4 - 4 s,
+    // which would otherwise land on the first compaction in the middle of the stream.
+    SpareStore& sp = spare_store();
+    std::lock_guard<std::mutex> g(sp.mu);
+    DevMemPtr& slot = sp.mem[current_device_id()];
+    if (!slot && sp.live[current_device_id()] == 1) {
+      try {
+        slot = dev_alloc(ubytes, s, false);
+      } catch (const Error&) {
+        (void)cudaGetLastError();  // no room for it now: the compaction will ask again
+      }
+    }
+  }
   // tiles holding padding rows (>= n) are read by the passes: keep them zero (never NaN)
   const int64_t first_pad_tile = n / kUTile;
   const int64_t ntile = ldu / kUTile;
