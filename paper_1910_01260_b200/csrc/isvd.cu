@@ -964,18 +964,12 @@ template <int GB>
 int launch_compact_pass(const Store& src, const int32_t* base_dev, const int32_t* c_dev, const int32_t* r_dev,
                          const double* T, int64_t ldt, int cmax, int rmax, const Store& dst, double* part, int QP,
                          cudaStream_t s) {
-  int tr = compact_pass_rows(cmax, rmax);
-  int ctas_per_sm = 1;
-  // STROM_COMPACT_TWO_CTA=1 (small Gram blocks, r <= 64): half tiles let two CTAs share an SM, so
-  // one loads its next tile while the other multiplies.  Off by default: at cfg2 it saves well
-  // under a millisecond per step, and the other split of the Gram partials re-rolls the
-  // noise-level decisions (262 / 220 / 324 dependent updates on the three bench streams
-  // instead of 331 / 226 / 280: no net gain).
-  static const bool two = getenv("STROM_COMPACT_TWO_CTA") != nullptr;
-  if (GB == 1 && two && 2 * (compact_pass_smem(cmax, rmax, 32) + 1024) <= max_smem_optin()) {
-    tr = 32;
-    ctas_per_sm = 2;
-  }
+  // (Half tiles with two CTAs per SM at r <= 64 -- one loads while the other multiplies -- were
+  // tried: under a millisecond per cfg2 step, bought with a 128-register cap that slows the
+  // whole-tile sweep by 9 %, and the other split of the Gram partials only re-rolled the
+  // noise-level decisions: dropped.)
+  const int tr = compact_pass_rows(cmax, rmax);
+  const int ctas_per_sm = 1;
   const size_t smem = compact_pass_smem(cmax, rmax, tr);
   static PerDevice<size_t> cfg;
   set_smem_attr(k_compact_pass<GB>, smem, &cfg.get());

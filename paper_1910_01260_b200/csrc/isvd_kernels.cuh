@@ -1651,7 +1651,7 @@ constexpr int kCompactThreads = 256;
 // U and U_new staging buffers halve, so T (c x r), the U half-tile and the U_new half-tile
 // fit shared memory up to r = 128, c ~ 140: 225 KB at cfg5's r = 100 instead of 294 KB).
 template <int GB>
-__global__ void __launch_bounds__(kCompactThreads, GB == 1 ? 2 : 1) k_compact_pass(const double* __restrict__ U, int64_t src_ccap,
+__global__ void __launch_bounds__(kCompactThreads, 1) k_compact_pass(const double* __restrict__ U, int64_t src_ccap,
                                                                      const int32_t* base_dev, const int32_t* c_dev,
                                                                      const int32_t* r_dev, const double* __restrict__ T,
                                                                      int64_t ldt, double* __restrict__ Unew,
