@@ -11,6 +11,7 @@ has no CPU oracle; its checks are invariants, exercised here on 2^18 rows:
 
 import math
 
+import numpy as np
 import pytest
 import torch
 
@@ -62,3 +63,52 @@ def test_capacity_stream_invariants(cuda):
     # every truncation (the full-size cfg2 test measures the same effect against
     # the batch SVD); the per-snapshot and window ingestion paths land at 9-10x
     assert sin_max <= 20 * noise_rel / float(s.sigma[m - 1])
+
+
+def test_spare_store_is_reused_and_released(cuda):
+    """Stores of 1 GiB and more keep one spare block for their compactions (csrc/isvd.cu
+    SpareStore): reused by every compaction, handed back by strom_trim_cache and with the last
+    state; the footprint must not grow from compaction to compaction."""
+    import gc
+
+    from paper_1910_01260_b200 import _capi
+
+    torch.cuda.synchronize()
+    gc.collect()
+    _capi.lib.strom_trim_cache()
+    torch.cuda.empty_cache()
+    free0 = torch.cuda.mem_get_info()[0]
+    n, rank = 1 << 20, 100  # c_cap = 151 columns: a 1.2 GiB store
+    # noise well above tol: every snapshot appends a column, a compaction every ~50 updates
+    s = wl.HadamardStream(n, 420, rank, decades_per=12.0, seed=1, noise=1e-8)
+    st = basis.isvd_init(s.batch(0, 1)[:, 0].contiguous(), 1e-9, tol_sv=1e-9, r_max=rank, cap_mode="truncate")
+    used_mid = None
+    for t0 in range(1, 417, 8):  # rank 100 from ~snapshot 100, then a compaction every ~50 appends
+        st = basis.ingest_simulation(st, s.batch(t0, 8))
+        if t0 == 201:
+            torch.cuda.synchronize()
+            used_mid = free0 - torch.cuda.mem_get_info()[0]
+    assert st.rank == rank and st.n_truncated >= 300
+    sig = st.sigma.cpu().numpy()
+    known = torch.linalg.svdvals(s.w[:417] * s.sigma).cpu().numpy()
+    assert np.max(np.abs(sig[:16] - known[:16])) <= 2e-5  # Weyl: |d sigma| <= ||E||_2 ~ 1e-8 (sqrt(n) + sqrt(k))
+    torch.cuda.synchronize()
+    used2 = free0 - torch.cuda.mem_get_info()[0]
+    store = 8 * n * 151
+    # two blocks of the final capacity (the store and the spare its compactions ping-pong with)
+    # plus small state: the compactions after snapshot 200 must not have grown the footprint
+    assert used2 <= used_mid + store // 4, (used_mid, used2)
+    assert used2 <= 3 * store, (used2, store)
+    _capi.lib.strom_trim_cache()
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    used3 = free0 - torch.cuda.mem_get_info()[0]
+    # the release threshold keeps freed blocks in the stream-ordered pool; what must hold is
+    # that a second trim + state release brings everything back
+    del st, sig
+    gc.collect()
+    _capi.lib.strom_trim_cache()
+    torch.cuda.synchronize()
+    del s
+    torch.cuda.empty_cache()
+    assert used3 <= used2
