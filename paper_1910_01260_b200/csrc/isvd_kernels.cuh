@@ -1301,13 +1301,13 @@ __device__ inline void step_b_body(const StateView& src, const StateView& dst, c
   {
     const int kdim = dep ? r : m;
     if (ns_ok)
-      cta_gemm_dmma_n2(cn, mk, kdim, WB, 1, P.ccap, WS, 1, m, [&](int a, int k, double v) {
+      cta_gemm_dmma_blk<4, 2>(cn, mk, kdim, WB, 1, P.ccap, WS, 1, m, [&](int a, int k, double v) {
         dst.N[(int64_t)k * dst.ldn + a] = v;
         NS[k * cn + a] = v;
       });
     else
-      cta_gemm_dmma_n2(cn, mk, kdim, WB, 1, P.ccap, WS, 1, m,
-                       [&](int a, int k, double v) { dst.N[(int64_t)k * dst.ldn + a] = v; });
+      cta_gemm_dmma_blk<4, 2>(cn, mk, kdim, WB, 1, P.ccap, WS, 1, m,
+                              [&](int a, int k, double v) { dst.N[(int64_t)k * dst.ldn + a] = v; });
   }
   for (int k = threadIdx.x; k < mk; k += blockDim.x) dst.sigma[k] = svs[k];
   __syncthreads();

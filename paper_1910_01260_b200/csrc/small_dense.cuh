@@ -374,6 +374,65 @@ __device__ inline void cta_gemm_dmma_n2(int M, int N, int K, const double* A, in
   }
 }
 
+// The same product with an MT x NT block of accumulator tiles per warp (8 MT x 8 NT outputs:
+// MT + NT fragment loads feed MT * NT independent DMMA chains per k-step), blocks dealt to
+// the warps round-robin.  For the core step's N update (c x r times r x r, c ~ 90, r = 64):
+// 4 x 2 tiles per warp make 12-16 blocks, one per warp, eight chains each -- enough to keep
+// the fp64 pipe (one DMMA per 16 cycles per sub-partition) busy.  Same k order per output:
+// identical results.
+template <int MT, int NT, class Store>
+__device__ inline void cta_gemm_dmma_blk(int M, int N, int K, const double* A, int64_t asi, int64_t ask,
+                                         const double* B, int64_t bsk, int64_t bsj, Store store) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int bm = (M + 8 * MT - 1) / (8 * MT), bn = (N + 8 * NT - 1) / (8 * NT), ks = (K + 3) >> 2;
+  for (int blk = wid; blk < bm * bn; blk += nw) {
+    const int i0 = (blk % bm) * 8 * MT, j0 = (blk / bm) * 8 * NT;
+    const double* ap[MT];
+    const double* bp[NT];
+    bool va[MT], vb[NT];
+#pragma unroll
+    for (int x = 0; x < MT; ++x) {
+      va[x] = i0 + 8 * x + g < M;
+      ap[x] = A + (int64_t)(va[x] ? i0 + 8 * x + g : 0) * asi;
+    }
+#pragma unroll
+    for (int y = 0; y < NT; ++y) {
+      vb[y] = j0 + 8 * y + g < N;
+      bp[y] = B + (int64_t)(vb[y] ? j0 + 8 * y + g : 0) * bsj;
+    }
+    double c[MT][NT][2];
+#pragma unroll
+    for (int x = 0; x < MT; ++x)
+#pragma unroll
+      for (int y = 0; y < NT; ++y) c[x][y][0] = c[x][y][1] = 0.0;
+#pragma unroll 2
+    for (int kk = 0; kk < ks; ++kk) {
+      const int k = (kk << 2) + t;
+      const bool vk = k < K;
+      double av[MT], bv[NT];
+#pragma unroll
+      for (int x = 0; x < MT; ++x) av[x] = (va[x] && vk) ? ap[x][(int64_t)k * ask] : 0.0;
+#pragma unroll
+      for (int y = 0; y < NT; ++y) bv[y] = (vb[y] && vk) ? bp[y][(int64_t)k * bsk] : 0.0;
+#pragma unroll
+      for (int x = 0; x < MT; ++x)
+#pragma unroll
+        for (int y = 0; y < NT; ++y) dmma884(c[x][y][0], c[x][y][1], av[x], bv[y]);
+    }
+#pragma unroll
+    for (int x = 0; x < MT; ++x)
+#pragma unroll
+      for (int y = 0; y < NT; ++y) {
+        const int r = i0 + 8 * x + g, cc = j0 + 8 * y + 2 * t;
+        if (r < M) {
+          if (cc < N) store(r, cc, c[x][y][0]);
+          if (cc + 1 < N) store(r, cc + 1, c[x][y][1]);
+        }
+      }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // In-place lower Cholesky B = L L^T (n x n, column-major, ld), right-looking,
 // block-parallel, two barriers per column.  Returns min/max pivot ratio, or -1
