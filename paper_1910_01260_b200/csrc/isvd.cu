@@ -960,25 +960,33 @@ int compact_pass_rows(int cmax, int rmax) {
   return 0;
 }
 
+template <int GB, int TR>
+int launch_compact_pass_t(const Store& src, const int32_t* base_dev, const int32_t* c_dev, const int32_t* r_dev,
+                          const double* T, int64_t ldt, int cmax, int rmax, const Store& dst, double* part, int QP,
+                          cudaStream_t s) {
+  const size_t smem = compact_pass_smem(cmax, rmax, TR);
+  static PerDevice<size_t> cfg;
+  set_smem_attr(k_compact_pass<GB, TR>, smem, &cfg.get());
+  ProfScope ps(P_TALL_GEMM, s);
+  k_compact_pass<GB, TR><<<sm_count(), kCompactThreads, smem, s>>>(src.U(), src.ccap, base_dev, c_dev, r_dev, T, ldt,
+                                                                   dst.U(), dst.ccap, src.ldu / kUTile, part, QP,
+                                                                   prof_dev_bytes());
+  STROM_LAUNCH_CHECK();
+  return sm_count();  // per-CTA Gram partials written
+}
+// (Half tiles with two CTAs per SM at r <= 64 -- one loads while the other multiplies -- were
+// tried: under a millisecond per cfg2 step, bought with a 128-register cap that slows the
+// whole-tile sweep by 9 %, and the other split of the Gram partials only re-rolled the
+// noise-level decisions: dropped.)
 template <int GB>
 int launch_compact_pass(const Store& src, const int32_t* base_dev, const int32_t* c_dev, const int32_t* r_dev,
-                         const double* T, int64_t ldt, int cmax, int rmax, const Store& dst, double* part, int QP,
-                         cudaStream_t s) {
-  // (Half tiles with two CTAs per SM at r <= 64 -- one loads while the other multiplies -- were
-  // tried: under a millisecond per cfg2 step, bought with a 128-register cap that slows the
-  // whole-tile sweep by 9 %, and the other split of the Gram partials only re-rolled the
-  // noise-level decisions: dropped.)
-  const int tr = compact_pass_rows(cmax, rmax);
-  const int ctas_per_sm = 1;
-  const size_t smem = compact_pass_smem(cmax, rmax, tr);
-  static PerDevice<size_t> cfg;
-  set_smem_attr(k_compact_pass<GB>, smem, &cfg.get());
-  ProfScope ps(P_TALL_GEMM, s);
-  k_compact_pass<GB><<<sm_count() * ctas_per_sm, kCompactThreads, smem, s>>>(src.U(), src.ccap, base_dev, c_dev, r_dev, T, ldt,
-                                                               dst.U(), dst.ccap, src.ldu / kUTile, part, QP,
-                                                               prof_dev_bytes(), tr);
-  STROM_LAUNCH_CHECK();
-  return sm_count() * ctas_per_sm;  // per-CTA Gram partials written
+                        const double* T, int64_t ldt, int cmax, int rmax, const Store& dst, double* part, int QP,
+                        cudaStream_t s) {
+  if (compact_pass_rows(cmax, rmax) == 64)
+    return launch_compact_pass_t<GB, 64>(src, base_dev, c_dev, r_dev, T, ldt, cmax, rmax, dst, part, QP, s);
+  if constexpr (GB >= 3)  // half tiles are only ever needed for 96- and 128-column Gram blocks
+    return launch_compact_pass_t<GB, 32>(src, base_dev, c_dev, r_dev, T, ldt, cmax, rmax, dst, part, QP, s);
+  throw Error(kInternal, "compaction sweep: no shared-memory layout");
 }
 
 // L = chol(A[:, col0:col0+q]^T A[:, col0:col0+q]) with the DMMA tall Gram.

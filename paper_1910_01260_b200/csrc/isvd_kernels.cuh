@@ -1647,17 +1647,18 @@ __global__ void __launch_bounds__(256) k_w_to_n(StateView v, double* tmp) {
 // persistent blocks of G.  Per-CTA Gram partials (QP x QP) go to `part`.
 // ---------------------------------------------------------------------------
 constexpr int kCompactThreads = 256;
-// tr: rows of a store tile handled per step, 64 (the whole tile) or 32 (two half-tiles: the
+// TR: rows of a store tile handled per step, 64 (the whole tile) or 32 (two half-tiles: the
 // U and U_new staging buffers halve, so T (c x r), the U half-tile and the U_new half-tile
 // fit shared memory up to r = 128, c ~ 140: 225 KB at cfg5's r = 100 instead of 294 KB).
-template <int GB>
+template <int GB, int TR>
 __global__ void __launch_bounds__(kCompactThreads, 1) k_compact_pass(const double* __restrict__ U, int64_t src_ccap,
                                                                      const int32_t* base_dev, const int32_t* c_dev,
                                                                      const int32_t* r_dev, const double* __restrict__ T,
                                                                      int64_t ldt, double* __restrict__ Unew,
                                                                      int64_t dst_ccap, int64_t ntiles,
                                                                      double* __restrict__ part, int QP,
-                                                                     unsigned long long* prof, int tr) {
+                                                                     unsigned long long* prof) {
+  constexpr int tr = TR;
   extern __shared__ __align__(16) double csm[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
