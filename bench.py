@@ -902,6 +902,46 @@ def run_device(args):
         print(json.dumps(line), flush=True)
 
 
+# --------------------------------------------------------------------------- row-sharded stream
+def run_sharded(args):
+    """The cfg2 stream row-sharded over the ranks of one NVSwitch domain:
+    every rank owns n / G rows of U and of each snapshot, sigma / V / decisions are replicated,
+    the per-rank partial sums cross the GPUs in one small kernel over peer-memory mailboxes.
+    Strong scaling: total work fixed.  At G = 1 the exchange degenerates to a copy through the
+    mailbox: the line then measures the protocol's overhead against the unsharded run."""
+    import torch
+
+    ws, rank, local = dist_setup(args.gpus)
+    torch.cuda.set_device(local)
+    from paper_1910_01260_b200 import basis
+    from paper_1910_01260_b200.sharded import ShardGroup
+
+    dev = torch.device("cuda", local)
+    xh, start, gen_s = cfg2_host()
+    group = ShardGroup.connect(N_S)
+    r0, nl = group.row0, group.n_local
+    xd = torch.as_tensor(np.ascontiguousarray(xh[r0:r0 + nl, WARM_COLS:].T), device=dev).T  # n_local x 400, col-major
+    with group:
+        st100 = basis.SvdState(np.ascontiguousarray(start["phi"][r0:r0 + nl]), start["sigma"], start["v"], start["k"],
+                               TOL, tol_sv=TOL, r_max=RANK, cap_mode="truncate")
+    ms, last, launches, clocks = time_ingest(st100, xd, args.steps, args.warmup, ws, clocks=(rank == 0))
+    ms_max = allmax(ws, ms)
+    nsnap = COLS - WARM_COLS
+    info = last.info()
+    nex, err = group.status()
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "mode": "row-sharded (one stream over all ranks)", "value": nsnap * args.steps /
+            (ms_max / 1e3), "unit": "snapshots/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (BASELINE config 2 construction, numpy default_rng(0))",
+            "config": dict(config_block(1), parallelism=f"row-sharded x{ws}", rows_per_rank=nl),
+            "gpu_launches": launches, "clocks": clocks, "exchanges": nex, "exchange_errors": err,
+            "final_state": dict(rank=int(info.rank), n_dependent=int(info.n_dependent),
+                                n_truncated=int(info.n_truncated), sigma0=float(last.sigma[0]))}), flush=True)
+    barrier(ws)
+
+
 # --------------------------------------------------------------------------- reference arm
 def run_reference(args):
     """The reference's algorithm (oracle port, bit-identical to strom.basis in this
@@ -961,11 +1001,16 @@ def main():
     ap.add_argument("--no-seeds", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", action="store_true",
+                    help="one cfg2 stream ROW-SHARDED over the ranks (sharded.ShardGroup, strong scaling) "
+                         "instead of one replica per rank; prints its own JSON line")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif args.shard:
+        run_sharded(args)
     else:
         run_device(args)
 
