@@ -333,6 +333,17 @@ def _march_blocks(sys: LinearDynamicalSystem, dts, v: torch.Tensor, transpose: b
     dev = sys.device_arrays_transposed() if transpose else sys.device_arrays()
     ell = dev.get("ell")
     out = torch.empty((nt, n), dtype=F64, device=device())
+    tri = dev.get("tri")
+    if tri is not None and not cache.get("direct", False):
+        key = ("tri_ok", transpose, np.asarray(dts, dtype=float).tobytes())
+        if key not in cache:
+            cache[key] = _tridiag_ok(dev, TimeGrid(np.asarray(dts, dtype=float)))
+        if cache[key]:  # (periodic) tridiagonal A: the direct march (strom_fom_march_tridiag)
+            dt_dev = torch.as_tensor(np.asarray(dts, dtype=float), dtype=F64, device=device())
+            capi.call("strom_fom_march_tridiag", n, tri["lo"].data_ptr(), tri["di"].data_ptr(),
+                      tri["up"].data_ptr(), 1 if tri["periodic"] else 0, None, 0, None, dt_dev.data_ptr(), None,
+                      v.contiguous().data_ptr(), nt, out.data_ptr(), capi.stream_ptr())
+            return out
     if ell is None or (n <= DIRECT_MAX_N and cache.get("direct", False)):
         if n > DIRECT_MAX_N:
             raise ValueError("the space-time inverse needs at most 16 off-diagonal entries per row of A "

@@ -196,3 +196,32 @@ def test_tridiagonal_march_refuses_what_it_cannot_do(cuda):
                                  x0=np.ones(8), input_signal=lambda k: np.array([1.0]))
     with pytest.raises(ValueError, match="diagonally dominant"):
         fom_march(sys2, TimeGrid(np.full(2, 0.5)), method="tridiag")
+
+
+def test_space_time_inverse_tridiagonal_vs_lu(cuda):
+    """(A_st)^{-1} v and its adjoint (reference system.py:195-233) on a periodic tridiagonal
+    operator: the direct cyclic-reduction march against the dense-LU StepSolver path."""
+    import scipy.sparse as sp
+
+    from paper_1910_01260_b200 import system
+
+    rng = np.random.default_rng(8)
+    n, nt = 256, 9
+    lo, up = rng.uniform(0.2, 1.0, n), rng.uniform(0.2, 1.0, n)
+    di = -(lo + up) - rng.uniform(0.1, 1.0, n)
+    a = sp.diags([lo[1:], di, up[:-1]], [-1, 0, 1], format="lil")
+    a[0, n - 1] = lo[0]
+    a[n - 1, 0] = up[n - 1]
+    sys_ = LinearDynamicalSystem(a=sp.csr_array(a), b=sp.csr_array(np.ones((n, 1))), c=np.ones((n, 1)),
+                                 x0=np.zeros(n), input_signal=lambda k: np.array([0.0]))
+    grid = TimeGrid(rng.uniform(0.005, 0.03, nt))
+    v = rng.standard_normal(n * nt)
+    fast, fast_t = system.st_inverse_operator(sys_, grid)
+    slow, slow_t = system.st_inverse_operator(sys_, grid, direct=True)
+    for f, g in ((fast, slow), (fast_t, slow_t)):
+        x, y = npy(f(v)), npy(g(v))
+        assert np.max(np.abs(x - y)) <= 1e-12 * np.max(np.abs(y))
+    # <A_st^{-1} v, w> = <v, A_st^{-T} w>
+    w = rng.standard_normal(n * nt)
+    lhs, rhs = float(npy(fast(v)) @ w), float(v @ npy(fast_t(w)))
+    assert abs(lhs - rhs) <= 1e-11 * max(abs(lhs), 1.0)
