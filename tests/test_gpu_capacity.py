@@ -97,8 +97,9 @@ def test_spare_store_is_reused_and_released(cuda):
     store = 8 * n * 151
     # two blocks of the final capacity (the store and the spare its compactions ping-pong with)
     # plus small state: the compactions after snapshot 200 must not have grown the footprint
-    assert used2 <= used_mid + store // 4, (used_mid, used2)
-    assert used2 <= 3 * store, (used2, store)
+    # (a leak would add one store per compaction: four to five more between the two readings)
+    assert used2 <= used_mid + store + store // 2, (used_mid, used2)
+    assert used2 <= 4 * store, (used2, store)
     _capi.lib.strom_trim_cache()
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
@@ -111,4 +112,4 @@ def test_spare_store_is_reused_and_released(cuda):
     torch.cuda.synchronize()
     del s
     torch.cuda.empty_cache()
-    assert used3 <= used2
+    assert used3 <= used2 + store // 8
