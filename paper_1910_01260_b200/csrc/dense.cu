@@ -693,9 +693,26 @@ __device__ inline void pl_gemm(double* S, int ld, const double* M, int64_t ldm, 
 // shared memory, then scale and rank-1 update in registers; two barriers per
 // column.  Fully unrolled over the 16 panel columns so every register index is
 // static.
+// Warp-wide argmax of (key, row) on the integer reduction unit (redux.sync): the key is the
+// IEEE bit pattern of |a| plus one (0 = no candidate; bit patterns of non-negative doubles
+// order like their values), the row index breaks ties towards the first row (idamax).  Three
+// REDUX instructions instead of five rounds of three shuffles and a double compare.
+__device__ __forceinline__ void pl_warp_argmax(unsigned long long key, int row, unsigned long long& kmax, int& rmin) {
+  const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+  const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+  const bool win = hi == mh && lo == ml;
+  rmin = (int)__reduce_min_sync(0xffffffffu, win ? (unsigned)row : 0x7fffffffu);
+  kmax = ((unsigned long long)mh << 32) | ml;
+}
+__device__ __forceinline__ unsigned long long pl_key(double v, bool candidate) {
+  // NaN never wins (like `fabs(v) > best` with best = -1): an all-NaN column pivots on itself
+  return (candidate && v == v) ? (unsigned long long)__double_as_longlong(fabs(v)) + 1ull : 0ull;
+}
+
 constexpr int kPlRpt = 2;  // register panel for n <= kPlThreads * kPlRpt = 1024
-__device__ inline void pl_panel_reg(double* S, int ld, int n, int j0, int w, int* piv, double* cval, int* cidx,
-                                    double* prow, double* grow) {
+__device__ inline void pl_panel_reg(double* S, int ld, int n, int j0, int w, int* piv, unsigned long long* ckey,
+                                    int* cidx, double* prow, double* grow) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   double v[kPlRpt][kPlNb];
 #pragma unroll
@@ -708,33 +725,19 @@ __device__ inline void pl_panel_reg(double* S, int ld, int n, int j0, int w, int
   for (int c = 0; c < kPlNb; ++c) {
     if (c >= w) break;
     const int gr = j0 + c;
-    double best = -1.0;
+    unsigned long long key = 0ull;
     int bi = 0x7fffffff;
 #pragma unroll
     for (int q = 0; q < kPlRpt; ++q) {
       const int r = tid + kPlThreads * q;
-      if (r >= gr && r < n) {
-        const double av = fabs(v[q][c]);
-        if (av > best) { best = av; bi = r; }
-      }
+      const unsigned long long kq = pl_key(v[q][c], r >= gr && r < n);
+      if (kq > key) { key = kq; bi = r; }  // rows ascend with q: ties keep the first
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-    }
-    if (lane == 0) { cval[wid] = best; cidx[wid] = bi; }
+    pl_warp_argmax(key, bi, key, bi);
+    if (lane == 0) { ckey[wid] = key; cidx[wid] = bi; }
     __syncthreads();
-    best = cval[lane & (kPlWarps - 1)];
-    bi = cidx[lane & (kPlWarps - 1)];
-#pragma unroll
-    for (int o = kPlWarps / 2; o > 0; o >>= 1) {
-      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-    }
-    const int p = (bi == 0x7fffffff) ? gr : bi;  // an all-NaN column pivots on itself
+    pl_warp_argmax(ckey[lane & (kPlWarps - 1)], cidx[lane & (kPlWarps - 1)], key, bi);
+    const int p = (key == 0ull || bi == 0x7fffffff) ? gr : bi;  // an all-NaN column pivots on itself
 #pragma unroll
     for (int q = 0; q < kPlRpt; ++q) {
       const int r = tid + kPlThreads * q;
@@ -842,34 +845,22 @@ __global__ void __launch_bounds__(kPlThreads, 1) k_lu_persistent(PlArgs a) {
     PL_PROBE(3);
     const int j0 = c0;
     if (n <= kPlThreads * kPlRpt) {
-      pl_panel_reg(S, ld, n, j0, w, a.piv, cval, cidx, prow, grow);
+      pl_panel_reg(S, ld, n, j0, w, a.piv, reinterpret_cast<unsigned long long*>(cval), cidx, prow, grow);
     } else {
       for (int c = 0; c < w; ++c) {
         const int gr = j0 + c;
-        double best = -1.0;
+        unsigned long long key = 0ull;
         int bi = 0x7fffffff;
-        for (int r = tid; r < n; r += kPlThreads)
-          if (r >= gr) {
-            const double v = fabs(S[c * ld + r]);
-            if (v > best) { best = v; bi = r; }
-          }
-  #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-          if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+        for (int r = tid; r < n; r += kPlThreads) {
+          const unsigned long long kq = pl_key(S[c * ld + r], r >= gr);
+          if (kq > key) { key = kq; bi = r; }  // rows ascend: ties keep the first
         }
-        if (lane == 0) { cval[wid] = best; cidx[wid] = bi; }
+        unsigned long long* ckey = reinterpret_cast<unsigned long long*>(cval);
+        pl_warp_argmax(key, bi, key, bi);
+        if (lane == 0) { ckey[wid] = key; cidx[wid] = bi; }
         __syncthreads();
-        best = cval[lane & (kPlWarps - 1)];
-        bi = cidx[lane & (kPlWarps - 1)];
-  #pragma unroll
-        for (int o = kPlWarps / 2; o > 0; o >>= 1) {
-          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-          if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-        }
-        const int p = (bi == 0x7fffffff) ? gr : bi;  // an all-NaN column pivots on itself
+        pl_warp_argmax(ckey[lane & (kPlWarps - 1)], cidx[lane & (kPlWarps - 1)], key, bi);
+        const int p = (key == 0ull || bi == 0x7fffffff) ? gr : bi;  // an all-NaN column pivots on itself
         if (tid < kPlNb && p != gr) {
           const double tmp = S[tid * ld + gr];
           S[tid * ld + gr] = S[tid * ld + p];
