@@ -136,8 +136,14 @@ def _csr_device(a, dev) -> dict:
              indices=torch.as_tensor(a.indices.astype(it), device=dev),
              data=torch.as_tensor(a.data.astype(np.float64), device=dev),
              index_bits=64 if big else 32)
-    rows = np.repeat(np.arange(a.shape[0]), np.diff(a.indptr))
-    offd = np.bincount(rows[a.indices != rows], minlength=a.shape[0]) if a.nnz else np.zeros(1, int)
+    # off-diagonal entries per row = row length - stored diagonal entries (the diagonal entries'
+    # column indices are their rows: one comparison over the entries and a bincount over <= n)
+    if a.nnz:
+        rn = np.diff(a.indptr)
+        isd = a.indices == np.repeat(np.arange(a.shape[0], dtype=a.indices.dtype), rn)
+        offd = rn - np.bincount(a.indices[isd], minlength=a.shape[0])
+    else:
+        offd = np.zeros(1, int)
     kell = next((k for k in (4, 6, 8, 16) if int(offd.max()) <= k), None)
     if kell is not None and not big:
         from . import _capi as capi
