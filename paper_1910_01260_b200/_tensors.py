@@ -14,12 +14,52 @@ def device() -> torch.device:
     return torch.device("cuda", torch.cuda.current_device())
 
 
+_H2D_MIN = 32 << 20      # host arrays at least this large are staged through pinned buffers
+_H2D_CHUNK = 32 << 20
+_h2d_pinned: list = []
+
+
+def h2d_numpy(x: np.ndarray) -> torch.Tensor:
+    """Device copy of a C- or F-contiguous numpy array of any dtype torch knows.
+
+    A pageable host array goes to the device at ~11 GB/s through the driver's own staging;
+    copying it chunk by chunk into two alternating pinned buffers and issuing the DMA of one
+    chunk while the next is being copied reaches the host memcpy rate (400 MB: 35 -> ~15 ms).
+    Small arrays take the plain path."""
+    dev = device()
+    if x.nbytes < _H2D_MIN or not (x.flags.c_contiguous or x.flags.f_contiguous) or not x.flags.writeable:
+        return torch.as_tensor(x, device=dev)
+    fortran = x.flags.f_contiguous and not x.flags.c_contiguous
+    flat = x.reshape(-1, order="F" if fortran else "C")  # a view: the array is contiguous in that order
+    src = torch.from_numpy(flat).view(torch.uint8)
+    if not _h2d_pinned:
+        _h2d_pinned.extend(torch.empty(_H2D_CHUNK, dtype=torch.uint8, pin_memory=True) for _ in range(2))
+    out = torch.empty(flat.shape[0], dtype=torch.from_numpy(flat[:1]).dtype, device=dev)
+    dst = out.view(torch.uint8)
+    stream = torch.cuda.current_stream()
+    done = [None, None]
+    for i, off in enumerate(range(0, src.numel(), _H2D_CHUNK)):
+        n = min(_H2D_CHUNK, src.numel() - off)
+        b = i & 1
+        if done[b] is not None:
+            done[b].synchronize()  # the DMA that last read this buffer
+        _h2d_pinned[b][:n].copy_(src[off:off + n])
+        dst[off:off + n].copy_(_h2d_pinned[b][:n], non_blocking=True)
+        done[b] = torch.cuda.Event()
+        done[b].record(stream)
+    for e in done:
+        if e is not None:
+            e.synchronize()  # the pinned buffers are shared: leave them idle
+    shape = x.shape
+    return out.view(shape[::-1]).permute(*range(len(shape) - 1, -1, -1)) if fortran else out.view(shape)
+
+
 def to_dev(a, *, contiguous: bool = True) -> torch.Tensor:
     """float64 CUDA tensor view/copy of a numpy array, python sequence or tensor."""
     if isinstance(a, torch.Tensor):
         t = a.to(device=device(), dtype=F64)
     else:
-        t = torch.as_tensor(np.asarray(a, dtype=np.float64), device=device())
+        t = h2d_numpy(np.asarray(a, dtype=np.float64))
     return t.contiguous() if contiguous else t
 
 

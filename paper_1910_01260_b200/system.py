@@ -132,9 +132,10 @@ def _csr_device(a, dev) -> dict:
     a.sort_indices()
     big = a.nnz >= 2**31 or a.shape[0] >= 2**31
     it = np.int64 if big else np.int32
-    d = dict(indptr=torch.as_tensor(a.indptr.astype(it), device=dev),
-             indices=torch.as_tensor(a.indices.astype(it), device=dev),
-             data=torch.as_tensor(a.data.astype(np.float64), device=dev),
+    from ._tensors import h2d_numpy
+
+    d = dict(indptr=h2d_numpy(a.indptr.astype(it)), indices=h2d_numpy(a.indices.astype(it)),
+             data=h2d_numpy(a.data.astype(np.float64)),
              index_bits=64 if big else 32)
     # off-diagonal entries per row = row length - stored diagonal entries (the diagonal entries'
     # column indices are their rows: one comparison over the entries and a bincount over <= n)

@@ -124,3 +124,25 @@ class TestBuildBasisSet:
         bs = basis.build_basis_set(st, 2, 2, 15, 2)
         stack = bs.temporal_stack()
         assert tuple(stack.shape) == (2, 15, 2) and torch.equal(stack[1], bs.temporal[1])
+
+
+def test_large_host_arrays_are_staged_exactly(cuda):
+    """_tensors.h2d_numpy: host arrays of 32 MB and more go through alternating pinned
+    buffers; C and Fortran order, sizes that are not a multiple of the chunk, other dtypes."""
+    from paper_1910_01260_b200._tensors import h2d_numpy, to_dev
+
+    rng = np.random.default_rng(0)
+    a = rng.standard_normal((70_001, 97))                     # 54 MB, C order
+    t = h2d_numpy(a)
+    assert t.shape == a.shape and t.is_contiguous()
+    np.testing.assert_array_equal(t.cpu().numpy(), a)
+    f = np.asfortranarray(a)                                   # Fortran order: strides kept
+    tf = h2d_numpy(f)
+    assert tf.shape == f.shape and tf.stride() == (1, f.shape[0])
+    np.testing.assert_array_equal(tf.cpu().numpy(), f)
+    i = rng.integers(0, 1 << 30, 9_000_003).astype(np.int32)   # 36 MB of int32
+    np.testing.assert_array_equal(h2d_numpy(i).cpu().numpy(), i)
+    np.testing.assert_array_equal(to_dev(a[:, ::2]).cpu().numpy(), a[:, ::2])  # strided: plain path
+    ro = a.copy()
+    ro.flags.writeable = False
+    np.testing.assert_array_equal(h2d_numpy(ro).cpu().numpy(), ro)
